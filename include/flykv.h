@@ -1,0 +1,294 @@
+/*
+ * flykv.h -- C ABI of libflykv.so: the KV Cache Adaptor DP<->TP re-layout
+ * and the zero-copy weight shard view of Flying Serving (arXiv 2602.22593),
+ * built for NVIDIA B200 (sm_100a).
+ *
+ * Citations: P:n = line n of the paper's LaTeX, S:n = SPEC.md,
+ * Rn = reading n in DESIGN.md section 3.
+ *
+ * Conventions for every entry point
+ *   - Returns kv_status; KV_OK == 0.  No exceptions cross the ABI.  On error
+ *     kv_last_error() returns a thread-local message with detail.
+ *   - "host" pointers are CPU memory owned by the caller and only read (or
+ *     written, for outputs) during the call.  "device" pointers are CUDA
+ *     global memory owned by the caller; the library never frees them.
+ *   - The library owns kv_cache and kv_plan objects (and their device
+ *     workspaces); release them with kv_cache_destroy / kv_plan_destroy.
+ *   - One caller thread per kv_cache.
+ *   - Layout terms (R1-R4):
+ *       L layers, H KV heads, d head_dim, B = B_base tokens per DP block,
+ *       e bytes per element (2 for bf16);
+ *       H_loc(p) = H/p if p <= H else 1                  (Eq.3, R2)
+ *       B(p)     = B * H / H_loc(p)  (= p*B when p | H)   (Eq.2)
+ *       M        = 2*H*B*d*e bytes per block per layer    (M_block P:338-340, R1)
+ *     A block of one layer at degree p is [2 (K,V)][H_loc(p)][B(p)][d]
+ *     elements, K first (R4; BJ north_star "[blocks, K/V, kv_heads,
+ *     block_size, head_dim]").  Rank r of a degree-p group holds heads
+ *     [r*H_loc, (r+1)*H_loc) (p <= H, R3) or head r/(p/H) (p > H, R2).
+ */
+#ifndef FLYKV_H
+#define FLYKV_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    KV_OK = 0,
+    KV_ERR_INVALID_ARG = 1,        /* null pointer, negative size, bad geometry        */
+    KV_ERR_INDIVISIBLE_DEGREE = 2, /* p does not divide H and H does not divide p (R2) */
+    KV_ERR_UNKNOWN_GROUP = 3,      /* group not an aligned segment of a degree in {1} U P */
+    KV_ERR_RANK_OUT_OF_RANGE = 4,  /* weight view rank outside [0, m)          */
+    KV_ERR_INDIVISIBLE_EXTENT = 5, /* weight extent not divisible by m         */
+    KV_ERR_OUT_OF_BLOCKS = 6,      /* destination does not fit; state unchanged */
+    KV_ERR_BAD_BLOCK_TABLE = 7,    /* wrong length, out of range, not held, or shared (R14) */
+    KV_ERR_DUPLICATE_REQUEST = 8,  /* same req_id twice in one plan (S:207 DoubleAllocate) */
+    KV_ERR_BAD_STATE = 9,          /* call out of order (e.g. reshard after commit)    */
+    KV_ERR_CUDA = 10               /* a CUDA runtime call failed; see kv_last_error()  */
+} kv_status;
+
+/* Model KV geometry.  block_base = B (DP tokens per block).  Requirement:
+ * B*d*e (one "atom", the bytes of B tokens of one head) is a multiple of 16. */
+typedef struct {
+    int32_t num_layers;
+    int32_t num_kv_heads;
+    int32_t head_dim;
+    int32_t block_base;
+    int32_t elem_bytes;
+} kv_geometry;
+
+/* A DP engine (degree 1) or an aligned TP group [first_gpu, first_gpu+degree)
+ * (only aligned contiguous segments; first_gpu % degree == 0). */
+typedef struct {
+    int32_t first_gpu;
+    int32_t degree;
+} kv_group;
+
+/* One live request to re-lay-out.  src_blocks: host array of the request's
+ * block IDs at the source degree, length n_src_blocks == ceil(num_tokens /
+ * B(src.degree)) (uniform across the source group, R6).  Caller-owned. */
+typedef struct {
+    int64_t req_id;
+    int32_t num_tokens;
+    kv_group src;
+    const int32_t* src_blocks;
+    int32_t n_src_blocks;
+    kv_group dst;
+} kv_request;
+
+typedef struct kv_cache kv_cache; /* opaque: pools, allocator bitmaps      */
+typedef struct kv_plan kv_plan;   /* opaque: validated, allocated switch    */
+
+/* Plan statistics (algorithmic bytes). */
+typedef struct {
+    int64_t n_requests;     /* requests in the plan                         */
+    int64_t n_moving;       /* requests with src != dst                     */
+    int64_t n_atoms;        /* source atoms read (B*d*e bytes each)         */
+    int64_t n_atom_writes;  /* destination atoms written (>= n_atoms, GQA)  */
+    int64_t atom_bytes;     /* B*d*e                                        */
+    int64_t payload_bytes;  /* n_atom_writes * atom_bytes                   */
+    int64_t h2d_bytes;      /* descriptor bytes uploaded per plan           */
+    int64_t n_segments;     /* (request, source GPU) work segments          */
+} kv_plan_stats;
+
+/* ---------------------------------------------------------------- cache */
+
+/*
+ * kv_cache_create: register the per-GPU paged KV pools and the set of
+ * supported TP degrees P (the paper's per-worker persistent pool P:223, the
+ * fixed-M physical block pool P:334-340, aligned groups P:421-424).
+ *   geom            host, layout geometry (validated; see kv_geometry)
+ *   n_gpus          number of pools ("GPUs"/engines); several pools may live
+ *                   on one physical device ("virtual ranks")
+ *   num_blocks      host [n_gpus], blocks in each pool (same IDs in every layer, R5)
+ *   layer_base      host [n_gpus * num_layers] device pointers, row-major by
+ *                   GPU: layer l of GPU g starts at layer_base[g*L + l] and
+ *                   holds num_blocks[g] * M bytes, 16-byte aligned.  The
+ *                   pointers must be dereferenceable from the device that
+ *                   later runs kv_reshard (local, same-device virtual ranks,
+ *                   or peer/IPC-mapped over NVLink).  May be fake (never
+ *                   dereferenced) if kv_reshard is never called.
+ *   tp_degrees      host [n_degrees], the set P (degree 1 is always legal)
+ * All blocks start free.  No CUDA call is made here.
+ */
+kv_status kv_cache_create(const kv_geometry* geom, int32_t n_gpus, const int32_t* num_blocks,
+                          void* const* layer_base, const int32_t* tp_degrees, int32_t n_degrees,
+                          kv_cache** out);
+void kv_cache_destroy(kv_cache* cache);
+
+/* Layout helpers (Eq.2/Eq.3): *h_loc = H_loc(p), *block_tokens = B(p),
+ * *block_bytes = M.  KV_ERR_INDIVISIBLE_DEGREE if neither p | H nor H | p. */
+kv_status kv_layout(const kv_geometry* geom, int32_t degree, int32_t* h_loc, int32_t* block_tokens,
+                    int64_t* block_bytes);
+/* *n = ceil(num_tokens / B(degree)) blocks per rank. */
+kv_status kv_blocks_for(const kv_geometry* geom, int32_t num_tokens, int32_t degree, int32_t* n);
+
+/* ------------------------------------------------------------ allocator */
+
+/* kv_alloc: take the n lowest block IDs free on every GPU of group g and
+ * mark them held on all members (Alg.1 "KVCacheMgr.Allocate" P:493; uniform
+ * IDs R6, lowest-first R8).  out_ids: host [n].  OUT_OF_BLOCKS leaves the
+ * state unchanged. */
+kv_status kv_alloc(kv_cache* cache, kv_group g, int32_t n, int32_t* out_ids);
+/* kv_reserve: mark the given IDs held on every GPU of g (registers a live
+ * request whose table already exists).  BAD_BLOCK_TABLE if any ID is out of
+ * range or already held; state unchanged on error. */
+kv_status kv_reserve(kv_cache* cache, kv_group g, const int32_t* ids, int32_t n);
+/* kv_free: release IDs on every GPU of g.  BAD_BLOCK_TABLE if any is
+ * not held; state unchanged on error. */
+kv_status kv_free(kv_cache* cache, kv_group g, const int32_t* ids, int32_t n);
+/* *n_free = free blocks of pool gpu (conservation checks). */
+kv_status kv_free_count(const kv_cache* cache, int32_t gpu, int32_t* n_free);
+/* held: host [num_blocks[gpu]] bytes, 1 = held. */
+kv_status kv_held_mask(const kv_cache* cache, int32_t gpu, uint8_t* held);
+
+/* ---------------------------------------------------------------- switch */
+
+/*
+ * kv_plan_switch: validate and plan the re-layout of reqs[0..n_reqs) (host,
+ * caller order = the globally agreed Q_wait order) and allocate every
+ * destination table (a1-a3 of DESIGN.md section 1).
+ *   For each request with src != dst: n1 = ceil(T / B(dst.degree)) IDs, the
+ *   lowest free on every destination GPU, not taken earlier in this plan
+ *   (R6, R8).  src == dst requests are no-ops that keep their table (R12).
+ * Validation (state unchanged on any error):
+ *   INVALID_ARG          null pointers, n_reqs < 0, num_tokens < 0
+ *   UNKNOWN_GROUP        group not aligned / degree not in {1} U P / out of range
+ *   INDIVISIBLE_DEGREE   degree incompatible with H (R2)
+ *   BAD_BLOCK_TABLE      n_src_blocks != ceil(T/B(src)), ID out of range, ID not
+ *                        held on every source GPU, or an ID in two requests (R14)
+ *   DUPLICATE_REQUEST    req_id repeated
+ *   OUT_OF_BLOCKS        destination does not fit next to the sources (R13)
+ * The plan is a deterministic function of (cache state, reqs): every SPMD
+ * process builds the identical plan.  No CUDA call is made here; descriptors
+ * are uploaded to the device at the first kv_reshard.
+ */
+kv_status kv_plan_switch(kv_cache* cache, const kv_request* reqs, int32_t n_reqs, kv_plan** out);
+
+/* kv_plan_upload: enqueue on `stream` the host->device copy of the plan's
+ * descriptors (segments, tables, remap records: kv_plan_stats.h2d_bytes,
+ * from pinned staging) into a stream-ordered device workspace.  Optional:
+ * kv_reshard / kv_remap_block_tables upload on first use.  Lets a caller
+ * prefetch descriptors while earlier work runs.  Idempotent. */
+kv_status kv_plan_upload(kv_plan* plan, void* stream);
+
+/*
+ * kv_reshard: move the bytes (a4, the hot loop).  Enqueues on `stream`
+ * (a cudaStream_t, NULL = legacy default) the copy of every atom whose
+ * canonical source replica (R10) lives on pool `gpu`, or of all atoms when
+ * gpu == -1 (all pools addressable from the current device, e.g. virtual
+ * ranks on one B200).  An atom (request, layer, K/V, head, chunk of B
+ * tokens) is B*d*e contiguous bytes in every degree's layout; it is read
+ * once and written to each destination replica (1, or p/H under GQA
+ * replication, R2), local or over NVLink peer mappings.  Idempotent until
+ * the plan is committed.  The caller must order kv_remap_block_tables after
+ * every GPU's reshard has completed (stream order, or a group barrier, a5).
+ * Current device must be the one that can address the pools.
+ */
+kv_status kv_reshard(kv_plan* plan, int32_t gpu, void* stream);
+
+/* Sizes of pool gpu's table after the switch: *n_resident requests resident
+ * on gpu (dst group contains gpu), *n_ids block IDs in their tables. */
+kv_status kv_plan_resident(const kv_plan* plan, int32_t gpu, int32_t* n_resident, int32_t* n_ids);
+
+/*
+ * kv_remap_block_tables: a6 + a7.  Enqueues on `stream` a kernel writing
+ * the post-switch "logical table" of pool gpu for the plan's
+ * requests resident on it, in plan order:
+ *   req_ptr       device int32 [n_resident + 1]  CSR row pointers
+ *   block_ids     device int32 [n_ids]           destination block IDs
+ *   per_req_meta  device int32 [4 * n_resident]  {plan request index, B(p),
+ *                 H_loc(p), first head held by gpu} = the per-request
+ *                 "stride and capacity" the attention kernel needs
+ * The first call on a plan (any gpu) commits it on the host: every moving
+ * request's source IDs are released on its source GPUs (sources are freed
+ * only after the group barrier, R13).  Requests absent from the plan are not
+ * listed and are untouched.
+ */
+kv_status kv_remap_block_tables(kv_plan* plan, int32_t gpu, int32_t* req_ptr, int32_t* block_ids,
+                                int32_t* per_req_meta, void* stream);
+
+/* Host copies of every destination table, in plan order: dst_ptr host
+ * [n_reqs+1], dst_ids host [dst_ptr[n_reqs]] (pass dst_ids = NULL to size). */
+kv_status kv_plan_dst_tables(const kv_plan* plan, int32_t* dst_ptr, int32_t* dst_ids);
+/* Statistics; bytes_matrix (host [n_gpus*n_gpus] or NULL) receives the
+ * destination bytes each source GPU sends to each destination GPU (row =
+ * source), the input of the roofline of SURVEY 8(d). */
+kv_status kv_plan_get_stats(const kv_plan* plan, kv_plan_stats* stats, int64_t* bytes_matrix);
+/* Destroy a plan.  A plan that was never committed rolls back its
+ * destination allocations. */
+void kv_plan_destroy(kv_plan* plan);
+
+/* ------------------------------------------------------- weight views */
+
+typedef enum {
+    KV_W_COLUMN = 0,   /* column-parallel [out, in]: rank takes out-rows */
+    KV_W_ROW = 1,      /* row-parallel [out, in]: rank takes in-columns  */
+    KV_W_QKV = 2       /* fused stacked [Q; K; V] rows, head-aligned (R17, GQA R2)    */
+} kv_weight_kind;
+
+typedef struct {
+    const void* ptr;      /* device (or host) base of the full matrix     */
+    int64_t rows;         /* out features                                  */
+    int64_t cols;         /* in features                                   */
+    int64_t ld;           /* elements between consecutive rows (>= cols)  */
+    int32_t elem_bytes;
+    int32_t kind;         /* kv_weight_kind                                */
+    int32_t num_q_heads;  /* KV_W_QKV only                                 */
+    int32_t num_kv_heads; /* KV_W_QKV only                                 */
+    int32_t head_dim;     /* KV_W_QKV only                                 */
+} kv_weight_desc;
+
+typedef struct {
+    const void* ptr;  /* first element of the segment (inside the full matrix) */
+    int64_t rows, cols, ld;
+    int64_t row0, col0; /* position of the segment in the full matrix       */
+} kv_view_segment;
+
+typedef struct {
+    int32_t n_seg;            /* 1 (COLUMN, ROW) or 3 (QKV: Q, K, V)          */
+    int32_t elem_bytes;
+    kv_view_segment seg[3];
+} kv_view;
+
+/*
+ * weight_shard_view: Eq.1 W_active^(r) = View(W_full, dim, r, m).
+ * Pure pointer arithmetic on the caller's matrix: 0 bytes moved or
+ * allocated; the segments alias the full matrix.  rank in [0, m)
+ * else RANK_OUT_OF_RANGE; the sharded extent must divide by m (QKV: Hq % m
+ * and Hkv % m, or m % Hkv under GQA replication) else INDIVISIBLE_EXTENT.
+ */
+kv_status weight_shard_view(const kv_weight_desc* full, int32_t rank, int32_t degree, kv_view* out);
+
+/* Test utility (DESIGN.md a8): gather a view's segments, in order, into the
+ * contiguous device buffer dst (row-major, total rows x cols of the
+ * segments) on `stream`.  Used only to check views against the oracle. */
+kv_status kv_gather_view(const kv_view* view, void* dst, void* stream);
+
+/* ------------------------------------------------------- multi-process */
+
+/* CUDA IPC helpers for peer pools (one process per GPU).  kv_ipc_export
+ * writes a 64-byte handle of the allocation containing dptr plus dptr's
+ * offset inside it; kv_ipc_import maps it (lazy peer access) in this
+ * process and returns the base + offset pointer; kv_ipc_close unmaps
+ * (pass the pointer kv_ipc_import returned). */
+kv_status kv_ipc_export(const void* dptr, uint8_t handle[64], uint64_t* offset);
+kv_status kv_ipc_import(const uint8_t handle[64], uint64_t offset, void** dptr);
+kv_status kv_ipc_close(void* dptr, uint64_t offset);
+
+/* Make all prior writes of this device (incl. NVLink peer stores) visible
+ * system-wide before a host-side barrier: synchronizes `stream`. */
+kv_status kv_stream_sync(void* stream);
+
+/* ---------------------------------------------------------------- misc */
+const char* kv_strerror(kv_status s);
+const char* kv_last_error(void);
+/* Number of kernels this library launched since load (evidence counter). */
+int64_t kv_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FLYKV_H */

@@ -130,6 +130,7 @@ enum { OR_OK = 0, OR_OUT_OF_BLOCKS = 6, OR_INVALID = 1 };
  * to its destination group/layout.
  *
  *   pools[gpu]       host buffer [L][num_blocks[gpu]][M] bytes, modified
+ *   do_copy          0: allocation and release only (pools may be NULL)
  *   held[gpu][b]     1 if block b of gpu is held by any live request
  *                    (moving or not); updated: dst IDs set, src IDs cleared
  *   request i: T[i] tokens, source group [src_g0[i], +src_p[i]) with table
@@ -140,7 +141,7 @@ enum { OR_OK = 0, OR_OUT_OF_BLOCKS = 6, OR_INVALID = 1 };
  * oracle is not transactional; callers discard it).
  */
 int32_t or_switch(const or_geom* g, int32_t n_gpus, const int32_t* num_blocks,
-                  uint8_t** pools, uint8_t** held, int32_t n_reqs,
+                  uint8_t** pools, int32_t do_copy, uint8_t** held, int32_t n_reqs,
                   const int32_t* T, const int32_t* src_g0, const int32_t* src_p,
                   const int32_t* src_ptr, const int32_t* src_ids,
                   const int32_t* dst_g0, const int32_t* dst_p,
@@ -182,6 +183,7 @@ int32_t or_switch(const or_geom* g, int32_t n_gpus, const int32_t* num_blocks,
         if (k < n1) return OR_OUT_OF_BLOCKS;
 
         /* 2. copy, token by token (R9: whole B-token atoms) */
+        if (!do_copy) continue;  /* tables-only mode (full-size sampled checks) */
         int32_t t_end = ((T[i] + g->B - 1) / g->B) * g->B;
         int32_t reps = or_replicas(g, dst_p[i]);
         for (l = 0; l < g->L; l++)

@@ -75,7 +75,7 @@ def lib():
         L.or_locate.argtypes = [G, C.c_int32, C.c_int32, _P32, C.c_int32, C.c_int32,
                                 C.c_int32, C.c_int32, _P32, C.POINTER(C.c_int64)]
         L.or_locate.restype = None
-        L.or_switch.argtypes = [G, C.c_int32, _P32, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
+        L.or_switch.argtypes = [G, C.c_int32, _P32, C.POINTER(C.c_void_p), C.c_int32, C.POINTER(C.c_void_p),
                                 C.c_int32, _P32, _P32, _P32, _P32, _P32, _P32, _P32, _P32, _P32,
                                 C.c_int32]
         L.or_switch.restype = C.c_int32
@@ -139,17 +139,21 @@ class Req:
     dst: tuple  # (first_gpu, degree)
 
 
-def switch(g: Geom, pools: list, held: list, reqs: list):
+def switch(g: Geom, pools: list, held: list, reqs: list, copy: bool = True):
     """Run the oracle switch in place.
 
-    pools[gpu]: contiguous uint8 array of L*num_blocks*M bytes ([L][nb][M]).
+    pools[gpu]: contiguous uint8 array of L*num_blocks*M bytes ([L][nb][M]),
+                or None when copy=False (allocation/release only).
     held[gpu]:  uint8 array [num_blocks], 1 = held by a live request.
     Returns (status, dst_tables as list of np.int32 arrays).
     """
     M = block_bytes(g)
-    nb = _i32([p.size // (g.L * M) for p in pools])
-    for p, n in zip(pools, nb):
-        assert p.dtype == np.uint8 and p.flags.c_contiguous and p.size == g.L * int(n) * M
+    if copy:
+        nb = _i32([p.size // (g.L * M) for p in pools])
+        for p, n in zip(pools, nb):
+            assert p.dtype == np.uint8 and p.flags.c_contiguous and p.size == g.L * int(n) * M
+    else:
+        nb = _i32([h.size for h in held])
     for hb, n in zip(held, nb):
         assert hb.dtype == np.uint8 and hb.flags.c_contiguous and hb.size == int(n)
     n = len(reqs)
@@ -166,9 +170,9 @@ def switch(g: Geom, pools: list, held: list, reqs: list):
     cap = max(cap, 1)
     dptr = np.zeros(n + 1, dtype=np.int32)
     dids = np.zeros(cap, dtype=np.int32)
-    pool_ptrs = (C.c_void_p * len(pools))(*[p.ctypes.data for p in pools])
+    pool_ptrs = (C.c_void_p * len(held))(*([p.ctypes.data for p in pools] if copy else [0] * len(held)))
     held_ptrs = (C.c_void_p * len(held))(*[h.ctypes.data for h in held])
-    st = lib().or_switch(C.byref(g.c()), len(pools), _ptr(nb), pool_ptrs, held_ptrs, n,
+    st = lib().or_switch(C.byref(g.c()), len(held), _ptr(nb), pool_ptrs, int(copy), held_ptrs, n,
                          _ptr(T), _ptr(sg0), _ptr(sp), _ptr(sptr), _ptr(sids), _ptr(dg0), _ptr(dp),
                          _ptr(dptr), _ptr(dids), cap)
     tabs = [dids[dptr[i]:dptr[i + 1]].copy() for i in range(n)] if st == 0 else None

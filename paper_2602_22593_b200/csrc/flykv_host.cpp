@@ -1,0 +1,795 @@
+// flykv_host.cpp -- host side of libflykv.so: the C ABI declared in
+// include/flykv.h, the block allocator (per-GPU bitmaps), the switch planner
+// and the launches of the sm_100a kernels in flykv_kernels.cu.
+//
+// Citations: P:n = PAPER.md line, S:n = SPEC.md line, Rn = DESIGN.md reading.
+#include "flykv.h"
+
+#include <algorithm>
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <unordered_set>
+#include <vector>
+
+#include "flykv_internal.h"
+
+using namespace flykv;
+
+// ------------------------------------------------------------ errors
+static thread_local std::string g_err;
+static std::atomic<int64_t> g_launches{0};
+
+static kv_status fail(kv_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
+static kv_status cuda_fail(cudaError_t e, const char* what) {
+    return fail(KV_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define CUDA_TRY(call)                                            \
+    do {                                                          \
+        cudaError_t _e = (call);                                  \
+        if (_e != cudaSuccess) return cuda_fail(_e, #call);       \
+    } while (0)
+
+// ------------------------------------------------------------ objects
+struct kv_cache {
+    kv_geometry geo;
+    int32_t n_gpus = 0;
+    std::vector<int32_t> num_blocks;
+    std::vector<void*> layer_base;        // [n_gpus * L]
+    std::vector<int32_t> degrees;         // the set P (degree 1 always legal)
+    std::vector<std::vector<uint64_t>> held;  // per GPU bitmap, bit = held
+    int64_t M = 0;                        // block bytes per layer
+    int64_t atom_bytes = 0;               // B*d*e
+    // device copy of layer_base (uploaded once per device)
+    int dev = -1;
+    char** d_layer_base = nullptr;
+    // pinned staging for descriptor uploads, guarded by an event
+    void* stage = nullptr;
+    size_t stage_bytes = 0;
+    cudaEvent_t stage_ev = nullptr;
+    bool stage_pending = false;
+};
+
+struct ReqPlan {
+    int64_t req_id;
+    int32_t T;
+    kv_group src, dst;
+    int32_t src_off, n0;  // source table in plan->tables
+    int32_t dst_off, n1;  // destination table in plan->tables
+    bool moving;
+};
+
+enum { PLAN_PLANNED = 0, PLAN_COMMITTED = 1 };
+
+struct kv_plan {
+    kv_cache* c = nullptr;
+    int state = PLAN_PLANNED;
+    std::vector<ReqPlan> reqs;
+    std::vector<int32_t> tables;
+    std::vector<Seg> segs;
+    std::vector<int64_t> seg_begin;
+    std::vector<int32_t> gpu_seg_lo, gpu_seg_hi;
+    std::vector<int64_t> bytes;  // n_gpus * n_gpus
+    std::vector<int32_t> n_res, n_res_ids;
+    std::vector<ReqRec> recs;
+    kv_plan_stats st{};
+    // device workspace: [seg_begin | segs | tables | recs]
+    int dev = -1;
+    char* dbuf = nullptr;
+    size_t dbytes = 0;
+    size_t off_seg_begin = 0, off_segs = 0, off_tables = 0, off_recs = 0;
+    cudaStream_t last_stream = nullptr;
+};
+
+// ------------------------------------------------------------ helpers
+static inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+static kv_status check_geometry(const kv_geometry* g) {
+    if (!g) return fail(KV_ERR_INVALID_ARG, "geometry is NULL");
+    if (g->num_layers < 1 || g->num_kv_heads < 1 || g->head_dim < 1 || g->block_base < 1 ||
+        g->elem_bytes < 1)
+        return fail(KV_ERR_INVALID_ARG, "geometry fields must be >= 1");
+    int64_t atom = (int64_t)g->block_base * g->head_dim * g->elem_bytes;
+    if (atom % 16)
+        return fail(KV_ERR_INVALID_ARG, "B*d*e = %lld bytes is not a multiple of 16", (long long)atom);
+    int64_t M = 2 * (int64_t)g->num_kv_heads * atom;
+    if (M > ((int64_t)1 << 40)) return fail(KV_ERR_INVALID_ARG, "block too large");
+    return KV_OK;
+}
+
+// Degree compatibility with H (R2): p | H, or H | p (GQA replication).
+static kv_status check_degree(int32_t H, int32_t p) {
+    if (p < 1) return fail(KV_ERR_UNKNOWN_GROUP, "degree %d < 1", p);
+    if (p <= H ? (H % p) : (p % H))
+        return fail(KV_ERR_INDIVISIBLE_DEGREE, "degree %d incompatible with %d KV heads", p, H);
+    return KV_OK;
+}
+
+// Aligned contiguous segment of a supported degree (R12).
+static kv_status check_group(const kv_cache* c, kv_group g) {
+    if (g.degree < 1) return fail(KV_ERR_UNKNOWN_GROUP, "degree %d < 1", g.degree);
+    if (g.degree != 1 &&
+        std::find(c->degrees.begin(), c->degrees.end(), g.degree) == c->degrees.end())
+        return fail(KV_ERR_UNKNOWN_GROUP, "degree %d not in the pool's TP degrees", g.degree);
+    if (g.first_gpu < 0 || g.first_gpu % g.degree || g.first_gpu + g.degree > c->n_gpus)
+        return fail(KV_ERR_UNKNOWN_GROUP, "group [%d, +%d) is not an aligned segment of %d GPUs",
+                    g.first_gpu, g.degree, c->n_gpus);
+    return check_degree(c->geo.num_kv_heads, g.degree);
+}
+
+static inline bool bit_get(const std::vector<uint64_t>& bm, int32_t b) {
+    return (bm[(size_t)b >> 6] >> (b & 63)) & 1u;
+}
+static inline void bit_set(std::vector<uint64_t>& bm, int32_t b) { bm[(size_t)b >> 6] |= 1ull << (b & 63); }
+static inline void bit_clr(std::vector<uint64_t>& bm, int32_t b) { bm[(size_t)b >> 6] &= ~(1ull << (b & 63)); }
+
+static int32_t group_min_blocks(const kv_cache* c, kv_group g) {
+    int32_t nb = c->num_blocks[g.first_gpu];
+    for (int32_t r = 1; r < g.degree; ++r) nb = std::min(nb, c->num_blocks[g.first_gpu + r]);
+    return nb;
+}
+
+// The n lowest IDs free on every GPU of g (R6, R8): OR the members' held
+// words, then walk free bits with count-trailing-zeros.  Marks them held on
+// every member when found.  Returns false (nothing marked) if fewer than n.
+static bool alloc_lowest(kv_cache* c, kv_group g, int32_t n, int32_t* out) {
+    if (n == 0) return true;
+    const int32_t nb = group_min_blocks(c, g);
+    const int32_t words = (nb + 63) >> 6;
+    int32_t got = 0;
+    for (int32_t w = 0; w < words && got < n; ++w) {
+        uint64_t used = 0;
+        for (int32_t r = 0; r < g.degree; ++r) used |= c->held[g.first_gpu + r][w];
+        uint64_t fr = ~used;
+        const int32_t top = nb - (w << 6);
+        if (top < 64) fr &= (top <= 0) ? 0ull : ((1ull << top) - 1);
+        while (fr && got < n) {
+            out[got++] = (w << 6) + __builtin_ctzll(fr);
+            fr &= fr - 1;
+        }
+    }
+    if (got < n) return false;
+    for (int32_t r = 0; r < g.degree; ++r)
+        for (int32_t k = 0; k < n; ++k) bit_set(c->held[g.first_gpu + r], out[k]);
+    return true;
+}
+
+// ------------------------------------------------------------ cache API
+extern "C" kv_status kv_cache_create(const kv_geometry* geom, int32_t n_gpus, const int32_t* num_blocks,
+                                     void* const* layer_base, const int32_t* tp_degrees, int32_t n_degrees,
+                                     kv_cache** out) {
+    if (!out) return fail(KV_ERR_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    kv_status s = check_geometry(geom);
+    if (s) return s;
+    if (n_gpus < 1 || !num_blocks || !layer_base || n_degrees < 0 || (n_degrees > 0 && !tp_degrees))
+        return fail(KV_ERR_INVALID_ARG, "bad pool arguments");
+    const int32_t L = geom->num_layers;
+    for (int32_t g = 0; g < n_gpus; ++g) {
+        if (num_blocks[g] < 0) return fail(KV_ERR_INVALID_ARG, "num_blocks[%d] < 0", g);
+        for (int32_t l = 0; l < L; ++l)
+            if ((uintptr_t)layer_base[(size_t)g * L + l] & 15)
+                return fail(KV_ERR_INVALID_ARG, "layer_base[%d][%d] not 16-byte aligned", g, l);
+    }
+    for (int32_t i = 0; i < n_degrees; ++i) {
+        s = check_degree(geom->num_kv_heads, tp_degrees[i]);
+        if (s) return s;
+    }
+    kv_cache* c = new (std::nothrow) kv_cache();
+    if (!c) return fail(KV_ERR_INVALID_ARG, "out of host memory");
+    c->geo = *geom;
+    c->n_gpus = n_gpus;
+    c->num_blocks.assign(num_blocks, num_blocks + n_gpus);
+    c->layer_base.assign(layer_base, layer_base + (size_t)n_gpus * L);
+    c->degrees.assign(tp_degrees, tp_degrees + n_degrees);
+    c->held.resize(n_gpus);
+    for (int32_t g = 0; g < n_gpus; ++g) c->held[g].assign(((size_t)num_blocks[g] + 63) / 64, 0ull);
+    c->atom_bytes = (int64_t)geom->block_base * geom->head_dim * geom->elem_bytes;
+    c->M = 2 * (int64_t)geom->num_kv_heads * c->atom_bytes;
+    *out = c;
+    return KV_OK;
+}
+
+extern "C" void kv_cache_destroy(kv_cache* c) {
+    if (!c) return;
+    if (c->stage_ev) {
+        cudaEventSynchronize(c->stage_ev);
+        cudaEventDestroy(c->stage_ev);
+    }
+    if (c->stage) cudaFreeHost(c->stage);
+    if (c->d_layer_base) cudaFree(c->d_layer_base);
+    delete c;
+}
+
+extern "C" kv_status kv_layout(const kv_geometry* geom, int32_t degree, int32_t* h_loc, int32_t* block_tokens,
+                               int64_t* block_bytes) {
+    kv_status s = check_geometry(geom);
+    if (s) return s;
+    s = check_degree(geom->num_kv_heads, degree);
+    if (s) return s;
+    Layout L = layout_of(geom->num_kv_heads, degree);
+    if (h_loc) *h_loc = L.hloc;
+    if (block_tokens) *block_tokens = geom->block_base * L.k;
+    if (block_bytes)
+        *block_bytes = 2 * (int64_t)geom->num_kv_heads * geom->block_base * geom->head_dim * geom->elem_bytes;
+    return KV_OK;
+}
+
+extern "C" kv_status kv_blocks_for(const kv_geometry* geom, int32_t num_tokens, int32_t degree, int32_t* n) {
+    int32_t bt = 0;
+    kv_status s = kv_layout(geom, degree, nullptr, &bt, nullptr);
+    if (s) return s;
+    if (num_tokens < 0 || !n) return fail(KV_ERR_INVALID_ARG, "num_tokens < 0 or n NULL");
+    *n = (int32_t)ceil_div(num_tokens, bt);
+    return KV_OK;
+}
+
+// ------------------------------------------------------------ allocator API
+extern "C" kv_status kv_alloc(kv_cache* c, kv_group g, int32_t n, int32_t* out_ids) {
+    if (!c || n < 0 || (n > 0 && !out_ids)) return fail(KV_ERR_INVALID_ARG, "bad kv_alloc arguments");
+    kv_status s = check_group(c, g);
+    if (s) return s;
+    if (!alloc_lowest(c, g, n, out_ids))
+        return fail(KV_ERR_OUT_OF_BLOCKS, "%d blocks not free on group [%d,+%d)", n, g.first_gpu, g.degree);
+    return KV_OK;
+}
+
+static kv_status check_ids(const kv_cache* c, kv_group g, const int32_t* ids, int32_t n, bool want_held) {
+    const int32_t nb = group_min_blocks(c, g);
+    std::vector<uint64_t> seen(((size_t)nb + 63) / 64, 0ull);
+    for (int32_t k = 0; k < n; ++k) {
+        const int32_t b = ids[k];
+        if (b < 0 || b >= nb) return fail(KV_ERR_BAD_BLOCK_TABLE, "block id %d out of range", b);
+        if (bit_get(seen, b)) return fail(KV_ERR_BAD_BLOCK_TABLE, "block id %d repeated", b);
+        bit_set(seen, b);
+        for (int32_t r = 0; r < g.degree; ++r)
+            if (bit_get(c->held[g.first_gpu + r], b) != want_held)
+                return fail(KV_ERR_BAD_BLOCK_TABLE, "block id %d is %s on GPU %d", b,
+                            want_held ? "not held" : "already held", g.first_gpu + r);
+    }
+    return KV_OK;
+}
+
+extern "C" kv_status kv_reserve(kv_cache* c, kv_group g, const int32_t* ids, int32_t n) {
+    if (!c || n < 0 || (n > 0 && !ids)) return fail(KV_ERR_INVALID_ARG, "bad kv_reserve arguments");
+    kv_status s = check_group(c, g);
+    if (s) return s;
+    s = check_ids(c, g, ids, n, false);
+    if (s) return s;
+    for (int32_t r = 0; r < g.degree; ++r)
+        for (int32_t k = 0; k < n; ++k) bit_set(c->held[g.first_gpu + r], ids[k]);
+    return KV_OK;
+}
+
+extern "C" kv_status kv_free(kv_cache* c, kv_group g, const int32_t* ids, int32_t n) {
+    if (!c || n < 0 || (n > 0 && !ids)) return fail(KV_ERR_INVALID_ARG, "bad kv_free arguments");
+    kv_status s = check_group(c, g);
+    if (s) return s;
+    s = check_ids(c, g, ids, n, true);
+    if (s) return s;
+    for (int32_t r = 0; r < g.degree; ++r)
+        for (int32_t k = 0; k < n; ++k) bit_clr(c->held[g.first_gpu + r], ids[k]);
+    return KV_OK;
+}
+
+extern "C" kv_status kv_free_count(const kv_cache* c, int32_t gpu, int32_t* n_free) {
+    if (!c || !n_free || gpu < 0 || gpu >= c->n_gpus) return fail(KV_ERR_INVALID_ARG, "bad arguments");
+    int64_t held = 0;
+    for (uint64_t w : c->held[gpu]) held += __builtin_popcountll(w);
+    *n_free = (int32_t)(c->num_blocks[gpu] - held);
+    return KV_OK;
+}
+
+extern "C" kv_status kv_held_mask(const kv_cache* c, int32_t gpu, uint8_t* held) {
+    if (!c || !held || gpu < 0 || gpu >= c->n_gpus) return fail(KV_ERR_INVALID_ARG, "bad arguments");
+    for (int32_t b = 0; b < c->num_blocks[gpu]; ++b) held[b] = bit_get(c->held[gpu], b) ? 1 : 0;
+    return KV_OK;
+}
+
+// ------------------------------------------------------------ planner
+extern "C" kv_status kv_plan_switch(kv_cache* c, const kv_request* reqs, int32_t n_reqs, kv_plan** out) {
+    if (!c || !out || n_reqs < 0 || (n_reqs > 0 && !reqs))
+        return fail(KV_ERR_INVALID_ARG, "bad kv_plan_switch arguments");
+    *out = nullptr;
+    const kv_geometry& G = c->geo;
+    const int32_t H = G.num_kv_heads, L = G.num_layers, B = G.block_base;
+    const int32_t n = c->n_gpus;
+
+    // ---- a2 validation (no state change) ----
+    std::unordered_set<int64_t> ids_seen;
+    std::vector<std::vector<uint64_t>> in_plan(n);
+    for (int32_t g = 0; g < n; ++g) in_plan[g].assign(c->held[g].size(), 0ull);
+    int64_t total_src = 0, total_dst_bound = 0;
+    for (int32_t i = 0; i < n_reqs; ++i) {
+        const kv_request& r = reqs[i];
+        if (r.num_tokens < 0) return fail(KV_ERR_INVALID_ARG, "request %d: num_tokens < 0", i);
+        kv_status s = check_group(c, r.src);
+        if (s) return s;
+        s = check_group(c, r.dst);
+        if (s) return s;
+        if (!ids_seen.insert(r.req_id).second)
+            return fail(KV_ERR_DUPLICATE_REQUEST, "req_id %lld repeated", (long long)r.req_id);
+        const Layout l0 = layout_of(H, r.src.degree);
+        const int64_t n0 = ceil_div(r.num_tokens, (int64_t)B * l0.k);
+        if (r.n_src_blocks != n0 || (n0 > 0 && !r.src_blocks))
+            return fail(KV_ERR_BAD_BLOCK_TABLE, "request %d: %d source blocks, expected %lld", i,
+                        r.n_src_blocks, (long long)n0);
+        const int32_t nb = group_min_blocks(c, r.src);
+        for (int32_t k = 0; k < r.n_src_blocks; ++k) {
+            const int32_t b = r.src_blocks[k];
+            if (b < 0 || b >= nb) return fail(KV_ERR_BAD_BLOCK_TABLE, "request %d: block %d out of range", i, b);
+            for (int32_t q = 0; q < r.src.degree; ++q) {
+                const int32_t g = r.src.first_gpu + q;
+                if (!bit_get(c->held[g], b))
+                    return fail(KV_ERR_BAD_BLOCK_TABLE, "request %d: block %d not held on GPU %d", i, b, g);
+                if (bit_get(in_plan[g], b))
+                    return fail(KV_ERR_BAD_BLOCK_TABLE, "block %d of GPU %d appears twice in the plan (R14)", b, g);
+                bit_set(in_plan[g], b);
+            }
+        }
+        total_src += r.n_src_blocks;
+        total_dst_bound += ceil_div(r.num_tokens, B);
+    }
+
+    kv_plan* p = new (std::nothrow) kv_plan();
+    if (!p) return fail(KV_ERR_INVALID_ARG, "out of host memory");
+    p->c = c;
+    p->reqs.resize(n_reqs);
+    p->tables.reserve((size_t)(total_src + total_dst_bound + n_reqs));
+
+    // source tables first
+    for (int32_t i = 0; i < n_reqs; ++i) {
+        const kv_request& r = reqs[i];
+        ReqPlan& q = p->reqs[i];
+        q.req_id = r.req_id;
+        q.T = r.num_tokens;
+        q.src = r.src;
+        q.dst = r.dst;
+        q.moving = !(r.src.first_gpu == r.dst.first_gpu && r.src.degree == r.dst.degree);
+        q.src_off = (int32_t)p->tables.size();
+        q.n0 = r.n_src_blocks;
+        p->tables.insert(p->tables.end(), r.src_blocks, r.src_blocks + r.n_src_blocks);
+    }
+
+    // ---- a3 allocation, request order, lowest common free IDs ----
+    for (int32_t i = 0; i < n_reqs; ++i) {
+        ReqPlan& q = p->reqs[i];
+        q.dst_off = (int32_t)p->tables.size();
+        if (!q.moving) {  // no-op keeps its table (R12)
+            q.n1 = q.n0;
+            for (int32_t k = 0; k < q.n0; ++k) p->tables.push_back(p->tables[q.src_off + k]);
+            continue;
+        }
+        const Layout l1 = layout_of(H, q.dst.degree);
+        q.n1 = (int32_t)ceil_div(q.T, (int64_t)B * l1.k);
+        p->tables.resize(p->tables.size() + q.n1);
+        if (!alloc_lowest(c, q.dst, q.n1, p->tables.data() + q.dst_off)) {
+            // roll back this plan's allocations: state unchanged
+            for (int32_t j = 0; j < i; ++j) {
+                const ReqPlan& u = p->reqs[j];
+                if (!u.moving) continue;
+                for (int32_t r = 0; r < u.dst.degree; ++r)
+                    for (int32_t k = 0; k < u.n1; ++k) bit_clr(c->held[u.dst.first_gpu + r], p->tables[u.dst_off + k]);
+            }
+            delete p;
+            return fail(KV_ERR_OUT_OF_BLOCKS, "request %d needs %d blocks on group [%d,+%d)", i, q.n1,
+                        q.dst.first_gpu, q.dst.degree);
+        }
+    }
+
+    // ---- work segments: (request, canonical source replica) ----
+    p->bytes.assign((size_t)n * n, 0);
+    struct SegKey { int32_t gpu, idx; };
+    std::vector<Seg> segs;
+    std::vector<int64_t> seg_atoms;
+    for (int32_t i = 0; i < n_reqs; ++i) {
+        const ReqPlan& q = p->reqs[i];
+        if (!q.moving) continue;
+        const int32_t C = (int32_t)ceil_div(q.T, B);
+        if (C == 0) continue;
+        const Layout l0 = layout_of(H, q.src.degree), l1 = layout_of(H, q.dst.degree);
+        for (int32_t r = 0; r < q.src.degree; ++r) {
+            if (l0.rep > 1 && r % l0.rep) continue;  // only the lowest replica is read (R10)
+            Seg s{};
+            s.src_gpu = q.src.first_gpu + r;
+            s.dst_g0 = q.dst.first_gpu;
+            s.C = C;
+            s.nh = l0.hloc;
+            s.h0 = first_head_of_rank(l0, r);
+            s.src_tab = q.src_off;
+            s.dst_tab = q.dst_off;
+            s.hloc0 = l0.hloc;
+            s.k0 = l0.k;
+            s.hloc1 = l1.hloc;
+            s.k1 = l1.k;
+            s.rep1 = l1.rep;
+            segs.push_back(s);
+            const int64_t head_bytes = (int64_t)L * 2 * C * c->atom_bytes;
+            for (int32_t hh = 0; hh < s.nh; ++hh)
+                for (int32_t j = 0; j < l1.rep; ++j) {
+                    const int32_t dg = s.dst_g0 + owner_rank(l1, s.h0 + hh, j);
+                    p->bytes[(size_t)s.src_gpu * n + dg] += head_bytes;
+                }
+        }
+    }
+    // group segments by source GPU (stable: request order within a GPU)
+    std::stable_sort(segs.begin(), segs.end(), [](const Seg& a, const Seg& b) { return a.src_gpu < b.src_gpu; });
+    p->segs = segs;
+    p->seg_begin.resize(segs.size() + 1);
+    p->gpu_seg_lo.assign(n, 0);
+    p->gpu_seg_hi.assign(n, 0);
+    int64_t acc = 0, writes = 0;
+    for (size_t s = 0; s < segs.size(); ++s) {
+        p->seg_begin[s] = acc;
+        const int64_t a = (int64_t)L * 2 * segs[s].C * segs[s].nh;
+        acc += a;
+        writes += a * segs[s].rep1;
+    }
+    p->seg_begin[segs.size()] = acc;
+    for (int32_t g = 0; g < n; ++g) {
+        auto lo = std::lower_bound(segs.begin(), segs.end(), g, [](const Seg& a, int32_t v) { return a.src_gpu < v; });
+        auto hi = std::lower_bound(segs.begin(), segs.end(), g + 1, [](const Seg& a, int32_t v) { return a.src_gpu < v; });
+        p->gpu_seg_lo[g] = (int32_t)(lo - segs.begin());
+        p->gpu_seg_hi[g] = (int32_t)(hi - segs.begin());
+    }
+
+    // ---- per-GPU residency (a6 sizes) and remap records ----
+    p->n_res.assign(n, 0);
+    p->n_res_ids.assign(n, 0);
+    p->recs.resize(n_reqs);
+    int64_t n_moving = 0;
+    for (int32_t i = 0; i < n_reqs; ++i) {
+        const ReqPlan& q = p->reqs[i];
+        n_moving += q.moving;
+        p->recs[i] = ReqRec{q.dst.first_gpu, q.dst.degree, q.n1, q.dst_off};
+        for (int32_t r = 0; r < q.dst.degree; ++r) {
+            p->n_res[q.dst.first_gpu + r] += 1;
+            p->n_res_ids[q.dst.first_gpu + r] += q.n1;
+        }
+    }
+
+    // ---- device workspace layout ----
+    auto align = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    p->off_seg_begin = 0;
+    p->off_segs = align(p->off_seg_begin + p->seg_begin.size() * sizeof(int64_t));
+    p->off_tables = align(p->off_segs + p->segs.size() * sizeof(Seg));
+    p->off_recs = align(p->off_tables + p->tables.size() * sizeof(int32_t));
+    p->dbytes = align(p->off_recs + p->recs.size() * sizeof(ReqRec));
+
+    p->st.n_requests = n_reqs;
+    p->st.n_moving = n_moving;
+    p->st.n_atoms = acc;
+    p->st.n_atom_writes = writes;
+    p->st.atom_bytes = c->atom_bytes;
+    p->st.payload_bytes = writes * c->atom_bytes;
+    p->st.h2d_bytes = (int64_t)p->dbytes;
+    p->st.n_segments = (int64_t)p->segs.size();
+    *out = p;
+    return KV_OK;
+}
+
+// Upload the cache's pool pointer table (once per device) and the plan's
+// descriptors (once per plan) -- the only host->device crossing of a switch.
+static kv_status ensure_device(kv_plan* p, cudaStream_t stream) {
+    kv_cache* c = p->c;
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    if (c->dev != dev) {
+        if (c->d_layer_base) {
+            cudaFree(c->d_layer_base);
+            c->d_layer_base = nullptr;
+        }
+        const size_t nbytes = c->layer_base.size() * sizeof(void*);
+        CUDA_TRY(cudaMalloc(&c->d_layer_base, nbytes));
+        CUDA_TRY(cudaMemcpy(c->d_layer_base, c->layer_base.data(), nbytes, cudaMemcpyHostToDevice));
+        c->dev = dev;
+    }
+    if (p->dbuf) {
+        if (p->dev != dev) return fail(KV_ERR_BAD_STATE, "plan was uploaded to device %d, current is %d", p->dev, dev);
+        return KV_OK;
+    }
+    // pinned staging buffer shared by the cache's plans, reused once the
+    // previous upload has been consumed by the copy engine
+    if (!c->stage_ev) CUDA_TRY(cudaEventCreateWithFlags(&c->stage_ev, cudaEventDisableTiming));
+    if (c->stage_pending) {
+        CUDA_TRY(cudaEventSynchronize(c->stage_ev));
+        c->stage_pending = false;
+    }
+    if (c->stage_bytes < p->dbytes) {
+        if (c->stage) cudaFreeHost(c->stage);
+        c->stage = nullptr;
+        size_t want = std::max(p->dbytes, (size_t)1 << 20);
+        CUDA_TRY(cudaMallocHost(&c->stage, want));
+        c->stage_bytes = want;
+    }
+    char* h = static_cast<char*>(c->stage);
+    std::memcpy(h + p->off_seg_begin, p->seg_begin.data(), p->seg_begin.size() * sizeof(int64_t));
+    if (!p->segs.empty()) std::memcpy(h + p->off_segs, p->segs.data(), p->segs.size() * sizeof(Seg));
+    if (!p->tables.empty()) std::memcpy(h + p->off_tables, p->tables.data(), p->tables.size() * sizeof(int32_t));
+    if (!p->recs.empty()) std::memcpy(h + p->off_recs, p->recs.data(), p->recs.size() * sizeof(ReqRec));
+    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&p->dbuf), p->dbytes, stream));
+    CUDA_TRY(cudaMemcpyAsync(p->dbuf, h, p->dbytes, cudaMemcpyHostToDevice, stream));
+    CUDA_TRY(cudaEventRecord(c->stage_ev, stream));
+    c->stage_pending = true;
+    p->dev = dev;
+    p->last_stream = stream;
+    return KV_OK;
+}
+
+extern "C" kv_status kv_plan_upload(kv_plan* p, void* stream) {
+    if (!p) return fail(KV_ERR_INVALID_ARG, "plan is NULL");
+    return ensure_device(p, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" kv_status kv_reshard(kv_plan* p, int32_t gpu, void* stream_) {
+    if (!p) return fail(KV_ERR_INVALID_ARG, "plan is NULL");
+    if (p->state != PLAN_PLANNED)
+        return fail(KV_ERR_BAD_STATE, "plan already committed; its source blocks may be reused");
+    kv_cache* c = p->c;
+    if (gpu < -1 || gpu >= c->n_gpus) return fail(KV_ERR_INVALID_ARG, "gpu %d out of range", gpu);
+    cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+    kv_status s = ensure_device(p, stream);
+    if (s) return s;
+    p->last_stream = stream;
+    ReshardArgs a{};
+    a.seg_begin = reinterpret_cast<const int64_t*>(p->dbuf + p->off_seg_begin);
+    a.segs = reinterpret_cast<const Seg*>(p->dbuf + p->off_segs);
+    a.tables = reinterpret_cast<const int32_t*>(p->dbuf + p->off_tables);
+    a.layer_base = c->d_layer_base;
+    a.seg_lo = gpu < 0 ? 0 : p->gpu_seg_lo[gpu];
+    a.seg_hi = gpu < 0 ? (int32_t)p->segs.size() : p->gpu_seg_hi[gpu];
+    a.atom_lo = p->seg_begin[a.seg_lo];
+    a.atom_hi = p->seg_begin[a.seg_hi];
+    a.L = c->geo.num_layers;
+    a.atom_bytes = (int32_t)c->atom_bytes;
+    a.M = c->M;
+    a.fence_sys = gpu >= 0 ? 1 : 0;
+    if (a.atom_hi <= a.atom_lo) return KV_OK;
+    cudaError_t e = launch_reshard(a, p->dev, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "flykv_reshard_kernel launch");
+    g_launches.fetch_add(1);
+    return KV_OK;
+}
+
+extern "C" kv_status kv_plan_resident(const kv_plan* p, int32_t gpu, int32_t* n_resident, int32_t* n_ids) {
+    if (!p || gpu < 0 || gpu >= p->c->n_gpus) return fail(KV_ERR_INVALID_ARG, "bad arguments");
+    if (n_resident) *n_resident = p->n_res[gpu];
+    if (n_ids) *n_ids = p->n_res_ids[gpu];
+    return KV_OK;
+}
+
+static void commit(kv_plan* p) {
+    if (p->state == PLAN_COMMITTED) return;
+    kv_cache* c = p->c;
+    for (const ReqPlan& q : p->reqs) {
+        if (!q.moving) continue;
+        for (int32_t r = 0; r < q.src.degree; ++r)
+            for (int32_t k = 0; k < q.n0; ++k) bit_clr(c->held[q.src.first_gpu + r], p->tables[q.src_off + k]);
+    }
+    p->state = PLAN_COMMITTED;
+}
+
+extern "C" kv_status kv_remap_block_tables(kv_plan* p, int32_t gpu, int32_t* req_ptr, int32_t* block_ids,
+                                           int32_t* per_req_meta, void* stream_) {
+    if (!p) return fail(KV_ERR_INVALID_ARG, "plan is NULL");
+    kv_cache* c = p->c;
+    if (gpu < 0 || gpu >= c->n_gpus) return fail(KV_ERR_INVALID_ARG, "gpu %d out of range", gpu);
+    if (!req_ptr || (p->n_res[gpu] > 0 && (!per_req_meta || (p->n_res_ids[gpu] > 0 && !block_ids))))
+        return fail(KV_ERR_INVALID_ARG, "NULL output buffer");
+    cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+    kv_status s = ensure_device(p, stream);
+    if (s) return s;
+    p->last_stream = stream;
+    commit(p);
+    RemapArgs a{};
+    a.reqs = reinterpret_cast<const ReqRec*>(p->dbuf + p->off_recs);
+    a.tables = reinterpret_cast<const int32_t*>(p->dbuf + p->off_tables);
+    a.n_reqs = (int32_t)p->reqs.size();
+    a.gpu = gpu;
+    a.H = c->geo.num_kv_heads;
+    a.B = c->geo.block_base;
+    a.req_ptr = req_ptr;
+    a.block_ids = block_ids;
+    a.meta = per_req_meta;
+    cudaError_t e = launch_remap(a, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "flykv_remap_kernel launch");
+    g_launches.fetch_add(1);
+    return KV_OK;
+}
+
+extern "C" kv_status kv_plan_dst_tables(const kv_plan* p, int32_t* dst_ptr, int32_t* dst_ids) {
+    if (!p || !dst_ptr) return fail(KV_ERR_INVALID_ARG, "bad arguments");
+    dst_ptr[0] = 0;
+    for (size_t i = 0; i < p->reqs.size(); ++i) {
+        const ReqPlan& q = p->reqs[i];
+        if (dst_ids)
+            std::memcpy(dst_ids + dst_ptr[i], p->tables.data() + q.dst_off, (size_t)q.n1 * sizeof(int32_t));
+        dst_ptr[i + 1] = dst_ptr[i] + q.n1;
+    }
+    return KV_OK;
+}
+
+extern "C" kv_status kv_plan_get_stats(const kv_plan* p, kv_plan_stats* st, int64_t* bytes_matrix) {
+    if (!p) return fail(KV_ERR_INVALID_ARG, "plan is NULL");
+    if (st) *st = p->st;
+    if (bytes_matrix) std::memcpy(bytes_matrix, p->bytes.data(), p->bytes.size() * sizeof(int64_t));
+    return KV_OK;
+}
+
+extern "C" void kv_plan_destroy(kv_plan* p) {
+    if (!p) return;
+    if (p->state == PLAN_PLANNED) {  // roll back destination allocations
+        kv_cache* c = p->c;
+        for (const ReqPlan& q : p->reqs) {
+            if (!q.moving) continue;
+            for (int32_t r = 0; r < q.dst.degree; ++r)
+                for (int32_t k = 0; k < q.n1; ++k) bit_clr(c->held[q.dst.first_gpu + r], p->tables[q.dst_off + k]);
+        }
+    }
+    if (p->dbuf) cudaFreeAsync(p->dbuf, p->last_stream);
+    delete p;
+}
+
+// ------------------------------------------------------------ weight views
+extern "C" kv_status weight_shard_view(const kv_weight_desc* w, int32_t rank, int32_t m, kv_view* out) {
+    if (!w || !out) return fail(KV_ERR_INVALID_ARG, "NULL argument");
+    if (w->rows < 1 || w->cols < 1 || w->ld < w->cols || w->elem_bytes < 1)
+        return fail(KV_ERR_INVALID_ARG, "bad matrix shape");
+    if (m < 1 || rank < 0 || rank >= m) return fail(KV_ERR_RANK_OUT_OF_RANGE, "rank %d of %d", rank, m);
+    const char* base = static_cast<const char*>(w->ptr);
+    const int64_t e = w->elem_bytes;
+    std::memset(out, 0, sizeof *out);
+    out->elem_bytes = w->elem_bytes;
+    auto rows_seg = [&](int k, int64_t r0, int64_t nr) {
+        out->seg[k].ptr = base + r0 * w->ld * e;
+        out->seg[k].rows = nr;
+        out->seg[k].cols = w->cols;
+        out->seg[k].ld = w->ld;
+        out->seg[k].row0 = r0;
+        out->seg[k].col0 = 0;
+    };
+    switch (w->kind) {
+        case KV_W_COLUMN: {  // output features = rows of [out, in]
+            if (w->rows % m) return fail(KV_ERR_INDIVISIBLE_EXTENT, "%lld rows / %d", (long long)w->rows, m);
+            const int64_t k = w->rows / m;
+            out->n_seg = 1;
+            rows_seg(0, rank * k, k);
+            return KV_OK;
+        }
+        case KV_W_ROW: {  // input features = columns of [out, in]
+            if (w->cols % m) return fail(KV_ERR_INDIVISIBLE_EXTENT, "%lld cols / %d", (long long)w->cols, m);
+            const int64_t k = w->cols / m;
+            out->n_seg = 1;
+            out->seg[0].ptr = base + rank * k * e;
+            out->seg[0].rows = w->rows;
+            out->seg[0].cols = k;
+            out->seg[0].ld = w->ld;
+            out->seg[0].row0 = 0;
+            out->seg[0].col0 = rank * k;
+            return KV_OK;
+        }
+        case KV_W_QKV: {  // stacked [Q; K; V] rows, head-aligned (R17, GQA R2)
+            const int64_t Hq = w->num_q_heads, Hk = w->num_kv_heads, d = w->head_dim;
+            if (Hq < 1 || Hk < 1 || d < 1 || w->rows != (Hq + 2 * Hk) * d)
+                return fail(KV_ERR_INVALID_ARG, "QKV rows != (Hq + 2*Hkv) * head_dim");
+            if (Hq % m) return fail(KV_ERR_INDIVISIBLE_EXTENT, "%lld query heads / %d", (long long)Hq, m);
+            int64_t h0, nh;
+            if (m <= Hk) {
+                if (Hk % m) return fail(KV_ERR_INDIVISIBLE_EXTENT, "%lld KV heads / %d", (long long)Hk, m);
+                nh = Hk / m;
+                h0 = rank * nh;
+            } else {
+                if (m % Hk) return fail(KV_ERR_INDIVISIBLE_EXTENT, "degree %d not a multiple of %lld KV heads", m, (long long)Hk);
+                nh = 1;
+                h0 = rank / (m / Hk);
+            }
+            const int64_t q = Hq / m;
+            out->n_seg = 3;
+            rows_seg(0, rank * q * d, q * d);
+            rows_seg(1, (Hq + h0) * d, nh * d);
+            rows_seg(2, (Hq + Hk + h0) * d, nh * d);
+            return KV_OK;
+        }
+        default:
+            return fail(KV_ERR_INVALID_ARG, "unknown weight kind %d", w->kind);
+    }
+}
+
+extern "C" kv_status kv_gather_view(const kv_view* v, void* dst, void* stream) {
+    if (!v || !dst || v->n_seg < 1 || v->n_seg > 3) return fail(KV_ERR_INVALID_ARG, "bad view");
+    GatherSeg g[3];
+    int64_t off = 0;
+    for (int k = 0; k < v->n_seg; ++k) {
+        g[k].ptr = static_cast<const char*>(v->seg[k].ptr);
+        g[k].rows = v->seg[k].rows;
+        g[k].row_bytes = v->seg[k].cols * v->elem_bytes;
+        g[k].ld_bytes = v->seg[k].ld * v->elem_bytes;
+        g[k].out_off = off;
+        off += g[k].rows * g[k].row_bytes;
+    }
+    cudaError_t e = launch_gather(g, v->n_seg, static_cast<char*>(dst), static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "flykv_gather_kernel launch");
+    g_launches.fetch_add(1);
+    return KV_OK;
+}
+
+// ------------------------------------------------------------ IPC (peer pools)
+typedef int (*cuMemGetAddressRange_t)(unsigned long long*, size_t*, unsigned long long);
+
+extern "C" kv_status kv_ipc_export(const void* dptr, uint8_t handle[64], uint64_t* offset) {
+    if (!dptr || !handle || !offset) return fail(KV_ERR_INVALID_ARG, "NULL argument");
+    static cuMemGetAddressRange_t fn = nullptr;
+    if (!fn) {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        CUDA_TRY(cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q));
+        if (!f || q != cudaDriverEntryPointSuccess) return fail(KV_ERR_CUDA, "cuMemGetAddressRange unavailable");
+        fn = reinterpret_cast<cuMemGetAddressRange_t>(f);
+    }
+    unsigned long long base = 0;
+    size_t size = 0;
+    int r = fn(&base, &size, (unsigned long long)(uintptr_t)dptr);
+    if (r != 0) return fail(KV_ERR_CUDA, "cuMemGetAddressRange failed (%d)", r);
+    cudaIpcMemHandle_t h;
+    CUDA_TRY(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+    static_assert(sizeof(h) == 64, "IPC handle is 64 bytes");
+    std::memcpy(handle, &h, 64);
+    *offset = (uint64_t)((uintptr_t)dptr - base);
+    return KV_OK;
+}
+
+extern "C" kv_status kv_ipc_import(const uint8_t handle[64], uint64_t offset, void** dptr) {
+    if (!handle || !dptr) return fail(KV_ERR_INVALID_ARG, "NULL argument");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, 64);
+    void* base = nullptr;
+    CUDA_TRY(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+    *dptr = static_cast<char*>(base) + offset;
+    return KV_OK;
+}
+
+extern "C" kv_status kv_ipc_close(void* dptr, uint64_t offset) {
+    if (!dptr) return fail(KV_ERR_INVALID_ARG, "NULL argument");
+    CUDA_TRY(cudaIpcCloseMemHandle(static_cast<char*>(dptr) - offset));
+    return KV_OK;
+}
+
+extern "C" kv_status kv_stream_sync(void* stream) {
+    CUDA_TRY(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+    return KV_OK;
+}
+
+// ------------------------------------------------------------ misc
+extern "C" const char* kv_strerror(kv_status s) {
+    switch (s) {
+        case KV_OK: return "ok";
+        case KV_ERR_INVALID_ARG: return "invalid argument";
+        case KV_ERR_INDIVISIBLE_DEGREE: return "degree incompatible with the KV head count";
+        case KV_ERR_UNKNOWN_GROUP: return "unknown (unaligned or unsupported) group";
+        case KV_ERR_RANK_OUT_OF_RANGE: return "rank out of range";
+        case KV_ERR_INDIVISIBLE_EXTENT: return "extent not divisible by the degree";
+        case KV_ERR_OUT_OF_BLOCKS: return "out of blocks";
+        case KV_ERR_BAD_BLOCK_TABLE: return "bad block table";
+        case KV_ERR_DUPLICATE_REQUEST: return "duplicate request";
+        case KV_ERR_BAD_STATE: return "bad state";
+        case KV_ERR_CUDA: return "CUDA error";
+    }
+    return "unknown status";
+}
+
+extern "C" const char* kv_last_error(void) { return g_err.c_str(); }
+
+extern "C" int64_t kv_launch_count(void) { return g_launches.load(); }

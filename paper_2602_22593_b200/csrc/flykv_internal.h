@@ -1,0 +1,99 @@
+// flykv_internal.h -- structures shared by the host planner (flykv_host.cpp)
+// and the sm_100a kernels (flykv_kernels.cu).  Not part of the ABI.
+#pragma once
+#include <stdint.h>
+#include <cuda_runtime.h>
+
+#define FLYKV_HD __host__ __device__ __forceinline__
+
+namespace flykv {
+
+// Layout of one degree p for a model with H KV heads (R1-R3):
+//   hloc = H_loc(p) = H/p (p <= H) or 1 (p > H)       Eq.3, R2
+//   k    = B(p)/B = H/hloc  (B-token chunks per block) Eq.2
+//   rep  = replicas of each head: 1 (p <= H) or p/H   R2
+struct Layout {
+    int32_t hloc, k, rep;
+};
+
+FLYKV_HD Layout layout_of(int32_t H, int32_t p) {
+    Layout L;
+    if (p <= H) { L.hloc = H / p; L.rep = 1; }
+    else        { L.hloc = 1;     L.rep = p / H; }
+    L.k = H / L.hloc;
+    return L;
+}
+
+// Rank (within the group) of replica j of head h, and the head's index
+// inside that rank's block.  Contiguous head slices (R3, Eq.1).
+FLYKV_HD int32_t owner_rank(const Layout& L, int32_t h, int32_t j) {
+    return L.rep == 1 ? h / L.hloc : h * L.rep + j;
+}
+FLYKV_HD int32_t local_head(const Layout& L, int32_t h) {
+    return L.rep == 1 ? h % L.hloc : 0;
+}
+FLYKV_HD int32_t first_head_of_rank(const Layout& L, int32_t r) {
+    return L.rep == 1 ? r * L.hloc : r / L.rep;
+}
+
+// One work segment: the atoms of one request whose canonical source replica
+// (R10) is pool src_gpu.  Atom a (0 <= a < L*2*C*nh) inside the segment is
+//   a = ((l*2 + kv)*C + c)*nh + hh,   head h = h0 + hh,   chunk c (B tokens)
+// -- head innermost, so consecutive warps fan out over destination ranks and
+// read consecutive 4 KiB pieces of the same source block.
+struct Seg {
+    int32_t src_gpu;   // pool holding the source replica
+    int32_t dst_g0;    // first pool of the destination group
+    int32_t C;         // chunks = ceil(T/B)
+    int32_t nh;        // heads in this segment
+    int32_t h0;        // first head
+    int32_t src_tab;   // offset of the source table in the plan's table array
+    int32_t dst_tab;   // offset of the destination table
+    int32_t hloc0, k0; // source layout
+    int32_t hloc1, k1, rep1; // destination layout
+    int32_t pad[4];
+};
+static_assert(sizeof(Seg) == 64, "Seg is 64 bytes");
+
+// Per-request record used by the remap kernel (a6).
+struct ReqRec {
+    int32_t dst_g0, dst_p, n1, dst_tab;
+};
+
+struct ReshardArgs {
+    const int64_t* seg_begin;  // [n_seg + 1] exclusive prefix of atom counts (global)
+    const Seg* segs;           // [n_seg]
+    const int32_t* tables;     // source + destination tables
+    char* const* layer_base;   // [n_gpus * L] pool layer pointers
+    int32_t seg_lo, seg_hi;    // segment range of this launch
+    int64_t atom_lo, atom_hi;  // atom range (= seg_begin[seg_lo], seg_begin[seg_hi])
+    int32_t L;
+    int32_t atom_bytes;        // B*d*e
+    int64_t M;                 // block bytes per layer
+    int32_t fence_sys;         // 1: release-fence writes at system scope (peer pools)
+};
+
+struct RemapArgs {
+    const ReqRec* reqs;  // [n_reqs]
+    const int32_t* tables;
+    int32_t n_reqs;
+    int32_t gpu;
+    int32_t H;
+    int32_t B;
+    int32_t* req_ptr;
+    int32_t* block_ids;
+    int32_t* meta;
+};
+
+struct GatherSeg {
+    const char* ptr;
+    int64_t rows, row_bytes, ld_bytes;
+    int64_t out_off;  // byte offset of the segment in the output
+};
+
+// Kernel launchers (flykv_kernels.cu).  Return cudaSuccess or the launch error.
+cudaError_t launch_reshard(const ReshardArgs& a, int device, cudaStream_t s);
+cudaError_t launch_remap(const RemapArgs& a, cudaStream_t s);
+cudaError_t launch_gather(const GatherSeg* segs, int n_seg, char* dst, cudaStream_t s);
+
+}  // namespace flykv

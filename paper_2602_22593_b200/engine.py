@@ -1,0 +1,79 @@
+"""KVSwitchEngine: the user-facing switch API over libflykv.so.
+
+One call = one live DP<->TP switch of a set of requests:
+  kv_plan_switch (host: validate, allocate, plan; descriptors uploaded once)
+  -> kv_reshard  (sm_100a kernel, the hot loop)
+  -> kv_remap_block_tables per pool (sm_100a kernel; commits the plan)
+  -> optional read-back of the new block tables to pinned host memory.
+torch supplies device memory and streams only.  Single process: every pool
+lives on devices this process can address (virtual ranks on one B200, or
+peer-enabled GPUs).  One process per GPU: see comm.py.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from . import flykv
+from .pools import DevicePools
+
+
+@dataclass
+class GpuTable:
+    """Post-switch logical table of one pool."""
+    req_ptr: torch.Tensor     # int32 [n_res + 1]
+    block_ids: torch.Tensor   # int32 [n_ids]
+    meta: torch.Tensor        # int32 [n_res, 4]: plan index, B(p), H_loc, first head
+
+
+class KVSwitchEngine:
+    def __init__(self, geom: flykv.Geometry, num_blocks, device="cuda:0", tp_degrees=(2, 4, 8), fill=None,
+                 stream=None):
+        self.device = torch.device(device)
+        self.pools = DevicePools(geom, num_blocks, self.device, fill=fill)
+        self.cache = self.pools.make_cache(tp_degrees)
+        self.geom = geom
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+
+    @property
+    def n_gpus(self) -> int:
+        return self.cache.n_gpus
+
+    def plan(self, requests) -> flykv.Plan:
+        return flykv.kv_plan_switch(self.cache, requests)
+
+    def alloc_tables(self, plan: flykv.Plan, gpus):
+        out = {}
+        for g in gpus:
+            n_res, n_ids = plan.resident(g)
+            out[g] = GpuTable(torch.empty(n_res + 1, dtype=torch.int32, device=self.device),
+                              torch.empty(max(n_ids, 1), dtype=torch.int32, device=self.device),
+                              torch.empty((max(n_res, 1), 4), dtype=torch.int32, device=self.device))
+        return out
+
+    def execute(self, plan: flykv.Plan, gpus=None, tables=None):
+        """Reshard every atom (one launch) and remap the tables of `gpus`."""
+        gpus = range(self.n_gpus) if gpus is None else gpus
+        tables = tables if tables is not None else self.alloc_tables(plan, gpus)
+        with torch.cuda.stream(self.stream):
+            flykv.kv_reshard(plan, -1, self.stream)
+            for g, t in tables.items():
+                flykv.kv_remap_block_tables(plan, g, t.req_ptr, t.block_ids, t.meta, self.stream)
+        return tables
+
+    def switch(self, requests, gpus=None, read_back=False):
+        """Plan + reshard + remap.  With read_back, the new tables are copied
+        to host and the call returns after the switch has completed."""
+        plan = self.plan(requests)
+        tables = self.execute(plan, gpus)
+        host = None
+        if read_back:
+            host = {}
+            with torch.cuda.stream(self.stream):
+                for g, t in tables.items():
+                    n_res, n_ids = plan.resident(g)
+                    host[g] = (t.req_ptr.to("cpu", non_blocking=True), t.block_ids[:n_ids].to("cpu", non_blocking=True),
+                               t.meta[:n_res].to("cpu", non_blocking=True))
+            self.stream.synchronize()
+        return plan, tables, host

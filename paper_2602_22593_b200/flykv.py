@@ -1,0 +1,362 @@
+"""Thin ctypes binding of libflykv.so (include/flykv.h).
+
+Argument marshalling only: every step of the re-layout runs in the C++ host
+planner and the sm_100a kernels of libflykv.so.  There is no CPU fallback:
+importing this module raises if the library is missing.  Pointers may be
+passed as ints or as objects exposing ``data_ptr()`` (torch tensors); streams
+as ints, ``None`` (legacy default stream) or objects exposing
+``cuda_stream`` (torch.cuda.Stream).
+
+Names follow the C ABI: kv_plan_switch, kv_reshard, kv_remap_block_tables,
+weight_shard_view (+ the cache/allocator/IPC helpers).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "lib", "libflykv.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"libflykv.so not found at {LIB_PATH}: build it with "
+        "`python -c 'import __graft_entry__ as g; g.build()'` (there is no CPU fallback)")
+
+_lib = C.CDLL(LIB_PATH)
+
+# ----------------------------------------------------------------- statuses
+KV_OK = 0
+STATUS_NAMES = {
+    0: "KV_OK", 1: "KV_ERR_INVALID_ARG", 2: "KV_ERR_INDIVISIBLE_DEGREE", 3: "KV_ERR_UNKNOWN_GROUP",
+    4: "KV_ERR_RANK_OUT_OF_RANGE", 5: "KV_ERR_INDIVISIBLE_EXTENT", 6: "KV_ERR_OUT_OF_BLOCKS",
+    7: "KV_ERR_BAD_BLOCK_TABLE", 8: "KV_ERR_DUPLICATE_REQUEST", 9: "KV_ERR_BAD_STATE", 10: "KV_ERR_CUDA",
+}
+
+
+class FlyKVError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        self.status = status
+        self.name = STATUS_NAMES.get(status, str(status))
+        super().__init__(f"{self.name}: {msg}")
+
+
+def _check(status: int):
+    if status != KV_OK:
+        raise FlyKVError(status, _lib.kv_last_error().decode())
+
+
+# ----------------------------------------------------------------- structs
+class Geometry(C.Structure):
+    _fields_ = [("num_layers", C.c_int32), ("num_kv_heads", C.c_int32), ("head_dim", C.c_int32),
+                ("block_base", C.c_int32), ("elem_bytes", C.c_int32)]
+
+
+class Group(C.Structure):
+    _fields_ = [("first_gpu", C.c_int32), ("degree", C.c_int32)]
+
+
+class Request(C.Structure):
+    _fields_ = [("req_id", C.c_int64), ("num_tokens", C.c_int32), ("src", Group),
+                ("src_blocks", C.POINTER(C.c_int32)), ("n_src_blocks", C.c_int32), ("dst", Group)]
+
+
+class PlanStats(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in ("n_requests", "n_moving", "n_atoms", "n_atom_writes", "atom_bytes",
+                                         "payload_bytes", "h2d_bytes", "n_segments")]
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+
+KV_W_COLUMN, KV_W_ROW, KV_W_QKV = 0, 1, 2
+
+
+class WeightDesc(C.Structure):
+    _fields_ = [("ptr", C.c_void_p), ("rows", C.c_int64), ("cols", C.c_int64), ("ld", C.c_int64),
+                ("elem_bytes", C.c_int32), ("kind", C.c_int32), ("num_q_heads", C.c_int32),
+                ("num_kv_heads", C.c_int32), ("head_dim", C.c_int32)]
+
+
+class ViewSegment(C.Structure):
+    _fields_ = [("ptr", C.c_void_p), ("rows", C.c_int64), ("cols", C.c_int64), ("ld", C.c_int64),
+                ("row0", C.c_int64), ("col0", C.c_int64)]
+
+
+class View(C.Structure):
+    _fields_ = [("n_seg", C.c_int32), ("elem_bytes", C.c_int32), ("seg", ViewSegment * 3)]
+
+    def segments(self):
+        return [self.seg[k] for k in range(self.n_seg)]
+
+
+_P = C.c_void_p
+_I32P = C.POINTER(C.c_int32)
+_I64P = C.POINTER(C.c_int64)
+
+
+def _sig(name, res, *args):
+    f = getattr(_lib, name)
+    f.restype = res
+    f.argtypes = list(args)
+
+
+_sig("kv_cache_create", C.c_int, C.POINTER(Geometry), C.c_int32, _I32P, C.POINTER(C.c_void_p), _I32P,
+     C.c_int32, C.POINTER(_P))
+_sig("kv_cache_destroy", None, _P)
+_sig("kv_layout", C.c_int, C.POINTER(Geometry), C.c_int32, _I32P, _I32P, _I64P)
+_sig("kv_blocks_for", C.c_int, C.POINTER(Geometry), C.c_int32, C.c_int32, _I32P)
+_sig("kv_alloc", C.c_int, _P, Group, C.c_int32, _I32P)
+_sig("kv_reserve", C.c_int, _P, Group, _I32P, C.c_int32)
+_sig("kv_free", C.c_int, _P, Group, _I32P, C.c_int32)
+_sig("kv_free_count", C.c_int, _P, C.c_int32, _I32P)
+_sig("kv_held_mask", C.c_int, _P, C.c_int32, C.POINTER(C.c_uint8))
+_sig("kv_plan_switch", C.c_int, _P, C.POINTER(Request), C.c_int32, C.POINTER(_P))
+_sig("kv_plan_upload", C.c_int, _P, _P)
+_sig("kv_reshard", C.c_int, _P, C.c_int32, _P)
+_sig("kv_plan_resident", C.c_int, _P, C.c_int32, _I32P, _I32P)
+_sig("kv_remap_block_tables", C.c_int, _P, C.c_int32, _P, _P, _P, _P)
+_sig("kv_plan_dst_tables", C.c_int, _P, _I32P, _I32P)
+_sig("kv_plan_get_stats", C.c_int, _P, C.POINTER(PlanStats), _I64P)
+_sig("kv_plan_destroy", None, _P)
+_sig("weight_shard_view", C.c_int, C.POINTER(WeightDesc), C.c_int32, C.c_int32, C.POINTER(View))
+_sig("kv_gather_view", C.c_int, C.POINTER(View), _P, _P)
+_sig("kv_ipc_export", C.c_int, _P, C.POINTER(C.c_uint8), C.POINTER(C.c_uint64))
+_sig("kv_ipc_import", C.c_int, C.POINTER(C.c_uint8), C.c_uint64, C.POINTER(_P))
+_sig("kv_ipc_close", C.c_int, _P, C.c_uint64)
+_sig("kv_stream_sync", C.c_int, _P)
+_sig("kv_strerror", C.c_char_p, C.c_int)
+_sig("kv_last_error", C.c_char_p)
+_sig("kv_launch_count", C.c_int64)
+
+EXPORTED = ["kv_cache_create", "kv_cache_destroy", "kv_layout", "kv_blocks_for", "kv_alloc", "kv_reserve",
+            "kv_free", "kv_free_count", "kv_held_mask", "kv_plan_switch", "kv_plan_upload", "kv_reshard", "kv_plan_resident",
+            "kv_remap_block_tables", "kv_plan_dst_tables", "kv_plan_get_stats", "kv_plan_destroy",
+            "weight_shard_view", "kv_gather_view", "kv_ipc_export", "kv_ipc_import", "kv_ipc_close",
+            "kv_stream_sync", "kv_strerror", "kv_last_error", "kv_launch_count"]
+
+
+# ----------------------------------------------------------------- marshalling
+def ptr_of(x) -> int:
+    if x is None:
+        return 0
+    if isinstance(x, int):
+        return x
+    if hasattr(x, "data_ptr"):
+        return int(x.data_ptr())
+    raise TypeError(f"cannot take a device pointer of {type(x)}")
+
+
+def stream_of(s) -> int:
+    if s is None:
+        return 0
+    if isinstance(s, int):
+        return s
+    if hasattr(s, "cuda_stream"):
+        return int(s.cuda_stream)
+    raise TypeError(f"cannot take a CUDA stream of {type(s)}")
+
+
+def _i32(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.int32).reshape(-1))
+
+
+def geometry(L: int, H: int, d: int, B: int, e: int = 2) -> Geometry:
+    return Geometry(L, H, d, B, e)
+
+
+def kv_layout(geom: Geometry, degree: int):
+    """(H_loc(p), B(p), M) -- Eq.3 / Eq.2 / M_block eq."""
+    hl, bt, M = C.c_int32(), C.c_int32(), C.c_int64()
+    _check(_lib.kv_layout(C.byref(geom), degree, C.byref(hl), C.byref(bt), C.byref(M)))
+    return hl.value, bt.value, M.value
+
+
+def kv_blocks_for(geom: Geometry, num_tokens: int, degree: int) -> int:
+    n = C.c_int32()
+    _check(_lib.kv_blocks_for(C.byref(geom), num_tokens, degree, C.byref(n)))
+    return n.value
+
+
+def launch_count() -> int:
+    return int(_lib.kv_launch_count())
+
+
+def strerror(status: int) -> str:
+    return _lib.kv_strerror(status).decode()
+
+
+# ----------------------------------------------------------------- cache
+class KVCache:
+    """Owns a kv_cache*: per-GPU pools (caller memory) + allocator bitmaps."""
+
+    def __init__(self, geom: Geometry, num_blocks, layer_base, tp_degrees=(2, 4, 8)):
+        self.geom = geom
+        self.n_gpus = len(num_blocks)
+        nb = _i32(num_blocks)
+        flat = [ptr_of(p) for row in layer_base for p in row]
+        if len(flat) != self.n_gpus * geom.num_layers:
+            raise ValueError("layer_base must be [n_gpus][num_layers]")
+        self._bases = (C.c_void_p * len(flat))(*flat)
+        deg = _i32(tp_degrees) if len(tp_degrees) else _i32([0])
+        h = C.c_void_p()
+        _check(_lib.kv_cache_create(C.byref(geom), self.n_gpus, nb.ctypes.data_as(_I32P), self._bases,
+                                    deg.ctypes.data_as(_I32P), len(tp_degrees), C.byref(h)))
+        self._h = h
+        self.num_blocks = [int(x) for x in nb]
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.kv_cache_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def alloc(self, group, n: int) -> np.ndarray:
+        out = np.zeros(max(n, 1), dtype=np.int32)
+        _check(_lib.kv_alloc(self._h, Group(*group), n, out.ctypes.data_as(_I32P)))
+        return out[:n]
+
+    def reserve(self, group, ids):
+        ids = _i32(ids)
+        _check(_lib.kv_reserve(self._h, Group(*group), ids.ctypes.data_as(_I32P), ids.size))
+
+    def free(self, group, ids):
+        ids = _i32(ids)
+        _check(_lib.kv_free(self._h, Group(*group), ids.ctypes.data_as(_I32P), ids.size))
+
+    def free_count(self, gpu: int) -> int:
+        n = C.c_int32()
+        _check(_lib.kv_free_count(self._h, gpu, C.byref(n)))
+        return n.value
+
+    def held_mask(self, gpu: int) -> np.ndarray:
+        out = np.zeros(max(self.num_blocks[gpu], 1), dtype=np.uint8)
+        _check(_lib.kv_held_mask(self._h, gpu, out.ctypes.data_as(C.POINTER(C.c_uint8))))
+        return out[:self.num_blocks[gpu]]
+
+    def plan_switch(self, requests) -> "Plan":
+        return kv_plan_switch(self, requests)
+
+
+# ----------------------------------------------------------------- plan
+class Plan:
+    def __init__(self, cache: KVCache, handle: C.c_void_p, n_reqs: int):
+        self.cache = cache
+        self._h = handle
+        self.n_reqs = n_reqs
+
+    def destroy(self):
+        if getattr(self, "_h", None):
+            _lib.kv_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+    def upload(self, stream=None):
+        _check(_lib.kv_plan_upload(self._h, stream_of(stream)))
+
+    def reshard(self, gpu: int = -1, stream=None):
+        return kv_reshard(self, gpu, stream)
+
+    def resident(self, gpu: int):
+        n, m = C.c_int32(), C.c_int32()
+        _check(_lib.kv_plan_resident(self._h, gpu, C.byref(n), C.byref(m)))
+        return n.value, m.value
+
+    def remap_block_tables(self, gpu, req_ptr, block_ids, per_req_meta, stream=None):
+        return kv_remap_block_tables(self, gpu, req_ptr, block_ids, per_req_meta, stream)
+
+    def dst_tables(self) -> list:
+        ptr = np.zeros(self.n_reqs + 1, dtype=np.int32)
+        _check(_lib.kv_plan_dst_tables(self._h, ptr.ctypes.data_as(_I32P), None))
+        ids = np.zeros(max(int(ptr[-1]), 1), dtype=np.int32)
+        _check(_lib.kv_plan_dst_tables(self._h, ptr.ctypes.data_as(_I32P), ids.ctypes.data_as(_I32P)))
+        return [ids[ptr[i]:ptr[i + 1]].copy() for i in range(self.n_reqs)]
+
+    def stats(self):
+        st = PlanStats()
+        n = self.cache.n_gpus
+        mat = np.zeros(n * n, dtype=np.int64)
+        _check(_lib.kv_plan_get_stats(self._h, C.byref(st), mat.ctypes.data_as(_I64P)))
+        return st.as_dict(), mat.reshape(n, n)
+
+
+def make_requests(reqs):
+    """reqs: iterable of (req_id, num_tokens, (g0, p0), src_ids, (g1, p1)).
+    Returns (ctypes array, keep-alive list)."""
+    reqs = list(reqs)
+    arr = (Request * max(len(reqs), 1))()
+    keep = []
+    for i, (rid, T, src, ids, dst) in enumerate(reqs):
+        a = _i32(ids)
+        keep.append(a)
+        arr[i] = Request(int(rid), int(T), Group(*src), a.ctypes.data_as(_I32P), a.size, Group(*dst))
+    return arr, keep
+
+
+def kv_plan_switch(cache: KVCache, requests) -> Plan:
+    """Validate, allocate and plan a switch (see include/flykv.h)."""
+    arr, keep = make_requests(requests)
+    n = len(keep)
+    h = C.c_void_p()
+    _check(_lib.kv_plan_switch(cache._h, arr, n, C.byref(h)))
+    return Plan(cache, h, n)
+
+
+def kv_reshard(plan: Plan, gpu: int = -1, stream=None):
+    _check(_lib.kv_reshard(plan._h, gpu, stream_of(stream)))
+
+
+def kv_remap_block_tables(plan: Plan, gpu: int, req_ptr, block_ids, per_req_meta, stream=None):
+    _check(_lib.kv_remap_block_tables(plan._h, gpu, ptr_of(req_ptr), ptr_of(block_ids), ptr_of(per_req_meta),
+                                      stream_of(stream)))
+
+
+# ----------------------------------------------------------------- weights
+def weight_shard_view(desc: WeightDesc, rank: int, degree: int) -> View:
+    v = View()
+    _check(_lib.weight_shard_view(C.byref(desc), rank, degree, C.byref(v)))
+    return v
+
+
+def weight_desc(ptr, rows, cols, elem_bytes, kind, ld=None, num_q_heads=0, num_kv_heads=0, head_dim=0):
+    return WeightDesc(ptr_of(ptr), rows, cols, cols if ld is None else ld, elem_bytes, kind, num_q_heads,
+                      num_kv_heads, head_dim)
+
+
+def kv_gather_view(view: View, dst, stream=None):
+    _check(_lib.kv_gather_view(C.byref(view), ptr_of(dst), stream_of(stream)))
+
+
+# ----------------------------------------------------------------- IPC
+def ipc_export(dptr):
+    h = (C.c_uint8 * 64)()
+    off = C.c_uint64()
+    _check(_lib.kv_ipc_export(ptr_of(dptr), h, C.byref(off)))
+    return bytes(h), off.value
+
+
+def ipc_import(handle: bytes, offset: int) -> int:
+    h = (C.c_uint8 * 64).from_buffer_copy(handle)
+    p = C.c_void_p()
+    _check(_lib.kv_ipc_import(h, offset, C.byref(p)))
+    return int(p.value)
+
+
+def ipc_close(dptr: int, offset: int):
+    _check(_lib.kv_ipc_close(dptr, offset))
+
+
+def stream_sync(stream=None):
+    _check(_lib.kv_stream_sync(stream_of(stream)))

@@ -153,24 +153,33 @@ def pool_blocks(w: Workload, slack: float = 1.10, extra: int = 8) -> list:
 
 def source_tables(w: Workload, counts: list, num_blocks: list, seed: int = 1) -> list:
     """Fragmented source tables: per source group a seeded permutation of the
-    IDs [0, min pool size over the group), consumed in request order.
+    IDs [0, min pool size over the group), consumed in request order, skipping
+    IDs already used on any member GPU (groups may overlap).
     counts[i] = blocks request i holds (computed by the caller's own code)."""
     rng = np.random.default_rng(seed)
-    perms = {}
-    cursor = {}
+    perms, cursor = {}, {}
+    used = [np.zeros(n, dtype=bool) for n in num_blocks]
     out = []
-    for i, (grp, n) in enumerate(zip(w.src, counts)):
+    for grp, n in zip(w.src, counts):
         grp = tuple(grp)
+        members = range(grp[0], grp[0] + grp[1])
         if grp not in perms:
-            nb = min(num_blocks[g] for g in range(grp[0], grp[0] + grp[1]))
+            nb = min(num_blocks[g] for g in members)
             perms[grp] = rng.permutation(nb).astype(np.int32)
             cursor[grp] = 0
-        c = cursor[grp]
-        if c + n > len(perms[grp]):
-            raise ValueError("pool too small for source tables")
-        out.append(perms[grp][c:c + n].copy())
-        cursor[grp] = c + n
-    # groups in one workload never overlap in GPUs at source time
+        perm, c = perms[grp], cursor[grp]
+        ids = []
+        while len(ids) < n:
+            if c >= len(perm):
+                raise ValueError("pool too small for source tables")
+            b = int(perm[c])
+            c += 1
+            if not any(used[g][b] for g in members):
+                ids.append(b)
+        for g in members:
+            used[g][ids] = True
+        cursor[grp] = c
+        out.append(np.asarray(ids, dtype=np.int32))
     return out
 
 

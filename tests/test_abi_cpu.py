@@ -1,0 +1,236 @@
+"""C-ABI library on CPU (no GPU needed): it loads, exports every symbol
+include/flykv.h declares, and its host logic (validation, allocator, planner,
+byte matrix, weight views) matches the oracle and the paper's rules.
+No compute call is made here (pool pointers are fake, never dereferenced)."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2602_22593_b200 import flykv as F
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_header_symbols_exported():
+    hdr = open(os.path.join(ROOT, "include", "flykv.h")).read()
+    names = set(re.findall(r"^\s*(?:kv_status|void|const char\*|int64_t)\s+\**(\w+)\s*\(", hdr, re.M))
+    assert {"kv_plan_switch", "kv_reshard", "kv_remap_block_tables", "weight_shard_view"} <= names
+    for n in names:
+        assert hasattr(F._lib, n), n
+    assert set(F.EXPORTED) == names
+
+
+def fake_cache(geo, nb, degrees=(2, 4, 8)):
+    g = F.geometry(*geo)
+    bases = [[(1 << 40) + (gpu << 36) + (l << 30) for l in range(geo[0])] for gpu in range(len(nb))]
+    return F.KVCache(g, nb, bases, degrees)
+
+
+def test_layout_matches_oracle():
+    for H in (1, 2, 4, 8):
+        for p in (1, 2, 4, 8, 16):
+            g = F.geometry(3, H, 64, 16, 2)
+            og = O.Geom(3, H, 64, 16, 2)
+            hl, bt, M = F.kv_layout(g, p)
+            assert (hl, bt, M) == (O.h_loc(og, p), O.block_tokens(og, p), O.block_bytes(og))
+            for T in (0, 1, 16, 17, 1000):
+                assert F.kv_blocks_for(g, T, p) == O.num_blocks(og, T, p)
+    with pytest.raises(F.FlyKVError) as e:
+        F.kv_layout(F.geometry(1, 8, 64, 16, 2), 3)
+    assert e.value.name == "KV_ERR_INDIVISIBLE_DEGREE"
+
+
+def test_alloc_lowest_uniform_and_conservation():
+    c = fake_cache((2, 4, 8, 4, 2), [16, 16])
+    a = c.alloc((0, 1), 3)
+    assert list(a) == [0, 1, 2]
+    b = c.alloc((1, 1), 2)
+    assert list(b) == [0, 1]
+    t = c.alloc((0, 2), 3)          # lowest free on both GPUs (R6, R8)
+    assert list(t) == [3, 4, 5]
+    c.free((0, 1), [1])
+    t2 = c.alloc((0, 2), 2)         # 1 is free on GPU0 but held on GPU1
+    assert list(t2) == [6, 7]
+    assert c.free_count(0) == 16 - 7 and c.free_count(1) == 16 - 7
+    with pytest.raises(F.FlyKVError) as e:
+        c.alloc((0, 2), 100)
+    assert e.value.name == "KV_ERR_OUT_OF_BLOCKS"
+    with pytest.raises(F.FlyKVError):
+        c.free((0, 1), [1])         # not held any more
+    with pytest.raises(F.FlyKVError) as e:
+        c.alloc((1, 2), 1)          # unaligned group
+    assert e.value.name == "KV_ERR_UNKNOWN_GROUP"
+
+
+def _random_case(rng, H, n_gpus, n_req, degrees, nb):
+    T = rng.integers(0, 90, size=n_req)
+    spec = []
+    for i in range(n_req):
+        p0 = int(rng.choice(degrees))
+        p1 = int(rng.choice(degrees))
+        g0 = int(rng.integers(0, n_gpus // p0)) * p0
+        g1 = int(rng.integers(0, n_gpus // p1)) * p1
+        spec.append((int(T[i]), (g0, p0), (g1, p1)))
+    return spec
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_plan_tables_match_oracle(seed):
+    """The product's host allocator/planner chooses exactly the oracle's
+    destination tables (R6, R8) and leaves the same held sets (R13)."""
+    rng = np.random.default_rng(seed)
+    H = [1, 2, 4, 8][seed % 4]
+    n_gpus = 8
+    geo = (2, H, 4, 4, 2)
+    og = O.Geom(*geo)
+    nb = [256] * n_gpus
+    spec = _random_case(rng, H, n_gpus, 10, [1, 2, 4, 8], nb)
+    c = fake_cache(geo, nb)
+    M = O.block_bytes(og)
+    pools = [np.zeros(geo[0] * n * M, dtype=np.uint8) for n in nb]
+    held = [np.zeros(n, dtype=np.uint8) for n in nb]
+    oreqs, freqs = [], []
+    for i, (T, src, dst) in enumerate(spec):
+        n = F.kv_blocks_for(c.geom, T, src[1])
+        ids = c.alloc(src, n)                 # sources placed by the product allocator
+        for r in range(src[1]):
+            held[src[0] + r][ids] = 1
+        oreqs.append(O.Req(T, src, list(ids), dst))
+        freqs.append((100 + i, T, src, ids, dst))
+    for g in range(n_gpus):
+        assert np.array_equal(c.held_mask(g), held[g])
+    st, otabs = O.switch(og, pools, held, oreqs)
+    if st != 0:  # both sides must refuse, and the product must change nothing
+        before = [c.held_mask(g).copy() for g in range(n_gpus)]
+        with pytest.raises(F.FlyKVError) as e:
+            c.plan_switch(freqs)
+        assert e.value.name == "KV_ERR_OUT_OF_BLOCKS"
+        assert all(np.array_equal(c.held_mask(g), before[g]) for g in range(n_gpus))
+        return
+    plan = c.plan_switch(freqs)
+    ftabs = plan.dst_tables()
+    assert [list(a) for a in ftabs] == [list(b) for b in otabs]
+    # residency sizes agree with the oracle's CSR tables
+    for g in range(n_gpus):
+        rp, ids, meta = O.tables(og, g, oreqs, otabs)
+        assert plan.resident(g) == (len(meta), len(ids))
+    # a plan that is never committed rolls back on destroy
+    plan.destroy()
+    for g in range(n_gpus):
+        hm = c.held_mask(g)
+        want = np.zeros(nb[g], dtype=np.uint8)
+        for (T, src, ids_, dst) in [(f[1], f[2], f[3], f[4]) for f in freqs]:
+            if src[0] <= g < src[0] + src[1]:
+                want[ids_] = 1
+        assert np.array_equal(hm, want)
+
+
+def test_plan_validation_errors():
+    geo = (2, 4, 8, 4, 2)
+    c = fake_cache(geo, [32, 32, 32, 32])
+    a = c.alloc((0, 1), 3)   # T up to 12
+    b = c.alloc((1, 1), 2)
+    def expect(reqs, name):
+        before = [c.held_mask(g).copy() for g in range(4)]
+        with pytest.raises(F.FlyKVError) as e:
+            c.plan_switch(reqs)
+        assert e.value.name == name, e.value
+        for g in range(4):
+            assert np.array_equal(c.held_mask(g), before[g])
+
+    expect([(1, 12, (0, 1), a[:2], (0, 2))], "KV_ERR_BAD_BLOCK_TABLE")        # wrong length
+    expect([(1, 12, (0, 1), [a[0], a[1], 31], (0, 2))], "KV_ERR_BAD_BLOCK_TABLE")  # 31 not held
+    expect([(1, 12, (0, 1), [a[0], a[1], 99], (0, 2))], "KV_ERR_BAD_BLOCK_TABLE")  # out of range
+    expect([(1, 12, (0, 1), a, (1, 2))], "KV_ERR_UNKNOWN_GROUP")              # unaligned
+    expect([(1, 12, (0, 1), a, (0, 3))], "KV_ERR_UNKNOWN_GROUP")              # degree not in P
+    expect([(1, 12, (0, 1), a, (0, 2)), (1, 8, (1, 1), b, (0, 2))], "KV_ERR_DUPLICATE_REQUEST")
+    expect([(1, 12, (0, 1), a, (0, 2)), (2, 12, (0, 1), a, (0, 2))], "KV_ERR_BAD_BLOCK_TABLE")  # shared (R14)
+    expect([(1, -1, (0, 1), [], (0, 2))], "KV_ERR_INVALID_ARG")
+    # out of blocks is transactional: first request fits, second does not
+    big = c.alloc((2, 1), 30)
+    expect([(1, 12, (0, 1), a, (0, 2)), (2, 120, (2, 1), big, (2, 2))], "KV_ERR_OUT_OF_BLOCKS")
+
+
+def test_gqa_degree_rules():
+    c = fake_cache((1, 2, 8, 4, 2), [16] * 8, degrees=(2, 4, 8))
+    a = c.alloc((0, 1), 2)
+    plan = c.plan_switch([(1, 8, (0, 1), a, (0, 8))])   # 8 > H=2 -> replication x4
+    st, mat = plan.stats()
+    # B(8) = H*B = 8 -> one block per rank; every rank receives one head copy
+    assert [len(t) for t in plan.dst_tables()] == [1]
+    assert st["n_atoms"] == 1 * 2 * 2 * 2            # L*2*C*H
+    assert st["n_atom_writes"] == st["n_atoms"] * 4
+    assert (mat[0] > 0).sum() == 8
+    plan.destroy()
+    with pytest.raises(F.FlyKVError) as e:
+        fake_cache((1, 3, 8, 4, 2), [4] * 2, degrees=(2,))
+    assert e.value.name == "KV_ERR_INDIVISIBLE_DEGREE"
+
+
+def test_byte_matrix_matches_atom_enumeration():
+    """kv_plan_get_stats byte matrix == counting every atom with the oracle's owner map."""
+    rng = np.random.default_rng(3)
+    geo = (3, 4, 8, 4, 2)
+    og = O.Geom(*geo)
+    n_gpus = 8
+    c = fake_cache(geo, [128] * n_gpus)
+    spec = _random_case(rng, 4, n_gpus, 12, [1, 2, 4, 8], None)
+    reqs = []
+    for i, (T, src, dst) in enumerate(spec):
+        ids = c.alloc(src, F.kv_blocks_for(c.geom, T, src[1]))
+        reqs.append((i, T, src, ids, dst))
+    plan = c.plan_switch(reqs)
+    st, mat = plan.stats()
+    want = np.zeros((n_gpus, n_gpus), dtype=np.int64)
+    atom = og.B * og.d * og.e
+    tabs = plan.dst_tables()
+    for (i, T, src, ids, dst), t1 in zip(reqs, tabs):
+        if src == dst:
+            continue
+        for h in range(og.H):
+            sg = src[0] + O.owner_rank(og, src[1], h, 0)
+            for j in range(O.replicas(og, dst[1])):
+                dg = dst[0] + O.owner_rank(og, dst[1], h, j)
+                want[sg, dg] += og.L * 2 * (-(-T // og.B)) * atom
+    assert np.array_equal(mat, want)
+    assert st["payload_bytes"] == want.sum()
+    plan.destroy()
+
+
+def test_weight_views_match_oracle():
+    from oracle import weights as W
+    Hq, Hkv, d, hidden = 8, 2, 4, 16
+    rows = (Hq + 2 * Hkv) * d
+    base = 1 << 32
+    full = np.arange(rows * hidden).reshape(rows, hidden)
+    for m in (1, 2, 4, 8):
+        for r in range(m):
+            v = F.weight_shard_view(F.weight_desc(base, rows, hidden, 2, F.KV_W_QKV, num_q_heads=Hq,
+                                                  num_kv_heads=Hkv, head_dim=d), r, m)
+            ref = W.view_qkv(full, r, m, Hq, Hkv, d)
+            assert v.n_seg == 3
+            for s, rs in zip(v.segments(), ref):
+                # the segment addresses exactly the oracle's rows (zero-copy alias)
+                r0 = (s.ptr - base) // (2 * hidden)
+                assert np.array_equal(full[r0:r0 + s.rows, :s.cols], rs)
+                assert s.row0 == r0 and s.ld == hidden
+    Wf = np.arange(6 * 8).reshape(6, 8)
+    for m in (1, 2, 4, 8):
+        for r in range(m):
+            v = F.weight_shard_view(F.weight_desc(base, 6, 8, 4, F.KV_W_ROW), r, m)
+            (ref,) = W.view_row(Wf, r, m)
+            s = v.seg[0]
+            c0 = (s.ptr - base) // 4
+            assert s.col0 == c0 and np.array_equal(Wf[:, c0:c0 + s.cols], ref) and s.ld == 8
+            v = F.weight_shard_view(F.weight_desc(base, 8, 6, 4, F.KV_W_COLUMN), r, m)
+            (ref,) = W.view_col(np.arange(48).reshape(8, 6), r, m)
+            assert v.seg[0].rows == ref.shape[0] and v.seg[0].row0 == r * 8 // m
+    with pytest.raises(F.FlyKVError) as e:
+        F.weight_shard_view(F.weight_desc(base, 6, 8, 4, F.KV_W_ROW), 0, 3)
+    assert e.value.name == "KV_ERR_INDIVISIBLE_EXTENT"
+    with pytest.raises(F.FlyKVError) as e:
+        F.weight_shard_view(F.weight_desc(base, 6, 8, 4, F.KV_W_ROW), 4, 4)
+    assert e.value.name == "KV_ERR_RANK_OUT_OF_RANGE"

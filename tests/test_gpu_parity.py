@@ -1,0 +1,270 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle,
+element by element, tolerance 0 (byte copies + integer tables, BJ).
+
+Small cases: whole pools copied back and compared byte for byte with the C
+oracle run on the same seeded host inputs; destination tables, per-GPU CSR
+tables and allocator state compared exactly.  Full BASELINE size (config 2,
+the bench's launch configuration): sampled atoms checked one by one against
+the oracle's locate() and the content hash (synth.py), tables compared in
+full with the oracle's allocator.
+"""
+import numpy as np
+import pytest
+
+import synth
+from oracle import oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def _F():
+    from paper_2602_22593_b200 import flykv
+    return flykv
+
+
+def run_parity(geo, nb, spec, seed=0, per_gpu_launch=False, check_pools=True):
+    """spec: list of (T, src_group, dst_group).  Runs the product on cuda:0
+    (virtual ranks) and the oracle on host copies; asserts exact equality."""
+    F = _F()
+    from paper_2602_22593_b200.engine import KVSwitchEngine
+    og = O.Geom(*geo)
+    g = F.geometry(*geo)
+    eng = KVSwitchEngine(g, nb, "cuda:0", tp_degrees=(2, 4, 8, 16))
+    for gpu, t in enumerate(eng.pools.tensors):
+        synth.fill_hash_torch(t, gpu, seed=seed + 2)
+    torch.cuda.synchronize()
+    host_pools = [t.cpu().numpy().reshape(-1).copy() for t in eng.pools.tensors]
+    held = [np.zeros(n, dtype=np.uint8) for n in nb]
+    counts = [O.num_blocks(og, T, src[1]) for (T, src, dst) in spec]
+    w = synth.Workload("t", *geo, len(nb), [s[0] for s in spec], [s[1] for s in spec], [s[2] for s in spec])
+    tabs0 = synth.source_tables(w, counts, nb, seed=seed + 1)
+    oreqs, freqs = [], []
+    for i, ((T, src, dst), ids) in enumerate(zip(spec, tabs0)):
+        eng.cache.reserve(src, ids)
+        for r in range(src[1]):
+            held[src[0] + r][ids] = 1
+        oreqs.append(O.Req(T, src, list(ids), dst))
+        freqs.append((1000 + i, T, src, ids, dst))
+    # GQA sources: replicas identical (R10) -- copy on both sides
+    M = O.block_bytes(og)
+    for (T, src, dst), ids in zip(spec, tabs0):
+        if src[1] > og.H:
+            rep = src[1] // og.H
+            for r in range(src[1]):
+                lo = src[0] + (r // rep) * rep
+                if lo == src[0] + r:
+                    continue
+                idx = torch.as_tensor(np.asarray(ids, dtype=np.int64), device="cuda:0")
+                eng.pools.tensors[src[0] + r][:, idx] = eng.pools.tensors[lo][:, idx]
+                hp = host_pools[src[0] + r].reshape(og.L, nb[src[0] + r], M)
+                hp[:, ids] = host_pools[lo].reshape(og.L, nb[lo], M)[:, ids]
+    plan = eng.plan(freqs)
+    tables = eng.alloc_tables(plan, range(len(nb)))
+    if per_gpu_launch:
+        for gpu in range(len(nb)):
+            F.kv_reshard(plan, gpu, eng.stream)
+        for gpu, t in tables.items():
+            F.kv_remap_block_tables(plan, gpu, t.req_ptr, t.block_ids, t.meta, eng.stream)
+    else:
+        eng.execute(plan, tables=tables)
+    torch.cuda.synchronize()
+    st, otabs = O.switch(og, host_pools, held, oreqs)
+    assert st == 0
+    ftabs = plan.dst_tables()
+    assert [list(a) for a in ftabs] == [list(b) for b in otabs]
+    for gpu in range(len(nb)):
+        assert np.array_equal(eng.cache.held_mask(gpu), held[gpu]), f"allocator state differs on {gpu}"
+        rp, ids, meta = O.tables(og, gpu, oreqs, otabs)
+        n_res, n_ids = plan.resident(gpu)
+        t = tables[gpu]
+        assert np.array_equal(t.req_ptr.cpu().numpy(), rp)
+        assert np.array_equal(t.block_ids[:n_ids].cpu().numpy(), ids)
+        assert np.array_equal(t.meta[:n_res].cpu().numpy(), meta)
+    if check_pools:
+        for gpu, t in enumerate(eng.pools.tensors):
+            got = t.cpu().numpy().reshape(-1)
+            bad = np.nonzero(got != host_pools[gpu])[0]
+            assert bad.size == 0, f"GPU {gpu}: {bad.size} bytes differ, first at {bad[:5]}"
+    return eng, plan, otabs
+
+
+def test_tiny_config_dp2_tp2_and_back():
+    """BASELINE configs[0]: L=2, H=4, d=64, B=16, 8 x 256 tokens, DP2 -> TP2 -> DP2."""
+    w = synth.tiny()
+    geo = (w.L, w.H, w.d, w.B, w.e)
+    nb = synth.pool_blocks(w)
+    spec = list(zip(w.T, w.src, w.dst))
+    run_parity(geo, nb, spec)
+    # and back (fresh pools, TP2 source)
+    run_parity(geo, nb, [(T, d, s) for (T, s, d) in spec], seed=5)
+
+
+GRID = [(H, p0, p1) for H in (1, 2, 4, 8) for p0 in (1, 2, 4, 8) for p1 in (1, 2, 4, 8) if p0 != p1]
+
+
+@pytest.mark.parametrize("H,p0,p1", GRID)
+def test_grid_ragged(H, p0, p1):
+    """All degree pairs up to 8 (incl. GQA replication p > H), ragged T
+    spanning many blocks, partial tail atoms, 2 KiB atoms, 8 virtual ranks."""
+    geo = (3, H, 64, 16, 2)
+    n_gpus = 8
+    Ts = [1, 15, 16, 17, 33, 100, 257, 1000, 31, 64]
+    spec = [(T, ((i * p0) % n_gpus, p0), (((i + 3) * p1) % n_gpus, p1)) for i, T in enumerate(Ts)]
+    nb = [256] * n_gpus
+    run_parity(geo, nb, spec, seed=H * 7 + p0 + 3 * p1)
+
+
+@pytest.mark.parametrize("d,B,e", [(128, 16, 2), (24, 16, 2), (8, 4, 2), (256, 16, 2), (64, 16, 4), (16, 1, 2)])
+def test_atom_sizes(d, B, e):
+    """4 KiB (the configs), 768 B / 64 B / 32 B (generic path), 8 KiB, fp32-sized elements."""
+    geo = (2, 4, d, B, e)
+    spec = [(T, (i % 4, 1), (0, 4) if i % 2 else (i % 4 // 2 * 2, 2)) for i, T in enumerate([5, 130, 77, 1, 64, 200])]
+    run_parity(geo, [96] * 4, spec, seed=d + B + e)
+
+
+def test_per_gpu_launches_and_mixed_plan():
+    """Per-source-GPU launches (the one-process-per-GPU launch shape), a
+    mixed plan with no-ops, empty requests and merges/splits together."""
+    geo = (2, 8, 128, 16, 2)
+    spec = [(300, (0, 1), (0, 2)), (0, (1, 1), (0, 4)), (77, (2, 2), (2, 2)), (513, (4, 4), (4, 1)),
+            (129, (3, 1), (0, 8)), (1, (6, 2), (0, 4)), (64, (5, 1), (5, 1))]
+    run_parity(geo, [128] * 8, spec, seed=11, per_gpu_launch=True)
+
+
+def test_empty_plan():
+    F = _F()
+    from paper_2602_22593_b200.engine import KVSwitchEngine
+    eng = KVSwitchEngine(F.geometry(2, 4, 64, 16, 2), [8, 8], "cuda:0")
+    plan, tables, host = eng.switch([], read_back=True)
+    for g in (0, 1):
+        assert plan.resident(g) == (0, 0)
+        assert host[g][0].tolist() == [0]
+
+
+def test_round_trip_restores_contents():
+    """DP4 -> TP2x2 -> DP4 (config 2 shape, shortened): the logical KV of
+    every request is back byte for byte (checked via the oracle locate)."""
+    geo = (4, 8, 128, 16, 2)
+    og = O.Geom(*geo)
+    w = synth.llama8b_dp4_tp2x2(n_req=16)
+    w.T = [t // 8 for t in w.T]
+    spec = list(zip(w.T, w.src, w.dst))
+    nb = synth.pool_blocks(w)
+    eng, plan, tabs1 = run_parity(geo, nb, spec, seed=3)
+    F = _F()
+    before = [t.clone() for t in eng.pools.tensors]
+    back = [(2000 + i, T, d, tabs1[i], s) for i, (T, s, d) in enumerate(spec)]
+    plan2, tables2, _ = eng.switch(back, read_back=True)
+    torch.cuda.synchronize()
+    tabs2 = plan2.dst_tables()
+    atom = og.B * og.d * og.e
+    M = O.block_bytes(og)
+    for i, (T, s, d) in enumerate(spec):
+        for l in range(og.L):
+            for kv in range(2):
+                for h in range(og.H):
+                    for c in range(-(-T // og.B)):
+                        g1, o1 = O.locate(og, d[0], d[1], tabs1[i], kv, h, c * og.B)
+                        g2, o2 = O.locate(og, s[0], s[1], tabs2[i], kv, h, c * og.B)
+                        a = before[g1].view(-1)[l * nb[g1] * M + o1:][:atom]
+                        b = eng.pools.tensors[g2].view(-1)[l * nb[g2] * M + o2:][:atom]
+                        assert torch.equal(a, b)
+
+
+@pytest.mark.slow
+def test_full_size_config2_sampled():
+    """BASELINE configs[1] at full size in the bench's launch configuration
+    (4 virtual ranks on one B200, one reshard launch): destination tables equal
+    the oracle's allocator in full; 4096 sampled atoms (all replicas) equal the
+    content hash of their oracle-located source; sampled free blocks keep their
+    poison."""
+    F = _F()
+    from paper_2602_22593_b200.engine import KVSwitchEngine
+    w = synth.llama8b_dp4_tp2x2()
+    og = O.Geom(w.L, w.H, w.d, w.B, w.e)
+    nb = synth.pool_blocks(w)
+    eng = KVSwitchEngine(F.geometry(w.L, w.H, w.d, w.B, w.e), nb, "cuda:0")
+    for gpu, t in enumerate(eng.pools.tensors):
+        synth.fill_hash_torch(t, gpu)
+    counts = [O.num_blocks(og, T, s[1]) for T, s in zip(w.T, w.src)]
+    tabs0 = synth.source_tables(w, counts, nb)
+    held = [np.zeros(n, dtype=np.uint8) for n in nb]
+    reqs, oreqs = [], []
+    for i, (T, s, d, ids) in enumerate(zip(w.T, w.src, w.dst, tabs0)):
+        eng.cache.reserve(s, ids)
+        for r in range(s[1]):
+            held[s[0] + r][ids] = 1
+        reqs.append((i, T, s, ids, d))
+        oreqs.append(O.Req(T, s, list(ids), d))
+    plan, tables, host = eng.switch(reqs, read_back=True)
+    st, otabs = O.switch(og, None, held, oreqs, copy=False)
+    assert st == 0
+    assert [list(a) for a in plan.dst_tables()] == [list(b) for b in otabs]
+    for gpu in range(w.n_gpus):
+        rp, ids, meta = O.tables(og, gpu, oreqs, otabs)
+        assert np.array_equal(host[gpu][0].numpy(), rp)
+        assert np.array_equal(host[gpu][1].numpy(), ids)
+        assert np.array_equal(host[gpu][2].numpy(), meta)
+        assert np.array_equal(eng.cache.held_mask(gpu), held[gpu])
+    rng = np.random.default_rng(123)
+    M = O.block_bytes(og)
+    atom_words = og.B * og.d * og.e // 4
+    src_words, dst_idx = [], []
+    for _ in range(4096):
+        i = int(rng.integers(len(w.T)))
+        l, kv, h = int(rng.integers(og.L)), int(rng.integers(2)), int(rng.integers(og.H))
+        c = int(rng.integers(-(-w.T[i] // og.B)))
+        sg, so = O.locate(og, w.src[i][0], w.src[i][1], tabs0[i], kv, h, c * og.B)
+        dg, do = O.locate(og, w.dst[i][0], w.dst[i][1], otabs[i], kv, h, c * og.B)
+        s0 = (l * nb[sg] * M + so) // 4
+        d0 = (l * nb[dg] * M + do) // 4
+        src_words.append(synth.hash32_np(sg, np.arange(s0, s0 + atom_words)))
+        dst_idx.append((dg, d0))
+    for (dg, d0), want in zip(dst_idx, src_words):
+        got = eng.pools.tensors[dg].view(torch.int32).view(-1)[d0:d0 + atom_words].cpu().numpy().view(np.uint32)
+        assert np.array_equal(got, want)
+    # poison survives in blocks nobody holds
+    for gpu in range(w.n_gpus):
+        free = np.nonzero(held[gpu] == 0)[0]
+        for b in rng.choice(free, size=min(16, free.size), replace=False):
+            l = int(rng.integers(og.L))
+            w0 = (l * nb[gpu] * M + int(b) * M) // 4
+            got = eng.pools.tensors[gpu].view(torch.int32).view(-1)[w0:w0 + M // 4].cpu().numpy().view(np.uint32)
+            assert np.array_equal(got, synth.hash32_np(gpu, np.arange(w0, w0 + M // 4)))
+
+
+def test_weight_views_gather():
+    """Eq.1 views on a device matrix, materialised by the gather kernel, equal
+    the numpy oracle slices (bit exact)."""
+    F = _F()
+    from oracle import weights as W
+    Hq, Hkv, d, hidden = 16, 4, 32, 96
+    rows = (Hq + 2 * Hkv) * d
+    full = torch.randn(rows, hidden, device="cuda:0").to(torch.bfloat16)
+    host = full.view(torch.int16).cpu().numpy()
+    for m in (1, 2, 4, 8):
+        for r in range(m):
+            v = F.weight_shard_view(F.weight_desc(full, rows, hidden, 2, F.KV_W_QKV, num_q_heads=Hq,
+                                                  num_kv_heads=Hkv, head_dim=d), r, m)
+            nrow = sum(s.rows for s in v.segments())
+            out = torch.empty(nrow, hidden, dtype=torch.bfloat16, device="cuda:0")
+            F.kv_gather_view(v, out)
+            ref = np.concatenate(W.view_qkv(host, r, m, Hq, Hkv, d))
+            torch.cuda.synchronize()
+            assert np.array_equal(out.view(torch.int16).cpu().numpy(), ref)
+            v = F.weight_shard_view(F.weight_desc(full, rows, hidden, 2, F.KV_W_ROW), r, m)
+            out = torch.empty(rows, hidden // m, dtype=torch.bfloat16, device="cuda:0")
+            F.kv_gather_view(v, out)
+            torch.cuda.synchronize()
+            (ref,) = W.view_row(host, r, m)
+            assert np.array_equal(out.view(torch.int16).cpu().numpy(), ref)
+
+
+def test_launch_counter_moves():
+    F = _F()
+    before = F.launch_count()
+    test_empty_plan()
+    geo = (1, 2, 64, 16, 2)
+    run_parity(geo, [16, 16], [(40, (0, 1), (0, 2))])
+    assert F.launch_count() >= before + 3
