@@ -216,7 +216,7 @@ def fill_hash_torch(pool, gpu: int, seed: int = 2, chunk: int = 1 << 26) -> None
     """Fill a device (or CPU) torch uint8 pool with the same hash, in place.
     torch int64 arithmetic wraps identically; all products stay < 2^63."""
     import torch
-    w = pool.view(torch.int32)
+    w = pool.reshape(-1).view(torch.int32)
     n = w.numel()
     dev = pool.device
     for s in range(0, n, chunk):

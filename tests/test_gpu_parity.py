@@ -120,7 +120,8 @@ def test_atom_sizes(d, B, e):
     """4 KiB (the configs), 768 B / 64 B / 32 B (generic path), 8 KiB, fp32-sized elements."""
     geo = (2, 4, d, B, e)
     spec = [(T, (i % 4, 1), (0, 4) if i % 2 else (i % 4 // 2 * 2, 2)) for i, T in enumerate([5, 130, 77, 1, 64, 200])]
-    run_parity(geo, [96] * 4, spec, seed=d + B + e)
+    w = synth.Workload("t", *geo, 4, [s[0] for s in spec], [s[1] for s in spec], [s[2] for s in spec])
+    run_parity(geo, synth.pool_blocks(w, slack=1.5), spec, seed=d + B + e)
 
 
 def test_per_gpu_launches_and_mixed_plan():
