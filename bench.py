@@ -140,11 +140,14 @@ def build_workload(args, world: int, rank: int):
     return w
 
 
-def src_tables_product(w, nb):
+def pools_and_tables(w):
+    """Pool sizes + fragmented source tables; block counts from the product's
+    own kv_blocks_for (Eq.2)."""
     from paper_2602_22593_b200 import flykv as F
     g = F.geometry(w.L, w.H, w.d, w.B, w.e)
-    counts = [F.kv_blocks_for(g, T, s[1]) for T, s in zip(w.T, w.src)]
-    return synth.source_tables(w, counts, nb)
+    n0 = [F.kv_blocks_for(g, T, s[1]) for T, s in zip(w.T, w.src)]
+    n1 = [F.kv_blocks_for(g, T, d[1]) for T, d in zip(w.T, w.dst)]
+    return synth.realistic_pools(w, n0, n1)
 
 
 # --------------------------------------------------------------- reference arm
@@ -216,12 +219,11 @@ def run_single(args):
     torch.cuda.set_device(dev)
     w = build_workload(args, 1, 0)
     g = F.geometry(w.L, w.H, w.d, w.B, w.e)
-    nb = synth.pool_blocks(w)
+    nb, tabs = pools_and_tables(w)
     eng = KVSwitchEngine(g, nb, dev, tp_degrees=(2, 4, 8))
     if not args.no_fill:
         for i, t in enumerate(eng.pools.tensors):
             synth.fill_hash_torch(t, i)
-    tabs = src_tables_product(w, nb)
     for s, ids in zip(w.src, tabs):
         eng.cache.reserve(s, ids)
     state = {"reqs": [(i, T, s, ids, d) for i, (T, s, d, ids) in enumerate(zip(w.T, w.src, w.dst, tabs))]}
@@ -320,7 +322,7 @@ def run_single(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic",
-        "config": {"workload": w.name + " (4 virtual ranks on 1 GPU)" if w.n_gpus > 1 else w.name,
+        "config": {"workload": w.name + (f" ({w.n_gpus} virtual ranks on 1 GPU)" if w.n_gpus > 1 else ""),
                    "layers": w.L, "kv_heads": w.H, "head_dim": w.d, "block_base": w.B, "requests": len(w.T),
                    "tokens": w.tokens(), "payload_bytes_per_step": payload,
                    "l2": "inputs larger than L2 (payload >> 126 MB), no flush needed",
@@ -339,14 +341,169 @@ def run_single(args):
     return 0
 
 
+def nvlink_roofline(bytes_matrix, hbm_gbs, link_gbs=FALLBACK_NVLINK_GBS):
+    """t_min of SURVEY 8(d): max over GPUs of egress/link, ingress/link,
+    (reads + writes)/HBM, in seconds; plus the per-GPU byte vectors."""
+    m = np.asarray(bytes_matrix, dtype=np.float64)
+    n = m.shape[0]
+    off = m * (1 - np.eye(n))
+    egress = off.sum(1)
+    ingress = off.sum(0)
+    hbm = m.sum(1) + m.sum(0)          # source reads + destination writes
+    t = np.maximum(np.maximum(egress, ingress) / (link_gbs * 1e9), hbm / (hbm_gbs * 1e9))
+    return float(t.max()), egress, ingress, hbm
+
+
+def run_multi(args):
+    """One process per GPU (torchrun).  Every rank pushes the atoms it holds
+    into peer pools (IPC-mapped, NVLink P2P stores), then a group barrier."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2602_22593_b200 import comm
+    from paper_2602_22593_b200 import flykv as F
+
+    world = int(os.environ["WORLD_SIZE"])
+    rank = int(os.environ["RANK"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    same_dev = os.environ.get("FLYKV_SAME_DEVICE") == "1"   # test mode: all ranks on cuda:0, gloo
+    dev = torch.device("cuda", 0 if same_dev else local)
+    torch.cuda.set_device(dev)
+    nccl = not same_dev
+    if nccl:
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        dist.init_process_group("gloo")
+    degrees = [p for p in (2, 4, 8) if p <= world and world % p == 0]
+    cpool = comm.CommunicatorPool(world, degrees, backend="nccl" if nccl else "gloo")
+    w = build_workload(args, world, rank)
+    g = F.geometry(w.L, w.H, w.d, w.B, w.e)
+    _, _, M = F.kv_layout(g, 1)
+    nb, tabs = pools_and_tables(w)
+    local_pool = torch.empty((w.L, nb[rank], M), dtype=torch.uint8, device=dev)
+    if not args.no_fill:
+        synth.fill_hash_torch(local_pool, rank)
+    bases, nbs, imported = comm.exchange_pools(local_pool, rank, world, w.L, M)
+    cache = F.KVCache(g, nbs, bases, degrees)
+    for s_, ids in zip(w.src, tabs):
+        cache.reserve(s_, ids)
+    stream = torch.cuda.Stream(dev)
+    state = {"reqs": [(i, T, s_, ids, d) for i, (T, s_, d, ids) in enumerate(zip(w.T, w.src, w.dst, tabs))]}
+    ev_pairs = []
+    world_key = tuple(range(world))
+
+    def barrier_group(reqs):
+        key = cpool.covering([r[2] for r in reqs] + [r[4] for r in reqs]) if reqs else world_key
+        return key, (None if key == world_key else cpool.get(key))
+
+    def step(timed=False, read_back=False):
+        plan = F.kv_plan_switch(cache, state["reqs"])
+        plan.upload(stream)
+        if timed:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+        F.kv_reshard(plan, rank, stream)
+        if timed:
+            e1.record(stream)
+            ev_pairs.append((e0, e1))
+        key, grp = barrier_group(state["reqs"])
+        comm.switch_barrier(stream, grp, nccl=nccl, device=dev, members=key, rank=rank)
+        n_res, n_ids = plan.resident(rank)
+        rp = torch.empty(n_res + 1, dtype=torch.int32, device=dev)
+        ids = torch.empty(max(n_ids, 1), dtype=torch.int32, device=dev)
+        meta = torch.empty((max(n_res, 1), 4), dtype=torch.int32, device=dev)
+        F.kv_remap_block_tables(plan, rank, rp, ids, meta, stream)
+        host_bytes = 0
+        if read_back:
+            with torch.cuda.stream(stream):
+                h = [rp.to("cpu", non_blocking=True), ids[:n_ids].to("cpu", non_blocking=True),
+                     meta[:n_res].to("cpu", non_blocking=True)]
+            stream.synchronize()
+            host_bytes = sum(int(x.numel()) * 4 for x in h)
+        new = plan.dst_tables()
+        state["reqs"] = [(rid, T, d, t, s_) for (rid, T, s_, _, d), t in zip(state["reqs"], new)]
+        return plan, host_bytes
+
+    plan0 = F.kv_plan_switch(cache, state["reqs"])
+    stats, mat = plan0.stats()
+    plan0.destroy()
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    n_launch0 = F.launch_count()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    keep = []
+    with ClockSampler(dev.index) as clk:
+        start.record(stream)
+        for _ in range(args.steps):
+            keep.append(step(timed=True))
+        end.record(stream)
+        torch.cuda.synchronize()
+    dist.barrier()
+    launches = F.launch_count() - n_launch0
+    my_ms = start.elapsed_time(end)
+    my_kern = sum(a.elapsed_time(b) for a, b in ev_pairs) / len(ev_pairs)
+    keep.clear()
+    lat = []
+    h2d = d2h = 0
+    if not args.no_e2e:
+        for _ in range(args.steps):
+            dist.barrier()
+            t0 = time.perf_counter()
+            plan, hb = step(read_back=True)
+            lat.append((time.perf_counter() - t0) * 1e3)
+            h2d += plan.stats()[0]["h2d_bytes"]
+            d2h += hb
+    red = torch.tensor([my_ms, my_kern, max(lat) if lat else 0.0, (sum(lat) / len(lat)) if lat else 0.0,
+                        float(launches)], dtype=torch.float64, device=dev if nccl else "cpu")
+    dist.all_reduce(red, op=dist.ReduceOp.MAX)
+    total_ms, kern_ms, _, lat_mean, launches_max = [float(x) for x in red.tolist()]
+    comm.close_pools(imported)
+    if rank == 0:
+        payload = stats["payload_bytes"]
+        hbm_peak, peak_src = peaks()
+        t_min, egress, ingress, hbm = nvlink_roofline(mat, hbm_peak)
+        busiest = float(max(egress.max(), ingress.max()))
+        achieved = busiest / (kern_ms / 1e3) / 1e9
+        line = {
+            "metric": "DP<->TP KV re-layout GB/s", "value": round(payload * args.steps / (total_ms / 1e3) / 1e9, 3),
+            "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": w.name + (" (ranks share cuda:0, gloo)" if same_dev else ""), "layers": w.L,
+                       "kv_heads": w.H, "head_dim": w.d, "block_base": w.B, "requests": len(w.T),
+                       "tokens": w.tokens(), "payload_bytes_per_step": payload,
+                       "l2": "inputs larger than L2, no flush needed",
+                       "step": "plan + upload + reshard (P2P push over NVLink) + group barrier + remap"},
+            "switch_latency_ms": round(total_ms / args.steps, 4),
+            "reshard_kernel_ms": round(kern_ms, 4),
+            "roofline": {"bound": "nvlink", "achieved": round(achieved, 1), "peak": FALLBACK_NVLINK_GBS,
+                         "unit": "GB/s", "frac": round(achieved / FALLBACK_NVLINK_GBS, 4), "traffic": None,
+                         "peak_source": "measured peer copy per direction (B200_PROFILING.md 770 GB/s)",
+                         "t_min_ms": round(t_min * 1e3, 4), "frac_of_t_min": round(t_min * 1e3 / kern_ms, 4),
+                         "kernel": "flykv_reshard_kernel (busiest GPU's egress/ingress per launch)"},
+            "cpu_baseline": None,
+            "e2e": ({"value": round(payload / (lat_mean / 1e3) / 1e9, 3), "unit": "GB/s",
+                     "h2d_bytes_per_step": int(h2d // max(len(lat), 1)),
+                     "d2h_bytes_per_step": int(d2h // max(len(lat), 1)),
+                     "switch_latency_ms_mean_max_over_ranks": round(lat_mean, 3)} if lat else None),
+            "gpu_launches": int(launches_max),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if world > 1:
-        from paper_2602_22593_b200 import comm
-        return comm.run_bench_multi(args)
+        return run_multi(args)
     return run_single(args)
 
 

@@ -151,10 +151,10 @@ def pool_blocks(w: Workload, slack: float = 1.10, extra: int = 8) -> list:
     return [int(n * slack) + extra for n in need]
 
 
-def source_tables(w: Workload, counts: list, num_blocks: list, seed: int = 1) -> list:
+def source_tables(w: Workload, counts: list, num_blocks: list, seed: int = 1, window=None) -> list:
     """Fragmented source tables: per source group a seeded permutation of the
-    IDs [0, min pool size over the group), consumed in request order, skipping
-    IDs already used on any member GPU (groups may overlap).
+    IDs [0, window) (default: the whole pool), consumed in request order,
+    skipping IDs already used on any member GPU (groups may overlap).
     counts[i] = blocks request i holds (computed by the caller's own code)."""
     rng = np.random.default_rng(seed)
     perms, cursor = {}, {}
@@ -165,6 +165,8 @@ def source_tables(w: Workload, counts: list, num_blocks: list, seed: int = 1) ->
         members = range(grp[0], grp[0] + grp[1])
         if grp not in perms:
             nb = min(num_blocks[g] for g in members)
+            if window is not None:
+                nb = min(nb, int(window))
             perms[grp] = rng.permutation(nb).astype(np.int32)
             cursor[grp] = 0
         perm, c = perms[grp], cursor[grp]
@@ -181,6 +183,29 @@ def source_tables(w: Workload, counts: list, num_blocks: list, seed: int = 1) ->
         cursor[grp] = c
         out.append(np.asarray(ids, dtype=np.int32))
     return out
+
+
+def realistic_pools(w: Workload, n_src: list, n_dst: list, frag: float = 1.25, slack: float = 1.05,
+                    seed: int = 1):
+    """Equal-sized pools and fragmented source tables for the benches.
+
+    Each live engine's blocks are scattered (seeded permutation) over the low
+    window [0, frag * max per-GPU source blocks) of its pool -- fragmented but
+    not spread over the whole pool, as a running engine's are -- and the pool
+    adds room for the largest per-GPU destination need.  n_src[i] / n_dst[i]:
+    blocks request i holds per rank at its source / destination degree,
+    computed by the caller's own code.  Returns (num_blocks, tables)."""
+    src_need = [0] * w.n_gpus
+    dst_need = [0] * w.n_gpus
+    for s, d, a, b in zip(w.src, w.dst, n_src, n_dst):
+        for g in range(s[0], s[0] + s[1]):
+            src_need[g] += a
+        for g in range(d[0], d[0] + d[1]):
+            dst_need[g] += b
+    window = int(frag * max(src_need)) + 16
+    nb_all = window + int(slack * max(max(dst_need), max(src_need))) + 32
+    nb = [nb_all] * w.n_gpus
+    return nb, source_tables(w, n_src, nb, seed=seed, window=window)
 
 
 # ------------------------------------------------------------ content hashing

@@ -1,0 +1,93 @@
+"""Communicator pool and replicated planning, world_size 2 and 4 over gloo on
+CPU (no GPU): aligned-group enumeration, eager construction and
+O(1) lookup, and every rank building the identical plan from the
+globally agreed request order -- the property the one-process-per-GPU
+path relies on."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2602_22593_b200 import comm
+
+
+def test_enumerate_groups_paper_example():
+    assert comm.enumerate_tp_groups(4, [2, 4]) == [(0, 1), (2, 3), (0, 1, 2, 3)]
+    assert len(comm.enumerate_tp_groups(8, [2, 4, 8])) == 7
+    assert comm.enumerate_tp_groups(2, []) == []
+    with pytest.raises(ValueError):
+        comm.enumerate_tp_groups(4, [3])
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2602_22593_b200 import flykv as F
+        import synth
+        pool = comm.CommunicatorPool(world, [2, 4], backend="gloo")
+        out = {"keys": sorted(pool.groups.keys())}
+        try:
+            pool.get((1, 2))
+            out["unaligned"] = "found"
+        except comm.UnknownGroup:
+            out["unaligned"] = "UnknownGroup"
+        out["cover"] = pool.covering([(0, 1), (1, 1)])
+        out["cover2"] = pool.covering([(2, 1), (0, 2)])
+        # replicated allocator + identical plan on every rank (fake pointers)
+        w = synth.dp_to_tp(world, 12, L=2, H=8, d=64, B=16, lo=10, hi=300)
+        g = F.geometry(w.L, w.H, w.d, w.B, w.e)
+        n0 = [F.kv_blocks_for(g, T, s[1]) for T, s in zip(w.T, w.src)]
+        n1 = [F.kv_blocks_for(g, T, d[1]) for T, d in zip(w.T, w.dst)]
+        nb, tabs = synth.realistic_pools(w, n0, n1)
+        bases = [[(1 << 40) + (r << 36) + (l << 30) for l in range(w.L)] for r in range(world)]
+        cache = F.KVCache(g, nb, bases, (2, 4))
+        for s_, ids in zip(w.src, tabs):
+            cache.reserve(s_, ids)
+        plan = F.kv_plan_switch(cache, [(i, T, s_, ids, d) for i, (T, s_, d, ids) in
+                                        enumerate(zip(w.T, w.src, w.dst, tabs))])
+        digest = np.concatenate(plan.dst_tables()).astype(np.int64)
+        st, mat = plan.stats()
+        mine = (int(digest.sum()), int((digest * np.arange(digest.size)).sum()), int(mat.sum()))
+        allv = [None] * world
+        dist.all_gather_object(allv, mine)
+        out["identical_plans"] = all(v == allv[0] for v in allv)
+        # a barrier on a pooled subgroup
+        sub = pool.get((0, 1)) if rank < 2 else pool.get((2, 3))
+        dist.barrier(group=sub)
+        out["ok"] = True
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_pool_and_replicated_plans_gloo(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    for r in range(world):
+        o = res[r]
+        assert o["ok"] and o["identical_plans"]
+        assert o["unaligned"] == "UnknownGroup"
+        assert o["cover"] == (0, 1)
+        if world == 4:
+            assert o["keys"] == [(0, 1), (0, 1, 2, 3), (2, 3)]
+            assert o["cover2"] == (0, 1, 2, 3)

@@ -1,0 +1,115 @@
+"""One process per pool, peer pools mapped through CUDA IPC, each rank's
+reshard kernel pushing its atoms into the other ranks' pools (the N-GPU launch
+shape).  On a 1-GPU box both processes share cuda:0 (CUDA IPC between two
+processes on one device) and gloo carries the barrier; the data path is the
+same P2P-store kernel.  Whole pools are compared with the oracle."""
+import os
+import socket
+import tempfile
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+GEO = (3, 8, 128, 16, 2)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _workload(world):
+    w = synth.dp_to_tp(world, 6 * world, L=GEO[0], H=GEO[1], d=GEO[2], B=GEO[3], lo=1, hi=700, seed=4)
+    return w
+
+
+def _rank(rank, world, port, outdir):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2602_22593_b200 import comm
+        from paper_2602_22593_b200 import flykv as F
+        w = _workload(world)
+        g = F.geometry(*GEO)
+        _, _, M = F.kv_layout(g, 1)
+        n0 = [F.kv_blocks_for(g, T, s[1]) for T, s in zip(w.T, w.src)]
+        n1 = [F.kv_blocks_for(g, T, d[1]) for T, d in zip(w.T, w.dst)]
+        nb, tabs = synth.realistic_pools(w, n0, n1)
+        pool = torch.empty((w.L, nb[rank], M), dtype=torch.uint8, device="cuda:0")
+        synth.fill_hash_torch(pool, rank)
+        torch.cuda.synchronize()
+        bases, nbs, imported = comm.exchange_pools(pool, rank, world, w.L, M)
+        cache = F.KVCache(g, nbs, bases, [p for p in (2, 4, 8) if p <= world])
+        for s_, ids in zip(w.src, tabs):
+            cache.reserve(s_, ids)
+        stream = torch.cuda.Stream()
+        plan = F.kv_plan_switch(cache, [(i, T, s_, ids, d) for i, (T, s_, d, ids) in
+                                        enumerate(zip(w.T, w.src, w.dst, tabs))])
+        F.kv_reshard(plan, rank, stream)
+        comm.switch_barrier(stream, None, nccl=False)
+        n_res, n_ids = plan.resident(rank)
+        rp = torch.empty(n_res + 1, dtype=torch.int32, device="cuda:0")
+        ids = torch.empty(max(n_ids, 1), dtype=torch.int32, device="cuda:0")
+        meta = torch.empty((max(n_res, 1), 4), dtype=torch.int32, device="cuda:0")
+        F.kv_remap_block_tables(plan, rank, rp, ids, meta, stream)
+        stream.synchronize()
+        dist.barrier()
+        np.save(os.path.join(outdir, f"pool{rank}.npy"), pool.cpu().numpy().reshape(-1))
+        np.save(os.path.join(outdir, f"rp{rank}.npy"), rp.cpu().numpy())
+        np.save(os.path.join(outdir, f"ids{rank}.npy"), ids[:n_ids].cpu().numpy())
+        np.save(os.path.join(outdir, f"meta{rank}.npy"), meta[:n_res].cpu().numpy())
+        dist.barrier()
+        comm.close_pools(imported)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_ipc_push_matches_oracle(world):
+    import torch.multiprocessing as mp
+    w = _workload(world)
+    og = O.Geom(*GEO)
+    n0 = [O.num_blocks(og, T, s[1]) for T, s in zip(w.T, w.src)]
+    n1 = [O.num_blocks(og, T, d[1]) for T, d in zip(w.T, w.dst)]
+    nb, tabs = synth.realistic_pools(w, n0, n1)
+    with tempfile.TemporaryDirectory() as td:
+        ctx = mp.get_context("spawn")
+        port = _free_port()
+        procs = [ctx.Process(target=_rank, args=(r, world, port, td)) for r in range(world)]
+        for p in procs:
+            p.start()
+        for p in procs:
+            p.join(timeout=300)
+            assert p.exitcode == 0
+        M = O.block_bytes(og)
+        pools = []
+        for r in range(world):
+            a = np.zeros(og.L * nb[r] * M, dtype=np.uint8)
+            synth.fill_hash_np(a, r)
+            pools.append(a)
+        held = [np.zeros(n, dtype=np.uint8) for n in nb]
+        oreqs = []
+        for T, s, d, ids in zip(w.T, w.src, w.dst, tabs):
+            held[s[0]][ids] = 1
+            oreqs.append(O.Req(T, s, list(ids), d))
+        st, otabs = O.switch(og, pools, held, oreqs)
+        assert st == 0
+        for r in range(world):
+            got = np.load(os.path.join(td, f"pool{r}.npy"))
+            assert np.array_equal(got, pools[r]), f"rank {r} pool differs"
+            rp, ids, meta = O.tables(og, r, oreqs, otabs)
+            assert np.array_equal(np.load(os.path.join(td, f"rp{r}.npy")), rp)
+            assert np.array_equal(np.load(os.path.join(td, f"ids{r}.npy")), ids)
+            assert np.array_equal(np.load(os.path.join(td, f"meta{r}.npy")), meta)
