@@ -557,6 +557,7 @@ extern "C" kv_status kv_reshard(kv_plan* p, int32_t gpu, void* stream_) {
     a.atom_bytes = (int32_t)c->atom_bytes;
     a.M = c->M;
     a.fence_sys = gpu >= 0 ? 1 : 0;
+    a.peer = gpu >= 0 ? 1 : 0;
     if (a.atom_hi <= a.atom_lo) return KV_OK;
     cudaError_t e = launch_reshard(a, p->dev, stream);
     if (e != cudaSuccess) return cuda_fail(e, "flykv_reshard_kernel launch");
@@ -793,3 +794,10 @@ extern "C" const char* kv_strerror(kv_status s) {
 extern "C" const char* kv_last_error(void) { return g_err.c_str(); }
 
 extern "C" int64_t kv_launch_count(void) { return g_launches.load(); }
+
+extern "C" kv_status kv_set_reshard_impl(int32_t impl, int32_t ctas_per_sm) {
+    if (impl < 0 || impl > 3 || ctas_per_sm < 0 || ctas_per_sm > 32)
+        return fail(KV_ERR_INVALID_ARG, "impl %d / ctas_per_sm %d", impl, ctas_per_sm);
+    set_reshard_impl(impl, ctas_per_sm);
+    return KV_OK;
+}

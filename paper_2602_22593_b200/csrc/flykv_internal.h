@@ -71,6 +71,7 @@ struct ReshardArgs {
     int32_t atom_bytes;        // B*d*e
     int64_t M;                 // block bytes per layer
     int32_t fence_sys;         // 1: release-fence writes at system scope (peer pools)
+    int32_t peer;              // 1: destinations may be peer (NVLink) mappings -> LDG/STG path
 };
 
 struct RemapArgs {
@@ -93,6 +94,7 @@ struct GatherSeg {
 
 // Kernel launchers (flykv_kernels.cu).  Return cudaSuccess or the launch error.
 cudaError_t launch_reshard(const ReshardArgs& a, int device, cudaStream_t s);
+void set_reshard_impl(int impl, int ctas_per_sm);
 cudaError_t launch_remap(const RemapArgs& a, cudaStream_t s);
 cudaError_t launch_gather(const GatherSeg* segs, int n_seg, char* dst, cudaStream_t s);
 

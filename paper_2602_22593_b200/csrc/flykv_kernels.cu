@@ -85,70 +85,294 @@ __device__ __forceinline__ char* dst_ptr(const ReshardArgs& a, const AtomAddr& a
     return a.layer_base[(ad.dst_g0 + r) * a.L + ad.l] + ad.doff;
 }
 
-// VPL = 16-byte vectors per lane per atom (atom_bytes = VPL * 512); VPL = 0
-// is the generic path for atoms that are a multiple of 16 but not of 512.
-template <int VPL>
-__global__ void __launch_bounds__(256) flykv_reshard_kernel(const ReshardArgs a) {
+// Lane-parallel decode: each lane of the warp decodes one of 32 consecutive
+// atoms, then the warp walks them, receiving addresses by shuffle -- the
+// index arithmetic costs 1/32 of an issue slot per atom.  Only the source,
+// replica-0 destination and replica count stay live; replicas > 0 (GQA)
+// re-decode their atom.
+struct LaneAtom {
+    const char* src;
+    char* dst0;
+    int32_t rep1;
+};
+
+__device__ __forceinline__ void lane_decode(const ReshardArgs& a, int64_t atom, LaneAtom& la) {
+    const int s = find_seg(a.seg_begin, a.seg_lo, a.seg_hi, atom);
+    AtomAddr ad;
+    decode(a, atom, s, ad);
+    la.src = ad.src;
+    la.rep1 = ad.rep1;
+    la.dst0 = dst_ptr(a, ad, 0);
+}
+
+template <typename T>
+__device__ __forceinline__ T shfl_ptr(T p, int k) {
+    return reinterpret_cast<T>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(p), k));
+}
+
+// Destination of replica j of `atom` (warp-uniform re-decode, rare path).
+__device__ __forceinline__ char* replica_ptr(const ReshardArgs& a, int64_t atom, int j) {
+    const int s = find_seg(a.seg_begin, a.seg_lo, a.seg_hi, atom);
+    AtomAddr ad;
+    decode(a, atom, s, ad);
+    return dst_ptr(a, ad, j);
+}
+
+// ---------------------------------------------------------------- LDG/STG
+// VPL = 16-byte vectors per lane per atom (atom_bytes = VPL * 512).  Each
+// warp moves one 4 KiB atom per iteration: 8 x LDG.128 per lane issued back
+// to back (32 KiB... per warp in flight: 4 KiB), then 8 x STG.128 per
+// destination replica.  VPL = 0: generic atoms (multiple of 16 bytes).
+// U = atoms per warp iteration: the loads of U atoms (U * 8 LDG.128 per
+// lane for 4 KiB atoms) are in flight before their stores are issued.
+template <int VPL, int U>
+__global__ void __launch_bounds__(256, ((U == 1 && VPL <= 8) ? 4 : 2)) flykv_reshard_kernel(const ReshardArgs a) {
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t atom = a.atom_lo + warp; atom < a.atom_hi; atom += nwarps) {
-        const int s = find_seg(a.seg_begin, a.seg_lo, a.seg_hi, atom);
-        AtomAddr ad;
-        decode(a, atom, s, ad);
-        if constexpr (VPL > 0) {
-            const int4* src = reinterpret_cast<const int4*>(ad.src) + lane;
-            int4 v[VPL];
+    for (int64_t base = a.atom_lo + warp * 32; base < a.atom_hi; base += nwarps * 32) {
+        LaneAtom la;
+        const int64_t mine = base + lane;
+        if (mine < a.atom_hi) lane_decode(a, mine, la);
+        const int64_t left = a.atom_hi - base;
+        const int n = left < 32 ? (int)left : 32;
+        if constexpr (VPL > 0 && U == 1) {
+            for (int k = 0; k < n; ++k) {
+                const int4* src = reinterpret_cast<const int4*>(shfl_ptr(la.src, k)) + lane;
+                int4* dst = reinterpret_cast<int4*>(shfl_ptr(la.dst0, k)) + lane;
+                const int rep = __shfl_sync(0xffffffffu, la.rep1, k);
+                int4 v[VPL];
 #pragma unroll
-            for (int i = 0; i < VPL; ++i) v[i] = ld_stream(src + i * 32);
-            for (int j = 0; j < ad.rep1; ++j) {
-                int4* dst = reinterpret_cast<int4*>(dst_ptr(a, ad, j)) + lane;
+                for (int i = 0; i < VPL; ++i) v[i] = ld_stream(src + i * 32);
 #pragma unroll
                 for (int i = 0; i < VPL; ++i) st_stream(dst + i * 32, v[i]);
+                for (int j = 1; j < rep; ++j) {
+                    int4* dj = reinterpret_cast<int4*>(replica_ptr(a, base + k, j)) + lane;
+#pragma unroll
+                    for (int i = 0; i < VPL; ++i) st_stream(dj + i * 32, v[i]);
+                }
+            }
+        } else if constexpr (VPL > 0) {
+            for (int k0 = 0; k0 < n; k0 += U) {
+                int4 v[U][VPL];
+                const char* s[U];
+                char* d0[U];
+                int rep[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int k = (k0 + u < n) ? k0 + u : k0;
+                    s[u] = shfl_ptr(la.src, k);
+                    d0[u] = shfl_ptr(la.dst0, k);
+                    rep[u] = (k0 + u < n) ? __shfl_sync(0xffffffffu, la.rep1, k) : 0;
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int4* src = reinterpret_cast<const int4*>(s[u]) + lane;
+#pragma unroll
+                    for (int i = 0; i < VPL; ++i) v[u][i] = ld_stream(src + i * 32);
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    for (int j = 0; j < rep[u]; ++j) {
+                        int4* dst = reinterpret_cast<int4*>(j == 0 ? d0[u] : replica_ptr(a, base + k0 + u, j)) + lane;
+#pragma unroll
+                        for (int i = 0; i < VPL; ++i) st_stream(dst + i * 32, v[u][i]);
+                    }
+                }
             }
         } else {
-            const int nv = a.atom_bytes >> 4;
-            const int4* src = reinterpret_cast<const int4*>(ad.src);
-            for (int i = lane; i < nv; i += 32) {
-                int4 v = ld_stream(src + i);
-                for (int j = 0; j < ad.rep1; ++j) st_stream(reinterpret_cast<int4*>(dst_ptr(a, ad, j)) + i, v);
+            for (int k = 0; k < n; ++k) {
+                const char* s = shfl_ptr(la.src, k);
+                char* d0 = shfl_ptr(la.dst0, k);
+                const int rep = __shfl_sync(0xffffffffu, la.rep1, k);
+                const int nv = a.atom_bytes >> 4;
+                for (int j = 0; j < rep; ++j) {
+                    char* dj = j == 0 ? d0 : replica_ptr(a, base + k, j);
+                    for (int i = lane; i < nv; i += 32)
+                        st_stream(reinterpret_cast<int4*>(dj) + i, ld_stream(reinterpret_cast<const int4*>(s) + i));
+                }
             }
         }
     }
     if (a.fence_sys) __threadfence_system();
 }
 
-template <int VPL>
-static cudaError_t launch_reshard_t(const ReshardArgs& a, int device, cudaStream_t s) {
-    static int sm_count[64] = {0};
-    static int per_sm[64] = {0};
+// ---------------------------------------------------------------- TMA bulk
+// Each warp runs its own S-stage shared-memory ring; lane 0 drives the
+// async-copy engine: cp.async.bulk global->shared (completes on a per-stage
+// mbarrier), then cp.async.bulk shared->global to every destination replica
+// (bulk_group, one commit per atom).  Loads run D = S - 2 atoms ahead of the
+// stores; a stage is refilled once cp.async.bulk.wait_group.read shows its
+// stores have finished reading it.  No data passes through registers.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+
+template <int S>
+__global__ void __launch_bounds__(128) flykv_reshard_tma_kernel(const ReshardArgs a, int stage_bytes) {
+    constexpr int D = S - 2;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int lane = threadIdx.x & 31;
+    const int wid = threadIdx.x >> 5;
+    const int nw = blockDim.x >> 5;
+    unsigned char* ring = smem + (size_t)wid * S * stage_bytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)nw * S * stage_bytes) + wid * S;
+    // per-stage pending store: replica-0 destination, replica count, atom index (lane 0 only)
+    __shared__ char* pend_dst[4][S];
+    __shared__ int32_t pend_rep[4][S];
+    __shared__ int64_t pend_atom[4][S];
+    if (lane == 0) {
+        for (int i = 0; i < S; ++i)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bars + i)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    uint64_t policy;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+    const uint32_t bytes = (uint32_t)a.atom_bytes;
+    const int64_t warp = (int64_t)blockIdx.x * nw + wid;
+    const int64_t nwarps = (int64_t)gridDim.x * nw;
+    uint32_t issued = 0, stored = 0;
+    auto store_one = [&](uint32_t j) {
+        const int st = j % S;
+        mbar_wait(smem_u32(bars + st), (j / S) & 1u);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        const uint32_t src = smem_u32(ring + (size_t)st * stage_bytes);
+        const int rep = pend_rep[wid][st];
+        for (int r = 0; r < rep; ++r) {
+            char* dst = r == 0 ? pend_dst[wid][st] : replica_ptr(a, pend_atom[wid][st], r);
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(dst),
+                         "r"(src), "r"(bytes), "l"(policy)
+                         : "memory");
+        }
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    };
+    for (int64_t base = a.atom_lo + warp * 32; base < a.atom_hi; base += nwarps * 32) {
+        LaneAtom la;
+        const int64_t mine = base + lane;
+        if (mine < a.atom_hi) lane_decode(a, mine, la);
+        const int64_t left = a.atom_hi - base;
+        const int n = left < 32 ? (int)left : 32;
+        for (int k = 0; k < n; ++k) {
+            const char* s = shfl_ptr(la.src, k);
+            char* d0 = shfl_ptr(la.dst0, k);
+            const int rep = __shfl_sync(0xffffffffu, la.rep1, k);
+            if (lane == 0) {
+                if (issued >= (uint32_t)D) store_one(stored++);
+                const int st = issued % S;
+                // stage st last held atom issued - S; after the store above,
+                // the S - D most recent bulk groups are atoms issued-S+1 ..
+                // issued-D, so waiting down to S - D pending frees stage st.
+                asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(S - D) : "memory");
+                pend_dst[wid][st] = d0;
+                pend_rep[wid][st] = rep;
+                pend_atom[wid][st] = base + k;
+                const uint32_t bar = smem_u32(bars + st);
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                             : "memory");
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, "
+                    "[%3], %4;" ::"r"(smem_u32(ring + (size_t)st * stage_bytes)),
+                    "l"(s), "r"(bytes), "r"(bar), "l"(policy)
+                    : "memory");
+                ++issued;
+            }
+        }
+    }
+    if (lane == 0) {
+        while (stored < issued) store_one(stored++);
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        if (a.fence_sys) __threadfence_system();
+    }
+    __syncwarp();
+}
+
+// ---------------------------------------------------------------- launch
+static int g_impl = 0;          // 0 auto, 1 LDG, 2 TMA
+static int g_ctas_per_sm = 0;   // 0 auto
+
+void set_reshard_impl(int impl, int ctas_per_sm) {
+    g_impl = impl;
+    g_ctas_per_sm = ctas_per_sm;
+}
+
+static int sm_count_of(int device) {
+    static int cache[64] = {0};
     if (device < 0 || device >= 64) device = 0;
-    if (sm_count[device] == 0) {
-        cudaError_t e = cudaDeviceGetAttribute(&sm_count[device], cudaDevAttrMultiProcessorCount, device);
-        if (e != cudaSuccess) return e;
+    if (cache[device] == 0) cudaDeviceGetAttribute(&cache[device], cudaDevAttrMultiProcessorCount, device);
+    return cache[device] > 0 ? cache[device] : 148;
+}
+
+template <int VPL, int U = 1>
+static cudaError_t launch_ldg(const ReshardArgs& a, int device, cudaStream_t s) {
+    static int per_sm = 0;
+    if (per_sm == 0) {
         int nb = 0;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, flykv_reshard_kernel<VPL>, 256, 0);
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, flykv_reshard_kernel<VPL, U>, 256, 0);
         if (e != cudaSuccess) return e;
-        per_sm[device] = nb > 0 ? nb : 1;
+        per_sm = nb > 0 ? nb : 1;
     }
     const int64_t atoms = a.atom_hi - a.atom_lo;
-    int64_t want = (atoms + 7) / 8;
-    int64_t cap = (int64_t)sm_count[device] * per_sm[device];
+    const int per = g_ctas_per_sm > 0 ? g_ctas_per_sm : per_sm;
+    int64_t want = (atoms + 8 * 32 - 1) / (8 * 32);
+    int64_t cap = (int64_t)sm_count_of(device) * per;
     int grid = (int)(want < cap ? want : cap);
     if (grid < 1) grid = 1;
-    flykv_reshard_kernel<VPL><<<grid, 256, 0, s>>>(a);
+    flykv_reshard_kernel<VPL, U><<<grid, 256, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+template <int S>
+static cudaError_t launch_tma(const ReshardArgs& a, int device, cudaStream_t s) {
+    constexpr int W = 4;
+    const int stage = (a.atom_bytes + 127) & ~127;
+    const size_t smem = (size_t)W * S * stage + (size_t)W * S * 8;
+    static size_t configured = 0;
+    if (smem > configured) {
+        cudaError_t e = cudaFuncSetAttribute(flykv_reshard_tma_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        configured = smem;
+    }
+    int per = g_ctas_per_sm;
+    if (per <= 0) {
+        int nb = 0;
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, flykv_reshard_tma_kernel<S>, W * 32, smem);
+        if (e != cudaSuccess) return e;
+        per = nb > 0 ? nb : 1;
+    }
+    const int64_t atoms = a.atom_hi - a.atom_lo;
+    int64_t want = (atoms + W * 32 - 1) / (W * 32);
+    int64_t cap = (int64_t)sm_count_of(device) * per;
+    int grid = (int)(want < cap ? want : cap);
+    if (grid < 1) grid = 1;
+    flykv_reshard_tma_kernel<S><<<grid, W * 32, smem, s>>>(a, stage);
     return cudaGetLastError();
 }
 
 cudaError_t launch_reshard(const ReshardArgs& a, int device, cudaStream_t s) {
     if (a.atom_hi <= a.atom_lo) return cudaSuccess;
+    const bool tma_ok = (a.atom_bytes % 16) == 0 && a.atom_bytes <= 16384;
+    if (g_impl == 2 && tma_ok && !a.peer) return launch_tma<8>(a, device, s);
+    if (g_impl == 3 && a.atom_bytes == 4096) return launch_ldg<8, 2>(a, device, s);
+    if (g_impl == 3 && a.atom_bytes == 2048) return launch_ldg<4, 2>(a, device, s);
     switch (a.atom_bytes) {
-        case 512: return launch_reshard_t<1>(a, device, s);
-        case 1024: return launch_reshard_t<2>(a, device, s);
-        case 2048: return launch_reshard_t<4>(a, device, s);
-        case 4096: return launch_reshard_t<8>(a, device, s);
-        case 8192: return launch_reshard_t<16>(a, device, s);
-        default: return launch_reshard_t<0>(a, device, s);
+        case 512: return launch_ldg<1>(a, device, s);
+        case 1024: return launch_ldg<2>(a, device, s);
+        case 2048: return launch_ldg<4>(a, device, s);
+        case 4096: return launch_ldg<8>(a, device, s);
+        case 8192: return launch_ldg<16>(a, device, s);
+        default: return launch_ldg<0>(a, device, s);
     }
 }
 

@@ -130,12 +130,13 @@ _sig("kv_stream_sync", C.c_int, _P)
 _sig("kv_strerror", C.c_char_p, C.c_int)
 _sig("kv_last_error", C.c_char_p)
 _sig("kv_launch_count", C.c_int64)
+_sig("kv_set_reshard_impl", C.c_int, C.c_int32, C.c_int32)
 
 EXPORTED = ["kv_cache_create", "kv_cache_destroy", "kv_layout", "kv_blocks_for", "kv_alloc", "kv_reserve",
             "kv_free", "kv_free_count", "kv_held_mask", "kv_plan_switch", "kv_plan_upload", "kv_reshard", "kv_plan_resident",
             "kv_remap_block_tables", "kv_plan_dst_tables", "kv_plan_get_stats", "kv_plan_destroy",
             "weight_shard_view", "kv_gather_view", "kv_ipc_export", "kv_ipc_import", "kv_ipc_close",
-            "kv_stream_sync", "kv_strerror", "kv_last_error", "kv_launch_count"]
+            "kv_stream_sync", "kv_strerror", "kv_last_error", "kv_launch_count", "kv_set_reshard_impl"]
 
 
 # ----------------------------------------------------------------- marshalling
@@ -182,6 +183,11 @@ def kv_blocks_for(geom: Geometry, num_tokens: int, degree: int) -> int:
 
 def launch_count() -> int:
     return int(_lib.kv_launch_count())
+
+
+def set_reshard_impl(impl: int = 0, ctas_per_sm: int = 0):
+    """0 default (LDG/STG), 1 LDG/STG, 2 TMA bulk ring (local pools)."""
+    _check(_lib.kv_set_reshard_impl(impl, ctas_per_sm))
 
 
 def strerror(status: int) -> str:

@@ -1,0 +1,66 @@
+"""Kernel-variant sweep on one B200: reshard kernel time for the bench's c2
+plan (idempotent until commit, so one plan is re-run), for each variant and
+CTA count, next to a plain device-to-device copy of the same byte count."""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import synth  # noqa: E402
+from paper_2602_22593_b200 import flykv as F  # noqa: E402
+from paper_2602_22593_b200.engine import KVSwitchEngine  # noqa: E402
+
+
+def main():
+    cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
+    w = synth.WORKLOADS[cfg]()
+    g = F.geometry(w.L, w.H, w.d, w.B, w.e)
+    nb, tabs = bench.pools_and_tables(w)
+    eng = KVSwitchEngine(g, nb, "cuda:0")
+    for s_, ids in zip(w.src, tabs):
+        eng.cache.reserve(s_, ids)
+    plan = eng.plan([(i, T, s_, ids, d) for i, (T, s_, d, ids) in enumerate(zip(w.T, w.src, w.dst, tabs))])
+    st, _ = plan.stats()
+    algo = (st["n_atoms"] + st["n_atom_writes"]) * st["atom_bytes"]
+    stream = eng.stream
+    plan.upload(stream)
+    res = {"config": cfg, "algorithmic_bytes": algo}
+
+    def timeit(fn, reps=10):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        evs = []
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            evs.append((a, b))
+        torch.cuda.synchronize()
+        ts = sorted(x.elapsed_time(y) for x, y in evs)
+        return ts[len(ts) // 2]
+
+    for impl, ctas in [(1, 0), (1, 2), (3, 0), (2, 0), (1, 0)]:
+        try:
+            F.set_reshard_impl(impl, ctas)
+            ms = timeit(lambda: F.kv_reshard(plan, -1, stream))
+            res[f"impl{impl}_ctas{ctas}"] = {"ms": ms, "GBps": algo / ms / 1e6}
+        except Exception as e:  # noqa: BLE001
+            res[f"impl{impl}_ctas{ctas}"] = str(e)
+        print(json.dumps(res), flush=True)
+    F.set_reshard_impl(0, 0)
+    n = st["payload_bytes"]
+    a = torch.empty(n, dtype=torch.uint8, device="cuda:0")
+    b = torch.empty(n, dtype=torch.uint8, device="cuda:0")
+    with torch.cuda.stream(stream):
+        ms = timeit(lambda: b.copy_(a))
+    res["torch_copy_same_bytes"] = {"ms": ms, "GBps": 2 * n / ms / 1e6}
+    print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    main()
