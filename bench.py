@@ -48,7 +48,7 @@ FALLBACK_NVLINK_GBS = 770.0     # measured peer copy per direction (B200_PROFILI
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=int(os.environ.get("WORLD_SIZE", "1")))
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=4)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", help="workload key of synth.WORKLOADS (N=1)")
@@ -79,7 +79,9 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region:
+    a background `nvidia-smi --query-gpu=... -lms 50` started before the
+    region and stopped after it (B200_PROFILING.md clocks line)."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -88,36 +90,43 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.rows = []
-        self._stop = threading.Event()
-        self._t = None
-
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([x.strip() for x in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+        self._p = None
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        try:
+            self._p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                        "--format=csv,noheader,nounits", "-lms", "50"],
+                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.15)  # first sample lands before the region starts
+        except Exception:
+            self._p = None
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        if self._t:
-            self._t.join(timeout=10)
+        if self._p is None:
+            return
+        time.sleep(0.06)
+        self._p.terminate()
+        try:
+            out, _ = self._p.communicate(timeout=5)
+        except Exception:
+            self._p.kill()
+            out, _ = self._p.communicate()
+        for line in out.splitlines():
+            if line.strip():
+                self.rows.append([x.strip() for x in line.split(",")])
 
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [v for v in (num(r[1]) for r in self.rows if len(r) > 2) if v is not None]
+        mx = [v for v in (num(r[2]) for r in self.rows if len(r) > 2) if v is not None]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = set()
         for r in self.rows:
@@ -235,10 +244,14 @@ def run_single(args):
 
     ev_pairs = []
 
+    step_stats = []
+
     def step(timed_kernel=False):
         plan = eng.plan(state["reqs"])
         plan.upload(stream)
         if timed_kernel:
+            st_, _ = plan.stats()
+            step_stats.append(st_)
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
@@ -265,19 +278,27 @@ def run_single(args):
             step()
         torch.cuda.synchronize()
         # ------------------------------------------------ device-timed region
+        # per-step events; when the payload fits in L2 a 512 MiB buffer is
+        # rewritten between steps, outside the step events (L2 flush)
+        flush = None
+        if 2 * stats["payload_bytes"] < 4 * 126 * 2 ** 20:
+            flush = torch.empty(512 * 2 ** 20, dtype=torch.uint8, device=dev)
         n_launch0 = F.launch_count()
-        start = torch.cuda.Event(enable_timing=True)
-        end = torch.cuda.Event(enable_timing=True)
+        step_ev = []
         with ClockSampler(torch.cuda.current_device()) as clk:
             torch.cuda.synchronize()
-            start.record(stream)
             plans = []
             for _ in range(args.steps):
+                if flush is not None:
+                    flush.fill_(1)
+                a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a_.record(stream)
                 plans.append(step(timed_kernel=True))
-            end.record(stream)
+                b_.record(stream)
+                step_ev.append((a_, b_))
             torch.cuda.synchronize()
         launches = F.launch_count() - n_launch0
-        total_ms = start.elapsed_time(end)
+        total_ms = sum(a_.elapsed_time(b_) for a_, b_ in step_ev)
         kern_ms = [a.elapsed_time(b) for a, b in ev_pairs]
         plans.clear()
         clocks = clk.summary()
@@ -286,6 +307,7 @@ def run_single(args):
         lat_ms = []
         if not args.no_e2e:
             h2d = d2h = 0
+            e2e_payload = 0
             for it in range(args.steps):
                 t0 = time.perf_counter()
                 plan, tables, host = eng.switch(state["reqs"], read_back=True)
@@ -293,17 +315,22 @@ def run_single(args):
                 lat_ms.append((t1 - t0) * 1e3)
                 st_, _ = plan.stats()
                 h2d += st_["h2d_bytes"]
+                e2e_payload += st_["payload_bytes"]
                 d2h += sum(int(x.numel()) * 4 for v in host.values() for x in v)
                 state["reqs"] = next_requests(plan)
-            e2e = {"value": round(stats["payload_bytes"] * len(lat_ms) / (sum(lat_ms) / 1e3) / 1e9, 3), "unit": "GB/s",
+            e2e = {"value": round(e2e_payload / (sum(lat_ms) / 1e3) / 1e9, 3), "unit": "GB/s",
                    "h2d_bytes_per_step": int(h2d // len(lat_ms)), "d2h_bytes_per_step": int(d2h // len(lat_ms)),
                    "switch_latency_ms_p50": round(statistics.median(lat_ms), 3),
                    "switch_latency_ms_p99": round(float(np.percentile(lat_ms, 99)), 3)}
 
-    payload = stats["payload_bytes"]
-    value = payload * args.steps / (total_ms / 1e3) / 1e9
+    # per-step statistics: directions alternate, and under GQA replication the
+    # two directions move different byte counts (TP>H writes p/H replicas)
+    payload_sum = sum(x["payload_bytes"] for x in step_stats)
+    payload = payload_sum / len(step_stats)
+    value = payload_sum / (total_ms / 1e3) / 1e9
     kmean = sum(kern_ms) / len(kern_ms)
-    algo_bytes = (stats["n_atoms"] + stats["n_atom_writes"]) * stats["atom_bytes"]  # read + write, all local HBM
+    # read once + write every replica, all local HBM (virtual ranks share one device)
+    algo_bytes = sum((x["n_atoms"] + x["n_atom_writes"]) * x["atom_bytes"] for x in step_stats) / len(step_stats)
     hbm_peak, peak_src = peaks()
     achieved = algo_bytes / (kmean / 1e3) / 1e9
     traffic = None
@@ -324,14 +351,16 @@ def run_single(args):
         "data": "synthetic",
         "config": {"workload": w.name + (f" ({w.n_gpus} virtual ranks on 1 GPU)" if w.n_gpus > 1 else ""),
                    "layers": w.L, "kv_heads": w.H, "head_dim": w.d, "block_base": w.B, "requests": len(w.T),
-                   "tokens": w.tokens(), "payload_bytes_per_step": payload,
-                   "l2": "inputs larger than L2 (payload >> 126 MB), no flush needed",
+                   "tokens": w.tokens(), "payload_bytes_per_step": int(payload),
+                   "payload_bytes_forward": stats["payload_bytes"],
+                   "l2": ("L2 flushed between steps (512 MiB rewrite, outside the step events)" if flush is not None
+                          else "inputs larger than L2 (payload >> 126 MB), no flush needed"),
                    "step": "plan + descriptor upload + reshard + remap (alternating direction)"},
         "switch_latency_ms": round(total_ms / args.steps, 4),
         "reshard_kernel_ms": round(kmean, 4),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                      "frac": round(achieved / hbm_peak, 4), "traffic": traffic, "peak_source": peak_src,
-                     "kernel": "flykv_reshard_kernel", "algorithmic_bytes_per_launch": algo_bytes},
+                     "kernel": "flykv_reshard_kernel", "algorithmic_bytes_per_launch": int(algo_bytes)},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,
@@ -396,10 +425,13 @@ def run_multi(args):
         key = cpool.covering([r[2] for r in reqs] + [r[4] for r in reqs]) if reqs else world_key
         return key, (None if key == world_key else cpool.get(key))
 
+    step_stats = []
+
     def step(timed=False, read_back=False):
         plan = F.kv_plan_switch(cache, state["reqs"])
         plan.upload(stream)
         if timed:
+            step_stats.append(plan.stats())
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
         F.kv_reshard(plan, rank, stream)
@@ -447,6 +479,7 @@ def run_multi(args):
     keep.clear()
     lat = []
     h2d = d2h = 0
+    e2e_payload = 0
     if not args.no_e2e:
         for _ in range(args.steps):
             dist.barrier()
@@ -454,6 +487,7 @@ def run_multi(args):
             plan, hb = step(read_back=True)
             lat.append((time.perf_counter() - t0) * 1e3)
             h2d += plan.stats()[0]["h2d_bytes"]
+            e2e_payload += plan.stats()[0]["payload_bytes"]
             d2h += hb
     red = torch.tensor([my_ms, my_kern, max(lat) if lat else 0.0, (sum(lat) / len(lat)) if lat else 0.0,
                         float(launches)], dtype=torch.float64, device=dev if nccl else "cpu")
@@ -461,30 +495,40 @@ def run_multi(args):
     total_ms, kern_ms, _, lat_mean, launches_max = [float(x) for x in red.tolist()]
     comm.close_pools(imported)
     if rank == 0:
-        payload = stats["payload_bytes"]
+        payload_sum = sum(x[0]["payload_bytes"] for x in step_stats)
+        payload = payload_sum / len(step_stats)
         hbm_peak, peak_src = peaks()
-        t_min, egress, ingress, hbm = nvlink_roofline(mat, hbm_peak)
-        busiest = float(max(egress.max(), ingress.max()))
+        t_min = busiest = 0.0
+        for _, m in step_stats:
+            t, eg, ing, _ = nvlink_roofline(m, hbm_peak)
+            t_min += t / len(step_stats)
+            busiest += float(max(eg.max(), ing.max())) / len(step_stats)
         achieved = busiest / (kern_ms / 1e3) / 1e9
+        hbm_algo = sum((x[0]["n_atoms"] + x[0]["n_atom_writes"]) * x[0]["atom_bytes"] for x in step_stats) / len(step_stats)
         line = {
-            "metric": "DP<->TP KV re-layout GB/s", "value": round(payload * args.steps / (total_ms / 1e3) / 1e9, 3),
+            "metric": "DP<->TP KV re-layout GB/s", "value": round(payload_sum / (total_ms / 1e3) / 1e9, 3),
             "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": w.name + (" (ranks share cuda:0, gloo)" if same_dev else ""), "layers": w.L,
                        "kv_heads": w.H, "head_dim": w.d, "block_base": w.B, "requests": len(w.T),
-                       "tokens": w.tokens(), "payload_bytes_per_step": payload,
+                       "tokens": w.tokens(), "payload_bytes_per_step": int(payload),
                        "l2": "inputs larger than L2, no flush needed",
                        "step": "plan + upload + reshard (P2P push over NVLink) + group barrier + remap"},
             "switch_latency_ms": round(total_ms / args.steps, 4),
             "reshard_kernel_ms": round(kern_ms, 4),
-            "roofline": {"bound": "nvlink", "achieved": round(achieved, 1), "peak": FALLBACK_NVLINK_GBS,
-                         "unit": "GB/s", "frac": round(achieved / FALLBACK_NVLINK_GBS, 4), "traffic": None,
-                         "peak_source": "measured peer copy per direction (B200_PROFILING.md 770 GB/s)",
-                         "t_min_ms": round(t_min * 1e3, 4), "frac_of_t_min": round(t_min * 1e3 / kern_ms, 4),
-                         "kernel": "flykv_reshard_kernel (busiest GPU's egress/ingress per launch)"},
+            "roofline": ({"bound": "nvlink", "achieved": round(achieved, 1), "peak": FALLBACK_NVLINK_GBS,
+                          "unit": "GB/s", "frac": round(achieved / FALLBACK_NVLINK_GBS, 4), "traffic": None,
+                          "peak_source": "measured peer copy per direction (B200_PROFILING.md 770 GB/s)",
+                          "t_min_ms": round(t_min * 1e3, 4), "frac_of_t_min": round(t_min * 1e3 / kern_ms, 4),
+                          "kernel": "flykv_reshard_kernel (busiest GPU's egress/ingress per launch)"}
+                         if not same_dev else
+                         {"bound": "hbm", "achieved": round(hbm_algo / (kern_ms / 1e3) / 1e9, 1), "peak": hbm_peak,
+                          "unit": "GB/s", "frac": round(hbm_algo / (kern_ms / 1e3) / 1e9 / hbm_peak, 4),
+                          "traffic": None, "peak_source": peak_src,
+                          "kernel": "flykv_reshard_kernel (all ranks' launches run concurrently on cuda:0)"}),
             "cpu_baseline": None,
-            "e2e": ({"value": round(payload / (lat_mean / 1e3) / 1e9, 3), "unit": "GB/s",
+            "e2e": ({"value": round(e2e_payload / len(lat) / (lat_mean / 1e3) / 1e9, 3), "unit": "GB/s",
                      "h2d_bytes_per_step": int(h2d // max(len(lat), 1)),
                      "d2h_bytes_per_step": int(d2h // max(len(lat), 1)),
                      "switch_latency_ms_mean_max_over_ranks": round(lat_mean, 3)} if lat else None),
