@@ -210,6 +210,27 @@ kv_status kv_plan_resident(const kv_plan* plan, int32_t gpu, int32_t* n_resident
 kv_status kv_remap_block_tables(kv_plan* plan, int32_t gpu, int32_t* req_ptr, int32_t* block_ids,
                                 int32_t* per_req_meta, void* stream);
 
+/* kv_plan_commit: a7 on the host -- release every moving request's source
+ * IDs (R13).  Implied by the first kv_remap_block_tables; call it directly
+ * when the caller builds its block tables itself.  Idempotent.  Only after
+ * every GPU's reshard of this plan has completed (group barrier). */
+kv_status kv_plan_commit(kv_plan* plan);
+
+/*
+ * kv_plan_waves: memory-bounded waves (for the memory-driven
+ * long-context promotion).  Partitions reqs (in order) into
+ * consecutive waves such that each wave, planned after the previous waves
+ * have been committed (their sources released), fits next to its own
+ * sources, and (if max_wave_bytes > 0) moves at most max_wave_bytes of
+ * destination payload unless a single request exceeds it.  Simulates the
+ * allocator; no state change.  wave_start: host [n_reqs + 1], wave k is
+ * reqs[wave_start[k] .. wave_start[k+1]); *n_waves >= 1.  OUT_OF_BLOCKS if a
+ * request does not fit even alone.  The caller then runs, per wave:
+ * kv_plan_switch -> kv_reshard -> barrier -> kv_remap_block_tables.
+ */
+kv_status kv_plan_waves(const kv_cache* cache, const kv_request* reqs, int32_t n_reqs, int64_t max_wave_bytes,
+                        int32_t* wave_start, int32_t* n_waves);
+
 /* Host copies of every destination table, in plan order: dst_ptr host
  * [n_reqs+1], dst_ids host [dst_ptr[n_reqs]] (pass dst_ids = NULL to size). */
 kv_status kv_plan_dst_tables(const kv_plan* plan, int32_t* dst_ptr, int32_t* dst_ids);

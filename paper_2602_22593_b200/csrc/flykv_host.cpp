@@ -145,14 +145,16 @@ static int32_t group_min_blocks(const kv_cache* c, kv_group g) {
 // The n lowest IDs free on every GPU of g (R6, R8): OR the members' held
 // words, then walk free bits with count-trailing-zeros.  Marks them held on
 // every member when found.  Returns false (nothing marked) if fewer than n.
-static bool alloc_lowest(kv_cache* c, kv_group g, int32_t n, int32_t* out) {
+typedef std::vector<std::vector<uint64_t>> Bitmaps;
+
+static bool alloc_lowest_in(const kv_cache* c, Bitmaps& held, kv_group g, int32_t n, int32_t* out) {
     if (n == 0) return true;
     const int32_t nb = group_min_blocks(c, g);
     const int32_t words = (nb + 63) >> 6;
     int32_t got = 0;
     for (int32_t w = 0; w < words && got < n; ++w) {
         uint64_t used = 0;
-        for (int32_t r = 0; r < g.degree; ++r) used |= c->held[g.first_gpu + r][w];
+        for (int32_t r = 0; r < g.degree; ++r) used |= held[g.first_gpu + r][w];
         uint64_t fr = ~used;
         const int32_t top = nb - (w << 6);
         if (top < 64) fr &= (top <= 0) ? 0ull : ((1ull << top) - 1);
@@ -163,8 +165,12 @@ static bool alloc_lowest(kv_cache* c, kv_group g, int32_t n, int32_t* out) {
     }
     if (got < n) return false;
     for (int32_t r = 0; r < g.degree; ++r)
-        for (int32_t k = 0; k < n; ++k) bit_set(c->held[g.first_gpu + r], out[k]);
+        for (int32_t k = 0; k < n; ++k) bit_set(held[g.first_gpu + r], out[k]);
     return true;
+}
+
+static bool alloc_lowest(kv_cache* c, kv_group g, int32_t n, int32_t* out) {
+    return alloc_lowest_in(c, c->held, g, n, out);
 }
 
 // ------------------------------------------------------------ cache API
@@ -300,15 +306,11 @@ extern "C" kv_status kv_held_mask(const kv_cache* c, int32_t gpu, uint8_t* held)
 }
 
 // ------------------------------------------------------------ planner
-extern "C" kv_status kv_plan_switch(kv_cache* c, const kv_request* reqs, int32_t n_reqs, kv_plan** out) {
-    if (!c || !out || n_reqs < 0 || (n_reqs > 0 && !reqs))
-        return fail(KV_ERR_INVALID_ARG, "bad kv_plan_switch arguments");
-    *out = nullptr;
-    const kv_geometry& G = c->geo;
-    const int32_t H = G.num_kv_heads, L = G.num_layers, B = G.block_base;
+// a2: validate a request list against the cache (no state change).
+static kv_status validate_requests(const kv_cache* c, const kv_request* reqs, int32_t n_reqs, int64_t* total_src_out,
+                                   int64_t* total_dst_bound_out) {
+    const int32_t H = c->geo.num_kv_heads, B = c->geo.block_base;
     const int32_t n = c->n_gpus;
-
-    // ---- a2 validation (no state change) ----
     std::unordered_set<int64_t> ids_seen;
     std::vector<std::vector<uint64_t>> in_plan(n);
     for (int32_t g = 0; g < n; ++g) in_plan[g].assign(c->held[g].size(), 0ull);
@@ -343,6 +345,24 @@ extern "C" kv_status kv_plan_switch(kv_cache* c, const kv_request* reqs, int32_t
         total_src += r.n_src_blocks;
         total_dst_bound += ceil_div(r.num_tokens, B);
     }
+
+    *total_src_out = total_src;
+    *total_dst_bound_out = total_dst_bound;
+    return KV_OK;
+}
+
+extern "C" kv_status kv_plan_switch(kv_cache* c, const kv_request* reqs, int32_t n_reqs, kv_plan** out) {
+    if (!c || !out || n_reqs < 0 || (n_reqs > 0 && !reqs))
+        return fail(KV_ERR_INVALID_ARG, "bad kv_plan_switch arguments");
+    *out = nullptr;
+    const kv_geometry& G = c->geo;
+    const int32_t H = G.num_kv_heads, L = G.num_layers, B = G.block_base;
+    const int32_t n = c->n_gpus;
+
+    // ---- a2 validation (no state change) ----
+    int64_t total_src = 0, total_dst_bound = 0;
+    kv_status vs = validate_requests(c, reqs, n_reqs, &total_src, &total_dst_bound);
+    if (vs) return vs;
 
     kv_plan* p = new (std::nothrow) kv_plan();
     if (!p) return fail(KV_ERR_INVALID_ARG, "out of host memory");
@@ -581,6 +601,63 @@ static void commit(kv_plan* p) {
             for (int32_t k = 0; k < q.n0; ++k) bit_clr(c->held[q.src.first_gpu + r], p->tables[q.src_off + k]);
     }
     p->state = PLAN_COMMITTED;
+}
+
+extern "C" kv_status kv_plan_commit(kv_plan* p) {
+    if (!p) return fail(KV_ERR_INVALID_ARG, "plan is NULL");
+    commit(p);
+    return KV_OK;
+}
+
+extern "C" kv_status kv_plan_waves(const kv_cache* c, const kv_request* reqs, int32_t n_reqs, int64_t max_wave_bytes,
+                                   int32_t* wave_start, int32_t* n_waves) {
+    if (!c || !wave_start || !n_waves || n_reqs < 0 || (n_reqs > 0 && !reqs) || max_wave_bytes < 0)
+        return fail(KV_ERR_INVALID_ARG, "bad kv_plan_waves arguments");
+    int64_t ts = 0, td = 0;
+    kv_status s = validate_requests(c, reqs, n_reqs, &ts, &td);
+    if (s) return s;
+    const kv_geometry& G = c->geo;
+    const int32_t H = G.num_kv_heads, B = G.block_base;
+    Bitmaps sim = c->held;  // simulated allocator state
+    std::vector<int32_t> ids;
+    int32_t w = 0, start = 0;
+    int64_t wave_bytes = 0;
+    auto close_wave = [&](int32_t end) {  // release the wave's sources (its remap commits it)
+        for (int32_t j = start; j < end; ++j) {
+            const kv_request& r = reqs[j];
+            if (r.src.first_gpu == r.dst.first_gpu && r.src.degree == r.dst.degree) continue;
+            for (int32_t q = 0; q < r.src.degree; ++q)
+                for (int32_t k = 0; k < r.n_src_blocks; ++k) bit_clr(sim[r.src.first_gpu + q], r.src_blocks[k]);
+        }
+        wave_start[w++] = start;
+        start = end;
+        wave_bytes = 0;
+    };
+    for (int32_t i = 0; i < n_reqs; ++i) {
+        const kv_request& r = reqs[i];
+        const bool moving = !(r.src.first_gpu == r.dst.first_gpu && r.src.degree == r.dst.degree);
+        if (!moving) continue;
+        const Layout l1 = layout_of(H, r.dst.degree);
+        const int32_t n1 = (int32_t)ceil_div(r.num_tokens, (int64_t)B * l1.k);
+        const int64_t bytes = (int64_t)G.num_layers * 2 * H * ceil_div(r.num_tokens, B) * c->atom_bytes * l1.rep;
+        if (max_wave_bytes > 0 && i > start && wave_bytes + bytes > max_wave_bytes) close_wave(i);
+        ids.resize(n1);
+        if (!alloc_lowest_in(c, sim, r.dst, n1, ids.data())) {
+            if (i > start) {
+                close_wave(i);
+                if (alloc_lowest_in(c, sim, r.dst, n1, ids.data())) {
+                    wave_bytes += bytes;
+                    continue;
+                }
+            }
+            return fail(KV_ERR_OUT_OF_BLOCKS, "request %d does not fit even in a wave of its own", i);
+        }
+        wave_bytes += bytes;
+    }
+    if (n_reqs > start || w == 0) close_wave(n_reqs);
+    wave_start[w] = n_reqs;
+    *n_waves = w;
+    return KV_OK;
 }
 
 extern "C" kv_status kv_remap_block_tables(kv_plan* p, int32_t gpu, int32_t* req_ptr, int32_t* block_ids,

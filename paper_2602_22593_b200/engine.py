@@ -77,3 +77,14 @@ class KVSwitchEngine:
                                t.meta[:n_res].to("cpu", non_blocking=True))
             self.stream.synchronize()
         return plan, tables, host
+
+    def switch_waves(self, requests, max_wave_bytes: int = 0, read_back=False):
+        """Memory-bounded switch: waves planned by
+        kv_plan_waves; each wave is a full switch whose commit frees its
+        sources before the next wave allocates.  Returns [(plan, tables, host)]."""
+        requests = list(requests)
+        waves = flykv.kv_plan_waves(self.cache, requests, max_wave_bytes)
+        out = []
+        for a, b in waves:
+            out.append(self.switch(requests[a:b], read_back=read_back))
+        return out

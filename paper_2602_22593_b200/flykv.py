@@ -119,6 +119,8 @@ _sig("kv_reshard", C.c_int, _P, C.c_int32, _P)
 _sig("kv_plan_resident", C.c_int, _P, C.c_int32, _I32P, _I32P)
 _sig("kv_remap_block_tables", C.c_int, _P, C.c_int32, _P, _P, _P, _P)
 _sig("kv_plan_dst_tables", C.c_int, _P, _I32P, _I32P)
+_sig("kv_plan_commit", C.c_int, _P)
+_sig("kv_plan_waves", C.c_int, _P, C.POINTER(Request), C.c_int32, C.c_int64, _I32P, _I32P)
 _sig("kv_plan_get_stats", C.c_int, _P, C.POINTER(PlanStats), _I64P)
 _sig("kv_plan_destroy", None, _P)
 _sig("weight_shard_view", C.c_int, C.POINTER(WeightDesc), C.c_int32, C.c_int32, C.POINTER(View))
@@ -134,7 +136,7 @@ _sig("kv_set_reshard_impl", C.c_int, C.c_int32, C.c_int32)
 
 EXPORTED = ["kv_cache_create", "kv_cache_destroy", "kv_layout", "kv_blocks_for", "kv_alloc", "kv_reserve",
             "kv_free", "kv_free_count", "kv_held_mask", "kv_plan_switch", "kv_plan_upload", "kv_reshard", "kv_plan_resident",
-            "kv_remap_block_tables", "kv_plan_dst_tables", "kv_plan_get_stats", "kv_plan_destroy",
+            "kv_remap_block_tables", "kv_plan_dst_tables", "kv_plan_commit", "kv_plan_waves", "kv_plan_get_stats", "kv_plan_destroy",
             "weight_shard_view", "kv_gather_view", "kv_ipc_export", "kv_ipc_import", "kv_ipc_close",
             "kv_stream_sync", "kv_strerror", "kv_last_error", "kv_launch_count", "kv_set_reshard_impl"]
 
@@ -283,6 +285,9 @@ class Plan:
     def remap_block_tables(self, gpu, req_ptr, block_ids, per_req_meta, stream=None):
         return kv_remap_block_tables(self, gpu, req_ptr, block_ids, per_req_meta, stream)
 
+    def commit(self):
+        _check(_lib.kv_plan_commit(self._h))
+
     def dst_tables(self) -> list:
         ptr = np.zeros(self.n_reqs + 1, dtype=np.int32)
         _check(_lib.kv_plan_dst_tables(self._h, ptr.ctypes.data_as(_I32P), None))
@@ -318,6 +323,16 @@ def kv_plan_switch(cache: KVCache, requests) -> Plan:
     h = C.c_void_p()
     _check(_lib.kv_plan_switch(cache._h, arr, n, C.byref(h)))
     return Plan(cache, h, n)
+
+
+def kv_plan_waves(cache: KVCache, requests, max_wave_bytes: int = 0) -> list:
+    """Memory-bounded waves: list of (start, end) request index ranges."""
+    arr, keep = make_requests(requests)
+    n = len(keep)
+    ws = np.zeros(n + 2, dtype=np.int32)
+    nw = C.c_int32()
+    _check(_lib.kv_plan_waves(cache._h, arr, n, int(max_wave_bytes), ws.ctypes.data_as(_I32P), C.byref(nw)))
+    return [(int(ws[k]), int(ws[k + 1])) for k in range(nw.value)]
 
 
 def kv_reshard(plan: Plan, gpu: int = -1, stream=None):

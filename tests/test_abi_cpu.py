@@ -234,3 +234,46 @@ def test_weight_views_match_oracle():
     with pytest.raises(F.FlyKVError) as e:
         F.weight_shard_view(F.weight_desc(base, 6, 8, 4, F.KV_W_ROW), 4, 4)
     assert e.value.name == "KV_ERR_RANK_OUT_OF_RANGE"
+
+
+def test_memory_bounded_waves_match_oracle():
+    """a DP -> TP8 promotion that does not fit in one shot
+    (OUT_OF_BLOCKS) succeeds in waves; every wave's tables equal the oracle's
+    allocator applied wave after wave, and allocator states agree."""
+    geo = (2, 8, 8, 4, 2)
+    og = O.Geom(*geo)
+    n_gpus, nb = 8, [56] * 8
+    c = fake_cache(geo, nb)
+    rng = np.random.default_rng(9)
+    held = [np.zeros(n, dtype=np.uint8) for n in nb]
+    reqs = []
+    for i in range(24):
+        T = int(rng.integers(20, 50))
+        src = (i % n_gpus, 1)
+        ids = c.alloc(src, F.kv_blocks_for(c.geom, T, 1))
+        held[src[0]][ids] = 1
+        reqs.append((i, T, src, ids, (0, 8)))
+    with pytest.raises(F.FlyKVError) as e:
+        c.plan_switch(reqs)
+    assert e.value.name == "KV_ERR_OUT_OF_BLOCKS"
+    waves = F.kv_plan_waves(c, reqs)
+    assert len(waves) > 1 and waves[0][0] == 0 and waves[-1][1] == len(reqs)
+    assert all(a < b for a, b in waves) and all(waves[k][1] == waves[k + 1][0] for k in range(len(waves) - 1))
+    for a, b in waves:
+        plan = c.plan_switch(reqs[a:b])
+        st, otabs = O.switch(og, None, held, [O.Req(T, s, list(ids), d) for (_, T, s, ids, d) in reqs[a:b]],
+                             copy=False)
+        assert st == 0
+        assert [list(x) for x in plan.dst_tables()] == [list(y) for y in otabs]
+        plan.commit()
+        for g in range(n_gpus):
+            assert np.array_equal(c.held_mask(g), held[g])
+    # a byte cap splits further
+    c2 = fake_cache(geo, [4096] * 8)
+    reqs2 = []
+    for i in range(8):
+        ids = c2.alloc((i, 1), F.kv_blocks_for(c2.geom, 64, 1))
+        reqs2.append((i, 64, (i, 1), ids, (0, 8)))
+    one = 2 * 2 * 8 * 64 * 8 * 2   # L*2*H*T*d*e per request
+    assert len(F.kv_plan_waves(c2, reqs2)) == 1
+    assert [b - a for a, b in F.kv_plan_waves(c2, reqs2, max_wave_bytes=3 * one)] == [3, 3, 2]

@@ -286,3 +286,62 @@ def test_reshard_variants(impl, H, p0, p1, d):
         run_parity(geo, [400] * 8, spec, seed=impl * 31 + H + p0 + p1)
     finally:
         F.set_reshard_impl(0, 0)
+
+
+def test_memory_bounded_waves_gpu():
+    """SURVEY 8(f) N1 on the device: a promotion that does not fit in one
+    shot runs in waves (kv_plan_waves -> switch per wave); whole pools equal
+    the oracle applied wave after wave."""
+    F = _F()
+    from paper_2602_22593_b200.engine import KVSwitchEngine
+    geo = (2, 8, 64, 16, 2)
+    og = O.Geom(*geo)
+    nb = [56] * 8
+    eng = KVSwitchEngine(F.geometry(*geo), nb, "cuda:0")
+    for gpu, t in enumerate(eng.pools.tensors):
+        synth.fill_hash_torch(t, gpu, seed=77)
+    torch.cuda.synchronize()
+    host = [t.cpu().numpy().reshape(-1).copy() for t in eng.pools.tensors]
+    held = [np.zeros(n, dtype=np.uint8) for n in nb]
+    rng = np.random.default_rng(9)
+    reqs = []
+    for i in range(24):
+        T = int(rng.integers(80, 200))
+        src = (i % 8, 1)
+        ids = eng.cache.alloc(src, F.kv_blocks_for(eng.geom, T, 1))
+        held[src[0]][ids] = 1
+        reqs.append((i, T, src, ids, (0, 8)))
+    with pytest.raises(F.FlyKVError):
+        eng.plan(reqs)
+    waves = F.kv_plan_waves(eng.cache, reqs)
+    assert len(waves) > 1
+    out = eng.switch_waves(reqs, read_back=True)
+    assert len(out) == len(waves)
+    for (a, b), (plan, tables, hb) in zip(waves, out):
+        st, otabs = O.switch(og, host, held, [O.Req(T, s, list(ids), d) for (_, T, s, ids, d) in reqs[a:b]])
+        assert st == 0
+        assert [list(x) for x in plan.dst_tables()] == [list(y) for y in otabs]
+    for gpu, t in enumerate(eng.pools.tensors):
+        assert np.array_equal(t.cpu().numpy().reshape(-1), host[gpu])
+        assert np.array_equal(eng.cache.held_mask(gpu), held[gpu])
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_random_mixed_plans(seed):
+    """Randomised plans: random H, head_dim, degrees (merge, split, lateral,
+    no-op), lengths incl. 0, 8 virtual ranks; bit-exact against the oracle."""
+    rng = np.random.default_rng(1000 + seed)
+    H = int(rng.choice([1, 2, 4, 8]))
+    d = int(rng.choice([64, 128]))
+    geo = (int(rng.integers(1, 4)), H, d, 16, 2)
+    n_gpus = 8
+    spec = []
+    used_src = set()
+    for i in range(int(rng.integers(1, 14))):
+        p0 = int(rng.choice([1, 2, 4, 8]))
+        p1 = int(rng.choice([1, 2, 4, 8]))
+        g0 = int(rng.integers(0, n_gpus // p0)) * p0
+        g1 = int(rng.integers(0, n_gpus // p1)) * p1
+        T = int(rng.choice([0, 1, int(rng.integers(2, 40)), int(rng.integers(40, 900))]))
+        spec.append((T, (g0, p0), (g1, p1)))
+    run_parity(geo, [480] * n_gpus, spec, seed=seed)
