@@ -307,10 +307,10 @@ kv_status kv_stream_sync(void* stream);
 const char* kv_strerror(kv_status s);
 const char* kv_last_error(void);
 /* Tuning knob for the reshard kernel (process-wide): impl 0 = default
- * (LDG/STG warp copy, one atom per warp iteration), 1 = same, 2 = TMA
- * bulk-copy ring (local pools only; peer pools always use LDG/STG), 3 =
- * LDG/STG with two atoms in flight per warp; ctas_per_sm 0 = occupancy
- * maximum.  Measured alternatives, see DESIGN.md section 7. */
+ * (LDG/STG warp copy, two atoms in flight per warp for 2/4 KiB atoms), 1 =
+ * LDG/STG one atom per warp iteration, 2 = TMA bulk-copy ring (local pools
+ * only; peer pools always use LDG/STG), 3 = same as 0; ctas_per_sm 0 =
+ * occupancy maximum.  Measured alternatives, see DESIGN.md section 7. */
 kv_status kv_set_reshard_impl(int32_t impl, int32_t ctas_per_sm);
 
 /* Number of kernels this library launched since load (evidence counter). */

@@ -57,9 +57,9 @@ __device__ __forceinline__ void decode(const ReshardArgs& a, int64_t atom, int s
     uint32_t nh = (uint32_t)sg.nh, C = (uint32_t)sg.C;
     uint32_t hh = local % nh;
     local /= nh;
-    uint32_t c = local % C;
-    uint32_t lkv = local / C;
-    uint32_t kv = lkv & 1u, l = lkv >> 1;
+    const uint32_t c = local % C;  // ((l*2 + kv)*C + c)*nh + hh
+    const uint32_t lkv = local / C;
+    const uint32_t kv = lkv & 1u, l = lkv >> 1;
     int32_t h = sg.h0 + (int32_t)hh;
     const int64_t half = a.M >> 1;
     const int64_t ab = a.atom_bytes;
@@ -364,8 +364,9 @@ cudaError_t launch_reshard(const ReshardArgs& a, int device, cudaStream_t s) {
     if (a.atom_hi <= a.atom_lo) return cudaSuccess;
     const bool tma_ok = (a.atom_bytes % 16) == 0 && a.atom_bytes <= 16384;
     if (g_impl == 2 && tma_ok && !a.peer) return launch_tma<8>(a, device, s);
-    if (g_impl == 3 && a.atom_bytes == 4096) return launch_ldg<8, 2>(a, device, s);
-    if (g_impl == 3 && a.atom_bytes == 2048) return launch_ldg<4, 2>(a, device, s);
+    // default (0) and 3: two atoms in flight per warp (measured +1%)
+    if ((g_impl == 0 || g_impl == 3) && a.atom_bytes == 4096) return launch_ldg<8, 2>(a, device, s);
+    if ((g_impl == 0 || g_impl == 3) && a.atom_bytes == 2048) return launch_ldg<4, 2>(a, device, s);
     switch (a.atom_bytes) {
         case 512: return launch_ldg<1>(a, device, s);
         case 1024: return launch_ldg<2>(a, device, s);
