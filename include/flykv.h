@@ -288,6 +288,26 @@ kv_status weight_shard_view(const kv_weight_desc* full, int32_t rank, int32_t de
  * segments) on `stream`.  Used only to check views against the oracle. */
 kv_status kv_gather_view(const kv_view* view, void* dst, void* stream);
 
+/* ------------------------------------------------------- consumer proof */
+
+/*
+ * kv_paged_decode: SURVEY 8(f) N3 -- paged decode attention over one layer
+ * of one pool, reading the cache through the per-request "stride and
+ * capacity" the Adaptor gives the attention kernel: the CSR table of
+ * kv_remap_block_tables (req_ptr, block_ids) and per_req_meta {index, B(p),
+ * H_loc(p), first KV head}.  Local query head j uses local KV head
+ * j / (q_heads_local / H_loc) (GQA).  out[r][j] = softmax(scale * q.K^T) V
+ * over tokens 0..seq_lens[r]-1, fp32 online softmax in token order (so a TP
+ * rank and the DP replica produce identical bits for the same head).
+ *   layer_base  device, layer l region of the pool
+ *   q           device bf16 [n_res][q_heads_local][head_dim]
+ *   out         device fp32 [n_res][q_heads_local][head_dim]
+ * bf16 and head_dim 64/128/256 only (INVALID_ARG otherwise).
+ */
+kv_status kv_paged_decode(const kv_geometry* geom, const void* layer_base, int32_t n_res, const int32_t* req_ptr,
+                          const int32_t* block_ids, const int32_t* per_req_meta, const int32_t* seq_lens,
+                          int32_t q_heads_local, const void* q, float* out, float scale, void* stream);
+
 /* ------------------------------------------------------- multi-process */
 
 /* CUDA IPC helpers for peer pools (one process per GPU).  kv_ipc_export

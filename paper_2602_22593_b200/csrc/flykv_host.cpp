@@ -804,6 +804,37 @@ extern "C" kv_status kv_gather_view(const kv_view* v, void* dst, void* stream) {
     return KV_OK;
 }
 
+// ------------------------------------------------------------ consumer proof
+extern "C" kv_status kv_paged_decode(const kv_geometry* geom, const void* layer_base, int32_t n_res,
+                                     const int32_t* req_ptr, const int32_t* block_ids, const int32_t* per_req_meta,
+                                     const int32_t* seq_lens, int32_t q_heads_local, const void* q, float* out,
+                                     float scale, void* stream) {
+    kv_status s = check_geometry(geom);
+    if (s) return s;
+    if (geom->elem_bytes != 2 || (geom->head_dim != 64 && geom->head_dim != 128 && geom->head_dim != 256))
+        return fail(KV_ERR_INVALID_ARG, "kv_paged_decode needs bf16 and head_dim 64/128/256");
+    if (n_res < 0 || q_heads_local < 1 || (n_res > 0 && (!layer_base || !req_ptr || !block_ids || !per_req_meta ||
+                                                         !seq_lens || !q || !out)))
+        return fail(KV_ERR_INVALID_ARG, "bad kv_paged_decode arguments");
+    DecodeArgs a{};
+    a.layer = static_cast<const char*>(layer_base);
+    a.M = 2 * (int64_t)geom->num_kv_heads * geom->block_base * geom->head_dim * geom->elem_bytes;
+    a.d = geom->head_dim;
+    a.n_res = n_res;
+    a.q_local = q_heads_local;
+    a.req_ptr = req_ptr;
+    a.block_ids = block_ids;
+    a.meta = per_req_meta;
+    a.seq_lens = seq_lens;
+    a.q = static_cast<const __nv_bfloat16*>(q);
+    a.out = out;
+    a.scale = scale;
+    cudaError_t e = launch_decode(a, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "flykv_paged_decode_kernel launch");
+    if (n_res > 0) g_launches.fetch_add(1);
+    return KV_OK;
+}
+
 // ------------------------------------------------------------ IPC (peer pools)
 typedef int (*cuMemGetAddressRange_t)(unsigned long long*, size_t*, unsigned long long);
 

@@ -2,6 +2,7 @@
 // and the sm_100a kernels (flykv_kernels.cu).  Not part of the ABI.
 #pragma once
 #include <stdint.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #define FLYKV_HD __host__ __device__ __forceinline__
@@ -92,10 +93,25 @@ struct GatherSeg {
     int64_t out_off;  // byte offset of the segment in the output
 };
 
-// Kernel launchers (flykv_kernels.cu).  Return cudaSuccess or the launch error.
+struct DecodeArgs {
+    const char* layer;          // layer region of one pool
+    int64_t M;                  // block bytes per layer
+    int32_t d;                  // head_dim (bf16)
+    int32_t n_res, q_local;     // resident requests, local query heads
+    const int32_t* req_ptr;     // CSR from kv_remap_block_tables
+    const int32_t* block_ids;
+    const int32_t* meta;        // {plan index, B(p), H_loc, first head}
+    const int32_t* seq_lens;    // tokens per resident request
+    const __nv_bfloat16* q;     // [n_res][q_local][d]
+    float* out;                 // [n_res][q_local][d]
+    float scale;
+};
+
+// Kernel launchers (flykv_kernels.cu, flykv_decode.cu).  Return cudaSuccess or the launch error.
 cudaError_t launch_reshard(const ReshardArgs& a, int device, cudaStream_t s);
 void set_reshard_impl(int impl, int ctas_per_sm);
 cudaError_t launch_remap(const RemapArgs& a, cudaStream_t s);
 cudaError_t launch_gather(const GatherSeg* segs, int n_seg, char* dst, cudaStream_t s);
+cudaError_t launch_decode(const DecodeArgs& a, cudaStream_t s);
 
 }  // namespace flykv

@@ -125,6 +125,8 @@ _sig("kv_plan_get_stats", C.c_int, _P, C.POINTER(PlanStats), _I64P)
 _sig("kv_plan_destroy", None, _P)
 _sig("weight_shard_view", C.c_int, C.POINTER(WeightDesc), C.c_int32, C.c_int32, C.POINTER(View))
 _sig("kv_gather_view", C.c_int, C.POINTER(View), _P, _P)
+_sig("kv_paged_decode", C.c_int, C.POINTER(Geometry), _P, C.c_int32, _P, _P, _P, _P, C.c_int32, _P, _P, C.c_float,
+     _P)
 _sig("kv_ipc_export", C.c_int, _P, C.POINTER(C.c_uint8), C.POINTER(C.c_uint64))
 _sig("kv_ipc_import", C.c_int, C.POINTER(C.c_uint8), C.c_uint64, C.POINTER(_P))
 _sig("kv_ipc_close", C.c_int, _P, C.c_uint64)
@@ -137,7 +139,7 @@ _sig("kv_set_reshard_impl", C.c_int, C.c_int32, C.c_int32)
 EXPORTED = ["kv_cache_create", "kv_cache_destroy", "kv_layout", "kv_blocks_for", "kv_alloc", "kv_reserve",
             "kv_free", "kv_free_count", "kv_held_mask", "kv_plan_switch", "kv_plan_upload", "kv_reshard", "kv_plan_resident",
             "kv_remap_block_tables", "kv_plan_dst_tables", "kv_plan_commit", "kv_plan_waves", "kv_plan_get_stats", "kv_plan_destroy",
-            "weight_shard_view", "kv_gather_view", "kv_ipc_export", "kv_ipc_import", "kv_ipc_close",
+            "weight_shard_view", "kv_gather_view", "kv_paged_decode", "kv_ipc_export", "kv_ipc_import", "kv_ipc_close",
             "kv_stream_sync", "kv_strerror", "kv_last_error", "kv_launch_count", "kv_set_reshard_impl"]
 
 
@@ -358,6 +360,14 @@ def weight_desc(ptr, rows, cols, elem_bytes, kind, ld=None, num_q_heads=0, num_k
 
 def kv_gather_view(view: View, dst, stream=None):
     _check(_lib.kv_gather_view(C.byref(view), ptr_of(dst), stream_of(stream)))
+
+
+# ----------------------------------------------------------------- consumer proof
+def kv_paged_decode(geom: Geometry, layer_base, n_res: int, req_ptr, block_ids, per_req_meta, seq_lens,
+                    q_heads_local: int, q, out, scale: float, stream=None):
+    _check(_lib.kv_paged_decode(C.byref(geom), ptr_of(layer_base), n_res, ptr_of(req_ptr), ptr_of(block_ids),
+                                ptr_of(per_req_meta), ptr_of(seq_lens), q_heads_local, ptr_of(q), ptr_of(out),
+                                float(scale), stream_of(stream)))
 
 
 # ----------------------------------------------------------------- IPC

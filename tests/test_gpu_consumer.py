@@ -1,0 +1,114 @@
+"""Consumer proof: the re-laid-out cache is usable.
+
+Paged decode attention (kv_paged_decode, sm_100a) reads each pool through the
+CSR tables and per-request (B(p), H_loc, first head) that
+kv_remap_block_tables produces -- the "stride and capacity" the paper's
+Adaptor passes to the attention kernel.  On synthetic Q and finite
+bf16 KV:
+  * the DP replica's output matches an fp64 numpy attention (the oracle's
+    locate() gives each token's bytes) within fp32 tolerance;
+  * after DP -> TP (incl. GQA replication, TP > kv_heads), every TP rank's
+    output for its query heads (the Eq.1 column slice of Q) is bit-identical
+    to the DP output for the same heads.
+"""
+import numpy as np
+import pytest
+
+import synth
+from oracle import oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def _decode_all(F, eng, geo, plan, tables, q_full, gpus, q_slices, seq):
+    """Run decode on each GPU's table; returns {(plan_index, global_q_head): out row}."""
+    L, H, d, B, e = geo
+    M = F.kv_layout(eng.geom, 1)[2]
+    res = {}
+    for g in gpus:
+        n_res, n_ids = plan.resident(g)
+        if n_res == 0:
+            continue
+        t = tables[g]
+        meta = t.meta[:n_res].cpu().numpy()
+        qlo, qhi = q_slices(g, meta)
+        idx = torch.as_tensor(meta[:, 0].astype(np.int64), device="cuda:0")
+        q = q_full[idx, qlo:qhi].contiguous()
+        lens = torch.as_tensor([seq[i] for i in meta[:, 0]], dtype=torch.int32, device="cuda:0")
+        out = torch.empty((n_res, qhi - qlo, d), dtype=torch.float32, device="cuda:0")
+        layer = eng.pools.tensors[g][1]  # layer 1 of pool g
+        F.kv_paged_decode(eng.geom, layer.data_ptr(), n_res, t.req_ptr, t.block_ids, t.meta, lens, qhi - qlo, q, out,
+                          1.0 / np.sqrt(d), eng.stream)
+        torch.cuda.synchronize()
+        o = out.cpu().numpy()
+        for k, i in enumerate(meta[:, 0]):
+            for jj in range(qhi - qlo):
+                res[(int(i), qlo + jj)] = o[k, jj]
+    return res
+
+
+@pytest.mark.parametrize("H,Hq,p1", [(8, 32, 2), (8, 32, 4), (8, 64, 8), (4, 32, 8), (2, 16, 8), (8, 8, 2)])
+def test_tp_after_relayout_equals_dp(H, Hq, p1):
+    F = pytest.importorskip("paper_2602_22593_b200.flykv")
+    from paper_2602_22593_b200.engine import KVSwitchEngine
+    geo = (2, H, 128, 16, 2)
+    og = O.Geom(*geo)
+    n_gpus = 8
+    rng = np.random.default_rng(H * 100 + Hq + p1)
+    seq = [int(x) for x in rng.integers(1, 300, size=10)]
+    src = [((i % n_gpus), 1) for i in range(len(seq))]
+    dst = [((i * p1) % n_gpus // p1 * p1, p1) for i in range(len(seq))]
+    w = synth.Workload("c", *geo, n_gpus, seq, src, dst)
+    nb = synth.pool_blocks(w, slack=1.3)
+    eng = KVSwitchEngine(F.geometry(*geo), nb, "cuda:0")
+    gen = torch.Generator(device="cuda:0").manual_seed(int(H + Hq + p1))
+    for t in eng.pools.tensors:  # finite bf16 contents
+        t.view(torch.bfloat16).copy_(torch.randn(t.numel() // 2, generator=gen, device="cuda:0").view(t.shape[0], t.shape[1], -1))
+    counts = [O.num_blocks(og, T, s[1]) for T, s in zip(seq, src)]
+    tabs0 = synth.source_tables(w, counts, nb)
+    for s_, ids in zip(src, tabs0):
+        eng.cache.reserve(s_, ids)
+    q_full = torch.randn((len(seq), Hq, 128), generator=gen, device="cuda:0").to(torch.bfloat16)
+    # DP tables via a no-op plan (src == dst keeps the table, remap lists it)
+    noop = [(i, T, s_, ids, s_) for i, (T, s_, ids) in enumerate(zip(seq, src, tabs0))]
+    plan_dp, tables_dp, _ = eng.switch(noop, read_back=True)
+    out_dp = _decode_all(F, eng, geo, plan_dp, tables_dp, q_full, range(n_gpus), lambda g, meta: (0, Hq), seq)
+    # fp64 oracle on the DP layout (layer 1)
+    host = [t.view(torch.int16).cpu().numpy().reshape(-1).view(np.uint16) for t in eng.pools.tensors]
+    M = O.block_bytes(og)
+
+    def bf16_to_f64(u16):
+        return (u16.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+
+    qf = q_full.float().cpu().numpy().astype(np.float64)
+    G = Hq // H
+    for i in (0, 3, 7):
+        T = seq[i]
+        for qh in (0, Hq - 1):
+            h = qh // G
+            K = np.zeros((T, 128))
+            V = np.zeros((T, 128))
+            for t_ in range(T):
+                gpu, off = O.locate(og, src[i][0], 1, tabs0[i], 0, h, t_)
+                base = (1 * nb[gpu] * M + off) // 2
+                K[t_] = bf16_to_f64(host[gpu][base:base + 128])
+                gpu, off = O.locate(og, src[i][0], 1, tabs0[i], 1, h, t_)
+                base = (1 * nb[gpu] * M + off) // 2
+                V[t_] = bf16_to_f64(host[gpu][base:base + 128])
+            s_ = K @ qf[i, qh] / np.sqrt(128)
+            p_ = np.exp(s_ - s_.max())
+            ref = (p_ / p_.sum()) @ V
+            assert np.allclose(out_dp[(i, qh)], ref, rtol=2e-3, atol=2e-3)
+    # switch DP -> TP_p1 and decode on every rank with its Eq.1 Q slice
+    move = [(i, T, s_, ids, d_) for i, (T, s_, ids, d_) in enumerate(zip(seq, src, tabs0, dst))]
+    plan_tp, tables_tp, _ = eng.switch(move, read_back=True)
+    ql = Hq // p1
+
+    def q_slice(g, meta):
+        r = g % p1  # rank inside its aligned group
+        return r * ql, (r + 1) * ql
+    out_tp = _decode_all(F, eng, geo, plan_tp, tables_tp, q_full, range(n_gpus), q_slice, seq)
+    assert set(out_tp) == set(out_dp)
+    for k, v in out_dp.items():
+        assert np.array_equal(out_tp[k], v), k
