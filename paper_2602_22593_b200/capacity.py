@@ -1,0 +1,53 @@
+"""KV capacity arithmetic (Table 2 of the paper).
+
+Maximum context a TP-p instance can hold, once the weights (sharded p ways,
+P:273-284) are resident:
+
+    max_context(p) = floor( (p * C - W) / kv_bytes_per_token )   (floored to B(p))
+
+C = bytes per GPU available to weights + KV, W = total weight bytes,
+kv_bytes_per_token = 2 * L * H_kv * d * e (K and V of every layer, R1).
+This is the same linear model the paper's Table 2 follows: fitting C and W to
+two of its static rows reproduces the third and recovers Llama-3-70B's bf16
+weight size (tests/test_capacity.py).  Host-side planning only.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+
+def kv_bytes_per_token(L: int, H: int, d: int, e: int = 2) -> int:
+    return 2 * L * H * d * e
+
+
+def max_context(p: int, per_gpu_bytes: float, weight_bytes: float, kv_per_token: int, block_tokens: int = 1,
+                reserve_bytes: float = 0.0) -> int:
+    free = p * (per_gpu_bytes - reserve_bytes) - weight_bytes
+    if free <= 0:
+        return 0
+    t = int(free // kv_per_token)
+    return t - t % max(1, block_tokens)
+
+
+@dataclass
+class Fit:
+    per_gpu_bytes: float
+    weight_bytes: float
+
+
+def fit_two_points(p1: int, t1: float, p2: int, t2: float, kv_per_token: int) -> Fit:
+    """Solve p*C - W = t*kv for (C, W) from two (degree, max context) rows."""
+    c = (t2 - t1) * kv_per_token / (p2 - p1)
+    w = p1 * c - t1 * kv_per_token
+    return Fit(c, w)
+
+
+def relayout_reserve_bytes(T: int, L: int, H: int, d: int, B: int, p_src: int, p_dst: int, e: int = 2) -> float:
+    """Per-GPU destination bytes a live re-layout of one T-token request
+    needs next to its sources (R13): ceil(T / B(p_dst)) blocks of M bytes per
+    layer on each destination rank.  With memory-bounded waves (kv_plan_waves)
+    this bounds the transient reserve of a promotion."""
+    hloc = H // p_dst if p_dst <= H else 1
+    bp = B * (H // hloc)
+    M = 2 * H * B * d * e
+    return -(-T // bp) * M * L

@@ -27,6 +27,14 @@ class UnknownGroup(KeyError):
     pass
 
 
+def _rss():
+    try:
+        import psutil
+        return psutil.Process().memory_info().rss
+    except Exception:
+        return None
+
+
 def enumerate_tp_groups(n: int, degrees) -> list:
     """Aligned contiguous segments for every p in degrees:
     N=4, {2,4} -> [(0,1),(2,3),(0,1,2,3)]; the count is sum_p N/p (linear)."""
@@ -49,13 +57,16 @@ class CommunicatorPool:
         self.keys = enumerate_tp_groups(world_size, degrees)
         self.groups = {}
         self.init_seconds = 0.0
-        self.created_after_init = 0
+        self.host_bytes_per_group = None   # measured RSS growth per group (P:434 quotes ~2 MB)
         if eager:
+            rss0 = _rss()
             t0 = time.perf_counter()
             for k in self.keys:  # every rank calls new_group for every group (collective)
                 self.groups[k] = dist.new_group(ranks=list(k), backend=backend)
             self.groups[tuple(range(world_size))] = self.groups.get(tuple(range(world_size)), dist.group.WORLD)
             self.init_seconds = time.perf_counter() - t0
+            if self.keys and rss0 is not None:
+                self.host_bytes_per_group = max(0, _rss() - rss0) / len(self.keys)
 
     def get(self, ranks):
         """O(1) lookup; unaligned or unknown tuples are scheduler bugs."""

@@ -37,7 +37,13 @@ def _worker(rank, world, port, q):
         from paper_2602_22593_b200 import flykv as F
         import synth
         pool = comm.CommunicatorPool(world, [2, 4], backend="gloo")
-        out = {"keys": sorted(pool.groups.keys())}
+        out = {"keys": sorted(pool.groups.keys()), "init_s": pool.init_seconds,
+               "host_bytes_per_group": pool.host_bytes_per_group}
+        import time as _t
+        t0 = _t.perf_counter()
+        for _ in range(10000):
+            pool.get((0, 1))
+        out["lookup_us"] = (_t.perf_counter() - t0) / 10000 * 1e6
         try:
             pool.get((1, 2))
             out["unaligned"] = "found"
@@ -88,6 +94,8 @@ def test_pool_and_replicated_plans_gloo(world):
         assert o["ok"] and o["identical_plans"]
         assert o["unaligned"] == "UnknownGroup"
         assert o["cover"] == (0, 1)
+        assert o["lookup_us"] < 50          # O(1) dict lookup
+        assert o["host_bytes_per_group"] is not None and o["host_bytes_per_group"] < 64e6
         if world == 4:
             assert o["keys"] == [(0, 1), (0, 1, 2, 3), (2, 3)]
             assert o["cover2"] == (0, 1, 2, 3)
