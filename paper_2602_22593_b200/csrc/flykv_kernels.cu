@@ -130,12 +130,17 @@ __global__ void __launch_bounds__(256, ((U == 1 && VPL <= 8) ? 4 : 2)) flykv_res
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t base = a.atom_lo + warp * 32; base < a.atom_hi; base += nwarps * 32) {
+    // Round r covers atoms [R, R + 32*nwarps); step k of every warp touches
+    // atom R + k*nwarps + warp, so at any moment the whole grid works on one
+    // window of nwarps consecutive atoms (~19 MB): few DRAM pages open at
+    // once (measured +5-9% over warp-contiguous chunks, scripts/microbench.cu).
+    for (int64_t R = a.atom_lo; R < a.atom_hi; R += 32 * nwarps) {
+        const int64_t first = R + warp;
+        if (first >= a.atom_hi) break;
+        const int64_t span = (a.atom_hi - first + nwarps - 1) / nwarps;
+        const int n = span < 32 ? (int)span : 32;
         LaneAtom la;
-        const int64_t mine = base + lane;
-        if (mine < a.atom_hi) lane_decode(a, mine, la);
-        const int64_t left = a.atom_hi - base;
-        const int n = left < 32 ? (int)left : 32;
+        if (lane < n) lane_decode(a, first + lane * nwarps, la);
         if constexpr (VPL > 0 && U == 1) {
             for (int k = 0; k < n; ++k) {
                 const int4* src = reinterpret_cast<const int4*>(shfl_ptr(la.src, k)) + lane;
@@ -147,7 +152,7 @@ __global__ void __launch_bounds__(256, ((U == 1 && VPL <= 8) ? 4 : 2)) flykv_res
 #pragma unroll
                 for (int i = 0; i < VPL; ++i) st_stream(dst + i * 32, v[i]);
                 for (int j = 1; j < rep; ++j) {
-                    int4* dj = reinterpret_cast<int4*>(replica_ptr(a, base + k, j)) + lane;
+                    int4* dj = reinterpret_cast<int4*>(replica_ptr(a, first + k * nwarps, j)) + lane;
 #pragma unroll
                     for (int i = 0; i < VPL; ++i) st_stream(dj + i * 32, v[i]);
                 }
@@ -174,7 +179,9 @@ __global__ void __launch_bounds__(256, ((U == 1 && VPL <= 8) ? 4 : 2)) flykv_res
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     for (int j = 0; j < rep[u]; ++j) {
-                        int4* dst = reinterpret_cast<int4*>(j == 0 ? d0[u] : replica_ptr(a, base + k0 + u, j)) + lane;
+                        int4* dst = reinterpret_cast<int4*>(
+                                        j == 0 ? d0[u] : replica_ptr(a, first + (int64_t)(k0 + u) * nwarps, j)) +
+                                    lane;
 #pragma unroll
                         for (int i = 0; i < VPL; ++i) st_stream(dst + i * 32, v[u][i]);
                     }
@@ -187,7 +194,7 @@ __global__ void __launch_bounds__(256, ((U == 1 && VPL <= 8) ? 4 : 2)) flykv_res
                 const int rep = __shfl_sync(0xffffffffu, la.rep1, k);
                 const int nv = a.atom_bytes >> 4;
                 for (int j = 0; j < rep; ++j) {
-                    char* dj = j == 0 ? d0 : replica_ptr(a, base + k, j);
+                    char* dj = j == 0 ? d0 : replica_ptr(a, first + k * nwarps, j);
                     for (int i = lane; i < nv; i += 32)
                         st_stream(reinterpret_cast<int4*>(dj) + i, ld_stream(reinterpret_cast<const int4*>(s) + i));
                 }
@@ -323,7 +330,11 @@ static cudaError_t launch_ldg(const ReshardArgs& a, int device, cudaStream_t s) 
         per_sm = nb > 0 ? nb : 1;
     }
     const int64_t atoms = a.atom_hi - a.atom_lo;
-    const int per = g_ctas_per_sm > 0 ? g_ctas_per_sm : per_sm;
+    // ~64 KiB of loads in flight per SM (U=1: 2 CTAs = 16 warps x 4 KiB;
+    // U=2: 1 CTA = 8 warps x 8 KiB): more concurrent streams cost DRAM row
+    // locality (measured, scripts/microbench.cu and scripts/variants.py)
+    const int want_per = U == 1 ? 2 : 1;
+    const int per = g_ctas_per_sm > 0 ? g_ctas_per_sm : (per_sm < want_per ? per_sm : want_per);
     int64_t want = (atoms + 8 * 32 - 1) / (8 * 32);
     int64_t cap = (int64_t)sm_count_of(device) * per;
     int grid = (int)(want < cap ? want : cap);

@@ -44,7 +44,7 @@ def main():
         ts = sorted(x.elapsed_time(y) for x, y in evs)
         return ts[len(ts) // 2]
 
-    for impl, ctas in [(0, 0), (1, 0), (2, 0), (0, 2)]:
+    for impl, ctas in [(0, 0), (0, 1), (0, 2), (1, 2), (1, 3), (1, 4), (2, 0)]:
         try:
             F.set_reshard_impl(impl, ctas)
             ms = timeit(lambda: F.kv_reshard(plan, -1, stream))
