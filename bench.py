@@ -57,6 +57,7 @@ def parse():
     ap.add_argument("--cpu-baseline-steps", type=int, default=6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--clock-ms", type=int, default=200, help="nvidia-smi sampling period in the timed region (0: off)")
     ap.add_argument("--profile-steps", type=int, default=0, help="(ncu) run N steps only, no JSON")
     ap.add_argument("--no-fill", action="store_true", help="skip the content hash fill (profiling runs)")
     ap.add_argument("--requests", type=int, default=0, help="use only the first N requests (profiling)")
@@ -80,22 +81,25 @@ def peaks():
 
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled DURING the timed region:
-    a background `nvidia-smi --query-gpu=... -lms 50` started before the
+    a background `nvidia-smi --query-gpu=... -lms 200` started before the
     region and stopped after it (B200_PROFILING.md clocks line)."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, period_ms: int = 50):
         self.index = index
+        self.period_ms = period_ms
         self.rows = []
         self._p = None
 
     def __enter__(self):
+        if self.period_ms <= 0:
+            return self
         try:
             self._p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                        "--format=csv,noheader,nounits", "-lms", "50"],
+                                        "--format=csv,noheader,nounits", "-lms", str(self.period_ms)],
                                        stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             time.sleep(0.15)  # first sample lands before the region starts
         except Exception:
@@ -285,7 +289,7 @@ def run_single(args):
             flush = torch.empty(512 * 2 ** 20, dtype=torch.uint8, device=dev)
         n_launch0 = F.launch_count()
         step_ev = []
-        with ClockSampler(torch.cuda.current_device()) as clk:
+        with ClockSampler(torch.cuda.current_device(), args.clock_ms) as clk:
             torch.cuda.synchronize()
             plans = []
             for _ in range(args.steps):
@@ -466,7 +470,7 @@ def run_multi(args):
     n_launch0 = F.launch_count()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     keep = []
-    with ClockSampler(dev.index) as clk:
+    with ClockSampler(dev.index, args.clock_ms) as clk:
         start.record(stream)
         for _ in range(args.steps):
             keep.append(step(timed=True))
