@@ -283,6 +283,24 @@ typedef struct {
  */
 kv_status weight_shard_view(const kv_weight_desc* full, int32_t rank, int32_t degree, kv_view* out);
 
+/* Contiguous zero-copy views ("contiguous in virtual memory but map
+ * to the existing physical memory of the DP replica").  kv_vmm_alloc gives a
+ * weight buffer backed by a CUDA VMM physical allocation (cuMemCreate,
+ * size rounded up to the granularity, *dptr its device address);
+ * weight_view_alias maps the view's row segments (COLUMN / QKV views, ld ==
+ * cols) back to back into a fresh virtual range aliasing the same physical
+ * memory: one contiguous [sum rows, cols] operand, 0 bytes copied.  Each
+ * segment's offset and size must be multiples of kv_vmm_granularity
+ * (INDIVISIBLE_EXTENT otherwise, e.g. Llama-3-70B QKV at TP2/4/8 fits);
+ * strided ROW views are INVALID_ARG.  Writes through either address are
+ * visible through the other.  weight_view_unalias releases the range. */
+typedef struct kv_vmm_buffer kv_vmm_buffer;
+kv_status kv_vmm_granularity(int32_t device, uint64_t* granularity);
+kv_status kv_vmm_alloc(int32_t device, uint64_t bytes, kv_vmm_buffer** out, void** dptr);
+kv_status kv_vmm_free(kv_vmm_buffer* buf);
+kv_status weight_view_alias(const kv_vmm_buffer* buf, const kv_view* view, void** contiguous, uint64_t* bytes);
+kv_status weight_view_unalias(void* contiguous, uint64_t bytes);
+
 /* Test utility (DESIGN.md a8): gather a view's segments, in order, into the
  * contiguous device buffer dst (row-major, total rows x cols of the
  * segments) on `stream`.  Used only to check views against the oracle. */

@@ -33,6 +33,17 @@ static kv_status fail(kv_status s, const char* fmt, ...) {
     return s;
 }
 
+// shared with flykv_vmm.cpp
+kv_status flykv_fail(kv_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
 static kv_status cuda_fail(cudaError_t e, const char* what) {
     return fail(KV_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
 }

@@ -125,6 +125,11 @@ _sig("kv_plan_get_stats", C.c_int, _P, C.POINTER(PlanStats), _I64P)
 _sig("kv_plan_destroy", None, _P)
 _sig("weight_shard_view", C.c_int, C.POINTER(WeightDesc), C.c_int32, C.c_int32, C.POINTER(View))
 _sig("kv_gather_view", C.c_int, C.POINTER(View), _P, _P)
+_sig("kv_vmm_granularity", C.c_int, C.c_int32, C.POINTER(C.c_uint64))
+_sig("kv_vmm_alloc", C.c_int, C.c_int32, C.c_uint64, C.POINTER(_P), C.POINTER(_P))
+_sig("kv_vmm_free", C.c_int, _P)
+_sig("weight_view_alias", C.c_int, _P, C.POINTER(View), C.POINTER(_P), C.POINTER(C.c_uint64))
+_sig("weight_view_unalias", C.c_int, _P, C.c_uint64)
 _sig("kv_paged_decode", C.c_int, C.POINTER(Geometry), _P, C.c_int32, _P, _P, _P, _P, C.c_int32, _P, _P, C.c_float,
      _P)
 _sig("kv_ipc_export", C.c_int, _P, C.POINTER(C.c_uint8), C.POINTER(C.c_uint64))
@@ -139,7 +144,8 @@ _sig("kv_set_reshard_impl", C.c_int, C.c_int32, C.c_int32)
 EXPORTED = ["kv_cache_create", "kv_cache_destroy", "kv_layout", "kv_blocks_for", "kv_alloc", "kv_reserve",
             "kv_free", "kv_free_count", "kv_held_mask", "kv_plan_switch", "kv_plan_upload", "kv_reshard", "kv_plan_resident",
             "kv_remap_block_tables", "kv_plan_dst_tables", "kv_plan_commit", "kv_plan_waves", "kv_plan_get_stats", "kv_plan_destroy",
-            "weight_shard_view", "kv_gather_view", "kv_paged_decode", "kv_ipc_export", "kv_ipc_import", "kv_ipc_close",
+            "weight_shard_view", "kv_gather_view", "kv_vmm_granularity", "kv_vmm_alloc", "kv_vmm_free",
+            "weight_view_alias", "weight_view_unalias", "kv_paged_decode", "kv_ipc_export", "kv_ipc_import", "kv_ipc_close",
             "kv_stream_sync", "kv_strerror", "kv_last_error", "kv_launch_count", "kv_set_reshard_impl"]
 
 
@@ -360,6 +366,45 @@ def weight_desc(ptr, rows, cols, elem_bytes, kind, ld=None, num_q_heads=0, num_k
 
 def kv_gather_view(view: View, dst, stream=None):
     _check(_lib.kv_gather_view(C.byref(view), ptr_of(dst), stream_of(stream)))
+
+
+class VmmBuffer:
+    """A weight buffer in CUDA VMM memory (kv_vmm_alloc): aliasable views."""
+
+    def __init__(self, nbytes: int, device: int = 0):
+        h, p = C.c_void_p(), C.c_void_p()
+        _check(_lib.kv_vmm_alloc(device, nbytes, C.byref(h), C.byref(p)))
+        self._h = h
+        self.ptr = int(p.value)
+        self.nbytes = nbytes
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.kv_vmm_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def vmm_granularity(device: int = 0) -> int:
+    g = C.c_uint64()
+    _check(_lib.kv_vmm_granularity(device, C.byref(g)))
+    return g.value
+
+
+def weight_view_alias(buf: VmmBuffer, view: View):
+    """(contiguous device pointer, bytes) aliasing the view's segments."""
+    p, n = C.c_void_p(), C.c_uint64()
+    _check(_lib.weight_view_alias(buf._h, C.byref(view), C.byref(p), C.byref(n)))
+    return int(p.value), n.value
+
+
+def weight_view_unalias(ptr: int, nbytes: int):
+    _check(_lib.weight_view_unalias(ptr, nbytes))
 
 
 # ----------------------------------------------------------------- consumer proof

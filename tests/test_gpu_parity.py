@@ -345,3 +345,55 @@ def test_random_mixed_plans(seed):
         T = int(rng.choice([0, 1, int(rng.integers(2, 40)), int(rng.integers(40, 900))]))
         spec.append((T, (g0, p0), (g1, p1)))
     run_parity(geo, [480] * n_gpus, spec, seed=seed)
+
+
+def test_weight_view_contiguous_alias():
+    """the TP-rank view of the fused W^QKV is contiguous in virtual
+    memory but maps the DP replica's physical memory (CUDA VMM alias, 0 bytes
+    copied).  Llama-3-70B-shaped QKV (64 q heads, 8 kv heads, d=128,
+    hidden 8192, bf16) at TP2/4/8: the alias reads back exactly the oracle's
+    Eq.1 slices, and a write through the DP address is visible through it."""
+    F = _F()
+    from oracle import weights as W
+    Hq, Hkv, d, hidden = 64, 8, 128, 8192
+    rows = (Hq + 2 * Hkv) * d
+    g = F.vmm_granularity(0)
+    assert g <= 2 * 2 ** 20
+    full = torch.randn(rows, hidden, device="cuda:0").to(torch.bfloat16)
+    host = full.view(torch.int16).cpu().numpy()
+    buf = F.VmmBuffer(rows * hidden * 2)
+    F.kv_gather_view(F.weight_shard_view(F.weight_desc(full, rows, hidden, 2, F.KV_W_COLUMN), 0, 1), buf.ptr)
+    torch.cuda.synchronize()
+    for m in (2, 4, 8):
+        for r in (0, m - 1):
+            v = F.weight_shard_view(F.weight_desc(buf.ptr, rows, hidden, 2, F.KV_W_QKV, num_q_heads=Hq,
+                                                  num_kv_heads=Hkv, head_dim=d), r, m)
+            ptr, nbytes = F.weight_view_alias(buf, v)
+            nrow = nbytes // (2 * hidden)
+            out = torch.empty(nrow, hidden, dtype=torch.bfloat16, device="cuda:0")
+            F.kv_gather_view(F.weight_shard_view(F.weight_desc(ptr, nrow, hidden, 2, F.KV_W_COLUMN), 0, 1), out)
+            torch.cuda.synchronize()
+            ref = np.concatenate(W.view_qkv(host, r, m, Hq, Hkv, d))
+            assert np.array_equal(out.view(torch.int16).cpu().numpy(), ref)
+            if m == 8 and r == m - 1:
+                # write-through: overwrite the DP replica's K rows of this rank's head
+                new = torch.full((d, hidden), 3.0, dtype=torch.bfloat16, device="cuda:0")
+                kseg = v.seg[1]
+                F.kv_gather_view(F.weight_shard_view(F.weight_desc(new, d, hidden, 2, F.KV_W_COLUMN), 0, 1), kseg.ptr)
+                F.kv_gather_view(F.weight_shard_view(F.weight_desc(ptr, nrow, hidden, 2, F.KV_W_COLUMN), 0, 1), out)
+                torch.cuda.synchronize()
+                q_rows = v.seg[0].rows
+                assert torch.equal(out[q_rows:q_rows + d], new)
+            F.weight_view_unalias(ptr, nbytes)
+    # a view whose K/V segments are not granularity-aligned cannot be aliased
+    small = F.VmmBuffer((8 + 2 * 2) * 64 * 256 * 2)
+    v = F.weight_shard_view(F.weight_desc(small.ptr, (8 + 4) * 64, 256, 2, F.KV_W_QKV, num_q_heads=8, num_kv_heads=2,
+                                          head_dim=64), 0, 2)
+    with pytest.raises(F.FlyKVError) as e:
+        F.weight_view_alias(small, v)
+    assert e.value.name == "KV_ERR_INDIVISIBLE_EXTENT"
+    row = F.weight_shard_view(F.weight_desc(buf.ptr, rows, hidden, 2, F.KV_W_ROW), 0, 2)
+    with pytest.raises(F.FlyKVError):
+        F.weight_view_alias(buf, row)
+    small.close()
+    buf.close()
