@@ -241,3 +241,38 @@ int32_t or_tables(const or_geom* g, int32_t gpu, int32_t n_reqs,
     }
     return n;
 }
+
+/*
+ * or_atom_map: every (layer, kv, head, chunk, replica) atom of one request
+ * as (source GPU, source byte offset in that GPU's pool, destination GPU,
+ * destination byte offset), offsets including the layer region
+ * (l * num_blocks * M).  Enumerates exactly the copies or_switch performs,
+ * one B-token atom per entry (R9), in the order l, kv, h, c, j.  Used for
+ * full-size checks of the device result.  Returns the number of entries.
+ */
+int64_t or_atom_map(const or_geom* g, const int32_t* num_blocks, int32_t T,
+                    int32_t src_g0, int32_t src_p, const int32_t* tab0,
+                    int32_t dst_g0, int32_t dst_p, const int32_t* tab1,
+                    int32_t* src_gpu, int64_t* src_off, int32_t* dst_gpu, int64_t* dst_off) {
+    int64_t M = or_block_bytes(g);
+    int32_t C = (T + g->B - 1) / g->B;
+    int32_t reps = or_replicas(g, dst_p);
+    int64_t n = 0;
+    int32_t l, kv, h, c, j;
+    for (l = 0; l < g->L; l++)
+        for (kv = 0; kv < 2; kv++)
+            for (h = 0; h < g->H; h++)
+                for (c = 0; c < C; c++)
+                    for (j = 0; j < reps; j++) {
+                        int32_t sg, dg;
+                        int64_t so, dof;
+                        or_locate(g, src_g0, src_p, tab0, kv, h, c * g->B, 0, &sg, &so);
+                        or_locate(g, dst_g0, dst_p, tab1, kv, h, c * g->B, j, &dg, &dof);
+                        src_gpu[n] = sg;
+                        src_off[n] = (int64_t)l * num_blocks[sg] * M + so;
+                        dst_gpu[n] = dg;
+                        dst_off[n] = (int64_t)l * num_blocks[dg] * M + dof;
+                        n++;
+                    }
+    return n;
+}

@@ -81,6 +81,10 @@ def lib():
         L.or_switch.restype = C.c_int32
         L.or_tables.argtypes = [G, C.c_int32, C.c_int32, _P32, _P32, _P32, _P32, _P32, _P32, _P32]
         L.or_tables.restype = C.c_int32
+        _P64 = C.POINTER(C.c_int64)
+        L.or_atom_map.argtypes = [G, _P32, C.c_int32, C.c_int32, C.c_int32, _P32, C.c_int32, C.c_int32, _P32,
+                                  _P32, _P64, _P32, _P64]
+        L.or_atom_map.restype = C.c_int64
     return _lib
 
 
@@ -192,3 +196,20 @@ def tables(g: Geom, gpu: int, reqs: list, dst_tabs: list):
     nres = lib().or_tables(C.byref(g.c()), gpu, n, _ptr(dg0), _ptr(dp), _ptr(dptr), _ptr(dids),
                            _ptr(req_ptr), _ptr(ids), _ptr(meta))
     return req_ptr[:nres + 1].copy(), ids[:req_ptr[nres]].copy(), meta[:4 * nres].reshape(nres, 4).copy()
+
+
+def atom_map(g: Geom, num_blocks, T: int, src, tab0, dst, tab1):
+    """All atom copies of one request: arrays (src_gpu, src_off, dst_gpu, dst_off)."""
+    nb = _i32(num_blocks)
+    C_ = -(-T // g.B)
+    n = g.L * 2 * g.H * C_ * replicas(g, dst[1])
+    sg = np.zeros(max(n, 1), dtype=np.int32)
+    dg = np.zeros(max(n, 1), dtype=np.int32)
+    so = np.zeros(max(n, 1), dtype=np.int64)
+    do = np.zeros(max(n, 1), dtype=np.int64)
+    t0, t1 = _i32(tab0 if len(tab0) else [0]), _i32(tab1 if len(tab1) else [0])
+    P64 = C.POINTER(C.c_int64)
+    m = lib().or_atom_map(C.byref(g.c()), _ptr(nb), T, src[0], src[1], _ptr(t0), dst[0], dst[1], _ptr(t1),
+                          _ptr(sg), so.ctypes.data_as(P64), _ptr(dg), do.ctypes.data_as(P64))
+    assert m == n
+    return sg[:n], so[:n], dg[:n], do[:n]

@@ -237,6 +237,23 @@ def fill_hash_np(pool_u8: np.ndarray, gpu: int, seed: int = 2) -> None:
         w[s:e] = hash32_np(gpu, np.arange(s, e, dtype=np.int64), seed)
 
 
+def hash32_torch(gpu, word, seed: int = 2):
+    """Device twin of hash32_np: int32 tensor of the uint32 hash bits.
+    gpu: int or int64 tensor broadcastable to word (int64 tensor)."""
+    import torch
+    lo = word & _M32
+    hi = word >> 32
+    x = (lo * _K1) & _M32
+    x ^= (hi * _K2 + gpu * _K3 + seed * 977) & _M32
+    x ^= x >> 15
+    x = (x * _K4) & _M32
+    x ^= x >> 13
+    x = (x * _K1) & _M32
+    x ^= x >> 16
+    x = torch.where(x >= (1 << 31), x - (1 << 32), x)
+    return x.to(torch.int32)
+
+
 def fill_hash_torch(pool, gpu: int, seed: int = 2, chunk: int = 1 << 26) -> None:
     """Fill a device (or CPU) torch uint8 pool with the same hash, in place.
     torch int64 arithmetic wraps identically; all products stay < 2^63."""
@@ -247,15 +264,5 @@ def fill_hash_torch(pool, gpu: int, seed: int = 2, chunk: int = 1 << 26) -> None
     for s in range(0, n, chunk):
         e = min(n, s + chunk)
         idx = torch.arange(s, e, dtype=torch.int64, device=dev)
-        lo = idx & _M32
-        hi = idx >> 32
-        x = (lo * _K1) & _M32
-        x ^= (hi * _K2 + gpu * _K3 + seed * 977) & _M32
-        x ^= x >> 15
-        x = (x * _K4) & _M32
-        x ^= x >> 13
-        x = (x * _K1) & _M32
-        x ^= x >> 16
-        x = torch.where(x >= (1 << 31), x - (1 << 32), x)
-        w[s:e] = x.to(torch.int32)
-        del idx, lo, hi, x
+        w[s:e] = hash32_torch(gpu, idx, seed)
+        del idx

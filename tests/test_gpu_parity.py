@@ -174,22 +174,24 @@ def test_round_trip_restores_contents():
 
 
 @pytest.mark.slow
-def test_full_size_config2_sampled():
-    """BASELINE configs[1] at full size in the bench's launch configuration
-    (4 virtual ranks on one B200, one reshard launch): destination tables equal
-    the oracle's allocator in full; 4096 sampled atoms (all replicas) equal the
-    content hash of their oracle-located source; sampled free blocks keep their
-    poison."""
+@pytest.mark.parametrize("cfg", ["c2", "c4"])
+def test_full_size_all_atoms(cfg):
+    """BASELINE configs[1] (c2) and configs[3] (c4, Llama-3-70B 8xDP1->TP8) at
+    full size in the bench's launch configuration (virtual ranks on one B200,
+    the bench's pool sizing and placement, one reshard launch): destination tables equal
+    the oracle's allocator in full; EVERY destination atom (4.8M x 4 KiB) equals
+    the content hash of the source position the oracle maps it from; sampled
+    free blocks keep their poison."""
     F = _F()
     from paper_2602_22593_b200.engine import KVSwitchEngine
-    w = synth.llama8b_dp4_tp2x2()
+    w = synth.WORKLOADS[cfg]()
     og = O.Geom(w.L, w.H, w.d, w.B, w.e)
-    nb = synth.pool_blocks(w)
+    n0 = [O.num_blocks(og, T, s[1]) for T, s in zip(w.T, w.src)]
+    n1 = [O.num_blocks(og, T, d[1]) for T, d in zip(w.T, w.dst)]
+    nb, tabs0 = synth.realistic_pools(w, n0, n1)
     eng = KVSwitchEngine(F.geometry(w.L, w.H, w.d, w.B, w.e), nb, "cuda:0")
     for gpu, t in enumerate(eng.pools.tensors):
         synth.fill_hash_torch(t, gpu)
-    counts = [O.num_blocks(og, T, s[1]) for T, s in zip(w.T, w.src)]
-    tabs0 = synth.source_tables(w, counts, nb)
     held = [np.zeros(n, dtype=np.uint8) for n in nb]
     reqs, oreqs = [], []
     for i, (T, s, d, ids) in enumerate(zip(w.T, w.src, w.dst, tabs0)):
@@ -208,23 +210,28 @@ def test_full_size_config2_sampled():
         assert np.array_equal(host[gpu][1].numpy(), ids)
         assert np.array_equal(host[gpu][2].numpy(), meta)
         assert np.array_equal(eng.cache.held_mask(gpu), held[gpu])
-    rng = np.random.default_rng(123)
+    # every destination atom of the full switch (all replicas): its 4 KiB
+    # equal the content hash of the source position the oracle maps it from
     M = O.block_bytes(og)
     atom_words = og.B * og.d * og.e // 4
-    src_words, dst_idx = [], []
-    for _ in range(4096):
-        i = int(rng.integers(len(w.T)))
-        l, kv, h = int(rng.integers(og.L)), int(rng.integers(2)), int(rng.integers(og.H))
-        c = int(rng.integers(-(-w.T[i] // og.B)))
-        sg, so = O.locate(og, w.src[i][0], w.src[i][1], tabs0[i], kv, h, c * og.B)
-        dg, do = O.locate(og, w.dst[i][0], w.dst[i][1], otabs[i], kv, h, c * og.B)
-        s0 = (l * nb[sg] * M + so) // 4
-        d0 = (l * nb[dg] * M + do) // 4
-        src_words.append(synth.hash32_np(sg, np.arange(s0, s0 + atom_words)))
-        dst_idx.append((dg, d0))
-    for (dg, d0), want in zip(dst_idx, src_words):
-        got = eng.pools.tensors[dg].view(torch.int32).view(-1)[d0:d0 + atom_words].cpu().numpy().view(np.uint32)
-        assert np.array_equal(got, want)
+    ar = torch.arange(atom_words, dtype=torch.int64, device="cuda:0")
+    flat = [t.reshape(-1).view(torch.int32) for t in eng.pools.tensors]
+    checked = 0
+    for i in range(len(w.T)):
+        sg, so, dg, do = O.atom_map(og, nb, w.T[i], w.src[i], tabs0[i], w.dst[i], otabs[i])
+        for gd in np.unique(dg):
+            m = dg == gd
+            s_g = torch.as_tensor(sg[m].astype(np.int64), device="cuda:0")
+            s_w = torch.as_tensor(so[m] // 4, device="cuda:0")
+            d_w = torch.as_tensor(do[m] // 4, device="cuda:0")
+            for c0 in range(0, s_w.numel(), 16384):
+                sl = slice(c0, c0 + 16384)
+                want = synth.hash32_torch(s_g[sl, None], s_w[sl, None] + ar[None, :])
+                got = flat[int(gd)][d_w[sl, None] + ar[None, :]]
+                assert torch.equal(got, want), f"request {i}: destination atoms differ"
+                checked += want.shape[0]
+    assert checked * og.B * og.d * og.e == plan.stats()[0]["payload_bytes"]
+    rng = np.random.default_rng(123)
     # poison survives in blocks nobody holds
     for gpu in range(w.n_gpus):
         free = np.nonzero(held[gpu] == 0)[0]

@@ -342,3 +342,22 @@ def test_tables_csr():
     assert list(rp) == [0, len(tabs[0]), len(tabs[0]) + len(tabs[1])]
     rp3, ids3, meta3 = O.tables(g, 3, reqs, tabs)
     assert list(meta3[:, 0]) == [1, 2, 3] and list(meta3[2, 1:]) == [4, 8, 0]
+
+
+def test_atom_map_matches_switch():
+    """or_atom_map enumerates exactly the bytes or_switch moves: applying the
+    map with numpy copies reproduces the oracle's pools."""
+    geo = (2, 4, 8, 4, 2)
+    g, pools, held, reqs = _setup(geo, [64] * 8, [(37, (0, 1), (0, 2)), (9, (2, 2), (0, 8)), (70, (4, 4), (4, 1))],
+                                  seed=12)
+    before = [p.copy() for p in pools]
+    mine = [p.copy() for p in pools]
+    st, tabs = O.switch(g, pools, held, reqs)
+    assert st == 0
+    atom = g.B * g.d * g.e
+    for r, t in zip(reqs, tabs):
+        sg, so, dg, do = O.atom_map(g, [64] * 8, r.T, r.src, r.src_ids, r.dst, t)
+        for a, b, c, d in zip(sg, so, dg, do):
+            mine[c][d:d + atom] = before[a][b:b + atom]
+    for a, b in zip(mine, pools):
+        assert np.array_equal(a, b)
