@@ -80,45 +80,72 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled DURING the timed region:
-    a background `nvidia-smi --query-gpu=... -lms 200` started before the
-    region and stopped after it (B200_PROFILING.md clocks line)."""
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region.
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    A background `nvidia-smi --query-gpu=timestamp,... -lms <period>` is
+    started before the warm-up (its NVML start-up stalls the driver, which
+    must not land in the timed region) and stopped after the region; only the
+    samples stamped inside [begin, end] (plus the nearest one on each side)
+    are summarised (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index: int, period_ms: int = 50):
+    def __init__(self, index: int, period_ms: int = 200):
         self.index = index
         self.period_ms = period_ms
         self.rows = []
         self._p = None
+        self.t0 = self.t1 = None
 
-    def __enter__(self):
+    def start(self):
         if self.period_ms <= 0:
             return self
         try:
             self._p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
                                         "--format=csv,noheader,nounits", "-lms", str(self.period_ms)],
                                        stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            time.sleep(0.15)  # first sample lands before the region starts
         except Exception:
             self._p = None
         return self
 
-    def __exit__(self, *a):
+    def begin(self):
+        self.t0 = time.time()
+
+    def end(self):
+        self.t1 = time.time()
+        if self._p is not None:
+            time.sleep(self.period_ms / 1000.0 + 0.05)  # one sample after the region
+        self.stop()
+
+    def stop(self):
         if self._p is None:
             return
-        time.sleep(0.06)
         self._p.terminate()
         try:
             out, _ = self._p.communicate(timeout=5)
         except Exception:
             self._p.kill()
             out, _ = self._p.communicate()
+        self._p = None
+        rows = []
         for line in out.splitlines():
-            if line.strip():
-                self.rows.append([x.strip() for x in line.split(",")])
+            r = [x.strip() for x in line.split(",")]
+            if len(r) < 10:
+                continue
+            try:
+                import datetime
+                r[0] = datetime.datetime.strptime(r[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+            except Exception:
+                continue
+            rows.append(r)
+        if self.t0 is not None and rows:
+            inside = [r for r in rows if self.t0 <= r[0] <= (self.t1 or r[0])]
+            before = [r for r in rows if r[0] < self.t0][-1:]
+            after = [r for r in rows if self.t1 is not None and r[0] > self.t1][:1]
+            rows = before + inside + after
+        self.rows = rows
 
     def summary(self):
         if not self.rows:
@@ -129,12 +156,12 @@ class ClockSampler:
                 return float(x)
             except ValueError:
                 return None
-        sm = [v for v in (num(r[1]) for r in self.rows if len(r) > 2) if v is not None]
-        mx = [v for v in (num(r[2]) for r in self.rows if len(r) > 2) if v is not None]
+        sm = [v for v in (num(r[2]) for r in self.rows) if v is not None]
+        mx = [v for v in (num(r[3]) for r in self.rows) if v is not None]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = set()
         for r in self.rows:
-            for n, v in zip(names, r[5:9]):
+            for n, v in zip(names, r[6:10]):
                 if v.strip().lower() in ("active", "1", "yes"):
                     reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
@@ -278,6 +305,7 @@ def run_single(args):
                 step()
             torch.cuda.synchronize()
             return 0
+        clk = ClockSampler(torch.cuda.current_device(), args.clock_ms).start()
         for _ in range(args.warmup):
             step()
         torch.cuda.synchronize()
@@ -289,18 +317,19 @@ def run_single(args):
             flush = torch.empty(512 * 2 ** 20, dtype=torch.uint8, device=dev)
         n_launch0 = F.launch_count()
         step_ev = []
-        with ClockSampler(torch.cuda.current_device(), args.clock_ms) as clk:
-            torch.cuda.synchronize()
-            plans = []
-            for _ in range(args.steps):
-                if flush is not None:
-                    flush.fill_(1)
-                a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a_.record(stream)
-                plans.append(step(timed_kernel=True))
-                b_.record(stream)
-                step_ev.append((a_, b_))
-            torch.cuda.synchronize()
+        torch.cuda.synchronize()
+        clk.begin()
+        plans = []
+        for _ in range(args.steps):
+            if flush is not None:
+                flush.fill_(1)
+            a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_.record(stream)
+            plans.append(step(timed_kernel=True))
+            b_.record(stream)
+            step_ev.append((a_, b_))
+        torch.cuda.synchronize()
+        clk.end()
         launches = F.launch_count() - n_launch0
         total_ms = sum(a_.elapsed_time(b_) for a_, b_ in step_ev)
         kern_ms = [a.elapsed_time(b) for a, b in ev_pairs]
@@ -312,11 +341,22 @@ def run_single(args):
         if not args.no_e2e:
             h2d = d2h = 0
             e2e_payload = 0
+            plan_ms = []
             for it in range(args.steps):
                 t0 = time.perf_counter()
-                plan, tables, host = eng.switch(state["reqs"], read_back=True)
+                plan = eng.plan(state["reqs"])          # host: validate, allocate, segment index
+                tp = time.perf_counter()
+                tables = eng.execute(plan)               # descriptor H2D, reshard, remap
+                host = {}
+                for gg, t in tables.items():            # new block tables -> host
+                    n_res, n_ids = plan.resident(gg)
+                    host[gg] = (t.req_ptr.to("cpu", non_blocking=True),
+                                t.block_ids[:n_ids].to("cpu", non_blocking=True),
+                                t.meta[:n_res].to("cpu", non_blocking=True))
+                stream.synchronize()
                 t1 = time.perf_counter()
                 lat_ms.append((t1 - t0) * 1e3)
+                plan_ms.append((tp - t0) * 1e3)
                 st_, _ = plan.stats()
                 h2d += st_["h2d_bytes"]
                 e2e_payload += st_["payload_bytes"]
@@ -325,7 +365,8 @@ def run_single(args):
             e2e = {"value": round(e2e_payload / (sum(lat_ms) / 1e3) / 1e9, 3), "unit": "GB/s",
                    "h2d_bytes_per_step": int(h2d // len(lat_ms)), "d2h_bytes_per_step": int(d2h // len(lat_ms)),
                    "switch_latency_ms_p50": round(statistics.median(lat_ms), 3),
-                   "switch_latency_ms_p99": round(float(np.percentile(lat_ms, 99)), 3)}
+                   "switch_latency_ms_p99": round(float(np.percentile(lat_ms, 99)), 3),
+                   "host_plan_ms_p50": round(statistics.median(plan_ms), 3)}
 
     # per-step statistics: directions alternate, and under GQA replication the
     # two directions move different byte counts (TP>H writes p/H replicas)
@@ -463,6 +504,7 @@ def run_multi(args):
     plan0 = F.kv_plan_switch(cache, state["reqs"])
     stats, mat = plan0.stats()
     plan0.destroy()
+    clk = ClockSampler(dev.index, args.clock_ms).start()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -470,12 +512,13 @@ def run_multi(args):
     n_launch0 = F.launch_count()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     keep = []
-    with ClockSampler(dev.index, args.clock_ms) as clk:
-        start.record(stream)
-        for _ in range(args.steps):
-            keep.append(step(timed=True))
-        end.record(stream)
-        torch.cuda.synchronize()
+    clk.begin()
+    start.record(stream)
+    for _ in range(args.steps):
+        keep.append(step(timed=True))
+    end.record(stream)
+    torch.cuda.synchronize()
+    clk.end()
     dist.barrier()
     launches = F.launch_count() - n_launch0
     my_ms = start.elapsed_time(end)
@@ -527,10 +570,12 @@ def run_multi(args):
                           "t_min_ms": round(t_min * 1e3, 4), "frac_of_t_min": round(t_min * 1e3 / kern_ms, 4),
                           "kernel": "flykv_reshard_kernel (busiest GPU's egress/ingress per launch)"}
                          if not same_dev else
-                         {"bound": "hbm", "achieved": round(hbm_algo / (kern_ms / 1e3) / 1e9, 1), "peak": hbm_peak,
-                          "unit": "GB/s", "frac": round(hbm_algo / (kern_ms / 1e3) / 1e9 / hbm_peak, 4),
+                         {"bound": "hbm", "achieved": round(hbm_algo / (total_ms / args.steps / 1e3) / 1e9, 1),
+                          "peak": hbm_peak, "unit": "GB/s",
+                          "frac": round(hbm_algo / (total_ms / args.steps / 1e3) / 1e9 / hbm_peak, 4),
                           "traffic": None, "peak_source": peak_src,
-                          "kernel": "flykv_reshard_kernel (all ranks' launches run concurrently on cuda:0)"}),
+                          "kernel": "flykv_reshard_kernel of all ranks sharing cuda:0; per-step time (incl. gloo "
+                                    "barrier) as the denominator since the ranks' launches overlap"}),
             "cpu_baseline": None,
             "e2e": ({"value": round(e2e_payload / len(lat) / (lat_mean / 1e3) / 1e9, 3), "unit": "GB/s",
                      "h2d_bytes_per_step": int(h2d // max(len(lat), 1)),

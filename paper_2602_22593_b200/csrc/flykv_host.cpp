@@ -423,7 +423,6 @@ extern "C" kv_status kv_plan_switch(kv_cache* c, const kv_request* reqs, int32_t
 
     // ---- work segments: (request, canonical source replica) ----
     p->bytes.assign((size_t)n * n, 0);
-    struct SegKey { int32_t gpu, idx; };
     std::vector<Seg> segs;
     std::vector<int64_t> seg_atoms;
     for (int32_t i = 0; i < n_reqs; ++i) {
