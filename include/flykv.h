@@ -189,6 +189,14 @@ kv_status kv_plan_upload(kv_plan* plan, void* stream);
  */
 kv_status kv_reshard(kv_plan* plan, int32_t gpu, void* stream);
 
+/* Bench comparator only: the same re-layout split into two
+ * passes through a staging buffer, as a pack -> all-to-all -> unpack
+ * implementation would do.  mode 1 packs every atom of the range (source
+ * replica) into staging[(i - first) * B*d*e]; mode 2 unpacks staging to
+ * every destination replica.  staging: device, >= atoms * B*d*e bytes. */
+kv_status kv_reshard_staged(kv_plan* plan, int32_t gpu, void* staging, int64_t staging_bytes, int32_t mode,
+                            void* stream);
+
 /* Sizes of pool gpu's table after the switch: *n_resident requests resident
  * on gpu (dst group contains gpu), *n_ids block IDs in their tables. */
 kv_status kv_plan_resident(const kv_plan* plan, int32_t gpu, int32_t* n_resident, int32_t* n_ids);

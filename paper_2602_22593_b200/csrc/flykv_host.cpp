@@ -595,6 +595,40 @@ extern "C" kv_status kv_reshard(kv_plan* p, int32_t gpu, void* stream_) {
     return KV_OK;
 }
 
+extern "C" kv_status kv_reshard_staged(kv_plan* p, int32_t gpu, void* staging, int64_t staging_bytes, int32_t mode,
+                                       void* stream_) {
+    if (!p || !staging || (mode != 1 && mode != 2)) return fail(KV_ERR_INVALID_ARG, "bad kv_reshard_staged arguments");
+    if (p->state != PLAN_PLANNED) return fail(KV_ERR_BAD_STATE, "plan already committed");
+    kv_cache* c = p->c;
+    if (gpu < -1 || gpu >= c->n_gpus) return fail(KV_ERR_INVALID_ARG, "gpu %d out of range", gpu);
+    cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+    kv_status s = ensure_device(p, stream);
+    if (s) return s;
+    ReshardArgs a{};
+    a.seg_begin = reinterpret_cast<const int64_t*>(p->dbuf + p->off_seg_begin);
+    a.segs = reinterpret_cast<const Seg*>(p->dbuf + p->off_segs);
+    a.tables = reinterpret_cast<const int32_t*>(p->dbuf + p->off_tables);
+    a.layer_base = c->d_layer_base;
+    a.seg_lo = gpu < 0 ? 0 : p->gpu_seg_lo[gpu];
+    a.seg_hi = gpu < 0 ? (int32_t)p->segs.size() : p->gpu_seg_hi[gpu];
+    a.atom_lo = p->seg_begin[a.seg_lo];
+    a.atom_hi = p->seg_begin[a.seg_hi];
+    a.L = c->geo.num_layers;
+    a.atom_bytes = (int32_t)c->atom_bytes;
+    a.M = c->M;
+    a.peer = 1;  // LDG/STG path
+    a.staged = mode;
+    a.staging = static_cast<char*>(staging);
+    if ((a.atom_hi - a.atom_lo) * c->atom_bytes > staging_bytes)
+        return fail(KV_ERR_INVALID_ARG, "staging buffer too small: %lld bytes needed",
+                    (long long)((a.atom_hi - a.atom_lo) * c->atom_bytes));
+    if (a.atom_hi <= a.atom_lo) return KV_OK;
+    cudaError_t e = launch_reshard(a, p->dev, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "flykv_reshard_kernel (staged) launch");
+    g_launches.fetch_add(1);
+    return KV_OK;
+}
+
 extern "C" kv_status kv_plan_resident(const kv_plan* p, int32_t gpu, int32_t* n_resident, int32_t* n_ids) {
     if (!p || gpu < 0 || gpu >= p->c->n_gpus) return fail(KV_ERR_INVALID_ARG, "bad arguments");
     if (n_resident) *n_resident = p->n_res[gpu];

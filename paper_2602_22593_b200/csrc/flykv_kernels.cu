@@ -103,6 +103,15 @@ __device__ __forceinline__ void lane_decode(const ReshardArgs& a, int64_t atom, 
     la.src = ad.src;
     la.rep1 = ad.rep1;
     la.dst0 = dst_ptr(a, ad, 0);
+    if (a.staged) {  // bench comparator: pack (source -> staging) or unpack (staging -> destinations)
+        char* slot = a.staging + (atom - a.atom_lo) * (int64_t)a.atom_bytes;
+        if (a.staged == 1) {
+            la.dst0 = slot;
+            la.rep1 = 1;
+        } else {
+            la.src = slot;
+        }
+    }
 }
 
 template <typename T>

@@ -117,6 +117,7 @@ _sig("kv_plan_switch", C.c_int, _P, C.POINTER(Request), C.c_int32, C.POINTER(_P)
 _sig("kv_plan_upload", C.c_int, _P, _P)
 _sig("kv_reshard", C.c_int, _P, C.c_int32, _P)
 _sig("kv_plan_resident", C.c_int, _P, C.c_int32, _I32P, _I32P)
+_sig("kv_reshard_staged", C.c_int, _P, C.c_int32, _P, C.c_int64, C.c_int32, _P)
 _sig("kv_remap_block_tables", C.c_int, _P, C.c_int32, _P, _P, _P, _P)
 _sig("kv_plan_dst_tables", C.c_int, _P, _I32P, _I32P)
 _sig("kv_plan_commit", C.c_int, _P)
@@ -142,7 +143,7 @@ _sig("kv_launch_count", C.c_int64)
 _sig("kv_set_reshard_impl", C.c_int, C.c_int32, C.c_int32)
 
 EXPORTED = ["kv_cache_create", "kv_cache_destroy", "kv_layout", "kv_blocks_for", "kv_alloc", "kv_reserve",
-            "kv_free", "kv_free_count", "kv_held_mask", "kv_plan_switch", "kv_plan_upload", "kv_reshard", "kv_plan_resident",
+            "kv_free", "kv_free_count", "kv_held_mask", "kv_plan_switch", "kv_plan_upload", "kv_reshard", "kv_reshard_staged", "kv_plan_resident",
             "kv_remap_block_tables", "kv_plan_dst_tables", "kv_plan_commit", "kv_plan_waves", "kv_plan_get_stats", "kv_plan_destroy",
             "weight_shard_view", "kv_gather_view", "kv_vmm_granularity", "kv_vmm_alloc", "kv_vmm_free",
             "weight_view_alias", "weight_view_unalias", "kv_paged_decode", "kv_ipc_export", "kv_ipc_import", "kv_ipc_close",
@@ -345,6 +346,11 @@ def kv_plan_waves(cache: KVCache, requests, max_wave_bytes: int = 0) -> list:
 
 def kv_reshard(plan: Plan, gpu: int = -1, stream=None):
     _check(_lib.kv_reshard(plan._h, gpu, stream_of(stream)))
+
+
+def kv_reshard_staged(plan: Plan, gpu: int, staging, staging_bytes: int, mode: int, stream=None):
+    """Bench comparator: mode 1 pack -> staging, mode 2 unpack staging -> destinations."""
+    _check(_lib.kv_reshard_staged(plan._h, gpu, ptr_of(staging), int(staging_bytes), mode, stream_of(stream)))
 
 
 def kv_remap_block_tables(plan: Plan, gpu: int, req_ptr, block_ids, per_req_meta, stream=None):

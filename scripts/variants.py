@@ -53,6 +53,13 @@ def main():
             res[f"impl{impl}_ctas{ctas}"] = str(e)
         print(json.dumps(res), flush=True)
     F.set_reshard_impl(0, 0)
+    # comparator: the same re-layout through a staging buffer (pack, then
+    # unpack) -- what pack -> all-to-all -> unpack costs in HBM alone
+    stg = torch.empty(st["n_atoms"] * st["atom_bytes"], dtype=torch.uint8, device="cuda:0")
+    ms = timeit(lambda: (F.kv_reshard_staged(plan, -1, stg, stg.numel(), 1, stream),
+                         F.kv_reshard_staged(plan, -1, stg, stg.numel(), 2, stream)))
+    res["staged_pack_unpack"] = {"ms": ms, "GBps_of_fused_bytes": algo / ms / 1e6}
+    del stg
     n = st["payload_bytes"]
     a = torch.empty(n, dtype=torch.uint8, device="cuda:0")
     b = torch.empty(n, dtype=torch.uint8, device="cuda:0")

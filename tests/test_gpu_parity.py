@@ -23,7 +23,7 @@ def _F():
     return flykv
 
 
-def run_parity(geo, nb, spec, seed=0, per_gpu_launch=False, check_pools=True):
+def run_parity(geo, nb, spec, seed=0, per_gpu_launch=False, check_pools=True, staged=False):
     """spec: list of (T, src_group, dst_group).  Runs the product on cuda:0
     (virtual ranks) and the oracle on host copies; asserts exact equality."""
     F = _F()
@@ -61,7 +61,14 @@ def run_parity(geo, nb, spec, seed=0, per_gpu_launch=False, check_pools=True):
                 hp[:, ids] = host_pools[lo].reshape(og.L, nb[lo], M)[:, ids]
     plan = eng.plan(freqs)
     tables = eng.alloc_tables(plan, range(len(nb)))
-    if per_gpu_launch:
+    if staged:  # comparator path: pack -> staging -> unpack
+        st_, _ = plan.stats()
+        stg = torch.empty(max(st_["n_atoms"] * st_["atom_bytes"], 16), dtype=torch.uint8, device="cuda:0")
+        F.kv_reshard_staged(plan, -1, stg, stg.numel(), 1, eng.stream)
+        F.kv_reshard_staged(plan, -1, stg, stg.numel(), 2, eng.stream)
+        for gpu, t in tables.items():
+            F.kv_remap_block_tables(plan, gpu, t.req_ptr, t.block_ids, t.meta, eng.stream)
+    elif per_gpu_launch:
         for gpu in range(len(nb)):
             F.kv_reshard(plan, gpu, eng.stream)
         for gpu, t in tables.items():
@@ -404,3 +411,12 @@ def test_weight_view_contiguous_alias():
         F.weight_view_alias(buf, row)
     small.close()
     buf.close()
+
+
+@pytest.mark.parametrize("H,p0,p1", [(8, 1, 2), (4, 1, 8), (8, 4, 1)])
+def test_staged_comparator_matches(H, p0, p1):
+    """The bench comparator (pack -> staging -> unpack) produces the same bytes."""
+    geo = (2, H, 128, 16, 2)
+    Ts = [1, 17, 100, 257, 1000, 64]
+    spec = [(T, ((i * p0) % 8, p0), (((i + 3) * p1) % 8, p1)) for i, T in enumerate(Ts)]
+    run_parity(geo, [300] * 8, spec, seed=H + p0 + p1, staged=True)
