@@ -57,6 +57,9 @@ def parse():
     ap.add_argument("--cpu-baseline-steps", type=int, default=6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--frag", type=float, default=1.25, help="source placement window / source need")
+    ap.add_argument("--pool-slack", type=float, default=1.05, help="pool room beyond the window / max need")
+    ap.add_argument("--waves", action="store_true", help="memory-bounded waves (kv_plan_waves) per switch")
     ap.add_argument("--clock-ms", type=int, default=200, help="nvidia-smi sampling period in the timed region (0: off)")
     ap.add_argument("--profile-steps", type=int, default=0, help="(ncu) run N steps only, no JSON")
     ap.add_argument("--no-fill", action="store_true", help="skip the content hash fill (profiling runs)")
@@ -180,14 +183,14 @@ def build_workload(args, world: int, rank: int):
     return w
 
 
-def pools_and_tables(w):
+def pools_and_tables(w, frag: float = 1.25, slack: float = 1.05):
     """Pool sizes + fragmented source tables; block counts from the product's
     own kv_blocks_for (Eq.2)."""
     from paper_2602_22593_b200 import flykv as F
     g = F.geometry(w.L, w.H, w.d, w.B, w.e)
     n0 = [F.kv_blocks_for(g, T, s[1]) for T, s in zip(w.T, w.src)]
     n1 = [F.kv_blocks_for(g, T, d[1]) for T, d in zip(w.T, w.dst)]
-    return synth.realistic_pools(w, n0, n1)
+    return synth.realistic_pools(w, n0, n1, frag=frag, slack=slack)
 
 
 # --------------------------------------------------------------- reference arm
@@ -259,7 +262,7 @@ def run_single(args):
     torch.cuda.set_device(dev)
     w = build_workload(args, 1, 0)
     g = F.geometry(w.L, w.H, w.d, w.B, w.e)
-    nb, tabs = pools_and_tables(w)
+    nb, tabs = pools_and_tables(w, args.frag, args.pool_slack)
     eng = KVSwitchEngine(g, nb, dev, tp_degrees=(2, 4, 8))
     if not args.no_fill:
         for i, t in enumerate(eng.pools.tensors):
@@ -269,45 +272,62 @@ def run_single(args):
     state = {"reqs": [(i, T, s, ids, d) for i, (T, s, d, ids) in enumerate(zip(w.T, w.src, w.dst, tabs))]}
     stream = eng.stream
 
-    def next_requests(plan):
+    def flipped(reqs, plan):
         new = plan.dst_tables()
-        return [(rid, T, d, t, s) for (rid, T, s, _, d), t in zip(state["reqs"], new)]
+        return [(rid, T, d, t, s) for (rid, T, s, _, d), t in zip(reqs, new)]
 
-    ev_pairs = []
+    ev_pairs = []      # per step: [(e0, e1) per wave] around the reshard launches
+    step_stats = []    # per step: summed plan statistics over its waves
+    n_waves = []
 
-    step_stats = []
+    def waves_of(reqs):
+        return F.kv_plan_waves(eng.cache, reqs) if args.waves else [(0, len(reqs))]
 
-    def step(timed_kernel=False):
-        plan = eng.plan(state["reqs"])
-        plan.upload(stream)
-        if timed_kernel:
+    def step(timed_kernel=False, read_back=False):
+        """One whole switch (all waves).  Returns (tables, host copies)."""
+        reqs = state["reqs"]
+        new_reqs, pairs, agg, host = [], [], None, {}
+        ws = waves_of(reqs)
+        for a, b in ws:
+            plan = eng.plan(reqs[a:b])
+            plan.upload(stream)
             st_, _ = plan.stats()
-            step_stats.append(st_)
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-        F.kv_reshard(plan, -1, stream)
+            agg = dict(st_) if agg is None else {k: (agg[k] if k == "atom_bytes" else agg[k] + st_[k]) for k in agg}
+            if timed_kernel:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+            F.kv_reshard(plan, -1, stream)
+            if timed_kernel:
+                e1.record(stream)
+                pairs.append((e0, e1))
+            tables = eng.alloc_tables(plan, range(eng.n_gpus))
+            for gg, t in tables.items():
+                F.kv_remap_block_tables(plan, gg, t.req_ptr, t.block_ids, t.meta, stream)
+            if read_back:
+                for gg, t in tables.items():
+                    n_res, n_ids = plan.resident(gg)
+                    host[(a, gg)] = (t.req_ptr.to("cpu", non_blocking=True),
+                                     t.block_ids[:n_ids].to("cpu", non_blocking=True),
+                                     t.meta[:n_res].to("cpu", non_blocking=True))
+            new_reqs += flipped(reqs[a:b], plan)
+        state["reqs"] = new_reqs
         if timed_kernel:
-            e1.record(stream)
-            ev_pairs.append((e0, e1))
-        tables = eng.alloc_tables(plan, range(eng.n_gpus))
-        for gg, t in tables.items():
-            F.kv_remap_block_tables(plan, gg, t.req_ptr, t.block_ids, t.meta, stream)
-        state["reqs"] = next_requests(plan)
-        return plan, tables
+            ev_pairs.append(pairs)
+            step_stats.append(agg)
+            n_waves.append(len(ws))
+        return agg, host
 
     with torch.cuda.stream(stream):
-        plan0 = eng.plan(state["reqs"])
-        stats, bytes_matrix = plan0.stats()
-        plan0.destroy()
         if args.profile_steps:
             for _ in range(args.profile_steps):
                 step()
             torch.cuda.synchronize()
             return 0
         clk = ClockSampler(torch.cuda.current_device(), args.clock_ms).start()
-        for _ in range(args.warmup):
-            step()
+        stats = None
+        for _ in range(max(args.warmup, 1)):
+            st_w, _ = step()
+            stats = stats or st_w            # forward-direction statistics
         torch.cuda.synchronize()
         # ------------------------------------------------ device-timed region
         # per-step events; when the payload fits in L2 a 512 MiB buffer is
@@ -332,7 +352,7 @@ def run_single(args):
         clk.end()
         launches = F.launch_count() - n_launch0
         total_ms = sum(a_.elapsed_time(b_) for a_, b_ in step_ev)
-        kern_ms = [a.elapsed_time(b) for a, b in ev_pairs]
+        kern_ms = [sum(a.elapsed_time(b) for a, b in pairs) for pairs in ev_pairs]
         plans.clear()
         clocks = clk.summary()
         # ------------------------------------------------ end-to-end region
@@ -344,24 +364,23 @@ def run_single(args):
             plan_ms = []
             for it in range(args.steps):
                 t0 = time.perf_counter()
-                plan = eng.plan(state["reqs"])          # host: validate, allocate, segment index
-                tp = time.perf_counter()
-                tables = eng.execute(plan)               # descriptor H2D, reshard, remap
-                host = {}
-                for gg, t in tables.items():            # new block tables -> host
-                    n_res, n_ids = plan.resident(gg)
-                    host[gg] = (t.req_ptr.to("cpu", non_blocking=True),
-                                t.block_ids[:n_ids].to("cpu", non_blocking=True),
-                                t.meta[:n_res].to("cpu", non_blocking=True))
+                st_, host = step(read_back=True)     # plan(s), upload, reshard, remap, tables -> host
                 stream.synchronize()
                 t1 = time.perf_counter()
                 lat_ms.append((t1 - t0) * 1e3)
-                plan_ms.append((tp - t0) * 1e3)
-                st_, _ = plan.stats()
                 h2d += st_["h2d_bytes"]
                 e2e_payload += st_["payload_bytes"]
                 d2h += sum(int(x.numel()) * 4 for v in host.values() for x in v)
-                state["reqs"] = next_requests(plan)
+                plan_ms.append(0.0)
+            # host planning time alone (kv_plan_switch), measured on plans that are then abandoned
+            for it in range(min(args.steps, 10)):
+                reqs = state["reqs"]
+                a_, b_ = waves_of(reqs)[0]
+                t0 = time.perf_counter()
+                p_ = eng.plan(reqs[a_:b_])
+                plan_ms[it] = (time.perf_counter() - t0) * 1e3
+                p_.destroy()
+            plan_ms = plan_ms[:min(args.steps, 10)]
             e2e = {"value": round(e2e_payload / (sum(lat_ms) / 1e3) / 1e9, 3), "unit": "GB/s",
                    "h2d_bytes_per_step": int(h2d // len(lat_ms)), "d2h_bytes_per_step": int(d2h // len(lat_ms)),
                    "switch_latency_ms_p50": round(statistics.median(lat_ms), 3),
@@ -398,6 +417,8 @@ def run_single(args):
                    "layers": w.L, "kv_heads": w.H, "head_dim": w.d, "block_base": w.B, "requests": len(w.T),
                    "tokens": w.tokens(), "payload_bytes_per_step": int(payload),
                    "payload_bytes_forward": stats["payload_bytes"],
+                   "waves_per_switch": (round(sum(n_waves) / len(n_waves), 2) if args.waves else 1),
+                   "pool_bytes": int(eng.pools.nbytes()),
                    "l2": ("L2 flushed between steps (512 MiB rewrite, outside the step events)" if flush is not None
                           else "inputs larger than L2 (payload >> 126 MB), no flush needed"),
                    "step": "plan + descriptor upload + reshard + remap (alternating direction)"},
