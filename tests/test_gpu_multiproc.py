@@ -17,6 +17,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 GEO = (3, 8, 128, 16, 2)
+GEOS = {"dp_tp": (3, 8, 128, 16, 2), "tp_dp": (3, 8, 128, 16, 2), "gqa": (2, 2, 128, 16, 2), "tp_tp": (2, 8, 64, 16, 2)}
 
 
 def _free_port():
@@ -27,12 +28,20 @@ def _free_port():
     return p
 
 
-def _workload(world):
-    w = synth.dp_to_tp(world, 6 * world, L=GEO[0], H=GEO[1], d=GEO[2], B=GEO[3], lo=1, hi=700, seed=4)
+def _workload(world, kind="dp_tp"):
+    """dp_tp: DP_N -> TP_N merge; tp_dp: the split back (round-robin engines);
+    gqa: H_kv=2 < N (replication, TP_N > kv_heads); tp_tp: TP2 pairs -> TP_N."""
+    L, H, d, B, _ = GEOS[kind]
+    w = synth.dp_to_tp(world, 6 * world, L=L, H=H, d=d, B=B, lo=1, hi=700, seed=4)
+    if kind == "tp_dp":
+        w = synth.Workload(w.name, L, H, d, B, 2, world, w.T, list(w.dst), list(w.src))
+    elif kind == "tp_tp":
+        w = synth.Workload(w.name, L, H, d, B, 2, world, w.T, [((i % (world // 2)) * 2, 2) for i in range(len(w.T))],
+                           list(w.dst))
     return w
 
 
-def _rank(rank, world, port, outdir):
+def _rank(rank, world, port, outdir, kind):
     import torch
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -41,14 +50,16 @@ def _rank(rank, world, port, outdir):
     try:
         from paper_2602_22593_b200 import comm
         from paper_2602_22593_b200 import flykv as F
-        w = _workload(world)
-        g = F.geometry(*GEO)
+        w = _workload(world, kind)
+        g = F.geometry(*GEOS[kind])
         _, _, M = F.kv_layout(g, 1)
         n0 = [F.kv_blocks_for(g, T, s[1]) for T, s in zip(w.T, w.src)]
         n1 = [F.kv_blocks_for(g, T, d[1]) for T, d in zip(w.T, w.dst)]
         nb, tabs = synth.realistic_pools(w, n0, n1)
         pool = torch.empty((w.L, nb[rank], M), dtype=torch.uint8, device="cuda:0")
         synth.fill_hash_torch(pool, rank)
+        if w.src[0][1] > w.H:  # GQA replicated sources: replicas identical (R10)
+            raise RuntimeError("replicated sources not used here")
         torch.cuda.synchronize()
         bases, nbs, imported = comm.exchange_pools(pool, rank, world, w.L, M)
         cache = F.KVCache(g, nbs, bases, [p for p in (2, 4, 8) if p <= world])
@@ -76,18 +87,18 @@ def _rank(rank, world, port, outdir):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_ipc_push_matches_oracle(world):
+@pytest.mark.parametrize("world,kind", [(2, "dp_tp"), (4, "dp_tp"), (4, "tp_dp"), (4, "gqa"), (4, "tp_tp")])
+def test_ipc_push_matches_oracle(world, kind):
     import torch.multiprocessing as mp
-    w = _workload(world)
-    og = O.Geom(*GEO)
+    w = _workload(world, kind)
+    og = O.Geom(*GEOS[kind])
     n0 = [O.num_blocks(og, T, s[1]) for T, s in zip(w.T, w.src)]
     n1 = [O.num_blocks(og, T, d[1]) for T, d in zip(w.T, w.dst)]
     nb, tabs = synth.realistic_pools(w, n0, n1)
     with tempfile.TemporaryDirectory() as td:
         ctx = mp.get_context("spawn")
         port = _free_port()
-        procs = [ctx.Process(target=_rank, args=(r, world, port, td)) for r in range(world)]
+        procs = [ctx.Process(target=_rank, args=(r, world, port, td, kind)) for r in range(world)]
         for p in procs:
             p.start()
         for p in procs:
@@ -102,7 +113,8 @@ def test_ipc_push_matches_oracle(world):
         held = [np.zeros(n, dtype=np.uint8) for n in nb]
         oreqs = []
         for T, s, d, ids in zip(w.T, w.src, w.dst, tabs):
-            held[s[0]][ids] = 1
+            for r in range(s[1]):
+                held[s[0] + r][ids] = 1
             oreqs.append(O.Req(T, s, list(ids), d))
         st, otabs = O.switch(og, pools, held, oreqs)
         assert st == 0
