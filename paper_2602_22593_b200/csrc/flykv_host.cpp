@@ -430,6 +430,17 @@ extern "C" kv_status kv_plan_switch(kv_cache* c, const kv_request* reqs, int32_t
         if (!q.moving) continue;
         const int32_t C = (int32_t)ceil_div(q.T, B);
         if (C == 0) continue;
+        if ((int64_t)L * 2 * C * H >= ((int64_t)1 << 31)) {  // per-segment atom index is 32-bit on the device
+            for (int32_t j = 0; j < n_reqs; ++j) {
+                const ReqPlan& u = p->reqs[j];
+                if (!u.moving) continue;
+                for (int32_t r = 0; r < u.dst.degree; ++r)
+                    for (int32_t k = 0; k < u.n1; ++k) bit_clr(c->held[u.dst.first_gpu + r], p->tables[u.dst_off + k]);
+            }
+            delete p;
+            return fail(KV_ERR_INVALID_ARG, "request %d: %lld atoms exceed the 2^31 per-request limit", i,
+                        (long long)L * 2 * C * H);
+        }
         const Layout l0 = layout_of(H, q.src.degree), l1 = layout_of(H, q.dst.degree);
         for (int32_t r = 0; r < q.src.degree; ++r) {
             if (l0.rep > 1 && r % l0.rep) continue;  // only the lowest replica is read (R10)

@@ -420,3 +420,44 @@ def test_staged_comparator_matches(H, p0, p1):
     Ts = [1, 17, 100, 257, 1000, 64]
     spec = [(T, ((i * p0) % 8, p0), (((i + 3) * p1) % 8, p1)) for i, T in enumerate(Ts)]
     run_parity(geo, [300] * 8, spec, seed=H + p0 + p1, staged=True)
+
+
+def test_million_token_request():
+    """One 1,048,581-token request DP -> TP8 (65,537 chunks, ragged tail):
+    every destination atom checked against the oracle's atom map."""
+    F = _F()
+    from paper_2602_22593_b200.engine import KVSwitchEngine
+    geo = (1, 8, 64, 16, 2)
+    og = O.Geom(*geo)
+    T = (1 << 20) + 5
+    n0 = O.num_blocks(og, T, 1)
+    n1 = O.num_blocks(og, T, 8)
+    nb = [n0 + n1 + 64] * 8  # uniform IDs across the TP8 group (R6): equal ID ranges
+    eng = KVSwitchEngine(F.geometry(*geo), nb, "cuda:0")
+    for gpu, t in enumerate(eng.pools.tensors):
+        synth.fill_hash_torch(t, gpu, seed=5)
+    ids = eng.cache.alloc((0, 1), n0)
+    plan, tables, host = eng.switch([(0, T, (0, 1), ids, (0, 8))], read_back=True)
+    tab1 = plan.dst_tables()[0]
+    sg, so, dg, do = O.atom_map(og, nb, T, (0, 1), ids, (0, 8), tab1)
+    atom_words = og.B * og.d * og.e // 4
+    ar = torch.arange(atom_words, dtype=torch.int64, device="cuda:0")
+    flat = [t.reshape(-1).view(torch.int32) for t in eng.pools.tensors]
+    for gd in range(8):
+        m = dg == gd
+        s_w = torch.as_tensor(so[m] // 4, device="cuda:0")
+        d_w = torch.as_tensor(do[m] // 4, device="cuda:0")
+        for c0 in range(0, s_w.numel(), 32768):
+            sl = slice(c0, c0 + 32768)
+            want = synth.hash32_torch(0, s_w[sl, None] + ar[None, :], seed=5)
+            assert torch.equal(flat[gd][d_w[sl, None] + ar[None, :]], want)
+    assert host[0][2].tolist() == [[0, 128, 1, 0]]
+
+
+def test_many_small_requests_remap_tiles():
+    """5,000 requests (1..40 tokens) DP8 -> TP8: the remap kernel's
+    1024-request tiles and carries, whole pools and CSR tables vs the oracle."""
+    rng = np.random.default_rng(21)
+    geo = (1, 8, 64, 16, 2)
+    spec = [(int(rng.integers(1, 41)), (i % 8, 1), (0, 8)) for i in range(5000)]
+    run_parity(geo, [20000] * 8, spec, seed=21)
