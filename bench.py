@@ -11,9 +11,11 @@ back), so every step moves the full payload with fresh allocations.
 N=1 (default): BASELINE configs[1] (Llama-3.1-8B-shaped cache, 64 requests,
 DP4 -> TP2x2) with the 4 engines as virtual ranks (4 pools) on one B200; the
 bound is HBM (read + write of every byte).  N>1 (torchrun, one process per
-GPU): DP_N -> TP_N merge of the same geometry with 16 requests per GPU, every
-GPU pushing its atoms into peer pools over NVLink (IPC-mapped), bound by
-NVLink per-direction bandwidth ("weak" scaling).
+GPU, every GPU pushing its atoms into peer pools over NVLink, IPC-mapped,
+bound by NVLink per-direction bandwidth): N=4 runs configs[1] as stated
+(DP4 -> TP2x2 on 4 GPUs), N=8 the headline configs[3] (Llama-3-70B
+8 x DP1 -> TP8), N=2 a DP2 -> TP2 merge of the configs[1] geometry with the
+same ~4.9 GB per GPU ("weak" scaling: per-GPU bytes roughly fixed).
 
 `value`  = payload bytes of the K timed steps / device time (CUDA events on
            the switch stream; max over ranks), pools resident in HBM.
@@ -175,8 +177,12 @@ class ClockSampler:
 def build_workload(args, world: int, rank: int):
     if world == 1:
         w = synth.WORKLOADS[args.config]()
+    elif world == 4:
+        w = synth.llama8b_dp4_tp2x2()       # BJ configs[1] as stated: DP4 -> TP2x2 on 4 GPUs
+    elif world == 8:
+        w = synth.llama70b_dp8_tp8()        # BJ configs[3]: the headline 8 x DP1 -> TP8
     else:
-        w = synth.dp_to_tp(world, 16 * world)
+        w = synth.dp_to_tp(world, 16 * world)  # ~4.9 GB per GPU, like configs[1] per GPU
     if args.requests:
         w = synth.Workload(w.name + f" first{args.requests}", w.L, w.H, w.d, w.B, w.e, w.n_gpus,
                            w.T[:args.requests], w.src[:args.requests], w.dst[:args.requests])
@@ -243,7 +249,9 @@ def run_reference(args):
         "impl": "reference", "metric": "DP<->TP KV re-layout GB/s", "value": round(gbs, 4), "unit": "GB/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(sec * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": w.name, "sample": info},
+        "config": {"workload": w.name + (f" ({w.n_gpus} virtual ranks on 1 GPU)" if w.n_gpus > 1 and world == 1 else ""),
+                   "layers": w.L, "kv_heads": w.H, "head_dim": w.d, "block_base": w.B, "requests": len(w.T),
+                   "tokens": w.tokens(), "sample": info},
         "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": info},
         "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
