@@ -68,7 +68,13 @@ typedef struct {
 
 /* One live request to re-lay-out.  src_blocks: host array of the request's
  * block IDs at the source degree, length n_src_blocks == ceil(num_tokens /
- * B(src.degree)) (uniform across the source group, R6).  Caller-owned. */
+ * B(src.degree)) (uniform across the source group, R6).  Caller-owned.
+ * src_rank_ids / dst_rank_ids (optional, NULL = identity, R3): host arrays
+ * of degree entries, a permutation; member engine first_gpu + m of the group
+ * holds the head slice of rank ID rank_ids[m] ("the Manager assigns each
+ * engine a unique rank ID r"; the weight view of that engine is then
+ * View(W, dim, rank_ids[m], degree), Eq.1).  kv_suggest_rank_ids picks a
+ * movement-minimising assignment. */
 typedef struct {
     int64_t req_id;
     int32_t num_tokens;
@@ -76,6 +82,8 @@ typedef struct {
     const int32_t* src_blocks;
     int32_t n_src_blocks;
     kv_group dst;
+    const int32_t* src_rank_ids;
+    const int32_t* dst_rank_ids;
 } kv_request;
 
 typedef struct kv_cache kv_cache; /* opaque: pools, allocator bitmaps      */
@@ -198,7 +206,9 @@ kv_status kv_reshard_staged(kv_plan* plan, int32_t gpu, void* staging, int64_t s
                             void* stream);
 
 /* Sizes of pool gpu's table after the switch: *n_resident requests resident
- * on gpu (dst group contains gpu), *n_ids block IDs in their tables. */
+ * on gpu (dst group contains gpu), *n_ids block IDs in their tables.  The
+ * per_req_meta first head of kv_remap_block_tables follows the request's
+ * dst_rank_ids. */
 kv_status kv_plan_resident(const kv_plan* plan, int32_t gpu, int32_t* n_resident, int32_t* n_ids);
 
 /*
@@ -238,6 +248,15 @@ kv_status kv_plan_commit(kv_plan* plan);
  */
 kv_status kv_plan_waves(const kv_cache* cache, const kv_request* reqs, int32_t n_reqs, int64_t max_wave_bytes,
                         int32_t* wave_start, int32_t* n_waves);
+
+/* kv_suggest_rank_ids: N2 egress reduction.  For the requests of reqs whose
+ * destination is group dst, choose the rank-ID assignment of dst's members
+ * (out: host [dst.degree], rank ID of member m) that maximises the bytes
+ * already resident on the engine that will own them (exact assignment over
+ * the members, deterministic: ties keep the lower rank ID on the lower
+ * member).  Pass it as dst_rank_ids of those requests.  No state change. */
+kv_status kv_suggest_rank_ids(const kv_cache* cache, const kv_request* reqs, int32_t n_reqs, kv_group dst,
+                              int32_t* out_rank_ids);
 
 /* Host copies of every destination table, in plan order: dst_ptr host
  * [n_reqs+1], dst_ids host [dst_ptr[n_reqs]] (pass dst_ids = NULL to size). */

@@ -44,11 +44,12 @@ def block_view(pool: np.ndarray, L: int, nb: int, M: int, l: int, blk: int,
     return raw.reshape(2, h_loc(H, p), b_of(H, B, p), d * e)
 
 
-def read_request(pools, geo, group, table, T_slots):
+def read_request(pools, geo, group, table, T_slots, rid=None):
     """Gather the logical KV of one request: array [L, 2, H, T_slots, d*e] (uint8).
 
     Every replica of a head is read; an assertion checks replicas agree
-    (head-ownership invariant).
+    (head-ownership invariant).  rid[m] = rank ID of member m (None =
+    identity): member m holds the head slice of rank ID rid[m].
     """
     L, H, d, B, e = geo
     M = 2 * H * B * d * e
@@ -59,7 +60,7 @@ def read_request(pools, geo, group, table, T_slots):
     for r in range(p):
         pool = pools[g0 + r]
         nb = pool.size // (L * M)
-        heads = heads_of_rank(H, p, r)
+        heads = heads_of_rank(H, p, rid[r] if rid is not None else r)
         for t in range(T_slots):
             blk = table[t // bp]
             s = t % bp
@@ -76,7 +77,7 @@ def read_request(pools, geo, group, table, T_slots):
     return out
 
 
-def write_request(pools, geo, group, table, logical):
+def write_request(pools, geo, group, table, logical, rid=None):
     """Scatter logical KV [L, 2, H, T_slots, d*e] into every owner's blocks."""
     L, H, d, B, e = geo
     M = 2 * H * B * d * e
@@ -86,7 +87,7 @@ def write_request(pools, geo, group, table, logical):
     for r in range(p):
         pool = pools[g0 + r]
         nb = pool.size // (L * M)
-        heads = heads_of_rank(H, p, r)
+        heads = heads_of_rank(H, p, rid[r] if rid is not None else r)
         for t in range(T_slots):
             blk = table[t // bp]
             s = t % bp
@@ -116,8 +117,14 @@ def switch(pools, held, geo, reqs):
     """
     L, H, d, B, e = geo
     tabs = []
+
+    def same(rq):  # same group and same rank IDs (R12, R19)
+        a = getattr(rq, "src_rid", None) or list(range(rq.src[1]))
+        b = getattr(rq, "dst_rid", None) or list(range(rq.dst[1]))
+        return tuple(rq.src) == tuple(rq.dst) and list(a) == list(b)
+
     for rq in reqs:
-        if tuple(rq.src) == tuple(rq.dst):
+        if same(rq):
             tabs.append(list(rq.src_ids))
             continue
         n1 = -(-rq.T // b_of(H, B, rq.dst[1]))
@@ -127,11 +134,11 @@ def switch(pools, held, geo, reqs):
         for r in range(rq.dst[1]):
             held[rq.dst[0] + r][ids] = 1
         slots = -(-rq.T // B) * B  # whole B-token atoms (R9)
-        logical = read_request(pools, geo, rq.src, rq.src_ids, slots)
-        write_request(pools, geo, rq.dst, ids, logical)
+        logical = read_request(pools, geo, rq.src, rq.src_ids, slots, getattr(rq, "src_rid", None))
+        write_request(pools, geo, rq.dst, ids, logical, getattr(rq, "dst_rid", None))
         tabs.append(ids)
     for rq in reqs:
-        if tuple(rq.src) == tuple(rq.dst):
+        if same(rq):
             continue
         for r in range(rq.src[1]):
             held[rq.src[0] + r][list(rq.src_ids)] = 0

@@ -100,13 +100,24 @@ int32_t or_first_head(const or_geom* g, int32_t p, int32_t r) {
     return r / (p / g->H);
 }
 
+/* Rank-ID assignment ("the Manager assigns each engine a unique
+ * rank ID r in [0, m-1]"): rid[m] is the rank ID of member engine g0 + m of
+ * the group; NULL means the identity (R3).  The member holding rank ID r. */
+int32_t or_member(const int32_t* rid, int32_t p, int32_t r) {
+    int32_t m;
+    if (!rid) return r;
+    for (m = 0; m < p; m++)
+        if (rid[m] == r) return m;
+    return -1;
+}
+
 /* Where the d*e bytes of (kv, h, token t) of a request live, for replica j:
  * GPU index and byte offset inside that GPU's layer region (add
  * l * num_blocks * M for layer l).  tab = the request's block table at
- * degree p, group starting at GPU g0. */
-void or_locate(const or_geom* g, int32_t g0, int32_t p, const int32_t* tab,
-               int32_t kv, int32_t h, int32_t t, int32_t j,
-               int32_t* gpu, int64_t* off) {
+ * degree p, group starting at GPU g0, rank IDs rid (NULL = identity). */
+void or_locate_rid(const or_geom* g, int32_t g0, int32_t p, const int32_t* rid, const int32_t* tab,
+                   int32_t kv, int32_t h, int32_t t, int32_t j,
+                   int32_t* gpu, int64_t* off) {
     int32_t bp = or_block_tokens(g, p);
     int32_t hl = or_h_loc(g, p);
     int64_t row = (int64_t)g->d * g->e;           /* bytes of one token of one head */
@@ -114,14 +125,30 @@ void or_locate(const or_geom* g, int32_t g0, int32_t p, const int32_t* tab,
     int32_t block = tab[t / bp];
     int32_t slot = t % bp;
     int32_t lh = or_local_head(g, p, h);
-    *gpu = g0 + or_owner_rank(g, p, h, j);
+    *gpu = g0 + or_member(rid, p, or_owner_rank(g, p, h, j));
     *off = (int64_t)block * M                   /* block                   */
          + (int64_t)kv * (M / 2)                /* K half, then V half     */
          + ((int64_t)lh * bp + slot) * row;     /* [H_loc][B(p)][d]        */
     (void)hl;
 }
 
+void or_locate(const or_geom* g, int32_t g0, int32_t p, const int32_t* tab,
+               int32_t kv, int32_t h, int32_t t, int32_t j,
+               int32_t* gpu, int64_t* off) {
+    or_locate_rid(g, g0, p, NULL, tab, kv, h, t, j, gpu, off);
+}
+
 /* ---------------- the switch ------------------------------------------- */
+
+/* A request is a no-op only if it stays in the same group with the same
+ * rank IDs (R12, R19). */
+static int same_layout(int32_t g0a, int32_t pa, const int32_t* ra, int32_t g0b, int32_t pb, const int32_t* rb) {
+    int32_t m;
+    if (g0a != g0b || pa != pb) return 0;
+    for (m = 0; m < pa; m++)
+        if ((ra ? ra[m] : m) != (rb ? rb[m] : m)) return 0;
+    return 1;
+}
 
 enum { OR_OK = 0, OR_OUT_OF_BLOCKS = 6, OR_INVALID = 1 };
 
@@ -145,6 +172,7 @@ int32_t or_switch(const or_geom* g, int32_t n_gpus, const int32_t* num_blocks,
                   const int32_t* T, const int32_t* src_g0, const int32_t* src_p,
                   const int32_t* src_ptr, const int32_t* src_ids,
                   const int32_t* dst_g0, const int32_t* dst_p,
+                  const int32_t* const* src_rid, const int32_t* const* dst_rid,
                   int32_t* dst_ptr, int32_t* dst_ids, int32_t dst_cap) {
     int64_t M = or_block_bytes(g);
     int64_t row = (int64_t)g->d * g->e;
@@ -156,7 +184,9 @@ int32_t or_switch(const or_geom* g, int32_t n_gpus, const int32_t* num_blocks,
     for (i = 0; i < n_reqs; i++) {
         const int32_t* tab0 = src_ids + src_ptr[i];
         int32_t* tab1 = dst_ids + dst_ptr[i];
-        int same = (src_g0[i] == dst_g0[i] && src_p[i] == dst_p[i]);
+        const int32_t* rid0 = src_rid ? src_rid[i] : NULL;
+        const int32_t* rid1 = dst_rid ? dst_rid[i] : NULL;
+        int same = same_layout(src_g0[i], src_p[i], rid0, dst_g0[i], dst_p[i], rid1);
         int32_t n1 = same ? (src_ptr[i + 1] - src_ptr[i])
                           : or_num_blocks(g, T[i], dst_p[i]);
         if (dst_ptr[i] + n1 > dst_cap) return OR_INVALID;
@@ -193,10 +223,10 @@ int32_t or_switch(const or_geom* g, int32_t n_gpus, const int32_t* num_blocks,
                         int32_t sg, dg;
                         int64_t so, dof;
                         /* lowest source replica (R10) */
-                        or_locate(g, src_g0[i], src_p[i], tab0, kv, h, t, 0, &sg, &so);
+                        or_locate_rid(g, src_g0[i], src_p[i], rid0, tab0, kv, h, t, 0, &sg, &so);
                         const uint8_t* src = pools[sg] + (int64_t)l * num_blocks[sg] * M + so;
                         for (j = 0; j < reps; j++) {
-                            or_locate(g, dst_g0[i], dst_p[i], tab1, kv, h, t, j, &dg, &dof);
+                            or_locate_rid(g, dst_g0[i], dst_p[i], rid1, tab1, kv, h, t, j, &dg, &dof);
                             uint8_t* dst = pools[dg] + (int64_t)l * num_blocks[dg] * M + dof;
                             memcpy(dst, src, (size_t)row);
                         }
@@ -205,7 +235,8 @@ int32_t or_switch(const or_geom* g, int32_t n_gpus, const int32_t* num_blocks,
 
     /* release every source block (after all copies, R13) */
     for (i = 0; i < n_reqs; i++) {
-        int same = (src_g0[i] == dst_g0[i] && src_p[i] == dst_p[i]);
+        int same = same_layout(src_g0[i], src_p[i], src_rid ? src_rid[i] : NULL,
+                               dst_g0[i], dst_p[i], dst_rid ? dst_rid[i] : NULL);
         int32_t r;
         if (same) continue;
         for (k = src_ptr[i]; k < src_ptr[i + 1]; k++)
@@ -224,7 +255,7 @@ int32_t or_switch(const or_geom* g, int32_t n_gpus, const int32_t* num_blocks,
  * Returns n_res.
  */
 int32_t or_tables(const or_geom* g, int32_t gpu, int32_t n_reqs,
-                  const int32_t* dst_g0, const int32_t* dst_p,
+                  const int32_t* dst_g0, const int32_t* dst_p, const int32_t* const* dst_rid,
                   const int32_t* dst_ptr, const int32_t* dst_ids,
                   int32_t* req_ptr, int32_t* ids, int32_t* meta) {
     int32_t i, k, n = 0, pos = 0;
@@ -235,7 +266,11 @@ int32_t or_tables(const or_geom* g, int32_t gpu, int32_t n_reqs,
         meta[4 * n + 0] = i;
         meta[4 * n + 1] = or_block_tokens(g, dst_p[i]);
         meta[4 * n + 2] = or_h_loc(g, dst_p[i]);
-        meta[4 * n + 3] = or_first_head(g, dst_p[i], gpu - dst_g0[i]);
+        {
+            const int32_t* rid = dst_rid ? dst_rid[i] : NULL;
+            int32_t m = gpu - dst_g0[i];
+            meta[4 * n + 3] = or_first_head(g, dst_p[i], rid ? rid[m] : m);
+        }
         n++;
         req_ptr[n] = pos;
     }
@@ -251,8 +286,8 @@ int32_t or_tables(const or_geom* g, int32_t gpu, int32_t n_reqs,
  * full-size checks of the device result.  Returns the number of entries.
  */
 int64_t or_atom_map(const or_geom* g, const int32_t* num_blocks, int32_t T,
-                    int32_t src_g0, int32_t src_p, const int32_t* tab0,
-                    int32_t dst_g0, int32_t dst_p, const int32_t* tab1,
+                    int32_t src_g0, int32_t src_p, const int32_t* rid0, const int32_t* tab0,
+                    int32_t dst_g0, int32_t dst_p, const int32_t* rid1, const int32_t* tab1,
                     int32_t* src_gpu, int64_t* src_off, int32_t* dst_gpu, int64_t* dst_off) {
     int64_t M = or_block_bytes(g);
     int32_t C = (T + g->B - 1) / g->B;
@@ -266,8 +301,8 @@ int64_t or_atom_map(const or_geom* g, const int32_t* num_blocks, int32_t T,
                     for (j = 0; j < reps; j++) {
                         int32_t sg, dg;
                         int64_t so, dof;
-                        or_locate(g, src_g0, src_p, tab0, kv, h, c * g->B, 0, &sg, &so);
-                        or_locate(g, dst_g0, dst_p, tab1, kv, h, c * g->B, j, &dg, &dof);
+                        or_locate_rid(g, src_g0, src_p, rid0, tab0, kv, h, c * g->B, 0, &sg, &so);
+                        or_locate_rid(g, dst_g0, dst_p, rid1, tab1, kv, h, c * g->B, j, &dg, &dof);
                         src_gpu[n] = sg;
                         src_off[n] = (int64_t)l * num_blocks[sg] * M + so;
                         dst_gpu[n] = dg;

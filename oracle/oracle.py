@@ -75,15 +75,19 @@ def lib():
         L.or_locate.argtypes = [G, C.c_int32, C.c_int32, _P32, C.c_int32, C.c_int32,
                                 C.c_int32, C.c_int32, _P32, C.POINTER(C.c_int64)]
         L.or_locate.restype = None
+        L.or_locate_rid.argtypes = [G, C.c_int32, C.c_int32, _P32, _P32, C.c_int32, C.c_int32,
+                                    C.c_int32, C.c_int32, _P32, C.POINTER(C.c_int64)]
+        L.or_locate_rid.restype = None
         L.or_switch.argtypes = [G, C.c_int32, _P32, C.POINTER(C.c_void_p), C.c_int32, C.POINTER(C.c_void_p),
-                                C.c_int32, _P32, _P32, _P32, _P32, _P32, _P32, _P32, _P32, _P32,
-                                C.c_int32]
+                                C.c_int32, _P32, _P32, _P32, _P32, _P32, _P32, _P32,
+                                C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), _P32, _P32, C.c_int32]
         L.or_switch.restype = C.c_int32
-        L.or_tables.argtypes = [G, C.c_int32, C.c_int32, _P32, _P32, _P32, _P32, _P32, _P32, _P32]
+        L.or_tables.argtypes = [G, C.c_int32, C.c_int32, _P32, _P32, C.POINTER(C.c_void_p), _P32, _P32, _P32, _P32,
+                                _P32]
         L.or_tables.restype = C.c_int32
         _P64 = C.POINTER(C.c_int64)
-        L.or_atom_map.argtypes = [G, _P32, C.c_int32, C.c_int32, C.c_int32, _P32, C.c_int32, C.c_int32, _P32,
-                                  _P32, _P64, _P32, _P64]
+        L.or_atom_map.argtypes = [G, _P32, C.c_int32, C.c_int32, C.c_int32, _P32, _P32, C.c_int32, C.c_int32,
+                                  _P32, _P32, _P32, _P64, _P32, _P64]
         L.or_atom_map.restype = C.c_int64
     return _lib
 
@@ -125,13 +129,23 @@ def first_head(g: Geom, p: int, r: int) -> int:
     return lib().or_first_head(C.byref(g.c()), p, r)
 
 
-def locate(g: Geom, g0: int, p: int, tab, kv: int, h: int, t: int, j: int = 0):
-    """(gpu, byte offset inside that GPU's layer region) of token t of head h."""
+def locate(g: Geom, g0: int, p: int, tab, kv: int, h: int, t: int, j: int = 0, rid=None):
+    """(gpu, byte offset inside that GPU's layer region) of token t of head h;
+    rid = rank IDs of the group's members (None = identity)."""
     tab = _i32(tab)
     gpu = C.c_int32()
     off = C.c_int64()
-    lib().or_locate(C.byref(g.c()), g0, p, _ptr(tab), kv, h, t, j, C.byref(gpu), C.byref(off))
+    r = _i32(rid) if rid is not None else None
+    lib().or_locate_rid(C.byref(g.c()), g0, p, _ptr(r) if r is not None else None, _ptr(tab), kv, h, t, j,
+                        C.byref(gpu), C.byref(off))
     return gpu.value, off.value
+
+
+def _rid_array(rids):
+    """ctypes array of int32* (NULL = identity) + keep-alive list."""
+    keep = [(_i32(r) if r is not None else None) for r in rids]
+    arr = (C.c_void_p * max(len(keep), 1))(*[(k.ctypes.data if k is not None else None) for k in keep])
+    return arr, keep
 
 
 # ---------------------------------------------------------------- the switch
@@ -141,6 +155,8 @@ class Req:
     src: tuple  # (first_gpu, degree)
     src_ids: list
     dst: tuple  # (first_gpu, degree)
+    src_rid: list = None  # rank IDs of the source group's members (None = identity)
+    dst_rid: list = None
 
 
 def switch(g: Geom, pools: list, held: list, reqs: list, copy: bool = True):
@@ -176,9 +192,11 @@ def switch(g: Geom, pools: list, held: list, reqs: list, copy: bool = True):
     dids = np.zeros(cap, dtype=np.int32)
     pool_ptrs = (C.c_void_p * len(held))(*([p.ctypes.data for p in pools] if copy else [0] * len(held)))
     held_ptrs = (C.c_void_p * len(held))(*[h.ctypes.data for h in held])
+    srid, k1 = _rid_array([r.src_rid for r in reqs])
+    drid, k2 = _rid_array([r.dst_rid for r in reqs])
     st = lib().or_switch(C.byref(g.c()), len(held), _ptr(nb), pool_ptrs, int(copy), held_ptrs, n,
                          _ptr(T), _ptr(sg0), _ptr(sp), _ptr(sptr), _ptr(sids), _ptr(dg0), _ptr(dp),
-                         _ptr(dptr), _ptr(dids), cap)
+                         srid, drid, _ptr(dptr), _ptr(dids), cap)
     tabs = [dids[dptr[i]:dptr[i + 1]].copy() for i in range(n)] if st == 0 else None
     return st, tabs
 
@@ -193,12 +211,13 @@ def tables(g: Geom, gpu: int, reqs: list, dst_tabs: list):
     req_ptr = np.zeros(n + 1, dtype=np.int32)
     ids = np.zeros(max(int(dptr[-1]), 1), dtype=np.int32)
     meta = np.zeros(4 * max(n, 1), dtype=np.int32)
-    nres = lib().or_tables(C.byref(g.c()), gpu, n, _ptr(dg0), _ptr(dp), _ptr(dptr), _ptr(dids),
+    drid, keep = _rid_array([r.dst_rid for r in reqs])
+    nres = lib().or_tables(C.byref(g.c()), gpu, n, _ptr(dg0), _ptr(dp), drid, _ptr(dptr), _ptr(dids),
                            _ptr(req_ptr), _ptr(ids), _ptr(meta))
     return req_ptr[:nres + 1].copy(), ids[:req_ptr[nres]].copy(), meta[:4 * nres].reshape(nres, 4).copy()
 
 
-def atom_map(g: Geom, num_blocks, T: int, src, tab0, dst, tab1):
+def atom_map(g: Geom, num_blocks, T: int, src, tab0, dst, tab1, src_rid=None, dst_rid=None):
     """All atom copies of one request: arrays (src_gpu, src_off, dst_gpu, dst_off)."""
     nb = _i32(num_blocks)
     C_ = -(-T // g.B)
@@ -209,7 +228,10 @@ def atom_map(g: Geom, num_blocks, T: int, src, tab0, dst, tab1):
     do = np.zeros(max(n, 1), dtype=np.int64)
     t0, t1 = _i32(tab0 if len(tab0) else [0]), _i32(tab1 if len(tab1) else [0])
     P64 = C.POINTER(C.c_int64)
-    m = lib().or_atom_map(C.byref(g.c()), _ptr(nb), T, src[0], src[1], _ptr(t0), dst[0], dst[1], _ptr(t1),
+    r0 = _i32(src_rid) if src_rid is not None else None
+    r1 = _i32(dst_rid) if dst_rid is not None else None
+    m = lib().or_atom_map(C.byref(g.c()), _ptr(nb), T, src[0], src[1], _ptr(r0) if r0 is not None else None, _ptr(t0),
+                          dst[0], dst[1], _ptr(r1) if r1 is not None else None, _ptr(t1),
                           _ptr(sg), so.ctypes.data_as(P64), _ptr(dg), do.ctypes.data_as(P64))
     assert m == n
     return sg[:n], so[:n], dg[:n], do[:n]

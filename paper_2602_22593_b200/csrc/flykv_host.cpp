@@ -81,6 +81,8 @@ struct ReqPlan {
     int32_t src_off, n0;  // source table in plan->tables
     int32_t dst_off, n1;  // destination table in plan->tables
     bool moving;
+    int32_t src_rid[64], dst_rid[64];  // rank ID of each member, identity by default
+    bool dst_rid_identity;
 };
 
 enum { PLAN_PLANNED = 0, PLAN_COMMITTED = 1 };
@@ -131,7 +133,7 @@ static kv_status check_degree(int32_t H, int32_t p) {
 
 // Aligned contiguous segment of a supported degree (R12).
 static kv_status check_group(const kv_cache* c, kv_group g) {
-    if (g.degree < 1) return fail(KV_ERR_UNKNOWN_GROUP, "degree %d < 1", g.degree);
+    if (g.degree < 1 || g.degree > 64) return fail(KV_ERR_UNKNOWN_GROUP, "degree %d outside [1, 64]", g.degree);
     if (g.degree != 1 &&
         std::find(c->degrees.begin(), c->degrees.end(), g.degree) == c->degrees.end())
         return fail(KV_ERR_UNKNOWN_GROUP, "degree %d not in the pool's TP degrees", g.degree);
@@ -316,6 +318,17 @@ extern "C" kv_status kv_held_mask(const kv_cache* c, int32_t gpu, uint8_t* held)
     return KV_OK;
 }
 
+// A request moves unless it stays in the same group with the same rank IDs (R12).
+static bool request_moves(const kv_request& r) {
+    if (r.src.first_gpu != r.dst.first_gpu || r.src.degree != r.dst.degree) return true;
+    for (int32_t m = 0; m < r.src.degree; ++m) {
+        const int32_t a = r.src_rank_ids ? r.src_rank_ids[m] : m;
+        const int32_t b = r.dst_rank_ids ? r.dst_rank_ids[m] : m;
+        if (a != b) return true;
+    }
+    return false;
+}
+
 // ------------------------------------------------------------ planner
 // a2: validate a request list against the cache (no state change).
 static kv_status validate_requests(const kv_cache* c, const kv_request* reqs, int32_t n_reqs, int64_t* total_src_out,
@@ -335,6 +348,18 @@ static kv_status validate_requests(const kv_cache* c, const kv_request* reqs, in
         if (s) return s;
         if (!ids_seen.insert(r.req_id).second)
             return fail(KV_ERR_DUPLICATE_REQUEST, "req_id %lld repeated", (long long)r.req_id);
+        for (int side = 0; side < 2; ++side) {
+            const int32_t* rid = side ? r.dst_rank_ids : r.src_rank_ids;
+            const int32_t p = side ? r.dst.degree : r.src.degree;
+            if (!rid) continue;
+            uint64_t seen = 0;
+            for (int32_t m = 0; m < p; ++m) {
+                if (rid[m] < 0 || rid[m] >= p || ((seen >> rid[m]) & 1ull))
+                    return fail(KV_ERR_INVALID_ARG, "request %d: %s rank IDs are not a permutation of [0,%d)", i,
+                                side ? "dst" : "src", p);
+                seen |= 1ull << rid[m];
+            }
+        }
         const Layout l0 = layout_of(H, r.src.degree);
         const int64_t n0 = ceil_div(r.num_tokens, (int64_t)B * l0.k);
         if (r.n_src_blocks != n0 || (n0 > 0 && !r.src_blocks))
@@ -389,7 +414,15 @@ extern "C" kv_status kv_plan_switch(kv_cache* c, const kv_request* reqs, int32_t
         q.T = r.num_tokens;
         q.src = r.src;
         q.dst = r.dst;
-        q.moving = !(r.src.first_gpu == r.dst.first_gpu && r.src.degree == r.dst.degree);
+        for (int32_t m = 0; m < 64; ++m) {
+            q.src_rid[m] = (r.src_rank_ids && m < r.src.degree) ? r.src_rank_ids[m] : m;
+            q.dst_rid[m] = (r.dst_rank_ids && m < r.dst.degree) ? r.dst_rank_ids[m] : m;
+        }
+        q.dst_rid_identity = true;
+        for (int32_t m = 0; m < r.dst.degree; ++m) q.dst_rid_identity &= q.dst_rid[m] == m;
+        bool same_ids = true;
+        for (int32_t m = 0; m < r.src.degree; ++m) same_ids &= q.src_rid[m] == q.dst_rid[m];
+        q.moving = !(r.src.first_gpu == r.dst.first_gpu && r.src.degree == r.dst.degree && same_ids);
         q.src_off = (int32_t)p->tables.size();
         q.n0 = r.n_src_blocks;
         p->tables.insert(p->tables.end(), r.src_blocks, r.src_blocks + r.n_src_blocks);
@@ -421,10 +454,22 @@ extern "C" kv_status kv_plan_switch(kv_cache* c, const kv_request* reqs, int32_t
         }
     }
 
+    // ---- rank-ID tables of non-identity destinations: rank ID of
+    // member m (remap's first head) and member of rank ID (reshard's owner) ----
+    std::vector<int32_t> dst_rid_off(n_reqs, -1), dst_inv_off(n_reqs, -1);
+    for (int32_t i = 0; i < n_reqs; ++i) {
+        const ReqPlan& q = p->reqs[i];
+        if (q.dst_rid_identity) continue;
+        dst_rid_off[i] = (int32_t)p->tables.size();
+        p->tables.insert(p->tables.end(), q.dst_rid, q.dst_rid + q.dst.degree);
+        dst_inv_off[i] = (int32_t)p->tables.size();
+        p->tables.resize(p->tables.size() + q.dst.degree);
+        for (int32_t m = 0; m < q.dst.degree; ++m) p->tables[dst_inv_off[i] + q.dst_rid[m]] = m;
+    }
+
     // ---- work segments: (request, canonical source replica) ----
     p->bytes.assign((size_t)n * n, 0);
     std::vector<Seg> segs;
-    std::vector<int64_t> seg_atoms;
     for (int32_t i = 0; i < n_reqs; ++i) {
         const ReqPlan& q = p->reqs[i];
         if (!q.moving) continue;
@@ -442,14 +487,18 @@ extern "C" kv_status kv_plan_switch(kv_cache* c, const kv_request* reqs, int32_t
                         (long long)L * 2 * C * H);
         }
         const Layout l0 = layout_of(H, q.src.degree), l1 = layout_of(H, q.dst.degree);
-        for (int32_t r = 0; r < q.src.degree; ++r) {
-            if (l0.rep > 1 && r % l0.rep) continue;  // only the lowest replica is read (R10)
+        int32_t inv1[64];
+        for (int32_t m = 0; m < q.dst.degree; ++m) inv1[q.dst_rid[m]] = m;
+        for (int32_t m = 0; m < q.src.degree; ++m) {
+            const int32_t rid = q.src_rid[m];         // member m holds rank ID rid's slice
+            if (l0.rep > 1 && rid % l0.rep) continue;  // only replica 0 of each head is read (R10)
             Seg s{};
-            s.src_gpu = q.src.first_gpu + r;
+            s.src_gpu = q.src.first_gpu + m;
             s.dst_g0 = q.dst.first_gpu;
             s.C = C;
             s.nh = l0.hloc;
-            s.h0 = first_head_of_rank(l0, r);
+            s.h0 = first_head_of_rank(l0, rid);
+            s.dst_inv = dst_inv_off[i];
             s.src_tab = q.src_off;
             s.dst_tab = q.dst_off;
             s.hloc0 = l0.hloc;
@@ -461,7 +510,7 @@ extern "C" kv_status kv_plan_switch(kv_cache* c, const kv_request* reqs, int32_t
             const int64_t head_bytes = (int64_t)L * 2 * C * c->atom_bytes;
             for (int32_t hh = 0; hh < s.nh; ++hh)
                 for (int32_t j = 0; j < l1.rep; ++j) {
-                    const int32_t dg = s.dst_g0 + owner_rank(l1, s.h0 + hh, j);
+                    const int32_t dg = s.dst_g0 + inv1[owner_rank(l1, s.h0 + hh, j)];
                     p->bytes[(size_t)s.src_gpu * n + dg] += head_bytes;
                 }
         }
@@ -495,7 +544,7 @@ extern "C" kv_status kv_plan_switch(kv_cache* c, const kv_request* reqs, int32_t
     for (int32_t i = 0; i < n_reqs; ++i) {
         const ReqPlan& q = p->reqs[i];
         n_moving += q.moving;
-        p->recs[i] = ReqRec{q.dst.first_gpu, q.dst.degree, q.n1, q.dst_off};
+        p->recs[i] = ReqRec{q.dst.first_gpu, q.dst.degree, q.n1, q.dst_off, dst_rid_off[i], {0, 0, 0}};
         for (int32_t r = 0; r < q.dst.degree; ++r) {
             p->n_res[q.dst.first_gpu + r] += 1;
             p->n_res_ids[q.dst.first_gpu + r] += q.n1;
@@ -680,7 +729,7 @@ extern "C" kv_status kv_plan_waves(const kv_cache* c, const kv_request* reqs, in
     auto close_wave = [&](int32_t end) {  // release the wave's sources (its remap commits it)
         for (int32_t j = start; j < end; ++j) {
             const kv_request& r = reqs[j];
-            if (r.src.first_gpu == r.dst.first_gpu && r.src.degree == r.dst.degree) continue;
+            if (!request_moves(r)) continue;
             for (int32_t q = 0; q < r.src.degree; ++q)
                 for (int32_t k = 0; k < r.n_src_blocks; ++k) bit_clr(sim[r.src.first_gpu + q], r.src_blocks[k]);
         }
@@ -690,8 +739,7 @@ extern "C" kv_status kv_plan_waves(const kv_cache* c, const kv_request* reqs, in
     };
     for (int32_t i = 0; i < n_reqs; ++i) {
         const kv_request& r = reqs[i];
-        const bool moving = !(r.src.first_gpu == r.dst.first_gpu && r.src.degree == r.dst.degree);
-        if (!moving) continue;
+        if (!request_moves(r)) continue;
         const Layout l1 = layout_of(H, r.dst.degree);
         const int32_t n1 = (int32_t)ceil_div(r.num_tokens, (int64_t)B * l1.k);
         const int64_t bytes = (int64_t)G.num_layers * 2 * H * ceil_div(r.num_tokens, B) * c->atom_bytes * l1.rep;
@@ -712,6 +760,65 @@ extern "C" kv_status kv_plan_waves(const kv_cache* c, const kv_request* reqs, in
     if (n_reqs > start || w == 0) close_wave(n_reqs);
     wave_start[w] = n_reqs;
     *n_waves = w;
+    return KV_OK;
+}
+
+extern "C" kv_status kv_suggest_rank_ids(const kv_cache* c, const kv_request* reqs, int32_t n_reqs, kv_group dst,
+                                         int32_t* out) {
+    if (!c || !out || n_reqs < 0 || (n_reqs > 0 && !reqs)) return fail(KV_ERR_INVALID_ARG, "bad arguments");
+    kv_status s = check_group(c, dst);
+    if (s) return s;
+    const int32_t p = dst.degree, H = c->geo.num_kv_heads, B = c->geo.block_base, L = c->geo.num_layers;
+    for (int32_t m = 0; m < p; ++m) out[m] = m;
+    if (p > 16) return KV_OK;  // exact assignment only up to 16 members; identity beyond
+    const Layout l1 = layout_of(H, p);
+    // gain[m][r]: bytes already on member m's GPU that rank ID r would own
+    std::vector<int64_t> gain((size_t)p * p, 0);
+    for (int32_t i = 0; i < n_reqs; ++i) {
+        const kv_request& r = reqs[i];
+        if (r.dst.first_gpu != dst.first_gpu || r.dst.degree != p) continue;
+        s = check_group(c, r.src);
+        if (s) return s;
+        const Layout l0 = layout_of(H, r.src.degree);
+        const int64_t head_bytes = (int64_t)L * 2 * ceil_div(r.num_tokens, B) * c->atom_bytes;
+        for (int32_t rid = 0; rid < p; ++rid) {
+            const int32_t h0 = first_head_of_rank(l1, rid);
+            const int32_t nh = l1.rep == 1 ? l1.hloc : 1;
+            for (int32_t h = h0; h < h0 + nh; ++h) {
+                const int32_t src_rid = owner_rank(l0, h, 0);  // canonical replica (R10)
+                int32_t sm = src_rid;
+                if (r.src_rank_ids)
+                    for (int32_t q = 0; q < r.src.degree; ++q)
+                        if (r.src_rank_ids[q] == src_rid) sm = q;
+                const int32_t g = r.src.first_gpu + sm;
+                if (g >= dst.first_gpu && g < dst.first_gpu + p) gain[(size_t)(g - dst.first_gpu) * p + rid] += head_bytes;
+            }
+        }
+    }
+    // exact assignment by DP over subsets of rank IDs (members in order)
+    const uint32_t full = (1u << p) - 1;
+    std::vector<int64_t> dp((size_t)full + 1, -1);
+    std::vector<int8_t> parent((size_t)full + 1, -1);
+    dp[0] = 0;
+    for (uint32_t mask = 0; mask < full; ++mask) {
+        if (dp[mask] < 0) continue;
+        const int32_t m = __builtin_popcount(mask);
+        for (int32_t rid = 0; rid < p; ++rid) {
+            if (mask & (1u << rid)) continue;
+            const uint32_t nm = mask | (1u << rid);
+            const int64_t v = dp[mask] + gain[(size_t)m * p + rid];
+            if (v > dp[nm]) {
+                dp[nm] = v;
+                parent[nm] = (int8_t)rid;
+            }
+        }
+    }
+    uint32_t mask = full;
+    for (int32_t m = p - 1; m >= 0; --m) {
+        const int32_t rid = parent[mask];
+        out[m] = rid;
+        mask ^= 1u << rid;
+    }
     return KV_OK;
 }
 

@@ -52,13 +52,16 @@ struct Seg {
     int32_t dst_tab;   // offset of the destination table
     int32_t hloc0, k0; // source layout
     int32_t hloc1, k1, rep1; // destination layout
-    int32_t pad[4];
+    int32_t dst_inv;   // offset of the destination's member-of-rank-ID table in tables, -1 = identity
+    int32_t pad[3];
 };
 static_assert(sizeof(Seg) == 64, "Seg is 64 bytes");
 
 // Per-request record used by the remap kernel (a6).
 struct ReqRec {
     int32_t dst_g0, dst_p, n1, dst_tab;
+    int32_t dst_rid;   // offset of the destination rank IDs (rank ID of member m) in tables, -1 = identity
+    int32_t pad[3];
 };
 
 struct ReshardArgs {

@@ -38,6 +38,7 @@ struct AtomAddr {
     int64_t doff;      // byte offset of the atom inside a destination layer region
     int32_t l, h;      // layer, head
     int32_t dst_g0, rep1, hloc1;
+    int32_t dst_inv;   // member-of-rank-ID table offset (-1 = identity rank IDs)
 };
 
 __device__ __forceinline__ int find_seg(const int64_t* __restrict__ seg_begin, int lo, int hi,
@@ -77,12 +78,15 @@ __device__ __forceinline__ void decode(const ReshardArgs& a, int64_t atom, int s
     out.dst_g0 = sg.dst_g0;
     out.rep1 = sg.rep1;
     out.hloc1 = sg.hloc1;
+    out.dst_inv = sg.dst_inv;
 }
 
-// Pointer to replica j of the decoded atom (1 replica, or p/H under GQA, R2).
+// Pointer to replica j of the decoded atom (1 replica, or p/H under GQA, R2):
+// rank ID owning head h, then the member engine holding that rank ID.
 __device__ __forceinline__ char* dst_ptr(const ReshardArgs& a, const AtomAddr& ad, int j) {
-    const int32_t r = ad.rep1 == 1 ? ad.h / ad.hloc1 : ad.h * ad.rep1 + j;
-    return a.layer_base[(ad.dst_g0 + r) * a.L + ad.l] + ad.doff;
+    const int32_t rid = ad.rep1 == 1 ? ad.h / ad.hloc1 : ad.h * ad.rep1 + j;
+    const int32_t m = ad.dst_inv < 0 ? rid : __ldg(a.tables + ad.dst_inv + rid);
+    return a.layer_base[(ad.dst_g0 + m) * a.L + ad.l] + ad.doff;
 }
 
 // Lane-parallel decode: each lane of the warp decodes one of 32 consecutive
@@ -447,7 +451,8 @@ __global__ void __launch_bounds__(1024) flykv_remap_kernel(const RemapArgs a) {
             a.meta[4 * ef + 0] = i;
             a.meta[4 * ef + 1] = a.B * L.k;
             a.meta[4 * ef + 2] = L.hloc;
-            a.meta[4 * ef + 3] = first_head_of_rank(L, a.gpu - rr.dst_g0);
+            const int32_t m = a.gpu - rr.dst_g0;
+            a.meta[4 * ef + 3] = first_head_of_rank(L, rr.dst_rid < 0 ? m : a.tables[rr.dst_rid + m]);
         }
         __syncthreads();
         if (tid == 0) { carry_f += wf[31]; carry_c += wc[31]; }

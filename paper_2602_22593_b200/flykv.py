@@ -60,7 +60,8 @@ class Group(C.Structure):
 
 class Request(C.Structure):
     _fields_ = [("req_id", C.c_int64), ("num_tokens", C.c_int32), ("src", Group),
-                ("src_blocks", C.POINTER(C.c_int32)), ("n_src_blocks", C.c_int32), ("dst", Group)]
+                ("src_blocks", C.POINTER(C.c_int32)), ("n_src_blocks", C.c_int32), ("dst", Group),
+                ("src_rank_ids", C.POINTER(C.c_int32)), ("dst_rank_ids", C.POINTER(C.c_int32))]
 
 
 class PlanStats(C.Structure):
@@ -122,6 +123,7 @@ _sig("kv_remap_block_tables", C.c_int, _P, C.c_int32, _P, _P, _P, _P)
 _sig("kv_plan_dst_tables", C.c_int, _P, _I32P, _I32P)
 _sig("kv_plan_commit", C.c_int, _P)
 _sig("kv_plan_waves", C.c_int, _P, C.POINTER(Request), C.c_int32, C.c_int64, _I32P, _I32P)
+_sig("kv_suggest_rank_ids", C.c_int, _P, C.POINTER(Request), C.c_int32, Group, _I32P)
 _sig("kv_plan_get_stats", C.c_int, _P, C.POINTER(PlanStats), _I64P)
 _sig("kv_plan_destroy", None, _P)
 _sig("weight_shard_view", C.c_int, C.POINTER(WeightDesc), C.c_int32, C.c_int32, C.POINTER(View))
@@ -144,7 +146,7 @@ _sig("kv_set_reshard_impl", C.c_int, C.c_int32, C.c_int32)
 
 EXPORTED = ["kv_cache_create", "kv_cache_destroy", "kv_layout", "kv_blocks_for", "kv_alloc", "kv_reserve",
             "kv_free", "kv_free_count", "kv_held_mask", "kv_plan_switch", "kv_plan_upload", "kv_reshard", "kv_reshard_staged", "kv_plan_resident",
-            "kv_remap_block_tables", "kv_plan_dst_tables", "kv_plan_commit", "kv_plan_waves", "kv_plan_get_stats", "kv_plan_destroy",
+            "kv_remap_block_tables", "kv_plan_dst_tables", "kv_plan_commit", "kv_plan_waves", "kv_suggest_rank_ids", "kv_plan_get_stats", "kv_plan_destroy",
             "weight_shard_view", "kv_gather_view", "kv_vmm_granularity", "kv_vmm_alloc", "kv_vmm_free",
             "weight_view_alias", "weight_view_unalias", "kv_paged_decode", "kv_ipc_export", "kv_ipc_import", "kv_ipc_close",
             "kv_stream_sync", "kv_strerror", "kv_last_error", "kv_launch_count", "kv_set_reshard_impl"]
@@ -313,15 +315,27 @@ class Plan:
 
 
 def make_requests(reqs):
-    """reqs: iterable of (req_id, num_tokens, (g0, p0), src_ids, (g1, p1)).
-    Returns (ctypes array, keep-alive list)."""
+    """reqs: iterable of (req_id, num_tokens, (g0, p0), src_ids, (g1, p1)
+    [, src_rank_ids [, dst_rank_ids]]) -- rank IDs None = identity.
+    Returns (ctypes array, keep-alive list of the block tables)."""
     reqs = list(reqs)
     arr = (Request * max(len(reqs), 1))()
-    keep = []
-    for i, (rid, T, src, ids, dst) in enumerate(reqs):
+    keep, extra = [], []
+    for i, r in enumerate(reqs):
+        rid, T, src, ids, dst = r[:5]
         a = _i32(ids)
         keep.append(a)
-        arr[i] = Request(int(rid), int(T), Group(*src), a.ctypes.data_as(_I32P), a.size, Group(*dst))
+        rids = []
+        for x in (r[5] if len(r) > 5 else None, r[6] if len(r) > 6 else None):
+            if x is None:
+                rids.append(None)
+            else:
+                b = _i32(x)
+                extra.append(b)
+                rids.append(b.ctypes.data_as(_I32P))
+        arr[i] = Request(int(rid), int(T), Group(*src), a.ctypes.data_as(_I32P), a.size, Group(*dst),
+                         rids[0], rids[1])
+    arr._keep_extra = extra
     return arr, keep
 
 
@@ -332,6 +346,14 @@ def kv_plan_switch(cache: KVCache, requests) -> Plan:
     h = C.c_void_p()
     _check(_lib.kv_plan_switch(cache._h, arr, n, C.byref(h)))
     return Plan(cache, h, n)
+
+
+def kv_suggest_rank_ids(cache: KVCache, requests, dst) -> list:
+    """N2: movement-minimising rank-ID assignment of group dst's members."""
+    arr, keep = make_requests(requests)
+    out = np.zeros(max(dst[1], 1), dtype=np.int32)
+    _check(_lib.kv_suggest_rank_ids(cache._h, arr, len(keep), Group(*dst), out.ctypes.data_as(_I32P)))
+    return [int(x) for x in out[:dst[1]]]
 
 
 def kv_plan_waves(cache: KVCache, requests, max_wave_bytes: int = 0) -> list:

@@ -277,3 +277,35 @@ def test_memory_bounded_waves_match_oracle():
     one = 2 * 2 * 8 * 64 * 8 * 2   # L*2*H*T*d*e per request
     assert len(F.kv_plan_waves(c2, reqs2)) == 1
     assert [b - a for a, b in F.kv_plan_waves(c2, reqs2, max_wave_bytes=3 * one)] == [3, 3, 2]
+
+
+def test_rank_ids_plan_and_suggestion():
+    """N2: the product's planner follows per-request rank IDs exactly like the
+    oracle (destination tables, byte matrix); kv_suggest_rank_ids finds the
+    assignment that keeps half of a TP4 -> TP8 promotion local (vs 1/8)."""
+    geo = (2, 8, 8, 4, 2)
+    og = O.Geom(*geo)
+    c = fake_cache(geo, [256] * 8)
+    reqs = []
+    for i, T in enumerate([64, 130, 7]):
+        ids = c.alloc((0, 4), F.kv_blocks_for(c.geom, T, 4))
+        reqs.append((i, T, (0, 4), ids, (0, 8)))
+    sugg = F.kv_suggest_rank_ids(c, reqs, (0, 8))
+    assert sorted(sugg) == list(range(8))
+    assert all(sugg[m] // 2 == m for m in range(4))   # member m < 4 owns one of its own two heads
+    for rid, local in ((None, 1 / 8), (sugg, 1 / 2)):
+        rq = [r + (None, rid) for r in reqs]
+        plan = c.plan_switch(rq)
+        st, mat = plan.stats()
+        assert np.trace(mat) / mat.sum() == pytest.approx(local)
+        # byte matrix equals the oracle's atom map
+        want = np.zeros((8, 8), dtype=np.int64)
+        tabs = plan.dst_tables()
+        for (i, T, s_, ids, d_), t in zip(reqs, tabs):
+            sg, so, dg, do = O.atom_map(og, [256] * 8, T, s_, ids, d_, t, None, rid)
+            np.add.at(want, (sg, dg), og.B * og.d * og.e)
+        assert np.array_equal(mat, want)
+        plan.destroy()
+    with pytest.raises(F.FlyKVError) as e:
+        c.plan_switch([reqs[0] + (None, [0, 1, 2, 3, 4, 5, 6, 6])])
+    assert e.value.name == "KV_ERR_INVALID_ARG"

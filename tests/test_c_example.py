@@ -11,9 +11,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def _bin():
     from paper_2602_22593_b200 import _build
-    if not os.path.exists(_build.EXAMPLE_BIN):
+    b = _build.EXAMPLE_BIN
+    deps = [_build.EXAMPLE_SRC, os.path.join(_build.INCLUDE, "flykv.h"), _build.LIB]
+    if not os.path.exists(b) or any(os.path.getmtime(d) > os.path.getmtime(b) for d in deps):
         _build.build_example()
-    return _build.EXAMPLE_BIN
+    return b
 
 
 def test_c_example_builds():

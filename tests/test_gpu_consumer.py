@@ -48,8 +48,10 @@ def _decode_all(F, eng, geo, plan, tables, q_full, gpus, q_slices, seq):
     return res
 
 
-@pytest.mark.parametrize("H,Hq,p1", [(8, 32, 2), (8, 32, 4), (8, 64, 8), (4, 32, 8), (2, 16, 8), (8, 8, 2)])
-def test_tp_after_relayout_equals_dp(H, Hq, p1):
+@pytest.mark.parametrize("H,Hq,p1,permuted", [(8, 32, 2, False), (8, 32, 4, False), (8, 64, 8, False),
+                                               (4, 32, 8, False), (2, 16, 8, False), (8, 8, 2, False),
+                                               (8, 32, 4, True), (4, 32, 8, True)])
+def test_tp_after_relayout_equals_dp(H, Hq, p1, permuted):
     F = pytest.importorskip("paper_2602_22593_b200.flykv")
     from paper_2602_22593_b200.engine import KVSwitchEngine
     geo = (2, H, 128, 16, 2)
@@ -101,12 +103,15 @@ def test_tp_after_relayout_equals_dp(H, Hq, p1):
             ref = (p_ / p_.sum()) @ V
             assert np.allclose(out_dp[(i, qh)], ref, rtol=2e-3, atol=2e-3)
     # switch DP -> TP_p1 and decode on every rank with its Eq.1 Q slice
-    move = [(i, T, s_, ids, d_) for i, (T, s_, ids, d_) in enumerate(zip(seq, src, tabs0, dst))]
+    # rank IDs of the destination members: identity or a permutation;
+    # member m then takes the Eq.1 Q slice of its rank ID
+    rid = [int(x) for x in np.random.default_rng(p1).permutation(p1)] if permuted else list(range(p1))
+    move = [(i, T, s_, ids, d_, None, rid) for i, (T, s_, ids, d_) in enumerate(zip(seq, src, tabs0, dst))]
     plan_tp, tables_tp, _ = eng.switch(move, read_back=True)
     ql = Hq // p1
 
     def q_slice(g, meta):
-        r = g % p1  # rank inside its aligned group
+        r = rid[g % p1]  # rank ID of this member of its aligned group
         return r * ql, (r + 1) * ql
     out_tp = _decode_all(F, eng, geo, plan_tp, tables_tp, q_full, range(n_gpus), q_slice, seq)
     assert set(out_tp) == set(out_dp)

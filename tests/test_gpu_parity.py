@@ -36,23 +36,25 @@ def run_parity(geo, nb, spec, seed=0, per_gpu_launch=False, check_pools=True, st
     torch.cuda.synchronize()
     host_pools = [t.cpu().numpy().reshape(-1).copy() for t in eng.pools.tensors]
     held = [np.zeros(n, dtype=np.uint8) for n in nb]
-    counts = [O.num_blocks(og, T, src[1]) for (T, src, dst) in spec]
-    w = synth.Workload("t", *geo, len(nb), [s[0] for s in spec], [s[1] for s in spec], [s[2] for s in spec])
+    spec = [tuple(x) + (None,) * (5 - len(x)) for x in spec]  # (T, src, dst, src_rid, dst_rid)
+    counts = [O.num_blocks(og, x[0], x[1][1]) for x in spec]
+    w = synth.Workload("t", *geo, len(nb), [x[0] for x in spec], [x[1] for x in spec], [x[2] for x in spec])
     tabs0 = synth.source_tables(w, counts, nb, seed=seed + 1)
     oreqs, freqs = [], []
-    for i, ((T, src, dst), ids) in enumerate(zip(spec, tabs0)):
+    for i, ((T, src, dst, srid, drid), ids) in enumerate(zip(spec, tabs0)):
         eng.cache.reserve(src, ids)
         for r in range(src[1]):
             held[src[0] + r][ids] = 1
-        oreqs.append(O.Req(T, src, list(ids), dst))
-        freqs.append((1000 + i, T, src, ids, dst))
-    # GQA sources: replicas identical (R10) -- copy on both sides
+        oreqs.append(O.Req(T, src, list(ids), dst, srid, drid))
+        freqs.append((1000 + i, T, src, ids, dst, srid, drid))
+    # GQA sources: replicas identical (R10) under the source rank IDs -- copy on both sides
     M = O.block_bytes(og)
-    for (T, src, dst), ids in zip(spec, tabs0):
+    for (T, src, dst, srid, drid), ids in zip(spec, tabs0):
         if src[1] > og.H:
             rep = src[1] // og.H
+            rid = list(srid) if srid is not None else list(range(src[1]))
             for r in range(src[1]):
-                lo = src[0] + (r // rep) * rep
+                lo = src[0] + rid.index((rid[r] // rep) * rep)
                 if lo == src[0] + r:
                     continue
                 idx = torch.as_tensor(np.asarray(ids, dtype=np.int64), device="cuda:0")
@@ -461,3 +463,20 @@ def test_many_small_requests_remap_tiles():
     geo = (1, 8, 64, 16, 2)
     spec = [(int(rng.integers(1, 41)), (i % 8, 1), (0, 8)) for i in range(5000)]
     run_parity(geo, [20000] * 8, spec, seed=21)
+
+
+@pytest.mark.parametrize("H,p0,p1", [(8, 4, 8), (8, 2, 8), (8, 8, 4), (4, 8, 8), (2, 4, 8), (8, 1, 4), (8, 4, 4)])
+def test_rank_ids_parity(H, p0, p1):
+    """Rank-ID assignments on both sides (N2) incl. GQA replication and
+    same-group re-permutation: whole pools, tables and first heads equal the
+    oracle."""
+    rng = np.random.default_rng(H * 31 + p0 * 5 + p1)
+    geo = (2, H, 64, 16, 2)
+    spec = []
+    for i, T in enumerate([1, 17, 100, 257, 1000, 33]):
+        src = ((i * p0) % 8, p0)
+        dst = (((i + 1) * p1) % 8, p1)
+        srid = [int(x) for x in rng.permutation(p0)]
+        drid = [int(x) for x in rng.permutation(p1)]
+        spec.append((T, src, dst, srid, drid))
+    run_parity(geo, [400] * 8, spec, seed=H + p0 + p1)

@@ -361,3 +361,101 @@ def test_atom_map_matches_switch():
             mine[c][d:d + atom] = before[a][b:b + atom]
     for a, b in zip(mine, pools):
         assert np.array_equal(a, b)
+
+
+# ------------------------------------------------------------ rank-ID assignment (N2)
+def _perm(rng, p):
+    return [int(x) for x in rng.permutation(p)]
+
+
+@pytest.mark.parametrize("H,p0,p1", [(4, 1, 2), (4, 2, 4), (4, 4, 2), (2, 1, 4), (2, 4, 1), (1, 2, 4), (4, 4, 4)])
+def test_rank_ids_c_oracle_matches_brute(H, p0, p1):
+    """Rank-ID assignments (member m holds rank ID rid[m]'s slice):
+    the C oracle and the brute-force enumerator agree for random
+    permutations on both sides; replicated sources are made consistent
+    under their own rank IDs first."""
+    rng = np.random.default_rng(H * 13 + p0 * 7 + p1)
+    geo = (2, H, 4, 4, 2)
+    g = O.Geom(*geo)
+    M = O.block_bytes(g)
+    n_gpus = 4
+    nb = [256] * n_gpus
+    spec = [(T, ((i * p0) % n_gpus // p0 * p0, p0), (((i + 1) * p1) % n_gpus // p1 * p1, p1))
+            for i, T in enumerate([1, 17, 33, 64, 70])]
+    g_, pools, held, reqs = _setup(geo, nb, spec, seed=3)
+    for r in reqs:
+        r.src_rid = _perm(rng, r.src[1])
+        r.dst_rid = _perm(rng, r.dst[1]) if tuple(r.dst) != tuple(r.src) else r.src_rid
+        if r.src[1] > H:  # replicas identical under the source rank IDs
+            rep = r.src[1] // H
+            for m in range(r.src[1]):
+                lo = r.src_rid.index((r.src_rid[m] // rep) * rep)
+                for l in range(g.L):
+                    for b in r.src_ids:
+                        a = (l * nb[r.src[0] + lo] + b) * M
+                        z = (l * nb[r.src[0] + m] + b) * M
+                        pools[r.src[0] + m][z:z + M] = pools[r.src[0] + lo][a:a + M]
+    pools_b = [p.copy() for p in pools]
+    held_b = [h.copy() for h in held]
+    st, tabs = O.switch(g, pools, held, reqs)
+    tabs_b = brute.switch(pools_b, held_b, geo, reqs)
+    assert st == 0 and [list(t) for t in tabs] == [list(t) for t in tabs_b]
+    for a, b in zip(pools, pools_b):
+        assert np.array_equal(a, b)
+
+
+def test_rank_ids_identity_and_round_trip():
+    """rid = identity reproduces the default layout (R3) byte for byte, and a
+    permuted TP4 -> TP8 -> permuted TP4 round trip restores the logical KV."""
+    geo = (2, 8, 4, 4, 2)
+    g = O.Geom(*geo)
+    spec = [(T, (0, 4), (0, 8)) for T in (5, 64, 131)]
+    _, p1, h1, r1 = _setup(geo, [128] * 8, spec, seed=4)
+    _, p2, h2, r2 = _setup(geo, [128] * 8, spec, seed=4)
+    for r in r2:
+        r.src_rid, r.dst_rid = [0, 1, 2, 3], list(range(8))
+    assert O.switch(g, p1, h1, r1)[0] == 0 and O.switch(g, p2, h2, r2)[0] == 0
+    assert all(np.array_equal(a, b) for a, b in zip(p1, p2))
+    _, pools, held, reqs = _setup(geo, [128] * 8, spec, seed=5)
+    for r in reqs:
+        r.src_rid = [2, 0, 3, 1]
+        r.dst_rid = [0, 2, 4, 6, 1, 3, 5, 7]
+    slots = [-(-r.T // 4) * 4 for r in reqs]
+    before = [brute.read_request(pools, geo, r.src, r.src_ids, s, r.src_rid) for r, s in zip(reqs, slots)]
+    st, tabs = O.switch(g, pools, held, reqs)
+    assert st == 0
+    back = [O.Req(r.T, r.dst, list(t), r.src, r.dst_rid, r.src_rid) for r, t in zip(reqs, tabs)]
+    st, tabs2 = O.switch(g, pools, held, back)
+    assert st == 0
+    after = [brute.read_request(pools, geo, r.src, t, s, r.src_rid) for r, t, s in zip(reqs, tabs2, slots)]
+    assert all(np.array_equal(a, b) for a, b in zip(before, after))
+
+
+def test_rank_ids_keep_heads_local():
+    """N2: promoting TP4 -> TP8 with rank IDs [0,2,4,6,1,3,5,7] keeps one of
+    each source GPU's two heads on that GPU: half the atoms stay local,
+    against 1/8 with the identity assignment."""
+    g = O.Geom(2, 8, 4, 4, 2)
+    _, pools, held, reqs = _setup((2, 8, 4, 4, 2), [128] * 8, [(64, (0, 4), (0, 8))], seed=6)
+    r = reqs[0]
+    tab1 = list(range(100, 100 + O.num_blocks(g, 64, 8)))
+    for rid, want in ((None, 1 / 8), ([0, 2, 4, 6, 1, 3, 5, 7], 1 / 2)):
+        sg, so, dg, do = O.atom_map(g, [128] * 8, 64, (0, 4), r.src_ids, (0, 8), tab1, None, rid)
+        assert np.mean(sg == dg) == pytest.approx(want)
+
+
+def test_same_group_repermutation_moves():
+    """R19: staying in the same TP4 group with new rank IDs moves every head
+    whose owner changes; brute force and the C oracle agree."""
+    geo = (2, 8, 4, 4, 2)
+    g = O.Geom(*geo)
+    _, pools, held, reqs = _setup(geo, [64] * 4, [(40, (0, 4), (0, 4)), (9, (0, 4), (0, 4))], seed=8)
+    for r in reqs:
+        r.src_rid, r.dst_rid = [0, 1, 2, 3], [1, 0, 3, 2]
+    pools_b = [p.copy() for p in pools]
+    held_b = [h.copy() for h in held]
+    st, tabs = O.switch(g, pools, held, reqs)
+    tabs_b = brute.switch(pools_b, held_b, geo, reqs)
+    assert st == 0 and [list(t) for t in tabs] == [list(t) for t in tabs_b]
+    assert all(set(t).isdisjoint(r.src_ids) for t, r in zip(tabs, reqs))  # fresh blocks
+    assert all(np.array_equal(a, b) for a, b in zip(pools, pools_b))
