@@ -62,6 +62,8 @@ def parse():
     ap.add_argument("--frag", type=float, default=1.25, help="source placement window / source need")
     ap.add_argument("--pool-slack", type=float, default=1.05, help="pool room beyond the window / max need")
     ap.add_argument("--waves", action="store_true", help="memory-bounded waves (kv_plan_waves) per switch")
+    ap.add_argument("--rank-ids", default="identity", choices=["identity", "suggest"],
+                    help="destination rank-ID assignment (P:291): identity (R3) or kv_suggest_rank_ids (N2)")
     ap.add_argument("--clock-ms", type=int, default=200, help="nvidia-smi sampling period in the timed region (0: off)")
     ap.add_argument("--profile-steps", type=int, default=0, help="(ncu) run N steps only, no JSON")
     ap.add_argument("--no-fill", action="store_true", help="skip the content hash fill (profiling runs)")
@@ -277,12 +279,19 @@ def run_single(args):
             synth.fill_hash_torch(t, i)
     for s, ids in zip(w.src, tabs):
         eng.cache.reserve(s, ids)
-    state = {"reqs": [(i, T, s, ids, d) for i, (T, s, d, ids) in enumerate(zip(w.T, w.src, w.dst, tabs))]}
+    reqs0 = [(i, T, s, ids, d, None, None) for i, (T, s, d, ids) in enumerate(zip(w.T, w.src, w.dst, tabs))]
+    rank_ids = {}
+    if args.rank_ids == "suggest":  # N2: one assignment per destination group (R19)
+        for grp in sorted(set(tuple(d) for d in w.dst)):
+            if grp[1] > 1:
+                rank_ids[grp] = F.kv_suggest_rank_ids(eng.cache, reqs0, grp)
+        reqs0 = [r[:6] + (rank_ids.get(tuple(r[4])),) for r in reqs0]
+    state = {"reqs": reqs0}
     stream = eng.stream
 
     def flipped(reqs, plan):
         new = plan.dst_tables()
-        return [(rid, T, d, t, s) for (rid, T, s, _, d), t in zip(reqs, new)]
+        return [(rid, T, d, t, s, drid, srid) for (rid, T, s, _, d, srid, drid), t in zip(reqs, new)]
 
     ev_pairs = []      # per step: [(e0, e1) per wave] around the reshard launches
     step_stats = []    # per step: summed plan statistics over its waves
@@ -331,6 +340,9 @@ def run_single(args):
                 step()
             torch.cuda.synchronize()
             return 0
+        p0_ = eng.plan(state["reqs"][:waves_of(state["reqs"])[0][1]])
+        fwd_matrix = p0_.stats()[1]
+        p0_.destroy()
         clk = ClockSampler(torch.cuda.current_device(), args.clock_ms).start()
         stats = None
         for _ in range(max(args.warmup, 1)):
@@ -405,6 +417,19 @@ def run_single(args):
     algo_bytes = sum((x["n_atoms"] + x["n_atom_writes"]) * x["atom_bytes"] for x in step_stats) / len(step_stats)
     hbm_peak, peak_src = peaks()
     achieved = algo_bytes / (kmean / 1e3) / 1e9
+    # What the same plan would be bound by if the virtual ranks were real
+    # GPUs on NVSwitch: SURVEY 8(d) t_min from the forward plan's byte matrix
+    # (a model, not a measurement).
+    modeled = None
+    if w.n_gpus > 1:
+        t_min, eg, ing, hb = nvlink_roofline(fwd_matrix, hbm_peak)
+        off = fwd_matrix.sum() - np.trace(fwd_matrix)
+        modeled = {"n_gpus": w.n_gpus, "t_min_ms": round(t_min * 1e3, 3),
+                   "max_egress_GB": round(float(eg.max()) / 1e9, 3), "max_ingress_GB": round(float(ing.max()) / 1e9, 3),
+                   "local_fraction": round(float(np.trace(fwd_matrix) / max(fwd_matrix.sum(), 1)), 4),
+                   "rank_ids": args.rank_ids, "link_GBps": FALLBACK_NVLINK_GBS,
+                   "note": "model of an N-GPU run from the plan's byte matrix, not measured"}
+        del off
     traffic = None
     tpath = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.config}.json")
     if os.path.exists(tpath):
@@ -432,6 +457,7 @@ def run_single(args):
                    "step": "plan + descriptor upload + reshard + remap (alternating direction)"},
         "switch_latency_ms": round(total_ms / args.steps, 4),
         "reshard_kernel_ms": round(kmean, 4),
+        "modeled_nvlink": modeled,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                      "frac": round(achieved / hbm_peak, 4), "traffic": traffic, "peak_source": peak_src,
                      "kernel": "flykv_reshard_kernel", "algorithmic_bytes_per_launch": int(algo_bytes)},
@@ -491,7 +517,12 @@ def run_multi(args):
     for s_, ids in zip(w.src, tabs):
         cache.reserve(s_, ids)
     stream = torch.cuda.Stream(dev)
-    state = {"reqs": [(i, T, s_, ids, d) for i, (T, s_, d, ids) in enumerate(zip(w.T, w.src, w.dst, tabs))]}
+    reqs0 = [(i, T, s_, ids, d, None, None) for i, (T, s_, d, ids) in enumerate(zip(w.T, w.src, w.dst, tabs))]
+    if args.rank_ids == "suggest":  # N2 (R19): identical on every rank (deterministic)
+        rank_ids = {grp: F.kv_suggest_rank_ids(cache, reqs0, grp) for grp in sorted(set(tuple(d) for d in w.dst))
+                    if grp[1] > 1}
+        reqs0 = [r[:6] + (rank_ids.get(tuple(r[4])),) for r in reqs0]
+    state = {"reqs": reqs0}
     ev_pairs = []
     world_key = tuple(range(world))
 
@@ -527,7 +558,8 @@ def run_multi(args):
             stream.synchronize()
             host_bytes = sum(int(x.numel()) * 4 for x in h)
         new = plan.dst_tables()
-        state["reqs"] = [(rid, T, d, t, s_) for (rid, T, s_, _, d), t in zip(state["reqs"], new)]
+        state["reqs"] = [(rid, T, d, t, s_, drid, srid)
+                         for (rid, T, s_, _, d, srid, drid), t in zip(state["reqs"], new)]
         return plan, host_bytes
 
     plan0 = F.kv_plan_switch(cache, state["reqs"])
