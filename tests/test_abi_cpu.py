@@ -309,3 +309,22 @@ def test_rank_ids_plan_and_suggestion():
     with pytest.raises(F.FlyKVError) as e:
         c.plan_switch([reqs[0] + (None, [0, 1, 2, 3, 4, 5, 6, 6])])
     assert e.value.name == "KV_ERR_INVALID_ARG"
+
+
+def test_plan_state_machine():
+    """kv_plan_commit releases sources once (idempotent); a committed plan
+    refuses kv_reshard (its sources may be reused, BAD_STATE) and destroy
+    keeps the destination allocation."""
+    c = fake_cache((1, 4, 8, 4, 2), [32, 32])
+    a = c.alloc((0, 1), 3)
+    plan = c.plan_switch([(1, 12, (0, 1), a, (0, 2))])
+    held_planned = [c.held_mask(g).sum() for g in (0, 1)]
+    plan.commit()
+    plan.commit()
+    assert [c.held_mask(g).sum() for g in (0, 1)] == [held_planned[0] - 3, held_planned[1]]
+    with pytest.raises(F.FlyKVError) as e:
+        F.kv_reshard(plan, -1)
+    assert e.value.name == "KV_ERR_BAD_STATE"
+    dst = plan.dst_tables()[0]
+    plan.destroy()
+    assert all(c.held_mask(g)[dst].all() for g in (0, 1))
