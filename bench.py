@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--frag", type=float, default=1.25, help="source placement window / source need")
     ap.add_argument("--pool-slack", type=float, default=1.05, help="pool room beyond the window / max need")
+    ap.add_argument("--placement", default="fragmented", choices=["fragmented", "contiguous"],
+                    help="source block placement: seeded permutation (default) or ascending IDs")
     ap.add_argument("--waves", action="store_true", help="memory-bounded waves (kv_plan_waves) per switch")
     ap.add_argument("--rank-ids", default="identity", choices=["identity", "suggest"],
                     help="destination rank-ID assignment (P:291): identity (R3) or kv_suggest_rank_ids (N2)")
@@ -191,14 +193,14 @@ def build_workload(args, world: int, rank: int):
     return w
 
 
-def pools_and_tables(w, frag: float = 1.25, slack: float = 1.05):
+def pools_and_tables(w, frag: float = 1.25, slack: float = 1.05, contiguous: bool = False):
     """Pool sizes + fragmented source tables; block counts from the product's
     own kv_blocks_for (Eq.2)."""
     from paper_2602_22593_b200 import flykv as F
     g = F.geometry(w.L, w.H, w.d, w.B, w.e)
     n0 = [F.kv_blocks_for(g, T, s[1]) for T, s in zip(w.T, w.src)]
     n1 = [F.kv_blocks_for(g, T, d[1]) for T, d in zip(w.T, w.dst)]
-    return synth.realistic_pools(w, n0, n1, frag=frag, slack=slack)
+    return synth.realistic_pools(w, n0, n1, frag=frag, slack=slack, contiguous=contiguous)
 
 
 # --------------------------------------------------------------- reference arm
@@ -272,7 +274,7 @@ def run_single(args):
     torch.cuda.set_device(dev)
     w = build_workload(args, 1, 0)
     g = F.geometry(w.L, w.H, w.d, w.B, w.e)
-    nb, tabs = pools_and_tables(w, args.frag, args.pool_slack)
+    nb, tabs = pools_and_tables(w, args.frag, args.pool_slack, args.placement == "contiguous")
     eng = KVSwitchEngine(g, nb, dev, tp_degrees=(2, 4, 8))
     if not args.no_fill:
         for i, t in enumerate(eng.pools.tensors):
@@ -450,6 +452,7 @@ def run_single(args):
                    "layers": w.L, "kv_heads": w.H, "head_dim": w.d, "block_base": w.B, "requests": len(w.T),
                    "tokens": w.tokens(), "payload_bytes_per_step": int(payload),
                    "payload_bytes_forward": stats["payload_bytes"],
+                   "placement": args.placement,
                    "waves_per_switch": (round(sum(n_waves) / len(n_waves), 2) if args.waves else 1),
                    "pool_bytes": int(eng.pools.nbytes()),
                    "l2": ("L2 flushed between steps (512 MiB rewrite, outside the step events)" if flush is not None

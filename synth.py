@@ -151,7 +151,8 @@ def pool_blocks(w: Workload, slack: float = 1.10, extra: int = 8) -> list:
     return [int(n * slack) + extra for n in need]
 
 
-def source_tables(w: Workload, counts: list, num_blocks: list, seed: int = 1, window=None) -> list:
+def source_tables(w: Workload, counts: list, num_blocks: list, seed: int = 1, window=None,
+                  contiguous: bool = False) -> list:
     """Fragmented source tables: per source group a seeded permutation of the
     IDs [0, window) (default: the whole pool), consumed in request order,
     skipping IDs already used on any member GPU (groups may overlap).
@@ -167,7 +168,7 @@ def source_tables(w: Workload, counts: list, num_blocks: list, seed: int = 1, wi
             nb = min(num_blocks[g] for g in members)
             if window is not None:
                 nb = min(nb, int(window))
-            perms[grp] = rng.permutation(nb).astype(np.int32)
+            perms[grp] = (np.arange(nb, dtype=np.int32) if contiguous else rng.permutation(nb).astype(np.int32))
             cursor[grp] = 0
         perm, c = perms[grp], cursor[grp]
         ids = []
@@ -186,7 +187,7 @@ def source_tables(w: Workload, counts: list, num_blocks: list, seed: int = 1, wi
 
 
 def realistic_pools(w: Workload, n_src: list, n_dst: list, frag: float = 1.25, slack: float = 1.05,
-                    seed: int = 1):
+                    seed: int = 1, contiguous: bool = False):
     """Equal-sized pools and fragmented source tables for the benches.
 
     Each live engine's blocks are scattered (seeded permutation) over the low
@@ -205,7 +206,7 @@ def realistic_pools(w: Workload, n_src: list, n_dst: list, frag: float = 1.25, s
     window = int(frag * max(src_need)) + 16
     nb_all = window + int(slack * max(max(dst_need), max(src_need))) + 32
     nb = [nb_all] * w.n_gpus
-    return nb, source_tables(w, n_src, nb, seed=seed, window=window)
+    return nb, source_tables(w, n_src, nb, seed=seed, window=window, contiguous=contiguous)
 
 
 # ------------------------------------------------------------ content hashing
