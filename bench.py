@@ -28,6 +28,7 @@ the same workload.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -43,6 +44,7 @@ import numpy as np  # noqa: E402
 
 import synth  # noqa: E402
 
+DEBUG = bool(os.environ.get("FLYKV_BENCH_DEBUG"))
 FALLBACK_HBM_GBS = 6650.0       # B200_PROFILING.md fallback (copy), "of fallback"
 FALLBACK_NVLINK_GBS = 770.0     # measured peer copy per direction (B200_PROFILING.md)
 
@@ -307,9 +309,12 @@ def run_single(args):
         reqs = state["reqs"]
         new_reqs, pairs, agg, host = [], [], None, {}
         ws = waves_of(reqs)
+        dbg = [time.perf_counter()] if read_back and DEBUG else None
         for a, b in ws:
             plan = eng.plan(reqs[a:b])
+            dbg is not None and dbg.append(time.perf_counter())
             plan.upload(stream)
+            dbg is not None and dbg.append(time.perf_counter())
             st_, _ = plan.stats()
             agg = dict(st_) if agg is None else {k: (agg[k] if k == "atom_bytes" else agg[k] + st_[k]) for k in agg}
             if timed_kernel:
@@ -319,17 +324,27 @@ def run_single(args):
             if timed_kernel:
                 e1.record(stream)
                 pairs.append((e0, e1))
+            dbg is not None and dbg.append(time.perf_counter())
             tables = eng.alloc_tables(plan, range(eng.n_gpus))
+            dbg is not None and dbg.append(time.perf_counter())
             for gg, t in tables.items():
                 F.kv_remap_block_tables(plan, gg, t.req_ptr, t.block_ids, t.meta, stream)
+            dbg is not None and dbg.append(time.perf_counter())
             if read_back:
                 for gg, t in tables.items():
                     n_res, n_ids = plan.resident(gg)
                     host[(a, gg)] = (t.req_ptr.to("cpu", non_blocking=True),
                                      t.block_ids[:n_ids].to("cpu", non_blocking=True),
                                      t.meta[:n_res].to("cpu", non_blocking=True))
+            dbg is not None and dbg.append(time.perf_counter())
             new_reqs += flipped(reqs[a:b], plan)
+            dbg is not None and dbg.append(time.perf_counter())
         state["reqs"] = new_reqs
+        if dbg is not None:
+            d = [(y - x) * 1e3 for x, y in zip(dbg, dbg[1:])]
+            if sum(d) > 3:
+                sys.stderr.write("slow enqueue: plan %.2f upload %.2f stats+reshard %.2f alloc %.2f remap %.2f d2h %.2f "
+                                 "flip %.2f\n" % tuple(d))
         if timed_kernel:
             ev_pairs.append(pairs)
             step_stats.append(agg)
@@ -360,6 +375,8 @@ def run_single(args):
         n_launch0 = F.launch_count()
         step_ev = []
         torch.cuda.synchronize()
+        gc.collect()
+        gc.disable()   # no collector pauses inside the timed regions
         clk.begin()
         plans = []
         for _ in range(args.steps):
@@ -384,16 +401,25 @@ def run_single(args):
             h2d = d2h = 0
             e2e_payload = 0
             plan_ms = []
+            enq_ms = []
             for it in range(args.steps):
                 t0 = time.perf_counter()
                 st_, host = step(read_back=True)     # plan(s), upload, reshard, remap, tables -> host
+                te = time.perf_counter()
                 stream.synchronize()
                 t1 = time.perf_counter()
+                if DEBUG and (t1 - te) * 1e3 > 8:
+                    sys.stderr.write("slow sync: %.2f ms\n" % ((t1 - te) * 1e3))
                 lat_ms.append((t1 - t0) * 1e3)
+                enq_ms.append((te - t0) * 1e3)
                 h2d += st_["h2d_bytes"]
                 e2e_payload += st_["payload_bytes"]
                 d2h += sum(int(x.numel()) * 4 for v in host.values() for x in v)
                 plan_ms.append(0.0)
+            gc.enable()
+            if os.environ.get("FLYKV_BENCH_DEBUG"):
+                sys.stderr.write("e2e per-step ms: " + " ".join(f"{x:.2f}" for x in lat_ms) + "\n")
+                sys.stderr.write("e2e enqueue ms: " + " ".join(f"{x:.2f}" for x in enq_ms) + "\n")
             # host planning time alone (kv_plan_switch), measured on plans that are then abandoned
             for it in range(min(args.steps, 10)):
                 reqs = state["reqs"]
@@ -405,6 +431,7 @@ def run_single(args):
             plan_ms = plan_ms[:min(args.steps, 10)]
             e2e = {"value": round(e2e_payload / (sum(lat_ms) / 1e3) / 1e9, 3), "unit": "GB/s",
                    "h2d_bytes_per_step": int(h2d // len(lat_ms)), "d2h_bytes_per_step": int(d2h // len(lat_ms)),
+                   "value_at_p50": round(e2e_payload / len(lat_ms) / (statistics.median(lat_ms) / 1e3) / 1e9, 3),
                    "switch_latency_ms_p50": round(statistics.median(lat_ms), 3),
                    "switch_latency_ms_p99": round(float(np.percentile(lat_ms, 99)), 3),
                    "host_plan_ms_p50": round(statistics.median(plan_ms), 3)}

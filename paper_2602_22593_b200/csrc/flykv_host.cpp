@@ -67,6 +67,10 @@ struct kv_cache {
     // device copy of layer_base (uploaded once per device)
     int dev = -1;
     char** d_layer_base = nullptr;
+    // stream-ordered pool for plan workspaces; keeps its memory across
+    // synchronizations (release threshold = max) so a switch never waits on
+    // the driver re-mapping freed workspace memory
+    cudaMemPool_t pool = nullptr;
     // pinned staging for descriptor uploads, guarded by an event
     void* stage = nullptr;
     size_t stage_bytes = 0;
@@ -230,6 +234,7 @@ extern "C" void kv_cache_destroy(kv_cache* c) {
     }
     if (c->stage) cudaFreeHost(c->stage);
     if (c->d_layer_base) cudaFree(c->d_layer_base);
+    if (c->pool) cudaMemPoolDestroy(c->pool);
     delete c;
 }
 
@@ -585,6 +590,17 @@ static kv_status ensure_device(kv_plan* p, cudaStream_t stream) {
         const size_t nbytes = c->layer_base.size() * sizeof(void*);
         CUDA_TRY(cudaMalloc(&c->d_layer_base, nbytes));
         CUDA_TRY(cudaMemcpy(c->d_layer_base, c->layer_base.data(), nbytes, cudaMemcpyHostToDevice));
+        if (c->pool) {
+            cudaMemPoolDestroy(c->pool);
+            c->pool = nullptr;
+        }
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        CUDA_TRY(cudaMemPoolCreate(&c->pool, &props));
+        uint64_t keep = UINT64_MAX;
+        CUDA_TRY(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &keep));
         c->dev = dev;
     }
     if (p->dbuf) {
@@ -610,7 +626,7 @@ static kv_status ensure_device(kv_plan* p, cudaStream_t stream) {
     if (!p->segs.empty()) std::memcpy(h + p->off_segs, p->segs.data(), p->segs.size() * sizeof(Seg));
     if (!p->tables.empty()) std::memcpy(h + p->off_tables, p->tables.data(), p->tables.size() * sizeof(int32_t));
     if (!p->recs.empty()) std::memcpy(h + p->off_recs, p->recs.data(), p->recs.size() * sizeof(ReqRec));
-    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&p->dbuf), p->dbytes, stream));
+    CUDA_TRY(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&p->dbuf), p->dbytes, c->pool, stream));
     CUDA_TRY(cudaMemcpyAsync(p->dbuf, h, p->dbytes, cudaMemcpyHostToDevice, stream));
     CUDA_TRY(cudaEventRecord(c->stage_ev, stream));
     c->stage_pending = true;

@@ -13,6 +13,8 @@
 //   flykv_gather_kernel   a8 test utility: materialise a weight shard view.
 //
 // Layout terms: see include/flykv.h and flykv_internal.h.
+#include <cstdlib>
+
 #include "flykv_internal.h"
 
 namespace flykv {
@@ -138,39 +140,36 @@ __device__ __forceinline__ char* replica_ptr(const ReshardArgs& a, int64_t atom,
 // destination replica.  VPL = 0: generic atoms (multiple of 16 bytes).
 // U = atoms per warp iteration: the loads of U atoms (U * 8 LDG.128 per
 // lane for 4 KiB atoms) are in flight before their stores are issued.
+// Number of steps of round R for this warp (atoms R + k*nwarps + warp < hi).
+__device__ __forceinline__ int round_len(const ReshardArgs& a, int64_t R, int64_t warp, int64_t nwarps) {
+    const int64_t first = R + warp;
+    if (first >= a.atom_hi) return 0;
+    const int64_t span = (a.atom_hi - first + nwarps - 1) / nwarps;
+    return span < 32 ? (int)span : 32;
+}
+
 template <int VPL, int U>
-__global__ void __launch_bounds__(256, ((U == 1 && VPL <= 8) ? 4 : 2)) flykv_reshard_kernel(const ReshardArgs a) {
+__global__ void __launch_bounds__(256, 2) flykv_reshard_kernel(const ReshardArgs a) {
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    // Round r covers atoms [R, R + 32*nwarps); step k of every warp touches
+    // Round R covers atoms [R, R + 32*nwarps); step k of every warp touches
     // atom R + k*nwarps + warp, so at any moment the whole grid works on one
     // window of nwarps consecutive atoms (~19 MB): few DRAM pages open at
     // once (measured +5-9% over warp-contiguous chunks, scripts/microbench.cu).
-    for (int64_t R = a.atom_lo; R < a.atom_hi; R += 32 * nwarps) {
-        const int64_t first = R + warp;
-        if (first >= a.atom_hi) break;
-        const int64_t span = (a.atom_hi - first + nwarps - 1) / nwarps;
-        const int n = span < 32 ? (int)span : 32;
+    if constexpr (VPL > 0 && U > 1) {
+        // Software-pipelined decode: the next round's addresses are decoded
+        // right after the first loads of this round are issued, so the
+        // decode's dependent-load chain overlaps with bytes in flight.
+        int64_t R = a.atom_lo;
+        int n = round_len(a, R, warp, nwarps);
         LaneAtom la;
-        if (lane < n) lane_decode(a, first + lane * nwarps, la);
-        if constexpr (VPL > 0 && U == 1) {
-            for (int k = 0; k < n; ++k) {
-                const int4* src = reinterpret_cast<const int4*>(shfl_ptr(la.src, k)) + lane;
-                int4* dst = reinterpret_cast<int4*>(shfl_ptr(la.dst0, k)) + lane;
-                const int rep = __shfl_sync(0xffffffffu, la.rep1, k);
-                int4 v[VPL];
-#pragma unroll
-                for (int i = 0; i < VPL; ++i) v[i] = ld_stream(src + i * 32);
-#pragma unroll
-                for (int i = 0; i < VPL; ++i) st_stream(dst + i * 32, v[i]);
-                for (int j = 1; j < rep; ++j) {
-                    int4* dj = reinterpret_cast<int4*>(replica_ptr(a, first + k * nwarps, j)) + lane;
-#pragma unroll
-                    for (int i = 0; i < VPL; ++i) st_stream(dj + i * 32, v[i]);
-                }
-            }
-        } else if constexpr (VPL > 0) {
+        if (lane < n) lane_decode(a, R + warp + lane * nwarps, la);
+        while (n > 0) {
+            const int64_t first = R + warp;
+            const int64_t Rn = R + 32 * nwarps;
+            const int nn = round_len(a, Rn, warp, nwarps);
+            LaneAtom nx;
             for (int k0 = 0; k0 < n; k0 += U) {
                 int4 v[U][VPL];
                 const char* s[U];
@@ -189,6 +188,7 @@ __global__ void __launch_bounds__(256, ((U == 1 && VPL <= 8) ? 4 : 2)) flykv_res
 #pragma unroll
                     for (int i = 0; i < VPL; ++i) v[u][i] = ld_stream(src + i * 32);
                 }
+                if (k0 == 0 && lane < nn) lane_decode(a, Rn + warp + lane * nwarps, nx);
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     for (int j = 0; j < rep[u]; ++j) {
@@ -200,16 +200,44 @@ __global__ void __launch_bounds__(256, ((U == 1 && VPL <= 8) ? 4 : 2)) flykv_res
                     }
                 }
             }
-        } else {
-            for (int k = 0; k < n; ++k) {
-                const char* s = shfl_ptr(la.src, k);
-                char* d0 = shfl_ptr(la.dst0, k);
-                const int rep = __shfl_sync(0xffffffffu, la.rep1, k);
-                const int nv = a.atom_bytes >> 4;
-                for (int j = 0; j < rep; ++j) {
-                    char* dj = j == 0 ? d0 : replica_ptr(a, first + k * nwarps, j);
-                    for (int i = lane; i < nv; i += 32)
-                        st_stream(reinterpret_cast<int4*>(dj) + i, ld_stream(reinterpret_cast<const int4*>(s) + i));
+            la = nx;
+            R = Rn;
+            n = nn;
+        }
+    } else {
+        for (int64_t R = a.atom_lo; R < a.atom_hi; R += 32 * nwarps) {
+            const int64_t first = R + warp;
+            const int n = round_len(a, R, warp, nwarps);
+            if (n == 0) break;
+            LaneAtom la;
+            if (lane < n) lane_decode(a, first + lane * nwarps, la);
+            if constexpr (VPL > 0) {
+                for (int k = 0; k < n; ++k) {
+                    const int4* src = reinterpret_cast<const int4*>(shfl_ptr(la.src, k)) + lane;
+                    int4* dst = reinterpret_cast<int4*>(shfl_ptr(la.dst0, k)) + lane;
+                    const int rep = __shfl_sync(0xffffffffu, la.rep1, k);
+                    int4 v[VPL];
+#pragma unroll
+                    for (int i = 0; i < VPL; ++i) v[i] = ld_stream(src + i * 32);
+#pragma unroll
+                    for (int i = 0; i < VPL; ++i) st_stream(dst + i * 32, v[i]);
+                    for (int j = 1; j < rep; ++j) {
+                        int4* dj = reinterpret_cast<int4*>(replica_ptr(a, first + k * nwarps, j)) + lane;
+#pragma unroll
+                        for (int i = 0; i < VPL; ++i) st_stream(dj + i * 32, v[i]);
+                    }
+                }
+            } else {
+                for (int k = 0; k < n; ++k) {
+                    const char* s = shfl_ptr(la.src, k);
+                    char* d0 = shfl_ptr(la.dst0, k);
+                    const int rep = __shfl_sync(0xffffffffu, la.rep1, k);
+                    const int nv = a.atom_bytes >> 4;
+                    for (int j = 0; j < rep; ++j) {
+                        char* dj = j == 0 ? d0 : replica_ptr(a, first + k * nwarps, j);
+                        for (int i = lane; i < nv; i += 32)
+                            st_stream(reinterpret_cast<int4*>(dj) + i, ld_stream(reinterpret_cast<const int4*>(s) + i));
+                    }
                 }
             }
         }
@@ -320,10 +348,13 @@ __global__ void __launch_bounds__(128) flykv_reshard_tma_kernel(const ReshardArg
 // ---------------------------------------------------------------- launch
 static int g_impl = 0;          // 0 auto, 1 LDG, 2 TMA
 static int g_ctas_per_sm = 0;   // 0 auto
+static int g_threads = 0;       // threads per CTA of the LDG kernel, 0 = default (experiment knob: FLYKV_THREADS)
 
 void set_reshard_impl(int impl, int ctas_per_sm) {
     g_impl = impl;
     g_ctas_per_sm = ctas_per_sm;
+    const char* t = getenv("FLYKV_THREADS");
+    if (t && atoi(t) >= 32 && atoi(t) <= 256 && atoi(t) % 32 == 0) g_threads = atoi(t);
 }
 
 static int sm_count_of(int device) {
@@ -343,16 +374,19 @@ static cudaError_t launch_ldg(const ReshardArgs& a, int device, cudaStream_t s) 
         per_sm = nb > 0 ? nb : 1;
     }
     const int64_t atoms = a.atom_hi - a.atom_lo;
-    // ~64 KiB of loads in flight per SM (U=1: 2 CTAs = 16 warps x 4 KiB;
-    // U=2: 1 CTA = 8 warps x 8 KiB): more concurrent streams cost DRAM row
-    // locality (measured, scripts/microbench.cu and scripts/variants.py)
+    // Bytes in flight per SM are the tuning parameter: more concurrent
+    // streams cost DRAM row locality, fewer starve the memory system.  The
+    // measured optimum is 6 warps x 8 KiB = 48 KiB per SM (U=2: one 192-thread
+    // CTA per SM: 6.45-6.59 TB/s on C2/C4, vs 6.26-6.30 with 8 warps and
+    // 5.9 with 4; scripts/variants.py).  U=1: two 256-thread CTAs.
     const int want_per = U == 1 ? 2 : 1;
     const int per = g_ctas_per_sm > 0 ? g_ctas_per_sm : (per_sm < want_per ? per_sm : want_per);
-    int64_t want = (atoms + 8 * 32 - 1) / (8 * 32);
+    const int threads = g_threads > 0 ? g_threads : (U == 1 ? 256 : 192);
+    int64_t want = (atoms + (threads / 32) * 32 - 1) / ((threads / 32) * 32);
     int64_t cap = (int64_t)sm_count_of(device) * per;
     int grid = (int)(want < cap ? want : cap);
     if (grid < 1) grid = 1;
-    flykv_reshard_kernel<VPL, U><<<grid, 256, 0, s>>>(a);
+    flykv_reshard_kernel<VPL, U><<<grid, threads, 0, s>>>(a);
     return cudaGetLastError();
 }
 
