@@ -664,6 +664,8 @@ extern "C" kv_status kv_reshard(kv_plan* p, int32_t gpu, void* stream_) {
     a.M = c->M;
     a.fence_sys = gpu >= 0 ? 1 : 0;
     a.peer = gpu >= 0 ? 1 : 0;
+    a.max_rep = 1;
+    for (int32_t k = a.seg_lo; k < a.seg_hi; ++k) a.max_rep = std::max(a.max_rep, p->segs[k].rep1);
     if (a.atom_hi <= a.atom_lo) return KV_OK;
     cudaError_t e = launch_reshard(a, p->dev, stream);
     if (e != cudaSuccess) return cuda_fail(e, "flykv_reshard_kernel launch");
@@ -693,6 +695,8 @@ extern "C" kv_status kv_reshard_staged(kv_plan* p, int32_t gpu, void* staging, i
     a.atom_bytes = (int32_t)c->atom_bytes;
     a.M = c->M;
     a.peer = 1;  // LDG/STG path
+    a.max_rep = 1;
+    for (int32_t k = a.seg_lo; k < a.seg_hi; ++k) a.max_rep = std::max(a.max_rep, p->segs[k].rep1);
     a.staged = mode;
     a.staging = static_cast<char*>(staging);
     if ((a.atom_hi - a.atom_lo) * c->atom_bytes > staging_bytes)

@@ -76,6 +76,7 @@ struct ReshardArgs {
     int64_t M;                 // block bytes per layer
     int32_t fence_sys;         // 1: release-fence writes at system scope (peer pools)
     int32_t peer;              // 1: destinations may be peer (NVLink) mappings -> LDG/STG path
+    int32_t max_rep;           // largest destination replica count in the range (launch shape)
     int32_t staged;            // comparator only: 0 fused, 1 pack into staging, 2 unpack from staging
     char* staging;             // atom (i - atom_lo) at staging + (i - atom_lo) * atom_bytes
 };

@@ -381,7 +381,9 @@ static cudaError_t launch_ldg(const ReshardArgs& a, int device, cudaStream_t s) 
     // 5.9 with 4; scripts/variants.py).  U=1: two 256-thread CTAs.
     const int want_per = U == 1 ? 2 : 1;
     const int per = g_ctas_per_sm > 0 ? g_ctas_per_sm : (per_sm < want_per ? per_sm : want_per);
-    const int threads = g_threads > 0 ? g_threads : (U == 1 ? 256 : 192);
+    // GQA replication (p/H copies per read) is write-heavy and prefers 8 warps
+    // (measured: H_kv=4/1 at TP8 6.12/6.00 TB/s with 8 warps vs 6.06/<6 with 6).
+    const int threads = g_threads > 0 ? g_threads : ((U == 1 || a.max_rep > 1) ? 256 : 192);
     int64_t want = (atoms + (threads / 32) * 32 - 1) / ((threads / 32) * 32);
     int64_t cap = (int64_t)sm_count_of(device) * per;
     int grid = (int)(want < cap ? want : cap);
