@@ -22,7 +22,12 @@ def main():
     eng = KVSwitchEngine(g, nb, "cuda:0")
     for s_, ids in zip(w.src, tabs):
         eng.cache.reserve(s_, ids)
-    plan = eng.plan([(i, T, s_, ids, d) for i, (T, s_, d, ids) in enumerate(zip(w.T, w.src, w.dst, tabs))])
+    reqs = [(i, T, s_, ids, d) for i, (T, s_, d, ids) in enumerate(zip(w.T, w.src, w.dst, tabs))]
+    if os.environ.get("REVERSE"):  # measure the backward direction: commit the forward switch first
+        p_, _, _ = eng.switch(reqs, read_back=True)
+        reqs = [(i, T, d, t, s_) for (i, T, s_, _, d), t in zip(reqs, p_.dst_tables())]
+        del p_
+    plan = eng.plan(reqs)
     st, _ = plan.stats()
     algo = (st["n_atoms"] + st["n_atom_writes"]) * st["atom_bytes"]
     stream = eng.stream
