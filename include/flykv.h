@@ -99,6 +99,9 @@ typedef struct {
     int64_t payload_bytes;  /* n_atom_writes * atom_bytes                   */
     int64_t h2d_bytes;      /* descriptor bytes uploaded per plan           */
     int64_t n_segments;     /* (request, source GPU) work segments          */
+    int64_t n_atom_slots;   /* work slots of the kernels incl. holes of the
+                               destination-major order (>= n_atoms); the
+                               staging size of kv_reshard_staged           */
 } kv_plan_stats;
 
 /* ---------------------------------------------------------------- cache */
@@ -190,7 +193,8 @@ kv_status kv_plan_upload(kv_plan* plan, void* stream);
  * ranks on one B200).  An atom (request, layer, K/V, head, chunk of B
  * tokens) is B*d*e contiguous bytes in every degree's layout; it is read
  * once and written to each destination replica (1, or p/H under GQA
- * replication, R2), local or over NVLink peer mappings.  Idempotent until
+ * replication, R2), local or over NVLink peer mappings; atoms are visited in
+ * destination-major order so destination blocks are written sequentially.  Idempotent until
  * the plan is committed.  The caller must order kv_remap_block_tables after
  * every GPU's reshard has completed (stream order, or a group barrier, a5).
  * Current device must be the one that can address the pools.
@@ -201,7 +205,7 @@ kv_status kv_reshard(kv_plan* plan, int32_t gpu, void* stream);
  * passes through a staging buffer, as a pack -> all-to-all -> unpack
  * implementation would do.  mode 1 packs every atom of the range (source
  * replica) into staging[(i - first) * B*d*e]; mode 2 unpacks staging to
- * every destination replica.  staging: device, >= atoms * B*d*e bytes. */
+ * every destination replica.  staging: device, >= n_atom_slots * B*d*e bytes. */
 kv_status kv_reshard_staged(kv_plan* plan, int32_t gpu, void* staging, int64_t staging_bytes, int32_t mode,
                             void* stream);
 

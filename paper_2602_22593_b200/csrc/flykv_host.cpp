@@ -480,7 +480,7 @@ extern "C" kv_status kv_plan_switch(kv_cache* c, const kv_request* reqs, int32_t
         if (!q.moving) continue;
         const int32_t C = (int32_t)ceil_div(q.T, B);
         if (C == 0) continue;
-        if ((int64_t)L * 2 * C * H >= ((int64_t)1 << 31)) {  // per-segment atom index is 32-bit on the device
+        if ((int64_t)L * 2 * (C + H) * H >= ((int64_t)1 << 31)) {  // per-segment slot index is 32-bit on the device
             for (int32_t j = 0; j < n_reqs; ++j) {
                 const ReqPlan& u = p->reqs[j];
                 if (!u.moving) continue;
@@ -501,6 +501,7 @@ extern "C" kv_status kv_plan_switch(kv_cache* c, const kv_request* reqs, int32_t
             s.src_gpu = q.src.first_gpu + m;
             s.dst_g0 = q.dst.first_gpu;
             s.C = C;
+            s.J1 = (int32_t)ceil_div(C, l1.k);
             s.nh = l0.hloc;
             s.h0 = first_head_of_rank(l0, rid);
             s.dst_inv = dst_inv_off[i];
@@ -526,11 +527,13 @@ extern "C" kv_status kv_plan_switch(kv_cache* c, const kv_request* reqs, int32_t
     p->seg_begin.resize(segs.size() + 1);
     p->gpu_seg_lo.assign(n, 0);
     p->gpu_seg_hi.assign(n, 0);
-    int64_t acc = 0, writes = 0;
+    int64_t acc = 0, atoms = 0, writes = 0;
     for (size_t s = 0; s < segs.size(); ++s) {
         p->seg_begin[s] = acc;
-        const int64_t a = (int64_t)L * 2 * segs[s].C * segs[s].nh;
-        acc += a;
+        const int64_t slots = (int64_t)L * 2 * segs[s].J1 * segs[s].nh * segs[s].k1;  // incl. holes
+        const int64_t a = (int64_t)L * 2 * segs[s].C * segs[s].nh;                     // real atoms
+        acc += slots;
+        atoms += a;
         writes += a * segs[s].rep1;
     }
     p->seg_begin[segs.size()] = acc;
@@ -566,7 +569,8 @@ extern "C" kv_status kv_plan_switch(kv_cache* c, const kv_request* reqs, int32_t
 
     p->st.n_requests = n_reqs;
     p->st.n_moving = n_moving;
-    p->st.n_atoms = acc;
+    p->st.n_atoms = atoms;
+    p->st.n_atom_slots = acc;
     p->st.n_atom_writes = writes;
     p->st.atom_bytes = c->atom_bytes;
     p->st.payload_bytes = writes * c->atom_bytes;

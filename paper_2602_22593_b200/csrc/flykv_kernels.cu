@@ -57,13 +57,27 @@ __device__ __forceinline__ int find_seg(const int64_t* __restrict__ seg_begin, i
 __device__ __forceinline__ void decode(const ReshardArgs& a, int64_t atom, int s, AtomAddr& out) {
     const Seg sg = a.segs[s];
     uint32_t local = (uint32_t)(atom - __ldg(a.seg_begin + s));
-    uint32_t nh = (uint32_t)sg.nh, C = (uint32_t)sg.C;
-    uint32_t hh = local % nh;
+    const uint32_t nh = (uint32_t)sg.nh, k1 = (uint32_t)sg.k1, J1 = (uint32_t)sg.J1;
+    const uint32_t w = local % k1;        // (((l*2 + kv)*J1 + j)*nh + hh)*k1 + w
+    local /= k1;
+    const uint32_t hh = local % nh;
     local /= nh;
-    const uint32_t c = local % C;  // ((l*2 + kv)*C + c)*nh + hh
-    const uint32_t lkv = local / C;
+    const uint32_t jb = local % J1;
+    const uint32_t lkv = local / J1;
     const uint32_t kv = lkv & 1u, l = lkv >> 1;
+    const uint32_t c = jb * k1 + w;
     int32_t h = sg.h0 + (int32_t)hh;
+    if (c >= (uint32_t)sg.C) {  // hole past the request's last chunk
+        out.src = nullptr;
+        out.doff = 0;
+        out.l = (int32_t)l;
+        out.h = h;
+        out.dst_g0 = sg.dst_g0;
+        out.rep1 = 0;
+        out.hloc1 = sg.hloc1;
+        out.dst_inv = sg.dst_inv;
+        return;
+    }
     const int64_t half = a.M >> 1;
     const int64_t ab = a.atom_bytes;
     // source replica (lowest owner, R10): block tab0[c / k0], chunk c % k0
@@ -107,9 +121,9 @@ __device__ __forceinline__ void lane_decode(const ReshardArgs& a, int64_t atom, 
     AtomAddr ad;
     decode(a, atom, s, ad);
     la.src = ad.src;
-    la.rep1 = ad.rep1;
-    la.dst0 = dst_ptr(a, ad, 0);
-    if (a.staged) {  // bench comparator: pack (source -> staging) or unpack (staging -> destinations)
+    la.rep1 = ad.rep1;  // 0 for a hole: nothing is read or written
+    la.dst0 = ad.src ? dst_ptr(a, ad, 0) : nullptr;
+    if (a.staged && la.rep1 > 0) {  // bench comparator: pack (source -> staging) or unpack (staging -> destinations)
         char* slot = a.staging + (atom - a.atom_lo) * (int64_t)a.atom_bytes;
         if (a.staged == 1) {
             la.dst0 = slot;
@@ -184,6 +198,7 @@ __global__ void __launch_bounds__(256, 2) flykv_reshard_kernel(const ReshardArgs
                 }
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
+                    if (rep[u] == 0) continue;  // hole or past the round (warp-uniform)
                     const int4* src = reinterpret_cast<const int4*>(s[u]) + lane;
 #pragma unroll
                     for (int i = 0; i < VPL; ++i) v[u][i] = ld_stream(src + i * 32);
@@ -216,6 +231,7 @@ __global__ void __launch_bounds__(256, 2) flykv_reshard_kernel(const ReshardArgs
                     const int4* src = reinterpret_cast<const int4*>(shfl_ptr(la.src, k)) + lane;
                     int4* dst = reinterpret_cast<int4*>(shfl_ptr(la.dst0, k)) + lane;
                     const int rep = __shfl_sync(0xffffffffu, la.rep1, k);
+                    if (rep == 0) continue;  // hole (warp-uniform)
                     int4 v[VPL];
 #pragma unroll
                     for (int i = 0; i < VPL; ++i) v[i] = ld_stream(src + i * 32);
@@ -315,6 +331,7 @@ __global__ void __launch_bounds__(128) flykv_reshard_tma_kernel(const ReshardArg
             const char* s = shfl_ptr(la.src, k);
             char* d0 = shfl_ptr(la.dst0, k);
             const int rep = __shfl_sync(0xffffffffu, la.rep1, k);
+            if (rep == 0) continue;  // hole (warp-uniform)
             if (lane == 0) {
                 if (issued >= (uint32_t)D) store_one(stored++);
                 const int st = issued % S;

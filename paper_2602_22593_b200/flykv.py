@@ -66,7 +66,7 @@ class Request(C.Structure):
 
 class PlanStats(C.Structure):
     _fields_ = [(n, C.c_int64) for n in ("n_requests", "n_moving", "n_atoms", "n_atom_writes", "atom_bytes",
-                                         "payload_bytes", "h2d_bytes", "n_segments")]
+                                         "payload_bytes", "h2d_bytes", "n_segments", "n_atom_slots")]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}

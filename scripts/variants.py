@@ -62,7 +62,7 @@ def main():
     F.set_reshard_impl(0, 0)
     # comparator: the same re-layout through a staging buffer (pack, then
     # unpack) -- what pack -> all-to-all -> unpack costs in HBM alone
-    stg = torch.empty(st["n_atoms"] * st["atom_bytes"], dtype=torch.uint8, device="cuda:0")
+    stg = torch.empty(st["n_atom_slots"] * st["atom_bytes"], dtype=torch.uint8, device="cuda:0")
     ms = timeit(lambda: (F.kv_reshard_staged(plan, -1, stg, stg.numel(), 1, stream),
                          F.kv_reshard_staged(plan, -1, stg, stg.numel(), 2, stream)))
     res["staged_pack_unpack"] = {"ms": ms, "GBps_of_fused_bytes": algo / ms / 1e6}

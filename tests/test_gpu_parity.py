@@ -65,7 +65,7 @@ def run_parity(geo, nb, spec, seed=0, per_gpu_launch=False, check_pools=True, st
     tables = eng.alloc_tables(plan, range(len(nb)))
     if staged:  # comparator path: pack -> staging -> unpack
         st_, _ = plan.stats()
-        stg = torch.empty(max(st_["n_atoms"] * st_["atom_bytes"], 16), dtype=torch.uint8, device="cuda:0")
+        stg = torch.empty(max(st_["n_atom_slots"] * st_["atom_bytes"], 16), dtype=torch.uint8, device="cuda:0")
         F.kv_reshard_staged(plan, -1, stg, stg.numel(), 1, eng.stream)
         F.kv_reshard_staged(plan, -1, stg, stg.numel(), 2, eng.stream)
         for gpu, t in tables.items():
