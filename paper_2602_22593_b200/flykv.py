@@ -314,29 +314,76 @@ class Plan:
         return st.as_dict(), mat.reshape(n, n)
 
 
+# numpy twin of the kv_request struct (offsets checked against ctypes below),
+# so request lists are marshalled with a few vectorised column writes
+_REQ_DTYPE = np.dtype({
+    "names": ["req_id", "num_tokens", "src_g0", "src_p", "src_blocks", "n_src_blocks", "dst_g0", "dst_p",
+              "src_rank_ids", "dst_rank_ids"],
+    "formats": [np.int64, np.int32, np.int32, np.int32, np.uint64, np.int32, np.int32, np.int32, np.uint64,
+                np.uint64],
+    "offsets": [Request.req_id.offset, Request.num_tokens.offset, Request.src.offset, Request.src.offset + 4,
+                Request.src_blocks.offset, Request.n_src_blocks.offset, Request.dst.offset, Request.dst.offset + 4,
+                Request.src_rank_ids.offset, Request.dst_rank_ids.offset],
+    "itemsize": C.sizeof(Request)})
+
+
+class _ReqArray:
+    """A marshalled request list: .ptr (kv_request*), .n, plus keep-alive."""
+
+    def __init__(self, reqs):
+        reqs = list(reqs)
+        self.n = len(reqs)
+        self.buf = np.zeros(max(self.n, 1), dtype=_REQ_DTYPE)
+        self.keep = []
+        if self.n == 0:
+            self.ptr = C.cast(self.buf.ctypes.data, C.POINTER(Request))
+            return
+        tabs = []
+        for r in reqs:
+            a = r[3]
+            if not (isinstance(a, np.ndarray) and a.dtype == np.int32 and a.flags.c_contiguous and a.ndim == 1):
+                a = _i32(a)
+            tabs.append(a)
+        self.keep = tabs
+        b = self.buf
+        b["req_id"] = [r[0] for r in reqs]
+        b["num_tokens"] = [r[1] for r in reqs]
+        b["src_g0"] = [r[2][0] for r in reqs]
+        b["src_p"] = [r[2][1] for r in reqs]
+        b["dst_g0"] = [r[4][0] for r in reqs]
+        b["dst_p"] = [r[4][1] for r in reqs]
+        b["src_blocks"] = [a.ctypes.data if a.size else 0 for a in tabs]
+        b["n_src_blocks"] = [a.size for a in tabs]
+        for col, k in (("src_rank_ids", 5), ("dst_rank_ids", 6)):
+            ptrs = []
+            for r in reqs:
+                x = r[k] if len(r) > k else None
+                if x is None:
+                    ptrs.append(0)
+                else:
+                    xa = _i32(x)
+                    self.keep.append(xa)
+                    ptrs.append(xa.ctypes.data)
+            b[col] = ptrs
+        self.ptr = C.cast(b.ctypes.data, C.POINTER(Request))
+
+
 def make_requests(reqs):
     """reqs: iterable of (req_id, num_tokens, (g0, p0), src_ids, (g1, p1)
     [, src_rank_ids [, dst_rank_ids]]) -- rank IDs None = identity.
-    Returns (ctypes array, keep-alive list of the block tables)."""
-    reqs = list(reqs)
-    arr = (Request * max(len(reqs), 1))()
-    keep, extra = [], []
-    for i, r in enumerate(reqs):
-        rid, T, src, ids, dst = r[:5]
-        a = _i32(ids)
-        keep.append(a)
-        rids = []
-        for x in (r[5] if len(r) > 5 else None, r[6] if len(r) > 6 else None):
-            if x is None:
-                rids.append(None)
-            else:
-                b = _i32(x)
-                extra.append(b)
-                rids.append(b.ctypes.data_as(_I32P))
-        arr[i] = Request(int(rid), int(T), Group(*src), a.ctypes.data_as(_I32P), a.size, Group(*dst),
-                         rids[0], rids[1])
-    arr._keep_extra = extra
-    return arr, keep
+    Returns (kv_request* pointer, keep-alive list with one entry per request)."""
+    ra = _ReqArray(reqs)
+    keep = list(ra.keep[:ra.n])
+    keep_all = [ra]
+    return ra.ptr, _Keep(keep, keep_all)
+
+
+class _Keep(list):
+    """List of per-request tables that also pins the marshalled buffer."""
+
+    def __init__(self, items, extra):
+        super().__init__(items)
+        self._extra = extra
 
 
 def kv_plan_switch(cache: KVCache, requests) -> Plan:
