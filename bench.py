@@ -630,7 +630,10 @@ def run_multi(args):
     red = torch.tensor([my_ms, my_kern, max(lat) if lat else 0.0, (sum(lat) / len(lat)) if lat else 0.0,
                         float(launches)], dtype=torch.float64, device=dev if nccl else "cpu")
     dist.all_reduce(red, op=dist.ReduceOp.MAX)
-    total_ms, kern_ms, _, lat_mean, launches_max = [float(x) for x in red.tolist()]
+    total_ms, kern_ms, _, lat_mean, _ = [float(x) for x in red.tolist()]
+    n_l = torch.tensor([float(launches)], dtype=torch.float64, device=dev if nccl else "cpu")
+    dist.all_reduce(n_l, op=dist.ReduceOp.SUM)   # every rank's kernels count toward the job
+    launches_all = int(n_l.item())
     comm.close_pools(imported)
     if rank == 0:
         payload_sum = sum(x[0]["payload_bytes"] for x in step_stats)
@@ -672,7 +675,7 @@ def run_multi(args):
                      "h2d_bytes_per_step": int(h2d // max(len(lat), 1)),
                      "d2h_bytes_per_step": int(d2h // max(len(lat), 1)),
                      "switch_latency_ms_mean_max_over_ranks": round(lat_mean, 3)} if lat else None),
-            "gpu_launches": int(launches_max),
+            "gpu_launches": launches_all,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
