@@ -487,6 +487,8 @@ def run_single(args):
                    "step": "plan + descriptor upload + reshard + remap (alternating direction)"},
         "switch_latency_ms": round(total_ms / args.steps, 4),
         "reshard_kernel_ms": round(kmean, 4),
+        "reshard_kernel_ms_p50_p90": [round(float(np.percentile(kern_ms, 50)), 4),
+                                      round(float(np.percentile(kern_ms, 90)), 4)],
         "modeled_nvlink": modeled,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                      "frac": round(achieved / hbm_peak, 4), "traffic": traffic, "peak_source": peak_src,
