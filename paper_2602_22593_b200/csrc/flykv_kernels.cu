@@ -396,11 +396,16 @@ static cudaError_t launch_ldg(const ReshardArgs& a, int device, cudaStream_t s) 
     // measured optimum is 6 warps x 8 KiB = 48 KiB per SM (U=2: one 192-thread
     // CTA per SM: 6.45-6.59 TB/s on C2/C4, vs 6.26-6.30 with 8 warps and
     // 5.9 with 4; scripts/variants.py).  U=1: two 256-thread CTAs.
-    const int want_per = U == 1 ? 2 : 1;
+    // GQA replication (p/H copies per read) is write-heavy and wants more
+    // warps: 8 for 2-4 replicas, 10 for 8 (measured forward TP8: H_kv=4 6.12
+    // TB/s with 8 warps vs 6.06 with 6; H_kv=1 5.94 with 10 vs 5.47 with 8).
+    int want_per = U == 1 ? 2 : 1, want_threads = U == 1 ? 256 : 192;
+    if (U > 1 && a.max_rep > 1) {
+        want_threads = a.max_rep >= 8 ? 160 : 256;
+        want_per = a.max_rep >= 8 ? 2 : 1;
+    }
     const int per = g_ctas_per_sm > 0 ? g_ctas_per_sm : (per_sm < want_per ? per_sm : want_per);
-    // GQA replication (p/H copies per read) is write-heavy and prefers 8 warps
-    // (measured: H_kv=4/1 at TP8 6.12/6.00 TB/s with 8 warps vs 6.06/<6 with 6).
-    const int threads = g_threads > 0 ? g_threads : ((U == 1 || a.max_rep > 1) ? 256 : 192);
+    const int threads = g_threads > 0 ? g_threads : want_threads;
     int64_t want = (atoms + (threads / 32) * 32 - 1) / ((threads / 32) * 32);
     int64_t cap = (int64_t)sm_count_of(device) * per;
     int grid = (int)(want < cap ? want : cap);
