@@ -325,17 +325,12 @@ def run_single(args):
                 e1.record(stream)
                 pairs.append((e0, e1))
             dbg is not None and dbg.append(time.perf_counter())
-            tables = eng.alloc_tables(plan, range(eng.n_gpus))
+            views, packed = eng.alloc_packed(plan)            # every pool's table, one launch
             dbg is not None and dbg.append(time.perf_counter())
-            for gg, t in tables.items():
-                F.kv_remap_block_tables(plan, gg, t.req_ptr, t.block_ids, t.meta, stream)
+            F.kv_remap_block_tables(plan, -1, packed[0], packed[1], packed[2], stream)
             dbg is not None and dbg.append(time.perf_counter())
-            if read_back:
-                for gg, t in tables.items():
-                    n_res, n_ids = plan.resident(gg)
-                    host[(a, gg)] = (t.req_ptr.to("cpu", non_blocking=True),
-                                     t.block_ids[:n_ids].to("cpu", non_blocking=True),
-                                     t.meta[:n_res].to("cpu", non_blocking=True))
+            if read_back:                                     # three D2H copies for all pools
+                host[a] = tuple(x.to("cpu", non_blocking=True) for x in packed)
             dbg is not None and dbg.append(time.perf_counter())
             new_reqs += flipped(reqs[a:b], plan)
             dbg is not None and dbg.append(time.perf_counter())

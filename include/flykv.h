@@ -210,9 +210,9 @@ kv_status kv_reshard_staged(kv_plan* plan, int32_t gpu, void* staging, int64_t s
                             void* stream);
 
 /* Sizes of pool gpu's table after the switch: *n_resident requests resident
- * on gpu (dst group contains gpu), *n_ids block IDs in their tables.  The
- * per_req_meta first head of kv_remap_block_tables follows the request's
- * dst_rank_ids. */
+ * on gpu (dst group contains gpu), *n_ids block IDs in their tables; gpu ==
+ * -1 gives the totals over all pools.  The per_req_meta first head of
+ * kv_remap_block_tables follows the request's dst_rank_ids. */
 kv_status kv_plan_resident(const kv_plan* plan, int32_t gpu, int32_t* n_resident, int32_t* n_ids);
 
 /*
@@ -224,6 +224,11 @@ kv_status kv_plan_resident(const kv_plan* plan, int32_t gpu, int32_t* n_resident
  *   per_req_meta  device int32 [4 * n_resident]  {plan request index, B(p),
  *                 H_loc(p), first head held by gpu} = the per-request
  *                 "stride and capacity" the attention kernel needs
+ * gpu == -1 (all pools addressable from the current device): one launch
+ * writes every pool's table into packed outputs, pool g's slice starting at
+ * req_ptr + sum_{g'<g}(n_res[g'] + 1), block_ids + sum_{g'<g} n_ids[g'],
+ * per_req_meta + 4 * sum_{g'<g} n_res[g'] (sizes from kv_plan_resident;
+ * req_ptr then holds n_resident_total + n_gpus entries).
  * The first call on a plan (any gpu) commits it on the host: every moving
  * request's source IDs are released on its source GPUs (sources are freed
  * only after the group barrier, R13).  Requests absent from the plan are not

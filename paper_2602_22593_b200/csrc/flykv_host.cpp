@@ -103,11 +103,12 @@ struct kv_plan {
     std::vector<int32_t> n_res, n_res_ids;
     std::vector<ReqRec> recs;
     kv_plan_stats st{};
-    // device workspace: [seg_begin | segs | tables | recs]
+    std::vector<int32_t> out_off;  // [n_gpus][3] packed all-GPU remap output offsets
+    // device workspace: [seg_begin | segs | tables | recs | out_off]
     int dev = -1;
     char* dbuf = nullptr;
     size_t dbytes = 0;
-    size_t off_seg_begin = 0, off_segs = 0, off_tables = 0, off_recs = 0;
+    size_t off_seg_begin = 0, off_segs = 0, off_tables = 0, off_recs = 0, off_outs = 0;
     cudaStream_t last_stream = nullptr;
 };
 
@@ -565,7 +566,16 @@ extern "C" kv_status kv_plan_switch(kv_cache* c, const kv_request* reqs, int32_t
     p->off_segs = align(p->off_seg_begin + p->seg_begin.size() * sizeof(int64_t));
     p->off_tables = align(p->off_segs + p->segs.size() * sizeof(Seg));
     p->off_recs = align(p->off_tables + p->tables.size() * sizeof(int32_t));
-    p->dbytes = align(p->off_recs + p->recs.size() * sizeof(ReqRec));
+    p->out_off.assign((size_t)n * 3, 0);
+    for (int32_t g = 0, r0 = 0, i0 = 0; g < n; ++g) {  // packed outputs of kv_remap_block_tables(gpu = -1)
+        p->out_off[3 * g + 0] = r0 + g;  // req_ptr rows: n_res[g] + 1 each
+        p->out_off[3 * g + 1] = i0;
+        p->out_off[3 * g + 2] = 4 * r0;
+        r0 += p->n_res[g];
+        i0 += p->n_res_ids[g];
+    }
+    p->off_outs = align(p->off_recs + p->recs.size() * sizeof(ReqRec));
+    p->dbytes = align(p->off_outs + p->out_off.size() * sizeof(int32_t));
 
     p->st.n_requests = n_reqs;
     p->st.n_moving = n_moving;
@@ -630,6 +640,7 @@ static kv_status ensure_device(kv_plan* p, cudaStream_t stream) {
     if (!p->segs.empty()) std::memcpy(h + p->off_segs, p->segs.data(), p->segs.size() * sizeof(Seg));
     if (!p->tables.empty()) std::memcpy(h + p->off_tables, p->tables.data(), p->tables.size() * sizeof(int32_t));
     if (!p->recs.empty()) std::memcpy(h + p->off_recs, p->recs.data(), p->recs.size() * sizeof(ReqRec));
+    std::memcpy(h + p->off_outs, p->out_off.data(), p->out_off.size() * sizeof(int32_t));
     CUDA_TRY(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&p->dbuf), p->dbytes, c->pool, stream));
     CUDA_TRY(cudaMemcpyAsync(p->dbuf, h, p->dbytes, cudaMemcpyHostToDevice, stream));
     CUDA_TRY(cudaEventRecord(c->stage_ev, stream));
@@ -714,7 +725,17 @@ extern "C" kv_status kv_reshard_staged(kv_plan* p, int32_t gpu, void* staging, i
 }
 
 extern "C" kv_status kv_plan_resident(const kv_plan* p, int32_t gpu, int32_t* n_resident, int32_t* n_ids) {
-    if (!p || gpu < 0 || gpu >= p->c->n_gpus) return fail(KV_ERR_INVALID_ARG, "bad arguments");
+    if (!p || gpu < -1 || gpu >= p->c->n_gpus) return fail(KV_ERR_INVALID_ARG, "bad arguments");
+    if (gpu < 0) {  // totals over every pool (packed all-GPU outputs)
+        int32_t a = 0, b = 0;
+        for (int32_t g = 0; g < p->c->n_gpus; ++g) {
+            a += p->n_res[g];
+            b += p->n_res_ids[g];
+        }
+        if (n_resident) *n_resident = a;
+        if (n_ids) *n_ids = b;
+        return KV_OK;
+    }
     if (n_resident) *n_resident = p->n_res[gpu];
     if (n_ids) *n_ids = p->n_res_ids[gpu];
     return KV_OK;
@@ -850,8 +871,10 @@ extern "C" kv_status kv_remap_block_tables(kv_plan* p, int32_t gpu, int32_t* req
                                            int32_t* per_req_meta, void* stream_) {
     if (!p) return fail(KV_ERR_INVALID_ARG, "plan is NULL");
     kv_cache* c = p->c;
-    if (gpu < 0 || gpu >= c->n_gpus) return fail(KV_ERR_INVALID_ARG, "gpu %d out of range", gpu);
-    if (!req_ptr || (p->n_res[gpu] > 0 && (!per_req_meta || (p->n_res_ids[gpu] > 0 && !block_ids))))
+    if (gpu < -1 || gpu >= c->n_gpus) return fail(KV_ERR_INVALID_ARG, "gpu %d out of range", gpu);
+    int32_t n_res = 0, n_ids = 0;
+    kv_plan_resident(p, gpu, &n_res, &n_ids);
+    if (!req_ptr || (n_res > 0 && (!per_req_meta || (n_ids > 0 && !block_ids))))
         return fail(KV_ERR_INVALID_ARG, "NULL output buffer");
     cudaStream_t stream = static_cast<cudaStream_t>(stream_);
     kv_status s = ensure_device(p, stream);
@@ -861,6 +884,7 @@ extern "C" kv_status kv_remap_block_tables(kv_plan* p, int32_t gpu, int32_t* req
     RemapArgs a{};
     a.reqs = reinterpret_cast<const ReqRec*>(p->dbuf + p->off_recs);
     a.tables = reinterpret_cast<const int32_t*>(p->dbuf + p->off_tables);
+    a.out_off = gpu < 0 ? reinterpret_cast<const int32_t*>(p->dbuf + p->off_outs) : nullptr;
     a.n_reqs = (int32_t)p->reqs.size();
     a.gpu = gpu;
     a.H = c->geo.num_kv_heads;
@@ -868,7 +892,7 @@ extern "C" kv_status kv_remap_block_tables(kv_plan* p, int32_t gpu, int32_t* req
     a.req_ptr = req_ptr;
     a.block_ids = block_ids;
     a.meta = per_req_meta;
-    cudaError_t e = launch_remap(a, stream);
+    cudaError_t e = launch_remap(a, gpu < 0 ? c->n_gpus : 1, stream);
     if (e != cudaSuccess) return cuda_fail(e, "flykv_remap_kernel launch");
     g_launches.fetch_add(1);
     return KV_OK;

@@ -89,8 +89,9 @@ struct ReshardArgs {
 struct RemapArgs {
     const ReqRec* reqs;  // [n_reqs]
     const int32_t* tables;
+    const int32_t* out_off;  // all-GPU mode: [n_gpus][3] offsets of each GPU's req_ptr / block_ids / meta; else null
     int32_t n_reqs;
-    int32_t gpu;
+    int32_t gpu;             // single-GPU mode: the pool; all-GPU mode: blockIdx.x is the pool
     int32_t H;
     int32_t B;
     int32_t* req_ptr;
@@ -121,7 +122,7 @@ struct DecodeArgs {
 // Kernel launchers (flykv_kernels.cu, flykv_decode.cu).  Return cudaSuccess or the launch error.
 cudaError_t launch_reshard(const ReshardArgs& a, int device, cudaStream_t s);
 void set_reshard_impl(int impl, int ctas_per_sm);
-cudaError_t launch_remap(const RemapArgs& a, cudaStream_t s);
+cudaError_t launch_remap(const RemapArgs& a, int n_ctas, cudaStream_t s);
 cudaError_t launch_gather(const GatherSeg* segs, int n_seg, char* dst, cudaStream_t s);
 cudaError_t launch_decode(const DecodeArgs& a, cudaStream_t s);
 

@@ -469,6 +469,11 @@ __global__ void __launch_bounds__(1024) flykv_remap_kernel(const RemapArgs a) {
     __shared__ int32_t wf[32], wc[32];
     __shared__ int32_t carry_f, carry_c;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    // all-GPU mode: CTA g writes pool g's table into its slice of packed outputs
+    const int32_t gpu = a.out_off ? (int32_t)blockIdx.x : a.gpu;
+    int32_t* req_ptr = a.req_ptr + (a.out_off ? a.out_off[3 * gpu + 0] : 0);
+    int32_t* block_ids = a.block_ids + (a.out_off ? a.out_off[3 * gpu + 1] : 0);
+    int32_t* meta = a.meta + (a.out_off ? a.out_off[3 * gpu + 2] : 0);
     if (tid == 0) { carry_f = 0; carry_c = 0; }
     __syncthreads();
     for (int base = 0; base < a.n_reqs; base += 1024) {
@@ -477,7 +482,7 @@ __global__ void __launch_bounds__(1024) flykv_remap_kernel(const RemapArgs a) {
         ReqRec rr = {0, 1, 0, 0};
         if (i < a.n_reqs) {
             rr = a.reqs[i];
-            flag = (a.gpu >= rr.dst_g0 && a.gpu < rr.dst_g0 + rr.dst_p) ? 1 : 0;
+            flag = (gpu >= rr.dst_g0 && gpu < rr.dst_g0 + rr.dst_p) ? 1 : 0;
             cnt = flag ? rr.n1 : 0;
         }
         int32_t f = flag, c = cnt;
@@ -505,30 +510,30 @@ __global__ void __launch_bounds__(1024) flykv_remap_kernel(const RemapArgs a) {
         const int32_t ec = carry_c + (w ? wc[w - 1] : 0) + c - cnt;
         if (flag) {
             Layout L = layout_of(a.H, rr.dst_p);
-            a.req_ptr[ef] = ec;
-            a.meta[4 * ef + 0] = i;
-            a.meta[4 * ef + 1] = a.B * L.k;
-            a.meta[4 * ef + 2] = L.hloc;
-            const int32_t m = a.gpu - rr.dst_g0;
-            a.meta[4 * ef + 3] = first_head_of_rank(L, rr.dst_rid < 0 ? m : a.tables[rr.dst_rid + m]);
+            req_ptr[ef] = ec;
+            meta[4 * ef + 0] = i;
+            meta[4 * ef + 1] = a.B * L.k;
+            meta[4 * ef + 2] = L.hloc;
+            const int32_t m = gpu - rr.dst_g0;
+            meta[4 * ef + 3] = first_head_of_rank(L, rr.dst_rid < 0 ? m : a.tables[rr.dst_rid + m]);
         }
         __syncthreads();
         if (tid == 0) { carry_f += wf[31]; carry_c += wc[31]; }
         __syncthreads();
     }
     const int32_t n_res = carry_f;
-    if (tid == 0) a.req_ptr[n_res] = carry_c;
+    if (tid == 0) req_ptr[n_res] = carry_c;
     __syncthreads();
     for (int r = w; r < n_res; r += 32) {
-        const int32_t i = a.meta[4 * r];
+        const int32_t i = meta[4 * r];
         const ReqRec rr = a.reqs[i];
-        const int32_t start = a.req_ptr[r];
-        for (int k = lane; k < rr.n1; k += 32) a.block_ids[start + k] = a.tables[rr.dst_tab + k];
+        const int32_t start = req_ptr[r];
+        for (int k = lane; k < rr.n1; k += 32) block_ids[start + k] = a.tables[rr.dst_tab + k];
     }
 }
 
-cudaError_t launch_remap(const RemapArgs& a, cudaStream_t s) {
-    flykv_remap_kernel<<<1, 1024, 0, s>>>(a);
+cudaError_t launch_remap(const RemapArgs& a, int n_ctas, cudaStream_t s) {
+    flykv_remap_kernel<<<n_ctas, 1024, 0, s>>>(a);
     return cudaGetLastError();
 }
 

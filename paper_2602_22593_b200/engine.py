@@ -44,6 +44,7 @@ class KVSwitchEngine:
         return flykv.kv_plan_switch(self.cache, requests)
 
     def alloc_tables(self, plan: flykv.Plan, gpus):
+        """Separate per-pool table buffers (for per-pool kv_remap_block_tables calls)."""
         out = {}
         for g in gpus:
             n_res, n_ids = plan.resident(g)
@@ -52,12 +53,35 @@ class KVSwitchEngine:
                               torch.empty((max(n_res, 1), 4), dtype=torch.int32, device=self.device))
         return out
 
+    def alloc_packed(self, plan: flykv.Plan):
+        """Packed all-pool outputs of kv_remap_block_tables(gpu=-1) and the
+        per-pool views into them: {g: GpuTable}, (req_ptr, block_ids, meta)."""
+        n = self.n_gpus
+        res = [plan.resident(g) for g in range(n)]
+        tot_res = sum(r for r, _ in res)
+        tot_ids = sum(i for _, i in res)
+        rp = torch.empty(tot_res + n, dtype=torch.int32, device=self.device)
+        ids = torch.empty(max(tot_ids, 1), dtype=torch.int32, device=self.device)
+        meta = torch.empty((max(tot_res, 1), 4), dtype=torch.int32, device=self.device)
+        views, o_r, o_i = {}, 0, 0
+        for g, (n_res, n_ids) in enumerate(res):
+            views[g] = GpuTable(rp[o_r + g:o_r + g + n_res + 1], ids[o_i:o_i + n_ids], meta[o_r:o_r + n_res])
+            o_r += n_res
+            o_i += n_ids
+        return views, (rp, ids, meta)
+
     def execute(self, plan: flykv.Plan, gpus=None, tables=None):
-        """Reshard every atom (one launch) and remap the tables of `gpus`."""
-        gpus = range(self.n_gpus) if gpus is None else gpus
-        tables = tables if tables is not None else self.alloc_tables(plan, gpus)
+        """Reshard every atom (one launch) and remap the tables: by default
+        all pools in one launch into packed buffers (returns per-pool views);
+        with `tables` (from alloc_tables), one launch per listed pool."""
         with torch.cuda.stream(self.stream):
             flykv.kv_reshard(plan, -1, self.stream)
+            if tables is None and gpus is None:
+                views, (rp, ids, meta) = self.alloc_packed(plan)
+                flykv.kv_remap_block_tables(plan, -1, rp, ids, meta, self.stream)
+                self._packed = (rp, ids, meta)
+                return views
+            tables = tables if tables is not None else self.alloc_tables(plan, gpus)
             for g, t in tables.items():
                 flykv.kv_remap_block_tables(plan, g, t.req_ptr, t.block_ids, t.meta, self.stream)
         return tables
@@ -71,10 +95,21 @@ class KVSwitchEngine:
         if read_back:
             host = {}
             with torch.cuda.stream(self.stream):
-                for g, t in tables.items():
-                    n_res, n_ids = plan.resident(g)
-                    host[g] = (t.req_ptr.to("cpu", non_blocking=True), t.block_ids[:n_ids].to("cpu", non_blocking=True),
-                               t.meta[:n_res].to("cpu", non_blocking=True))
+                if gpus is None:  # packed: three device->host copies for every pool's table
+                    rp, ids, meta = (x.to("cpu", non_blocking=True) for x in self._packed)
+                    self.stream.synchronize()
+                    o_r = o_i = 0
+                    for g in range(self.n_gpus):
+                        n_res, n_ids = plan.resident(g)
+                        host[g] = (rp[o_r + g:o_r + g + n_res + 1], ids[o_i:o_i + n_ids], meta[o_r:o_r + n_res])
+                        o_r += n_res
+                        o_i += n_ids
+                else:
+                    for g, t in tables.items():
+                        n_res, n_ids = plan.resident(g)
+                        host[g] = (t.req_ptr.to("cpu", non_blocking=True),
+                                   t.block_ids[:n_ids].to("cpu", non_blocking=True),
+                                   t.meta[:n_res].to("cpu", non_blocking=True))
             self.stream.synchronize()
         return plan, tables, host
 

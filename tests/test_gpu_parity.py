@@ -62,7 +62,7 @@ def run_parity(geo, nb, spec, seed=0, per_gpu_launch=False, check_pools=True, st
                 hp = host_pools[src[0] + r].reshape(og.L, nb[src[0] + r], M)
                 hp[:, ids] = host_pools[lo].reshape(og.L, nb[lo], M)[:, ids]
     plan = eng.plan(freqs)
-    tables = eng.alloc_tables(plan, range(len(nb)))
+    tables = eng.alloc_tables(plan, range(len(nb))) if (staged or per_gpu_launch) else None
     if staged:  # comparator path: pack -> staging -> unpack
         st_, _ = plan.stats()
         stg = torch.empty(max(st_["n_atom_slots"] * st_["atom_bytes"], 16), dtype=torch.uint8, device="cuda:0")
@@ -75,8 +75,8 @@ def run_parity(geo, nb, spec, seed=0, per_gpu_launch=False, check_pools=True, st
             F.kv_reshard(plan, gpu, eng.stream)
         for gpu, t in tables.items():
             F.kv_remap_block_tables(plan, gpu, t.req_ptr, t.block_ids, t.meta, eng.stream)
-    else:
-        eng.execute(plan, tables=tables)
+    else:  # default: one reshard launch + one packed all-pool remap launch
+        tables = eng.execute(plan)
     torch.cuda.synchronize()
     st, otabs = O.switch(og, host_pools, held, oreqs)
     assert st == 0
