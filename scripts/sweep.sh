@@ -11,3 +11,4 @@ run --config c4gqa1
 run --config c3i --requests 64
 run --config c3ii --requests 64
 run --config c5 --requests 33
+run --config single

@@ -121,6 +121,12 @@ def dp_to_tp(n_gpus: int, n_req: int, L=32, H=8, d=128, B=16, lo=512, hi=4096, s
                     [(i % n_gpus, 1) for i in range(n_req)], [(0, n_gpus)] * n_req)
 
 
+def single_promotion(T: int = 4096) -> Workload:
+    """One live 4K-token request promoted from a DP engine into TP8
+    (Llama-3-70B geometry): the latency-bound end of the switch spectrum."""
+    return Workload(f"llama3-70b single {T}-token DP1->TP8", 80, 8, 128, 16, 2, 8, [T], [(3, 1)], [(0, 8)])
+
+
 WORKLOADS = {
     "tiny": tiny,
     "c2": llama8b_dp4_tp2x2,
@@ -131,6 +137,7 @@ WORKLOADS = {
     "c4gqa4": lambda **kw: llama70b_dp8_tp8(H=4, **kw),
     "c4gqa1": lambda **kw: llama70b_dp8_tp8(H=1, **kw),
     "c5": long_context_tp4_tp8,
+    "single": single_promotion,
 }
 
 
