@@ -525,10 +525,14 @@ def run_multi(args):
     same_dev = os.environ.get("FLYKV_SAME_DEVICE") == "1"   # test mode: all ranks on cuda:0, gloo
     dev = torch.device("cuda", 0 if same_dev else local)
     torch.cuda.set_device(dev)
-    nccl = not same_dev
+    nccl = not same_dev and os.environ.get("FLYKV_BARRIER", "nccl") == "nccl"
     if nccl:
-        dist.init_process_group("nccl", device_id=dev)
-    else:
+        try:
+            dist.init_process_group("nccl", device_id=dev)
+        except Exception as e:  # keep the P2P data path; synchronise through a host (gloo) barrier
+            sys.stderr.write(f"NCCL init failed ({e}); using a gloo host barrier\n")
+            nccl = False
+    if not nccl:
         dist.init_process_group("gloo")
     degrees = [p for p in (2, 4, 8) if p <= world and world % p == 0]
     cpool = comm.CommunicatorPool(world, degrees, backend="nccl" if nccl else "gloo")
