@@ -8,6 +8,7 @@ import re
 import numpy as np
 import pytest
 
+from helpers import oracle_alloc
 from oracle import oracle as O
 from paper_2602_22593_b200 import flykv as F
 
@@ -94,10 +95,8 @@ def test_plan_tables_match_oracle(seed):
     held = [np.zeros(n, dtype=np.uint8) for n in nb]
     oreqs, freqs = [], []
     for i, (T, src, dst) in enumerate(spec):
-        n = F.kv_blocks_for(c.geom, T, src[1])
-        ids = c.alloc(src, n)                 # sources placed by the product allocator
-        for r in range(src[1]):
-            held[src[0] + r][ids] = 1
+        n = O.num_blocks(og, T, src[1])
+        ids = oracle_alloc(c, held, src, n)   # oracle-chosen IDs, checked against kv_alloc
         oreqs.append(O.Req(T, src, list(ids), dst))
         freqs.append((100 + i, T, src, ids, dst))
     for g in range(n_gpus):
@@ -179,8 +178,9 @@ def test_byte_matrix_matches_atom_enumeration():
     c = fake_cache(geo, [128] * n_gpus)
     spec = _random_case(rng, 4, n_gpus, 12, [1, 2, 4, 8], None)
     reqs = []
+    mirror = [np.zeros(128, dtype=np.uint8) for _ in range(n_gpus)]
     for i, (T, src, dst) in enumerate(spec):
-        ids = c.alloc(src, F.kv_blocks_for(c.geom, T, src[1]))
+        ids = oracle_alloc(c, mirror, src, O.num_blocks(og, T, src[1]))
         reqs.append((i, T, src, ids, dst))
     plan = c.plan_switch(reqs)
     st, mat = plan.stats()
@@ -250,8 +250,7 @@ def test_memory_bounded_waves_match_oracle():
     for i in range(24):
         T = int(rng.integers(20, 50))
         src = (i % n_gpus, 1)
-        ids = c.alloc(src, F.kv_blocks_for(c.geom, T, 1))
-        held[src[0]][ids] = 1
+        ids = oracle_alloc(c, held, src, O.num_blocks(og, T, 1))
         reqs.append((i, T, src, ids, (0, 8)))
     with pytest.raises(F.FlyKVError) as e:
         c.plan_switch(reqs)
@@ -287,8 +286,9 @@ def test_rank_ids_plan_and_suggestion():
     og = O.Geom(*geo)
     c = fake_cache(geo, [256] * 8)
     reqs = []
+    mirror = [np.zeros(256, dtype=np.uint8) for _ in range(8)]
     for i, T in enumerate([64, 130, 7]):
-        ids = c.alloc((0, 4), F.kv_blocks_for(c.geom, T, 4))
+        ids = oracle_alloc(c, mirror, (0, 4), O.num_blocks(og, T, 4))
         reqs.append((i, T, (0, 4), ids, (0, 8)))
     sugg = F.kv_suggest_rank_ids(c, reqs, (0, 8))
     assert sorted(sugg) == list(range(8))

@@ -12,6 +12,7 @@ import numpy as np
 import pytest
 
 import synth
+from helpers import oracle_alloc
 from oracle import oracle as O
 
 torch = pytest.importorskip("torch")
@@ -324,8 +325,7 @@ def test_memory_bounded_waves_gpu():
     for i in range(24):
         T = int(rng.integers(80, 200))
         src = (i % 8, 1)
-        ids = eng.cache.alloc(src, F.kv_blocks_for(eng.geom, T, 1))
-        held[src[0]][ids] = 1
+        ids = oracle_alloc(eng.cache, held, src, O.num_blocks(og, T, 1))
         reqs.append((i, T, src, ids, (0, 8)))
     with pytest.raises(F.FlyKVError):
         eng.plan(reqs)
@@ -438,7 +438,8 @@ def test_million_token_request():
     eng = KVSwitchEngine(F.geometry(*geo), nb, "cuda:0")
     for gpu, t in enumerate(eng.pools.tensors):
         synth.fill_hash_torch(t, gpu, seed=5)
-    ids = eng.cache.alloc((0, 1), n0)
+    ids = np.arange(n0, dtype=np.int32)  # an oracle-side table, registered with kv_reserve
+    eng.cache.reserve((0, 1), ids)
     plan, tables, host = eng.switch([(0, T, (0, 1), ids, (0, 8))], read_back=True)
     tab1 = plan.dst_tables()[0]
     sg, so, dg, do = O.atom_map(og, nb, T, (0, 1), ids, (0, 8), tab1)

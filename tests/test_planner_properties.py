@@ -11,6 +11,8 @@ hyp = pytest.importorskip("hypothesis")
 from hypothesis import HealthCheck, given, settings  # noqa: E402
 from hypothesis import strategies as st  # noqa: E402
 
+from helpers import oracle_alloc  # noqa: E402
+from oracle import brute  # noqa: E402
 from oracle import oracle as O  # noqa: E402
 from paper_2602_22593_b200 import flykv as F  # noqa: E402
 
@@ -38,18 +40,15 @@ def test_random_sequences_keep_invariants(H, nb, ops):
     rid = 0
     for kind, T, g1, g2 in ops:
         before = [c.held_mask(x).copy() for x in range(N_GPUS)]
-        if kind == 0:  # admit a request
-            n = F.kv_blocks_for(c.geom, T, g1[1])
-            try:
-                ids = c.alloc(g1, n)
-            except F.FlyKVError as e:
-                assert e.name == "KV_ERR_OUT_OF_BLOCKS"
+        if kind == 0:  # admit a request (oracle-chosen IDs, checked against kv_alloc)
+            n = O.num_blocks(og, T, g1[1])
+            if brute.lowest_common_free(held, g1, n) is None:
+                with pytest.raises(F.FlyKVError) as e:
+                    c.alloc(g1, n)
+                assert e.value.name == "KV_ERR_OUT_OF_BLOCKS"
                 assert all(np.array_equal(c.held_mask(x), before[x]) for x in range(N_GPUS))
                 continue
-            assert len(set(ids.tolist())) == n
-            for r in range(g1[1]):
-                assert not held[g1[0] + r][ids].any()
-                held[g1[0] + r][ids] = 1
+            ids = oracle_alloc(c, held, g1, n)
             live.append((rid, T, g1, ids))
             rid += 1
         elif kind == 1 and live:  # finish a request
