@@ -9,6 +9,7 @@ product never imports this package.
   kv_oracle.c / oracle.py : C re-layout (per-token memcpy) + per-GPU tables
   brute.py                : pure-Python logical-tensor enumerator (tiny cases)
   weights.py              : Eq.1 zero-copy shard views as numpy views
+  attention.py            : single-query softmax attention (consumer proof, N3)
 
 Parity status: every function is pinned by tests/test_oracle.py (see
 DESIGN.md section 5); none is "parity unpinned".

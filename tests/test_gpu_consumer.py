@@ -16,6 +16,7 @@ import pytest
 
 import synth
 from oracle import oracle as O
+from oracle.attention import decode_attention
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -98,9 +99,7 @@ def test_tp_after_relayout_equals_dp(H, Hq, p1, permuted):
                 gpu, off = O.locate(og, src[i][0], 1, tabs0[i], 1, h, t_)
                 base = (1 * nb[gpu] * M + off) // 2
                 V[t_] = bf16_to_f64(host[gpu][base:base + 128])
-            s_ = K @ qf[i, qh] / np.sqrt(128)
-            p_ = np.exp(s_ - s_.max())
-            ref = (p_ / p_.sum()) @ V
+            ref = decode_attention(K, V, qf[i, qh], 1.0 / np.sqrt(128))
             assert np.allclose(out_dp[(i, qh)], ref, rtol=2e-3, atol=2e-3)
     # switch DP -> TP_p1 and decode on every rank with its Eq.1 Q slice
     # rank IDs of the destination members: identity or a permutation;
