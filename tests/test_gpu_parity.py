@@ -184,21 +184,25 @@ def test_round_trip_restores_contents():
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("cfg", ["c2", "c4"])
-def test_full_size_all_atoms(cfg):
-    """BASELINE configs[1] (c2) and configs[3] (c4, Llama-3-70B 8xDP1->TP8) at
-    full size in the bench's launch configuration (virtual ranks on one B200,
-    the bench's pool sizing and placement, one reshard launch): destination tables equal
-    the oracle's allocator in full; EVERY destination atom (4.8M x 4 KiB) equals
-    the content hash of the source position the oracle maps it from; sampled
-    free blocks keep their poison."""
+@pytest.mark.parametrize("cfg,n_req,frag", [("c2", 0, 1.25), ("c4", 0, 1.25), ("c4gqa4", 0, 1.25), ("c4gqa1", 0, 1.25),
+                                            ("c3i", 64, 1.25), ("c3ii", 64, 1.25), ("c5", 0, 1.0), ("single", 0, 1.25)])
+def test_full_size_all_atoms(cfg, n_req, frag):
+    """Every BASELINE config at the size and in the launch configuration the
+    bench times (virtual ranks on one B200, the bench's pool sizing and
+    placement, one reshard launch; config 3 on the bench's 64-request prefix,
+    config 5 in full with `--frag 1.0`): destination tables equal the oracle's
+    allocator in full; EVERY destination atom (up to 13.4M x 4 KiB, all GQA
+    replicas) equals the content hash of the source position the oracle maps
+    it from; sampled free blocks keep their poison."""
     F = _F()
     from paper_2602_22593_b200.engine import KVSwitchEngine
     w = synth.WORKLOADS[cfg]()
+    if n_req:
+        w = synth.Workload(w.name, w.L, w.H, w.d, w.B, w.e, w.n_gpus, w.T[:n_req], w.src[:n_req], w.dst[:n_req])
     og = O.Geom(w.L, w.H, w.d, w.B, w.e)
     n0 = [O.num_blocks(og, T, s[1]) for T, s in zip(w.T, w.src)]
     n1 = [O.num_blocks(og, T, d[1]) for T, d in zip(w.T, w.dst)]
-    nb, tabs0 = synth.realistic_pools(w, n0, n1)
+    nb, tabs0 = synth.realistic_pools(w, n0, n1, frag=frag)
     eng = KVSwitchEngine(F.geometry(w.L, w.H, w.d, w.B, w.e), nb, "cuda:0")
     for gpu, t in enumerate(eng.pools.tensors):
         synth.fill_hash_torch(t, gpu)
