@@ -120,7 +120,10 @@ typedef struct {
  *                   pointers must be dereferenceable from the device that
  *                   later runs kv_reshard (local, same-device virtual ranks,
  *                   or peer/IPC-mapped over NVLink).  May be fake (never
- *                   dereferenced) if kv_reshard is never called.
+ *                   dereferenced) if kv_reshard is never called.  The cache
+ *                   binds to the device current at its first upload; device
+ *                   calls made later from another device fail with
+ *                   KV_ERR_BAD_STATE.
  *   tp_degrees      host [n_degrees], the set P (degree 1 is always legal)
  * All blocks start free.  No CUDA call is made here.
  */
@@ -231,8 +234,11 @@ kv_status kv_plan_resident(const kv_plan* plan, int32_t gpu, int32_t* n_resident
  * req_ptr then holds n_resident_total + n_gpus entries).
  * The first call on a plan (any gpu) commits it on the host: every moving
  * request's source IDs are released on its source GPUs (sources are freed
- * only after the group barrier, R13).  Requests absent from the plan are not
- * listed and are untouched.
+ * only after the group barrier, R13).  The released IDs can be handed out by
+ * the very next kv_alloc / kv_plan_switch, so device work that writes them
+ * (the next plan's reshard) must be ordered after this plan's reshard: the
+ * same stream, or an event the caller records.  Requests absent from the
+ * plan are not listed and are untouched.
  */
 kv_status kv_remap_block_tables(kv_plan* plan, int32_t gpu, int32_t* req_ptr, int32_t* block_ids,
                                 int32_t* per_req_meta, void* stream);

@@ -23,24 +23,27 @@ using namespace flykv;
 static thread_local std::string g_err;
 static std::atomic<int64_t> g_launches{0};
 
-static kv_status fail(kv_status s, const char* fmt, ...) {
+static kv_status vfail(kv_status s, const char* fmt, va_list ap) {
     char buf[512];
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    g_err = buf;
+    return s;
+}
+
+static kv_status fail(kv_status s, const char* fmt, ...) {
     va_list ap;
     va_start(ap, fmt);
-    vsnprintf(buf, sizeof buf, fmt, ap);
+    vfail(s, fmt, ap);
     va_end(ap);
-    g_err = buf;
     return s;
 }
 
 // shared with flykv_vmm.cpp
 kv_status flykv_fail(kv_status s, const char* fmt, ...) {
-    char buf[512];
     va_list ap;
     va_start(ap, fmt);
-    vsnprintf(buf, sizeof buf, fmt, ap);
+    vfail(s, fmt, ap);
     va_end(ap);
-    g_err = buf;
     return s;
 }
 
@@ -596,18 +599,12 @@ static kv_status ensure_device(kv_plan* p, cudaStream_t stream) {
     kv_cache* c = p->c;
     int dev = 0;
     CUDA_TRY(cudaGetDevice(&dev));
-    if (c->dev != dev) {
-        if (c->d_layer_base) {
-            cudaFree(c->d_layer_base);
-            c->d_layer_base = nullptr;
-        }
+    if (c->dev >= 0 && c->dev != dev)  // plans' workspaces live in this device's pool
+        return fail(KV_ERR_BAD_STATE, "cache is bound to device %d, current device is %d", c->dev, dev);
+    if (c->dev < 0) {
         const size_t nbytes = c->layer_base.size() * sizeof(void*);
         CUDA_TRY(cudaMalloc(&c->d_layer_base, nbytes));
         CUDA_TRY(cudaMemcpy(c->d_layer_base, c->layer_base.data(), nbytes, cudaMemcpyHostToDevice));
-        if (c->pool) {
-            cudaMemPoolDestroy(c->pool);
-            c->pool = nullptr;
-        }
         cudaMemPoolProps props{};
         props.allocType = cudaMemAllocationTypePinned;
         props.location.type = cudaMemLocationTypeDevice;
@@ -655,16 +652,10 @@ extern "C" kv_status kv_plan_upload(kv_plan* p, void* stream) {
     return ensure_device(p, static_cast<cudaStream_t>(stream));
 }
 
-extern "C" kv_status kv_reshard(kv_plan* p, int32_t gpu, void* stream_) {
-    if (!p) return fail(KV_ERR_INVALID_ARG, "plan is NULL");
-    if (p->state != PLAN_PLANNED)
-        return fail(KV_ERR_BAD_STATE, "plan already committed; its source blocks may be reused");
-    kv_cache* c = p->c;
-    if (gpu < -1 || gpu >= c->n_gpus) return fail(KV_ERR_INVALID_ARG, "gpu %d out of range", gpu);
-    cudaStream_t stream = static_cast<cudaStream_t>(stream_);
-    kv_status s = ensure_device(p, stream);
-    if (s) return s;
-    p->last_stream = stream;
+// Launch arguments of the reshard kernel for the segments sourced on `gpu`
+// (-1: every segment of the plan).
+static ReshardArgs reshard_args(const kv_plan* p, int32_t gpu) {
+    const kv_cache* c = p->c;
     ReshardArgs a{};
     a.seg_begin = reinterpret_cast<const int64_t*>(p->dbuf + p->off_seg_begin);
     a.segs = reinterpret_cast<const Seg*>(p->dbuf + p->off_segs);
@@ -677,10 +668,25 @@ extern "C" kv_status kv_reshard(kv_plan* p, int32_t gpu, void* stream_) {
     a.L = c->geo.num_layers;
     a.atom_bytes = (int32_t)c->atom_bytes;
     a.M = c->M;
-    a.fence_sys = gpu >= 0 ? 1 : 0;
-    a.peer = gpu >= 0 ? 1 : 0;
     a.max_rep = 1;
     for (int32_t k = a.seg_lo; k < a.seg_hi; ++k) a.max_rep = std::max(a.max_rep, p->segs[k].rep1);
+    return a;
+}
+
+extern "C" kv_status kv_reshard(kv_plan* p, int32_t gpu, void* stream_) {
+    if (!p) return fail(KV_ERR_INVALID_ARG, "plan is NULL");
+    if (p->state != PLAN_PLANNED)
+        return fail(KV_ERR_BAD_STATE, "plan already committed; its source blocks may be reused");
+    if (gpu < -1 || gpu >= p->c->n_gpus) return fail(KV_ERR_INVALID_ARG, "gpu %d out of range", gpu);
+    cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+    kv_status s = ensure_device(p, stream);
+    if (s) return s;
+    p->last_stream = stream;
+    ReshardArgs a = reshard_args(p, gpu);
+    // one GPU's share (one process per GPU): destinations may be peer pools,
+    // released system-wide before the group barrier
+    a.fence_sys = gpu >= 0 ? 1 : 0;
+    a.peer = gpu >= 0 ? 1 : 0;
     if (a.atom_hi <= a.atom_lo) return KV_OK;
     cudaError_t e = launch_reshard(a, p->dev, stream);
     if (e != cudaSuccess) return cuda_fail(e, "flykv_reshard_kernel launch");
@@ -692,31 +698,18 @@ extern "C" kv_status kv_reshard_staged(kv_plan* p, int32_t gpu, void* staging, i
                                        void* stream_) {
     if (!p || !staging || (mode != 1 && mode != 2)) return fail(KV_ERR_INVALID_ARG, "bad kv_reshard_staged arguments");
     if (p->state != PLAN_PLANNED) return fail(KV_ERR_BAD_STATE, "plan already committed");
-    kv_cache* c = p->c;
-    if (gpu < -1 || gpu >= c->n_gpus) return fail(KV_ERR_INVALID_ARG, "gpu %d out of range", gpu);
+    if (gpu < -1 || gpu >= p->c->n_gpus) return fail(KV_ERR_INVALID_ARG, "gpu %d out of range", gpu);
     cudaStream_t stream = static_cast<cudaStream_t>(stream_);
     kv_status s = ensure_device(p, stream);
     if (s) return s;
-    ReshardArgs a{};
-    a.seg_begin = reinterpret_cast<const int64_t*>(p->dbuf + p->off_seg_begin);
-    a.segs = reinterpret_cast<const Seg*>(p->dbuf + p->off_segs);
-    a.tables = reinterpret_cast<const int32_t*>(p->dbuf + p->off_tables);
-    a.layer_base = c->d_layer_base;
-    a.seg_lo = gpu < 0 ? 0 : p->gpu_seg_lo[gpu];
-    a.seg_hi = gpu < 0 ? (int32_t)p->segs.size() : p->gpu_seg_hi[gpu];
-    a.atom_lo = p->seg_begin[a.seg_lo];
-    a.atom_hi = p->seg_begin[a.seg_hi];
-    a.L = c->geo.num_layers;
-    a.atom_bytes = (int32_t)c->atom_bytes;
-    a.M = c->M;
+    p->last_stream = stream;
+    ReshardArgs a = reshard_args(p, gpu);
     a.peer = 1;  // LDG/STG path
-    a.max_rep = 1;
-    for (int32_t k = a.seg_lo; k < a.seg_hi; ++k) a.max_rep = std::max(a.max_rep, p->segs[k].rep1);
     a.staged = mode;
     a.staging = static_cast<char*>(staging);
-    if ((a.atom_hi - a.atom_lo) * c->atom_bytes > staging_bytes)
+    if ((a.atom_hi - a.atom_lo) * p->c->atom_bytes > staging_bytes)
         return fail(KV_ERR_INVALID_ARG, "staging buffer too small: %lld bytes needed",
-                    (long long)((a.atom_hi - a.atom_lo) * c->atom_bytes));
+                    (long long)((a.atom_hi - a.atom_lo) * p->c->atom_bytes));
     if (a.atom_hi <= a.atom_lo) return KV_OK;
     cudaError_t e = launch_reshard(a, p->dev, stream);
     if (e != cudaSuccess) return cuda_fail(e, "flykv_reshard_kernel (staged) launch");
