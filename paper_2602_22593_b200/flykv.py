@@ -338,13 +338,15 @@ class _ReqArray:
         if self.n == 0:
             self.ptr = C.cast(self.buf.ctypes.data, C.POINTER(Request))
             return
-        tabs = []
-        for r in reqs:
-            a = r[3]
-            if not (isinstance(a, np.ndarray) and a.dtype == np.int32 and a.flags.c_contiguous and a.ndim == 1):
-                a = _i32(a)
-            tabs.append(a)
-        self.keep = tabs
+        # all source tables in one contiguous int32 buffer: one pointer fetch,
+        # per-request pointers = base + 4 * offset
+        tabs = [np.asarray(r[3], dtype=np.int32).reshape(-1) for r in reqs]
+        lens = np.fromiter((a.size for a in tabs), dtype=np.int64, count=self.n)
+        cat = np.concatenate(tabs) if lens.sum() else np.zeros(1, dtype=np.int32)
+        self.keep = [cat]
+        base = cat.__array_interface__["data"][0]
+        offs = np.zeros(self.n, dtype=np.int64)
+        np.cumsum(lens[:-1], out=offs[1:])
         b = self.buf
         b["req_id"] = [r[0] for r in reqs]
         b["num_tokens"] = [r[1] for r in reqs]
@@ -352,8 +354,8 @@ class _ReqArray:
         b["src_p"] = [r[2][1] for r in reqs]
         b["dst_g0"] = [r[4][0] for r in reqs]
         b["dst_p"] = [r[4][1] for r in reqs]
-        b["src_blocks"] = [a.ctypes.data if a.size else 0 for a in tabs]
-        b["n_src_blocks"] = [a.size for a in tabs]
+        b["src_blocks"] = np.where(lens > 0, base + 4 * offs, 0).astype(np.uint64)
+        b["n_src_blocks"] = lens
         for col, k in (("src_rank_ids", 5), ("dst_rank_ids", 6)):
             ptrs = []
             for r in reqs:
@@ -368,45 +370,34 @@ class _ReqArray:
         self.ptr = C.cast(b.ctypes.data, C.POINTER(Request))
 
 
-def make_requests(reqs):
+def make_requests(reqs) -> _ReqArray:
     """reqs: iterable of (req_id, num_tokens, (g0, p0), src_ids, (g1, p1)
     [, src_rank_ids [, dst_rank_ids]]) -- rank IDs None = identity.
-    Returns (kv_request* pointer, keep-alive list with one entry per request)."""
-    ra = _ReqArray(reqs)
-    keep = list(ra.keep[:ra.n])
-    keep_all = [ra]
-    return ra.ptr, _Keep(keep, keep_all)
-
-
-class _Keep(list):
-    """List of per-request tables that also pins the marshalled buffer."""
-
-    def __init__(self, items, extra):
-        super().__init__(items)
-        self._extra = extra
+    Returns the marshalled array: .ptr is the kv_request*, .n the count; it
+    owns every buffer the pointers refer to."""
+    return _ReqArray(reqs)
 
 
 def kv_plan_switch(cache: KVCache, requests) -> Plan:
     """Validate, allocate and plan a switch (see include/flykv.h)."""
-    arr, keep = make_requests(requests)
-    n = len(keep)
+    ra = make_requests(requests)
     h = C.c_void_p()
-    _check(_lib.kv_plan_switch(cache._h, arr, n, C.byref(h)))
-    return Plan(cache, h, n)
+    _check(_lib.kv_plan_switch(cache._h, ra.ptr, ra.n, C.byref(h)))
+    return Plan(cache, h, ra.n)
 
 
 def kv_suggest_rank_ids(cache: KVCache, requests, dst) -> list:
     """N2: movement-minimising rank-ID assignment of group dst's members."""
-    arr, keep = make_requests(requests)
+    ra = make_requests(requests)
     out = np.zeros(max(dst[1], 1), dtype=np.int32)
-    _check(_lib.kv_suggest_rank_ids(cache._h, arr, len(keep), Group(*dst), out.ctypes.data_as(_I32P)))
+    _check(_lib.kv_suggest_rank_ids(cache._h, ra.ptr, ra.n, Group(*dst), out.ctypes.data_as(_I32P)))
     return [int(x) for x in out[:dst[1]]]
 
 
 def kv_plan_waves(cache: KVCache, requests, max_wave_bytes: int = 0) -> list:
     """Memory-bounded waves: list of (start, end) request index ranges."""
-    arr, keep = make_requests(requests)
-    n = len(keep)
+    ra = make_requests(requests)
+    arr, n = ra.ptr, ra.n
     ws = np.zeros(n + 2, dtype=np.int32)
     nw = C.c_int32()
     _check(_lib.kv_plan_waves(cache._h, arr, n, int(max_wave_bytes), ws.ctypes.data_as(_I32P), C.byref(nw)))
