@@ -84,6 +84,7 @@ struct ReshardArgs {
     int32_t max_rep;           // largest destination replica count in the range (launch shape)
     int32_t staged;            // comparator only: 0 fused, 1 pack into staging, 2 unpack from staging
     char* staging;             // atom (i - atom_lo) at staging + (i - atom_lo) * atom_bytes
+    int32_t rep_flags;         // GQA replica stores: bit 0 = decode replicas lane-parallel, bit 1 = replica-major order
 };
 
 struct RemapArgs {

@@ -204,14 +204,44 @@ __global__ void __launch_bounds__(256, 2) flykv_reshard_kernel(const ReshardArgs
                     for (int i = 0; i < VPL; ++i) v[u][i] = ld_stream(src + i * 32);
                 }
                 if (k0 == 0 && lane < nn) lane_decode(a, Rn + warp + lane * nwarps, nx);
+                // GQA replicas (p > H): lane j decodes replica j's pointer, all
+                // replicas of an atom in one parallel pass while its loads are
+                // in flight; the stores receive them by shuffle
+                const bool par = a.rep_flags & 1;
+                char* rp[U];
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
-                    for (int j = 0; j < rep[u]; ++j) {
-                        int4* dst = reinterpret_cast<int4*>(
-                                        j == 0 ? d0[u] : replica_ptr(a, first + (int64_t)(k0 + u) * nwarps, j)) +
-                                    lane;
+                    rp[u] = nullptr;
+                    if (par && rep[u] > 1 && lane > 0 && lane < rep[u])
+                        rp[u] = replica_ptr(a, first + (int64_t)(k0 + u) * nwarps, lane);
+                }
+                auto dst_of = [&](int u, int j) -> int4* {
+                    char* dj = j == 0             ? d0[u]
+                               : (par && j < 32) ? shfl_ptr(rp[u], j)
+                                                 : replica_ptr(a, first + (int64_t)(k0 + u) * nwarps, j);
+                    return reinterpret_cast<int4*>(dj) + lane;
+                };
+                if (a.rep_flags & 2) {  // replica-major: replica j of all U atoms, then j + 1
+                    int maxr = 0;
 #pragma unroll
-                        for (int i = 0; i < VPL; ++i) st_stream(dst + i * 32, v[u][i]);
+                    for (int u = 0; u < U; ++u) maxr = rep[u] > maxr ? rep[u] : maxr;
+                    for (int j = 0; j < maxr; ++j) {
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            if (j >= rep[u]) continue;
+                            int4* dst = dst_of(u, j);
+#pragma unroll
+                            for (int i = 0; i < VPL; ++i) st_stream(dst + i * 32, v[u][i]);
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        for (int j = 0; j < rep[u]; ++j) {
+                            int4* dst = dst_of(u, j);
+#pragma unroll
+                            for (int i = 0; i < VPL; ++i) st_stream(dst + i * 32, v[u][i]);
+                        }
                     }
                 }
             }
@@ -367,11 +397,26 @@ static int g_impl = 0;          // 0 auto, 1 LDG, 2 TMA
 static int g_ctas_per_sm = 0;   // 0 auto
 static int g_threads = 0;       // threads per CTA of the LDG kernel, 0 = default (experiment knob: FLYKV_THREADS)
 
-void set_reshard_impl(int impl, int ctas_per_sm) {
-    g_impl = impl;
-    g_ctas_per_sm = ctas_per_sm;
+static int g_rep_flags = -1;    // replica store strategy (ReshardArgs::rep_flags), -1 = default
+
+// Experiment knobs (launch shape and replica strategy sweeps, scripts/): read
+// once from the environment; the defaults are the measured optima.
+static void read_env_knobs() {
+    static bool done = false;
+    if (done) return;
+    done = true;
     const char* t = getenv("FLYKV_THREADS");
     if (t && atoi(t) >= 32 && atoi(t) <= 256 && atoi(t) % 32 == 0) g_threads = atoi(t);
+    const char* c = getenv("FLYKV_CTAS");
+    if (c && atoi(c) >= 1 && atoi(c) <= 8) g_ctas_per_sm = atoi(c);
+    const char* r = getenv("FLYKV_REP_FLAGS");
+    if (r && atoi(r) >= 0 && atoi(r) <= 3) g_rep_flags = atoi(r);
+}
+
+void set_reshard_impl(int impl, int ctas_per_sm) {
+    read_env_knobs();
+    g_impl = impl;
+    g_ctas_per_sm = ctas_per_sm;
 }
 
 static int sm_count_of(int device) {
@@ -382,7 +427,14 @@ static int sm_count_of(int device) {
 }
 
 template <int VPL, int U = 1>
-static cudaError_t launch_ldg(const ReshardArgs& a, int device, cudaStream_t s) {
+static cudaError_t launch_ldg(const ReshardArgs& a_in, int device, cudaStream_t s) {
+    read_env_knobs();
+    ReshardArgs a = a_in;
+    // Replica stores (GQA): with 2-4 replicas the lane-parallel replica
+    // decode is 1.2% faster; with 8 the serial re-decode between replica
+    // stores is 5% faster (spacing the store bursts) -- scripts/gpu_gqa_rep.sh,
+    // profiles/r01_gqa_rep.jsonl.
+    a.rep_flags = g_rep_flags >= 0 ? g_rep_flags : (a.max_rep > 1 && a.max_rep < 8 ? 1 : 0);
     static int per_sm = 0;
     if (per_sm == 0) {
         int nb = 0;
@@ -396,13 +448,14 @@ static cudaError_t launch_ldg(const ReshardArgs& a, int device, cudaStream_t s) 
     // measured optimum is 6 warps x 8 KiB = 48 KiB per SM (U=2: one 192-thread
     // CTA per SM: 6.45-6.59 TB/s on C2/C4, vs 6.26-6.30 with 8 warps and
     // 5.9 with 4; scripts/variants.py).  U=1: two 256-thread CTAs.
-    // GQA replication (p/H copies per read) is write-heavy and wants more
-    // warps: 8 for 2-4 replicas, 10 for 8 (measured forward TP8: H_kv=4 6.12
-    // TB/s with 8 warps vs 6.06 with 6; H_kv=1 5.94 with 10 vs 5.47 with 8).
+    // GQA replication (p/H copies per read) is write-heavy: 8 replicas want
+    // 10 warps per SM (2 x 160 threads; H_kv=1 TP8 5.55 ms vs 5.73-7.2 for
+    // other shapes); 2-4 replicas with lane-parallel replica decode keep the
+    // default 6 warps (H_kv=4 TP8 9.74 ms vs 9.86 with 8 warps).
     int want_per = U == 1 ? 2 : 1, want_threads = U == 1 ? 256 : 192;
-    if (U > 1 && a.max_rep > 1) {
-        want_threads = a.max_rep >= 8 ? 160 : 256;
-        want_per = a.max_rep >= 8 ? 2 : 1;
+    if (U > 1 && a.max_rep >= 8) {
+        want_threads = 160;
+        want_per = 2;
     }
     const int per = g_ctas_per_sm > 0 ? g_ctas_per_sm : (per_sm < want_per ? per_sm : want_per);
     const int threads = g_threads > 0 ? g_threads : want_threads;
