@@ -312,19 +312,18 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         : "memory");
 }
 
-template <int S>
-__global__ void __launch_bounds__(128) flykv_reshard_tma_kernel(const ReshardArgs a, int stage_bytes) {
+template <int S, int W>
+__global__ void __launch_bounds__(W * 32) flykv_reshard_tma_kernel(const ReshardArgs a, int stage_bytes) {
     constexpr int D = S - 2;
     extern __shared__ __align__(128) unsigned char smem[];
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
-    const int nw = blockDim.x >> 5;
     unsigned char* ring = smem + (size_t)wid * S * stage_bytes;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)nw * S * stage_bytes) + wid * S;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)W * S * stage_bytes) + wid * S;
     // per-stage pending store: replica-0 destination, replica count, atom index (lane 0 only)
-    __shared__ char* pend_dst[4][S];
-    __shared__ int32_t pend_rep[4][S];
-    __shared__ int64_t pend_atom[4][S];
+    __shared__ char* pend_dst[W][S];
+    __shared__ int32_t pend_rep[W][S];
+    __shared__ int64_t pend_atom[W][S];
     if (lane == 0) {
         for (int i = 0; i < S; ++i)
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bars + i)));
@@ -334,8 +333,8 @@ __global__ void __launch_bounds__(128) flykv_reshard_tma_kernel(const ReshardArg
     uint64_t policy;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
     const uint32_t bytes = (uint32_t)a.atom_bytes;
-    const int64_t warp = (int64_t)blockIdx.x * nw + wid;
-    const int64_t nwarps = (int64_t)gridDim.x * nw;
+    const int64_t warp = (int64_t)blockIdx.x * W + wid;
+    const int64_t nwarps = (int64_t)gridDim.x * W;
     uint32_t issued = 0, stored = 0;
     auto store_one = [&](uint32_t j) {
         const int st = j % S;
@@ -351,12 +350,13 @@ __global__ void __launch_bounds__(128) flykv_reshard_tma_kernel(const ReshardArg
         }
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     };
-    for (int64_t base = a.atom_lo + warp * 32; base < a.atom_hi; base += nwarps * 32) {
+    // grid-interleaved like the LDG kernel: step k of round R is atom
+    // R + k*nwarps + warp, so the grid sweeps one window of consecutive atoms
+    for (int64_t R = a.atom_lo; R < a.atom_hi; R += 32 * nwarps) {
+        const int n = round_len(a, R, warp, nwarps);
+        if (n == 0) break;
         LaneAtom la;
-        const int64_t mine = base + lane;
-        if (mine < a.atom_hi) lane_decode(a, mine, la);
-        const int64_t left = a.atom_hi - base;
-        const int n = left < 32 ? (int)left : 32;
+        if (lane < n) lane_decode(a, R + warp + lane * nwarps, la);
         for (int k = 0; k < n; ++k) {
             const char* s = shfl_ptr(la.src, k);
             char* d0 = shfl_ptr(la.dst0, k);
@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(128) flykv_reshard_tma_kernel(const ReshardArg
                 asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(S - D) : "memory");
                 pend_dst[wid][st] = d0;
                 pend_rep[wid][st] = rep;
-                pend_atom[wid][st] = base + k;
+                pend_atom[wid][st] = R + warp + (int64_t)k * nwarps;
                 const uint32_t bar = smem_u32(bars + st);
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
                              : "memory");
@@ -467,38 +467,58 @@ static cudaError_t launch_ldg(const ReshardArgs& a_in, int device, cudaStream_t 
     return cudaGetLastError();
 }
 
-template <int S>
-static cudaError_t launch_tma(const ReshardArgs& a, int device, cudaStream_t s) {
-    constexpr int W = 4;
+template <int S, int W>
+static cudaError_t launch_tma(const ReshardArgs& a, int device, cudaStream_t s, int want_per = 0) {
     const int stage = (a.atom_bytes + 127) & ~127;
     const size_t smem = (size_t)W * S * stage + (size_t)W * S * 8;
     static size_t configured = 0;
     if (smem > configured) {
-        cudaError_t e = cudaFuncSetAttribute(flykv_reshard_tma_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(flykv_reshard_tma_kernel<S, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
         if (e != cudaSuccess) return e;
         configured = smem;
     }
-    int per = g_ctas_per_sm;
-    if (per <= 0) {
-        int nb = 0;
-        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, flykv_reshard_tma_kernel<S>, W * 32, smem);
-        if (e != cudaSuccess) return e;
-        per = nb > 0 ? nb : 1;
-    }
+    int per = g_ctas_per_sm > 0 ? g_ctas_per_sm : want_per;
+    int nb = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, flykv_reshard_tma_kernel<S, W>, W * 32, smem);
+    if (e != cudaSuccess) return e;
+    if (per <= 0 || per > nb) per = nb > 0 ? nb : 1;
     const int64_t atoms = a.atom_hi - a.atom_lo;
     int64_t want = (atoms + W * 32 - 1) / (W * 32);
     int64_t cap = (int64_t)sm_count_of(device) * per;
     int grid = (int)(want < cap ? want : cap);
     if (grid < 1) grid = 1;
-    flykv_reshard_tma_kernel<S><<<grid, W * 32, smem, s>>>(a, stage);
+    flykv_reshard_tma_kernel<S, W><<<grid, W * 32, smem, s>>>(a, stage);
     return cudaGetLastError();
+}
+
+// TMA ring shape (stages x warps per CTA), experiment knob FLYKV_TMA_SHAPE.
+// Default: 4 stages x 2 warps x 3 CTAs per SM = 6 warps with 2 loads ahead
+// each -- 48 KiB in flight per SM, the same optimum as the LDG kernel
+// (c2: 6.36 TB/s vs 4.9 for 8 stages x 4 warps; profiles/r01_tma.jsonl).
+static cudaError_t launch_tma_shape(const ReshardArgs& a, int device, cudaStream_t s) {
+    static int shape = -1;
+    if (shape < 0) {
+        const char* e = getenv("FLYKV_TMA_SHAPE");
+        shape = e ? atoi(e) : 0;
+    }
+    switch (shape) {
+        case 1: return launch_tma<4, 4>(a, device, s);
+        case 3: return launch_tma<6, 2>(a, device, s);
+        case 4: return launch_tma<8, 2>(a, device, s);
+        case 5: return launch_tma<4, 8>(a, device, s);
+        case 6: return launch_tma<3, 4>(a, device, s);
+        case 7: return launch_tma<6, 4>(a, device, s);
+        case 8: return launch_tma<3, 8>(a, device, s);
+        case 9: return launch_tma<8, 4>(a, device, s);
+        default: return launch_tma<4, 2>(a, device, s, 3);
+    }
 }
 
 cudaError_t launch_reshard(const ReshardArgs& a, int device, cudaStream_t s) {
     if (a.atom_hi <= a.atom_lo) return cudaSuccess;
     const bool tma_ok = (a.atom_bytes % 16) == 0 && a.atom_bytes <= 16384;
-    if (g_impl == 2 && tma_ok && !a.peer) return launch_tma<8>(a, device, s);
+    if (g_impl == 2 && tma_ok && !a.peer) return launch_tma_shape(a, device, s);
     // default (0) and 3: two atoms in flight per warp (measured +1%)
     if ((g_impl == 0 || g_impl == 3) && a.atom_bytes == 4096) return launch_ldg<8, 2>(a, device, s);
     if ((g_impl == 0 || g_impl == 3) && a.atom_bytes == 2048) return launch_ldg<4, 2>(a, device, s);
