@@ -61,6 +61,7 @@ def parse():
     ap.add_argument("--cpu-baseline-steps", type=int, default=6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-parallel", action="store_true", help="skip the all-cores oracle figure")
     ap.add_argument("--frag", type=float, default=1.25, help="source placement window / source need")
     ap.add_argument("--pool-slack", type=float, default=1.05, help="pool room beyond the window / max need")
     ap.add_argument("--placement", default="fragmented", choices=["fragmented", "contiguous"],
@@ -242,6 +243,84 @@ def cpu_oracle_run(w, n_sample: int, steps: int, warmup: int):
     info = (f"first {n_sample} of {len(w.T)} requests ({payload / 1e9:.3f} GB payload per switch), "
             f"oracle kv_oracle.c, 1 thread, {steps} timed switches")
     return payload / sec / 1e9, sec, info, payload
+
+
+def _mem_available_bytes() -> int:
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemAvailable:"):
+                return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 0
+
+
+def cpu_oracle_parallel(w, reqs_per_thread: int = 2, steps: int = 3, max_threads: int = 64):
+    """The same oracle, unchanged, run as independent switches on every host
+    core at once (SURVEY 8(d) asks for a single-thread and an all-cores
+    figure): thread k owns requests [k*r, (k+1)*r) of the workload and its own
+    pools, and alternates their direction `steps` times.  ctypes releases the
+    GIL around each or_switch call, so the threads run in parallel.  Thread
+    count is bounded by the cores this process may use, the workload's request
+    count and a quarter of the host's available memory.  Returns (GB/s over the
+    wall time of all threads, threads, info)."""
+    import threading
+
+    from oracle import oracle as O
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    og = O.Geom(w.L, w.H, w.d, w.B, w.e)
+    M = O.block_bytes(og)
+    subs = []
+    for k in range(min(cores, max_threads, len(w.T) // reqs_per_thread)):
+        a, b = k * reqs_per_thread, (k + 1) * reqs_per_thread
+        subs.append(synth.Workload(w.name, w.L, w.H, w.d, w.B, w.e, w.n_gpus, w.T[a:b], w.src[a:b], w.dst[a:b]))
+    budget = _mem_available_bytes() // 4
+    need = 0
+    for i, sub in enumerate(subs):
+        need += sum(synth.pool_blocks(sub)) * w.L * M
+        if budget and need > budget:
+            subs = subs[:max(i, 1)]
+            break
+    work = []
+    for sub in subs:
+        nb = synth.pool_blocks(sub)
+        pools = [np.full(w.L * n * M, 0x5A, dtype=np.uint8) for n in nb]
+        held = [np.zeros(n, dtype=np.uint8) for n in nb]
+        counts = [O.num_blocks(og, T, s_[1]) for T, s_ in zip(sub.T, sub.src)]
+        tabs = synth.source_tables(sub, counts, nb)
+        reqs = []
+        for T, s_, d, ids in zip(sub.T, sub.src, sub.dst, tabs):
+            for r in range(s_[1]):
+                held[s_[0] + r][ids] = 1
+            reqs.append(O.Req(T, s_, list(ids), d))
+        work.append([pools, held, reqs, 0])
+    start = threading.Barrier(len(work) + 1)
+
+    def run(item):
+        pools, held, reqs, _ = item
+        start.wait()
+        moved = 0
+        for _ in range(steps):
+            st, new = O.switch(og, pools, held, reqs)
+            assert st == 0
+            for r in reqs:
+                if tuple(r.src) != tuple(r.dst):
+                    moved += 2 * w.L * w.H * (-(-r.T // w.B)) * w.B * w.d * w.e * O.replicas(og, r.dst[1])
+            reqs = [O.Req(r.T, r.dst, list(t), r.src) for r, t in zip(reqs, new)]
+        item[3] = moved
+
+    threads = [threading.Thread(target=run, args=(it,)) for it in work]
+    for t in threads:
+        t.start()
+    start.wait()
+    t0 = time.perf_counter()
+    for t in threads:
+        t.join()
+    sec = time.perf_counter() - t0
+    payload = sum(it[3] for it in work)
+    info = (f"{len(work)} threads x {reqs_per_thread} requests each (requests 0..{len(work) * reqs_per_thread - 1}), "
+            f"{steps} switches per thread, {payload / 1e9:.2f} GB moved in {sec:.2f} s wall")
+    return payload / sec / 1e9, len(work), info
 
 
 def run_reference(args):
@@ -465,6 +544,9 @@ def run_single(args):
     if not args.no_cpu_baseline:
         gbs, sec, info, _ = cpu_oracle_run(w, args.cpu_baseline_reqs, args.cpu_baseline_steps, 0)
         cpu = {"value": round(gbs, 4), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": info}
+        if not args.no_cpu_parallel:
+            pg, nt, pinfo = cpu_oracle_parallel(w)
+            cpu["all_cores"] = {"value": round(pg, 4), "unit": "GB/s", "cores": nt, "sample": pinfo}
     line = {
         "metric": "DP<->TP KV re-layout GB/s", "value": round(value, 3), "unit": "GB/s", "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4),

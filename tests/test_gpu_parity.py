@@ -184,18 +184,29 @@ def test_round_trip_restores_contents():
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("cfg,n_req,frag", [("c2", 0, 1.25), ("c4", 0, 1.25), ("c4gqa4", 0, 1.25), ("c4gqa1", 0, 1.25),
-                                            ("c3i", 64, 1.25), ("c3ii", 64, 1.25), ("c5", 0, 1.0), ("single", 0, 1.25)])
-def test_full_size_all_atoms(cfg, n_req, frag):
+@pytest.mark.parametrize("cfg,n_req,frag,impl", [("c2", 0, 1.25, 0), ("c4", 0, 1.25, 0), ("c4gqa4", 0, 1.25, 0),
+                                                 ("c4gqa1", 0, 1.25, 0), ("c3i", 64, 1.25, 0), ("c3ii", 64, 1.25, 0),
+                                                 ("c5", 0, 1.0, 0), ("single", 0, 1.25, 0),
+                                                 ("c2", 0, 1.25, 2), ("c4gqa4", 0, 1.25, 2)])
+def test_full_size_all_atoms(cfg, n_req, frag, impl):
     """Every BASELINE config at the size and in the launch configuration the
     bench times (virtual ranks on one B200, the bench's pool sizing and
     placement, one reshard launch; config 3 on the bench's 64-request prefix,
     config 5 in full with `--frag 1.0`): destination tables equal the oracle's
     allocator in full; EVERY destination atom (up to 13.4M x 4 KiB, all GQA
     replicas) equals the content hash of the source position the oracle maps
-    it from; sampled free blocks keep their poison."""
+    it from; sampled free blocks keep their poison.  impl 2: the TMA bulk-ring
+    variant of the reshard kernel on the same checks."""
     F = _F()
     from paper_2602_22593_b200.engine import KVSwitchEngine
+    F.set_reshard_impl(impl, 0)
+    try:
+        _full_size_all_atoms(F, KVSwitchEngine, cfg, n_req, frag)
+    finally:
+        F.set_reshard_impl(0, 0)
+
+
+def _full_size_all_atoms(F, KVSwitchEngine, cfg, n_req, frag):
     w = synth.WORKLOADS[cfg]()
     if n_req:
         w = synth.Workload(w.name, w.L, w.H, w.d, w.B, w.e, w.n_gpus, w.T[:n_req], w.src[:n_req], w.dst[:n_req])
