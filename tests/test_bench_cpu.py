@@ -1,0 +1,51 @@
+"""Host logic of bench.py (CPU only): the NVLink/HBM roofline model of
+SURVEY 8(d), the reference arm's JSON contract (the oracle on host cores),
+its rank-0-only rule under torchrun, and the all-cores oracle figure."""
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+
+import bench
+import synth
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_nvlink_roofline_closed_form():
+    """2 GPUs: GPU0 keeps 4 GB and sends 2 GB to GPU1; GPU1 sends 1 GB to GPU0."""
+    m = np.array([[4e9, 2e9], [1e9, 0.0]])
+    t, eg, ing, hbm = bench.nvlink_roofline(m, hbm_gbs=8000.0, link_gbs=1000.0)
+    assert list(eg) == [2e9, 1e9] and list(ing) == [1e9, 2e9]
+    assert list(hbm) == [4e9 + 2e9 + 4e9 + 1e9, 1e9 + 0 + 2e9 + 0]   # reads (row) + writes (column)
+    assert t == max(2e9 / 1e12, 11e9 / 8e12)
+
+
+def _run_reference(env_extra):
+    env = dict(os.environ, **env_extra)
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--config", "tiny", "--steps", "2",
+                        "--warmup", "1"], cwd=ROOT, env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    return [ln for ln in r.stdout.splitlines() if ln.strip()]
+
+
+def test_reference_arm_json_contract():
+    lines = _run_reference({})
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["unit"] == "GB/s" and d["higher_is_better"] is True
+    assert d["value"] > 0 and d["steps"] == 2 and d["warmup"] == 1
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"] == {"value": d["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+    assert "workload" in d["config"]
+
+
+def test_reference_arm_other_ranks_print_nothing():
+    assert _run_reference({"WORLD_SIZE": "2", "RANK": "1"}) == []
+
+
+def test_all_cores_oracle_figure():
+    gbs, threads, info = bench.cpu_oracle_parallel(synth.WORKLOADS["tiny"](), reqs_per_thread=2, steps=2)
+    assert gbs > 0 and 1 <= threads <= 4 and "threads" in info
