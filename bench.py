@@ -568,7 +568,8 @@ def run_single(args):
                                       round(float(np.percentile(kern_ms, 90)), 4)],
         "modeled_nvlink": modeled,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
-                     "frac": round(achieved / hbm_peak, 4), "traffic": traffic, "peak_source": peak_src,
+                     "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
+                     "traffic_over_algorithmic_forward_launch": traffic_ratio, "peak_source": peak_src,
                      "kernel": "flykv_reshard_kernel", "algorithmic_bytes_per_launch": int(algo_bytes)},
         "cpu_baseline": cpu,
         "e2e": e2e,
