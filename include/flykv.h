@@ -212,6 +212,36 @@ kv_status kv_reshard(kv_plan* plan, int32_t gpu, void* stream);
 kv_status kv_reshard_staged(kv_plan* plan, int32_t gpu, void* staging, int64_t staging_bytes, int32_t mode,
                             void* stream);
 
+/*
+ * The alternative cross-GPU path BJ names next to direct P2P stores: pack
+ * into contiguous per-destination send buffers, an all-to-all (NCCL
+ * all_to_all_single, by the caller), unpack (SURVEY 8(e) comparator N6).
+ * Same bytes as kv_reshard; two extra HBM passes and a payload-sized buffer.
+ *
+ * Chunk (s -> d) holds every (atom, replica) sourced on GPU s whose
+ * destination is GPU d, its size in bytes is bytes_matrix[s * n_gpus + d] of
+ * kv_plan_get_stats.  Its layout: for each of s's segments (requests in plan
+ * order), the heads held by d's member of the destination group in
+ * ((head index * L + layer) * 2 + K/V) * ceil(T/B) + chunk order, B*d*e bytes
+ * each -- a function of the plan alone, so every process derives it.
+ *
+ * kv_pack: enqueue on `stream` the gather of GPU src_gpu's atoms into chunks:
+ *   buf        device, src_gpu's send buffer
+ *   chunk_off  host int64 [n_gpus]: byte offset in buf of the chunk for
+ *              each destination GPU (e.g. the exclusive prefix of row src_gpu
+ *              of the bytes matrix for all_to_all_single)
+ * kv_unpack: enqueue on `stream` the scatter of every chunk received by
+ * dst_gpu into its pool's destination blocks:
+ *   buf        device, dst_gpu's receive buffer
+ *   chunk_off  host int64 [n_gpus]: byte offset in buf of the chunk from each
+ *              source GPU (the exclusive prefix of column dst_gpu)
+ * Both read the plan's uploaded descriptors; valid until the plan commits
+ * (BAD_STATE after).  n_gpus <= 64.  The caller orders unpack after the
+ * all-to-all, and the all-to-all after every pack.
+ */
+kv_status kv_pack(kv_plan* plan, int32_t src_gpu, void* buf, const int64_t* chunk_off, void* stream);
+kv_status kv_unpack(kv_plan* plan, int32_t dst_gpu, const void* buf, const int64_t* chunk_off, void* stream);
+
 /* Sizes of pool gpu's table after the switch: *n_resident requests resident
  * on gpu (dst group contains gpu), *n_ids block IDs in their tables; gpu ==
  * -1 gives the totals over all pools.  The per_req_meta first head of

@@ -107,11 +107,18 @@ struct kv_plan {
     std::vector<ReqRec> recs;
     kv_plan_stats st{};
     std::vector<int32_t> out_off;  // [n_gpus][3] packed all-GPU remap output offsets
-    // device workspace: [seg_begin | segs | tables | recs | out_off]
+    // pack -> all-to-all -> unpack (kv_pack / kv_unpack): per (segment, member)
+    // atom base inside the chunk (source GPU -> member's GPU), and each
+    // receiver's (segment, member) pairs
+    std::vector<int64_t> a2a_base;
+    std::vector<A2AItem> items;
+    std::vector<int32_t> item_lo, item_hi;
+    std::vector<int64_t> recv_atoms;
+    // device workspace: [seg_begin | segs | tables | recs | out_off | a2a_base | items]
     int dev = -1;
     char* dbuf = nullptr;
     size_t dbytes = 0;
-    size_t off_seg_begin = 0, off_segs = 0, off_tables = 0, off_recs = 0, off_outs = 0;
+    size_t off_seg_begin = 0, off_segs = 0, off_tables = 0, off_recs = 0, off_outs = 0, off_a2a = 0, off_items = 0;
     cudaStream_t last_stream = nullptr;
 };
 
@@ -479,6 +486,7 @@ extern "C" kv_status kv_plan_switch(kv_cache* c, const kv_request* reqs, int32_t
     // ---- work segments: (request, canonical source replica) ----
     p->bytes.assign((size_t)n * n, 0);
     std::vector<Seg> segs;
+    std::vector<int32_t> seg_req;  // request of each segment
     for (int32_t i = 0; i < n_reqs; ++i) {
         const ReqPlan& q = p->reqs[i];
         if (!q.moving) continue;
@@ -517,6 +525,7 @@ extern "C" kv_status kv_plan_switch(kv_cache* c, const kv_request* reqs, int32_t
             s.k1 = l1.k;
             s.rep1 = l1.rep;
             segs.push_back(s);
+            seg_req.push_back(i);
             const int64_t head_bytes = (int64_t)L * 2 * C * c->atom_bytes;
             for (int32_t hh = 0; hh < s.nh; ++hh)
                 for (int32_t j = 0; j < l1.rep; ++j) {
@@ -526,7 +535,62 @@ extern "C" kv_status kv_plan_switch(kv_cache* c, const kv_request* reqs, int32_t
         }
     }
     // group segments by source GPU (stable: request order within a GPU)
-    std::stable_sort(segs.begin(), segs.end(), [](const Seg& a, const Seg& b) { return a.src_gpu < b.src_gpu; });
+    {
+        std::vector<int32_t> order(segs.size());
+        for (size_t k = 0; k < order.size(); ++k) order[k] = (int32_t)k;
+        std::stable_sort(order.begin(), order.end(),
+                         [&](int32_t a, int32_t b) { return segs[a].src_gpu < segs[b].src_gpu; });
+        std::vector<Seg> s2(segs.size());
+        std::vector<int32_t> r2(segs.size());
+        for (size_t k = 0; k < order.size(); ++k) {
+            s2[k] = segs[order[k]];
+            r2[k] = seg_req[order[k]];
+        }
+        segs.swap(s2);
+        seg_req.swap(r2);
+    }
+    // ---- pack -> all-to-all -> unpack layout (kv_pack / kv_unpack) ----
+    // chunk (s -> d) = for each segment sourced on s (plan order), for the
+    // member m of its destination group on d: the atoms of the heads m holds
+    // (rank ID rid = dst_rid[m]) in ((hi * L + l) * 2 + kv) * C + c order
+    {
+        std::vector<int64_t> run((size_t)n * n, 0), tot(n, 0);
+        std::vector<std::vector<A2AItem>> per(n);
+        for (size_t k = 0; k < segs.size(); ++k) {
+            Seg& sg = segs[k];
+            const ReqPlan& q = p->reqs[seg_req[k]];
+            sg.a2a = (int32_t)p->a2a_base.size();
+            const int64_t per_head = (int64_t)L * 2 * sg.C;
+            for (int32_t m = 0; m < q.dst.degree; ++m) {
+                const int32_t rid = q.dst_rid[m];
+                int32_t nh_m;
+                if (sg.rep1 == 1) {
+                    const int32_t lo = std::max(sg.h0, rid * sg.hloc1), hi = std::min(sg.h0 + sg.nh, (rid + 1) * sg.hloc1);
+                    nh_m = std::max(0, hi - lo);
+                } else {
+                    const int32_t h = rid / sg.rep1;
+                    nh_m = (h >= sg.h0 && h < sg.h0 + sg.nh) ? 1 : 0;
+                }
+                const int32_t d = sg.dst_g0 + m;
+                int64_t& r = run[(size_t)sg.src_gpu * n + d];
+                p->a2a_base.push_back(r);
+                const int64_t cnt = nh_m * per_head;
+                r += cnt;
+                if (cnt > 0) {
+                    per[d].push_back(A2AItem{(int32_t)k, m, rid, 0, tot[d]});
+                    tot[d] += cnt;
+                }
+            }
+        }
+        p->item_lo.assign(n, 0);
+        p->item_hi.assign(n, 0);
+        p->recv_atoms = tot;
+        for (int32_t d = 0; d < n; ++d) {
+            p->item_lo[d] = (int32_t)p->items.size();
+            p->items.insert(p->items.end(), per[d].begin(), per[d].end());
+            p->item_hi[d] = (int32_t)p->items.size();
+        }
+    }
     p->segs = segs;
     p->seg_begin.resize(segs.size() + 1);
     p->gpu_seg_lo.assign(n, 0);
@@ -578,7 +642,9 @@ extern "C" kv_status kv_plan_switch(kv_cache* c, const kv_request* reqs, int32_t
         i0 += p->n_res_ids[g];
     }
     p->off_outs = align(p->off_recs + p->recs.size() * sizeof(ReqRec));
-    p->dbytes = align(p->off_outs + p->out_off.size() * sizeof(int32_t));
+    p->off_a2a = align(p->off_outs + p->out_off.size() * sizeof(int32_t));
+    p->off_items = align(p->off_a2a + p->a2a_base.size() * sizeof(int64_t));
+    p->dbytes = align(p->off_items + p->items.size() * sizeof(A2AItem));
 
     p->st.n_requests = n_reqs;
     p->st.n_moving = n_moving;
@@ -638,6 +704,8 @@ static kv_status ensure_device(kv_plan* p, cudaStream_t stream) {
     if (!p->tables.empty()) std::memcpy(h + p->off_tables, p->tables.data(), p->tables.size() * sizeof(int32_t));
     if (!p->recs.empty()) std::memcpy(h + p->off_recs, p->recs.data(), p->recs.size() * sizeof(ReqRec));
     std::memcpy(h + p->off_outs, p->out_off.data(), p->out_off.size() * sizeof(int32_t));
+    if (!p->a2a_base.empty()) std::memcpy(h + p->off_a2a, p->a2a_base.data(), p->a2a_base.size() * sizeof(int64_t));
+    if (!p->items.empty()) std::memcpy(h + p->off_items, p->items.data(), p->items.size() * sizeof(A2AItem));
     CUDA_TRY(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&p->dbuf), p->dbytes, c->pool, stream));
     CUDA_TRY(cudaMemcpyAsync(p->dbuf, h, p->dbytes, cudaMemcpyHostToDevice, stream));
     CUDA_TRY(cudaEventRecord(c->stage_ev, stream));
@@ -713,6 +781,60 @@ extern "C" kv_status kv_reshard_staged(kv_plan* p, int32_t gpu, void* staging, i
     if (a.atom_hi <= a.atom_lo) return KV_OK;
     cudaError_t e = launch_reshard(a, p->dev, stream);
     if (e != cudaSuccess) return cuda_fail(e, "flykv_reshard_kernel (staged) launch");
+    g_launches.fetch_add(1);
+    return KV_OK;
+}
+
+extern "C" kv_status kv_pack(kv_plan* p, int32_t src_gpu, void* buf, const int64_t* chunk_off, void* stream_) {
+    if (!p || !buf || !chunk_off) return fail(KV_ERR_INVALID_ARG, "bad kv_pack arguments");
+    if (p->state != PLAN_PLANNED) return fail(KV_ERR_BAD_STATE, "plan already committed");
+    const int32_t n = p->c->n_gpus;
+    if (src_gpu < 0 || src_gpu >= n) return fail(KV_ERR_INVALID_ARG, "src_gpu %d out of range", src_gpu);
+    if (n > 64) return fail(KV_ERR_INVALID_ARG, "kv_pack supports up to 64 GPUs");
+    cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+    kv_status s = ensure_device(p, stream);
+    if (s) return s;
+    p->last_stream = stream;
+    ReshardArgs a = reshard_args(p, src_gpu);
+    a.peer = 1;  // LDG/STG path
+    a.staged = 3;
+    a.a2a_base = reinterpret_cast<const int64_t*>(p->dbuf + p->off_a2a);
+    a.a2a_buf = static_cast<char*>(buf);
+    for (int32_t d = 0; d < n; ++d) a.a2a_off[d] = chunk_off[d];
+    if (a.atom_hi <= a.atom_lo) return KV_OK;
+    cudaError_t e = launch_reshard(a, p->dev, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "flykv_reshard_kernel (pack) launch");
+    g_launches.fetch_add(1);
+    return KV_OK;
+}
+
+extern "C" kv_status kv_unpack(kv_plan* p, int32_t dst_gpu, const void* buf, const int64_t* chunk_off, void* stream_) {
+    if (!p || !buf || !chunk_off) return fail(KV_ERR_INVALID_ARG, "bad kv_unpack arguments");
+    if (p->state != PLAN_PLANNED) return fail(KV_ERR_BAD_STATE, "plan already committed");
+    const int32_t n = p->c->n_gpus;
+    if (dst_gpu < 0 || dst_gpu >= n) return fail(KV_ERR_INVALID_ARG, "dst_gpu %d out of range", dst_gpu);
+    if (n > 64) return fail(KV_ERR_INVALID_ARG, "kv_unpack supports up to 64 GPUs");
+    cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+    kv_status s = ensure_device(p, stream);
+    if (s) return s;
+    p->last_stream = stream;
+    const kv_cache* c = p->c;
+    UnpackArgs a{};
+    a.segs = reinterpret_cast<const Seg*>(p->dbuf + p->off_segs);
+    a.tables = reinterpret_cast<const int32_t*>(p->dbuf + p->off_tables);
+    a.a2a_base = reinterpret_cast<const int64_t*>(p->dbuf + p->off_a2a);
+    a.items = reinterpret_cast<const A2AItem*>(p->dbuf + p->off_items) + p->item_lo[dst_gpu];
+    a.n_items = p->item_hi[dst_gpu] - p->item_lo[dst_gpu];
+    a.n_atoms = p->recv_atoms[dst_gpu];
+    a.layer_base = c->d_layer_base;
+    a.L = c->geo.num_layers;
+    a.atom_bytes = (int32_t)c->atom_bytes;
+    a.M = c->M;
+    a.buf = static_cast<const char*>(buf);
+    for (int32_t g = 0; g < n; ++g) a.off[g] = chunk_off[g];
+    if (a.n_atoms <= 0) return KV_OK;
+    cudaError_t e = launch_unpack(a, p->dev, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "flykv_unpack_kernel launch");
     g_launches.fetch_add(1);
     return KV_OK;
 }

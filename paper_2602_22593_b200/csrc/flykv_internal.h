@@ -58,7 +58,8 @@ struct Seg {
     int32_t hloc1, k1, rep1; // destination layout
     int32_t dst_inv;   // offset of the destination's member-of-rank-ID table in tables, -1 = identity
     int32_t J1;        // destination-major order: ceil(C / k1) destination blocks per (layer, K/V)
-    int32_t pad[2];
+    int32_t a2a;       // offset of this segment's per-member chunk bases in the plan's a2a_base array
+    int32_t pad;
 };
 static_assert(sizeof(Seg) == 64, "Seg is 64 bytes");
 
@@ -85,6 +86,33 @@ struct ReshardArgs {
     int32_t staged;            // comparator only: 0 fused, 1 pack into staging, 2 unpack from staging
     char* staging;             // atom (i - atom_lo) at staging + (i - atom_lo) * atom_bytes
     int32_t rep_flags;         // GQA replica stores: bit 0 = decode replicas lane-parallel, bit 1 = replica-major order
+    // staged == 3 (kv_pack): every (atom, replica) goes to the send chunk of
+    // its destination GPU d at a2a_buf + a2a_off[d] + (base + pos) * atom_bytes,
+    // base = a2a_base[seg.a2a + member], pos = ((hi * L + l) * 2 + kv) * C + c
+    // (hi = index of the head among the segment's heads that member holds)
+    const int64_t* a2a_base;
+    char* a2a_buf;
+    int64_t a2a_off[64];
+};
+
+// One (segment, destination member) pair received by a GPU (kv_unpack).
+struct A2AItem {
+    int32_t seg, m, rid, pad;  // segment, member of its destination group, that member's rank ID
+    int64_t start;             // first atom of the pair in the receiver's atom order
+};
+
+struct UnpackArgs {
+    const Seg* segs;
+    const int32_t* tables;
+    const int64_t* a2a_base;
+    const A2AItem* items;      // the receiver's pairs, ordered by source GPU then plan order
+    int32_t n_items;
+    int64_t n_atoms;           // atoms the receiver unpacks
+    char* const* layer_base;
+    int32_t L, atom_bytes;
+    int64_t M;
+    const char* buf;           // receive buffer
+    int64_t off[64];           // byte offset in buf of the chunk from each source GPU
 };
 
 struct RemapArgs {
@@ -126,5 +154,6 @@ void set_reshard_impl(int impl, int ctas_per_sm);
 cudaError_t launch_remap(const RemapArgs& a, int n_ctas, cudaStream_t s);
 cudaError_t launch_gather(const GatherSeg* segs, int n_seg, char* dst, cudaStream_t s);
 cudaError_t launch_decode(const DecodeArgs& a, cudaStream_t s);
+cudaError_t launch_unpack(const UnpackArgs& a, int device, cudaStream_t s);
 
 }  // namespace flykv

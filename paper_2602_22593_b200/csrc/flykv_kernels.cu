@@ -41,6 +41,8 @@ struct AtomAddr {
     int32_t l, h;      // layer, head
     int32_t dst_g0, rep1, hloc1;
     int32_t dst_inv;   // member-of-rank-ID table offset (-1 = identity rank IDs)
+    int32_t kv, c;     // K/V half, chunk (kv_pack's send-chunk position)
+    int32_t h0, C, a2a;  // segment's first head, chunks, chunk-base offset (kv_pack)
 };
 
 __device__ __forceinline__ int find_seg(const int64_t* __restrict__ seg_begin, int lo, int hi,
@@ -67,6 +69,11 @@ __device__ __forceinline__ void decode(const ReshardArgs& a, int64_t atom, int s
     const uint32_t kv = lkv & 1u, l = lkv >> 1;
     const uint32_t c = jb * k1 + w;
     int32_t h = sg.h0 + (int32_t)hh;
+    out.kv = (int32_t)kv;
+    out.c = (int32_t)c;
+    out.h0 = sg.h0;
+    out.C = sg.C;
+    out.a2a = sg.a2a;
     if (c >= (uint32_t)sg.C) {  // hole past the request's last chunk
         out.src = nullptr;
         out.doff = 0;
@@ -102,6 +109,12 @@ __device__ __forceinline__ void decode(const ReshardArgs& a, int64_t atom, int s
 __device__ __forceinline__ char* dst_ptr(const ReshardArgs& a, const AtomAddr& ad, int j) {
     const int32_t rid = ad.rep1 == 1 ? ad.h / ad.hloc1 : ad.h * ad.rep1 + j;
     const int32_t m = ad.dst_inv < 0 ? rid : __ldg(a.tables + ad.dst_inv + rid);
+    if (a.staged == 3) {  // kv_pack: the send chunk of the destination GPU
+        const int32_t first = rid * ad.hloc1 > ad.h0 ? rid * ad.hloc1 : ad.h0;
+        const int32_t hi = ad.rep1 == 1 ? ad.h - first : 0;
+        const int64_t pos = (((int64_t)hi * a.L + ad.l) * 2 + ad.kv) * ad.C + ad.c;
+        return a.a2a_buf + a.a2a_off[ad.dst_g0 + m] + (__ldg(a.a2a_base + ad.a2a + m) + pos) * a.atom_bytes;
+    }
     return a.layer_base[(ad.dst_g0 + m) * a.L + ad.l] + ad.doff;
 }
 
@@ -123,7 +136,7 @@ __device__ __forceinline__ void lane_decode(const ReshardArgs& a, int64_t atom, 
     la.src = ad.src;
     la.rep1 = ad.rep1;  // 0 for a hole: nothing is read or written
     la.dst0 = ad.src ? dst_ptr(a, ad, 0) : nullptr;
-    if (a.staged && la.rep1 > 0) {  // bench comparator: pack (source -> staging) or unpack (staging -> destinations)
+    if ((a.staged == 1 || a.staged == 2) && la.rep1 > 0) {  // comparator: slot-order pack or unpack
         char* slot = a.staging + (atom - a.atom_lo) * (int64_t)a.atom_bytes;
         if (a.staged == 1) {
             la.dst0 = slot;
@@ -289,6 +302,68 @@ __global__ void __launch_bounds__(256, 2) flykv_reshard_kernel(const ReshardArgs
         }
     }
     if (a.fence_sys) __threadfence_system();
+}
+
+// ---------------------------------------------------------------- unpack
+// kv_unpack: the receiver's side of pack -> all-to-all -> unpack.  Atom i of
+// the receiver belongs to pair items[k] (start <= i); its position inside
+// that pair, ((hi * L + l) * 2 + kv) * C + c, gives the head, layer, K/V half
+// and chunk, hence the destination address in this GPU's pool; the source is
+// the chunk received from the segment's source GPU.  Lane-parallel decode as
+// in the reshard kernel: lane k decodes step k, the warp copies by shuffle.
+__device__ __forceinline__ void unpack_decode(const UnpackArgs& a, int64_t atom, const char*& src, char*& dst) {
+    int lo = 0, hi = a.n_items;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (a.items[mid].start <= atom) lo = mid;
+        else hi = mid;
+    }
+    const A2AItem it = a.items[lo];
+    const Seg sg = a.segs[it.seg];
+    const int64_t local = atom - it.start;
+    const int32_t c = (int32_t)(local % sg.C);
+    int64_t t = local / sg.C;
+    const int32_t kv = (int32_t)(t & 1);
+    t >>= 1;
+    const int32_t l = (int32_t)(t % a.L);
+    const int32_t hidx = (int32_t)(t / a.L);
+    const int32_t h = sg.rep1 == 1 ? (it.rid * sg.hloc1 > sg.h0 ? it.rid * sg.hloc1 : sg.h0) + hidx : it.rid / sg.rep1;
+    const int32_t blk1 = __ldg(a.tables + sg.dst_tab + c / sg.k1);
+    dst = a.layer_base[(sg.dst_g0 + it.m) * a.L + l] + (int64_t)blk1 * a.M + kv * (a.M >> 1) +
+          (int64_t)((h % sg.hloc1) * sg.k1 + c % sg.k1) * a.atom_bytes;
+    src = a.buf + a.off[sg.src_gpu] + (__ldg(a.a2a_base + sg.a2a + it.m) + local) * a.atom_bytes;
+}
+
+__global__ void __launch_bounds__(256) flykv_unpack_kernel(const UnpackArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int nv = a.atom_bytes >> 4;
+    for (int64_t R = 0; R < a.n_atoms; R += 32 * nwarps) {
+        const int64_t first = R + warp;
+        if (first >= a.n_atoms) break;
+        const int64_t span = (a.n_atoms - first + nwarps - 1) / nwarps;
+        const int n = span < 32 ? (int)span : 32;
+        const char* s = nullptr;
+        char* d = nullptr;
+        if (lane < n) unpack_decode(a, first + lane * nwarps, s, d);
+        for (int k = 0; k < n; ++k) {
+            const int4* sk = reinterpret_cast<const int4*>(shfl_ptr(s, k));
+            int4* dk = reinterpret_cast<int4*>(shfl_ptr(d, k));
+            for (int i = lane; i < nv; i += 32) st_stream(dk + i, ld_stream(sk + i));
+        }
+    }
+}
+
+static int sm_count_of(int device);
+
+cudaError_t launch_unpack(const UnpackArgs& a, int device, cudaStream_t s) {
+    if (a.n_atoms <= 0) return cudaSuccess;
+    int64_t want = (a.n_atoms + 255) / 256;
+    int64_t cap = (int64_t)sm_count_of(device) * 2;
+    const int grid = (int)(want < cap ? (want > 0 ? want : 1) : cap);
+    flykv_unpack_kernel<<<grid, 192, 0, s>>>(a);
+    return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------- TMA bulk

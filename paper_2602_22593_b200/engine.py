@@ -13,6 +13,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import numpy as np
+
 import torch
 
 from . import flykv
@@ -85,6 +87,31 @@ class KVSwitchEngine:
             for g, t in tables.items():
                 flykv.kv_remap_block_tables(plan, g, t.req_ptr, t.block_ids, t.meta, self.stream)
         return tables
+
+    def execute_pack_unpack(self, plan: flykv.Plan, buf=None):
+        """The pack -> all-to-all -> unpack alternative (kv_pack / kv_unpack)
+        with every pool on this device: one buffer holds chunk (s -> d) at the
+        row-major prefix of the plan's byte matrix, so the all-to-all is the
+        identity and unpack reads what pack wrote.  Then the all-pool remap.
+        buf: optional device uint8 buffer of >= payload bytes."""
+        st, mat = plan.stats()
+        n = self.n_gpus
+        flat = np.zeros(n * n + 1, dtype=np.int64)
+        flat[1:] = np.cumsum(mat.reshape(-1))
+        off = flat[:-1].reshape(n, n)
+        if buf is None:
+            buf = torch.empty(max(int(flat[-1]), 16), dtype=torch.uint8, device=self.device)
+        with torch.cuda.stream(self.stream):
+            for s_ in range(n):
+                if mat[s_].sum():
+                    flykv.kv_pack(plan, s_, buf, off[s_], self.stream)
+            for d in range(n):
+                if mat[:, d].sum():
+                    flykv.kv_unpack(plan, d, buf, off[:, d], self.stream)
+            views, (rp, ids, meta) = self.alloc_packed(plan)
+            flykv.kv_remap_block_tables(plan, -1, rp, ids, meta, self.stream)
+            self._packed = (rp, ids, meta)
+        return views, buf
 
     def switch(self, requests, gpus=None, read_back=False):
         """Plan + reshard + remap.  With read_back, the new tables are copied

@@ -120,6 +120,8 @@ _sig("kv_reshard", C.c_int, _P, C.c_int32, _P)
 _sig("kv_plan_resident", C.c_int, _P, C.c_int32, _I32P, _I32P)
 _sig("kv_reshard_staged", C.c_int, _P, C.c_int32, _P, C.c_int64, C.c_int32, _P)
 _sig("kv_remap_block_tables", C.c_int, _P, C.c_int32, _P, _P, _P, _P)
+_sig("kv_pack", C.c_int, _P, C.c_int32, _P, _I64P, _P)
+_sig("kv_unpack", C.c_int, _P, C.c_int32, _P, _I64P, _P)
 _sig("kv_plan_dst_tables", C.c_int, _P, _I32P, _I32P)
 _sig("kv_plan_commit", C.c_int, _P)
 _sig("kv_plan_waves", C.c_int, _P, C.POINTER(Request), C.c_int32, C.c_int64, _I32P, _I32P)
@@ -145,7 +147,8 @@ _sig("kv_launch_count", C.c_int64)
 _sig("kv_set_reshard_impl", C.c_int, C.c_int32, C.c_int32)
 
 EXPORTED = ["kv_cache_create", "kv_cache_destroy", "kv_layout", "kv_blocks_for", "kv_alloc", "kv_reserve",
-            "kv_free", "kv_free_count", "kv_held_mask", "kv_plan_switch", "kv_plan_upload", "kv_reshard", "kv_reshard_staged", "kv_plan_resident",
+            "kv_free", "kv_free_count", "kv_held_mask", "kv_plan_switch", "kv_plan_upload", "kv_reshard", "kv_reshard_staged",
+            "kv_pack", "kv_unpack", "kv_plan_resident",
             "kv_remap_block_tables", "kv_plan_dst_tables", "kv_plan_commit", "kv_plan_waves", "kv_suggest_rank_ids", "kv_plan_get_stats", "kv_plan_destroy",
             "weight_shard_view", "kv_gather_view", "kv_vmm_granularity", "kv_vmm_alloc", "kv_vmm_free",
             "weight_view_alias", "weight_view_unalias", "kv_paged_decode", "kv_ipc_export", "kv_ipc_import", "kv_ipc_close",
@@ -411,6 +414,30 @@ def kv_reshard(plan: Plan, gpu: int = -1, stream=None):
 def kv_reshard_staged(plan: Plan, gpu: int, staging, staging_bytes: int, mode: int, stream=None):
     """Bench comparator: mode 1 pack -> staging, mode 2 unpack staging -> destinations."""
     _check(_lib.kv_reshard_staged(plan._h, gpu, ptr_of(staging), int(staging_bytes), mode, stream_of(stream)))
+
+
+def a2a_offsets(bytes_matrix):
+    """(send_off, recv_off) for all_to_all_single buffers: send_off[s] is the
+    exclusive prefix of row s (chunks s -> d in d order), recv_off[d] of
+    column d (chunks s -> d in s order); int64 [n, n] byte offsets."""
+    m = np.asarray(bytes_matrix, dtype=np.int64)
+    send = np.zeros_like(m)
+    recv = np.zeros_like(m)
+    send[:, 1:] = np.cumsum(m, axis=1)[:, :-1]
+    recv[1:, :] = np.cumsum(m, axis=0)[:-1, :]
+    return send, recv.T.copy()
+
+
+def kv_pack(plan: Plan, src_gpu: int, buf, chunk_off, stream=None):
+    """Gather src_gpu's atoms into per-destination chunks of buf (chunk_off[d] = byte offset)."""
+    off = np.ascontiguousarray(np.asarray(chunk_off, dtype=np.int64))
+    _check(_lib.kv_pack(plan._h, src_gpu, ptr_of(buf), off.ctypes.data_as(_I64P), stream_of(stream)))
+
+
+def kv_unpack(plan: Plan, dst_gpu: int, buf, chunk_off, stream=None):
+    """Scatter the chunks received by dst_gpu (chunk_off[s] = byte offset of s's chunk) into its pool."""
+    off = np.ascontiguousarray(np.asarray(chunk_off, dtype=np.int64))
+    _check(_lib.kv_unpack(plan._h, dst_gpu, ptr_of(buf), off.ctypes.data_as(_I64P), stream_of(stream)))
 
 
 def kv_remap_block_tables(plan: Plan, gpu: int, req_ptr, block_ids, per_req_meta, stream=None):

@@ -5,6 +5,8 @@ import json
 import os
 import sys
 
+import numpy as np
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
@@ -67,6 +69,24 @@ def main():
                          F.kv_reshard_staged(plan, -1, stg, stg.numel(), 2, stream)))
     res["staged_pack_unpack"] = {"ms": ms, "GBps_of_fused_bytes": algo / ms / 1e6}
     del stg
+    # the per-destination variant (kv_pack -> identity all-to-all -> kv_unpack)
+    a2a_buf = torch.empty(st["payload_bytes"], dtype=torch.uint8, device="cuda:0")
+    _, mat = plan.stats()
+    nn = mat.shape[0]
+    flat = np.zeros(nn * nn + 1, dtype=np.int64)
+    flat[1:] = np.cumsum(mat.reshape(-1))
+    off = flat[:-1].reshape(nn, nn)
+
+    def pack_unpack():
+        for s_ in range(nn):
+            if mat[s_].sum():
+                F.kv_pack(plan, s_, a2a_buf, off[s_], stream)
+        for d in range(nn):
+            if mat[:, d].sum():
+                F.kv_unpack(plan, d, a2a_buf, off[:, d], stream)
+    ms = timeit(pack_unpack)
+    res["a2a_pack_unpack"] = {"ms": ms, "GBps_of_fused_bytes": algo / ms / 1e6}
+    del a2a_buf
     n = st["payload_bytes"]
     a = torch.empty(n, dtype=torch.uint8, device="cuda:0")
     b = torch.empty(n, dtype=torch.uint8, device="cuda:0")

@@ -41,7 +41,7 @@ def _workload(world, kind="dp_tp"):
     return w
 
 
-def _rank(rank, world, port, outdir, kind):
+def _rank(rank, world, port, outdir, kind, mode="push"):
     import torch
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -61,14 +61,31 @@ def _rank(rank, world, port, outdir, kind):
         if w.src[0][1] > w.H:  # GQA replicated sources: replicas identical (R10)
             raise RuntimeError("replicated sources not used here")
         torch.cuda.synchronize()
-        bases, nbs, imported = comm.exchange_pools(pool, rank, world, w.L, M)
+        if mode == "a2a":  # no peer mappings: other pools' addresses are never dereferenced
+            bases = [[pool[l].data_ptr() if r == rank else (1 << 44) + (r << 36) + (l << 30) for l in range(w.L)]
+                     for r in range(world)]
+            nbs, imported = nb, []
+        else:
+            bases, nbs, imported = comm.exchange_pools(pool, rank, world, w.L, M)
         cache = F.KVCache(g, nbs, bases, [p for p in (2, 4, 8) if p <= world])
         for s_, ids in zip(w.src, tabs):
             cache.reserve(s_, ids)
         stream = torch.cuda.Stream()
         plan = F.kv_plan_switch(cache, [(i, T, s_, ids, d) for i, (T, s_, d, ids) in
                                         enumerate(zip(w.T, w.src, w.dst, tabs))])
-        F.kv_reshard(plan, rank, stream)
+        if mode == "a2a":  # pack -> all_to_all_single (gloo, host copies) -> unpack
+            _, mat = plan.stats()
+            send_off, recv_off = F.a2a_offsets(mat)
+            send = torch.empty(max(int(mat[rank].sum()), 16), dtype=torch.uint8, device="cuda:0")
+            F.kv_pack(plan, rank, send, send_off[rank], stream)
+            stream.synchronize()
+            recv_h = torch.empty(int(mat[:, rank].sum()), dtype=torch.uint8)
+            dist.all_to_all_single(recv_h, send[:int(mat[rank].sum())].cpu(), [int(x) for x in mat[:, rank]],
+                                   [int(x) for x in mat[rank]])
+            recv = recv_h.to("cuda:0") if recv_h.numel() else torch.empty(16, dtype=torch.uint8, device="cuda:0")
+            F.kv_unpack(plan, rank, recv, recv_off[rank], stream)
+        else:
+            F.kv_reshard(plan, rank, stream)
         comm.switch_barrier(stream, None, nccl=False)
         n_res, n_ids = plan.resident(rank)
         rp = torch.empty(n_res + 1, dtype=torch.int32, device="cuda:0")
@@ -87,8 +104,14 @@ def _rank(rank, world, port, outdir, kind):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,kind", [(2, "dp_tp"), (4, "dp_tp"), (4, "tp_dp"), (4, "gqa"), (4, "tp_tp")])
-def test_ipc_push_matches_oracle(world, kind):
+@pytest.mark.parametrize("world,kind,mode", [(2, "dp_tp", "push"), (4, "dp_tp", "push"), (4, "tp_dp", "push"),
+                                             (4, "gqa", "push"), (4, "tp_tp", "push"),
+                                             (2, "dp_tp", "a2a"), (4, "tp_dp", "a2a"), (4, "gqa", "a2a"),
+                                             (4, "tp_tp", "a2a")])
+def test_ipc_push_matches_oracle(world, kind, mode):
+    """push: every rank's reshard kernel stores into peer pools (CUDA IPC).
+    a2a: kv_pack into per-destination chunks, all_to_all_single (gloo over
+    host copies here; NCCL on GPUs), kv_unpack -- no peer mappings at all."""
     import torch.multiprocessing as mp
     w = _workload(world, kind)
     og = O.Geom(*GEOS[kind])
@@ -98,7 +121,7 @@ def test_ipc_push_matches_oracle(world, kind):
     with tempfile.TemporaryDirectory() as td:
         ctx = mp.get_context("spawn")
         port = _free_port()
-        procs = [ctx.Process(target=_rank, args=(r, world, port, td, kind)) for r in range(world)]
+        procs = [ctx.Process(target=_rank, args=(r, world, port, td, kind, mode)) for r in range(world)]
         for p in procs:
             p.start()
         for p in procs:

@@ -24,7 +24,7 @@ def _F():
     return flykv
 
 
-def run_parity(geo, nb, spec, seed=0, per_gpu_launch=False, check_pools=True, staged=False):
+def run_parity(geo, nb, spec, seed=0, per_gpu_launch=False, check_pools=True, staged=False, a2a=False):
     """spec: list of (T, src_group, dst_group).  Runs the product on cuda:0
     (virtual ranks) and the oracle on host copies; asserts exact equality."""
     F = _F()
@@ -64,7 +64,9 @@ def run_parity(geo, nb, spec, seed=0, per_gpu_launch=False, check_pools=True, st
                 hp[:, ids] = host_pools[lo].reshape(og.L, nb[lo], M)[:, ids]
     plan = eng.plan(freqs)
     tables = eng.alloc_tables(plan, range(len(nb))) if (staged or per_gpu_launch) else None
-    if staged:  # comparator path: pack -> staging -> unpack
+    if a2a:  # pack into per-destination chunks -> (identity all-to-all) -> unpack
+        tables, _ = eng.execute_pack_unpack(plan)
+    elif staged:  # comparator path: pack -> staging -> unpack
         st_, _ = plan.stats()
         stg = torch.empty(max(st_["n_atom_slots"] * st_["atom_bytes"], 16), dtype=torch.uint8, device="cuda:0")
         F.kv_reshard_staged(plan, -1, stg, stg.numel(), 1, eng.stream)
@@ -97,6 +99,40 @@ def run_parity(geo, nb, spec, seed=0, per_gpu_launch=False, check_pools=True, st
             bad = np.nonzero(got != host_pools[gpu])[0]
             assert bad.size == 0, f"GPU {gpu}: {bad.size} bytes differ, first at {bad[:5]}"
     return eng, plan, otabs
+
+
+A2A_CASES = [(8, 1, 2), (8, 2, 1), (8, 1, 8), (8, 8, 1), (8, 2, 4), (8, 4, 2), (4, 1, 8), (4, 8, 1), (2, 4, 8),
+             (1, 8, 2), (1, 1, 8), (8, 8, 8)]
+
+
+@pytest.mark.parametrize("H,p0,p1", A2A_CASES)
+@pytest.mark.parametrize("rank_ids", [False, True])
+def test_pack_all_to_all_unpack(H, p0, p1, rank_ids):
+    """kv_pack -> (all-to-all) -> kv_unpack, the per-destination send-buffer
+    path, equals the oracle byte for byte: merges, splits, GQA replication,
+    same-degree regroupings, permuted rank IDs on both sides."""
+    geo = (3, H, 64, 16, 2)
+    rng = np.random.default_rng(H * 100 + p0 * 10 + p1 + 7 * rank_ids)
+    n = 8
+    T = [int(x) for x in rng.integers(1, 700, size=12)]
+    spec = []
+    for i, t in enumerate(T):
+        src = ((i * p0) % n, p0)
+        dst = (((i + 1) * p1) % n, p1)
+        srid = [int(x) for x in rng.permutation(p0)] if rank_ids and p0 > 1 else None
+        drid = [int(x) for x in rng.permutation(p1)] if rank_ids and p1 > 1 else None
+        spec.append((t, src, dst, srid, drid))
+    og = O.Geom(*geo)
+    nb = [0] * n
+    for t, s_, d_, _, _ in spec:
+        for r in range(s_[1]):
+            nb[s_[0] + r] += O.num_blocks(og, t, s_[1])
+        for r in range(d_[1]):
+            nb[d_[0] + r] += O.num_blocks(og, t, d_[1])
+    # sources are scattered over whole pools, so uniform-ID allocation (R6)
+    # over 8 GPUs needs room: 3x the largest per-GPU need
+    nb = [3 * max(nb) + 16] * n
+    run_parity(geo, nb, spec, seed=H + p0 + p1, a2a=True)
 
 
 def test_tiny_config_dp2_tp2_and_back():
@@ -187,7 +223,8 @@ def test_round_trip_restores_contents():
 @pytest.mark.parametrize("cfg,n_req,frag,impl", [("c2", 0, 1.25, 0), ("c4", 0, 1.25, 0), ("c4gqa4", 0, 1.25, 0),
                                                  ("c4gqa1", 0, 1.25, 0), ("c3i", 64, 1.25, 0), ("c3ii", 64, 1.25, 0),
                                                  ("c5", 0, 1.0, 0), ("single", 0, 1.25, 0),
-                                                 ("c2", 0, 1.25, 2), ("c4gqa4", 0, 1.25, 2)])
+                                                 ("c2", 0, 1.25, 2), ("c4gqa4", 0, 1.25, 2),
+                                                 ("c2", 0, 1.25, "a2a"), ("c4gqa1", 0, 1.25, "a2a")])
 def test_full_size_all_atoms(cfg, n_req, frag, impl):
     """Every BASELINE config at the size and in the launch configuration the
     bench times (virtual ranks on one B200, the bench's pool sizing and
@@ -199,14 +236,14 @@ def test_full_size_all_atoms(cfg, n_req, frag, impl):
     variant of the reshard kernel on the same checks."""
     F = _F()
     from paper_2602_22593_b200.engine import KVSwitchEngine
-    F.set_reshard_impl(impl, 0)
+    F.set_reshard_impl(0 if impl == "a2a" else impl, 0)
     try:
-        _full_size_all_atoms(F, KVSwitchEngine, cfg, n_req, frag)
+        _full_size_all_atoms(F, KVSwitchEngine, cfg, n_req, frag, a2a=impl == "a2a")
     finally:
         F.set_reshard_impl(0, 0)
 
 
-def _full_size_all_atoms(F, KVSwitchEngine, cfg, n_req, frag):
+def _full_size_all_atoms(F, KVSwitchEngine, cfg, n_req, frag, a2a=False):
     w = synth.WORKLOADS[cfg]()
     if n_req:
         w = synth.Workload(w.name, w.L, w.H, w.d, w.B, w.e, w.n_gpus, w.T[:n_req], w.src[:n_req], w.dst[:n_req])
@@ -225,7 +262,19 @@ def _full_size_all_atoms(F, KVSwitchEngine, cfg, n_req, frag):
             held[s[0] + r][ids] = 1
         reqs.append((i, T, s, ids, d))
         oreqs.append(O.Req(T, s, list(ids), d))
-    plan, tables, host = eng.switch(reqs, read_back=True)
+    if a2a:  # pack -> all-to-all -> unpack path, then the same checks
+        plan = eng.plan(reqs)
+        eng.execute_pack_unpack(plan)
+        rp_, ids_, meta_ = (x.cpu() for x in eng._packed)
+        host = {}
+        o_r = o_i = 0
+        for gpu in range(w.n_gpus):
+            n_res, n_ids = plan.resident(gpu)
+            host[gpu] = (rp_[o_r + gpu:o_r + gpu + n_res + 1], ids_[o_i:o_i + n_ids], meta_[o_r:o_r + n_res])
+            o_r += n_res
+            o_i += n_ids
+    else:
+        plan, tables, host = eng.switch(reqs, read_back=True)
     st, otabs = O.switch(og, None, held, oreqs, copy=False)
     assert st == 0
     assert [list(a) for a in plan.dst_tables()] == [list(b) for b in otabs]
