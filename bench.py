@@ -62,6 +62,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-parallel", action="store_true", help="skip the all-cores oracle figure")
+    ap.add_argument("--a2a", action="store_true",
+                    help="N>1 comparator: kv_pack -> all_to_all_single -> kv_unpack instead of the P2P-push kernel")
     ap.add_argument("--frag", type=float, default=1.25, help="source placement window / source need")
     ap.add_argument("--pool-slack", type=float, default=1.05, help="pool room beyond the window / max need")
     ap.add_argument("--placement", default="fragmented", choices=["fragmented", "contiguous"],
@@ -653,7 +655,25 @@ def run_multi(args):
             step_stats.append(plan.stats())
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-        F.kv_reshard(plan, rank, stream)
+        if args.a2a:  # comparator: per-destination chunks through NCCL all_to_all_single (gloo: host copies)
+            _, mat = plan.stats()
+            send_off, recv_off = F.a2a_offsets(mat)
+            n_send, n_recv = int(mat[rank].sum()), int(mat[:, rank].sum())
+            send = torch.empty(max(n_send, 16), dtype=torch.uint8, device=dev)
+            recv = torch.empty(max(n_recv, 16), dtype=torch.uint8, device=dev)
+            F.kv_pack(plan, rank, send, send_off[rank], stream)
+            with torch.cuda.stream(stream):
+                outs, ins = [int(x) for x in mat[:, rank]], [int(x) for x in mat[rank]]
+                if nccl:
+                    dist.all_to_all_single(recv[:n_recv], send[:n_send], outs, ins)
+                else:
+                    stream.synchronize()
+                    rh = torch.empty(n_recv, dtype=torch.uint8)
+                    dist.all_to_all_single(rh, send[:n_send].cpu(), outs, ins)
+                    recv[:n_recv].copy_(rh)
+            F.kv_unpack(plan, rank, recv, recv_off[rank], stream)
+        else:
+            F.kv_reshard(plan, rank, stream)
         if timed:
             e1.record(stream)
             ev_pairs.append((e0, e1))
@@ -735,11 +755,13 @@ def run_multi(args):
             "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": w.name + (" (ranks share cuda:0, gloo)" if same_dev else ""), "layers": w.L,
+            "config": {"workload": w.name + (" (ranks share cuda:0, gloo)" if same_dev else "") +
+                       (" [pack -> all_to_all_single -> unpack comparator]" if args.a2a else ""), "layers": w.L,
                        "kv_heads": w.H, "head_dim": w.d, "block_base": w.B, "requests": len(w.T),
                        "tokens": w.tokens(), "payload_bytes_per_step": int(payload),
                        "l2": "inputs larger than L2, no flush needed",
-                       "step": "plan + upload + reshard (P2P push over NVLink) + group barrier + remap"},
+                       "step": ("plan + upload + pack + all_to_all_single + unpack + group barrier + remap" if args.a2a
+                                else "plan + upload + reshard (P2P push over NVLink) + group barrier + remap")},
             "switch_latency_ms": round(total_ms / args.steps, 4),
             "reshard_kernel_ms": round(kern_ms, 4),
             "roofline": ({"bound": "nvlink", "achieved": round(achieved, 1), "peak": FALLBACK_NVLINK_GBS,
