@@ -328,3 +328,28 @@ def test_plan_state_machine():
     dst = plan.dst_tables()[0]
     plan.destroy()
     assert all(c.held_mask(g)[dst].all() for g in (0, 1))
+
+
+def test_pack_unpack_argument_errors():
+    """kv_pack / kv_unpack validate before touching the device: NULL buffer
+    or offsets -> INVALID_ARG, GPU out of range -> INVALID_ARG, committed plan
+    -> BAD_STATE; a2a_offsets gives the all_to_all_single prefixes."""
+    c = fake_cache((1, 4, 8, 4, 2), [32, 32])
+    a = c.alloc((0, 1), 3)
+    plan = c.plan_switch([(1, 12, (0, 1), a, (0, 2))])
+    for fn in (F.kv_pack, F.kv_unpack):
+        with pytest.raises(F.FlyKVError) as e:
+            fn(plan, 0, 0, [0, 0])
+        assert e.value.name == "KV_ERR_INVALID_ARG"
+        with pytest.raises(F.FlyKVError) as e:
+            fn(plan, 2, 1 << 40, [0, 0])
+        assert e.value.name == "KV_ERR_INVALID_ARG"
+    _, mat = plan.stats()
+    send, recv = F.a2a_offsets(mat)
+    # chunk (s -> d) sits at send[s][d] in s's send buffer and at recv[d][s] in d's receive buffer
+    assert send[0][0] == 0 and send[0][1] == mat[0][0] and recv[1][0] == 0 and recv[1][1] == mat[0][1]
+    plan.commit()
+    for fn in (F.kv_pack, F.kv_unpack):
+        with pytest.raises(F.FlyKVError) as e:
+            fn(plan, 0, 1 << 40, [0, 0])
+        assert e.value.name == "KV_ERR_BAD_STATE"
