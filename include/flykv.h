@@ -221,9 +221,10 @@ kv_status kv_reshard_staged(kv_plan* plan, int32_t gpu, void* staging, int64_t s
  * Chunk (s -> d) holds every (atom, replica) sourced on GPU s whose
  * destination is GPU d, its size in bytes is bytes_matrix[s * n_gpus + d] of
  * kv_plan_get_stats.  Its layout: for each of s's segments (requests in plan
- * order), the heads held by d's member of the destination group in
- * ((head index * L + layer) * 2 + K/V) * ceil(T/B) + chunk order, B*d*e bytes
- * each -- a function of the plan alone, so every process derives it.
+ * order), the atoms of the heads held by d's member of the destination group,
+ * B*d*e bytes each, per (layer, K/V) by destination block, then head, then
+ * chunk -- the order in which they fill d's blocks.  A function of the plan
+ * alone, so every process derives it.
  *
  * kv_pack: enqueue on `stream` the gather of GPU src_gpu's atoms into chunks:
  *   buf        device, src_gpu's send buffer

@@ -552,7 +552,7 @@ extern "C" kv_status kv_plan_switch(kv_cache* c, const kv_request* reqs, int32_t
     // ---- pack -> all-to-all -> unpack layout (kv_pack / kv_unpack) ----
     // chunk (s -> d) = for each segment sourced on s (plan order), for the
     // member m of its destination group on d: the atoms of the heads m holds
-    // (rank ID rid = dst_rid[m]) in ((hi * L + l) * 2 + kv) * C + c order
+    // (rank ID rid = dst_rid[m]) in destination-major order (a2a_pos)
     {
         std::vector<int64_t> run((size_t)n * n, 0), tot(n, 0);
         std::vector<std::vector<A2AItem>> per(n);
@@ -577,7 +577,7 @@ extern "C" kv_status kv_plan_switch(kv_cache* c, const kv_request* reqs, int32_t
                 const int64_t cnt = nh_m * per_head;
                 r += cnt;
                 if (cnt > 0) {
-                    per[d].push_back(A2AItem{(int32_t)k, m, rid, 0, tot[d]});
+                    per[d].push_back(A2AItem{(int32_t)k, m, rid, nh_m, tot[d]});
                     tot[d] += cnt;
                 }
             }

@@ -88,8 +88,7 @@ struct ReshardArgs {
     int32_t rep_flags;         // GQA replica stores: bit 0 = decode replicas lane-parallel, bit 1 = replica-major order
     // staged == 3 (kv_pack): every (atom, replica) goes to the send chunk of
     // its destination GPU d at a2a_buf + a2a_off[d] + (base + pos) * atom_bytes,
-    // base = a2a_base[seg.a2a + member], pos = ((hi * L + l) * 2 + kv) * C + c
-    // (hi = index of the head among the segment's heads that member holds)
+    // base = a2a_base[seg.a2a + member], pos = a2a_pos(...) (flykv_kernels.cu)
     const int64_t* a2a_base;
     char* a2a_buf;
     int64_t a2a_off[64];
@@ -97,7 +96,7 @@ struct ReshardArgs {
 
 // One (segment, destination member) pair received by a GPU (kv_unpack).
 struct A2AItem {
-    int32_t seg, m, rid, pad;  // segment, member of its destination group, that member's rank ID
+    int32_t seg, m, rid, nhm;  // segment, member of its destination group, its rank ID, heads it receives
     int64_t start;             // first atom of the pair in the receiver's atom order
 };
 

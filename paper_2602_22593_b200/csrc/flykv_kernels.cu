@@ -42,7 +42,7 @@ struct AtomAddr {
     int32_t dst_g0, rep1, hloc1;
     int32_t dst_inv;   // member-of-rank-ID table offset (-1 = identity rank IDs)
     int32_t kv, c;     // K/V half, chunk (kv_pack's send-chunk position)
-    int32_t h0, C, a2a;  // segment's first head, chunks, chunk-base offset (kv_pack)
+    int32_t h0, nh, C, k1, J1, a2a;  // segment fields kv_pack needs
 };
 
 __device__ __forceinline__ int find_seg(const int64_t* __restrict__ seg_begin, int lo, int hi,
@@ -72,7 +72,10 @@ __device__ __forceinline__ void decode(const ReshardArgs& a, int64_t atom, int s
     out.kv = (int32_t)kv;
     out.c = (int32_t)c;
     out.h0 = sg.h0;
+    out.nh = sg.nh;
     out.C = sg.C;
+    out.k1 = sg.k1;
+    out.J1 = sg.J1;
     out.a2a = sg.a2a;
     if (c >= (uint32_t)sg.C) {  // hole past the request's last chunk
         out.src = nullptr;
@@ -104,15 +107,31 @@ __device__ __forceinline__ void decode(const ReshardArgs& a, int64_t atom, int s
     out.dst_inv = sg.dst_inv;
 }
 
+// Position of an atom in its (segment, member) run of a send chunk: the
+// reshard's destination-major order restricted to the member's nhm heads,
+// holes removed -- per (layer, K/V): destination blocks jb, in each the
+// member's heads hm, in each chunk w < kk (kk = k1, or what is left of C in
+// the last block).  So unpack writes each destination block sequentially.
+__device__ __forceinline__ int64_t a2a_pos(int32_t l, int32_t kv, int32_t c, int32_t hm, int32_t nhm, int32_t C,
+                                           int32_t k1, int32_t J1) {
+    const int32_t jb = c / k1, w = c % k1;
+    const int32_t kk = jb == J1 - 1 ? C - jb * k1 : k1;
+    return (int64_t)(l * 2 + kv) * nhm * C + (int64_t)jb * nhm * k1 + (int64_t)hm * kk + w;
+}
+
 // Pointer to replica j of the decoded atom (1 replica, or p/H under GQA, R2):
 // rank ID owning head h, then the member engine holding that rank ID.
 __device__ __forceinline__ char* dst_ptr(const ReshardArgs& a, const AtomAddr& ad, int j) {
     const int32_t rid = ad.rep1 == 1 ? ad.h / ad.hloc1 : ad.h * ad.rep1 + j;
     const int32_t m = ad.dst_inv < 0 ? rid : __ldg(a.tables + ad.dst_inv + rid);
-    if (a.staged == 3) {  // kv_pack: the send chunk of the destination GPU
-        const int32_t first = rid * ad.hloc1 > ad.h0 ? rid * ad.hloc1 : ad.h0;
-        const int32_t hi = ad.rep1 == 1 ? ad.h - first : 0;
-        const int64_t pos = (((int64_t)hi * a.L + ad.l) * 2 + ad.kv) * ad.C + ad.c;
+    if (a.staged == 3) {  // kv_pack: position in the send chunk of the destination GPU (a2a_pos)
+        int32_t first = ad.h, nhm = 1;
+        if (ad.rep1 == 1) {
+            const int32_t lo = rid * ad.hloc1, hi = lo + ad.hloc1;
+            first = lo > ad.h0 ? lo : ad.h0;
+            nhm = (hi < ad.h0 + ad.nh ? hi : ad.h0 + ad.nh) - first;
+        }
+        const int64_t pos = a2a_pos(ad.l, ad.kv, ad.c, ad.h - first, nhm, ad.C, ad.k1, ad.J1);
         return a.a2a_buf + a.a2a_off[ad.dst_g0 + m] + (__ldg(a.a2a_base + ad.a2a + m) + pos) * a.atom_bytes;
     }
     return a.layer_base[(ad.dst_g0 + m) * a.L + ad.l] + ad.doff;
@@ -307,8 +326,8 @@ __global__ void __launch_bounds__(256, 2) flykv_reshard_kernel(const ReshardArgs
 // ---------------------------------------------------------------- unpack
 // kv_unpack: the receiver's side of pack -> all-to-all -> unpack.  Atom i of
 // the receiver belongs to pair items[k] (start <= i); its position inside
-// that pair, ((hi * L + l) * 2 + kv) * C + c, gives the head, layer, K/V half
-// and chunk, hence the destination address in this GPU's pool; the source is
+// that pair (a2a_pos) gives the layer, K/V half, head and chunk, hence the
+// destination address in this GPU's pool; the source is
 // the chunk received from the segment's source GPU.  Lane-parallel decode as
 // in the reshard kernel: lane k decodes step k, the warp copies by shuffle.
 __device__ __forceinline__ void unpack_decode(const UnpackArgs& a, int64_t atom, const char*& src, char*& dst) {
@@ -321,19 +340,36 @@ __device__ __forceinline__ void unpack_decode(const UnpackArgs& a, int64_t atom,
     const A2AItem it = a.items[lo];
     const Seg sg = a.segs[it.seg];
     const int64_t local = atom - it.start;
-    const int32_t c = (int32_t)(local % sg.C);
-    int64_t t = local / sg.C;
-    const int32_t kv = (int32_t)(t & 1);
-    t >>= 1;
-    const int32_t l = (int32_t)(t % a.L);
-    const int32_t hidx = (int32_t)(t / a.L);
-    const int32_t h = sg.rep1 == 1 ? (it.rid * sg.hloc1 > sg.h0 ? it.rid * sg.hloc1 : sg.h0) + hidx : it.rid / sg.rep1;
+    // invert a2a_pos: (layer, K/V), then destination block, member head, chunk
+    const int32_t nhm = it.nhm;
+    const int64_t per = (int64_t)nhm * sg.C;
+    const int32_t lkv = (int32_t)(local / per);
+    const int32_t r = (int32_t)(local % per);
+    const int32_t kv = lkv & 1, l = lkv >> 1;
+    const int32_t full = (sg.J1 - 1) * nhm * sg.k1;
+    int32_t jb, hm, w;
+    if (r < full) {
+        jb = r / (nhm * sg.k1);
+        const int32_t r2 = r % (nhm * sg.k1);
+        hm = r2 / sg.k1;
+        w = r2 % sg.k1;
+    } else {
+        jb = sg.J1 - 1;
+        const int32_t kk = sg.C - jb * sg.k1, r2 = r - full;
+        hm = r2 / kk;
+        w = r2 % kk;
+    }
+    const int32_t c = jb * sg.k1 + w;
+    const int32_t h = (sg.rep1 == 1 ? (it.rid * sg.hloc1 > sg.h0 ? it.rid * sg.hloc1 : sg.h0) : it.rid / sg.rep1) + hm;
     const int32_t blk1 = __ldg(a.tables + sg.dst_tab + c / sg.k1);
     dst = a.layer_base[(sg.dst_g0 + it.m) * a.L + l] + (int64_t)blk1 * a.M + kv * (a.M >> 1) +
           (int64_t)((h % sg.hloc1) * sg.k1 + c % sg.k1) * a.atom_bytes;
     src = a.buf + a.off[sg.src_gpu] + (__ldg(a.a2a_base + sg.a2a + it.m) + local) * a.atom_bytes;
 }
 
+// VPL = 16-byte vectors per lane per atom (8 for 4 KiB atoms, 0 = generic);
+// U = atoms whose loads are in flight before their stores (as in the reshard).
+template <int VPL, int U>
 __global__ void __launch_bounds__(256) flykv_unpack_kernel(const UnpackArgs a) {
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -347,10 +383,31 @@ __global__ void __launch_bounds__(256) flykv_unpack_kernel(const UnpackArgs a) {
         const char* s = nullptr;
         char* d = nullptr;
         if (lane < n) unpack_decode(a, first + lane * nwarps, s, d);
-        for (int k = 0; k < n; ++k) {
-            const int4* sk = reinterpret_cast<const int4*>(shfl_ptr(s, k));
-            int4* dk = reinterpret_cast<int4*>(shfl_ptr(d, k));
-            for (int i = lane; i < nv; i += 32) st_stream(dk + i, ld_stream(sk + i));
+        if constexpr (VPL > 0) {
+            for (int k0 = 0; k0 < n; k0 += U) {
+                int4 v[U][VPL];
+                int4* dk[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int k = k0 + u < n ? k0 + u : k0;
+                    const int4* sk = reinterpret_cast<const int4*>(shfl_ptr(s, k)) + lane;
+                    dk[u] = k0 + u < n ? reinterpret_cast<int4*>(shfl_ptr(d, k)) + lane : nullptr;
+#pragma unroll
+                    for (int i = 0; i < VPL; ++i) v[u][i] = ld_stream(sk + i * 32);
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    if (dk[u] == nullptr) continue;  // past the round (warp-uniform)
+#pragma unroll
+                    for (int i = 0; i < VPL; ++i) st_stream(dk[u] + i * 32, v[u][i]);
+                }
+            }
+        } else {
+            for (int k = 0; k < n; ++k) {
+                const int4* sk = reinterpret_cast<const int4*>(shfl_ptr(s, k));
+                int4* dk = reinterpret_cast<int4*>(shfl_ptr(d, k));
+                for (int i = lane; i < nv; i += 32) st_stream(dk + i, ld_stream(sk + i));
+            }
         }
     }
 }
@@ -359,10 +416,24 @@ static int sm_count_of(int device);
 
 cudaError_t launch_unpack(const UnpackArgs& a, int device, cudaStream_t s) {
     if (a.n_atoms <= 0) return cudaSuccess;
-    int64_t want = (a.n_atoms + 255) / 256;
-    int64_t cap = (int64_t)sm_count_of(device) * 2;
+    // experiment knob FLYKV_UNPACK_SHAPE: 0 = U2 x 1 CTA/SM, 1 = U1 x 2, 2 = U2 x 2, 3 = U1 x 4.
+    // Default 2: its reads stream the receive buffer, so unlike the reshard it
+    // wants 12 warps per SM (c2 unpack 6.30 ms vs 8.07 with 6 warps;
+    // profiles/r01_a2a_comparator.jsonl).
+    static int shape = -1;
+    if (shape < 0) {
+        const char* e = getenv("FLYKV_UNPACK_SHAPE");
+        shape = e ? atoi(e) : 2;
+    }
+    const int per = shape == 0 ? 1 : shape == 3 ? 4 : 2;
+    const bool u2 = shape == 0 || shape == 2;
+    const int64_t want = (a.n_atoms + 6 * 32 - 1) / (6 * 32);
+    const int64_t cap = (int64_t)sm_count_of(device) * per;
     const int grid = (int)(want < cap ? (want > 0 ? want : 1) : cap);
-    flykv_unpack_kernel<<<grid, 192, 0, s>>>(a);
+    if (a.atom_bytes == 4096 && u2) flykv_unpack_kernel<8, 2><<<grid, 192, 0, s>>>(a);
+    else if (a.atom_bytes == 4096) flykv_unpack_kernel<8, 1><<<grid, 192, 0, s>>>(a);
+    else if (a.atom_bytes == 2048) flykv_unpack_kernel<4, 2><<<grid, 192, 0, s>>>(a);
+    else flykv_unpack_kernel<0, 1><<<grid, 192, 0, s>>>(a);
     return cudaGetLastError();
 }
 

@@ -86,6 +86,18 @@ def main():
                 F.kv_unpack(plan, d, a2a_buf, off[:, d], stream)
     ms = timeit(pack_unpack)
     res["a2a_pack_unpack"] = {"ms": ms, "GBps_of_fused_bytes": algo / ms / 1e6}
+
+    def pack_only():
+        for s_ in range(nn):
+            if mat[s_].sum():
+                F.kv_pack(plan, s_, a2a_buf, off[s_], stream)
+
+    def unpack_only():
+        for d in range(nn):
+            if mat[:, d].sum():
+                F.kv_unpack(plan, d, a2a_buf, off[:, d], stream)
+    res["a2a_pack_only_ms"] = timeit(pack_only)
+    res["a2a_unpack_only_ms"] = timeit(unpack_only)
     del a2a_buf
     n = st["payload_bytes"]
     a = torch.empty(n, dtype=torch.uint8, device="cuda:0")
