@@ -274,6 +274,30 @@ kv_status kv_plan_resident(const kv_plan* plan, int32_t gpu, int32_t* n_resident
 kv_status kv_remap_block_tables(kv_plan* plan, int32_t gpu, int32_t* req_ptr, int32_t* block_ids,
                                 int32_t* per_req_meta, void* stream);
 
+/*
+ * kv_switch: the whole switch in one call, for a process that addresses
+ * every pool (virtual ranks, or peers mapped into one process):
+ * kv_plan_switch -> descriptor upload -> kv_reshard(all pools) -> (stream
+ * order is the barrier, a5) -> kv_remap_block_tables(all pools) into a
+ * plan-owned device buffer -> one device->host copy of every pool's table ->
+ * stream synchronisation.  On KV_OK the switch has completed, the plan is
+ * committed (sources released, R13) and kv_plan_tables gives the tables on
+ * the device (for the attention kernels) and on the host.  Errors from the
+ * planner leave no state change and *out NULL; a CUDA error after the remap
+ * returns the (committed) plan in *out so the caller can destroy it.
+ * Switch latency (R15) is this call's wall time.  Not for one process per
+ * GPU: there the group barrier sits between reshard and remap.
+ */
+kv_status kv_switch(kv_cache* cache, const kv_request* reqs, int32_t n_reqs, void* stream, kv_plan** out);
+
+/* kv_plan_tables: pool gpu's post-switch table of a plan run by kv_switch,
+ * as pointers into plan-owned memory (valid until kv_plan_destroy):
+ * on_device != 0 -> device pointers, else host pointers.  Layout as written
+ * by kv_remap_block_tables (sizes from kv_plan_resident).  BAD_STATE if the
+ * plan was not executed by kv_switch. */
+kv_status kv_plan_tables(const kv_plan* plan, int32_t gpu, int32_t on_device, const int32_t** req_ptr,
+                         const int32_t** block_ids, const int32_t** per_req_meta);
+
 /* kv_plan_commit: a7 on the host -- release every moving request's source
  * IDs (R13).  Implied by the first kv_remap_block_tables; call it directly
  * when the caller builds its block tables itself.  Idempotent.  Only after

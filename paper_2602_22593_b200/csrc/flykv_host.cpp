@@ -79,6 +79,9 @@ struct kv_cache {
     size_t stage_bytes = 0;
     cudaEvent_t stage_ev = nullptr;
     bool stage_pending = false;
+    // pinned landing buffer of kv_switch's one device->host table copy
+    void* back = nullptr;
+    size_t back_bytes = 0;
 };
 
 struct ReqPlan {
@@ -120,6 +123,11 @@ struct kv_plan {
     size_t dbytes = 0;
     size_t off_seg_begin = 0, off_segs = 0, off_tables = 0, off_recs = 0, off_outs = 0, off_a2a = 0, off_items = 0;
     cudaStream_t last_stream = nullptr;
+    // kv_switch: packed all-pool tables [req_ptr | block_ids | meta] on the
+    // device (plan-owned, from the cache's pool) and their host copy
+    int32_t* d_out = nullptr;
+    std::vector<int32_t> h_out;
+    int64_t out_rp = 0, out_ids = 0;  // element offsets of block_ids and meta in the packed buffer
 };
 
 // ------------------------------------------------------------ helpers
@@ -244,6 +252,7 @@ extern "C" void kv_cache_destroy(kv_cache* c) {
         cudaEventDestroy(c->stage_ev);
     }
     if (c->stage) cudaFreeHost(c->stage);
+    if (c->back) cudaFreeHost(c->back);
     if (c->d_layer_base) cudaFree(c->d_layer_base);
     if (c->pool) cudaMemPoolDestroy(c->pool);
     delete c;
@@ -1043,7 +1052,70 @@ extern "C" void kv_plan_destroy(kv_plan* p) {
         }
     }
     if (p->dbuf) cudaFreeAsync(p->dbuf, p->last_stream);
+    if (p->d_out) cudaFreeAsync(p->d_out, p->last_stream);
     delete p;
+}
+
+extern "C" kv_status kv_switch(kv_cache* c, const kv_request* reqs, int32_t n_reqs, void* stream_, kv_plan** out) {
+    if (!out) return fail(KV_ERR_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    kv_plan* p = nullptr;
+    kv_status s = kv_plan_switch(c, reqs, n_reqs, &p);
+    if (s) return s;
+    cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+    int32_t tot_res = 0, tot_ids = 0;
+    kv_plan_resident(p, -1, &tot_res, &tot_ids);
+    const int32_t n = c->n_gpus;
+    p->out_rp = tot_res + n;
+    p->out_ids = p->out_rp + tot_ids;
+    const int64_t elems = p->out_ids + 4 * (int64_t)tot_res;
+    auto abort_plan = [&](kv_status st) {
+        kv_plan_destroy(p);
+        return st;
+    };
+    s = ensure_device(p, stream);
+    if (s) return abort_plan(s);
+    p->last_stream = stream;
+    cudaError_t e = cudaMallocFromPoolAsync(reinterpret_cast<void**>(&p->d_out), (size_t)elems * 4, c->pool, stream);
+    if (e != cudaSuccess) return abort_plan(cuda_fail(e, "cudaMallocFromPoolAsync (tables)"));
+    s = kv_reshard(p, -1, stream);
+    if (s) return abort_plan(s);
+    // a5 is stream order here: every pool is addressable from this device
+    s = kv_remap_block_tables(p, -1, p->d_out, p->d_out + p->out_rp, p->d_out + p->out_ids, stream);
+    if (s) {  // the plan committed inside the remap call only if it got that far
+        *out = p;
+        return s;
+    }
+    if ((size_t)elems * 4 > c->back_bytes) {
+        if (c->back) cudaFreeHost(c->back);
+        c->back = nullptr;
+        c->back_bytes = 0;
+        const size_t want = std::max((size_t)elems * 4, (size_t)1 << 20);
+        e = cudaMallocHost(&c->back, want);
+        if (e != cudaSuccess) {
+            *out = p;
+            return cuda_fail(e, "cudaMallocHost (tables)");
+        }
+        c->back_bytes = want;
+    }
+    e = cudaMemcpyAsync(c->back, p->d_out, (size_t)elems * 4, cudaMemcpyDeviceToHost, stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+    *out = p;
+    if (e != cudaSuccess) return cuda_fail(e, "kv_switch table read-back");
+    p->h_out.assign(static_cast<int32_t*>(c->back), static_cast<int32_t*>(c->back) + elems);
+    return KV_OK;
+}
+
+extern "C" kv_status kv_plan_tables(const kv_plan* p, int32_t gpu, int32_t on_device, const int32_t** req_ptr,
+                                    const int32_t** block_ids, const int32_t** per_req_meta) {
+    if (!p || gpu < 0 || gpu >= p->c->n_gpus) return fail(KV_ERR_INVALID_ARG, "bad kv_plan_tables arguments");
+    if (!p->d_out) return fail(KV_ERR_BAD_STATE, "plan was not executed by kv_switch");
+    const int32_t* base = on_device ? p->d_out : p->h_out.data();
+    const int32_t* off = p->out_off.data() + 3 * gpu;  // packed layout of kv_remap_block_tables(gpu = -1)
+    if (req_ptr) *req_ptr = base + off[0];
+    if (block_ids) *block_ids = base + p->out_rp + off[1];
+    if (per_req_meta) *per_req_meta = base + p->out_ids + off[2];
+    return KV_OK;
 }
 
 // ------------------------------------------------------------ weight views

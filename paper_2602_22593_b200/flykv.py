@@ -120,6 +120,8 @@ _sig("kv_reshard", C.c_int, _P, C.c_int32, _P)
 _sig("kv_plan_resident", C.c_int, _P, C.c_int32, _I32P, _I32P)
 _sig("kv_reshard_staged", C.c_int, _P, C.c_int32, _P, C.c_int64, C.c_int32, _P)
 _sig("kv_remap_block_tables", C.c_int, _P, C.c_int32, _P, _P, _P, _P)
+_sig("kv_switch", C.c_int, _P, C.POINTER(Request), C.c_int32, _P, C.POINTER(_P))
+_sig("kv_plan_tables", C.c_int, _P, C.c_int32, C.c_int32, C.POINTER(_I32P), C.POINTER(_I32P), C.POINTER(_I32P))
 _sig("kv_pack", C.c_int, _P, C.c_int32, _P, _I64P, _P)
 _sig("kv_unpack", C.c_int, _P, C.c_int32, _P, _I64P, _P)
 _sig("kv_plan_dst_tables", C.c_int, _P, _I32P, _I32P)
@@ -148,7 +150,7 @@ _sig("kv_set_reshard_impl", C.c_int, C.c_int32, C.c_int32)
 
 EXPORTED = ["kv_cache_create", "kv_cache_destroy", "kv_layout", "kv_blocks_for", "kv_alloc", "kv_reserve",
             "kv_free", "kv_free_count", "kv_held_mask", "kv_plan_switch", "kv_plan_upload", "kv_reshard", "kv_reshard_staged",
-            "kv_pack", "kv_unpack", "kv_plan_resident",
+            "kv_pack", "kv_unpack", "kv_switch", "kv_plan_tables", "kv_plan_resident",
             "kv_remap_block_tables", "kv_plan_dst_tables", "kv_plan_commit", "kv_plan_waves", "kv_suggest_rank_ids", "kv_plan_get_stats", "kv_plan_destroy",
             "weight_shard_view", "kv_gather_view", "kv_vmm_granularity", "kv_vmm_alloc", "kv_vmm_free",
             "weight_view_alias", "weight_view_unalias", "kv_paged_decode", "kv_ipc_export", "kv_ipc_import", "kv_ipc_close",
@@ -309,6 +311,27 @@ class Plan:
         _check(_lib.kv_plan_dst_tables(self._h, ptr.ctypes.data_as(_I32P), ids.ctypes.data_as(_I32P)))
         return [ids[ptr[i]:ptr[i + 1]].copy() for i in range(self.n_reqs)]
 
+    def _tables(self, gpu: int, on_device: int):
+        rp, ids, meta = _I32P(), _I32P(), _I32P()
+        _check(_lib.kv_plan_tables(self._h, gpu, on_device, C.byref(rp), C.byref(ids), C.byref(meta)))
+        n_res, n_ids = self.resident(gpu)
+        return (C.cast(rp, C.c_void_p).value or 0, C.cast(ids, C.c_void_p).value or 0,
+                C.cast(meta, C.c_void_p).value or 0, n_res, n_ids)
+
+    def host_tables(self, gpu: int):
+        """(req_ptr, block_ids, meta) of pool gpu after kv_switch, as numpy copies."""
+        rp, ids, meta, n_res, n_ids = self._tables(gpu, 0)
+
+        def arr(ptr, n):
+            if n == 0:
+                return np.zeros(0, dtype=np.int32)
+            return np.ctypeslib.as_array(C.cast(ptr, _I32P), shape=(n,)).copy()
+        return arr(rp, n_res + 1), arr(ids, n_ids), arr(meta, 4 * n_res).reshape(n_res, 4)
+
+    def device_tables(self, gpu: int):
+        """(req_ptr, block_ids, meta, n_resident, n_ids) device pointers (ints) of pool gpu after kv_switch."""
+        return self._tables(gpu, 1)
+
     def stats(self):
         st = PlanStats()
         n = self.cache.n_gpus
@@ -387,6 +410,22 @@ def kv_plan_switch(cache: KVCache, requests) -> Plan:
     h = C.c_void_p()
     _check(_lib.kv_plan_switch(cache._h, ra.ptr, ra.n, C.byref(h)))
     return Plan(cache, h, ra.n)
+
+
+def kv_switch(cache: KVCache, requests, stream=None) -> Plan:
+    """The whole single-process switch in one C call (plan, upload, reshard,
+    remap, one table read-back, sync); tables via Plan.host_tables /
+    Plan.device_tables."""
+    ra = make_requests(requests)
+    h = C.c_void_p()
+    st = _lib.kv_switch(cache._h, ra.ptr, ra.n, stream_of(stream), C.byref(h))
+    plan = Plan(cache, h, ra.n) if h.value else None
+    if st != KV_OK:
+        msg = _lib.kv_last_error().decode()
+        if plan is not None:
+            plan.destroy()
+        raise FlyKVError(st, msg)
+    return plan
 
 
 def kv_suggest_rank_ids(cache: KVCache, requests, dst) -> list:

@@ -545,3 +545,71 @@ def test_rank_ids_parity(H, p0, p1):
         drid = [int(x) for x in rng.permutation(p1)]
         spec.append((T, src, dst, srid, drid))
     run_parity(geo, [400] * 8, spec, seed=H + p0 + p1)
+
+
+@pytest.mark.parametrize("H,p0,p1", [(8, 1, 2), (8, 2, 1), (4, 1, 8), (8, 4, 8)])
+def test_kv_switch_one_call(H, p0, p1):
+    """kv_switch (plan, upload, reshard, remap, read-back, sync in one C call)
+    leaves the same pools, allocator state and tables as the oracle; its
+    device tables equal its host tables."""
+    F = _F()
+    from paper_2602_22593_b200.engine import KVSwitchEngine
+    geo = (2, H, 64, 16, 2)
+    og = O.Geom(*geo)
+    n = 8
+    rng = np.random.default_rng(H + p0 + p1)
+    T = [int(x) for x in rng.integers(1, 500, size=10)]
+    spec = [(t, ((i * p0) % n, p0), (((i + 1) * p1) % n, p1)) for i, t in enumerate(T)]
+    nb = [0] * n
+    for t, s_, d_ in spec:
+        for r in range(s_[1]):
+            nb[s_[0] + r] += O.num_blocks(og, t, s_[1])
+        for r in range(d_[1]):
+            nb[d_[0] + r] += O.num_blocks(og, t, d_[1])
+    nb = [3 * max(nb) + 16] * n
+    eng = KVSwitchEngine(F.geometry(*geo), nb, "cuda:0")
+    for gpu, t in enumerate(eng.pools.tensors):
+        synth.fill_hash_torch(t, gpu, seed=3)
+    torch.cuda.synchronize()
+    host_pools = [t.cpu().numpy().reshape(-1).copy() for t in eng.pools.tensors]
+    w = synth.Workload("t", *geo, n, T, [x[1] for x in spec], [x[2] for x in spec])
+    tabs0 = synth.source_tables(w, [O.num_blocks(og, t, s_[1]) for t, s_, _ in spec], nb, seed=4)
+    held = [np.zeros(k, dtype=np.uint8) for k in nb]
+    oreqs, freqs = [], []
+    for i, ((t, s_, d_), ids) in enumerate(zip(spec, tabs0)):
+        eng.cache.reserve(s_, ids)
+        for r in range(s_[1]):
+            held[s_[0] + r][ids] = 1
+        oreqs.append(O.Req(t, s_, list(ids), d_))
+        freqs.append((i, t, s_, ids, d_))
+    if p0 > H:  # replicated sources identical (R10)
+        M = O.block_bytes(og)
+        for (t, s_, _), ids in zip(spec, tabs0):
+            for r in range(1, s_[1]):
+                lo = s_[0] + (r // (p0 // H)) * (p0 // H)
+                if lo != s_[0] + r:
+                    idx = torch.as_tensor(np.asarray(ids, dtype=np.int64), device="cuda:0")
+                    eng.pools.tensors[s_[0] + r][:, idx] = eng.pools.tensors[lo][:, idx]
+                    hp = host_pools[s_[0] + r].reshape(og.L, nb[0], M)
+                    hp[:, ids] = host_pools[lo].reshape(og.L, nb[0], M)[:, ids]
+    plan = F.kv_switch(eng.cache, freqs, eng.stream)
+    st, otabs = O.switch(og, host_pools, held, oreqs)
+    assert st == 0
+    assert [list(a) for a in plan.dst_tables()] == [list(b) for b in otabs]
+    for gpu in range(n):
+        assert np.array_equal(eng.cache.held_mask(gpu), held[gpu])
+        rp, ids, meta = O.tables(og, gpu, oreqs, otabs)
+        hrp, hids, hmeta = plan.host_tables(gpu)
+        assert np.array_equal(hrp, rp) and np.array_equal(hids, ids) and np.array_equal(hmeta, meta)
+        drp, dids, dmeta, n_res, n_ids = plan.device_tables(gpu)
+        got = torch.zeros(n_res + 1 + n_ids + 4 * n_res, dtype=torch.int32, device="cuda:0")
+        for ptr, k, o in ((drp, n_res + 1, 0), (dids, n_ids, n_res + 1), (dmeta, 4 * n_res, n_res + 1 + n_ids)):
+            if k:  # device-to-device copy of k int32 through a one-row view (gather kernel)
+                v = F.View()
+                v.n_seg, v.elem_bytes = 1, 4
+                v.seg[0].ptr, v.seg[0].rows, v.seg[0].cols, v.seg[0].ld = ptr, 1, k, k
+                F.kv_gather_view(v, got.data_ptr() + 4 * o)
+        torch.cuda.synchronize()
+        assert np.array_equal(got.cpu().numpy(), np.concatenate([hrp, hids, hmeta.reshape(-1)]))
+    for gpu, t in enumerate(eng.pools.tensors):
+        assert np.array_equal(t.cpu().numpy().reshape(-1), host_pools[gpu]), f"pool {gpu} differs"
