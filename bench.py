@@ -558,13 +558,17 @@ def run_single(args):
                    "rank_ids": args.rank_ids, "link_GBps": FALLBACK_NVLINK_GBS,
                    "note": "model of an N-GPU run from the plan's byte matrix, not measured"}
         del off
-    traffic = None
+    # DRAM bytes of one forward launch from a committed ncu --set full capture
+    # (plus that launch's algorithmic bytes: under GQA the two directions of
+    # a step move different byte counts, so compare the ratio)
+    traffic = traffic_ratio = None
     tpath = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.config}.json")
-    if os.path.exists(tpath):
+    if os.path.exists(tpath) and not args.requests:
         try:
-            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+            tj = json.load(open(tpath))
+            traffic, traffic_ratio = tj.get("dram_bytes_per_launch"), tj.get("traffic_over_algorithmic")
         except Exception:
-            traffic = None
+            traffic = traffic_ratio = None
     cpu = None
     if not args.no_cpu_baseline:
         gbs, sec, info, _ = cpu_oracle_run(w, args.cpu_baseline_reqs, args.cpu_baseline_steps, 0)

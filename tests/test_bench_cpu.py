@@ -49,3 +49,27 @@ def test_reference_arm_other_ranks_print_nothing():
 def test_all_cores_oracle_figure():
     gbs, threads, info = bench.cpu_oracle_parallel(synth.WORKLOADS["tiny"](), reqs_per_thread=2, steps=2)
     assert gbs > 0 and 1 <= threads <= 4 and "threads" in info
+
+
+def test_bench_has_no_undefined_names():
+    """bench.py's GPU paths cannot run here; at least every name they load is
+    bound somewhere (a crude pyflakes: catches typos in rarely-run branches)."""
+    import ast
+    import builtins
+    for path in ("bench.py", "__graft_entry__.py", os.path.join("paper_2602_22593_b200", "engine.py"),
+                 os.path.join("paper_2602_22593_b200", "comm.py")):
+        tree = ast.parse(open(os.path.join(ROOT, path)).read())
+        bound = set(dir(builtins)) | {"__file__"}
+        for node in ast.walk(tree):
+            if isinstance(node, (ast.FunctionDef, ast.ClassDef)):
+                bound.add(node.name)
+            elif isinstance(node, ast.arg):
+                bound.add(node.arg)
+            elif isinstance(node, ast.Name) and isinstance(node.ctx, (ast.Store, ast.Del)):
+                bound.add(node.id)
+            elif isinstance(node, (ast.Import, ast.ImportFrom)):
+                bound.update((a.asname or a.name).split(".")[0] for a in node.names)
+            elif isinstance(node, ast.ExceptHandler) and node.name:
+                bound.add(node.name)
+        loaded = {n.id for n in ast.walk(tree) if isinstance(n, ast.Name) and isinstance(n.ctx, ast.Load)}
+        assert loaded <= bound, f"{path}: undefined {sorted(loaded - bound)}"
