@@ -2,8 +2,9 @@
  * c_switch_demo.c -- the C ABI used from plain C (no Python, no torch).
  *
  * Allocates two paged KV pools with cudaMalloc (virtual ranks on one GPU),
- * registers three live DP requests, switches them DP2 -> TP2 and back with
- * kv_plan_switch / kv_reshard / kv_remap_block_tables, and checks the round
+ * registers three live DP requests, switches them DP2 -> TP2 with
+ * kv_plan_switch / kv_reshard / kv_remap_block_tables and back with the
+ * one-call kv_switch, and checks the round
  * trip: every source block of every layer is back, byte for byte, in the
  * blocks of the final DP tables (a DP block holds B tokens of all heads, so
  * whole blocks round-trip).  Exit code 0 on success.
@@ -57,6 +58,40 @@ static int switch_all(kv_cache* c, kv_request* r, int n, int32_t** out_tabs, int
         cudaFree(rp);
         cudaFree(ids);
         cudaFree(meta);
+    }
+    {
+        int32_t ptr[NREQ + 1];
+        int32_t all[4 * NB];
+        CHECK(kv_plan_dst_tables(p, ptr, all));
+        for (i = 0; i < n; ++i) {
+            out_len[i] = ptr[i + 1] - ptr[i];
+            memcpy(out_tabs[i], all + ptr[i], (size_t)out_len[i] * 4);
+        }
+    }
+    kv_plan_destroy(p);
+    return 0;
+}
+
+/* The same switch through kv_switch: one call plans, moves, remaps and
+ * reads every pool's new table back; kv_plan_tables exposes them. */
+static int switch_one_call(kv_cache* c, kv_request* r, int n, int32_t** out_tabs, int32_t* out_len) {
+    kv_plan* p = NULL;
+    int g, i;
+    CHECK(kv_switch(c, r, n, NULL, &p));
+    for (g = 0; g < 2; ++g) {
+        const int32_t *rp, *ids, *meta;
+        int32_t nres = 0, nids = 0;
+        CHECK(kv_plan_resident(p, g, &nres, &nids));
+        CHECK(kv_plan_tables(p, g, 0, &rp, &ids, &meta));
+        if (rp[0] != 0 || rp[nres] != nids) {
+            fprintf(stderr, "GPU %d: bad CSR table from kv_switch\n", g);
+            return 1;
+        }
+        for (i = 0; i < nres; ++i)  /* meta: plan index, B(p), H_loc, first head */
+            if (meta[4 * i + 1] != 16 || meta[4 * i + 2] != 4) {
+                fprintf(stderr, "GPU %d: bad per-request meta\n", g);
+                return 1;
+            }
     }
     {
         int32_t ptr[NREQ + 1];
@@ -126,7 +161,7 @@ int main(void) {
         kv_request r = {100 + i, T[i], src, tab1[i], len1[i], dst};
         req[i] = r;
     }
-    if (switch_all(c, req, NREQ, tab2, len2)) return 1;
+    if (switch_one_call(c, req, NREQ, tab2, len2)) return 1;
 
     for (g = 0; g < 2; ++g) CUDA(cudaMemcpy(after + g * bytes, pool[g], bytes, cudaMemcpyDeviceToHost));
     for (i = 0; i < NREQ; ++i) {
@@ -146,7 +181,7 @@ int main(void) {
         int32_t f0, f1;
         CHECK(kv_free_count(c, 0, &f0));
         CHECK(kv_free_count(c, 1, &f1));
-        printf("c_switch_demo ok: %d requests DP2->TP2->DP2 round-trip byte-exact; free blocks %d/%d; "
+        printf("c_switch_demo ok: %d requests DP2->TP2 (step by step) ->DP2 (kv_switch) round-trip byte-exact; free blocks %d/%d; "
                "%lld kernel launches\n", NREQ, f0, f1, (long long)kv_launch_count());
     }
     kv_cache_destroy(c);
