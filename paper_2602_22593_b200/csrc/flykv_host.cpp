@@ -412,26 +412,23 @@ static kv_status validate_requests(const kv_cache* c, const kv_request* reqs, in
     return KV_OK;
 }
 
-extern "C" kv_status kv_plan_switch(kv_cache* c, const kv_request* reqs, int32_t n_reqs, kv_plan** out) {
-    if (!c || !out || n_reqs < 0 || (n_reqs > 0 && !reqs))
-        return fail(KV_ERR_INVALID_ARG, "bad kv_plan_switch arguments");
-    *out = nullptr;
-    const kv_geometry& G = c->geo;
-    const int32_t H = G.num_kv_heads, L = G.num_layers, B = G.block_base;
-    const int32_t n = c->n_gpus;
+// ---- kv_plan_switch, step by step ----
 
-    // ---- a2 validation (no state change) ----
-    int64_t total_src = 0, total_dst_bound = 0;
-    kv_status vs = validate_requests(c, reqs, n_reqs, &total_src, &total_dst_bound);
-    if (vs) return vs;
+// Release the destination allocations of requests [0, upto) of a plan that
+// will not run (failed planning, or destroyed before committing): S:207.
+static void rollback_allocations(kv_plan* p, int32_t upto) {
+    kv_cache* c = p->c;
+    for (int32_t j = 0; j < upto; ++j) {
+        const ReqPlan& u = p->reqs[j];
+        if (!u.moving) continue;
+        for (int32_t r = 0; r < u.dst.degree; ++r)
+            for (int32_t k = 0; k < u.n1; ++k) bit_clr(c->held[u.dst.first_gpu + r], p->tables[u.dst_off + k]);
+    }
+}
 
-    kv_plan* p = new (std::nothrow) kv_plan();
-    if (!p) return fail(KV_ERR_INVALID_ARG, "out of host memory");
-    p->c = c;
-    p->reqs.resize(n_reqs);
-    p->tables.reserve((size_t)(total_src + total_dst_bound + n_reqs));
-
-    // source tables first
+// Per-request records and source tables (a2): rank IDs (identity unless
+// given), and whether the request moves (R12/R19).
+static void init_requests(kv_plan* p, const kv_request* reqs, int32_t n_reqs) {
     for (int32_t i = 0; i < n_reqs; ++i) {
         const kv_request& r = reqs[i];
         ReqPlan& q = p->reqs[i];
@@ -445,19 +442,23 @@ extern "C" kv_status kv_plan_switch(kv_cache* c, const kv_request* reqs, int32_t
         }
         q.dst_rid_identity = true;
         for (int32_t m = 0; m < r.dst.degree; ++m) q.dst_rid_identity &= q.dst_rid[m] == m;
-        bool same_ids = true;
-        for (int32_t m = 0; m < r.src.degree; ++m) same_ids &= q.src_rid[m] == q.dst_rid[m];
-        q.moving = !(r.src.first_gpu == r.dst.first_gpu && r.src.degree == r.dst.degree && same_ids);
+        q.moving = request_moves(r);
         q.src_off = (int32_t)p->tables.size();
         q.n0 = r.n_src_blocks;
         p->tables.insert(p->tables.end(), r.src_blocks, r.src_blocks + r.n_src_blocks);
     }
+}
 
-    // ---- a3 allocation, request order, lowest common free IDs ----
-    for (int32_t i = 0; i < n_reqs; ++i) {
+// a3: destination tables in request order, lowest common free IDs (R6, R8);
+// a no-op keeps its table (R12).  Returns the first request that does not
+// fit (its predecessors' allocations are still held), or -1.
+static int32_t allocate_destinations(kv_plan* p) {
+    kv_cache* c = p->c;
+    const int32_t H = c->geo.num_kv_heads, B = c->geo.block_base;
+    for (int32_t i = 0; i < (int32_t)p->reqs.size(); ++i) {
         ReqPlan& q = p->reqs[i];
         q.dst_off = (int32_t)p->tables.size();
-        if (!q.moving) {  // no-op keeps its table (R12)
+        if (!q.moving) {
             q.n1 = q.n0;
             for (int32_t k = 0; k < q.n0; ++k) p->tables.push_back(p->tables[q.src_off + k]);
             continue;
@@ -465,153 +466,149 @@ extern "C" kv_status kv_plan_switch(kv_cache* c, const kv_request* reqs, int32_t
         const Layout l1 = layout_of(H, q.dst.degree);
         q.n1 = (int32_t)ceil_div(q.T, (int64_t)B * l1.k);
         p->tables.resize(p->tables.size() + q.n1);
-        if (!alloc_lowest(c, q.dst, q.n1, p->tables.data() + q.dst_off)) {
-            // roll back this plan's allocations: state unchanged
-            for (int32_t j = 0; j < i; ++j) {
-                const ReqPlan& u = p->reqs[j];
-                if (!u.moving) continue;
-                for (int32_t r = 0; r < u.dst.degree; ++r)
-                    for (int32_t k = 0; k < u.n1; ++k) bit_clr(c->held[u.dst.first_gpu + r], p->tables[u.dst_off + k]);
-            }
-            delete p;
-            return fail(KV_ERR_OUT_OF_BLOCKS, "request %d needs %d blocks on group [%d,+%d)", i, q.n1,
-                        q.dst.first_gpu, q.dst.degree);
-        }
+        if (!alloc_lowest(c, q.dst, q.n1, p->tables.data() + q.dst_off)) return i;
     }
+    return -1;
+}
 
-    // ---- rank-ID tables of non-identity destinations: rank ID of
-    // member m (remap's first head) and member of rank ID (reshard's owner) ----
-    std::vector<int32_t> dst_rid_off(n_reqs, -1), dst_inv_off(n_reqs, -1);
+// Rank-ID tables of non-identity destinations: rank ID of member m
+// (remap's first head) and member of rank ID (reshard's owner lookup).
+static void rank_id_tables(kv_plan* p, std::vector<int32_t>& rid_off, std::vector<int32_t>& inv_off) {
+    const int32_t n_reqs = (int32_t)p->reqs.size();
+    rid_off.assign(n_reqs, -1);
+    inv_off.assign(n_reqs, -1);
     for (int32_t i = 0; i < n_reqs; ++i) {
         const ReqPlan& q = p->reqs[i];
         if (q.dst_rid_identity) continue;
-        dst_rid_off[i] = (int32_t)p->tables.size();
+        rid_off[i] = (int32_t)p->tables.size();
         p->tables.insert(p->tables.end(), q.dst_rid, q.dst_rid + q.dst.degree);
-        dst_inv_off[i] = (int32_t)p->tables.size();
+        inv_off[i] = (int32_t)p->tables.size();
         p->tables.resize(p->tables.size() + q.dst.degree);
-        for (int32_t m = 0; m < q.dst.degree; ++m) p->tables[dst_inv_off[i] + q.dst_rid[m]] = m;
+        for (int32_t m = 0; m < q.dst.degree; ++m) p->tables[inv_off[i] + q.dst_rid[m]] = m;
     }
+}
 
-    // ---- work segments: (request, canonical source replica) ----
+// Work segments (request, canonical source replica R10), the per-(source,
+// destination) byte matrix, grouped by source GPU (stable: request order
+// within a GPU).  seg_req: the request of each segment.  Returns the first
+// request whose atom count overflows the device's 32-bit per-segment slot
+// index, or -1.
+static int32_t build_segments(kv_plan* p, const std::vector<int32_t>& inv_off, std::vector<Seg>& segs,
+                              std::vector<int32_t>& seg_req) {
+    const kv_cache* c = p->c;
+    const int32_t H = c->geo.num_kv_heads, L = c->geo.num_layers, B = c->geo.block_base, n = c->n_gpus;
     p->bytes.assign((size_t)n * n, 0);
-    std::vector<Seg> segs;
-    std::vector<int32_t> seg_req;  // request of each segment
-    for (int32_t i = 0; i < n_reqs; ++i) {
+    for (int32_t i = 0; i < (int32_t)p->reqs.size(); ++i) {
         const ReqPlan& q = p->reqs[i];
         if (!q.moving) continue;
         const int32_t C = (int32_t)ceil_div(q.T, B);
         if (C == 0) continue;
-        if ((int64_t)L * 2 * (C + H) * H >= ((int64_t)1 << 31)) {  // per-segment slot index is 32-bit on the device
-            for (int32_t j = 0; j < n_reqs; ++j) {
-                const ReqPlan& u = p->reqs[j];
-                if (!u.moving) continue;
-                for (int32_t r = 0; r < u.dst.degree; ++r)
-                    for (int32_t k = 0; k < u.n1; ++k) bit_clr(c->held[u.dst.first_gpu + r], p->tables[u.dst_off + k]);
-            }
-            delete p;
-            return fail(KV_ERR_INVALID_ARG, "request %d: %lld atoms exceed the 2^31 per-request limit", i,
-                        (long long)L * 2 * C * H);
-        }
+        if ((int64_t)L * 2 * (C + H) * H >= ((int64_t)1 << 31)) return i;
         const Layout l0 = layout_of(H, q.src.degree), l1 = layout_of(H, q.dst.degree);
         int32_t inv1[64];
         for (int32_t m = 0; m < q.dst.degree; ++m) inv1[q.dst_rid[m]] = m;
         for (int32_t m = 0; m < q.src.degree; ++m) {
             const int32_t rid = q.src_rid[m];         // member m holds rank ID rid's slice
             if (l0.rep > 1 && rid % l0.rep) continue;  // only replica 0 of each head is read (R10)
-            Seg s{};
-            s.src_gpu = q.src.first_gpu + m;
-            s.dst_g0 = q.dst.first_gpu;
-            s.C = C;
-            s.J1 = (int32_t)ceil_div(C, l1.k);
-            s.nh = l0.hloc;
-            s.h0 = first_head_of_rank(l0, rid);
-            s.dst_inv = dst_inv_off[i];
-            s.src_tab = q.src_off;
-            s.dst_tab = q.dst_off;
-            s.hloc0 = l0.hloc;
-            s.k0 = l0.k;
-            s.hloc1 = l1.hloc;
-            s.k1 = l1.k;
-            s.rep1 = l1.rep;
-            segs.push_back(s);
+            Seg sg{};
+            sg.src_gpu = q.src.first_gpu + m;
+            sg.dst_g0 = q.dst.first_gpu;
+            sg.C = C;
+            sg.J1 = (int32_t)ceil_div(C, l1.k);
+            sg.nh = l0.hloc;
+            sg.h0 = first_head_of_rank(l0, rid);
+            sg.dst_inv = inv_off[i];
+            sg.src_tab = q.src_off;
+            sg.dst_tab = q.dst_off;
+            sg.hloc0 = l0.hloc;
+            sg.k0 = l0.k;
+            sg.hloc1 = l1.hloc;
+            sg.k1 = l1.k;
+            sg.rep1 = l1.rep;
+            segs.push_back(sg);
             seg_req.push_back(i);
             const int64_t head_bytes = (int64_t)L * 2 * C * c->atom_bytes;
-            for (int32_t hh = 0; hh < s.nh; ++hh)
+            for (int32_t hh = 0; hh < sg.nh; ++hh)
                 for (int32_t j = 0; j < l1.rep; ++j) {
-                    const int32_t dg = s.dst_g0 + inv1[owner_rank(l1, s.h0 + hh, j)];
-                    p->bytes[(size_t)s.src_gpu * n + dg] += head_bytes;
+                    const int32_t dg = sg.dst_g0 + inv1[owner_rank(l1, sg.h0 + hh, j)];
+                    p->bytes[(size_t)sg.src_gpu * n + dg] += head_bytes;
                 }
         }
     }
-    // group segments by source GPU (stable: request order within a GPU)
-    {
-        std::vector<int32_t> order(segs.size());
-        for (size_t k = 0; k < order.size(); ++k) order[k] = (int32_t)k;
-        std::stable_sort(order.begin(), order.end(),
-                         [&](int32_t a, int32_t b) { return segs[a].src_gpu < segs[b].src_gpu; });
-        std::vector<Seg> s2(segs.size());
-        std::vector<int32_t> r2(segs.size());
-        for (size_t k = 0; k < order.size(); ++k) {
-            s2[k] = segs[order[k]];
-            r2[k] = seg_req[order[k]];
-        }
-        segs.swap(s2);
-        seg_req.swap(r2);
+    std::vector<int32_t> order(segs.size());
+    for (size_t k = 0; k < order.size(); ++k) order[k] = (int32_t)k;
+    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return segs[a].src_gpu < segs[b].src_gpu; });
+    std::vector<Seg> s2(segs.size());
+    std::vector<int32_t> r2(segs.size());
+    for (size_t k = 0; k < order.size(); ++k) {
+        s2[k] = segs[order[k]];
+        r2[k] = seg_req[order[k]];
     }
-    // ---- pack -> all-to-all -> unpack layout (kv_pack / kv_unpack) ----
-    // chunk (s -> d) = for each segment sourced on s (plan order), for the
-    // member m of its destination group on d: the atoms of the heads m holds
-    // (rank ID rid = dst_rid[m]) in destination-major order (a2a_pos)
-    {
-        std::vector<int64_t> run((size_t)n * n, 0), tot(n, 0);
-        std::vector<std::vector<A2AItem>> per(n);
-        for (size_t k = 0; k < segs.size(); ++k) {
-            Seg& sg = segs[k];
-            const ReqPlan& q = p->reqs[seg_req[k]];
-            sg.a2a = (int32_t)p->a2a_base.size();
-            const int64_t per_head = (int64_t)L * 2 * sg.C;
-            for (int32_t m = 0; m < q.dst.degree; ++m) {
-                const int32_t rid = q.dst_rid[m];
-                int32_t nh_m;
-                if (sg.rep1 == 1) {
-                    const int32_t lo = std::max(sg.h0, rid * sg.hloc1), hi = std::min(sg.h0 + sg.nh, (rid + 1) * sg.hloc1);
-                    nh_m = std::max(0, hi - lo);
-                } else {
-                    const int32_t h = rid / sg.rep1;
-                    nh_m = (h >= sg.h0 && h < sg.h0 + sg.nh) ? 1 : 0;
-                }
-                const int32_t d = sg.dst_g0 + m;
-                int64_t& r = run[(size_t)sg.src_gpu * n + d];
-                p->a2a_base.push_back(r);
-                const int64_t cnt = nh_m * per_head;
-                r += cnt;
-                if (cnt > 0) {
-                    per[d].push_back(A2AItem{(int32_t)k, m, rid, nh_m, tot[d]});
-                    tot[d] += cnt;
-                }
+    segs.swap(s2);
+    seg_req.swap(r2);
+    return -1;
+}
+
+// Pack -> all-to-all -> unpack layout (kv_pack / kv_unpack).  Chunk (s -> d)
+// = for each segment sourced on s (plan order), for the member m of its
+// destination group on d: the atoms of the heads m holds (rank ID
+// dst_rid[m]) in destination-major order (a2a_pos in flykv_kernels.cu).
+static void build_a2a_layout(kv_plan* p, std::vector<Seg>& segs, const std::vector<int32_t>& seg_req) {
+    const int32_t L = p->c->geo.num_layers, n = p->c->n_gpus;
+    std::vector<int64_t> run((size_t)n * n, 0), tot(n, 0);
+    std::vector<std::vector<A2AItem>> per(n);
+    for (size_t k = 0; k < segs.size(); ++k) {
+        Seg& sg = segs[k];
+        const ReqPlan& q = p->reqs[seg_req[k]];
+        sg.a2a = (int32_t)p->a2a_base.size();
+        const int64_t per_head = (int64_t)L * 2 * sg.C;
+        for (int32_t m = 0; m < q.dst.degree; ++m) {
+            const int32_t rid = q.dst_rid[m];
+            int32_t nh_m;
+            if (sg.rep1 == 1) {
+                const int32_t lo = std::max(sg.h0, rid * sg.hloc1), hi = std::min(sg.h0 + sg.nh, (rid + 1) * sg.hloc1);
+                nh_m = std::max(0, hi - lo);
+            } else {
+                const int32_t h = rid / sg.rep1;
+                nh_m = (h >= sg.h0 && h < sg.h0 + sg.nh) ? 1 : 0;
+            }
+            const int32_t d = sg.dst_g0 + m;
+            int64_t& r = run[(size_t)sg.src_gpu * n + d];
+            p->a2a_base.push_back(r);
+            const int64_t cnt = nh_m * per_head;
+            r += cnt;
+            if (cnt > 0) {
+                per[d].push_back(A2AItem{(int32_t)k, m, rid, nh_m, tot[d]});
+                tot[d] += cnt;
             }
         }
-        p->item_lo.assign(n, 0);
-        p->item_hi.assign(n, 0);
-        p->recv_atoms = tot;
-        for (int32_t d = 0; d < n; ++d) {
-            p->item_lo[d] = (int32_t)p->items.size();
-            p->items.insert(p->items.end(), per[d].begin(), per[d].end());
-            p->item_hi[d] = (int32_t)p->items.size();
-        }
     }
-    p->segs = segs;
+    p->item_lo.assign(n, 0);
+    p->item_hi.assign(n, 0);
+    p->recv_atoms = tot;
+    for (int32_t d = 0; d < n; ++d) {
+        p->item_lo[d] = (int32_t)p->items.size();
+        p->items.insert(p->items.end(), per[d].begin(), per[d].end());
+        p->item_hi[d] = (int32_t)p->items.size();
+    }
+}
+
+// The kernels' atom index: exclusive prefix of each segment's slots (holes
+// of the destination-major order included), each source GPU's segment
+// range, and the plan's atom statistics.
+static void index_segments(kv_plan* p) {
+    const int32_t L = p->c->geo.num_layers, n = p->c->n_gpus;
+    const std::vector<Seg>& segs = p->segs;
     p->seg_begin.resize(segs.size() + 1);
     p->gpu_seg_lo.assign(n, 0);
     p->gpu_seg_hi.assign(n, 0);
     int64_t acc = 0, atoms = 0, writes = 0;
-    for (size_t s = 0; s < segs.size(); ++s) {
-        p->seg_begin[s] = acc;
-        const int64_t slots = (int64_t)L * 2 * segs[s].J1 * segs[s].nh * segs[s].k1;  // incl. holes
-        const int64_t a = (int64_t)L * 2 * segs[s].C * segs[s].nh;                     // real atoms
-        acc += slots;
+    for (size_t k = 0; k < segs.size(); ++k) {
+        p->seg_begin[k] = acc;
+        acc += (int64_t)L * 2 * segs[k].J1 * segs[k].nh * segs[k].k1;  // incl. holes
+        const int64_t a = (int64_t)L * 2 * segs[k].C * segs[k].nh;     // real atoms
         atoms += a;
-        writes += a * segs[s].rep1;
+        writes += a * segs[k].rep1;
     }
     p->seg_begin[segs.size()] = acc;
     for (int32_t g = 0; g < n; ++g) {
@@ -620,8 +617,15 @@ extern "C" kv_status kv_plan_switch(kv_cache* c, const kv_request* reqs, int32_t
         p->gpu_seg_lo[g] = (int32_t)(lo - segs.begin());
         p->gpu_seg_hi[g] = (int32_t)(hi - segs.begin());
     }
+    p->st.n_atoms = atoms;
+    p->st.n_atom_slots = acc;
+    p->st.n_atom_writes = writes;
+}
 
-    // ---- per-GPU residency (a6 sizes) and remap records ----
+// a6 sizes and the remap kernel's per-request records; packed all-pool output
+// offsets of kv_remap_block_tables(gpu = -1).
+static void build_remap_records(kv_plan* p, const std::vector<int32_t>& rid_off) {
+    const int32_t n = p->c->n_gpus, n_reqs = (int32_t)p->reqs.size();
     p->n_res.assign(n, 0);
     p->n_res_ids.assign(n, 0);
     p->recs.resize(n_reqs);
@@ -629,39 +633,80 @@ extern "C" kv_status kv_plan_switch(kv_cache* c, const kv_request* reqs, int32_t
     for (int32_t i = 0; i < n_reqs; ++i) {
         const ReqPlan& q = p->reqs[i];
         n_moving += q.moving;
-        p->recs[i] = ReqRec{q.dst.first_gpu, q.dst.degree, q.n1, q.dst_off, dst_rid_off[i], {0, 0, 0}};
+        p->recs[i] = ReqRec{q.dst.first_gpu, q.dst.degree, q.n1, q.dst_off, rid_off[i], {0, 0, 0}};
         for (int32_t r = 0; r < q.dst.degree; ++r) {
             p->n_res[q.dst.first_gpu + r] += 1;
             p->n_res_ids[q.dst.first_gpu + r] += q.n1;
         }
     }
-
-    // ---- device workspace layout ----
-    auto align = [](size_t x) { return (x + 255) & ~(size_t)255; };
-    p->off_seg_begin = 0;
-    p->off_segs = align(p->off_seg_begin + p->seg_begin.size() * sizeof(int64_t));
-    p->off_tables = align(p->off_segs + p->segs.size() * sizeof(Seg));
-    p->off_recs = align(p->off_tables + p->tables.size() * sizeof(int32_t));
     p->out_off.assign((size_t)n * 3, 0);
-    for (int32_t g = 0, r0 = 0, i0 = 0; g < n; ++g) {  // packed outputs of kv_remap_block_tables(gpu = -1)
+    for (int32_t g = 0, r0 = 0, i0 = 0; g < n; ++g) {
         p->out_off[3 * g + 0] = r0 + g;  // req_ptr rows: n_res[g] + 1 each
         p->out_off[3 * g + 1] = i0;
         p->out_off[3 * g + 2] = 4 * r0;
         r0 += p->n_res[g];
         i0 += p->n_res_ids[g];
     }
+    p->st.n_requests = n_reqs;
+    p->st.n_moving = n_moving;
+}
+
+// Device workspace: [seg_begin | segs | tables | recs | out_off | a2a_base | items], 256-byte aligned.
+static void layout_workspace(kv_plan* p) {
+    auto align = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    p->off_seg_begin = 0;
+    p->off_segs = align(p->off_seg_begin + p->seg_begin.size() * sizeof(int64_t));
+    p->off_tables = align(p->off_segs + p->segs.size() * sizeof(Seg));
+    p->off_recs = align(p->off_tables + p->tables.size() * sizeof(int32_t));
     p->off_outs = align(p->off_recs + p->recs.size() * sizeof(ReqRec));
     p->off_a2a = align(p->off_outs + p->out_off.size() * sizeof(int32_t));
     p->off_items = align(p->off_a2a + p->a2a_base.size() * sizeof(int64_t));
     p->dbytes = align(p->off_items + p->items.size() * sizeof(A2AItem));
+}
 
-    p->st.n_requests = n_reqs;
-    p->st.n_moving = n_moving;
-    p->st.n_atoms = atoms;
-    p->st.n_atom_slots = acc;
-    p->st.n_atom_writes = writes;
+extern "C" kv_status kv_plan_switch(kv_cache* c, const kv_request* reqs, int32_t n_reqs, kv_plan** out) {
+    if (!c || !out || n_reqs < 0 || (n_reqs > 0 && !reqs))
+        return fail(KV_ERR_INVALID_ARG, "bad kv_plan_switch arguments");
+    *out = nullptr;
+    int64_t total_src = 0, total_dst_bound = 0;
+    kv_status vs = validate_requests(c, reqs, n_reqs, &total_src, &total_dst_bound);  // a2, no state change
+    if (vs) return vs;
+    kv_plan* p = new (std::nothrow) kv_plan();
+    if (!p) return fail(KV_ERR_INVALID_ARG, "out of host memory");
+    p->c = c;
+    p->reqs.resize(n_reqs);
+    p->tables.reserve((size_t)(total_src + total_dst_bound + n_reqs));
+    init_requests(p, reqs, n_reqs);
+    const int32_t full = allocate_destinations(p);
+    if (full >= 0) {
+        rollback_allocations(p, full);
+        const ReqPlan& q = p->reqs[full];
+        kv_status st = fail(KV_ERR_OUT_OF_BLOCKS, "request %d needs %d blocks on group [%d,+%d)", full, q.n1,
+                            q.dst.first_gpu, q.dst.degree);
+        delete p;
+        return st;
+    }
+    std::vector<int32_t> rid_off, inv_off;
+    rank_id_tables(p, rid_off, inv_off);
+    std::vector<Seg> segs;
+    std::vector<int32_t> seg_req;
+    const int32_t big = build_segments(p, inv_off, segs, seg_req);
+    if (big >= 0) {
+        rollback_allocations(p, n_reqs);
+        const int64_t atoms = (int64_t)c->geo.num_layers * 2 * ceil_div(p->reqs[big].T, c->geo.block_base) *
+                              c->geo.num_kv_heads;
+        kv_status st = fail(KV_ERR_INVALID_ARG, "request %d: %lld atoms exceed the 2^31 per-request limit", big,
+                            (long long)atoms);
+        delete p;
+        return st;
+    }
+    build_a2a_layout(p, segs, seg_req);
+    p->segs.swap(segs);
+    index_segments(p);
+    build_remap_records(p, rid_off);
+    layout_workspace(p);
     p->st.atom_bytes = c->atom_bytes;
-    p->st.payload_bytes = writes * c->atom_bytes;
+    p->st.payload_bytes = p->st.n_atom_writes * c->atom_bytes;
     p->st.h2d_bytes = (int64_t)p->dbytes;
     p->st.n_segments = (int64_t)p->segs.size();
     *out = p;
@@ -1043,14 +1088,7 @@ extern "C" kv_status kv_plan_get_stats(const kv_plan* p, kv_plan_stats* st, int6
 
 extern "C" void kv_plan_destroy(kv_plan* p) {
     if (!p) return;
-    if (p->state == PLAN_PLANNED) {  // roll back destination allocations
-        kv_cache* c = p->c;
-        for (const ReqPlan& q : p->reqs) {
-            if (!q.moving) continue;
-            for (int32_t r = 0; r < q.dst.degree; ++r)
-                for (int32_t k = 0; k < q.n1; ++k) bit_clr(c->held[q.dst.first_gpu + r], p->tables[q.dst_off + k]);
-        }
-    }
+    if (p->state == PLAN_PLANNED) rollback_allocations(p, (int32_t)p->reqs.size());
     if (p->dbuf) cudaFreeAsync(p->dbuf, p->last_stream);
     if (p->d_out) cudaFreeAsync(p->d_out, p->last_stream);
     delete p;
