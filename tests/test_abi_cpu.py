@@ -353,3 +353,42 @@ def test_pack_unpack_argument_errors():
         with pytest.raises(F.FlyKVError) as e:
             fn(plan, 0, 1 << 40, [0, 0])
         assert e.value.name == "KV_ERR_BAD_STATE"
+
+
+def test_free_ten_thousand_random_requests():
+    """SPEC S:236 / S:250: 10,000 random requests admitted into random aligned
+    groups and freed in random order; allocated + free == num_blocks on every
+    GPU after every operation, the product's choices equal the oracle's
+    allocator, and the pools end empty."""
+    from oracle import brute
+    nb = 400
+    c = fake_cache((1, 8, 8, 4, 2), [nb] * 8)
+    og = O.Geom(1, 8, 8, 4, 2)
+    held = [np.zeros(nb, dtype=np.uint8) for _ in range(8)]
+    rng = np.random.default_rng(236)
+    live = []
+    admitted = 0
+    while admitted < 10000:
+        if live and (rng.random() < 0.45 or len(live) > 60):
+            grp, ids = live.pop(int(rng.integers(len(live))))
+            c.free(grp, ids)
+            for r in range(grp[1]):
+                held[grp[0] + r][ids] = 0
+        else:
+            p = int(rng.choice([1, 2, 4, 8]))
+            grp = (int(rng.integers(8 // p)) * p, p)
+            n = O.num_blocks(og, int(rng.integers(1, 200)), p)
+            want = brute.lowest_common_free(held, grp, n)
+            if want is None:
+                continue
+            ids = c.alloc(grp, n)
+            assert list(ids) == list(want)
+            for r in range(p):
+                held[grp[0] + r][ids] = 1
+            live.append((grp, ids))
+            admitted += 1
+        for g in range(8):
+            assert c.free_count(g) + int(held[g].sum()) == nb
+    for grp, ids in live:
+        c.free(grp, ids)
+    assert all(c.free_count(g) == nb for g in range(8))

@@ -613,3 +613,32 @@ def test_kv_switch_one_call(H, p0, p1):
         assert np.array_equal(got.cpu().numpy(), np.concatenate([hrp, hids, hmeta.reshape(-1)]))
     for gpu, t in enumerate(eng.pools.tensors):
         assert np.array_equal(t.cpu().numpy().reshape(-1), host_pools[gpu]), f"pool {gpu} differs"
+
+
+def test_weight_switches_allocate_nothing():
+    """S:152 / P:297 'no tensor movement': 1,000 DP<->TP weight-mode switches
+    (Eq.1 views of a Llama-3-70B-shaped W^QKV at degrees 1/2/4/8, each also
+    aliased contiguously over the replica's physical memory and released)
+    allocate no device memory: torch's allocator and the driver's free-memory
+    count are unchanged afterwards."""
+    F = _F()
+    Hq, Hkv, d, hidden = 64, 8, 128, 8192
+    rows = (Hq + 2 * Hkv) * d
+    buf = F.VmmBuffer(rows * hidden * 2)
+    torch.cuda.synchronize()
+    alloc0 = torch.cuda.memory_allocated()
+    free0, _ = torch.cuda.mem_get_info()
+    degrees = [1, 2, 4, 8]
+    for k in range(1000):
+        m = degrees[k % 4]
+        r = (k // 4) % m
+        v = F.weight_shard_view(F.weight_desc(buf.ptr, rows, hidden, 2, F.KV_W_QKV, num_q_heads=Hq, num_kv_heads=Hkv,
+                                              head_dim=d), r, m)
+        assert sum(s.rows for s in v.segments()) * hidden * 2 <= rows * hidden * 2
+        ptr, nbytes = F.weight_view_alias(buf, v)
+        F.weight_view_unalias(ptr, nbytes)
+    torch.cuda.synchronize()
+    free1, _ = torch.cuda.mem_get_info()
+    assert torch.cuda.memory_allocated() == alloc0
+    assert abs(free1 - free0) < 64 * 2 ** 20, (free0, free1)   # driver bookkeeping only, no weight copies
+    buf.close()
