@@ -640,5 +640,5 @@ def test_weight_switches_allocate_nothing():
     torch.cuda.synchronize()
     free1, _ = torch.cuda.mem_get_info()
     assert torch.cuda.memory_allocated() == alloc0
-    assert abs(free1 - free0) < 64 * 2 ** 20, (free0, free1)   # driver bookkeeping only, no weight copies
+    assert abs(free1 - free0) < 4 * 2 ** 20, (free0, free1)   # driver bookkeeping only: one TP8 view copy is 21 MB
     buf.close()
