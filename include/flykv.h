@@ -290,6 +290,14 @@ kv_status kv_remap_block_tables(kv_plan* plan, int32_t gpu, int32_t* req_ptr, in
  */
 kv_status kv_switch(kv_cache* cache, const kv_request* reqs, int32_t n_reqs, void* stream, kv_plan** out);
 
+/* kv_switch_back: kv_switch of the inverse of a committed plan -- every
+ * request from its destination (table, rank IDs) back to its source group
+ * (the paper's reset_TP_mode after set_TP_mode), built inside the
+ * library from the plan (no request list crosses the ABI).  The new plan
+ * allocates fresh blocks like any switch.  BAD_STATE if prev is not
+ * committed; INVALID_ARG if prev belongs to another cache. */
+kv_status kv_switch_back(kv_cache* cache, const kv_plan* prev, void* stream, kv_plan** out);
+
 /* kv_plan_tables: pool gpu's post-switch table of a plan run by kv_switch,
  * as pointers into plan-owned memory (valid until kv_plan_destroy):
  * on_device != 0 -> device pointers, else host pointers.  Layout as written

@@ -1144,6 +1144,28 @@ extern "C" kv_status kv_switch(kv_cache* c, const kv_request* reqs, int32_t n_re
     return KV_OK;
 }
 
+extern "C" kv_status kv_switch_back(kv_cache* c, const kv_plan* prev, void* stream, kv_plan** out) {
+    if (!c || !prev || !out) return fail(KV_ERR_INVALID_ARG, "bad kv_switch_back arguments");
+    *out = nullptr;
+    if (prev->c != c) return fail(KV_ERR_INVALID_ARG, "plan belongs to another cache");
+    if (prev->state != PLAN_COMMITTED) return fail(KV_ERR_BAD_STATE, "previous plan is not committed");
+    // every request of prev, from its destination (table, rank IDs) back to its source
+    std::vector<kv_request> reqs(prev->reqs.size());
+    for (size_t i = 0; i < prev->reqs.size(); ++i) {
+        const ReqPlan& q = prev->reqs[i];
+        kv_request& r = reqs[i];
+        r.req_id = q.req_id;
+        r.num_tokens = q.T;
+        r.src = q.dst;
+        r.src_blocks = prev->tables.data() + q.dst_off;
+        r.n_src_blocks = q.n1;
+        r.dst = q.src;
+        r.src_rank_ids = q.dst_rid;
+        r.dst_rank_ids = q.src_rid;
+    }
+    return kv_switch(c, reqs.data(), (int32_t)reqs.size(), stream, out);
+}
+
 extern "C" kv_status kv_plan_tables(const kv_plan* p, int32_t gpu, int32_t on_device, const int32_t** req_ptr,
                                     const int32_t** block_ids, const int32_t** per_req_meta) {
     if (!p || gpu < 0 || gpu >= p->c->n_gpus) return fail(KV_ERR_INVALID_ARG, "bad kv_plan_tables arguments");

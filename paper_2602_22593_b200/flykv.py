@@ -122,6 +122,7 @@ _sig("kv_reshard_staged", C.c_int, _P, C.c_int32, _P, C.c_int64, C.c_int32, _P)
 _sig("kv_remap_block_tables", C.c_int, _P, C.c_int32, _P, _P, _P, _P)
 _sig("kv_switch", C.c_int, _P, C.POINTER(Request), C.c_int32, _P, C.POINTER(_P))
 _sig("kv_plan_tables", C.c_int, _P, C.c_int32, C.c_int32, C.POINTER(_I32P), C.POINTER(_I32P), C.POINTER(_I32P))
+_sig("kv_switch_back", C.c_int, _P, _P, _P, C.POINTER(_P))
 _sig("kv_pack", C.c_int, _P, C.c_int32, _P, _I64P, _P)
 _sig("kv_unpack", C.c_int, _P, C.c_int32, _P, _I64P, _P)
 _sig("kv_plan_dst_tables", C.c_int, _P, _I32P, _I32P)
@@ -150,7 +151,7 @@ _sig("kv_set_reshard_impl", C.c_int, C.c_int32, C.c_int32)
 
 EXPORTED = ["kv_cache_create", "kv_cache_destroy", "kv_layout", "kv_blocks_for", "kv_alloc", "kv_reserve",
             "kv_free", "kv_free_count", "kv_held_mask", "kv_plan_switch", "kv_plan_upload", "kv_reshard", "kv_reshard_staged",
-            "kv_pack", "kv_unpack", "kv_switch", "kv_plan_tables", "kv_plan_resident",
+            "kv_pack", "kv_unpack", "kv_switch", "kv_switch_back", "kv_plan_tables", "kv_plan_resident",
             "kv_remap_block_tables", "kv_plan_dst_tables", "kv_plan_commit", "kv_plan_waves", "kv_suggest_rank_ids", "kv_plan_get_stats", "kv_plan_destroy",
             "weight_shard_view", "kv_gather_view", "kv_vmm_granularity", "kv_vmm_alloc", "kv_vmm_free",
             "weight_view_alias", "weight_view_unalias", "kv_paged_decode", "kv_ipc_export", "kv_ipc_import", "kv_ipc_close",
@@ -420,6 +421,20 @@ def kv_switch(cache: KVCache, requests, stream=None) -> Plan:
     h = C.c_void_p()
     st = _lib.kv_switch(cache._h, ra.ptr, ra.n, stream_of(stream), C.byref(h))
     plan = Plan(cache, h, ra.n) if h.value else None
+    if st != KV_OK:
+        msg = _lib.kv_last_error().decode()
+        if plan is not None:
+            plan.destroy()
+        raise FlyKVError(st, msg)
+    return plan
+
+
+def kv_switch_back(cache: KVCache, prev: Plan, stream=None) -> Plan:
+    """kv_switch of the inverse of a committed plan (every request back to its
+    source group), built inside the library."""
+    h = C.c_void_p()
+    st = _lib.kv_switch_back(cache._h, prev._h, stream_of(stream), C.byref(h))
+    plan = Plan(cache, h, prev.n_reqs) if h.value else None
     if st != KV_OK:
         msg = _lib.kv_last_error().decode()
         if plan is not None:

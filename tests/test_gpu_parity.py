@@ -551,7 +551,8 @@ def test_rank_ids_parity(H, p0, p1):
 def test_kv_switch_one_call(H, p0, p1):
     """kv_switch (plan, upload, reshard, remap, read-back, sync in one C call)
     leaves the same pools, allocator state and tables as the oracle; its
-    device tables equal its host tables."""
+    device tables equal its host tables; kv_switch_back of it equals the
+    oracle's inverse switch."""
     F = _F()
     from paper_2602_22593_b200.engine import KVSwitchEngine
     geo = (2, H, 64, 16, 2)
@@ -613,6 +614,19 @@ def test_kv_switch_one_call(H, p0, p1):
         assert np.array_equal(got.cpu().numpy(), np.concatenate([hrp, hids, hmeta.reshape(-1)]))
     for gpu, t in enumerate(eng.pools.tensors):
         assert np.array_equal(t.cpu().numpy().reshape(-1), host_pools[gpu]), f"pool {gpu} differs"
+    # and back: kv_switch_back builds the inverse requests inside the library
+    back = F.kv_switch_back(eng.cache, plan, eng.stream)
+    oback = [O.Req(t, d_, list(tab), s_) for (t, s_, d_), tab in zip(spec, otabs)]
+    st, otabs2 = O.switch(og, host_pools, held, oback)
+    assert st == 0
+    assert [list(a) for a in back.dst_tables()] == [list(b) for b in otabs2]
+    for gpu in range(n):
+        assert np.array_equal(eng.cache.held_mask(gpu), held[gpu])
+        rp, ids, meta = O.tables(og, gpu, oback, otabs2)
+        hrp, hids, hmeta = back.host_tables(gpu)
+        assert np.array_equal(hrp, rp) and np.array_equal(hids, ids) and np.array_equal(hmeta, meta)
+    for gpu, t in enumerate(eng.pools.tensors):
+        assert np.array_equal(t.cpu().numpy().reshape(-1), host_pools[gpu]), f"pool {gpu} differs after switch back"
 
 
 def test_weight_switches_allocate_nothing():
