@@ -107,7 +107,8 @@ def _rank(rank, world, port, outdir, kind, mode="push"):
 @pytest.mark.parametrize("world,kind,mode", [(2, "dp_tp", "push"), (4, "dp_tp", "push"), (4, "tp_dp", "push"),
                                              (4, "gqa", "push"), (4, "tp_tp", "push"),
                                              (2, "dp_tp", "a2a"), (4, "tp_dp", "a2a"), (4, "gqa", "a2a"),
-                                             (4, "tp_tp", "a2a")])
+                                             (4, "tp_tp", "a2a"), (8, "dp_tp", "push"), (8, "gqa", "push"),
+                                             (8, "tp_tp", "a2a")])
 def test_ipc_push_matches_oracle(world, kind, mode):
     """push: every rank's reshard kernel stores into peer pools (CUDA IPC).
     a2a: kv_pack into per-destination chunks, all_to_all_single (gloo over
