@@ -3,8 +3,11 @@
 One call = one live DP<->TP switch of a set of requests:
   kv_plan_switch (host: validate, allocate, plan; descriptors uploaded once)
   -> kv_reshard  (sm_100a kernel, the hot loop)
-  -> kv_remap_block_tables per pool (sm_100a kernel; commits the plan)
-  -> optional read-back of the new block tables to pinned host memory.
+  -> kv_remap_block_tables for every pool in one launch (sm_100a kernel;
+     commits the plan), into torch tensors the caller can hand to attention
+  -> optional read-back of the new block tables to host memory.
+flykv.kv_switch / kv_switch_back do the same in one C call with plan-owned
+tables; execute_pack_unpack runs the pack -> all-to-all -> unpack variant.
 torch supplies device memory and streams only.  Single process: every pool
 lives on devices this process can address (virtual ranks on one B200, or
 peer-enabled GPUs).  One process per GPU: see comm.py.
