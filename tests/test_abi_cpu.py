@@ -392,3 +392,28 @@ def test_free_ten_thousand_random_requests():
     for grp, ids in live:
         c.free(grp, ids)
     assert all(c.free_count(g) == nb for g in range(8))
+
+
+def test_kv_switch_errors_before_the_device():
+    """kv_switch fails in planning with no state change (OUT_OF_BLOCKS), and
+    kv_switch_back refuses an uncommitted plan (BAD_STATE) or a plan of
+    another cache (INVALID_ARG) -- all before any device work."""
+    c = fake_cache((1, 4, 8, 4, 2), [8, 8])
+    a = c.alloc((0, 1), 6)
+    before = [c.held_mask(g).copy() for g in (0, 1)]
+    with pytest.raises(F.FlyKVError) as e:
+        F.kv_switch(c, [(1, 24, (0, 1), a, (0, 2))])   # needs 3 blocks on both GPUs; GPU 0 has 2 free
+    assert e.value.name == "KV_ERR_OUT_OF_BLOCKS"
+    assert all(np.array_equal(c.held_mask(g), before[g]) for g in (0, 1))
+    plan = c.plan_switch([(1, 8, (0, 1), a[:2], (0, 2))])
+    with pytest.raises(F.FlyKVError) as e:
+        F.kv_switch_back(c, plan)
+    assert e.value.name == "KV_ERR_BAD_STATE"
+    other = fake_cache((1, 4, 8, 4, 2), [8, 8])
+    plan.commit()
+    with pytest.raises(F.FlyKVError) as e:
+        F.kv_switch_back(other, plan)
+    assert e.value.name == "KV_ERR_INVALID_ARG"
+    with pytest.raises(F.FlyKVError) as e:
+        plan.host_tables(0)   # not run by kv_switch
+    assert e.value.name == "KV_ERR_BAD_STATE"
