@@ -62,6 +62,11 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-parallel", action="store_true", help="skip the all-cores oracle figure")
+    ap.add_argument("--pieces", action="store_true",
+                    help="memory-bounded waves that may split a request into block-aligned token pieces (R20)")
+    ap.add_argument("--long-last", action="store_true", help="move the longest request to the end of the order")
+    ap.add_argument("--lifo", action="store_true",
+                    help="each switch moves the requests in the reverse order of the previous one (undo order)")
     ap.add_argument("--a2a", action="store_true",
                     help="N>1 comparator: kv_pack -> all_to_all_single -> kv_unpack instead of the P2P-push kernel")
     ap.add_argument("--frag", type=float, default=1.25, help="source placement window / source need")
@@ -195,6 +200,11 @@ def build_workload(args, world: int, rank: int):
     if args.requests:
         w = synth.Workload(w.name + f" first{args.requests}", w.L, w.H, w.d, w.B, w.e, w.n_gpus,
                            w.T[:args.requests], w.src[:args.requests], w.dst[:args.requests])
+    if getattr(args, "long_last", False):  # scheduling order (R8: requests move in caller order)
+        k = int(np.argmax(w.T))
+        idx = [i for i in range(len(w.T)) if i != k] + [k]
+        w = synth.Workload(w.name + " long-last", w.L, w.H, w.d, w.B, w.e, w.n_gpus, [w.T[i] for i in idx],
+                           [w.src[i] for i in idx], [w.dst[i] for i in idx])
     return w
 
 
@@ -383,21 +393,40 @@ def run_single(args):
     n_waves = []
 
     def waves_of(reqs):
-        return F.kv_plan_waves(eng.cache, reqs) if args.waves else [(0, len(reqs))]
+        """The switch of `reqs` as waves: [(plan requests, [(request index,
+        tok0, tok1) per plan request])].  One wave by default; --waves:
+        request-granular memory-bounded waves (N1); --pieces: waves that may
+        split a request into block-aligned token pieces (R20)."""
+        if args.pieces:
+            return [([F.piece_request(g, reqs[i], t0, t1) for i, t0, t1 in wv], wv)
+                    for wv in F.kv_plan_pieces(eng.cache, reqs)]
+        ranges = F.kv_plan_waves(eng.cache, reqs) if args.waves else [(0, len(reqs))]
+        return [(reqs[a:b], [(i, 0, reqs[i][1]) for i in range(a, b)]) for a, b in ranges]
+
+    def flip_all(reqs, ws, plans_):
+        """The requests after a switch run as waves ws by plans_: every request
+        from its destination (concatenated piece tables) back to its source."""
+        parts = [[] for _ in reqs]
+        for (_, owners), plan in zip(ws, plans_):
+            for (i, _, _), t in zip(owners, plan.dst_tables()):
+                parts[i].append(t)
+        out = [(rid, T, d, np.concatenate(parts[i]).astype(np.int32), s, drid, srid)
+               for i, (rid, T, s, _, d, srid, drid) in enumerate(reqs)]
+        return out[::-1] if args.lifo else out   # --lifo: undo a switch in the reverse request order
 
     def step(timed_kernel=False, read_back=False):
         """One whole switch (all waves).  Returns (tables, host copies)."""
         reqs = state["reqs"]
-        new_reqs, pairs, agg, host = [], [], None, {}
+        pairs, agg, host, plans_ = [], None, {}, []
         ws = waves_of(reqs)
         dbg = [time.perf_counter()] if read_back and DEBUG else None
-        for a, b in ws:
-            plan = eng.plan(reqs[a:b])
+        for k, (sub, _) in enumerate(ws):
+            plan = eng.plan(sub)
             dbg is not None and dbg.append(time.perf_counter())
             plan.upload(stream)
             dbg is not None and dbg.append(time.perf_counter())
             st_, _ = plan.stats()
-            agg = dict(st_) if agg is None else {k: (agg[k] if k == "atom_bytes" else agg[k] + st_[k]) for k in agg}
+            agg = dict(st_) if agg is None else {k_: (agg[k_] if k_ == "atom_bytes" else agg[k_] + st_[k_]) for k_ in agg}
             if timed_kernel:
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
@@ -411,16 +440,16 @@ def run_single(args):
             F.kv_remap_block_tables(plan, -1, packed[0], packed[1], packed[2], stream)
             dbg is not None and dbg.append(time.perf_counter())
             if read_back:                                     # three D2H copies for all pools
-                host[a] = tuple(x.to("cpu", non_blocking=True) for x in packed)
+                host[k] = tuple(x.to("cpu", non_blocking=True) for x in packed)
             dbg is not None and dbg.append(time.perf_counter())
-            new_reqs += flipped(reqs[a:b], plan)
+            plans_.append(plan)
             dbg is not None and dbg.append(time.perf_counter())
-        state["reqs"] = new_reqs
+        state["reqs"] = flip_all(reqs, ws, plans_)
         if dbg is not None:
             d = [(y - x) * 1e3 for x, y in zip(dbg, dbg[1:])]
             if sum(d) > 3:
                 sys.stderr.write("slow enqueue: plan %.2f upload %.2f stats+reshard %.2f alloc %.2f remap %.2f d2h %.2f "
-                                 "flip %.2f\n" % tuple(d))
+                                 "flip %.2f\n" % tuple(d[:7]))
         if timed_kernel:
             ev_pairs.append(pairs)
             step_stats.append(agg)
@@ -434,14 +463,15 @@ def run_single(args):
         request list is built inside the library, nothing is marshalled.
         Returns (aggregated stats, device->host bytes)."""
         chain = state.setdefault("chain", [])
-        if not args.waves and chain and len(chain[-1]) == 1:
-            plans_ = [F.kv_switch_back(eng.cache, chain[-1][0], stream)]
+        if not (args.waves or args.pieces) and chain:
+            plans_ = [F.kv_switch_back(eng.cache, chain[-1][2][0], stream)]
+            chain.append((None, None, plans_))
         else:
             settle_switches()
-            chain = state.setdefault("chain", [])
             reqs = state["reqs"]
-            plans_ = [F.kv_switch(eng.cache, reqs[a:b], stream) for a, b in waves_of(reqs)]
-        chain.append(plans_)
+            ws = waves_of(reqs)
+            plans_ = [F.kv_switch(eng.cache, sub, stream) for sub, _ in ws]
+            state["chain"] = [(reqs, ws, plans_)]
         agg, d2h_b = None, 0
         for plan in plans_:
             st_, _ = plan.stats()
@@ -453,12 +483,11 @@ def run_single(args):
     def settle_switches():
         """Replay the request tuples through the switches step_switch ran
         (outside the timed region), so state["reqs"] matches the cache."""
-        for plans_ in state.pop("chain", []):
-            reqs, new, o = state["reqs"], [], 0
-            for plan in plans_:
-                new += flipped(reqs[o:o + plan.n_reqs], plan)
-                o += plan.n_reqs
-            state["reqs"] = new
+        for reqs_, ws, plans_ in state.pop("chain", []):
+            reqs = state["reqs"]
+            if ws is None:  # kv_switch_back of a single-wave, unsplit switch
+                ws = [(reqs, [(i, 0, r[1]) for i, r in enumerate(reqs)])]
+            state["reqs"] = flip_all(reqs, ws, plans_)
 
     with torch.cuda.stream(stream):
         if args.profile_steps:
@@ -466,7 +495,7 @@ def run_single(args):
                 step()
             torch.cuda.synchronize()
             return 0
-        p0_ = eng.plan(state["reqs"][:waves_of(state["reqs"])[0][1]])
+        p0_ = eng.plan(waves_of(state["reqs"])[0][0])
         fwd_matrix = p0_.stats()[1]
         p0_.destroy()
         clk = ClockSampler(torch.cuda.current_device(), args.clock_ms).start()
@@ -536,10 +565,9 @@ def run_single(args):
                 sys.stderr.write("e2e enqueue ms: " + " ".join(f"{x:.2f}" for x in enq_ms) + "\n")
             # host planning time alone (kv_plan_switch), measured on plans that are then abandoned
             for it in range(min(args.steps, 10)):
-                reqs = state["reqs"]
-                a_, b_ = waves_of(reqs)[0]
+                sub0 = waves_of(state["reqs"])[0][0]
                 t0 = time.perf_counter()
-                p_ = eng.plan(reqs[a_:b_])
+                p_ = eng.plan(sub0)
                 plan_ms[it] = (time.perf_counter() - t0) * 1e3
                 p_.destroy()
             plan_ms = plan_ms[:min(args.steps, 10)]
@@ -604,7 +632,8 @@ def run_single(args):
                    "tokens": w.tokens(), "payload_bytes_per_step": int(payload),
                    "payload_bytes_forward": stats["payload_bytes"],
                    "placement": args.placement,
-                   "waves_per_switch": (round(sum(n_waves) / len(n_waves), 2) if args.waves else 1),
+                   "waves_per_switch": (round(sum(n_waves) / len(n_waves), 2) if (args.waves or args.pieces) else 1),
+                   "pieces": bool(args.pieces), "long_last": bool(args.long_last), "lifo": bool(args.lifo),
                    "pool_bytes": int(eng.pools.nbytes()),
                    "l2": ("L2 flushed between steps (512 MiB rewrite, outside the step events)" if flush is not None
                           else "inputs larger than L2 (payload >> 126 MB), no flush needed"),

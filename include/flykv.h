@@ -327,6 +327,30 @@ kv_status kv_plan_commit(kv_plan* plan);
 kv_status kv_plan_waves(const kv_cache* cache, const kv_request* reqs, int32_t n_reqs, int64_t max_wave_bytes,
                         int32_t* wave_start, int32_t* n_waves);
 
+/*
+ * kv_plan_pieces: memory-bounded waves that may split a request (R20): the
+ * memory-driven promotion of ONE long request (Use Case 3)
+ * when its source and destination do not fit side by side.  A request moves
+ * in consecutive token pieces [tok0, tok1), each starting and (but for the
+ * last) ending on a whole block of both layouts, so a piece is itself a
+ * plain request: num_tokens = tok1 - tok0, src_blocks = the request's table
+ * from tok0 / B(src degree) on, same groups and rank IDs.  Each wave is
+ * planned after the previous waves committed (their pieces' source blocks
+ * released); a piece takes the lowest common free IDs of its wave, and the
+ * request's final table is the concatenation of its pieces' tables.  Whole
+ * requests are kept whole when they fit (then this equals kv_plan_waves).
+ *   pieces  host [cap] out: {wave, request index, tok0, tok1}, in wave order,
+ *           request order within a wave; *n_pieces = count (also when cap is
+ *           too small: INVALID_ARG, call again with that cap)
+ * OUT_OF_BLOCKS if some piece cannot progress even in a wave of its own.
+ * Simulates the allocator; no state change.
+ */
+typedef struct {
+    int32_t wave, req, tok0, tok1;
+} kv_piece;
+kv_status kv_plan_pieces(const kv_cache* cache, const kv_request* reqs, int32_t n_reqs, int64_t max_wave_bytes,
+                         int32_t cap, kv_piece* pieces, int32_t* n_pieces);
+
 /* kv_suggest_rank_ids: N2 egress reduction.  For the requests of reqs whose
  * destination is group dst, choose the rank-ID assignment of dst's members
  * (out: host [dst.degree], rank ID of member m) that maximises the bytes

@@ -977,6 +977,99 @@ extern "C" kv_status kv_plan_waves(const kv_cache* c, const kv_request* reqs, in
     return KV_OK;
 }
 
+// IDs free on every GPU of g in the simulated state (the most blocks one
+// allocation on g can take).
+static int32_t common_free(const kv_cache* c, const Bitmaps& held, kv_group g) {
+    const int32_t nb = group_min_blocks(c, g);
+    int32_t cnt = 0;
+    for (int32_t w = 0; w < (nb + 63) >> 6; ++w) {
+        uint64_t used = 0;
+        for (int32_t r = 0; r < g.degree; ++r) used |= held[g.first_gpu + r][w];
+        uint64_t fr = ~used;
+        const int32_t top = nb - (w << 6);
+        if (top < 64) fr &= (top <= 0) ? 0ull : ((1ull << top) - 1);
+        cnt += __builtin_popcountll(fr);
+    }
+    return cnt;
+}
+
+extern "C" kv_status kv_plan_pieces(const kv_cache* c, const kv_request* reqs, int32_t n_reqs, int64_t max_wave_bytes,
+                                    int32_t cap, kv_piece* pieces, int32_t* n_pieces) {
+    if (!c || !n_pieces || n_reqs < 0 || (n_reqs > 0 && !reqs) || max_wave_bytes < 0 || cap < 0 ||
+        (cap > 0 && !pieces))
+        return fail(KV_ERR_INVALID_ARG, "bad kv_plan_pieces arguments");
+    int64_t ts = 0, td = 0;
+    kv_status s = validate_requests(c, reqs, n_reqs, &ts, &td);
+    if (s) return s;
+    const kv_geometry& G = c->geo;
+    const int32_t H = G.num_kv_heads, B = G.block_base;
+    Bitmaps sim = c->held;  // simulated allocator state
+    std::vector<kv_piece> out;
+    std::vector<int32_t> ids;
+    int32_t wave = 0;
+    size_t wave_first = 0;  // first piece of the open wave
+    int64_t wave_bytes = 0;
+    auto close_wave = [&]() {  // the wave's remap commits it: its pieces' sources are released
+        for (size_t k = wave_first; k < out.size(); ++k) {
+            const kv_piece& pc = out[k];
+            const kv_request& r = reqs[pc.req];
+            if (!request_moves(r)) continue;
+            const int32_t b0 = B * layout_of(H, r.src.degree).k;
+            const int32_t lo = pc.tok0 / b0, hi = (int32_t)ceil_div(pc.tok1, b0);
+            for (int32_t q = 0; q < r.src.degree; ++q)
+                for (int32_t k2 = lo; k2 < hi; ++k2) bit_clr(sim[r.src.first_gpu + q], r.src_blocks[k2]);
+        }
+        ++wave;
+        wave_first = out.size();
+        wave_bytes = 0;
+    };
+    for (int32_t i = 0; i < n_reqs; ++i) {
+        const kv_request& r = reqs[i];
+        if (!request_moves(r) || r.num_tokens == 0) {  // no-ops and empty requests stay whole
+            out.push_back(kv_piece{wave, i, 0, r.num_tokens});
+            continue;
+        }
+        const Layout l0 = layout_of(H, r.src.degree), l1 = layout_of(H, r.dst.degree);
+        const int32_t b1 = B * l1.k;
+        // piece boundaries: whole blocks of both layouts (k is a power of two)
+        const int32_t unit = B * std::max(l0.k, l1.k);
+        const int64_t bytes_per_chunk = (int64_t)G.num_layers * 2 * H * c->atom_bytes * l1.rep;  // per B tokens
+        int32_t t = 0;
+        while (t < r.num_tokens) {
+            const int32_t rest = r.num_tokens - t;
+            const int32_t free_ids = common_free(c, sim, r.dst);
+            const int64_t room = max_wave_bytes > 0 ? max_wave_bytes - wave_bytes : INT64_MAX;
+            int32_t len = 0;
+            if (ceil_div(rest, b1) <= free_ids && ceil_div(rest, B) * bytes_per_chunk <= room) {
+                len = rest;  // the whole remainder fits this wave
+            } else if (out.size() > wave_first) {
+                close_wave();  // a new wave first: the open one's sources are released at its commit
+                continue;
+            } else {  // even a fresh wave cannot take the remainder: the largest whole-unit prefix that fits
+                int64_t units = std::min<int64_t>(rest / unit, (int64_t)free_ids / (unit / b1));
+                if (max_wave_bytes > 0) units = std::min<int64_t>(units, room / ((unit / B) * bytes_per_chunk));
+                len = (int32_t)(units * unit);
+                if (len == 0 && max_wave_bytes > 0 && ceil_div(std::min(rest, unit), b1) <= free_ids)
+                    len = std::min(rest, unit);  // one unit exceeds the byte bound on its own: take it alone
+                if (len == 0)
+                    return fail(KV_ERR_OUT_OF_BLOCKS, "request %d: no room for %d more tokens even in a wave of "
+                                "its own", i, rest);
+            }
+            ids.resize(ceil_div(len, b1));
+            if (!alloc_lowest_in(c, sim, r.dst, (int32_t)ids.size(), ids.data()))
+                return fail(KV_ERR_OUT_OF_BLOCKS, "request %d: internal allocation mismatch", i);
+            out.push_back(kv_piece{wave, i, t, t + len});
+            wave_bytes += ceil_div(len, B) * bytes_per_chunk;
+            t += len;
+        }
+    }
+    *n_pieces = (int32_t)out.size();
+    if ((int32_t)out.size() > cap)
+        return fail(KV_ERR_INVALID_ARG, "%d pieces do not fit in cap %d (retry with *n_pieces)", (int32_t)out.size(), cap);
+    std::copy(out.begin(), out.end(), pieces);
+    return KV_OK;
+}
+
 extern "C" kv_status kv_suggest_rank_ids(const kv_cache* c, const kv_request* reqs, int32_t n_reqs, kv_group dst,
                                          int32_t* out) {
     if (!c || !out || n_reqs < 0 || (n_reqs > 0 && !reqs)) return fail(KV_ERR_INVALID_ARG, "bad arguments");

@@ -143,6 +143,26 @@ class KVSwitchEngine:
             self.stream.synchronize()
         return plan, tables, host
 
+    def switch_pieces(self, requests, max_wave_bytes: int = 0):
+        """Memory-bounded switch that may move a request in block-aligned token
+        pieces across waves (kv_plan_pieces, R20): the promotion of one long
+        request whose source and destination do not fit side by side.  Each
+        wave is one kv_switch (commit releases its pieces' sources before the
+        next wave allocates).  Returns (final destination table of every
+        request = concatenation of its pieces' tables, the wave plans)."""
+        requests = list(requests)
+        waves = flykv.kv_plan_pieces(self.cache, requests, max_wave_bytes)
+        parts = [[] for _ in requests]
+        plans = []
+        for wave in waves:
+            sub = [flykv.piece_request(self.geom, requests[i], t0, t1) for i, t0, t1 in wave]
+            plan = flykv.kv_switch(self.cache, sub, self.stream)
+            for (i, _, _), tab in zip(wave, plan.dst_tables()):
+                parts[i].append(tab)
+            plans.append(plan)
+        tables = [np.concatenate(p).astype(np.int32) if p else np.zeros(0, dtype=np.int32) for p in parts]
+        return tables, plans
+
     def switch_waves(self, requests, max_wave_bytes: int = 0, read_back=False):
         """Memory-bounded switch: waves planned by
         kv_plan_waves; each wave is a full switch whose commit frees its

@@ -129,6 +129,13 @@ _sig("kv_plan_dst_tables", C.c_int, _P, _I32P, _I32P)
 _sig("kv_plan_commit", C.c_int, _P)
 _sig("kv_plan_waves", C.c_int, _P, C.POINTER(Request), C.c_int32, C.c_int64, _I32P, _I32P)
 _sig("kv_suggest_rank_ids", C.c_int, _P, C.POINTER(Request), C.c_int32, Group, _I32P)
+
+
+class Piece(C.Structure):
+    _fields_ = [("wave", C.c_int32), ("req", C.c_int32), ("tok0", C.c_int32), ("tok1", C.c_int32)]
+
+
+_sig("kv_plan_pieces", C.c_int, _P, C.POINTER(Request), C.c_int32, C.c_int64, C.c_int32, C.POINTER(Piece), _I32P)
 _sig("kv_plan_get_stats", C.c_int, _P, C.POINTER(PlanStats), _I64P)
 _sig("kv_plan_destroy", None, _P)
 _sig("weight_shard_view", C.c_int, C.POINTER(WeightDesc), C.c_int32, C.c_int32, C.POINTER(View))
@@ -152,7 +159,8 @@ _sig("kv_set_reshard_impl", C.c_int, C.c_int32, C.c_int32)
 EXPORTED = ["kv_cache_create", "kv_cache_destroy", "kv_layout", "kv_blocks_for", "kv_alloc", "kv_reserve",
             "kv_free", "kv_free_count", "kv_held_mask", "kv_plan_switch", "kv_plan_upload", "kv_reshard", "kv_reshard_staged",
             "kv_pack", "kv_unpack", "kv_switch", "kv_switch_back", "kv_plan_tables", "kv_plan_resident",
-            "kv_remap_block_tables", "kv_plan_dst_tables", "kv_plan_commit", "kv_plan_waves", "kv_suggest_rank_ids", "kv_plan_get_stats", "kv_plan_destroy",
+            "kv_remap_block_tables", "kv_plan_dst_tables", "kv_plan_commit", "kv_plan_waves", "kv_plan_pieces",
+            "kv_suggest_rank_ids", "kv_plan_get_stats", "kv_plan_destroy",
             "weight_shard_view", "kv_gather_view", "kv_vmm_granularity", "kv_vmm_alloc", "kv_vmm_free",
             "weight_view_alias", "weight_view_unalias", "kv_paged_decode", "kv_ipc_export", "kv_ipc_import", "kv_ipc_close",
             "kv_stream_sync", "kv_strerror", "kv_last_error", "kv_launch_count", "kv_set_reshard_impl"]
@@ -459,6 +467,43 @@ def kv_plan_waves(cache: KVCache, requests, max_wave_bytes: int = 0) -> list:
     nw = C.c_int32()
     _check(_lib.kv_plan_waves(cache._h, arr, n, int(max_wave_bytes), ws.ctypes.data_as(_I32P), C.byref(nw)))
     return [(int(ws[k]), int(ws[k + 1])) for k in range(nw.value)]
+
+
+def kv_plan_pieces(cache: KVCache, requests, max_wave_bytes: int = 0) -> list:
+    """Memory-bounded waves that may split a request into block-aligned token
+    pieces (R20): list of waves, each a list of (request index, tok0, tok1)."""
+    ra = make_requests(requests)
+    cap = max(2 * ra.n, 16)
+    while True:
+        buf = (Piece * cap)()
+        n = C.c_int32()
+        st = _lib.kv_plan_pieces(cache._h, ra.ptr, ra.n, int(max_wave_bytes), cap, buf, C.byref(n))
+        if st == KV_OK:
+            break
+        if st == 1 and n.value > cap:  # INVALID_ARG with the needed count
+            cap = n.value
+            continue
+        raise FlyKVError(st, _lib.kv_last_error().decode())
+    waves = []
+    for k in range(n.value):
+        pc = buf[k]
+        while len(waves) <= pc.wave:
+            waves.append([])
+        waves[pc.wave].append((pc.req, pc.tok0, pc.tok1))
+    return waves
+
+
+def piece_request(geom: Geometry, req, tok0: int, tok1: int):
+    """The plain request that moves tokens [tok0, tok1) of `req` (a request
+    tuple as for kv_plan_switch), for a piece from kv_plan_pieces."""
+    rid, T, src, ids, dst = req[:5]
+    rest = tuple(req[5:])
+    if tok0 == 0 and tok1 == T:
+        return req
+    b0 = kv_layout(geom, src[1])[1]
+    ids = np.asarray(ids, dtype=np.int32)
+    sub = ids[tok0 // b0: -(-tok1 // b0)]
+    return (rid, tok1 - tok0, src, sub, dst) + rest
 
 
 def kv_reshard(plan: Plan, gpu: int = -1, stream=None):

@@ -417,3 +417,82 @@ def test_kv_switch_errors_before_the_device():
     with pytest.raises(F.FlyKVError) as e:
         plan.host_tables(0)   # not run by kv_switch
     assert e.value.name == "KV_ERR_BAD_STATE"
+
+
+def _run_pieces_against_oracle(c, og, held, reqs, waves, n_gpus):
+    """Execute kv_plan_pieces' waves on the product (plan + commit per wave,
+    fake pointers) and on the oracle's allocator with the same piece
+    requests; tables and allocator state must agree wave by wave.  Returns
+    each request's concatenated destination table."""
+    parts = [[] for _ in reqs]
+    for wave in waves:
+        sub = [F.piece_request(c.geom, reqs[i], t0, t1) for i, t0, t1 in wave]
+        plan = c.plan_switch(sub)
+        st, otabs = O.switch(og, None, held, [O.Req(T, s, list(ids), d) for (_, T, s, ids, d) in sub], copy=False)
+        assert st == 0
+        assert [list(x) for x in plan.dst_tables()] == [list(y) for y in otabs]
+        plan.commit()
+        for g in range(n_gpus):
+            assert np.array_equal(c.held_mask(g), held[g])
+        for (i, _, _), t in zip(wave, otabs):
+            parts[i].append(np.asarray(t, dtype=np.int32))
+    return [np.concatenate(p) for p in parts]
+
+
+def test_pieces_equal_waves_when_requests_fit():
+    """kv_plan_pieces keeps requests whole, in kv_plan_waves' partition, when
+    every request fits a fresh wave (R20 reduces to N1)."""
+    geo = (2, 8, 8, 4, 2)
+    og = O.Geom(*geo)
+    nb = [56] * 8
+    c = fake_cache(geo, nb)
+    rng = np.random.default_rng(9)
+    held = [np.zeros(n, dtype=np.uint8) for n in nb]
+    reqs = []
+    for i in range(24):
+        T = int(rng.integers(20, 50))
+        ids = oracle_alloc(c, held, (i % 8, 1), O.num_blocks(og, T, 1))
+        reqs.append((i, T, (i % 8, 1), ids, (0, 8)))
+    waves = F.kv_plan_waves(c, reqs)
+    pieces = F.kv_plan_pieces(c, reqs)
+    assert [[(i, 0, reqs[i][1]) for i in range(a, b)] for a, b in waves] == pieces
+
+
+def test_one_long_request_promoted_in_pieces():
+    """R20 / Use Case 3: one long TP4 request that fills most of
+    GPUs 0-3 is promoted to TP8.  Its source and destination cannot coexist
+    (one shot and request-granular waves both fail with OUT_OF_BLOCKS), but
+    block-aligned token pieces over several waves succeed: the pieces tile
+    [0, T) on whole blocks of both layouts, every wave's allocation equals
+    the oracle's, and the concatenated table has ceil(T / B(8)) blocks."""
+    geo = (2, 8, 8, 4, 2)
+    og = O.Geom(*geo)
+    nb = [80] * 8
+    c = fake_cache(geo, nb)
+    held = [np.zeros(n, dtype=np.uint8) for n in nb]
+    T = 66 * 16 + 5                       # B(4) = 16 tokens: 67 blocks on each of GPUs 0-3
+    ids = oracle_alloc(c, held, (0, 4), O.num_blocks(og, T, 4))
+    reqs = [(0, T, (0, 4), ids, (0, 8))]
+    with pytest.raises(F.FlyKVError) as e:
+        c.plan_switch(reqs)
+    assert e.value.name == "KV_ERR_OUT_OF_BLOCKS"
+    with pytest.raises(F.FlyKVError):
+        F.kv_plan_waves(c, reqs)
+    waves = F.kv_plan_pieces(c, reqs)
+    assert len(waves) >= 2 and all(len(w) == 1 for w in waves)
+    bounds = [w[0][1:] for w in waves]
+    assert bounds[0][0] == 0 and bounds[-1][1] == T
+    assert all(bounds[k][1] == bounds[k + 1][0] for k in range(len(bounds) - 1))
+    unit = 4 * 8                          # whole blocks of both layouts: B(8) = 32 tokens
+    assert all(t1 % unit == 0 for _, t1 in bounds[:-1])
+    final = _run_pieces_against_oracle(c, og, held, reqs, waves, 8)
+    assert len(final[0]) == O.num_blocks(og, T, 8)
+    assert all(c.free_count(g) + int(held[g].sum()) == nb[g] for g in range(8))
+    # a byte bound splits a request that would fit into more waves
+    c2 = fake_cache(geo, [4096] * 8)
+    held2 = [np.zeros(4096, dtype=np.uint8) for _ in range(8)]
+    ids2 = oracle_alloc(c2, held2, (0, 1), O.num_blocks(og, 1000, 1))
+    per_token = 2 * 2 * 8 * 8 * 2                      # L * 2 * H * d * e
+    w2 = F.kv_plan_pieces(c2, [(0, 1000, (0, 1), ids2, (0, 8))], max_wave_bytes=300 * per_token)
+    assert len(w2) >= 4 and all((t1 - t0) * per_token <= 300 * per_token for [(_, t0, t1)] in w2)
+    _run_pieces_against_oracle(c2, og, held2, [(0, 1000, (0, 1), ids2, (0, 8))], w2, 8)

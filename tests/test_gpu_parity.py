@@ -656,3 +656,65 @@ def test_weight_switches_allocate_nothing():
     assert torch.cuda.memory_allocated() == alloc0
     assert abs(free1 - free0) < 4 * 2 ** 20, (free0, free1)   # driver bookkeeping only: one TP8 view copy is 21 MB
     buf.close()
+
+
+@pytest.mark.parametrize("T,src,dst,H", [(66 * 16 + 5, (0, 4), (0, 8), 8), (2000, (0, 1), (0, 8), 8),
+                                         (700, (0, 2), (0, 8), 2)])
+def test_long_request_promoted_in_pieces(T, src, dst, H):
+    """R20 / Use Case 3: one long request whose source and destination cannot
+    coexist is promoted in block-aligned token pieces over waves
+    (kv_plan_pieces + one kv_switch per wave).  The pools equal the oracle's
+    after the same waves, and -- the property that makes pieces legal -- the
+    concatenated table is the whole request's layout at the destination
+    degree: every atom (all GQA replicas) the oracle's atom map sends from the
+    original source table holds the original bytes."""
+    F = _F()
+    from paper_2602_22593_b200.engine import KVSwitchEngine
+    geo = (2, H, 64, 16, 2)
+    og = O.Geom(*geo)
+    n0, n1 = O.num_blocks(og, T, src[1]), O.num_blocks(og, T, dst[1])
+    nb = [n0 + n1 - 1] * 8                # one block short of holding source and destination side by side
+    eng = KVSwitchEngine(F.geometry(*geo), nb, "cuda:0")
+    for gpu, t in enumerate(eng.pools.tensors):
+        synth.fill_hash_torch(t, gpu, seed=11)
+    held = [np.zeros(k, dtype=np.uint8) for k in nb]
+    ids = oracle_alloc(eng.cache, held, src, n0)
+    M = O.block_bytes(og)
+    if src[1] > H:  # replicated source heads identical (R10)
+        rep = src[1] // H
+        idx = torch.as_tensor(ids.astype(np.int64), device="cuda:0")
+        for r in range(src[1]):
+            if r % rep:
+                eng.pools.tensors[src[0] + r][:, idx] = eng.pools.tensors[src[0] + r - r % rep][:, idx]
+    torch.cuda.synchronize()
+    host = [t.cpu().numpy().reshape(-1).copy() for t in eng.pools.tensors]
+    orig = [h.copy() for h in host]
+    reqs = [(0, T, src, ids, dst)]
+    with pytest.raises(F.FlyKVError):
+        eng.cache.plan_switch(reqs)
+    final, plans = eng.switch_pieces(reqs)
+    assert len(plans) >= 2
+    # replay the same pieces (one per wave: a single request) on the oracle
+    parts = []
+    t0 = 0
+    for plan in plans:
+        tab = plan.dst_tables()[0]
+        t1 = min(T, t0 + len(tab) * O.block_tokens(og, dst[1]))
+        b0 = O.block_tokens(og, src[1])
+        piece = O.Req(t1 - t0, src, list(ids[t0 // b0: -(-t1 // b0)]), dst)
+        st, otabs = O.switch(og, host, held, [piece])
+        assert st == 0 and list(otabs[0]) == list(tab)
+        parts.append(tab)
+        t0 = t1
+    assert t0 == T
+    assert list(np.concatenate(parts)) == list(final[0])
+    for gpu, t in enumerate(eng.pools.tensors):
+        assert np.array_equal(t.cpu().numpy().reshape(-1), host[gpu]), f"pool {gpu} differs"
+        assert np.array_equal(eng.cache.held_mask(gpu), held[gpu])
+    # whole-request layout: original source bytes at every destination atom of the concatenated table
+    sg, so, dg, do = O.atom_map(og, nb, T, src, list(ids), dst, list(final[0]))
+    atom = og.B * og.d * og.e
+    for k in range(0, len(sg), 97):
+        a = orig[int(sg[k])][int(so[k]):int(so[k]) + atom]
+        b = eng.pools.tensors[int(dg[k])].reshape(-1)[int(do[k]):int(do[k]) + atom].cpu().numpy()
+        assert np.array_equal(a, b), f"atom {k}"
