@@ -459,3 +459,31 @@ def test_same_group_repermutation_moves():
     assert st == 0 and [list(t) for t in tabs] == [list(t) for t in tabs_b]
     assert all(set(t).isdisjoint(r.src_ids) for t, r in zip(tabs, reqs))  # fresh blocks
     assert all(np.array_equal(a, b) for a, b in zip(pools, pools_b))
+
+
+@pytest.mark.parametrize("H,p0,p1,T", [(4, 1, 4, 90), (4, 4, 1, 77), (2, 2, 8, 65), (4, 2, 4, 100), (8, 8, 2, 50)])
+def test_pieces_concatenate_to_the_whole_request(H, p0, p1, T):
+    """R20 pinned by brute force: moving a request as consecutive pieces cut
+    on whole blocks of both layouts (each a plain request on its slice of the
+    source table, one oracle switch per piece with sources released between)
+    leaves, under the concatenated destination table, exactly the logical KV
+    of the request (brute.read_request), as the one-shot move does."""
+    geo = (2, H, 4, 4, 2)
+    g = O.Geom(*geo)
+    nb = [120] * 8
+    g_, pools, held, reqs = _setup(geo, nb, [(T, (0, p0), (0, p1))], seed=H * 7 + p0 + p1)
+    r = reqs[0]
+    slots = -(-T // 4) * 4
+    before = brute.read_request(pools, geo, r.src, r.src_ids, slots)
+    b0, b1 = O.block_tokens(g, p0), O.block_tokens(g, p1)
+    unit = max(b0, b1)
+    cuts = [0] + [c for c in range(unit, T, 2 * unit)] + [T]   # pieces of 2 units, ragged last
+    parts = []
+    for t0, t1 in zip(cuts, cuts[1:]):
+        piece = O.Req(t1 - t0, r.src, list(r.src_ids[t0 // b0: -(-t1 // b0)]), r.dst)
+        st, tabs = O.switch(g, pools, held, [piece])
+        assert st == 0
+        parts += list(tabs[0])
+    assert len(parts) == O.num_blocks(g, T, p1)
+    after = brute.read_request(pools, geo, r.dst, parts, slots)
+    assert np.array_equal(before, after)
