@@ -76,6 +76,9 @@ def parse():
     ap.add_argument("--waves", action="store_true", help="memory-bounded waves (kv_plan_waves) per switch")
     ap.add_argument("--rank-ids", default="identity", choices=["identity", "suggest"],
                     help="destination rank-ID assignment (P:291): identity (R3) or kv_suggest_rank_ids (N2)")
+    ap.add_argument("--work-order", type=int, default=None, choices=[0, 1],
+                    help="kernel work order (kv_cache_set_work_order): 1 mixed, 0 plan order; default 0 at N=1 "
+                         "(all pools on one device) and 1 with one process per GPU")
     ap.add_argument("--clock-ms", type=int, default=200, help="nvidia-smi sampling period in the timed region (0: off)")
     ap.add_argument("--profile-steps", type=int, default=0, help="(ncu) run N steps only, no JSON")
     ap.add_argument("--no-fill", action="store_true", help="skip the content hash fill (profiling runs)")
@@ -369,6 +372,9 @@ def run_single(args):
     g = F.geometry(w.L, w.H, w.d, w.B, w.e)
     nb, tabs = pools_and_tables(w, args.frag, args.pool_slack, args.placement == "contiguous")
     eng = KVSwitchEngine(g, nb, dev, tp_degrees=(2, 4, 8))
+    if args.work_order is None:
+        args.work_order = 0
+    eng.cache.set_work_order(args.work_order)
     if not args.no_fill:
         for i, t in enumerate(eng.pools.tensors):
             synth.fill_hash_torch(t, i)
@@ -632,6 +638,7 @@ def run_single(args):
                    "tokens": w.tokens(), "payload_bytes_per_step": int(payload),
                    "payload_bytes_forward": stats["payload_bytes"],
                    "placement": args.placement,
+                   "work_order": ["plan", "mixed"][args.work_order],
                    "waves_per_switch": (round(sum(n_waves) / len(n_waves), 2) if (args.waves or args.pieces) else 1),
                    "pieces": bool(args.pieces), "long_last": bool(args.long_last), "lifo": bool(args.lifo),
                    "pool_bytes": int(eng.pools.nbytes()),
@@ -669,6 +676,73 @@ def nvlink_roofline(bytes_matrix, hbm_gbs, link_gbs=FALLBACK_NVLINK_GBS):
     return float(t.max()), egress, ingress, hbm
 
 
+def ordered_link_model(pieces, hbm_gbs, link_gbs=FALLBACK_NVLINK_GBS):
+    """Completion time (s) of an N-GPU push in which every GPU works through
+    its pieces in kernel order (flykv Plan.work_order: per piece the bytes
+    written to each GPU, last column the bytes read), all GPUs at once.
+    Fluid model: each sender moves its current piece's bytes in the piece's
+    destination mix; rates are max-min fair (progressive filling, bytes
+    written per second) under sender egress <= link, receiver ingress <=
+    link (remote writes only) and per-GPU HBM (reads of its pieces + every
+    write landing on it) <= hbm.  Unlike t_min (nvlink_roofline), which
+    assumes each GPU's traffic is spread evenly over the whole switch, this
+    charges senders that push into the same receiver at the same time
+    (ingress hot-spots) -- a model, not a measurement."""
+    n = len(pieces)
+    cap = np.concatenate([np.full(n, link_gbs * 1e9), np.full(n, link_gbs * 1e9), np.full(n, hbm_gbs * 1e9)])
+    idx = [0] * n
+    rem = np.ones(n)
+    t = 0.0
+    eye = np.eye(n, dtype=bool)
+    while True:
+        act = [g for g in range(n) if idx[g] < len(pieces[g])]
+        if not act:
+            return t
+        A = np.zeros((3 * n, n))      # resource use per byte/s written by sender g
+        W = np.zeros(n)
+        for g in act:
+            row = pieces[g][idx[g]].astype(np.float64)
+            v, r = row[:n], row[n]
+            W[g] = v.sum()
+            if W[g] <= 0:
+                continue
+            remote = np.where(eye[g], 0.0, v)
+            A[g, g] = remote.sum() / W[g]             # egress of g
+            A[n:2 * n, g] = remote / W[g]             # ingress of each receiver
+            A[2 * n:, g] = v / W[g]                   # writes landing in each HBM
+            A[2 * n + g, g] += r / W[g]               # reads of g
+        zero = [g for g in act if W[g] <= 0]
+        if zero:                                      # all-hole pieces take no time
+            for g in zero:
+                idx[g] += 1
+                rem[g] = 1.0
+            continue
+        y = np.zeros(n)
+        free = np.zeros(n, dtype=bool)
+        free[act] = True
+        load = np.zeros(3 * n)
+        while free.any():
+            s = A[:, free].sum(1)
+            ok = s > 1e-15
+            if not ok.any():
+                break
+            slack = (cap[ok] - load[ok]) / s[ok]
+            d = max(float(slack.min()), 0.0)
+            y[free] += d
+            load += d * s
+            sat = np.where(ok)[0][slack <= d * (1 + 1e-9) + 1e-300]
+            for c in sat:
+                free &= ~(A[c] > 1e-15)
+        dt = min(rem[g] * W[g] / y[g] for g in act if y[g] > 0)
+        t += dt
+        for g in act:
+            if y[g] > 0:
+                rem[g] -= dt * y[g] / W[g]
+                if rem[g] <= 1e-9:
+                    idx[g] += 1
+                    rem[g] = 1.0
+
+
 def run_multi(args):
     """One process per GPU (torchrun).  Every rank pushes the atoms it holds
     into peer pools (IPC-mapped, NVLink P2P stores), then a group barrier."""
@@ -704,6 +778,9 @@ def run_multi(args):
         synth.fill_hash_torch(local_pool, rank)
     bases, nbs, imported = comm.exchange_pools(local_pool, rank, world, w.L, M)
     cache = F.KVCache(g, nbs, bases, degrees)
+    if args.work_order is None:
+        args.work_order = 0 if same_dev else 1
+    cache.set_work_order(args.work_order)
     for s_, ids in zip(w.src, tabs):
         cache.reserve(s_, ids)
     stream = torch.cuda.Stream(dev)
@@ -831,6 +908,7 @@ def run_multi(args):
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": w.name + (" (ranks share cuda:0, gloo)" if same_dev else "") +
                        (" [pack -> all_to_all_single -> unpack comparator]" if args.a2a else ""), "layers": w.L,
+                       "work_order": ["plan", "mixed"][args.work_order],
                        "kv_heads": w.H, "head_dim": w.d, "block_base": w.B, "requests": len(w.T),
                        "tokens": w.tokens(), "payload_bytes_per_step": int(payload),
                        "l2": "inputs larger than L2, no flush needed",

@@ -100,8 +100,12 @@ typedef struct {
     int64_t h2d_bytes;      /* descriptor bytes uploaded per plan           */
     int64_t n_segments;     /* (request, source GPU) work segments          */
     int64_t n_atom_slots;   /* work slots of the kernels incl. holes of the
-                               destination-major order (>= n_atoms); the
-                               staging size of kv_reshard_staged           */
+                               destination-major and the mixed order
+                               (>= n_atoms); the staging size of
+                               kv_reshard_staged                           */
+    int64_t n_buckets;      /* destination buckets of the kernels' work
+                               order, summed over source GPUs
+                               (kv_cache_set_work_order)                    */
 } kv_plan_stats;
 
 /* ---------------------------------------------------------------- cache */
@@ -196,8 +200,11 @@ kv_status kv_plan_upload(kv_plan* plan, void* stream);
  * ranks on one B200).  An atom (request, layer, K/V, head, chunk of B
  * tokens) is B*d*e contiguous bytes in every degree's layout; it is read
  * once and written to each destination replica (1, or p/H under GQA
- * replication, R2), local or over NVLink peer mappings; atoms are visited in
- * destination-major order so destination blocks are written sequentially.  Idempotent until
+ * replication, R2), local or over NVLink peer mappings; inside a request
+ * atoms are visited in destination-major order so destination blocks are
+ * written sequentially, and across requests in the cache's work order
+ * (kv_cache_set_work_order: mixed by default, so concurrent senders do not
+ * converge on one receiver).  Idempotent until
  * the plan is committed.  The caller must order kv_remap_block_tables after
  * every GPU's reshard has completed (stream order, or a group barrier, a5).
  * Current device must be the one that can address the pools.
@@ -367,6 +374,15 @@ kv_status kv_plan_dst_tables(const kv_plan* plan, int32_t* dst_ptr, int32_t* dst
  * destination bytes each source GPU sends to each destination GPU (row =
  * source), the input of the roofline of SURVEY 8(d). */
 kv_status kv_plan_get_stats(const kv_plan* plan, kv_plan_stats* stats, int64_t* bytes_matrix);
+/* The kernel work order of source GPU `gpu` (kv_cache_set_work_order), for
+ * link models: *n_rows receives the number of consecutive 1024-slot ranges of
+ * the GPU's kernel slot order; out (host [n_rows * (n_gpus + 1)] or NULL)
+ * receives, per range in visiting order, the destination bytes it writes to
+ * each GPU (replicas included, holes excluded) and, in column n_gpus, the
+ * bytes it reads on `gpu`.  Summed over ranges, the first n_gpus columns are
+ * row `gpu` of kv_plan_get_stats' bytes_matrix.
+ * Errors: KV_ERR_INVALID_ARG (NULL plan / n_rows, gpu out of range). */
+kv_status kv_plan_work_order(const kv_plan* plan, int32_t gpu, int32_t* n_rows, int64_t* out);
 /* Destroy a plan.  A plan that was never committed rolls back its
  * destination allocations. */
 void kv_plan_destroy(kv_plan* plan);
@@ -473,6 +489,26 @@ kv_status kv_stream_sync(void* stream);
 /* ---------------------------------------------------------------- misc */
 const char* kv_strerror(kv_status s);
 const char* kv_last_error(void);
+/*
+ * kv_cache_set_work_order: the order in which each source GPU's kernel visits
+ * its atoms in plans built from now on (results are identical either way:
+ * every (atom, replica) is written once, to its own bytes).
+ *   order 1 (default) mixed: the GPU's work is bucketed by destination
+ *           group and the kernel walks it in quanta of about 1024 atom
+ *           slots, each quantum taking its share (1/K) of every bucket, in an
+ *           order rotated by the source GPU.  At every moment a sender's
+ *           traffic is split over its receivers in the proportions of the
+ *           whole switch, the assumption behind t_min.  When
+ *           all GPUs push at once (one process per GPU, NVSwitch),
+ *           concurrent senders therefore do not converge on one receiver --
+ *           e.g. TP8 -> 8 x DP1, where every sender holds a slice of every
+ *           request, no longer pushes request i from all 8 GPUs into engine
+ *           i mod 8 at the same time (ingress hot-spot).
+ *   order 0 plan order: each GPU's segments in request order.
+ * Errors: KV_ERR_INVALID_ARG (NULL cache, order not 0/1).  DESIGN.md 8.
+ */
+kv_status kv_cache_set_work_order(kv_cache* cache, int32_t order);
+
 /* Tuning knob for the reshard kernel (process-wide): impl 0 = default
  * (LDG/STG warp copy, two atoms in flight per warp for 2/4 KiB atoms), 1 =
  * LDG/STG one atom per warp iteration, 2 = TMA bulk-copy ring (local pools

@@ -82,6 +82,8 @@ struct kv_cache {
     // pinned landing buffer of kv_switch's one device->host table copy
     void* back = nullptr;
     size_t back_bytes = 0;
+    // kernel work order of new plans: 1 = destination-rotated (default), 0 = plan order
+    int32_t work_order = 1;
 };
 
 struct ReqPlan {
@@ -103,8 +105,14 @@ struct kv_plan {
     std::vector<ReqPlan> reqs;
     std::vector<int32_t> tables;
     std::vector<Seg> segs;
+    // kernel work order (build_work_order): pieces of segments, the exclusive
+    // prefix of their slot counts, each source GPU's piece range
+    std::vector<Piece> pieces;
     std::vector<int64_t> seg_begin;
     std::vector<int32_t> gpu_seg_lo, gpu_seg_hi;
+    std::vector<MixStream> streams;  // per source GPU: its mixed slot space
+    std::vector<MixBucket> buckets;
+    int64_t mixed_end = 0;           // slots of every GPU's mixed space (the kernels' atom index)
     std::vector<int64_t> bytes;  // n_gpus * n_gpus
     std::vector<int32_t> n_res, n_res_ids;
     std::vector<ReqRec> recs;
@@ -117,11 +125,11 @@ struct kv_plan {
     std::vector<A2AItem> items;
     std::vector<int32_t> item_lo, item_hi;
     std::vector<int64_t> recv_atoms;
-    // device workspace: [seg_begin | segs | tables | recs | out_off | a2a_base | items]
+    // device workspace: [seg_begin | pieces | segs | tables | recs | out_off | a2a_base | items]
     int dev = -1;
     char* dbuf = nullptr;
     size_t dbytes = 0;
-    size_t off_seg_begin = 0, off_segs = 0, off_tables = 0, off_recs = 0, off_outs = 0, off_a2a = 0, off_items = 0;
+    size_t off_seg_begin = 0, off_pieces = 0, off_streams = 0, off_buckets = 0, off_segs = 0, off_tables = 0, off_recs = 0, off_outs = 0, off_a2a = 0, off_items = 0;
     cudaStream_t last_stream = nullptr;
     // kv_switch: packed all-pool tables [req_ptr | block_ids | meta] on the
     // device (plan-owned, from the cache's pool) and their host copy
@@ -593,33 +601,104 @@ static void build_a2a_layout(kv_plan* p, std::vector<Seg>& segs, const std::vect
     }
 }
 
-// The kernels' atom index: exclusive prefix of each segment's slots (holes
-// of the destination-major order included), each source GPU's segment
-// range, and the plan's atom statistics.
-static void index_segments(kv_plan* p) {
-    const int32_t L = p->c->geo.num_layers, n = p->c->n_gpus;
+// Kernel work order of each source GPU.  The GPU's segments
+// are bucketed by destination group (order 1, the default) and laid out
+// bucket after bucket as pieces; the kernel then walks a mixed slot space of
+// K quanta, each quantum taking the next u_b = ceil(s_b / K) slots of every
+// bucket b (s_b its slots; slots past s_b are holes), so at every moment a
+// sender's traffic is split over its receivers in the proportions of the
+// whole switch -- the assumption under t_min.  Without it, a
+// TP group splitting into DP engines (TP8 -> 8 x DP1: every sender holds a
+// slice of every request) pushes request i from all senders into engine
+// i mod n at the same time (ingress hot-spot).  Buckets are
+// visited in an order rotated by the source GPU.  Order 0: one bucket (plan
+// order), K = 1.  Results do not depend on the order: every (atom, replica)
+// is written once, to its own bytes.
+static constexpr int64_t kQuantumSlots = 1024;  // target slots per quantum (4 MiB of 4 KiB atoms)
+
+static void build_work_order(kv_plan* p, const std::vector<int64_t>& slots) {
+    const int32_t n = p->c->n_gpus, H = p->c->geo.num_kv_heads;
     const std::vector<Seg>& segs = p->segs;
-    p->seg_begin.resize(segs.size() + 1);
+    p->pieces.clear();
+    p->seg_begin.clear();
+    p->streams.assign(n, MixStream{});
+    p->buckets.clear();
     p->gpu_seg_lo.assign(n, 0);
     p->gpu_seg_hi.assign(n, 0);
+    int64_t acc = 0, mixed = 0;
+    size_t k = 0;
+    for (int32_t g = 0; g < n; ++g) {
+        p->gpu_seg_lo[g] = (int32_t)p->pieces.size();
+        const size_t lo = k;
+        while (k < segs.size() && segs[k].src_gpu == g) ++k;
+        const size_t hi = k;
+        // buckets: (rotated destination rank, destination degree) -> the GPU's segments, plan order
+        std::vector<std::pair<int64_t, std::vector<int32_t>>> bk;
+        for (size_t s = lo; s < hi; ++s) {
+            const Seg& sg = segs[s];
+            int64_t key = 0;
+            if (p->c->work_order == 1)
+                key = (int64_t)(((sg.dst_g0 - g) % n + n) % n) * 128 + (int64_t)(H / sg.hloc1) * sg.rep1;
+            auto it = std::find_if(bk.begin(), bk.end(), [&](const auto& b) { return b.first == key; });
+            if (it == bk.end()) bk.push_back({key, {(int32_t)s}});
+            else it->second.push_back((int32_t)s);
+        }
+        std::stable_sort(bk.begin(), bk.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+        MixStream& ms = p->streams[g];
+        ms.begin = mixed;
+        ms.b0 = (int32_t)p->buckets.size();
+        ms.nb = (int32_t)bk.size();
+        int64_t total = 0;
+        for (const auto& b : bk) {
+            MixBucket mb{};
+            mb.start = acc;
+            for (int32_t s : b.second) {
+                p->pieces.push_back(Piece{s, 0});
+                p->seg_begin.push_back(acc);
+                acc += slots[s];
+            }
+            mb.size = acc - mb.start;
+            total += mb.size;
+            p->buckets.push_back(mb);
+        }
+        const int64_t K = bk.size() <= 1 ? 1 : std::max<int64_t>(1, total / kQuantumSlots);
+        int64_t qs = 0;
+        for (int32_t b = ms.b0; b < ms.b0 + ms.nb; ++b) {
+            MixBucket& mb = p->buckets[b];
+            mb.u = (int32_t)ceil_div(mb.size, K);
+            mb.P = (int32_t)qs;
+            qs += mb.u;
+        }
+        ms.Qs = (int32_t)std::max<int64_t>(qs, 1);
+        ms.K = (int32_t)K;
+        mixed += total ? K * qs : 0;
+        p->gpu_seg_hi[g] = (int32_t)p->pieces.size();
+    }
+    p->seg_begin.push_back(acc);
+    p->mixed_end = mixed;
+    p->st.n_buckets = (int64_t)p->buckets.size();
+}
+
+// The kernels' atom index: each segment's slots (holes of the
+// destination-major order included), the plan's atom statistics, and the
+// work order over them.
+static void index_segments(kv_plan* p) {
+    const int32_t L = p->c->geo.num_layers;
+    const std::vector<Seg>& segs = p->segs;
+    std::vector<int64_t> slots(segs.size());
     int64_t acc = 0, atoms = 0, writes = 0;
     for (size_t k = 0; k < segs.size(); ++k) {
-        p->seg_begin[k] = acc;
-        acc += (int64_t)L * 2 * segs[k].J1 * segs[k].nh * segs[k].k1;  // incl. holes
-        const int64_t a = (int64_t)L * 2 * segs[k].C * segs[k].nh;     // real atoms
+        slots[k] = (int64_t)L * 2 * segs[k].J1 * segs[k].nh * segs[k].k1;  // incl. holes
+        acc += slots[k];
+        const int64_t a = (int64_t)L * 2 * segs[k].C * segs[k].nh;         // real atoms
         atoms += a;
         writes += a * segs[k].rep1;
     }
-    p->seg_begin[segs.size()] = acc;
-    for (int32_t g = 0; g < n; ++g) {
-        auto lo = std::lower_bound(segs.begin(), segs.end(), g, [](const Seg& a, int32_t v) { return a.src_gpu < v; });
-        auto hi = std::lower_bound(segs.begin(), segs.end(), g + 1, [](const Seg& a, int32_t v) { return a.src_gpu < v; });
-        p->gpu_seg_lo[g] = (int32_t)(lo - segs.begin());
-        p->gpu_seg_hi[g] = (int32_t)(hi - segs.begin());
-    }
     p->st.n_atoms = atoms;
-    p->st.n_atom_slots = acc;
     p->st.n_atom_writes = writes;
+    (void)acc;
+    build_work_order(p, slots);
+    p->st.n_atom_slots = p->mixed_end;  // kernel slots: destination-major holes + mixed-order holes
 }
 
 // a6 sizes and the remap kernel's per-request records; packed all-pool output
@@ -651,17 +730,26 @@ static void build_remap_records(kv_plan* p, const std::vector<int32_t>& rid_off)
     p->st.n_moving = n_moving;
 }
 
-// Device workspace: [seg_begin | segs | tables | recs | out_off | a2a_base | items], 256-byte aligned.
+// Device workspace: [seg_begin | pieces | segs | tables | recs | out_off | a2a_base | items], 256-byte aligned.
 static void layout_workspace(kv_plan* p) {
     auto align = [](size_t x) { return (x + 255) & ~(size_t)255; };
     p->off_seg_begin = 0;
-    p->off_segs = align(p->off_seg_begin + p->seg_begin.size() * sizeof(int64_t));
+    p->off_pieces = align(p->off_seg_begin + p->seg_begin.size() * sizeof(int64_t));
+    p->off_streams = align(p->off_pieces + p->pieces.size() * sizeof(Piece));
+    p->off_buckets = align(p->off_streams + p->streams.size() * sizeof(MixStream));
+    p->off_segs = align(p->off_buckets + p->buckets.size() * sizeof(MixBucket));
     p->off_tables = align(p->off_segs + p->segs.size() * sizeof(Seg));
     p->off_recs = align(p->off_tables + p->tables.size() * sizeof(int32_t));
     p->off_outs = align(p->off_recs + p->recs.size() * sizeof(ReqRec));
     p->off_a2a = align(p->off_outs + p->out_off.size() * sizeof(int32_t));
     p->off_items = align(p->off_a2a + p->a2a_base.size() * sizeof(int64_t));
     p->dbytes = align(p->off_items + p->items.size() * sizeof(A2AItem));
+}
+
+extern "C" kv_status kv_cache_set_work_order(kv_cache* c, int32_t order) {
+    if (!c || (order != 0 && order != 1)) return fail(KV_ERR_INVALID_ARG, "bad kv_cache_set_work_order arguments");
+    c->work_order = order;
+    return KV_OK;
 }
 
 extern "C" kv_status kv_plan_switch(kv_cache* c, const kv_request* reqs, int32_t n_reqs, kv_plan** out) {
@@ -703,6 +791,19 @@ extern "C" kv_status kv_plan_switch(kv_cache* c, const kv_request* reqs, int32_t
     build_a2a_layout(p, segs, seg_req);
     p->segs.swap(segs);
     index_segments(p);
+    // the kernels index piece space with 32-bit slots and each GPU's mixed space with 31-bit ones
+    bool too_big = p->seg_begin.back() >= ((int64_t)1 << 32);
+    for (int32_t g = 0; g < c->n_gpus; ++g) {
+        const int64_t end = g + 1 < c->n_gpus ? p->streams[g + 1].begin : p->mixed_end;
+        too_big = too_big || end - p->streams[g].begin >= ((int64_t)1 << 31);
+    }
+    if (too_big) {
+        rollback_allocations(p, n_reqs);
+        kv_status st = fail(KV_ERR_INVALID_ARG, "plan of %lld atom slots exceeds the kernels' 32-bit index",
+                            (long long)p->seg_begin.back());
+        delete p;
+        return st;
+    }
     build_remap_records(p, rid_off);
     layout_workspace(p);
     p->st.atom_bytes = c->atom_bytes;
@@ -754,6 +855,9 @@ static kv_status ensure_device(kv_plan* p, cudaStream_t stream) {
     }
     char* h = static_cast<char*>(c->stage);
     std::memcpy(h + p->off_seg_begin, p->seg_begin.data(), p->seg_begin.size() * sizeof(int64_t));
+    if (!p->pieces.empty()) std::memcpy(h + p->off_pieces, p->pieces.data(), p->pieces.size() * sizeof(Piece));
+    if (!p->streams.empty()) std::memcpy(h + p->off_streams, p->streams.data(), p->streams.size() * sizeof(MixStream));
+    if (!p->buckets.empty()) std::memcpy(h + p->off_buckets, p->buckets.data(), p->buckets.size() * sizeof(MixBucket));
     if (!p->segs.empty()) std::memcpy(h + p->off_segs, p->segs.data(), p->segs.size() * sizeof(Seg));
     if (!p->tables.empty()) std::memcpy(h + p->off_tables, p->tables.data(), p->tables.size() * sizeof(int32_t));
     if (!p->recs.empty()) std::memcpy(h + p->off_recs, p->recs.data(), p->recs.size() * sizeof(ReqRec));
@@ -780,18 +884,27 @@ static ReshardArgs reshard_args(const kv_plan* p, int32_t gpu) {
     const kv_cache* c = p->c;
     ReshardArgs a{};
     a.seg_begin = reinterpret_cast<const int64_t*>(p->dbuf + p->off_seg_begin);
+    a.pieces = reinterpret_cast<const Piece*>(p->dbuf + p->off_pieces);
+    a.streams = reinterpret_cast<const MixStream*>(p->dbuf + p->off_streams);
+    a.buckets = reinterpret_cast<const MixBucket*>(p->dbuf + p->off_buckets);
     a.segs = reinterpret_cast<const Seg*>(p->dbuf + p->off_segs);
     a.tables = reinterpret_cast<const int32_t*>(p->dbuf + p->off_tables);
     a.layer_base = c->d_layer_base;
     a.seg_lo = gpu < 0 ? 0 : p->gpu_seg_lo[gpu];
-    a.seg_hi = gpu < 0 ? (int32_t)p->segs.size() : p->gpu_seg_hi[gpu];
-    a.atom_lo = p->seg_begin[a.seg_lo];
-    a.atom_hi = p->seg_begin[a.seg_hi];
+    a.seg_hi = gpu < 0 ? (int32_t)p->pieces.size() : p->gpu_seg_hi[gpu];
+    const int32_t n = c->n_gpus;
+    a.st_lo = gpu < 0 ? 0 : gpu;
+    a.st_hi = gpu < 0 ? n : gpu + 1;
+    a.atom_lo = p->streams[a.st_lo].begin;
+    a.atom_hi = a.st_hi < n ? p->streams[a.st_hi].begin : p->mixed_end;
+    if (gpu < 0) {  // the first GPU with work (the stream search needs streams[st_lo].begin <= slot)
+        while (a.st_lo + 1 < n && p->streams[a.st_lo + 1].begin == a.atom_lo) ++a.st_lo;
+    }
     a.L = c->geo.num_layers;
     a.atom_bytes = (int32_t)c->atom_bytes;
     a.M = c->M;
     a.max_rep = 1;
-    for (int32_t k = a.seg_lo; k < a.seg_hi; ++k) a.max_rep = std::max(a.max_rep, p->segs[k].rep1);
+    for (int32_t k = a.seg_lo; k < a.seg_hi; ++k) a.max_rep = std::max(a.max_rep, p->segs[p->pieces[k].seg].rep1);
     return a;
 }
 
@@ -1176,6 +1289,68 @@ extern "C" kv_status kv_plan_get_stats(const kv_plan* p, kv_plan_stats* st, int6
     if (!p) return fail(KV_ERR_INVALID_ARG, "plan is NULL");
     if (st) *st = p->st;
     if (bytes_matrix) std::memcpy(bytes_matrix, p->bytes.data(), p->bytes.size() * sizeof(int64_t));
+    return KV_OK;
+}
+
+// Bytes of piece-space slots [a0, a1) of segment piece k: destination bytes
+// per GPU (replicas included, holes excluded) and, in column n, source reads.
+static void count_piece(const kv_plan* p, int32_t k, int64_t a0, int64_t a1, int64_t* row_out) {
+    const int32_t n = p->c->n_gpus;
+    const int64_t ab = p->c->atom_bytes;
+    const Seg& sg = p->segs[p->pieces[k].seg];
+    const int64_t R = (int64_t)sg.nh * sg.k1;  // slots per (layer, K/V, destination block) row
+    for (int64_t r = a0 / R; r * R < a1; ++r) {
+        const int64_t j = r % sg.J1;
+        const int64_t valid = std::min<int64_t>(sg.k1, sg.C - j * sg.k1);  // chunks w < valid are real
+        const int64_t o0 = std::max<int64_t>(a0 - r * R, 0), o1 = std::min<int64_t>(a1 - r * R, R);
+        for (int64_t hh = o0 / sg.k1; hh * sg.k1 < o1; ++hh) {
+            const int64_t w0 = std::max<int64_t>(o0 - hh * sg.k1, 0), w1 = std::min<int64_t>(o1 - hh * sg.k1, valid);
+            if (w1 <= w0) continue;
+            const int64_t cnt = w1 - w0;
+            const int32_t h = sg.h0 + (int32_t)hh;
+            row_out[n] += cnt * ab;
+            for (int32_t rj = 0; rj < sg.rep1; ++rj) {
+                const int32_t rid = sg.rep1 == 1 ? h / sg.hloc1 : h * sg.rep1 + rj;
+                const int32_t m = sg.dst_inv < 0 ? rid : p->tables[sg.dst_inv + rid];
+                row_out[sg.dst_g0 + m] += cnt * ab;
+            }
+        }
+    }
+}
+
+// Piece-space range [b0, b1) (global) of GPU pieces [lo, hi).
+static void count_piece_range(const kv_plan* p, int32_t lo, int32_t hi, int64_t b0, int64_t b1, int64_t* row_out) {
+    auto it = std::upper_bound(p->seg_begin.begin() + lo, p->seg_begin.begin() + hi, b0);
+    for (int32_t k = (int32_t)(it - p->seg_begin.begin()) - 1; k < hi && p->seg_begin[k] < b1; ++k) {
+        const int64_t s0 = std::max(b0, p->seg_begin[k]), s1 = std::min(b1, p->seg_begin[k + 1]);
+        if (s1 > s0) count_piece(p, k, s0 - p->seg_begin[k] + p->pieces[k].slot0, s1 - p->seg_begin[k] + p->pieces[k].slot0, row_out);
+    }
+}
+
+extern "C" kv_status kv_plan_work_order(const kv_plan* p, int32_t gpu, int32_t* n_rows, int64_t* out) {
+    if (!p || !n_rows || gpu < 0 || gpu >= p->c->n_gpus) return fail(KV_ERR_INVALID_ARG, "bad kv_plan_work_order arguments");
+    const int32_t n = p->c->n_gpus;
+    const MixStream& ms = p->streams[gpu];
+    const int64_t len = (gpu + 1 < n ? p->streams[gpu + 1].begin : p->mixed_end) - ms.begin;
+    const int64_t rows = ceil_div(len, kQuantumSlots);
+    *n_rows = (int32_t)rows;
+    if (!out) return KV_OK;
+    std::memset(out, 0, sizeof(int64_t) * (size_t)rows * (n + 1));
+    const int32_t lo = p->gpu_seg_lo[gpu], hi = p->gpu_seg_hi[gpu];
+    for (int64_t r = 0; r < rows; ++r) {
+        int64_t* row_out = out + (size_t)r * (n + 1);
+        const int64_t x0 = r * kQuantumSlots, x1 = std::min(len, x0 + kQuantumSlots);
+        for (int64_t q = x0 / ms.Qs; q * ms.Qs < x1; ++q)
+            for (int32_t b = ms.b0; b < ms.b0 + ms.nb; ++b) {
+                const MixBucket& mb = p->buckets[b];
+                // mixed slots [q*Qs + P, q*Qs + P + u) hold bucket slots [q*u, q*u + u)
+                const int64_t m0 = std::max(x0, q * ms.Qs + mb.P), m1 = std::min(x1, q * ms.Qs + mb.P + mb.u);
+                if (m1 <= m0) continue;
+                const int64_t o0 = q * mb.u + (m0 - q * ms.Qs - mb.P);
+                const int64_t o1 = std::min(mb.size, o0 + (m1 - m0));
+                if (o1 > o0) count_piece_range(p, lo, hi, mb.start + o0, mb.start + o1, row_out);
+            }
+    }
     return KV_OK;
 }
 

@@ -63,6 +63,29 @@ struct Seg {
 };
 static_assert(sizeof(Seg) == 64, "Seg is 64 bytes");
 
+// One work piece: slots [slot0, slot0 + n) of segment seg (n = the next
+// piece's begin minus this one's), in piece space: a source GPU's segments
+// bucket after bucket (destination groups, build_work_order).
+struct Piece {
+    int32_t seg, slot0;
+};
+
+// A source GPU's mixed slot space (the kernels' atom index):
+// K quanta of Qs slots; quantum q holds, for each bucket b, the bucket's
+// slots [q*u_b, (q+1)*u_b) at offset P_b (slots >= size_b are holes).  So a
+// sender's traffic is split over its receivers in the switch's proportions
+// at every moment, not one receiver after another.
+struct MixStream {
+    int64_t begin;    // first mixed slot of the GPU (global)
+    int32_t Qs, K;    // slots per quantum, quanta
+    int32_t b0, nb;   // the GPU's buckets in the bucket array
+};
+struct MixBucket {
+    int64_t start;    // first piece-space slot of the bucket
+    int64_t size;     // its slots
+    int32_t u, P;     // slots per quantum, offset inside the quantum
+};
+
 // Per-request record used by the remap kernel (a6).
 struct ReqRec {
     int32_t dst_g0, dst_p, n1, dst_tab;
@@ -71,12 +94,16 @@ struct ReqRec {
 };
 
 struct ReshardArgs {
-    const int64_t* seg_begin;  // [n_seg + 1] exclusive prefix of atom counts (global)
+    const int64_t* seg_begin;  // [n_piece + 1] exclusive prefix of the pieces' slot counts (piece space)
+    const Piece* pieces;       // [n_piece]
+    const MixStream* streams;  // [n_gpus] mixed slot spaces
+    const MixBucket* buckets;
+    int32_t st_lo, st_hi;      // source GPUs of this launch
     const Seg* segs;           // [n_seg]
     const int32_t* tables;     // source + destination tables
     char* const* layer_base;   // [n_gpus * L] pool layer pointers
-    int32_t seg_lo, seg_hi;    // segment range of this launch
-    int64_t atom_lo, atom_hi;  // atom range (= seg_begin[seg_lo], seg_begin[seg_hi])
+    int32_t seg_lo, seg_hi;    // piece range of this launch
+    int64_t atom_lo, atom_hi;  // mixed slot range (streams[st_lo].begin .. end of st_hi - 1)
     int32_t L;
     int32_t atom_bytes;        // B*d*e
     int64_t M;                 // block bytes per layer

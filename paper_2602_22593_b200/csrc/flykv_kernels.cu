@@ -56,9 +56,29 @@ __device__ __forceinline__ int find_seg(const int64_t* __restrict__ seg_begin, i
     return lo;
 }
 
-__device__ __forceinline__ void decode(const ReshardArgs& a, int64_t atom, int s, AtomAddr& out) {
-    const Seg sg = a.segs[s];
-    uint32_t local = (uint32_t)(atom - __ldg(a.seg_begin + s));
+// Mixed slot (the kernels' atom index) -> piece-space slot, or -1 for a hole
+// (MixStream, flykv_internal.h).
+__device__ __forceinline__ int64_t unmix(const ReshardArgs& a, int64_t atom) {
+    int lo = a.st_lo, hi = a.st_hi;  // streams[lo].begin <= atom
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(&a.streams[mid].begin) <= atom) lo = mid;
+        else hi = mid;
+    }
+    const MixStream ms = a.streams[lo];
+    const uint32_t x = (uint32_t)(atom - ms.begin);
+    const uint32_t q = x / (uint32_t)ms.Qs, r = x - q * (uint32_t)ms.Qs;
+    int b = ms.b0;
+    while (b + 1 < ms.b0 + ms.nb && (uint32_t)__ldg(&a.buckets[b + 1].P) <= r) ++b;
+    const MixBucket mb = a.buckets[b];
+    const int64_t o = (int64_t)q * mb.u + (r - (uint32_t)mb.P);
+    return o < mb.size ? mb.start + o : -1;
+}
+
+// Slot `local` of the segment of piece s (local counts from the segment's
+// first slot: the piece's offset is already added).
+__device__ __forceinline__ void decode(const ReshardArgs& a, int s, uint32_t local, AtomAddr& out) {
+    const Seg sg = a.segs[__ldg(&a.pieces[s].seg)];
     const uint32_t nh = (uint32_t)sg.nh, k1 = (uint32_t)sg.k1, J1 = (uint32_t)sg.J1;
     const uint32_t w = local % k1;        // (((l*2 + kv)*J1 + j)*nh + hh)*k1 + w
     local /= k1;
@@ -146,22 +166,32 @@ struct LaneAtom {
     const char* src;
     char* dst0;
     int32_t rep1;
+    uint32_t patom;   // piece-space slot of the atom (< 2^32, host-checked): replicas > 0 re-decode from it
 };
 
-__device__ __forceinline__ void lane_decode(const ReshardArgs& a, int64_t atom, LaneAtom& la) {
+__device__ __forceinline__ void lane_decode(const ReshardArgs& a, int64_t slot, LaneAtom& la) {
+    const int64_t atom = unmix(a, slot);
+    if (atom < 0) {  // hole of the mixed order
+        la.src = nullptr;
+        la.dst0 = nullptr;
+        la.rep1 = 0;
+        return;
+    }
     const int s = find_seg(a.seg_begin, a.seg_lo, a.seg_hi, atom);
+    const uint32_t local = (uint32_t)(atom - __ldg(a.seg_begin + s)) + (uint32_t)__ldg(&a.pieces[s].slot0);
     AtomAddr ad;
-    decode(a, atom, s, ad);
+    decode(a, s, local, ad);
+    la.patom = (uint32_t)atom;
     la.src = ad.src;
     la.rep1 = ad.rep1;  // 0 for a hole: nothing is read or written
     la.dst0 = ad.src ? dst_ptr(a, ad, 0) : nullptr;
     if ((a.staged == 1 || a.staged == 2) && la.rep1 > 0) {  // comparator: slot-order pack or unpack
-        char* slot = a.staging + (atom - a.atom_lo) * (int64_t)a.atom_bytes;
+        char* stg = a.staging + (slot - a.atom_lo) * (int64_t)a.atom_bytes;
         if (a.staged == 1) {
-            la.dst0 = slot;
+            la.dst0 = stg;
             la.rep1 = 1;
         } else {
-            la.src = slot;
+            la.src = stg;
         }
     }
 }
@@ -171,11 +201,12 @@ __device__ __forceinline__ T shfl_ptr(T p, int k) {
     return reinterpret_cast<T>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(p), k));
 }
 
-// Destination of replica j of `atom` (warp-uniform re-decode, rare path).
-__device__ __forceinline__ char* replica_ptr(const ReshardArgs& a, int64_t atom, int j) {
-    const int s = find_seg(a.seg_begin, a.seg_lo, a.seg_hi, atom);
+// Destination of replica j of the atom at piece-space slot patom
+// (warp-uniform re-decode, GQA replication only).
+__device__ __forceinline__ char* replica_ptr(const ReshardArgs& a, uint32_t patom, int j) {
+    const int s = find_seg(a.seg_begin, a.seg_lo, a.seg_hi, (int64_t)patom);
     AtomAddr ad;
-    decode(a, atom, s, ad);
+    decode(a, s, (uint32_t)(patom - __ldg(a.seg_begin + s)) + (uint32_t)__ldg(&a.pieces[s].slot0), ad);
     return dst_ptr(a, ad, j);
 }
 
@@ -221,12 +252,14 @@ __global__ void __launch_bounds__(256, 2) flykv_reshard_kernel(const ReshardArgs
                 const char* s[U];
                 char* d0[U];
                 int rep[U];
+                uint32_t pa[U];
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     const int k = (k0 + u < n) ? k0 + u : k0;
                     s[u] = shfl_ptr(la.src, k);
                     d0[u] = shfl_ptr(la.dst0, k);
                     rep[u] = (k0 + u < n) ? __shfl_sync(0xffffffffu, la.rep1, k) : 0;
+                    pa[u] = __shfl_sync(0xffffffffu, la.patom, k);
                 }
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
@@ -245,12 +278,12 @@ __global__ void __launch_bounds__(256, 2) flykv_reshard_kernel(const ReshardArgs
                 for (int u = 0; u < U; ++u) {
                     rp[u] = nullptr;
                     if (par && rep[u] > 1 && lane > 0 && lane < rep[u])
-                        rp[u] = replica_ptr(a, first + (int64_t)(k0 + u) * nwarps, lane);
+                        rp[u] = replica_ptr(a, pa[u], lane);
                 }
                 auto dst_of = [&](int u, int j) -> int4* {
                     char* dj = j == 0             ? d0[u]
                                : (par && j < 32) ? shfl_ptr(rp[u], j)
-                                                 : replica_ptr(a, first + (int64_t)(k0 + u) * nwarps, j);
+                                                 : replica_ptr(a, pa[u], j);
                     return reinterpret_cast<int4*>(dj) + lane;
                 };
                 if (a.rep_flags & 2) {  // replica-major: replica j of all U atoms, then j + 1
@@ -293,6 +326,7 @@ __global__ void __launch_bounds__(256, 2) flykv_reshard_kernel(const ReshardArgs
                     const int4* src = reinterpret_cast<const int4*>(shfl_ptr(la.src, k)) + lane;
                     int4* dst = reinterpret_cast<int4*>(shfl_ptr(la.dst0, k)) + lane;
                     const int rep = __shfl_sync(0xffffffffu, la.rep1, k);
+                    const uint32_t pa = __shfl_sync(0xffffffffu, la.patom, k);
                     if (rep == 0) continue;  // hole (warp-uniform)
                     int4 v[VPL];
 #pragma unroll
@@ -300,7 +334,7 @@ __global__ void __launch_bounds__(256, 2) flykv_reshard_kernel(const ReshardArgs
 #pragma unroll
                     for (int i = 0; i < VPL; ++i) st_stream(dst + i * 32, v[i]);
                     for (int j = 1; j < rep; ++j) {
-                        int4* dj = reinterpret_cast<int4*>(replica_ptr(a, first + k * nwarps, j)) + lane;
+                        int4* dj = reinterpret_cast<int4*>(replica_ptr(a, pa, j)) + lane;
 #pragma unroll
                         for (int i = 0; i < VPL; ++i) st_stream(dj + i * 32, v[i]);
                     }
@@ -310,9 +344,10 @@ __global__ void __launch_bounds__(256, 2) flykv_reshard_kernel(const ReshardArgs
                     const char* s = shfl_ptr(la.src, k);
                     char* d0 = shfl_ptr(la.dst0, k);
                     const int rep = __shfl_sync(0xffffffffu, la.rep1, k);
+                    const uint32_t pa = __shfl_sync(0xffffffffu, la.patom, k);
                     const int nv = a.atom_bytes >> 4;
                     for (int j = 0; j < rep; ++j) {
-                        char* dj = j == 0 ? d0 : replica_ptr(a, first + k * nwarps, j);
+                        char* dj = j == 0 ? d0 : replica_ptr(a, pa, j);
                         for (int i = lane; i < nv; i += 32)
                             st_stream(reinterpret_cast<int4*>(dj) + i, ld_stream(reinterpret_cast<const int4*>(s) + i));
                     }
@@ -469,7 +504,7 @@ __global__ void __launch_bounds__(W * 32) flykv_reshard_tma_kernel(const Reshard
     // per-stage pending store: replica-0 destination, replica count, atom index (lane 0 only)
     __shared__ char* pend_dst[W][S];
     __shared__ int32_t pend_rep[W][S];
-    __shared__ int64_t pend_atom[W][S];
+    __shared__ uint32_t pend_atom[W][S];
     if (lane == 0) {
         for (int i = 0; i < S; ++i)
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bars + i)));
@@ -507,6 +542,7 @@ __global__ void __launch_bounds__(W * 32) flykv_reshard_tma_kernel(const Reshard
             const char* s = shfl_ptr(la.src, k);
             char* d0 = shfl_ptr(la.dst0, k);
             const int rep = __shfl_sync(0xffffffffu, la.rep1, k);
+            const uint32_t pa = __shfl_sync(0xffffffffu, la.patom, k);
             if (rep == 0) continue;  // hole (warp-uniform)
             if (lane == 0) {
                 if (issued >= (uint32_t)D) store_one(stored++);
@@ -517,7 +553,7 @@ __global__ void __launch_bounds__(W * 32) flykv_reshard_tma_kernel(const Reshard
                 asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(S - D) : "memory");
                 pend_dst[wid][st] = d0;
                 pend_rep[wid][st] = rep;
-                pend_atom[wid][st] = R + warp + (int64_t)k * nwarps;
+                pend_atom[wid][st] = pa;  // replicas re-decode from the piece-space slot
                 const uint32_t bar = smem_u32(bars + st);
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
                              : "memory");

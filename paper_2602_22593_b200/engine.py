@@ -38,6 +38,10 @@ class KVSwitchEngine:
         self.device = torch.device(device)
         self.pools = DevicePools(geom, num_blocks, self.device, fill=fill)
         self.cache = self.pools.make_cache(tp_degrees)
+        # every pool is on this one device: no links to balance, so the
+        # kernels visit atoms in plan order (the mixed order, for one
+        # process per GPU, measured 0.1-1.4% slower here)
+        self.cache.set_work_order(0)
         self.geom = geom
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
 

@@ -66,7 +66,8 @@ class Request(C.Structure):
 
 class PlanStats(C.Structure):
     _fields_ = [(n, C.c_int64) for n in ("n_requests", "n_moving", "n_atoms", "n_atom_writes", "atom_bytes",
-                                         "payload_bytes", "h2d_bytes", "n_segments", "n_atom_slots")]
+                                         "payload_bytes", "h2d_bytes", "n_segments", "n_atom_slots",
+                                         "n_buckets")]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
@@ -155,6 +156,8 @@ _sig("kv_strerror", C.c_char_p, C.c_int)
 _sig("kv_last_error", C.c_char_p)
 _sig("kv_launch_count", C.c_int64)
 _sig("kv_set_reshard_impl", C.c_int, C.c_int32, C.c_int32)
+_sig("kv_cache_set_work_order", C.c_int, _P, C.c_int32)
+_sig("kv_plan_work_order", C.c_int, _P, C.c_int32, _I32P, _I64P)
 
 EXPORTED = ["kv_cache_create", "kv_cache_destroy", "kv_layout", "kv_blocks_for", "kv_alloc", "kv_reserve",
             "kv_free", "kv_free_count", "kv_held_mask", "kv_plan_switch", "kv_plan_upload", "kv_reshard", "kv_reshard_staged",
@@ -163,7 +166,8 @@ EXPORTED = ["kv_cache_create", "kv_cache_destroy", "kv_layout", "kv_blocks_for",
             "kv_suggest_rank_ids", "kv_plan_get_stats", "kv_plan_destroy",
             "weight_shard_view", "kv_gather_view", "kv_vmm_granularity", "kv_vmm_alloc", "kv_vmm_free",
             "weight_view_alias", "weight_view_unalias", "kv_paged_decode", "kv_ipc_export", "kv_ipc_import", "kv_ipc_close",
-            "kv_stream_sync", "kv_strerror", "kv_last_error", "kv_launch_count", "kv_set_reshard_impl"]
+            "kv_stream_sync", "kv_strerror", "kv_last_error", "kv_launch_count", "kv_set_reshard_impl",
+            "kv_cache_set_work_order", "kv_plan_work_order"]
 
 
 # ----------------------------------------------------------------- marshalling
@@ -277,6 +281,10 @@ class KVCache:
     def plan_switch(self, requests) -> "Plan":
         return kv_plan_switch(self, requests)
 
+    def set_work_order(self, order: int):
+        """1 = destination-rotated (default), 0 = plan order (kv_cache_set_work_order)."""
+        _check(_lib.kv_cache_set_work_order(self._h, order))
+
 
 # ----------------------------------------------------------------- plan
 class Plan:
@@ -347,6 +355,16 @@ class Plan:
         mat = np.zeros(n * n, dtype=np.int64)
         _check(_lib.kv_plan_get_stats(self._h, C.byref(st), mat.ctypes.data_as(_I64P)))
         return st.as_dict(), mat.reshape(n, n)
+
+    def work_order(self, gpu: int) -> np.ndarray:
+        """[n_pieces, n_gpus + 1] int64: destination bytes per GPU of each of
+        `gpu`'s work pieces in kernel order, last column the bytes read."""
+        n = self.cache.n_gpus
+        k = C.c_int32()
+        _check(_lib.kv_plan_work_order(self._h, gpu, C.byref(k), None))
+        out = np.zeros((max(k.value, 1), n + 1), dtype=np.int64)
+        _check(_lib.kv_plan_work_order(self._h, gpu, C.byref(k), out.ctypes.data_as(_I64P)))
+        return out[:k.value]
 
 
 # numpy twin of the kv_request struct (offsets checked against ctypes below),

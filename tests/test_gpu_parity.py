@@ -24,14 +24,18 @@ def _F():
     return flykv
 
 
-def run_parity(geo, nb, spec, seed=0, per_gpu_launch=False, check_pools=True, staged=False, a2a=False):
+def run_parity(geo, nb, spec, seed=0, per_gpu_launch=False, check_pools=True, staged=False, a2a=False,
+               work_order=1):
     """spec: list of (T, src_group, dst_group).  Runs the product on cuda:0
-    (virtual ranks) and the oracle on host copies; asserts exact equality."""
+    (virtual ranks) and the oracle on host copies; asserts exact equality.
+    work_order: the kernels' visiting order (kv_cache_set_work_order); it
+    must not change any result."""
     F = _F()
     from paper_2602_22593_b200.engine import KVSwitchEngine
     og = O.Geom(*geo)
     g = F.geometry(*geo)
     eng = KVSwitchEngine(g, nb, "cuda:0", tp_degrees=(2, 4, 8, 16))
+    eng.cache.set_work_order(work_order)
     for gpu, t in enumerate(eng.pools.tensors):
         synth.fill_hash_torch(t, gpu, seed=seed + 2)
     torch.cuda.synchronize()
@@ -149,8 +153,9 @@ def test_tiny_config_dp2_tp2_and_back():
 GRID = [(H, p0, p1) for H in (1, 2, 4, 8) for p0 in (1, 2, 4, 8) for p1 in (1, 2, 4, 8) if p0 != p1]
 
 
+@pytest.mark.parametrize("work_order", [1, 0])
 @pytest.mark.parametrize("H,p0,p1", GRID)
-def test_grid_ragged(H, p0, p1):
+def test_grid_ragged(H, p0, p1, work_order):
     """All degree pairs up to 8 (incl. GQA replication p > H), ragged T
     spanning many blocks, partial tail atoms, 2 KiB atoms, 8 virtual ranks."""
     geo = (3, H, 64, 16, 2)
@@ -158,7 +163,7 @@ def test_grid_ragged(H, p0, p1):
     Ts = [1, 15, 16, 17, 33, 100, 257, 1000, 31, 64]
     spec = [(T, ((i * p0) % n_gpus, p0), (((i + 3) * p1) % n_gpus, p1)) for i, T in enumerate(Ts)]
     nb = [256] * n_gpus
-    run_parity(geo, nb, spec, seed=H * 7 + p0 + 3 * p1)
+    run_parity(geo, nb, spec, seed=H * 7 + p0 + 3 * p1, work_order=work_order)
 
 
 @pytest.mark.parametrize("d,B,e", [(128, 16, 2), (24, 16, 2), (8, 4, 2), (256, 16, 2), (64, 16, 4), (16, 1, 2)])
@@ -177,6 +182,22 @@ def test_per_gpu_launches_and_mixed_plan():
     spec = [(300, (0, 1), (0, 2)), (0, (1, 1), (0, 4)), (77, (2, 2), (2, 2)), (513, (4, 4), (4, 1)),
             (129, (3, 1), (0, 8)), (1, (6, 2), (0, 4)), (64, (5, 1), (5, 1))]
     run_parity(geo, [128] * 8, spec, seed=11, per_gpu_launch=True)
+
+
+@pytest.mark.parametrize("work_order", [1, 0])
+@pytest.mark.parametrize("mode", ["per_gpu", "staged", "a2a", "one_launch"])
+def test_mixed_order_splits(work_order, mode):
+    """TP8 -> 8 x DP1 and TP4 x 2 -> DP (the splits whose senders converge on
+    one receiver in plan order) with enough atoms per sender for many quanta
+    of the mixed order (K > 1, holes at the buckets' ragged ends): every
+    launch shape and both orders equal the oracle byte for byte."""
+    geo = (8, 8, 64, 16, 2)
+    rng = np.random.default_rng(31 + work_order)
+    T = [int(x) for x in rng.integers(900, 2600, size=16)]
+    spec = [(t, (0, 8), (i % 8, 1)) for i, t in enumerate(T[:10])]
+    spec += [(t, ((i % 2) * 4, 4), ((i % 2) * 4 + (i // 2) % 4, 1)) for i, t in enumerate(T[10:])]
+    run_parity(geo, [900] * 8, spec, seed=17, per_gpu_launch=mode == "per_gpu", staged=mode == "staged",
+               a2a=mode == "a2a", work_order=work_order)
 
 
 def test_empty_plan():
