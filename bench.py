@@ -504,6 +504,13 @@ def run_single(args):
         p0_ = eng.plan(waves_of(state["reqs"])[0][0])
         fwd_matrix = p0_.stats()[1]
         p0_.destroy()
+        fwd_rows = None
+        if w.n_gpus > 1:  # the forward plan in the mixed order an N-GPU run would use (link model)
+            eng.cache.set_work_order(1)
+            p0_ = eng.plan(waves_of(state["reqs"])[0][0])
+            fwd_rows = [p0_.work_order(x) for x in range(w.n_gpus)]
+            p0_.destroy()
+            eng.cache.set_work_order(args.work_order)
         clk = ClockSampler(torch.cuda.current_device(), args.clock_ms).start()
         stats = None
         for _ in range(max(args.warmup, 1)):
@@ -607,8 +614,10 @@ def run_single(args):
         modeled = {"n_gpus": w.n_gpus, "t_min_ms": round(t_min * 1e3, 3),
                    "max_egress_GB": round(float(eg.max()) / 1e9, 3), "max_ingress_GB": round(float(ing.max()) / 1e9, 3),
                    "local_fraction": round(float(np.trace(fwd_matrix) / max(fwd_matrix.sum(), 1)), 4),
+                   "t_model_mixed_order_ms": round(ordered_link_model(fwd_rows, hbm_peak) * 1e3, 3),
                    "rank_ids": args.rank_ids, "link_GBps": FALLBACK_NVLINK_GBS,
-                   "note": "model of an N-GPU run from the plan's byte matrix, not measured"}
+                   "note": "model of an N-GPU run of the forward plan, not measured: t_min from its byte matrix, "
+                           "t_model_mixed_order_ms from bench.ordered_link_model of its mixed kernel order"}
         del off
     # DRAM bytes of one forward launch from a committed ncu --set full capture
     # (plus that launch's algorithmic bytes: under GQA the two directions of
@@ -799,9 +808,13 @@ def run_multi(args):
 
     step_stats = []
 
+    orders = []   # rank 0: kernel work order of a forward and a return plan (warm-up), for the link model
+
     def step(timed=False, read_back=False):
         plan = F.kv_plan_switch(cache, state["reqs"])
         plan.upload(stream)
+        if rank == 0 and not timed and not read_back and len(orders) < 2:
+            orders.append([plan.work_order(x) for x in range(world)])
         if timed:
             step_stats.append(plan.stats())
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -900,6 +913,8 @@ def run_multi(args):
             t_min += t / len(step_stats)
             busiest += float(max(eg.max(), ing.max())) / len(step_stats)
         achieved = busiest / (kern_ms / 1e3) / 1e9
+        # fluid model of the same plans in the kernels' visiting order (ingress contention included)
+        t_model = (sum(ordered_link_model(o, hbm_peak) for o in orders) / len(orders)) if orders else None
         hbm_algo = sum((x[0]["n_atoms"] + x[0]["n_atom_writes"]) * x[0]["atom_bytes"] for x in step_stats) / len(step_stats)
         line = {
             "metric": "DP<->TP KV re-layout GB/s", "value": round(payload_sum / (total_ms / 1e3) / 1e9, 3),
@@ -920,6 +935,8 @@ def run_multi(args):
                           "unit": "GB/s", "frac": round(achieved / FALLBACK_NVLINK_GBS, 4), "traffic": None,
                           "peak_source": "measured peer copy per direction (B200_PROFILING.md 770 GB/s)",
                           "t_min_ms": round(t_min * 1e3, 4), "frac_of_t_min": round(t_min * 1e3 / kern_ms, 4),
+                          "t_model_ms": round(t_model * 1e3, 4) if t_model else None,
+                          "work_order": ["plan", "mixed"][args.work_order],
                           "kernel": "flykv_reshard_kernel (busiest GPU's egress/ingress per launch)"}
                          if not same_dev else
                          {"bound": "hbm", "achieved": round(hbm_algo / (total_ms / args.steps / 1e3) / 1e9, 1),
