@@ -1,8 +1,8 @@
 """Communicator pool and replicated planning, world_size 2 and 4 over gloo on
 CPU (no GPU): aligned-group enumeration, eager construction and
 O(1) lookup, and every rank building the identical plan from the
-globally agreed request order -- the property the one-process-per-GPU
-path relies on."""
+globally agreed request order, including the kernels' mixed work
+order -- the property the one-process-per-GPU path relies on."""
 import os
 import socket
 
@@ -65,7 +65,10 @@ def _worker(rank, world, port, q):
                                         enumerate(zip(w.T, w.src, w.dst, tabs))])
         digest = np.concatenate(plan.dst_tables()).astype(np.int64)
         st, mat = plan.stats()
-        mine = (int(digest.sum()), int((digest * np.arange(digest.size)).sum()), int(mat.sum()))
+        # the kernels' work order too: every rank can model (or check) every sender's schedule
+        wo = np.concatenate([plan.work_order(x).reshape(-1) for x in range(world)]).astype(np.int64)
+        mine = (int(digest.sum()), int((digest * np.arange(digest.size)).sum()), int(mat.sum()),
+                int((wo * (np.arange(wo.size) % 9973 + 1)).sum()), int(st["n_buckets"]), int(st["n_atom_slots"]))
         allv = [None] * world
         dist.all_gather_object(allv, mine)
         out["identical_plans"] = all(v == allv[0] for v in allv)
