@@ -963,7 +963,7 @@ extern "C" kv_status kv_pack(kv_plan* p, int32_t src_gpu, void* buf, const int64
     if (s) return s;
     p->last_stream = stream;
     ReshardArgs a = reshard_args(p, src_gpu);
-    a.peer = 1;  // LDG/STG path
+    a.peer = 0;  // the send buffer is local: LDG/STG, or the TMA bulk ring under kv_set_reshard_impl(2)
     a.staged = 3;
     a.a2a_base = reinterpret_cast<const int64_t*>(p->dbuf + p->off_a2a);
     a.a2a_buf = static_cast<char*>(buf);

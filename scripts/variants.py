@@ -98,6 +98,9 @@ def main():
                 F.kv_unpack(plan, d, a2a_buf, off[:, d], stream)
     res["a2a_pack_only_ms"] = timeit(pack_only)
     res["a2a_unpack_only_ms"] = timeit(unpack_only)
+    F.set_reshard_impl(2, 0)   # kv_pack through the TMA bulk ring (loads into shared memory, bulk stores into the send chunks)
+    res["a2a_pack_only_tma_ms"] = timeit(pack_only)
+    F.set_reshard_impl(0, 0)
     del a2a_buf
     n = st["payload_bytes"]
     a = torch.empty(n, dtype=torch.uint8, device="cuda:0")

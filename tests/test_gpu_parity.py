@@ -373,19 +373,22 @@ def test_launch_counter_moves():
     assert F.launch_count() >= before + 3
 
 
+@pytest.mark.parametrize("a2a", [False, True])
 @pytest.mark.parametrize("impl", [1, 2, 3])
 @pytest.mark.parametrize("H,p0,p1", [(8, 1, 2), (8, 2, 1), (4, 1, 8), (2, 8, 1), (8, 4, 8)])
 @pytest.mark.parametrize("d", [64, 128])
-def test_reshard_variants(impl, H, p0, p1, d):
+def test_reshard_variants(impl, H, p0, p1, d, a2a):
     """Every reshard kernel variant (LDG/STG, TMA bulk ring, 2 atoms in
-    flight) is bit-exact, incl. GQA replication, 2 KiB and 4 KiB atoms."""
+    flight) is bit-exact, incl. GQA replication, 2 KiB and 4 KiB atoms; with
+    a2a, the same variants as kv_pack into per-destination send chunks (TMA
+    bulk stores into the contiguous send buffer under impl 2)."""
     F = _F()
     F.set_reshard_impl(impl, 0)
     try:
         geo = (2, H, d, 16, 2)
         Ts = [1, 15, 16, 17, 33, 100, 257, 1000, 31, 64, 700, 2049]
         spec = [(T, ((i * p0) % 8, p0), (((i + 3) * p1) % 8, p1)) for i, T in enumerate(Ts)]
-        run_parity(geo, [400] * 8, spec, seed=impl * 31 + H + p0 + p1)
+        run_parity(geo, [400] * 8, spec, seed=impl * 31 + H + p0 + p1, a2a=a2a)
     finally:
         F.set_reshard_impl(0, 0)
 
