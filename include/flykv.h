@@ -512,7 +512,7 @@ kv_status kv_cache_set_work_order(kv_cache* cache, int32_t order);
 /* Tuning knob for the reshard kernel (process-wide): impl 0 = default
  * (LDG/STG warp copy, two atoms in flight per warp for 2/4 KiB atoms), 1 =
  * LDG/STG one atom per warp iteration, 2 = TMA bulk-copy ring (local pools
- * only; peer pools always use LDG/STG), 3 = same as 0; ctas_per_sm 0 =
+ * and kv_pack's send chunks only; peer pools always use LDG/STG), 3 = same as 0; ctas_per_sm 0 =
  * occupancy maximum.  Measured alternatives, see DESIGN.md section 7. */
 kv_status kv_set_reshard_impl(int32_t impl, int32_t ctas_per_sm);
 
