@@ -2,8 +2,8 @@
 pool pointers): random sequences of reserve/alloc/free/plan/commit/destroy
 keep the paper's invariants -- conservation allocated + free == num_blocks
 per GPU, uniform IDs across a TP group (R6), transactional failures
-(S:207), byte invariance of what the plan moves, and agreement with the
-oracle's allocator."""
+(S:207), byte invariance of what the plan moves (also per sender, over the
+kernels' work order), and agreement with the oracle's allocator."""
 import numpy as np
 import pytest
 
@@ -75,6 +75,11 @@ def test_random_sequences_keep_invariants(H, nb, ops):
             want = sum(2 * 2 * H * (-(-T_ // 4)) * 4 * 8 * 2 * O.replicas(og, g2[1])
                        for (_, T_, g_, _) in moving if tuple(g_) != tuple(g2))
             assert stt["payload_bytes"] == want == int(mat.sum())
+            # the kernels' work order covers exactly the plan's bytes, sender by sender
+            for x in range(N_GPUS):
+                rows = plan.work_order(x)
+                assert np.array_equal(rows[:, :N_GPUS].sum(0), mat[x])
+            assert stt["n_atom_slots"] >= stt["n_atoms"]
             if kind == 2:
                 plan.commit()
                 O.switch(og, None, held, [O.Req(T_, g_, list(ids_), g2) for (_, T_, g_, ids_) in moving],
