@@ -105,9 +105,10 @@ struct kv_plan {
     std::vector<ReqPlan> reqs;
     std::vector<int32_t> tables;
     std::vector<Seg> segs;
-    // kernel work order (build_work_order): pieces of segments, the exclusive
-    // prefix of their slot counts, each source GPU's piece range
-    std::vector<Piece> pieces;
+    // kernel work order (build_work_order).  Piece space: each source GPU's
+    // segments, bucket after bucket; seg_begin is the exclusive prefix of
+    // their slot counts, gpu_seg_lo/hi each GPU's range of positions
+    std::vector<int32_t> seg_of;     // segment at each piece-space position
     std::vector<int64_t> seg_begin;
     std::vector<int32_t> gpu_seg_lo, gpu_seg_hi;
     std::vector<MixStream> streams;  // per source GPU: its mixed slot space
@@ -125,11 +126,11 @@ struct kv_plan {
     std::vector<A2AItem> items;
     std::vector<int32_t> item_lo, item_hi;
     std::vector<int64_t> recv_atoms;
-    // device workspace: [seg_begin | pieces | segs | tables | recs | out_off | a2a_base | items]
+    // device workspace: [seg_begin | seg_of | streams | buckets | segs | tables | recs | out_off | a2a_base | items]
     int dev = -1;
     char* dbuf = nullptr;
     size_t dbytes = 0;
-    size_t off_seg_begin = 0, off_pieces = 0, off_streams = 0, off_buckets = 0, off_segs = 0, off_tables = 0, off_recs = 0, off_outs = 0, off_a2a = 0, off_items = 0;
+    size_t off_seg_begin = 0, off_seg_of = 0, off_streams = 0, off_buckets = 0, off_segs = 0, off_tables = 0, off_recs = 0, off_outs = 0, off_a2a = 0, off_items = 0;
     cudaStream_t last_stream = nullptr;
     // kv_switch: packed all-pool tables [req_ptr | block_ids | meta] on the
     // device (plan-owned, from the cache's pool) and their host copy
@@ -603,7 +604,7 @@ static void build_a2a_layout(kv_plan* p, std::vector<Seg>& segs, const std::vect
 
 // Kernel work order of each source GPU.  The GPU's segments
 // are bucketed by destination group (order 1, the default) and laid out
-// bucket after bucket as pieces; the kernel then walks a mixed slot space of
+// bucket after bucket (piece space); the kernel then walks a mixed slot space of
 // K quanta, each quantum taking the next u_b = ceil(s_b / K) slots of every
 // bucket b (s_b its slots; slots past s_b are holes), so at every moment a
 // sender's traffic is split over its receivers in the proportions of the
@@ -619,7 +620,7 @@ static constexpr int64_t kQuantumSlots = 1024;  // target slots per quantum (4 M
 static void build_work_order(kv_plan* p, const std::vector<int64_t>& slots) {
     const int32_t n = p->c->n_gpus, H = p->c->geo.num_kv_heads;
     const std::vector<Seg>& segs = p->segs;
-    p->pieces.clear();
+    p->seg_of.clear();
     p->seg_begin.clear();
     p->streams.assign(n, MixStream{});
     p->buckets.clear();
@@ -628,7 +629,7 @@ static void build_work_order(kv_plan* p, const std::vector<int64_t>& slots) {
     int64_t acc = 0, mixed = 0;
     size_t k = 0;
     for (int32_t g = 0; g < n; ++g) {
-        p->gpu_seg_lo[g] = (int32_t)p->pieces.size();
+        p->gpu_seg_lo[g] = (int32_t)p->seg_of.size();
         const size_t lo = k;
         while (k < segs.size() && segs[k].src_gpu == g) ++k;
         const size_t hi = k;
@@ -653,7 +654,7 @@ static void build_work_order(kv_plan* p, const std::vector<int64_t>& slots) {
             MixBucket mb{};
             mb.start = acc;
             for (int32_t s : b.second) {
-                p->pieces.push_back(Piece{s, 0});
+                p->seg_of.push_back(s);
                 p->seg_begin.push_back(acc);
                 acc += slots[s];
             }
@@ -672,7 +673,7 @@ static void build_work_order(kv_plan* p, const std::vector<int64_t>& slots) {
         ms.Qs = (int32_t)std::max<int64_t>(qs, 1);
         ms.K = (int32_t)K;
         mixed += total ? K * qs : 0;
-        p->gpu_seg_hi[g] = (int32_t)p->pieces.size();
+        p->gpu_seg_hi[g] = (int32_t)p->seg_of.size();
     }
     p->seg_begin.push_back(acc);
     p->mixed_end = mixed;
@@ -686,17 +687,15 @@ static void index_segments(kv_plan* p) {
     const int32_t L = p->c->geo.num_layers;
     const std::vector<Seg>& segs = p->segs;
     std::vector<int64_t> slots(segs.size());
-    int64_t acc = 0, atoms = 0, writes = 0;
+    int64_t atoms = 0, writes = 0;
     for (size_t k = 0; k < segs.size(); ++k) {
         slots[k] = (int64_t)L * 2 * segs[k].J1 * segs[k].nh * segs[k].k1;  // incl. holes
-        acc += slots[k];
         const int64_t a = (int64_t)L * 2 * segs[k].C * segs[k].nh;         // real atoms
         atoms += a;
         writes += a * segs[k].rep1;
     }
     p->st.n_atoms = atoms;
     p->st.n_atom_writes = writes;
-    (void)acc;
     build_work_order(p, slots);
     p->st.n_atom_slots = p->mixed_end;  // kernel slots: destination-major holes + mixed-order holes
 }
@@ -730,12 +729,12 @@ static void build_remap_records(kv_plan* p, const std::vector<int32_t>& rid_off)
     p->st.n_moving = n_moving;
 }
 
-// Device workspace: [seg_begin | pieces | segs | tables | recs | out_off | a2a_base | items], 256-byte aligned.
+// Device workspace: [seg_begin | seg_of | streams | buckets | segs | tables | recs | out_off | a2a_base | items], 256-byte aligned.
 static void layout_workspace(kv_plan* p) {
     auto align = [](size_t x) { return (x + 255) & ~(size_t)255; };
     p->off_seg_begin = 0;
-    p->off_pieces = align(p->off_seg_begin + p->seg_begin.size() * sizeof(int64_t));
-    p->off_streams = align(p->off_pieces + p->pieces.size() * sizeof(Piece));
+    p->off_seg_of = align(p->off_seg_begin + p->seg_begin.size() * sizeof(int64_t));
+    p->off_streams = align(p->off_seg_of + p->seg_of.size() * sizeof(int32_t));
     p->off_buckets = align(p->off_streams + p->streams.size() * sizeof(MixStream));
     p->off_segs = align(p->off_buckets + p->buckets.size() * sizeof(MixBucket));
     p->off_tables = align(p->off_segs + p->segs.size() * sizeof(Seg));
@@ -855,7 +854,7 @@ static kv_status ensure_device(kv_plan* p, cudaStream_t stream) {
     }
     char* h = static_cast<char*>(c->stage);
     std::memcpy(h + p->off_seg_begin, p->seg_begin.data(), p->seg_begin.size() * sizeof(int64_t));
-    if (!p->pieces.empty()) std::memcpy(h + p->off_pieces, p->pieces.data(), p->pieces.size() * sizeof(Piece));
+    if (!p->seg_of.empty()) std::memcpy(h + p->off_seg_of, p->seg_of.data(), p->seg_of.size() * sizeof(int32_t));
     if (!p->streams.empty()) std::memcpy(h + p->off_streams, p->streams.data(), p->streams.size() * sizeof(MixStream));
     if (!p->buckets.empty()) std::memcpy(h + p->off_buckets, p->buckets.data(), p->buckets.size() * sizeof(MixBucket));
     if (!p->segs.empty()) std::memcpy(h + p->off_segs, p->segs.data(), p->segs.size() * sizeof(Seg));
@@ -884,14 +883,14 @@ static ReshardArgs reshard_args(const kv_plan* p, int32_t gpu) {
     const kv_cache* c = p->c;
     ReshardArgs a{};
     a.seg_begin = reinterpret_cast<const int64_t*>(p->dbuf + p->off_seg_begin);
-    a.pieces = reinterpret_cast<const Piece*>(p->dbuf + p->off_pieces);
+    a.seg_of = reinterpret_cast<const int32_t*>(p->dbuf + p->off_seg_of);
     a.streams = reinterpret_cast<const MixStream*>(p->dbuf + p->off_streams);
     a.buckets = reinterpret_cast<const MixBucket*>(p->dbuf + p->off_buckets);
     a.segs = reinterpret_cast<const Seg*>(p->dbuf + p->off_segs);
     a.tables = reinterpret_cast<const int32_t*>(p->dbuf + p->off_tables);
     a.layer_base = c->d_layer_base;
     a.seg_lo = gpu < 0 ? 0 : p->gpu_seg_lo[gpu];
-    a.seg_hi = gpu < 0 ? (int32_t)p->pieces.size() : p->gpu_seg_hi[gpu];
+    a.seg_hi = gpu < 0 ? (int32_t)p->seg_of.size() : p->gpu_seg_hi[gpu];
     const int32_t n = c->n_gpus;
     a.st_lo = gpu < 0 ? 0 : gpu;
     a.st_hi = gpu < 0 ? n : gpu + 1;
@@ -904,7 +903,7 @@ static ReshardArgs reshard_args(const kv_plan* p, int32_t gpu) {
     a.atom_bytes = (int32_t)c->atom_bytes;
     a.M = c->M;
     a.max_rep = 1;
-    for (int32_t k = a.seg_lo; k < a.seg_hi; ++k) a.max_rep = std::max(a.max_rep, p->segs[p->pieces[k].seg].rep1);
+    for (int32_t k = a.seg_lo; k < a.seg_hi; ++k) a.max_rep = std::max(a.max_rep, p->segs[p->seg_of[k]].rep1);
     return a;
 }
 
@@ -1292,12 +1291,12 @@ extern "C" kv_status kv_plan_get_stats(const kv_plan* p, kv_plan_stats* st, int6
     return KV_OK;
 }
 
-// Bytes of piece-space slots [a0, a1) of segment piece k: destination bytes
+// Bytes of slots [a0, a1) of the segment at piece-space position k: destination bytes
 // per GPU (replicas included, holes excluded) and, in column n, source reads.
 static void count_piece(const kv_plan* p, int32_t k, int64_t a0, int64_t a1, int64_t* row_out) {
     const int32_t n = p->c->n_gpus;
     const int64_t ab = p->c->atom_bytes;
-    const Seg& sg = p->segs[p->pieces[k].seg];
+    const Seg& sg = p->segs[p->seg_of[k]];
     const int64_t R = (int64_t)sg.nh * sg.k1;  // slots per (layer, K/V, destination block) row
     for (int64_t r = a0 / R; r * R < a1; ++r) {
         const int64_t j = r % sg.J1;
@@ -1318,12 +1317,12 @@ static void count_piece(const kv_plan* p, int32_t k, int64_t a0, int64_t a1, int
     }
 }
 
-// Piece-space range [b0, b1) (global) of GPU pieces [lo, hi).
+// Piece-space slot range [b0, b1) (global) within positions [lo, hi).
 static void count_piece_range(const kv_plan* p, int32_t lo, int32_t hi, int64_t b0, int64_t b1, int64_t* row_out) {
     auto it = std::upper_bound(p->seg_begin.begin() + lo, p->seg_begin.begin() + hi, b0);
     for (int32_t k = (int32_t)(it - p->seg_begin.begin()) - 1; k < hi && p->seg_begin[k] < b1; ++k) {
         const int64_t s0 = std::max(b0, p->seg_begin[k]), s1 = std::min(b1, p->seg_begin[k + 1]);
-        if (s1 > s0) count_piece(p, k, s0 - p->seg_begin[k] + p->pieces[k].slot0, s1 - p->seg_begin[k] + p->pieces[k].slot0, row_out);
+        if (s1 > s0) count_piece(p, k, s0 - p->seg_begin[k], s1 - p->seg_begin[k], row_out);
     }
 }
 

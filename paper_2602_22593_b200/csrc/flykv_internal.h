@@ -63,13 +63,6 @@ struct Seg {
 };
 static_assert(sizeof(Seg) == 64, "Seg is 64 bytes");
 
-// One work piece: slots [slot0, slot0 + n) of segment seg (n = the next
-// piece's begin minus this one's), in piece space: a source GPU's segments
-// bucket after bucket (destination groups, build_work_order).
-struct Piece {
-    int32_t seg, slot0;
-};
-
 // A source GPU's mixed slot space (the kernels' atom index):
 // K quanta of Qs slots; quantum q holds, for each bucket b, the bucket's
 // slots [q*u_b, (q+1)*u_b) at offset P_b (slots >= size_b are holes).  So a
@@ -94,8 +87,10 @@ struct ReqRec {
 };
 
 struct ReshardArgs {
-    const int64_t* seg_begin;  // [n_piece + 1] exclusive prefix of the pieces' slot counts (piece space)
-    const Piece* pieces;       // [n_piece]
+    // piece space: every source GPU's segments, bucket after bucket
+    // (destination groups, build_work_order); piece s is segment seg_of[s]
+    const int64_t* seg_begin;  // [n_seg + 1] exclusive prefix of the pieces' slot counts
+    const int32_t* seg_of;     // [n_seg]
     const MixStream* streams;  // [n_gpus] mixed slot spaces
     const MixBucket* buckets;
     int32_t st_lo, st_hi;      // source GPUs of this launch

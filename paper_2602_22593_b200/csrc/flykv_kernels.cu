@@ -75,10 +75,9 @@ __device__ __forceinline__ int64_t unmix(const ReshardArgs& a, int64_t atom) {
     return o < mb.size ? mb.start + o : -1;
 }
 
-// Slot `local` of the segment of piece s (local counts from the segment's
-// first slot: the piece's offset is already added).
+// Slot `local` of the segment at piece-space position s.
 __device__ __forceinline__ void decode(const ReshardArgs& a, int s, uint32_t local, AtomAddr& out) {
-    const Seg sg = a.segs[__ldg(&a.pieces[s].seg)];
+    const Seg sg = a.segs[__ldg(a.seg_of + s)];
     const uint32_t nh = (uint32_t)sg.nh, k1 = (uint32_t)sg.k1, J1 = (uint32_t)sg.J1;
     const uint32_t w = local % k1;        // (((l*2 + kv)*J1 + j)*nh + hh)*k1 + w
     local /= k1;
@@ -178,7 +177,7 @@ __device__ __forceinline__ void lane_decode(const ReshardArgs& a, int64_t slot, 
         return;
     }
     const int s = find_seg(a.seg_begin, a.seg_lo, a.seg_hi, atom);
-    const uint32_t local = (uint32_t)(atom - __ldg(a.seg_begin + s)) + (uint32_t)__ldg(&a.pieces[s].slot0);
+    const uint32_t local = (uint32_t)(atom - __ldg(a.seg_begin + s));
     AtomAddr ad;
     decode(a, s, local, ad);
     la.patom = (uint32_t)atom;
@@ -206,7 +205,7 @@ __device__ __forceinline__ T shfl_ptr(T p, int k) {
 __device__ __forceinline__ char* replica_ptr(const ReshardArgs& a, uint32_t patom, int j) {
     const int s = find_seg(a.seg_begin, a.seg_lo, a.seg_hi, (int64_t)patom);
     AtomAddr ad;
-    decode(a, s, (uint32_t)(patom - __ldg(a.seg_begin + s)) + (uint32_t)__ldg(&a.pieces[s].slot0), ad);
+    decode(a, s, (uint32_t)(patom - __ldg(a.seg_begin + s)), ad);
     return dst_ptr(a, ad, j);
 }
 
