@@ -899,6 +899,7 @@ static ReshardArgs reshard_args(const kv_plan* p, int32_t gpu) {
     if (gpu < 0) {  // the first GPU with work (the stream search needs streams[st_lo].begin <= slot)
         while (a.st_lo + 1 < n && p->streams[a.st_lo + 1].begin == a.atom_lo) ++a.st_lo;
     }
+    for (int32_t g = a.st_lo; g < a.st_hi; ++g) a.mixed |= p->streams[g].nb > 1 ? 1 : 0;
     a.L = c->geo.num_layers;
     a.atom_bytes = (int32_t)c->atom_bytes;
     a.M = c->M;

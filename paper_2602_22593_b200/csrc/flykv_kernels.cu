@@ -59,6 +59,7 @@ __device__ __forceinline__ int find_seg(const int64_t* __restrict__ seg_begin, i
 // Mixed slot (the kernels' atom index) -> piece-space slot, or -1 for a hole
 // (MixStream, flykv_internal.h).
 __device__ __forceinline__ int64_t unmix(const ReshardArgs& a, int64_t atom) {
+    if (!a.mixed) return atom;       // plan order: the two index spaces coincide
     int lo = a.st_lo, hi = a.st_hi;  // streams[lo].begin <= atom
     while (hi - lo > 1) {
         const int mid = (lo + hi) >> 1;
