@@ -94,7 +94,8 @@ struct ReshardArgs {
     const MixStream* streams;  // [n_gpus] mixed slot spaces
     const MixBucket* buckets;
     int32_t st_lo, st_hi;      // source GPUs of this launch
-    int32_t mixed;             // 0: every launched stream is one bucket, K = 1 (mixed slot == piece-space slot)
+    int32_t mixed;             // 0: every launched stream is one bucket, K = 1 (mixed slot == piece-space
+                               // slot, seg_of is the identity over the launched positions)
     const Seg* segs;           // [n_seg]
     const int32_t* tables;     // source + destination tables
     char* const* layer_base;   // [n_gpus * L] pool layer pointers

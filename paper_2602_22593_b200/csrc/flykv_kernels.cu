@@ -57,9 +57,13 @@ __device__ __forceinline__ int find_seg(const int64_t* __restrict__ seg_begin, i
 }
 
 // Mixed slot (the kernels' atom index) -> piece-space slot, or -1 for a hole
-// (MixStream, flykv_internal.h).
+// (MixStream, flykv_internal.h).  MIX = false (launches whose streams are all
+// single buckets, a.mixed == 0): the two index spaces coincide and none of
+// this is compiled into the kernel.
+template <bool MIX>
 __device__ __forceinline__ int64_t unmix(const ReshardArgs& a, int64_t atom) {
-    if (!a.mixed) return atom;       // plan order: the two index spaces coincide
+    if constexpr (!MIX) return atom;
+    if (!a.mixed) return atom;
     int lo = a.st_lo, hi = a.st_hi;  // streams[lo].begin <= atom
     while (hi - lo > 1) {
         const int mid = (lo + hi) >> 1;
@@ -77,8 +81,9 @@ __device__ __forceinline__ int64_t unmix(const ReshardArgs& a, int64_t atom) {
 }
 
 // Slot `local` of the segment at piece-space position s.
+template <bool MIX>
 __device__ __forceinline__ void decode(const ReshardArgs& a, int s, uint32_t local, AtomAddr& out) {
-    const Seg sg = a.segs[__ldg(a.seg_of + s)];
+    const Seg sg = a.segs[MIX && a.mixed ? __ldg(a.seg_of + s) : s];  // plan order: seg_of is the identity
     const uint32_t nh = (uint32_t)sg.nh, k1 = (uint32_t)sg.k1, J1 = (uint32_t)sg.J1;
     const uint32_t w = local % k1;        // (((l*2 + kv)*J1 + j)*nh + hh)*k1 + w
     local /= k1;
@@ -166,11 +171,11 @@ struct LaneAtom {
     const char* src;
     char* dst0;
     int32_t rep1;
-    uint32_t patom;   // piece-space slot of the atom (< 2^32, host-checked): replicas > 0 re-decode from it
 };
 
+template <bool MIX>
 __device__ __forceinline__ void lane_decode(const ReshardArgs& a, int64_t slot, LaneAtom& la) {
-    const int64_t atom = unmix(a, slot);
+    const int64_t atom = unmix<MIX>(a, slot);
     if (atom < 0) {  // hole of the mixed order
         la.src = nullptr;
         la.dst0 = nullptr;
@@ -180,8 +185,7 @@ __device__ __forceinline__ void lane_decode(const ReshardArgs& a, int64_t slot, 
     const int s = find_seg(a.seg_begin, a.seg_lo, a.seg_hi, atom);
     const uint32_t local = (uint32_t)(atom - __ldg(a.seg_begin + s));
     AtomAddr ad;
-    decode(a, s, local, ad);
-    la.patom = (uint32_t)atom;
+    decode<MIX>(a, s, local, ad);
     la.src = ad.src;
     la.rep1 = ad.rep1;  // 0 for a hole: nothing is read or written
     la.dst0 = ad.src ? dst_ptr(a, ad, 0) : nullptr;
@@ -201,12 +205,14 @@ __device__ __forceinline__ T shfl_ptr(T p, int k) {
     return reinterpret_cast<T>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(p), k));
 }
 
-// Destination of replica j of the atom at piece-space slot patom
-// (warp-uniform re-decode, GQA replication only).
-__device__ __forceinline__ char* replica_ptr(const ReshardArgs& a, uint32_t patom, int j) {
-    const int s = find_seg(a.seg_begin, a.seg_lo, a.seg_hi, (int64_t)patom);
+// Destination of replica j of the atom at kernel slot `slot` (warp-uniform
+// re-decode, GQA replication only; nothing extra is kept live per atom).
+template <bool MIX>
+__device__ __forceinline__ char* replica_ptr(const ReshardArgs& a, int64_t slot, int j) {
+    const int64_t atom = unmix<MIX>(a, slot);
+    const int s = find_seg(a.seg_begin, a.seg_lo, a.seg_hi, atom);
     AtomAddr ad;
-    decode(a, s, (uint32_t)(patom - __ldg(a.seg_begin + s)), ad);
+    decode<MIX>(a, s, (uint32_t)(atom - __ldg(a.seg_begin + s)), ad);
     return dst_ptr(a, ad, j);
 }
 
@@ -225,7 +231,7 @@ __device__ __forceinline__ int round_len(const ReshardArgs& a, int64_t R, int64_
     return span < 32 ? (int)span : 32;
 }
 
-template <int VPL, int U>
+template <int VPL, int U, bool MIX>
 __global__ void __launch_bounds__(256, 2) flykv_reshard_kernel(const ReshardArgs a) {
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -241,7 +247,7 @@ __global__ void __launch_bounds__(256, 2) flykv_reshard_kernel(const ReshardArgs
         int64_t R = a.atom_lo;
         int n = round_len(a, R, warp, nwarps);
         LaneAtom la;
-        if (lane < n) lane_decode(a, R + warp + lane * nwarps, la);
+        if (lane < n) lane_decode<MIX>(a, R + warp + lane * nwarps, la);
         while (n > 0) {
             const int64_t first = R + warp;
             const int64_t Rn = R + 32 * nwarps;
@@ -252,14 +258,12 @@ __global__ void __launch_bounds__(256, 2) flykv_reshard_kernel(const ReshardArgs
                 const char* s[U];
                 char* d0[U];
                 int rep[U];
-                uint32_t pa[U];
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     const int k = (k0 + u < n) ? k0 + u : k0;
                     s[u] = shfl_ptr(la.src, k);
                     d0[u] = shfl_ptr(la.dst0, k);
                     rep[u] = (k0 + u < n) ? __shfl_sync(0xffffffffu, la.rep1, k) : 0;
-                    pa[u] = __shfl_sync(0xffffffffu, la.patom, k);
                 }
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
@@ -268,7 +272,7 @@ __global__ void __launch_bounds__(256, 2) flykv_reshard_kernel(const ReshardArgs
 #pragma unroll
                     for (int i = 0; i < VPL; ++i) v[u][i] = ld_stream(src + i * 32);
                 }
-                if (k0 == 0 && lane < nn) lane_decode(a, Rn + warp + lane * nwarps, nx);
+                if (k0 == 0 && lane < nn) lane_decode<MIX>(a, Rn + warp + lane * nwarps, nx);
                 // GQA replicas (p > H): lane j decodes replica j's pointer, all
                 // replicas of an atom in one parallel pass while its loads are
                 // in flight; the stores receive them by shuffle
@@ -278,12 +282,12 @@ __global__ void __launch_bounds__(256, 2) flykv_reshard_kernel(const ReshardArgs
                 for (int u = 0; u < U; ++u) {
                     rp[u] = nullptr;
                     if (par && rep[u] > 1 && lane > 0 && lane < rep[u])
-                        rp[u] = replica_ptr(a, pa[u], lane);
+                        rp[u] = replica_ptr<MIX>(a, first + (int64_t)(k0 + u) * nwarps, lane);
                 }
                 auto dst_of = [&](int u, int j) -> int4* {
                     char* dj = j == 0             ? d0[u]
                                : (par && j < 32) ? shfl_ptr(rp[u], j)
-                                                 : replica_ptr(a, pa[u], j);
+                                                 : replica_ptr<MIX>(a, first + (int64_t)(k0 + u) * nwarps, j);
                     return reinterpret_cast<int4*>(dj) + lane;
                 };
                 if (a.rep_flags & 2) {  // replica-major: replica j of all U atoms, then j + 1
@@ -320,13 +324,12 @@ __global__ void __launch_bounds__(256, 2) flykv_reshard_kernel(const ReshardArgs
             const int n = round_len(a, R, warp, nwarps);
             if (n == 0) break;
             LaneAtom la;
-            if (lane < n) lane_decode(a, first + lane * nwarps, la);
+            if (lane < n) lane_decode<MIX>(a, first + lane * nwarps, la);
             if constexpr (VPL > 0) {
                 for (int k = 0; k < n; ++k) {
                     const int4* src = reinterpret_cast<const int4*>(shfl_ptr(la.src, k)) + lane;
                     int4* dst = reinterpret_cast<int4*>(shfl_ptr(la.dst0, k)) + lane;
                     const int rep = __shfl_sync(0xffffffffu, la.rep1, k);
-                    const uint32_t pa = __shfl_sync(0xffffffffu, la.patom, k);
                     if (rep == 0) continue;  // hole (warp-uniform)
                     int4 v[VPL];
 #pragma unroll
@@ -334,7 +337,7 @@ __global__ void __launch_bounds__(256, 2) flykv_reshard_kernel(const ReshardArgs
 #pragma unroll
                     for (int i = 0; i < VPL; ++i) st_stream(dst + i * 32, v[i]);
                     for (int j = 1; j < rep; ++j) {
-                        int4* dj = reinterpret_cast<int4*>(replica_ptr(a, pa, j)) + lane;
+                        int4* dj = reinterpret_cast<int4*>(replica_ptr<MIX>(a, first + k * nwarps, j)) + lane;
 #pragma unroll
                         for (int i = 0; i < VPL; ++i) st_stream(dj + i * 32, v[i]);
                     }
@@ -344,10 +347,9 @@ __global__ void __launch_bounds__(256, 2) flykv_reshard_kernel(const ReshardArgs
                     const char* s = shfl_ptr(la.src, k);
                     char* d0 = shfl_ptr(la.dst0, k);
                     const int rep = __shfl_sync(0xffffffffu, la.rep1, k);
-                    const uint32_t pa = __shfl_sync(0xffffffffu, la.patom, k);
                     const int nv = a.atom_bytes >> 4;
                     for (int j = 0; j < rep; ++j) {
-                        char* dj = j == 0 ? d0 : replica_ptr(a, pa, j);
+                        char* dj = j == 0 ? d0 : replica_ptr<MIX>(a, first + k * nwarps, j);
                         for (int i = lane; i < nv; i += 32)
                             st_stream(reinterpret_cast<int4*>(dj) + i, ld_stream(reinterpret_cast<const int4*>(s) + i));
                     }
@@ -504,7 +506,7 @@ __global__ void __launch_bounds__(W * 32) flykv_reshard_tma_kernel(const Reshard
     // per-stage pending store: replica-0 destination, replica count, atom index (lane 0 only)
     __shared__ char* pend_dst[W][S];
     __shared__ int32_t pend_rep[W][S];
-    __shared__ uint32_t pend_atom[W][S];
+    __shared__ int64_t pend_atom[W][S];
     if (lane == 0) {
         for (int i = 0; i < S; ++i)
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bars + i)));
@@ -524,7 +526,7 @@ __global__ void __launch_bounds__(W * 32) flykv_reshard_tma_kernel(const Reshard
         const uint32_t src = smem_u32(ring + (size_t)st * stage_bytes);
         const int rep = pend_rep[wid][st];
         for (int r = 0; r < rep; ++r) {
-            char* dst = r == 0 ? pend_dst[wid][st] : replica_ptr(a, pend_atom[wid][st], r);
+            char* dst = r == 0 ? pend_dst[wid][st] : replica_ptr<true>(a, pend_atom[wid][st], r);
             asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(dst),
                          "r"(src), "r"(bytes), "l"(policy)
                          : "memory");
@@ -537,12 +539,11 @@ __global__ void __launch_bounds__(W * 32) flykv_reshard_tma_kernel(const Reshard
         const int n = round_len(a, R, warp, nwarps);
         if (n == 0) break;
         LaneAtom la;
-        if (lane < n) lane_decode(a, R + warp + lane * nwarps, la);
+        if (lane < n) lane_decode<true>(a, R + warp + lane * nwarps, la);
         for (int k = 0; k < n; ++k) {
             const char* s = shfl_ptr(la.src, k);
             char* d0 = shfl_ptr(la.dst0, k);
             const int rep = __shfl_sync(0xffffffffu, la.rep1, k);
-            const uint32_t pa = __shfl_sync(0xffffffffu, la.patom, k);
             if (rep == 0) continue;  // hole (warp-uniform)
             if (lane == 0) {
                 if (issued >= (uint32_t)D) store_one(stored++);
@@ -553,7 +554,7 @@ __global__ void __launch_bounds__(W * 32) flykv_reshard_tma_kernel(const Reshard
                 asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(S - D) : "memory");
                 pend_dst[wid][st] = d0;
                 pend_rep[wid][st] = rep;
-                pend_atom[wid][st] = pa;  // replicas re-decode from the piece-space slot
+                pend_atom[wid][st] = R + warp + (int64_t)k * nwarps;
                 const uint32_t bar = smem_u32(bars + st);
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
                              : "memory");
@@ -620,7 +621,7 @@ static cudaError_t launch_ldg(const ReshardArgs& a_in, int device, cudaStream_t 
     static int per_sm = 0;
     if (per_sm == 0) {
         int nb = 0;
-        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, flykv_reshard_kernel<VPL, U>, 256, 0);
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, flykv_reshard_kernel<VPL, U, false>, 256, 0);
         if (e != cudaSuccess) return e;
         per_sm = nb > 0 ? nb : 1;
     }
@@ -645,7 +646,8 @@ static cudaError_t launch_ldg(const ReshardArgs& a_in, int device, cudaStream_t 
     int64_t cap = (int64_t)sm_count_of(device) * per;
     int grid = (int)(want < cap ? want : cap);
     if (grid < 1) grid = 1;
-    flykv_reshard_kernel<VPL, U><<<grid, threads, 0, s>>>(a);
+    if (a.mixed) flykv_reshard_kernel<VPL, U, true><<<grid, threads, 0, s>>>(a);
+    else flykv_reshard_kernel<VPL, U, false><<<grid, threads, 0, s>>>(a);
     return cudaGetLastError();
 }
 
