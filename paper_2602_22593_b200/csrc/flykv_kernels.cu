@@ -464,7 +464,7 @@ cudaError_t launch_unpack(const UnpackArgs& a, int device, cudaStream_t s) {
     }
     const int per = shape == 0 ? 1 : shape == 3 ? 4 : 2;
     const bool u2 = shape == 0 || shape == 2;
-    const int64_t want = (a.n_atoms + 6 * 32 - 1) / (6 * 32);
+    const int64_t want = (a.n_atoms + 6 - 1) / 6;  // small transfers: every warp, few atoms each
     const int64_t cap = (int64_t)sm_count_of(device) * per;
     const int grid = (int)(want < cap ? (want > 0 ? want : 1) : cap);
     if (a.atom_bytes == 4096 && u2) flykv_unpack_kernel<8, 2><<<grid, 192, 0, s>>>(a);
@@ -642,7 +642,11 @@ static cudaError_t launch_ldg(const ReshardArgs& a_in, int device, cudaStream_t 
     }
     const int per = g_ctas_per_sm > 0 ? g_ctas_per_sm : (per_sm < want_per ? per_sm : want_per);
     const int threads = g_threads > 0 ? g_threads : want_threads;
-    int64_t want = (atoms + (threads / 32) * 32 - 1) / ((threads / 32) * 32);
+    // small plans: spread the atoms over every warp the grid can hold (one
+    // or a few atoms per warp) rather than 32 per warp on fewer CTAs -- a
+    // warp walks its atoms one after another, so latency, not bandwidth,
+    // bounds a switch of a few MB (the tiny config's 4 MiB took 27 us)
+    int64_t want = (atoms + (threads / 32) - 1) / (threads / 32);
     int64_t cap = (int64_t)sm_count_of(device) * per;
     int grid = (int)(want < cap ? want : cap);
     if (grid < 1) grid = 1;
@@ -668,7 +672,7 @@ static cudaError_t launch_tma(const ReshardArgs& a, int device, cudaStream_t s, 
     if (e != cudaSuccess) return e;
     if (per <= 0 || per > nb) per = nb > 0 ? nb : 1;
     const int64_t atoms = a.atom_hi - a.atom_lo;
-    int64_t want = (atoms + W * 32 - 1) / (W * 32);
+    int64_t want = (atoms + W - 1) / W;  // small plans: every warp, few atoms each
     int64_t cap = (int64_t)sm_count_of(device) * per;
     int grid = (int)(want < cap ? want : cap);
     if (grid < 1) grid = 1;
