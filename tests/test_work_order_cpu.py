@@ -118,3 +118,33 @@ def test_link_model_closed_forms():
     assert bench.ordered_link_model(rot, hbm, link) == pytest.approx(t_min)
     assert bench.ordered_link_model(mix, hbm, link) == pytest.approx(t_min)
     assert bench.ordered_link_model(same, hbm, link) > 1.5 * t_min   # the ingress hot-spot costs
+
+
+def test_link_model_never_beats_t_min():
+    """Any visiting order takes at least t_min: t_min is a
+    lower bound, the ordered model a schedule.  Random byte rows, random
+    orders, 2-8 GPUs; one row per GPU (perfect mixing) with no HBM limit in
+    play reaches the link bound exactly when every sender is link-bound."""
+    rng = np.random.default_rng(5)
+    hbm, link = 8000.0, 800.0
+    for trial in range(40):
+        n = int(rng.integers(2, 9))
+        pieces = []
+        mat = np.zeros((n, n))
+        for g in range(n):
+            k = int(rng.integers(1, 6))
+            rows = np.zeros((k, n + 1))
+            for r in range(k):
+                dests = rng.choice(n, size=int(rng.integers(1, n + 1)), replace=False)
+                rows[r, dests] = rng.integers(1, 50, size=dests.size) * 1e8
+                rows[r, n] = rows[r, :n].sum()
+            pieces.append(rows)
+            mat[g] = rows[:, :n].sum(0)
+        t_min = bench.nvlink_roofline(mat, hbm, link)[0]
+        t = bench.ordered_link_model(pieces, hbm, link)
+        assert t >= t_min * (1 - 1e-9), (trial, t, t_min)
+    # all-to-all of equal bytes, one mixed row per sender: exactly the egress bound
+    n, b = 4, 1e9
+    rows = [np.array([[b if d != g else 0.0 for d in range(n)] + [b * (n - 1)]]) for g in range(n)]
+    mat = np.array([r[0, :n] for r in rows])
+    assert bench.ordered_link_model(rows, hbm, link) == pytest.approx(bench.nvlink_roofline(mat, hbm, link)[0])
