@@ -463,8 +463,9 @@ def run_single(args):
         return agg, host
 
     def step_switch():
-        """One whole switch through kv_switch (one C call per wave: plan,
-        upload, reshard, remap, one table read-back, sync).  A single-wave
+        """One whole switch through kv_switch (plan, upload, reshard, remap,
+        one table read-back, sync), or kv_switch_multi for several waves (one
+        C call, one sync).  A single-wave
         switch that reverses the previous one is kv_switch_back: the inverse
         request list is built inside the library, nothing is marshalled.
         Returns (aggregated stats, device->host bytes)."""
@@ -476,7 +477,10 @@ def run_single(args):
             settle_switches()
             reqs = state["reqs"]
             ws = waves_of(reqs)
-            plans_ = [F.kv_switch(eng.cache, sub, stream) for sub, _ in ws]
+            # every wave in one C call, no host sync between waves (kv_switch_multi)
+            multi = len(ws) > 1 and os.environ.get("FLYKV_MULTI_WAVE", "1") == "1"   # 0: kv_switch per wave (A/B)
+            plans_ = (F.kv_switch_multi(eng.cache, [sub for sub, _ in ws], stream) if multi
+                      else [F.kv_switch(eng.cache, sub, stream) for sub, _ in ws])
             state["chain"] = [(reqs, ws, plans_)]
         agg, d2h_b = None, 0
         for plan in plans_:
@@ -592,7 +596,8 @@ def run_single(args):
                    "host_plan_ms_p50": round(statistics.median(plan_ms), 3),
                    "api": ("KVSwitchEngine.switch(read_back=True)" if DEBUG else
                            "flykv.kv_switch / kv_switch_back: one C-ABI call per switch (plan, upload, "
-                           "reshard, remap, one table read-back, sync)")}
+                           "reshard, remap, one table read-back, sync); several waves: kv_switch_multi, one call "
+                           "and one sync for all waves")}
 
     # per-step statistics: directions alternate, and under GQA replication the
     # two directions move different byte counts (TP>H writes p/H replicas)

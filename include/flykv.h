@@ -305,6 +305,22 @@ kv_status kv_switch(kv_cache* cache, const kv_request* reqs, int32_t n_reqs, voi
  * committed; INVALID_ARG if prev belongs to another cache. */
 kv_status kv_switch_back(kv_cache* cache, const kv_plan* prev, void* stream, kv_plan** out);
 
+/* kv_switch_multi: a switch in waves (kv_plan_waves, or the block-aligned
+ * pieces of kv_plan_pieces turned into plain requests) with no host sync
+ * between the waves: each wave is planned once the previous one committed
+ * on the host, its kernels are stream-ordered after the previous wave's
+ * (blocks a wave read may be the next wave's destinations), and the tables
+ * of every wave are read back after one stream sync at the end.
+ *   reqs      host, every wave's requests back to back
+ *   wave_ptr  host [n_waves + 1], wave w = reqs[wave_ptr[w] .. wave_ptr[w+1])
+ *   plans     host [n_waves] out: one committed plan per wave, tables as for
+ *             kv_switch (kv_plan_tables); entries stay NULL past a failure,
+ *             the caller destroys the non-NULL ones.
+ * Errors: as kv_plan_switch / kv_switch for the failing wave (the earlier
+ * waves have committed and completed). */
+kv_status kv_switch_multi(kv_cache* cache, const kv_request* reqs, const int32_t* wave_ptr, int32_t n_waves,
+                          void* stream, kv_plan** plans);
+
 /* kv_plan_tables: pool gpu's post-switch table of a plan run by kv_switch,
  * as pointers into plan-owned memory (valid until kv_plan_destroy):
  * on_device != 0 -> device pointers, else host pointers.  Layout as written

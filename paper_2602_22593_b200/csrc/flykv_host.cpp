@@ -1362,13 +1362,15 @@ extern "C" void kv_plan_destroy(kv_plan* p) {
     delete p;
 }
 
-extern "C" kv_status kv_switch(kv_cache* c, const kv_request* reqs, int32_t n_reqs, void* stream_, kv_plan** out) {
-    if (!out) return fail(KV_ERR_INVALID_ARG, "out is NULL");
+// kv_switch without its read-back: plan, upload, reshard, all-pool remap into
+// plan-owned device tables (the remap commits the plan on the host).  *out
+// is set when the plan exists past planning (the caller destroys it).
+static kv_status switch_enqueue(kv_cache* c, const kv_request* reqs, int32_t n_reqs, cudaStream_t stream,
+                                kv_plan** out) {
     *out = nullptr;
     kv_plan* p = nullptr;
     kv_status s = kv_plan_switch(c, reqs, n_reqs, &p);
     if (s) return s;
-    cudaStream_t stream = static_cast<cudaStream_t>(stream_);
     int32_t tot_res = 0, tot_ids = 0;
     kv_plan_resident(p, -1, &tot_res, &tot_ids);
     const int32_t n = c->n_gpus;
@@ -1388,27 +1390,64 @@ extern "C" kv_status kv_switch(kv_cache* c, const kv_request* reqs, int32_t n_re
     if (s) return abort_plan(s);
     // a5 is stream order here: every pool is addressable from this device
     s = kv_remap_block_tables(p, -1, p->d_out, p->d_out + p->out_rp, p->d_out + p->out_ids, stream);
-    if (s) {  // the plan committed inside the remap call only if it got that far
-        *out = p;
-        return s;
-    }
+    *out = p;  // the plan committed inside the remap call only if it got that far
+    return s;
+}
+
+// One device->host copy of a plan's packed tables (through the cache's
+// pinned buffer), then a stream sync.
+static kv_status switch_read_back(kv_plan* p, cudaStream_t stream) {
+    kv_cache* c = p->c;
+    const int64_t elems = p->out_ids + 4 * (int64_t)(p->out_rp - c->n_gpus);
+    cudaError_t e;
     if ((size_t)elems * 4 > c->back_bytes) {
         if (c->back) cudaFreeHost(c->back);
         c->back = nullptr;
         c->back_bytes = 0;
         const size_t want = std::max((size_t)elems * 4, (size_t)1 << 20);
         e = cudaMallocHost(&c->back, want);
-        if (e != cudaSuccess) {
-            *out = p;
-            return cuda_fail(e, "cudaMallocHost (tables)");
-        }
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMallocHost (tables)");
         c->back_bytes = want;
     }
     e = cudaMemcpyAsync(c->back, p->d_out, (size_t)elems * 4, cudaMemcpyDeviceToHost, stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
-    *out = p;
     if (e != cudaSuccess) return cuda_fail(e, "kv_switch table read-back");
     p->h_out.assign(static_cast<int32_t*>(c->back), static_cast<int32_t*>(c->back) + elems);
+    return KV_OK;
+}
+
+extern "C" kv_status kv_switch(kv_cache* c, const kv_request* reqs, int32_t n_reqs, void* stream_, kv_plan** out) {
+    if (!out) return fail(KV_ERR_INVALID_ARG, "out is NULL");
+    cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+    kv_status s = switch_enqueue(c, reqs, n_reqs, stream, out);
+    if (s) return s;
+    return switch_read_back(*out, stream);
+}
+
+extern "C" kv_status kv_switch_multi(kv_cache* c, const kv_request* reqs, const int32_t* wave_ptr, int32_t n_waves,
+                                     void* stream_, kv_plan** plans) {
+    if (!c || !wave_ptr || !plans || n_waves < 0 || (n_waves > 0 && wave_ptr[n_waves] > 0 && !reqs))
+        return fail(KV_ERR_INVALID_ARG, "bad kv_switch_multi arguments");
+    for (int32_t w = 0; w < n_waves; ++w) {
+        plans[w] = nullptr;
+        if (wave_ptr[w + 1] < wave_ptr[w] || wave_ptr[0] != 0)
+            return fail(KV_ERR_INVALID_ARG, "wave_ptr must be a non-decreasing prefix starting at 0");
+    }
+    cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+    // every wave is planned after the previous one committed (host state), and
+    // its kernels are stream-ordered after the previous wave's: a block the
+    // previous wave read as a source may be this wave's destination
+    for (int32_t w = 0; w < n_waves; ++w) {
+        kv_status s = switch_enqueue(c, reqs + wave_ptr[w], wave_ptr[w + 1] - wave_ptr[w], stream, &plans[w]);
+        if (s) {
+            cudaStreamSynchronize(stream);
+            return s;
+        }
+    }
+    for (int32_t w = 0; w < n_waves; ++w) {
+        kv_status s = switch_read_back(plans[w], stream);
+        if (s) return s;
+    }
     return KV_OK;
 }
 

@@ -151,19 +151,18 @@ class KVSwitchEngine:
         """Memory-bounded switch that may move a request in block-aligned token
         pieces across waves (kv_plan_pieces, R20): the promotion of one long
         request whose source and destination do not fit side by side.  Each
-        wave is one kv_switch (commit releases its pieces' sources before the
-        next wave allocates).  Returns (final destination table of every
-        request = concatenation of its pieces' tables, the wave plans)."""
+        wave commits (releasing its pieces' sources) before the next wave is
+        planned; the kernels of consecutive waves are stream-ordered.  Returns (final destination table of every
+        request = concatenation of its pieces' tables, the wave plans).  The
+        waves run back to back in one kv_switch_multi call."""
         requests = list(requests)
         waves = flykv.kv_plan_pieces(self.cache, requests, max_wave_bytes)
         parts = [[] for _ in requests]
-        plans = []
-        for wave in waves:
-            sub = [flykv.piece_request(self.geom, requests[i], t0, t1) for i, t0, t1 in wave]
-            plan = flykv.kv_switch(self.cache, sub, self.stream)
+        subs = [[flykv.piece_request(self.geom, requests[i], t0, t1) for i, t0, t1 in wave] for wave in waves]
+        plans = flykv.kv_switch_multi(self.cache, subs, self.stream)   # all waves, one sync
+        for wave, plan in zip(waves, plans):
             for (i, _, _), tab in zip(wave, plan.dst_tables()):
                 parts[i].append(tab)
-            plans.append(plan)
         tables = [np.concatenate(p).astype(np.int32) if p else np.zeros(0, dtype=np.int32) for p in parts]
         return tables, plans
 

@@ -124,6 +124,7 @@ _sig("kv_remap_block_tables", C.c_int, _P, C.c_int32, _P, _P, _P, _P)
 _sig("kv_switch", C.c_int, _P, C.POINTER(Request), C.c_int32, _P, C.POINTER(_P))
 _sig("kv_plan_tables", C.c_int, _P, C.c_int32, C.c_int32, C.POINTER(_I32P), C.POINTER(_I32P), C.POINTER(_I32P))
 _sig("kv_switch_back", C.c_int, _P, _P, _P, C.POINTER(_P))
+_sig("kv_switch_multi", C.c_int, _P, C.POINTER(Request), _I32P, C.c_int32, _P, C.POINTER(_P))
 _sig("kv_pack", C.c_int, _P, C.c_int32, _P, _I64P, _P)
 _sig("kv_unpack", C.c_int, _P, C.c_int32, _P, _I64P, _P)
 _sig("kv_plan_dst_tables", C.c_int, _P, _I32P, _I32P)
@@ -161,7 +162,7 @@ _sig("kv_plan_work_order", C.c_int, _P, C.c_int32, _I32P, _I64P)
 
 EXPORTED = ["kv_cache_create", "kv_cache_destroy", "kv_layout", "kv_blocks_for", "kv_alloc", "kv_reserve",
             "kv_free", "kv_free_count", "kv_held_mask", "kv_plan_switch", "kv_plan_upload", "kv_reshard", "kv_reshard_staged",
-            "kv_pack", "kv_unpack", "kv_switch", "kv_switch_back", "kv_plan_tables", "kv_plan_resident",
+            "kv_pack", "kv_unpack", "kv_switch", "kv_switch_back", "kv_switch_multi", "kv_plan_tables", "kv_plan_resident",
             "kv_remap_block_tables", "kv_plan_dst_tables", "kv_plan_commit", "kv_plan_waves", "kv_plan_pieces",
             "kv_suggest_rank_ids", "kv_plan_get_stats", "kv_plan_destroy",
             "weight_shard_view", "kv_gather_view", "kv_vmm_granularity", "kv_vmm_alloc", "kv_vmm_free",
@@ -453,6 +454,26 @@ def kv_switch(cache: KVCache, requests, stream=None) -> Plan:
             plan.destroy()
         raise FlyKVError(st, msg)
     return plan
+
+
+def kv_switch_multi(cache: KVCache, waves, stream=None) -> list:
+    """A switch in waves in one C call (kv_switch_multi): waves is a list of
+    request lists (kv_plan_waves slices, or kv_plan_pieces waves through
+    piece_request); no host sync between waves.  Returns one Plan per wave."""
+    waves = [list(w) for w in waves]
+    ra = make_requests([r for w in waves for r in w])
+    ptr = np.zeros(len(waves) + 1, dtype=np.int32)
+    np.cumsum([len(w) for w in waves], out=ptr[1:])
+    hs = (C.c_void_p * max(len(waves), 1))()
+    st = _lib.kv_switch_multi(cache._h, ra.ptr, ptr.ctypes.data_as(_I32P), len(waves), stream_of(stream), hs)
+    plans = [Plan(cache, C.c_void_p(hs[k]), len(w)) if hs[k] else None for k, w in enumerate(waves)]
+    if st != KV_OK:
+        msg = _lib.kv_last_error().decode()
+        for p in plans:
+            if p is not None:
+                p.destroy()
+        raise FlyKVError(st, msg)
+    return plans
 
 
 def kv_switch_back(cache: KVCache, prev: Plan, stream=None) -> Plan:

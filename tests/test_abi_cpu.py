@@ -419,6 +419,20 @@ def test_kv_switch_errors_before_the_device():
     assert e.value.name == "KV_ERR_BAD_STATE"
 
 
+def test_kv_switch_multi_errors_before_the_device():
+    """kv_switch_multi: no waves is a no-op; a wave that does not fit fails in
+    its planning with no state change and no plan returned -- before any
+    device work."""
+    c = fake_cache((1, 4, 8, 4, 2), [8, 8])
+    assert F.kv_switch_multi(c, []) == []
+    a = c.alloc((0, 1), 6)
+    before = [c.held_mask(g).copy() for g in (0, 1)]
+    with pytest.raises(F.FlyKVError) as e:
+        F.kv_switch_multi(c, [[(1, 24, (0, 1), a, (0, 2))]])
+    assert e.value.name == "KV_ERR_OUT_OF_BLOCKS"
+    assert all(np.array_equal(c.held_mask(g), before[g]) for g in (0, 1))
+
+
 def _run_pieces_against_oracle(c, og, held, reqs, waves, n_gpus):
     """Execute kv_plan_pieces' waves on the product (plan + commit per wave,
     fake pointers) and on the oracle's allocator with the same piece

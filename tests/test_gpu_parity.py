@@ -393,9 +393,11 @@ def test_reshard_variants(impl, H, p0, p1, d, a2a):
         F.set_reshard_impl(0, 0)
 
 
-def test_memory_bounded_waves_gpu():
+@pytest.mark.parametrize("one_call", [False, True])
+def test_memory_bounded_waves_gpu(one_call):
     """SURVEY 8(f) N1 on the device: a promotion that does not fit in one
-    shot runs in waves (kv_plan_waves -> switch per wave); whole pools equal
+    shot runs in waves (kv_plan_waves -> switch per wave, or every wave in
+    one kv_switch_multi call with no sync between waves); whole pools equal
     the oracle applied wave after wave."""
     F = _F()
     from paper_2602_22593_b200.engine import KVSwitchEngine
@@ -419,9 +421,19 @@ def test_memory_bounded_waves_gpu():
         eng.plan(reqs)
     waves = F.kv_plan_waves(eng.cache, reqs)
     assert len(waves) > 1
-    out = eng.switch_waves(reqs, read_back=True)
+    if one_call:
+        out = [(p, None, None) for p in F.kv_switch_multi(eng.cache, [reqs[a:b] for a, b in waves], eng.stream)]
+        torch.cuda.synchronize()
+    else:
+        out = eng.switch_waves(reqs, read_back=True)
     assert len(out) == len(waves)
     for (a, b), (plan, tables, hb) in zip(waves, out):
+        if one_call:  # the tables kv_switch_multi read back equal the plan's
+            for gpu in range(len(nb)):
+                rp, ids_, meta = plan.host_tables(gpu)
+                orp, oids, ometa = O.tables(og, gpu, [O.Req(T, s, list(ids), d) for (_, T, s, ids, d) in reqs[a:b]],
+                                            [list(x) for x in plan.dst_tables()])
+                assert np.array_equal(rp, orp) and np.array_equal(ids_, oids) and np.array_equal(meta, ometa)
         st, otabs = O.switch(og, host, held, [O.Req(T, s, list(ids), d) for (_, T, s, ids, d) in reqs[a:b]])
         assert st == 0
         assert [list(x) for x in plan.dst_tables()] == [list(y) for y in otabs]
