@@ -476,11 +476,13 @@ def run_single(args):
         else:
             settle_switches()
             reqs = state["reqs"]
-            ws = waves_of(reqs)
-            # every wave in one C call, no host sync between waves (kv_switch_multi)
-            multi = len(ws) > 1 and os.environ.get("FLYKV_MULTI_WAVE", "1") == "1"   # 0: kv_switch per wave (A/B)
-            plans_ = (F.kv_switch_multi(eng.cache, [sub for sub, _ in ws], stream) if multi
-                      else [F.kv_switch(eng.cache, sub, stream) for sub, _ in ws])
+            if (args.waves or args.pieces) and os.environ.get("FLYKV_MULTI_WAVE", "1") == "1":
+                # schedule + every wave in one C call, one sync (kv_switch_waves)
+                wv, plans_ = F.kv_switch_waves(eng.cache, reqs, split=args.pieces, stream=stream)
+                ws = [(None, owners) for owners in wv]
+            else:  # FLYKV_MULTI_WAVE=0 (A/B): one kv_switch per wave
+                ws = waves_of(reqs)
+                plans_ = [F.kv_switch(eng.cache, sub, stream) for sub, _ in ws]
             state["chain"] = [(reqs, ws, plans_)]
         agg, d2h_b = None, 0
         for plan in plans_:
@@ -596,8 +598,8 @@ def run_single(args):
                    "host_plan_ms_p50": round(statistics.median(plan_ms), 3),
                    "api": ("KVSwitchEngine.switch(read_back=True)" if DEBUG else
                            "flykv.kv_switch / kv_switch_back: one C-ABI call per switch (plan, upload, "
-                           "reshard, remap, one table read-back, sync); several waves: kv_switch_multi, one call "
-                           "and one sync for all waves")}
+                           "reshard, remap, one table read-back, sync); several waves: kv_switch_waves, one call "
+                           "(schedule + every wave) and one sync")}
 
     # per-step statistics: directions alternate, and under GQA replication the
     # two directions move different byte counts (TP>H writes p/H replicas)

@@ -374,6 +374,21 @@ typedef struct {
 kv_status kv_plan_pieces(const kv_cache* cache, const kv_request* reqs, int32_t n_reqs, int64_t max_wave_bytes,
                          int32_t cap, kv_piece* pieces, int32_t* n_pieces);
 
+/* kv_switch_waves: the whole memory-bounded switch in one call -- the wave
+ * schedule (split = 0: kv_plan_waves, whole requests; split = 1:
+ * kv_plan_pieces, block-aligned token pieces of a request when it cannot
+ * move whole), each piece turned into a plain request, and kv_switch_multi.
+ *   pieces    host [cap] out: the schedule {wave, request, tok0, tok1}
+ *             (whole requests have tok0 = 0, tok1 = num_tokens); *n_pieces
+ *   plans     host [cap] out: one committed plan per wave; *n_waves
+ * A request's final table is the concatenation, in wave order, of the
+ * destination tables of its pieces.  Errors: as kv_plan_waves /
+ * kv_plan_pieces (INVALID_ARG with *n_pieces = the needed cap when cap is
+ * too small; no state change) and kv_switch_multi. */
+kv_status kv_switch_waves(kv_cache* cache, const kv_request* reqs, int32_t n_reqs, int64_t max_wave_bytes,
+                          int32_t split, void* stream, int32_t cap, kv_piece* pieces, int32_t* n_pieces,
+                          kv_plan** plans, int32_t* n_waves);
+
 /* kv_suggest_rank_ids: N2 egress reduction.  For the requests of reqs whose
  * destination is group dst, choose the rank-ID assignment of dst's members
  * (out: host [dst.degree], rank ID of member m) that maximises the bytes

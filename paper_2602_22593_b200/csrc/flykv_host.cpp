@@ -1451,6 +1451,51 @@ extern "C" kv_status kv_switch_multi(kv_cache* c, const kv_request* reqs, const 
     return KV_OK;
 }
 
+extern "C" kv_status kv_switch_waves(kv_cache* c, const kv_request* reqs, int32_t n_reqs, int64_t max_wave_bytes,
+                                     int32_t split, void* stream, int32_t cap, kv_piece* pieces, int32_t* n_pieces,
+                                     kv_plan** plans, int32_t* n_waves) {
+    if (!c || !n_pieces || !n_waves || cap < 0 || (cap > 0 && (!pieces || !plans)) || n_reqs < 0 ||
+        (n_reqs > 0 && !reqs))
+        return fail(KV_ERR_INVALID_ARG, "bad kv_switch_waves arguments");
+    *n_waves = 0;
+    kv_status s;
+    if (split) {
+        s = kv_plan_pieces(c, reqs, n_reqs, max_wave_bytes, cap, pieces, n_pieces);
+        if (s) return s;
+    } else {  // request-granular waves, written as whole-request pieces
+        std::vector<int32_t> ws(n_reqs + 1);
+        int32_t nw = 0;
+        s = kv_plan_waves(c, reqs, n_reqs, max_wave_bytes, ws.data(), &nw);
+        if (s) return s;
+        *n_pieces = n_reqs;
+        if (n_reqs > cap) return fail(KV_ERR_INVALID_ARG, "cap %d < %d pieces", cap, n_reqs);
+        for (int32_t w = 0; w < nw; ++w)
+            for (int32_t i = ws[w]; i < ws[w + 1]; ++i) pieces[i] = kv_piece{w, i, 0, reqs[i].num_tokens};
+    }
+    // each piece as a plain request (kv_plan_pieces' contract), waves back to back
+    std::vector<kv_request> sub(*n_pieces);
+    std::vector<int32_t> wave_ptr(1, 0);
+    for (int32_t k = 0; k < *n_pieces; ++k) {
+        const kv_piece& pc = pieces[k];
+        kv_request r = reqs[pc.req];
+        if (pc.tok0 != 0 || pc.tok1 != r.num_tokens) {
+            const Layout l0 = layout_of(c->geo.num_kv_heads, r.src.degree);
+            const int32_t b0 = c->geo.block_base * l0.k;  // source block tokens B(p0)
+            const int32_t first = pc.tok0 / b0;
+            r.src_blocks += first;
+            r.n_src_blocks = (int32_t)ceil_div(pc.tok1, b0) - first;
+            r.num_tokens = pc.tok1 - pc.tok0;
+        }
+        sub[k] = r;
+        if (k > 0 && pc.wave != pieces[k - 1].wave) wave_ptr.push_back(k);
+    }
+    if (*n_pieces > 0) wave_ptr.push_back(*n_pieces);
+    const int32_t nw = (int32_t)wave_ptr.size() - 1;
+    s = kv_switch_multi(c, sub.data(), wave_ptr.data(), nw, stream, plans);
+    *n_waves = nw;
+    return s;
+}
+
 extern "C" kv_status kv_switch_back(kv_cache* c, const kv_plan* prev, void* stream, kv_plan** out) {
     if (!c || !prev || !out) return fail(KV_ERR_INVALID_ARG, "bad kv_switch_back arguments");
     *out = nullptr;

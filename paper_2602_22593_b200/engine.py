@@ -154,12 +154,11 @@ class KVSwitchEngine:
         wave commits (releasing its pieces' sources) before the next wave is
         planned; the kernels of consecutive waves are stream-ordered.  Returns (final destination table of every
         request = concatenation of its pieces' tables, the wave plans).  The
-        waves run back to back in one kv_switch_multi call."""
+        schedule and the waves run in one kv_switch_waves call."""
         requests = list(requests)
-        waves = flykv.kv_plan_pieces(self.cache, requests, max_wave_bytes)
         parts = [[] for _ in requests]
-        subs = [[flykv.piece_request(self.geom, requests[i], t0, t1) for i, t0, t1 in wave] for wave in waves]
-        plans = flykv.kv_switch_multi(self.cache, subs, self.stream)   # all waves, one sync
+        # schedule (kv_plan_pieces) and all waves in one C call, one sync
+        waves, plans = flykv.kv_switch_waves(self.cache, requests, max_wave_bytes, split=True, stream=self.stream)
         for wave, plan in zip(waves, plans):
             for (i, _, _), tab in zip(wave, plan.dst_tables()):
                 parts[i].append(tab)

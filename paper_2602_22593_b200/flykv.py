@@ -138,6 +138,8 @@ class Piece(C.Structure):
 
 
 _sig("kv_plan_pieces", C.c_int, _P, C.POINTER(Request), C.c_int32, C.c_int64, C.c_int32, C.POINTER(Piece), _I32P)
+_sig("kv_switch_waves", C.c_int, _P, C.POINTER(Request), C.c_int32, C.c_int64, C.c_int32, _P, C.c_int32,
+     C.POINTER(Piece), _I32P, C.POINTER(_P), _I32P)
 _sig("kv_plan_get_stats", C.c_int, _P, C.POINTER(PlanStats), _I64P)
 _sig("kv_plan_destroy", None, _P)
 _sig("weight_shard_view", C.c_int, C.POINTER(WeightDesc), C.c_int32, C.c_int32, C.POINTER(View))
@@ -162,7 +164,7 @@ _sig("kv_plan_work_order", C.c_int, _P, C.c_int32, _I32P, _I64P)
 
 EXPORTED = ["kv_cache_create", "kv_cache_destroy", "kv_layout", "kv_blocks_for", "kv_alloc", "kv_reserve",
             "kv_free", "kv_free_count", "kv_held_mask", "kv_plan_switch", "kv_plan_upload", "kv_reshard", "kv_reshard_staged",
-            "kv_pack", "kv_unpack", "kv_switch", "kv_switch_back", "kv_switch_multi", "kv_plan_tables", "kv_plan_resident",
+            "kv_pack", "kv_unpack", "kv_switch", "kv_switch_back", "kv_switch_multi", "kv_switch_waves", "kv_plan_tables", "kv_plan_resident",
             "kv_remap_block_tables", "kv_plan_dst_tables", "kv_plan_commit", "kv_plan_waves", "kv_plan_pieces",
             "kv_suggest_rank_ids", "kv_plan_get_stats", "kv_plan_destroy",
             "weight_shard_view", "kv_gather_view", "kv_vmm_granularity", "kv_vmm_alloc", "kv_vmm_free",
@@ -474,6 +476,40 @@ def kv_switch_multi(cache: KVCache, waves, stream=None) -> list:
                 p.destroy()
         raise FlyKVError(st, msg)
     return plans
+
+
+def kv_switch_waves(cache: KVCache, requests, max_wave_bytes: int = 0, split: bool = True, stream=None):
+    """The whole memory-bounded switch in one C call (kv_switch_waves): the
+    wave schedule (block-aligned token pieces with split, whole requests
+    without) and every wave back to back, one sync.  Returns (waves, plans):
+    waves[w] = [(request index, tok0, tok1)] in the order of plans[w]'s
+    requests; a request's final table is the concatenation of its pieces'."""
+    ra = make_requests(requests)
+    cap = max(2 * ra.n, 16)
+    while True:
+        buf = (Piece * cap)()
+        hs = (C.c_void_p * cap)()
+        n_p, n_w = C.c_int32(), C.c_int32()
+        st = _lib.kv_switch_waves(cache._h, ra.ptr, ra.n, int(max_wave_bytes), int(bool(split)), stream_of(stream),
+                                  cap, buf, C.byref(n_p), hs, C.byref(n_w))
+        if st == 1 and n_w.value == 0 and n_p.value > cap:  # INVALID_ARG with the needed count, nothing ran
+            cap = n_p.value
+            continue
+        break
+    plans = [Plan(cache, C.c_void_p(hs[k]), 0) if hs[k] else None for k in range(n_w.value)]
+    if st != KV_OK:
+        msg = _lib.kv_last_error().decode()
+        for p in plans:
+            if p is not None:
+                p.destroy()
+        raise FlyKVError(st, msg)
+    waves = [[] for _ in range(n_w.value)]
+    for k in range(n_p.value):
+        pc = buf[k]
+        waves[pc.wave].append((pc.req, pc.tok0, pc.tok1))
+    for p, wv in zip(plans, waves):
+        p.n_reqs = len(wv)
+    return waves, plans
 
 
 def kv_switch_back(cache: KVCache, prev: Plan, stream=None) -> Plan:

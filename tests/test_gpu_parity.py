@@ -393,7 +393,7 @@ def test_reshard_variants(impl, H, p0, p1, d, a2a):
         F.set_reshard_impl(0, 0)
 
 
-@pytest.mark.parametrize("one_call", [False, True])
+@pytest.mark.parametrize("one_call", [False, True, "schedule"])
 def test_memory_bounded_waves_gpu(one_call):
     """SURVEY 8(f) N1 on the device: a promotion that does not fit in one
     shot runs in waves (kv_plan_waves -> switch per wave, or every wave in
@@ -421,7 +421,11 @@ def test_memory_bounded_waves_gpu(one_call):
         eng.plan(reqs)
     waves = F.kv_plan_waves(eng.cache, reqs)
     assert len(waves) > 1
-    if one_call:
+    if one_call == "schedule":  # kv_switch_waves: the same schedule and every wave in one call
+        wv, plans = F.kv_switch_waves(eng.cache, reqs, split=False, stream=eng.stream)
+        assert wv == [[(i, 0, reqs[i][1]) for i in range(a, b)] for a, b in waves]
+        out = [(p, None, None) for p in plans]
+    elif one_call:
         out = [(p, None, None) for p in F.kv_switch_multi(eng.cache, [reqs[a:b] for a, b in waves], eng.stream)]
         torch.cuda.synchronize()
     else:
