@@ -99,10 +99,9 @@ typedef struct {
     int64_t payload_bytes;  /* n_atom_writes * atom_bytes                   */
     int64_t h2d_bytes;      /* descriptor bytes uploaded per plan           */
     int64_t n_segments;     /* (request, source GPU) work segments          */
-    int64_t n_atom_slots;   /* work slots of the kernels incl. holes of the
-                               destination-major and the mixed order
-                               (>= n_atoms); the staging size of
-                               kv_reshard_staged                           */
+    int64_t n_atom_slots;   /* work slots of the kernels: one per atom plus
+                               the mixed order's holes (>= n_atoms); the
+                               staging size of kv_reshard_staged           */
     int64_t n_buckets;      /* destination buckets of the kernels' work
                                order, summed over source GPUs
                                (kv_cache_set_work_order)                    */

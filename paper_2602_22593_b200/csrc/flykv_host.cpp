@@ -680,16 +680,15 @@ static void build_work_order(kv_plan* p, const std::vector<int64_t>& slots) {
     p->st.n_buckets = (int64_t)p->buckets.size();
 }
 
-// The kernels' atom index: each segment's slots (holes of the
-// destination-major order included), the plan's atom statistics, and the
-// work order over them.
+// The kernels' atom index: each segment's slots (one per atom, Seg), the
+// plan's atom statistics, and the work order over them.
 static void index_segments(kv_plan* p) {
     const int32_t L = p->c->geo.num_layers;
     const std::vector<Seg>& segs = p->segs;
     std::vector<int64_t> slots(segs.size());
     int64_t atoms = 0, writes = 0;
     for (size_t k = 0; k < segs.size(); ++k) {
-        slots[k] = (int64_t)L * 2 * segs[k].J1 * segs[k].nh * segs[k].k1;  // incl. holes
+        slots[k] = (int64_t)L * 2 * segs[k].C * segs[k].nh;  // every slot a real atom (Seg)
         const int64_t a = (int64_t)L * 2 * segs[k].C * segs[k].nh;         // real atoms
         atoms += a;
         writes += a * segs[k].rep1;
@@ -697,7 +696,7 @@ static void index_segments(kv_plan* p) {
     p->st.n_atoms = atoms;
     p->st.n_atom_writes = writes;
     build_work_order(p, slots);
-    p->st.n_atom_slots = p->mixed_end;  // kernel slots: destination-major holes + mixed-order holes
+    p->st.n_atom_slots = p->mixed_end;  // kernel slots: atoms + the mixed order's holes
 }
 
 // a6 sizes and the remap kernel's per-request records; packed all-pool output
@@ -1293,29 +1292,31 @@ extern "C" kv_status kv_plan_get_stats(const kv_plan* p, kv_plan_stats* st, int6
 }
 
 // Bytes of slots [a0, a1) of the segment at piece-space position k: destination bytes
-// per GPU (replicas included, holes excluded) and, in column n, source reads.
+// per GPU (replicas included) and, in column n, source reads.
 static void count_piece(const kv_plan* p, int32_t k, int64_t a0, int64_t a1, int64_t* row_out) {
     const int32_t n = p->c->n_gpus;
     const int64_t ab = p->c->atom_bytes;
     const Seg& sg = p->segs[p->seg_of[k]];
-    const int64_t R = (int64_t)sg.nh * sg.k1;  // slots per (layer, K/V, destination block) row
-    for (int64_t r = a0 / R; r * R < a1; ++r) {
-        const int64_t j = r % sg.J1;
-        const int64_t valid = std::min<int64_t>(sg.k1, sg.C - j * sg.k1);  // chunks w < valid are real
-        const int64_t o0 = std::max<int64_t>(a0 - r * R, 0), o1 = std::min<int64_t>(a1 - r * R, R);
-        for (int64_t hh = o0 / sg.k1; hh * sg.k1 < o1; ++hh) {
-            const int64_t w0 = std::max<int64_t>(o0 - hh * sg.k1, 0), w1 = std::min<int64_t>(o1 - hh * sg.k1, valid);
-            if (w1 <= w0) continue;
-            const int64_t cnt = w1 - w0;
-            const int32_t h = sg.h0 + (int32_t)hh;
-            row_out[n] += cnt * ab;
-            for (int32_t rj = 0; rj < sg.rep1; ++rj) {
-                const int32_t rid = sg.rep1 == 1 ? h / sg.hloc1 : h * sg.rep1 + rj;
-                const int32_t m = sg.dst_inv < 0 ? rid : p->tables[sg.dst_inv + rid];
-                row_out[sg.dst_g0 + m] += cnt * ab;
+    const int64_t per = (int64_t)sg.C * sg.nh;           // slots per (layer, K/V)
+    const int64_t kk = sg.C - (int64_t)(sg.J1 - 1) * sg.k1; // chunks of the last destination block
+    for (int64_t lkv = a0 / per; lkv * per < a1; ++lkv)
+        for (int64_t jb = std::max<int64_t>(0, (a0 - lkv * per) / ((int64_t)sg.nh * sg.k1)); jb < sg.J1; ++jb) {
+            const int64_t kj = jb == sg.J1 - 1 ? kk : sg.k1;
+            const int64_t b0 = lkv * per + jb * sg.nh * sg.k1;     // first slot of destination block jb
+            if (b0 >= a1) break;
+            const int64_t o0 = std::max<int64_t>(a0 - b0, 0), o1 = std::min<int64_t>(a1 - b0, sg.nh * kj);
+            if (o1 <= o0) continue;
+            for (int64_t hh = o0 / kj; hh * kj < o1; ++hh) {
+                const int64_t cnt = std::min<int64_t>(o1, (hh + 1) * kj) - std::max<int64_t>(o0, hh * kj);
+                const int32_t h = sg.h0 + (int32_t)hh;
+                row_out[n] += cnt * ab;
+                for (int32_t rj = 0; rj < sg.rep1; ++rj) {
+                    const int32_t rid = sg.rep1 == 1 ? h / sg.hloc1 : h * sg.rep1 + rj;
+                    const int32_t m = sg.dst_inv < 0 ? rid : p->tables[sg.dst_inv + rid];
+                    row_out[sg.dst_g0 + m] += cnt * ab;
+                }
             }
         }
-    }
 }
 
 // Piece-space slot range [b0, b1) (global) within positions [lo, hi).

@@ -38,14 +38,17 @@ FLYKV_HD int32_t first_head_of_rank(const Layout& L, int32_t r) {
 }
 
 // One work segment: the atoms of one request whose canonical source replica
-// (R10) is pool src_gpu.  Atom slots are in destination-major order
-//   a = (((l*2 + kv)*J1 + j)*nh + hh)*k1 + w,   chunk c = j*k1 + w,  head h = h0 + hh
-// (0 <= a < L*2*J1*nh*k1; slots with c >= C are holes and are skipped), so
-// consecutive slots fill one destination block sequentially: head hl's k1
-// chunks (contiguous B(p1)-token run), then the next head.  With k1 = 1 this
-// is ((l*2 + kv)*C + c)*nh + hh: consecutive 4 KiB pieces of one source block
-// fanning out over destination ranks.  (DRAM write locality is what matters:
-// writing contiguous runs measured +2-3%.)
+// (R10) is pool src_gpu.  Atom slots are in destination-major order: per
+// (layer, K/V), C*nh slots, destination block j after destination block j,
+// each holding its nh heads x k1 chunks (the last block, j = J1-1, its
+// kk = C - (J1-1)*k1 chunks), chunk c = j*k1 + w, head h = h0 + hh:
+//   a = (l*2 + kv)*C*nh + j*nh*k1 + hh*kk_j + w      (kk_j = k1, or kk for the last block)
+// so consecutive slots fill one destination block sequentially (head hl's
+// chunks are a contiguous B(p1)-token run, then the next head) and every
+// slot is a real atom.  With k1 = 1 this is ((l*2 + kv)*C + c)*nh + hh:
+// consecutive 4 KiB pieces of one source block fanning out over destination
+// ranks.  (DRAM write locality is what matters: writing contiguous runs
+// measured +2-3%.)
 struct Seg {
     int32_t src_gpu;   // pool holding the source replica
     int32_t dst_g0;    // first pool of the destination group

@@ -84,13 +84,27 @@ __device__ __forceinline__ int64_t unmix(const ReshardArgs& a, int64_t atom) {
 template <bool MIX>
 __device__ __forceinline__ void decode(const ReshardArgs& a, int s, uint32_t local, AtomAddr& out) {
     const Seg sg = a.segs[MIX && a.mixed ? __ldg(a.seg_of + s) : s];  // plan order: seg_of is the identity
-    const uint32_t nh = (uint32_t)sg.nh, k1 = (uint32_t)sg.k1, J1 = (uint32_t)sg.J1;
-    const uint32_t w = local % k1;        // (((l*2 + kv)*J1 + j)*nh + hh)*k1 + w
-    local /= k1;
-    const uint32_t hh = local % nh;
-    local /= nh;
-    const uint32_t jb = local % J1;
-    const uint32_t lkv = local / J1;
+    // destination-major order without holes (Seg, flykv_internal.h): per
+    // (layer, K/V) C*nh slots = the destination blocks jb in turn, each nh
+    // heads x k1 chunks, the last block nh x kk (kk = C - (J1-1)*k1)
+    const uint32_t nh = (uint32_t)sg.nh, k1 = (uint32_t)sg.k1, J1 = (uint32_t)sg.J1, C = (uint32_t)sg.C;
+    const uint32_t per = C * nh;
+    const uint32_t lkv = local / per;
+    uint32_t rem = local - lkv * per;
+    const uint32_t row = nh * k1, full = (J1 - 1) * row;
+    uint32_t jb, hh, w;
+    if (rem < full) {
+        jb = rem / row;
+        rem -= jb * row;
+        hh = rem / k1;
+        w = rem - hh * k1;
+    } else {
+        const uint32_t kk = C - (J1 - 1) * k1;
+        rem -= full;
+        jb = J1 - 1;
+        hh = rem / kk;
+        w = rem - hh * kk;
+    }
     const uint32_t kv = lkv & 1u, l = lkv >> 1;
     const uint32_t c = jb * k1 + w;
     int32_t h = sg.h0 + (int32_t)hh;
@@ -102,17 +116,6 @@ __device__ __forceinline__ void decode(const ReshardArgs& a, int s, uint32_t loc
     out.k1 = sg.k1;
     out.J1 = sg.J1;
     out.a2a = sg.a2a;
-    if (c >= (uint32_t)sg.C) {  // hole past the request's last chunk
-        out.src = nullptr;
-        out.doff = 0;
-        out.l = (int32_t)l;
-        out.h = h;
-        out.dst_g0 = sg.dst_g0;
-        out.rep1 = 0;
-        out.hloc1 = sg.hloc1;
-        out.dst_inv = sg.dst_inv;
-        return;
-    }
     const int64_t half = a.M >> 1;
     const int64_t ab = a.atom_bytes;
     // source replica (lowest owner, R10): block tab0[c / k0], chunk c % k0
@@ -187,7 +190,7 @@ __device__ __forceinline__ void lane_decode(const ReshardArgs& a, int64_t slot, 
     AtomAddr ad;
     decode<MIX>(a, s, local, ad);
     la.src = ad.src;
-    la.rep1 = ad.rep1;  // 0 for a hole: nothing is read or written
+    la.rep1 = ad.rep1;
     la.dst0 = ad.src ? dst_ptr(a, ad, 0) : nullptr;
     if ((a.staged == 1 || a.staged == 2) && la.rep1 > 0) {  // comparator: slot-order pack or unpack
         char* stg = a.staging + (slot - a.atom_lo) * (int64_t)a.atom_bytes;
