@@ -510,3 +510,23 @@ def test_one_long_request_promoted_in_pieces():
     w2 = F.kv_plan_pieces(c2, [(0, 1000, (0, 1), ids2, (0, 8))], max_wave_bytes=300 * per_token)
     assert len(w2) >= 4 and all((t1 - t0) * per_token <= 300 * per_token for [(_, t0, t1)] in w2)
     _run_pieces_against_oracle(c2, og, held2, [(0, 1000, (0, 1), ids2, (0, 8))], w2, 8)
+
+
+def test_kv_switch_waves_schedule_retry_before_the_device():
+    """kv_switch_waves grows its piece buffer when the schedule needs more
+    pieces than the first guess (a byte cap of 1 cuts every request into
+    block-aligned pieces, many more than 2 x requests), then plans the first
+    wave.  On a CPU-only host the device step then fails with KV_ERR_CUDA and
+    the failed wave's allocations are rolled back: no state change."""
+    torch = pytest.importorskip("torch")
+    if torch.cuda.is_available():
+        pytest.skip("checks the no-device failure path")
+    c = fake_cache((1, 4, 8, 4, 2), [256, 256])
+    a = c.alloc((0, 1), 40)              # 160 tokens at B = 4
+    before = [c.held_mask(g).copy() for g in (0, 1)]
+    reqs = [(1, 160, (0, 1), a, (0, 2))]
+    assert sum(len(w) for w in F.kv_plan_pieces(c, reqs, 1)) > 16   # beyond the binding's first buffer
+    with pytest.raises(F.FlyKVError) as e:
+        F.kv_switch_waves(c, reqs, max_wave_bytes=1, split=True)
+    assert e.value.name == "KV_ERR_CUDA"
+    assert all(np.array_equal(c.held_mask(g), before[g]) for g in (0, 1))
