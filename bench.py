@@ -55,10 +55,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=4)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", help="workload key of synth.WORKLOADS (N=1)")
-    ap.add_argument("--cpu-sample-reqs", type=int, default=6, help="oracle sample per --impl reference step")
-    ap.add_argument("--cpu-baseline-reqs", type=int, default=16, help="oracle sample for cpu_baseline")
-    ap.add_argument("--cpu-baseline-steps", type=int, default=6)
+    ap.add_argument("--config", default="c4",
+                    help="workload key of synth.WORKLOADS; default c4 = the north_star headline (Llama-3-70B "
+                         "8 x DP1 -> TP8), its 8 engines mapped onto the N GPUs as 8/N virtual ranks each")
+    ap.add_argument("--cpu-sample-reqs", type=int, default=4,
+                    help="oracle sample (first N requests) per step of --impl reference and of cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-parallel", action="store_true", help="skip the all-cores oracle figure")
@@ -192,14 +193,9 @@ class ClockSampler:
 
 # --------------------------------------------------------------- workload
 def build_workload(args, world: int, rank: int):
-    if world == 1:
-        w = synth.WORKLOADS[args.config]()
-    elif world == 4:
-        w = synth.llama8b_dp4_tp2x2()       # BJ configs[1] as stated: DP4 -> TP2x2 on 4 GPUs
-    elif world == 8:
-        w = synth.llama70b_dp8_tp8()        # BJ configs[3]: the headline 8 x DP1 -> TP8
-    else:
-        w = synth.dp_to_tp(world, 16 * world)  # ~4.9 GB per GPU, like configs[1] per GPU
+    """The same workload at every N (strong scaling): its engines are mapped
+    onto the N GPUs as consecutive blocks of engines/N virtual ranks."""
+    w = synth.WORKLOADS[args.config]()
     if args.requests:
         w = synth.Workload(w.name + f" first{args.requests}", w.L, w.H, w.d, w.B, w.e, w.n_gpus,
                            w.T[:args.requests], w.src[:args.requests], w.dst[:args.requests])
@@ -338,22 +334,47 @@ def cpu_oracle_parallel(w, reqs_per_thread: int = 2, steps: int = 3, max_threads
     return payload / sec / 1e9, len(work), info
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_baseline_of(w, args, parallel: bool = True) -> dict:
+    """The oracle as it stands, one host thread, on the same bounded sample
+    and with the same --steps/--warmup in both arms (cpu_baseline of our
+    line and the value of the --impl reference line are one measurement
+    procedure), plus the all-cores figure."""
+    gbs, sec, info, _ = cpu_oracle_run(w, args.cpu_sample_reqs, args.steps, args.warmup)
+    out = {"value": round(gbs, 4), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": info,
+           "cpu_model": cpu_model(), "ms_per_switch": round(sec * 1e3, 3)}
+    if parallel:
+        pg, nt, pinfo = cpu_oracle_parallel(w)
+        out["all_cores"] = {"value": round(pg, 4), "unit": "GB/s", "cores": nt, "sample": pinfo}
+    return out
+
+
 def run_reference(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     w = build_workload(args, world, rank)
-    gbs, sec, info, payload = cpu_oracle_run(w, args.cpu_sample_reqs, args.steps, args.warmup)
+    cpu = cpu_baseline_of(w, args, parallel=False)
+    gbs = cpu["value"]
     line = {
-        "impl": "reference", "metric": "DP<->TP KV re-layout GB/s", "value": round(gbs, 4), "unit": "GB/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(sec * 1e3, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": w.name + (f" ({w.n_gpus} virtual ranks on 1 GPU)" if w.n_gpus > 1 and world == 1 else ""),
+        "impl": "reference", "metric": "DP<->TP KV re-layout GB/s", "value": gbs, "unit": "GB/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": cpu["ms_per_switch"],
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": w.name + (f" ({w.n_gpus} engines)" if w.n_gpus > 1 else ""),
                    "layers": w.L, "kv_heads": w.H, "head_dim": w.d, "block_base": w.B, "requests": len(w.T),
-                   "tokens": w.tokens(), "sample": info},
-        "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": info},
-        "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                   "tokens": w.tokens(), "sample": cpu["sample"]},
+        "cpu_baseline": cpu,
+        "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -637,17 +658,11 @@ def run_single(args):
             traffic, traffic_ratio = tj.get("dram_bytes_per_launch"), tj.get("traffic_over_algorithmic")
         except Exception:
             traffic = traffic_ratio = None
-    cpu = None
-    if not args.no_cpu_baseline:
-        gbs, sec, info, _ = cpu_oracle_run(w, args.cpu_baseline_reqs, args.cpu_baseline_steps, 0)
-        cpu = {"value": round(gbs, 4), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": info}
-        if not args.no_cpu_parallel:
-            pg, nt, pinfo = cpu_oracle_parallel(w)
-            cpu["all_cores"] = {"value": round(pg, 4), "unit": "GB/s", "cores": nt, "sample": pinfo}
+    cpu = None if args.no_cpu_baseline else cpu_baseline_of(w, args, parallel=not args.no_cpu_parallel)
     line = {
         "metric": "DP<->TP KV re-layout GB/s", "value": round(value, 3), "unit": "GB/s", "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic",
         "config": {"workload": w.name + (f" ({w.n_gpus} virtual ranks on 1 GPU)" if w.n_gpus > 1 else ""),
                    "layers": w.L, "kv_heads": w.H, "head_dim": w.d, "block_base": w.B, "requests": len(w.T),
@@ -759,9 +774,22 @@ def ordered_link_model(pieces, hbm_gbs, link_gbs=FALLBACK_NVLINK_GBS):
                     rem[g] = 1.0
 
 
+def proc_matrix(bytes_matrix, v: int):
+    """Pool-level byte matrix -> process-level (process r owns pools
+    [r*v, (r+1)*v)): bytes between pools of one process stay in its HBM."""
+    m = np.asarray(bytes_matrix, dtype=np.float64)
+    n = m.shape[0] // v
+    return m.reshape(n, v, n, v).sum(axis=(1, 3))
+
+
 def run_multi(args):
-    """One process per GPU (torchrun).  Every rank pushes the atoms it holds
-    into peer pools (IPC-mapped, NVLink P2P stores), then a group barrier."""
+    """One process per GPU (torchrun; bench.py --gpus N self-launches it).
+    The workload's engines (8 for the default c4) are mapped onto the N
+    processes as consecutive blocks of v = engines/N virtual ranks, so the
+    same switch runs at every N (strong scaling).  Each process pushes the
+    atoms its pools hold into every destination pool (local, or a peer GPU's
+    through CUDA IPC over NVLink), then the device-side group barrier (a5,
+    kv_group_barrier), then remaps its own pools' tables."""
     import torch
     import torch.distributed as dist
 
@@ -771,31 +799,45 @@ def run_multi(args):
     world = int(os.environ["WORLD_SIZE"])
     rank = int(os.environ["RANK"])
     local = int(os.environ.get("LOCAL_RANK", rank))
-    same_dev = os.environ.get("FLYKV_SAME_DEVICE") == "1"   # test mode: all ranks on cuda:0, gloo
+    same_dev = os.environ.get("FLYKV_SAME_DEVICE") == "1"   # test mode: all ranks on cuda:0, gloo plumbing
+    if not same_dev and torch.cuda.device_count() < world:
+        sys.stderr.write(f"bench.py: {world} ranks but {torch.cuda.device_count()} visible GPU(s); "
+                         "set FLYKV_SAME_DEVICE=1 to run every rank on cuda:0 (test mode)\n")
+        return 2
     dev = torch.device("cuda", 0 if same_dev else local)
     torch.cuda.set_device(dev)
-    nccl = not same_dev and os.environ.get("FLYKV_BARRIER", "nccl") == "nccl"
-    if nccl:
-        try:
-            dist.init_process_group("nccl", device_id=dev)
-        except Exception as e:  # keep the P2P data path; synchronise through a host (gloo) barrier
-            sys.stderr.write(f"NCCL init failed ({e}); using a gloo host barrier\n")
-            nccl = False
-    if not nccl:
+    nccl = not same_dev
+    if nccl:   # NCCL init lines on stderr (the driver checks the rank count)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+        dist.init_process_group("nccl", device_id=dev)
+    else:
         dist.init_process_group("gloo")
-    degrees = [p for p in (2, 4, 8) if p <= world and world % p == 0]
-    cpool = comm.CommunicatorPool(world, degrees, backend="nccl" if nccl else "gloo")
     w = build_workload(args, world, rank)
+    if w.n_gpus % world:
+        if rank == 0:
+            sys.stderr.write(f"bench.py: workload {w.name} has {w.n_gpus} engines, not divisible by {world} GPUs\n")
+        dist.destroy_process_group()
+        return 2
+    v = w.n_gpus // world
+    mine = range(rank * v, (rank + 1) * v)
+    degrees = [p for p in (2, 4, 8) if p <= world and world % p == 0]
+    cpool = comm.CommunicatorPool(world, degrees, backend="nccl" if nccl else "gloo")   # eager
+    world_key = tuple(range(world))
+    barrier = comm.DeviceBarrier(rank, world, list(dict.fromkeys(list(cpool.keys) + [world_key])), dev)
     g = F.geometry(w.L, w.H, w.d, w.B, w.e)
     _, _, M = F.kv_layout(g, 1)
-    nb, tabs = pools_and_tables(w)
-    local_pool = torch.empty((w.L, nb[rank], M), dtype=torch.uint8, device=dev)
+    nb, tabs = pools_and_tables(w, args.frag, args.pool_slack, args.placement == "contiguous")
+    local_pools = torch.empty((v, w.L, nb[0], M), dtype=torch.uint8, device=dev)
     if not args.no_fill:
-        synth.fill_hash_torch(local_pool, rank)
-    bases, nbs, imported = comm.exchange_pools(local_pool, rank, world, w.L, M)
-    cache = F.KVCache(g, nbs, bases, degrees)
+        for k, gp in enumerate(mine):
+            synth.fill_hash_torch(local_pools[k], gp)
+    torch.cuda.synchronize()
+    bases, nbs, imported = comm.exchange_pools(local_pools, rank, world, w.L, M)
+    cache = F.KVCache(g, nbs, bases, tuple(p for p in (2, 4, 8) if p <= w.n_gpus))
     if args.work_order is None:
-        args.work_order = 0 if same_dev else 1
+        args.work_order = 0 if (same_dev or world == 1) else 1
     cache.set_work_order(args.work_order)
     for s_, ids in zip(w.src, tabs):
         cache.reserve(s_, ids)
@@ -807,26 +849,30 @@ def run_multi(args):
         reqs0 = [r[:6] + (rank_ids.get(tuple(r[4])),) for r in reqs0]
     state = {"reqs": reqs0}
     ev_pairs = []
-    world_key = tuple(range(world))
 
-    def barrier_group(reqs):
-        key = cpool.covering([r[2] for r in reqs] + [r[4] for r in reqs]) if reqs else world_key
-        return key, (None if key == world_key else cpool.get(key))
+    def barrier_key(reqs):
+        """Processes whose pools the switch touches: those of the smallest
+        pooled group covering every source and destination (R12)."""
+        if not reqs:
+            return world_key
+        lo = min(min(r[2][0], r[4][0]) for r in reqs)
+        hi = max(max(r[2][0] + r[2][1], r[4][0] + r[4][1]) for r in reqs)
+        key = cpool.covering([(lo // v, 1), ((hi - 1) // v, 1)])
+        return key if key in barrier.slot else world_key
 
     step_stats = []
-
-    orders = []   # rank 0: kernel work order of a forward and a return plan (warm-up), for the link model
+    out_bufs = {}
 
     def step(timed=False, read_back=False):
         plan = F.kv_plan_switch(cache, state["reqs"])
         plan.upload(stream)
-        if rank == 0 and not timed and not read_back and len(orders) < 2:
-            orders.append([plan.work_order(x) for x in range(world)])
         if timed:
             step_stats.append(plan.stats())
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
         if args.a2a:  # comparator: per-destination chunks through NCCL all_to_all_single (gloo: host copies)
+            if v != 1:
+                raise SystemExit("--a2a needs one pool per process")
             _, mat = plan.stats()
             send_off, recv_off = F.a2a_offsets(mat)
             n_send, n_recv = int(mat[rank].sum()), int(mat[:, rank].sum())
@@ -844,36 +890,38 @@ def run_multi(args):
                     recv[:n_recv].copy_(rh)
             F.kv_unpack(plan, rank, recv, recv_off[rank], stream)
         else:
-            F.kv_reshard(plan, rank, stream)
+            F.kv_reshard_range(plan, mine.start, mine.stop, stream)
         if timed:
             e1.record(stream)
             ev_pairs.append((e0, e1))
-        key, grp = barrier_group(state["reqs"])
-        comm.switch_barrier(stream, grp, nccl=nccl, device=dev, members=key, rank=rank)
-        n_res, n_ids = plan.resident(rank)
-        rp = torch.empty(n_res + 1, dtype=torch.int32, device=dev)
-        ids = torch.empty(max(n_ids, 1), dtype=torch.int32, device=dev)
-        meta = torch.empty((max(n_res, 1), 4), dtype=torch.int32, device=dev)
-        F.kv_remap_block_tables(plan, rank, rp, ids, meta, stream)
+        barrier.wait(barrier_key(state["reqs"]), stream)   # a5 on the device
         host_bytes = 0
+        for gp in mine:
+            n_res, n_ids = plan.resident(gp)
+            key = (gp, n_res, n_ids)
+            if key not in out_bufs:
+                out_bufs[key] = (torch.empty(n_res + 1, dtype=torch.int32, device=dev),
+                                 torch.empty(max(n_ids, 1), dtype=torch.int32, device=dev),
+                                 torch.empty((max(n_res, 1), 4), dtype=torch.int32, device=dev))
+            rp, ids, meta = out_bufs[key]
+            F.kv_remap_block_tables(plan, gp, rp, ids, meta, stream)
+            if read_back:
+                with torch.cuda.stream(stream):
+                    h = [rp.to("cpu", non_blocking=True), ids[:n_ids].to("cpu", non_blocking=True),
+                         meta[:n_res].to("cpu", non_blocking=True)]
+                host_bytes += sum(int(x.numel()) * 4 for x in h)
         if read_back:
-            with torch.cuda.stream(stream):
-                h = [rp.to("cpu", non_blocking=True), ids[:n_ids].to("cpu", non_blocking=True),
-                     meta[:n_res].to("cpu", non_blocking=True)]
             stream.synchronize()
-            host_bytes = sum(int(x.numel()) * 4 for x in h)
         new = plan.dst_tables()
         state["reqs"] = [(rid, T, d, t, s_, drid, srid)
                          for (rid, T, s_, _, d, srid, drid), t in zip(state["reqs"], new)]
         return plan, host_bytes
 
-    plan0 = F.kv_plan_switch(cache, state["reqs"])
-    stats, mat = plan0.stats()
-    plan0.destroy()
     clk = ClockSampler(dev.index, args.clock_ms).start()
-    for _ in range(args.warmup):
+    for _ in range(max(args.warmup, 1)):
         step()
     torch.cuda.synchronize()
+    barrier.check()
     dist.barrier()
     n_launch0 = F.launch_count()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -885,10 +933,12 @@ def run_multi(args):
     end.record(stream)
     torch.cuda.synchronize()
     clk.end()
+    barrier.check()
     dist.barrier()
     launches = F.launch_count() - n_launch0
     my_ms = start.elapsed_time(end)
-    my_kern = sum(a.elapsed_time(b) for a, b in ev_pairs) / len(ev_pairs)
+    kern = [a.elapsed_time(b) for a, b in ev_pairs]
+    my_kern = sum(kern) / len(kern)
     keep.clear()
     lat = []
     h2d = d2h = 0
@@ -902,13 +952,20 @@ def run_multi(args):
             h2d += plan.stats()[0]["h2d_bytes"]
             e2e_payload += plan.stats()[0]["payload_bytes"]
             d2h += hb
-    red = torch.tensor([my_ms, my_kern, max(lat) if lat else 0.0, (sum(lat) / len(lat)) if lat else 0.0,
-                        float(launches)], dtype=torch.float64, device=dev if nccl else "cpu")
+        barrier.check()
+    red = torch.tensor([my_ms, my_kern, (sum(lat) / len(lat)) if lat else 0.0,
+                        statistics.median(lat) if lat else 0.0, float(np.percentile(lat, 99)) if lat else 0.0],
+                       dtype=torch.float64, device=dev if nccl else "cpu")
     dist.all_reduce(red, op=dist.ReduceOp.MAX)
-    total_ms, kern_ms, _, lat_mean, _ = [float(x) for x in red.tolist()]
-    n_l = torch.tensor([float(launches)], dtype=torch.float64, device=dev if nccl else "cpu")
-    dist.all_reduce(n_l, op=dist.ReduceOp.SUM)   # every rank's kernels count toward the job
-    launches_all = int(n_l.item())
+    total_ms, kern_ms, lat_mean, lat_p50, lat_p99 = [float(x) for x in red.tolist()]
+    n_l = torch.tensor([float(launches), float(d2h)], dtype=torch.float64, device=dev if nccl else "cpu")
+    dist.all_reduce(n_l, op=dist.ReduceOp.SUM)   # every rank's kernels / read-backs count toward the job
+    launches_all, d2h_all = int(n_l[0].item()), int(n_l[1].item())
+    pool_cost = {"backend": "nccl" if nccl else "gloo", "groups": len(cpool.keys),
+                 "init_seconds": round(cpool.init_seconds, 4),
+                 "host_bytes_per_group": (int(cpool.host_bytes_per_group)
+                                          if cpool.host_bytes_per_group is not None else None)}
+    barrier.close()
     comm.close_pools(imported)
     if rank == 0:
         payload_sum = sum(x[0]["payload_bytes"] for x in step_stats)
@@ -916,47 +973,53 @@ def run_multi(args):
         hbm_peak, peak_src = peaks()
         t_min = busiest = 0.0
         for _, m in step_stats:
-            t, eg, ing, _ = nvlink_roofline(m, hbm_peak)
+            t, eg, ing, _ = nvlink_roofline(proc_matrix(m, v), hbm_peak)
             t_min += t / len(step_stats)
             busiest += float(max(eg.max(), ing.max())) / len(step_stats)
         achieved = busiest / (kern_ms / 1e3) / 1e9
-        # fluid model of the same plans in the kernels' visiting order (ingress contention included)
-        t_model = (sum(ordered_link_model(o, hbm_peak) for o in orders) / len(orders)) if orders else None
         hbm_algo = sum((x[0]["n_atoms"] + x[0]["n_atom_writes"]) * x[0]["atom_bytes"] for x in step_stats) / len(step_stats)
+        if same_dev:   # every rank on cuda:0: one HBM does all the reads and writes
+            a_ = hbm_algo / (total_ms / args.steps / 1e3) / 1e9
+            roof = {"bound": "hbm", "achieved": round(a_, 1), "peak": hbm_peak, "unit": "GB/s",
+                    "frac": round(a_ / hbm_peak, 4), "traffic": None, "peak_source": peak_src,
+                    "kernel": "flykv_reshard_kernel of every rank sharing cuda:0; per-step time (incl. the device "
+                              "barrier) as the denominator since the ranks' launches overlap"}
+        else:
+            roof = {"bound": "nvlink", "achieved": round(achieved, 1), "peak": FALLBACK_NVLINK_GBS,
+                    "unit": "GB/s", "frac": round(achieved / FALLBACK_NVLINK_GBS, 4), "traffic": None,
+                    "peak_source": "measured peer copy per direction (B200_PROFILING.md 770 GB/s)",
+                    "t_min_ms": round(t_min * 1e3, 4), "frac_of_t_min": round(t_min * 1e3 / kern_ms, 4),
+                    "work_order": ["plan", "mixed"][args.work_order],
+                    "kernel": "flykv_reshard_kernel (busiest GPU's egress/ingress per launch)"}
         line = {
             "metric": "DP<->TP KV re-layout GB/s", "value": round(payload_sum / (total_ms / 1e3) / 1e9, 3),
             "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": w.name + (" (ranks share cuda:0, gloo)" if same_dev else "") +
-                       (" [pack -> all_to_all_single -> unpack comparator]" if args.a2a else ""), "layers": w.L,
+            "config": {"workload": w.name + (f" ({v} virtual ranks per GPU)" if v > 1 else "") +
+                       (" (ranks share cuda:0, gloo plumbing)" if same_dev else "") +
+                       (" [pack -> all_to_all_single -> unpack comparator]" if args.a2a else ""),
+                       "engines": w.n_gpus, "pools_per_gpu": v, "layers": w.L,
                        "work_order": ["plan", "mixed"][args.work_order],
                        "kv_heads": w.H, "head_dim": w.d, "block_base": w.B, "requests": len(w.T),
                        "tokens": w.tokens(), "payload_bytes_per_step": int(payload),
                        "l2": "inputs larger than L2, no flush needed",
-                       "step": ("plan + upload + pack + all_to_all_single + unpack + group barrier + remap" if args.a2a
-                                else "plan + upload + reshard (P2P push over NVLink) + group barrier + remap")},
+                       "barrier": "kv_group_barrier (device-side, IPC counters)",
+                       "step": ("plan + upload + pack + all_to_all_single + unpack + device barrier + remap"
+                                if args.a2a else
+                                "plan + upload + reshard (P2P push over NVLink) + device barrier + remap")},
             "switch_latency_ms": round(total_ms / args.steps, 4),
             "reshard_kernel_ms": round(kern_ms, 4),
-            "roofline": ({"bound": "nvlink", "achieved": round(achieved, 1), "peak": FALLBACK_NVLINK_GBS,
-                          "unit": "GB/s", "frac": round(achieved / FALLBACK_NVLINK_GBS, 4), "traffic": None,
-                          "peak_source": "measured peer copy per direction (B200_PROFILING.md 770 GB/s)",
-                          "t_min_ms": round(t_min * 1e3, 4), "frac_of_t_min": round(t_min * 1e3 / kern_ms, 4),
-                          "t_model_ms": round(t_model * 1e3, 4) if t_model else None,
-                          "work_order": ["plan", "mixed"][args.work_order],
-                          "kernel": "flykv_reshard_kernel (busiest GPU's egress/ingress per launch)"}
-                         if not same_dev else
-                         {"bound": "hbm", "achieved": round(hbm_algo / (total_ms / args.steps / 1e3) / 1e9, 1),
-                          "peak": hbm_peak, "unit": "GB/s",
-                          "frac": round(hbm_algo / (total_ms / args.steps / 1e3) / 1e9 / hbm_peak, 4),
-                          "traffic": None, "peak_source": peak_src,
-                          "kernel": "flykv_reshard_kernel of all ranks sharing cuda:0; per-step time (incl. gloo "
-                                    "barrier) as the denominator since the ranks' launches overlap"}),
+            "roofline": roof,
             "cpu_baseline": None,
             "e2e": ({"value": round(e2e_payload / len(lat) / (lat_mean / 1e3) / 1e9, 3), "unit": "GB/s",
                      "h2d_bytes_per_step": int(h2d // max(len(lat), 1)),
-                     "d2h_bytes_per_step": int(d2h // max(len(lat), 1)),
-                     "switch_latency_ms_mean_max_over_ranks": round(lat_mean, 3)} if lat else None),
+                     "d2h_bytes_per_step": int(d2h_all // max(len(lat), 1)),
+                     "switch_latency_ms_p50": round(lat_p50, 3), "switch_latency_ms_p99": round(lat_p99, 3),
+                     "switch_latency_ms_mean": round(lat_mean, 3),
+                     "note": "per-rank wall clock from a host barrier to its tables on the host; max over ranks"}
+                    if lat else None),
+            "comm_pool": pool_cost,
             "gpu_launches": launches_all,
             "clocks": clk.summary(),
         }
@@ -966,11 +1029,28 @@ def run_multi(args):
     return 0
 
 
+def self_launch(args) -> int:
+    """bench.py --gpus N (N > 1) outside torchrun: re-run this script under
+    torch.distributed.run with N local ranks (127.0.0.1 rendezvous)."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "4")
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "0"))
+    if args.gpus > 1 and world == 0:   # not under torchrun: launch the N ranks ourselves
+        return self_launch(args)
     if args.impl == "reference":
         return run_reference(args)
-    world = int(os.environ.get("WORLD_SIZE", "1"))
     if world > 1:
         return run_multi(args)
     return run_single(args)

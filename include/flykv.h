@@ -210,6 +210,16 @@ kv_status kv_plan_upload(kv_plan* plan, void* stream);
  */
 kv_status kv_reshard(kv_plan* plan, int32_t gpu, void* stream);
 
+/* kv_reshard_range: kv_reshard of the atoms sourced on pools [gpu_lo,
+ * gpu_hi), one launch -- for a process that owns several pools (virtual
+ * ranks) of a cache whose other pools belong to other processes.  kv_reshard
+ * (gpu) == kv_reshard_range(gpu, gpu + 1); kv_reshard(-1) == range [0,
+ * n_gpus).  A range short of every pool may store into peer mappings: the
+ * kernel then ends with a system-scope fence for kv_group_barrier.
+ * Errors: KV_ERR_INVALID_ARG (range empty or outside [0, n_gpus)),
+ * KV_ERR_BAD_STATE (plan committed), KV_ERR_CUDA. */
+kv_status kv_reshard_range(kv_plan* plan, int32_t gpu_lo, int32_t gpu_hi, void* stream);
+
 /* Bench comparator only: the same re-layout split into two
  * passes through a staging buffer, as a pack -> all-to-all -> unpack
  * implementation would do.  mode 1 packs every atom of the range (source
@@ -511,6 +521,34 @@ kv_status kv_paged_decode(const kv_geometry* geom, const void* layer_base, int32
 kv_status kv_ipc_export(const void* dptr, uint8_t handle[64], uint64_t* offset);
 kv_status kv_ipc_import(const uint8_t handle[64], uint64_t offset, void** dptr);
 kv_status kv_ipc_close(void* dptr, uint64_t offset);
+
+/*
+ * kv_group_barrier: the group completion barrier between processes (a5;
+ * P:451 "safe points"), on the device, no host round trip.  Enqueues on
+ * `stream` one single-thread kernel that (1) fences at system scope (every
+ * earlier kernel of the stream -- this process's reshard and its NVLink
+ * peer stores -- is ordered before what follows), (2) adds 1 with
+ * system-scope release semantics to the 64-bit counter of every member,
+ * then (3) spins with acquire loads on its own counter until it is
+ * >= target.  Later work on the stream (the remap, the next switch) starts
+ * only after every member's arrival, so after every member's pushes.
+ *   flags       host array [n_members] of device pointers: this process's
+ *               mapping of each member's counter (its own, or a peer's
+ *               through kv_ipc_import); 8-byte aligned, zero-initialised
+ *               once by its owner; one counter per (process, group)
+ *   self        index of this process's own counter in flags
+ *   target      k * n_members for the k-th barrier (k = 1, 2, ...) on
+ *               these counters -- every member adds exactly once per
+ *               barrier, so the count is exact and no reset is needed
+ *   timeout_ns  a member that never arrives ends the wait after this long:
+ *               *status (device int32, may be NULL) is set to 1; with
+ *               status NULL the kernel traps (a CUDA error, never a hang)
+ * Counters are caller memory; ranks outside the group do not call.
+ * Errors: KV_ERR_INVALID_ARG (NULL / unaligned pointer, n_members outside
+ * [1, 64], self out of range, timeout <= 0), KV_ERR_CUDA (launch).
+ */
+kv_status kv_group_barrier(uint64_t* const* flags, int32_t n_members, int32_t self, uint64_t target,
+                           int64_t timeout_ns, int32_t* status, void* stream);
 
 /* Make all prior writes of this device (incl. NVLink peer stores) visible
  * system-wide before a host-side barrier: synchronizes `stream`. */

@@ -10,7 +10,13 @@
   every peer's pool, so the reshard kernel of rank g stores directly into the
   destination pools over NVLink 5 / NVSwitch (fused pack + all-to-all-v +
   unpack: no staging buffers, no NCCL data path).
-* switch_barrier: the group completion barrier (a5) after the pushes.
+* DeviceBarrier: the group completion barrier (a5) after the pushes, on the
+  device: per-process 64-bit counters in IPC-shared memory, one per pooled
+  group, advanced by kv_group_barrier (system-scope release adds + acquire
+  spin) -- no host round trip and no collective on the data path.
+* A process may own several consecutive pools ("virtual ranks": the 8
+  engines of a switch mapped onto fewer GPUs); exchange_pools and the
+  barrier work on processes, the plan on pools.
 """
 from __future__ import annotations
 
@@ -91,24 +97,82 @@ class CommunicatorPool:
 
 
 def exchange_pools(local: torch.Tensor, rank: int, world: int, L: int, M: int, group=None):
-    """All-gather IPC handles of every rank's pool [L, nb, M] and map the
-    peers'.  Returns (layer_base [world][L] pointers usable on this device,
-    num_blocks [world], imported [(ptr, offset)] to close later)."""
-    nb = local.shape[1]
+    """All-gather IPC handles of every process's pools and map the peers'.
+    local: [L, nb, M] (one pool per process) or [v, L, nb, M] (v consecutive
+    pools per process: process r owns pools [r*v, (r+1)*v)).  Returns
+    (layer_base [world*v][L] pointers usable on this device, num_blocks
+    [world*v], imported [(ptr, offset)] to close later)."""
+    v = 1 if local.dim() == 3 else int(local.shape[0])
+    nb = int(local.shape[-2])
     handle, off = flykv.ipc_export(local.data_ptr())
-    mine = (handle, off, int(nb), local.data_ptr(), os.getpid())
+    mine = (handle, off, nb, v, local.data_ptr(), os.getpid())
     allv = [None] * world
     dist.all_gather_object(allv, mine, group=group)
     bases, nbs, imported = [], [], []
-    for r, (h, o, n, p, pid) in enumerate(allv):
+    for r, (h, o, n, vr, p, pid) in enumerate(allv):
         if r == rank:
             base = local.data_ptr()
         else:
             base = flykv.ipc_import(h, o)
             imported.append((base, o))
-        bases.append([base + l * n * M for l in range(L)])
-        nbs.append(n)
+        for k in range(vr):
+            pb = base + k * L * n * M
+            bases.append([pb + l * n * M for l in range(L)])
+            nbs.append(n)
     return bases, nbs, imported
+
+
+class DeviceBarrier:
+    """a5 between processes, on the device (kv_group_barrier).
+
+    Each process owns one 128-byte line per barrier key (a tuple of process
+    ranks; keys must be the same list, in the same order, on every process)
+    holding a 64-bit counter, exported through CUDA IPC.  wait(key) enqueues
+    on the stream: add 1 to every member's counter, then spin until this
+    process's counter reaches (barriers on key so far) x members.  Only
+    members call wait(key); the count per key advances identically on every
+    member because switches are planned identically."""
+
+    LINE = 16  # int64 per key: one 128-byte line each
+
+    def __init__(self, rank: int, world: int, keys, device, timeout_s: float = 60.0, group=None):
+        self.rank, self.world = rank, world
+        self.keys = [tuple(k) for k in keys]
+        self.slot = {k: i for i, k in enumerate(self.keys)}
+        self.count = {k: 0 for k in self.keys}
+        self.timeout_ns = int(timeout_s * 1e9)
+        self.local = torch.zeros(max(len(self.keys), 1) * self.LINE, dtype=torch.int64, device=device)
+        self.status = torch.zeros(1, dtype=torch.int32, device=device)
+        torch.cuda.synchronize(device)
+        handle, off = flykv.ipc_export(self.local.data_ptr())
+        allv = [None] * world
+        dist.all_gather_object(allv, (handle, off), group=group)
+        self.bases, self.imported = [], []
+        for r, (h, o) in enumerate(allv):
+            if r == rank:
+                self.bases.append(self.local.data_ptr())
+            else:
+                b = flykv.ipc_import(h, o)
+                self.imported.append((b, o))
+                self.bases.append(b)
+
+    def wait(self, key, stream):
+        key = tuple(key)
+        if self.rank not in key or len(key) < 2:
+            return
+        self.count[key] += 1
+        s = self.slot[key] * self.LINE * 8
+        flykv.kv_group_barrier([self.bases[m] + s for m in key], key.index(self.rank),
+                               self.count[key] * len(key), self.timeout_ns, self.status, stream)
+
+    def check(self):
+        """Raise if any wait timed out (a member never arrived)."""
+        if int(self.status.item()) != 0:
+            raise RuntimeError("kv_group_barrier timed out: a member never arrived")
+
+    def close(self):
+        close_pools(self.imported)
+        self.imported = []
 
 
 def close_pools(imported):
@@ -120,11 +184,9 @@ def close_pools(imported):
 
 
 def switch_barrier(stream, group=None, nccl=True, device=None, members=None, rank=None):
-    """a5: every rank's pushes have landed before anyone remaps / reuses.
-    NCCL: a 1-element all_reduce enqueued on the switch stream after the
-    reshard kernel (device-side; the kernel ends with a system-scope fence).
-    gloo (CPU tests, several ranks sharing one device): stream sync + barrier.
-    Ranks outside `members` (when given) have nothing to wait for."""
+    """Host-side a5 (comparator / debugging only; the product path is
+    DeviceBarrier): NCCL 1-element all_reduce on the switch stream, or stream
+    sync + gloo barrier.  Ranks outside `members` (when given) return."""
     if members is not None and rank not in members:
         return
     if nccl:

@@ -876,9 +876,11 @@ extern "C" kv_status kv_plan_upload(kv_plan* p, void* stream) {
     return ensure_device(p, static_cast<cudaStream_t>(stream));
 }
 
-// Launch arguments of the reshard kernel for the segments sourced on `gpu`
-// (-1: every segment of the plan).
-static ReshardArgs reshard_args(const kv_plan* p, int32_t gpu) {
+// Launch arguments of the reshard kernel for the segments sourced on pools
+// [lo, hi) (every pool: [0, n_gpus)).  Piece space and the mixed slot space
+// are laid out source GPU after source GPU (build_work_order), so a range of
+// pools is one contiguous range of both.
+static ReshardArgs reshard_args(const kv_plan* p, int32_t lo, int32_t hi) {
     const kv_cache* c = p->c;
     ReshardArgs a{};
     a.seg_begin = reinterpret_cast<const int64_t*>(p->dbuf + p->off_seg_begin);
@@ -888,16 +890,15 @@ static ReshardArgs reshard_args(const kv_plan* p, int32_t gpu) {
     a.segs = reinterpret_cast<const Seg*>(p->dbuf + p->off_segs);
     a.tables = reinterpret_cast<const int32_t*>(p->dbuf + p->off_tables);
     a.layer_base = c->d_layer_base;
-    a.seg_lo = gpu < 0 ? 0 : p->gpu_seg_lo[gpu];
-    a.seg_hi = gpu < 0 ? (int32_t)p->seg_of.size() : p->gpu_seg_hi[gpu];
     const int32_t n = c->n_gpus;
-    a.st_lo = gpu < 0 ? 0 : gpu;
-    a.st_hi = gpu < 0 ? n : gpu + 1;
-    a.atom_lo = p->streams[a.st_lo].begin;
-    a.atom_hi = a.st_hi < n ? p->streams[a.st_hi].begin : p->mixed_end;
-    if (gpu < 0) {  // the first GPU with work (the stream search needs streams[st_lo].begin <= slot)
-        while (a.st_lo + 1 < n && p->streams[a.st_lo + 1].begin == a.atom_lo) ++a.st_lo;
-    }
+    a.seg_lo = p->gpu_seg_lo[lo];
+    a.seg_hi = p->gpu_seg_hi[hi - 1];
+    a.st_lo = lo;
+    a.st_hi = hi;
+    a.atom_lo = p->streams[lo].begin;
+    a.atom_hi = hi < n ? p->streams[hi].begin : p->mixed_end;
+    // the first GPU with work (the stream search needs streams[st_lo].begin <= slot)
+    while (a.st_lo + 1 < hi && p->streams[a.st_lo + 1].begin == a.atom_lo) ++a.st_lo;
     for (int32_t g = a.st_lo; g < a.st_hi; ++g) a.mixed |= p->streams[g].nb > 1 ? 1 : 0;
     a.L = c->geo.num_layers;
     a.atom_bytes = (int32_t)c->atom_bytes;
@@ -907,25 +908,38 @@ static ReshardArgs reshard_args(const kv_plan* p, int32_t gpu) {
     return a;
 }
 
-extern "C" kv_status kv_reshard(kv_plan* p, int32_t gpu, void* stream_) {
+static ReshardArgs reshard_args(const kv_plan* p, int32_t gpu) {
+    return gpu < 0 ? reshard_args(p, 0, p->c->n_gpus) : reshard_args(p, gpu, gpu + 1);
+}
+
+extern "C" kv_status kv_reshard_range(kv_plan* p, int32_t gpu_lo, int32_t gpu_hi, void* stream_) {
     if (!p) return fail(KV_ERR_INVALID_ARG, "plan is NULL");
     if (p->state != PLAN_PLANNED)
         return fail(KV_ERR_BAD_STATE, "plan already committed; its source blocks may be reused");
-    if (gpu < -1 || gpu >= p->c->n_gpus) return fail(KV_ERR_INVALID_ARG, "gpu %d out of range", gpu);
+    const int32_t n = p->c->n_gpus;
+    if (gpu_lo < 0 || gpu_hi > n || gpu_lo >= gpu_hi)
+        return fail(KV_ERR_INVALID_ARG, "pool range [%d, %d) is not inside [0, %d)", gpu_lo, gpu_hi, n);
     cudaStream_t stream = static_cast<cudaStream_t>(stream_);
     kv_status s = ensure_device(p, stream);
     if (s) return s;
     p->last_stream = stream;
-    ReshardArgs a = reshard_args(p, gpu);
-    // one GPU's share (one process per GPU): destinations may be peer pools,
-    // released system-wide before the group barrier
-    a.fence_sys = gpu >= 0 ? 1 : 0;
-    a.peer = gpu >= 0 ? 1 : 0;
+    ReshardArgs a = reshard_args(p, gpu_lo, gpu_hi);
+    // a share of the pools (one process per GPU): destinations may be peer
+    // pools, released system-wide before the group barrier
+    const bool part = gpu_lo > 0 || gpu_hi < n;
+    a.fence_sys = part ? 1 : 0;
+    a.peer = part ? 1 : 0;
     if (a.atom_hi <= a.atom_lo) return KV_OK;
     cudaError_t e = launch_reshard(a, p->dev, stream);
     if (e != cudaSuccess) return cuda_fail(e, "flykv_reshard_kernel launch");
     g_launches.fetch_add(1);
     return KV_OK;
+}
+
+extern "C" kv_status kv_reshard(kv_plan* p, int32_t gpu, void* stream_) {
+    if (!p) return fail(KV_ERR_INVALID_ARG, "plan is NULL");
+    if (gpu < -1 || gpu >= p->c->n_gpus) return fail(KV_ERR_INVALID_ARG, "gpu %d out of range", gpu);
+    return gpu < 0 ? kv_reshard_range(p, 0, p->c->n_gpus, stream_) : kv_reshard_range(p, gpu, gpu + 1, stream_);
 }
 
 extern "C" kv_status kv_reshard_staged(kv_plan* p, int32_t gpu, void* staging, int64_t staging_bytes, int32_t mode,
@@ -1688,6 +1702,27 @@ extern "C" kv_status kv_ipc_close(void* dptr, uint64_t offset) {
 
 extern "C" kv_status kv_stream_sync(void* stream) {
     CUDA_TRY(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+    return KV_OK;
+}
+
+extern "C" kv_status kv_group_barrier(uint64_t* const* flags, int32_t n_members, int32_t self, uint64_t target,
+                                      int64_t timeout_ns, int32_t* status, void* stream) {
+    if (!flags || n_members < 1 || n_members > 64 || self < 0 || self >= n_members || timeout_ns <= 0)
+        return fail(KV_ERR_INVALID_ARG, "bad kv_group_barrier arguments (n_members %d, self %d)", n_members, self);
+    BarrierArgs a{};
+    for (int32_t m = 0; m < n_members; ++m) {
+        if (!flags[m]) return fail(KV_ERR_INVALID_ARG, "counter of member %d is NULL", m);
+        if ((uintptr_t)flags[m] & 7) return fail(KV_ERR_INVALID_ARG, "counter of member %d is not 8-byte aligned", m);
+        a.flags[m] = reinterpret_cast<unsigned long long*>(flags[m]);
+    }
+    a.n = n_members;
+    a.self = self;
+    a.target = target;
+    a.timeout_ns = timeout_ns;
+    a.status = status;
+    cudaError_t e = launch_barrier(a, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "flykv_barrier_kernel launch");
+    g_launches.fetch_add(1);
     return KV_OK;
 }
 

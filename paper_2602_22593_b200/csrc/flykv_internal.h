@@ -174,6 +174,16 @@ struct DecodeArgs {
     float scale;
 };
 
+// Group completion barrier (kv_group_barrier): this process's mapping of
+// every member's counter, its own index, the count to wait for.
+struct BarrierArgs {
+    unsigned long long* flags[64];
+    int32_t n, self;
+    uint64_t target;
+    int64_t timeout_ns;
+    int32_t* status;
+};
+
 // Kernel launchers (flykv_kernels.cu, flykv_decode.cu).  Return cudaSuccess or the launch error.
 cudaError_t launch_reshard(const ReshardArgs& a, int device, cudaStream_t s);
 void set_reshard_impl(int impl, int ctas_per_sm);
@@ -181,5 +191,6 @@ cudaError_t launch_remap(const RemapArgs& a, int n_ctas, cudaStream_t s);
 cudaError_t launch_gather(const GatherSeg* segs, int n_seg, char* dst, cudaStream_t s);
 cudaError_t launch_decode(const DecodeArgs& a, cudaStream_t s);
 cudaError_t launch_unpack(const UnpackArgs& a, int device, cudaStream_t s);
+cudaError_t launch_barrier(const BarrierArgs& a, cudaStream_t s);
 
 }  // namespace flykv

@@ -801,6 +801,44 @@ cudaError_t launch_remap(const RemapArgs& a, int n_ctas, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- barrier
+// a5, group completion barrier between processes (one per GPU, "safe
+// points"): one thread.  Every earlier kernel of this stream (the reshard,
+// whose peer stores end with a system-scope fence) has completed; the
+// sequentially consistent system fence orders them before the arrivals.
+// Arrive: a system-scope release add of 1 to every member's counter
+// (including this process's own).  Wait: acquire loads of the own counter
+// until it reaches `target` = (barriers so far on this counter) x members:
+// every member then has arrived (each adds exactly once per barrier and
+// none can pass barrier k+1 before all have arrived at it).  A member that
+// never arrives ends the wait after timeout_ns (%globaltimer): *status = 1
+// if status is given, else the kernel traps (a loud CUDA error, never a hang).
+__global__ void flykv_barrier_kernel(const BarrierArgs a) {
+    asm volatile("fence.sc.sys;" ::: "memory");
+    for (int m = 0; m < a.n; ++m)
+        asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(a.flags[m]) : "memory");
+    uint64_t t0, t, v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (true) {
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(a.flags[a.self]) : "memory");
+        if (v >= a.target) break;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if ((int64_t)(t - t0) > a.timeout_ns) {
+            if (a.status) {
+                *a.status = 1;
+                return;
+            }
+            __trap();
+        }
+        __nanosleep(200);
+    }
+}
+
+cudaError_t launch_barrier(const BarrierArgs& a, cudaStream_t s) {
+    flykv_barrier_kernel<<<1, 1, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- gather
 struct GatherArgs {
     GatherSeg seg[3];

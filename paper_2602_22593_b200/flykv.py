@@ -118,6 +118,8 @@ _sig("kv_held_mask", C.c_int, _P, C.c_int32, C.POINTER(C.c_uint8))
 _sig("kv_plan_switch", C.c_int, _P, C.POINTER(Request), C.c_int32, C.POINTER(_P))
 _sig("kv_plan_upload", C.c_int, _P, _P)
 _sig("kv_reshard", C.c_int, _P, C.c_int32, _P)
+_sig("kv_reshard_range", C.c_int, _P, C.c_int32, C.c_int32, _P)
+_sig("kv_group_barrier", C.c_int, C.POINTER(C.c_void_p), C.c_int32, C.c_int32, C.c_uint64, C.c_int64, _P, _P)
 _sig("kv_plan_resident", C.c_int, _P, C.c_int32, _I32P, _I32P)
 _sig("kv_reshard_staged", C.c_int, _P, C.c_int32, _P, C.c_int64, C.c_int32, _P)
 _sig("kv_remap_block_tables", C.c_int, _P, C.c_int32, _P, _P, _P, _P)
@@ -163,13 +165,13 @@ _sig("kv_cache_set_work_order", C.c_int, _P, C.c_int32)
 _sig("kv_plan_work_order", C.c_int, _P, C.c_int32, _I32P, _I64P)
 
 EXPORTED = ["kv_cache_create", "kv_cache_destroy", "kv_layout", "kv_blocks_for", "kv_alloc", "kv_reserve",
-            "kv_free", "kv_free_count", "kv_held_mask", "kv_plan_switch", "kv_plan_upload", "kv_reshard", "kv_reshard_staged",
+            "kv_free", "kv_free_count", "kv_held_mask", "kv_plan_switch", "kv_plan_upload", "kv_reshard", "kv_reshard_range", "kv_reshard_staged",
             "kv_pack", "kv_unpack", "kv_switch", "kv_switch_back", "kv_switch_multi", "kv_switch_waves", "kv_plan_tables", "kv_plan_resident",
             "kv_remap_block_tables", "kv_plan_dst_tables", "kv_plan_commit", "kv_plan_waves", "kv_plan_pieces",
             "kv_suggest_rank_ids", "kv_plan_get_stats", "kv_plan_destroy",
             "weight_shard_view", "kv_gather_view", "kv_vmm_granularity", "kv_vmm_alloc", "kv_vmm_free",
             "weight_view_alias", "weight_view_unalias", "kv_paged_decode", "kv_ipc_export", "kv_ipc_import", "kv_ipc_close",
-            "kv_stream_sync", "kv_strerror", "kv_last_error", "kv_launch_count", "kv_set_reshard_impl",
+            "kv_group_barrier", "kv_stream_sync", "kv_strerror", "kv_last_error", "kv_launch_count", "kv_set_reshard_impl",
             "kv_cache_set_work_order", "kv_plan_work_order"]
 
 
@@ -585,6 +587,11 @@ def kv_reshard(plan: Plan, gpu: int = -1, stream=None):
     _check(_lib.kv_reshard(plan._h, gpu, stream_of(stream)))
 
 
+def kv_reshard_range(plan: Plan, gpu_lo: int, gpu_hi: int, stream=None):
+    """kv_reshard of the atoms sourced on pools [gpu_lo, gpu_hi), one launch."""
+    _check(_lib.kv_reshard_range(plan._h, gpu_lo, gpu_hi, stream_of(stream)))
+
+
 def kv_reshard_staged(plan: Plan, gpu: int, staging, staging_bytes: int, mode: int, stream=None):
     """Bench comparator: mode 1 pack -> staging, mode 2 unpack staging -> destinations."""
     _check(_lib.kv_reshard_staged(plan._h, gpu, ptr_of(staging), int(staging_bytes), mode, stream_of(stream)))
@@ -699,6 +706,14 @@ def ipc_import(handle: bytes, offset: int) -> int:
 
 def ipc_close(dptr: int, offset: int):
     _check(_lib.kv_ipc_close(dptr, offset))
+
+
+def kv_group_barrier(flags, self_index: int, target: int, timeout_ns: int, status=None, stream=None):
+    """Device-side group barrier (a5): flags = this process's pointers to
+    every member's 64-bit counter; waits for counter[self] >= target."""
+    arr = (C.c_void_p * len(flags))(*[ptr_of(f) for f in flags])
+    _check(_lib.kv_group_barrier(arr, len(flags), self_index, int(target), int(timeout_ns), ptr_of(status),
+                                 stream_of(stream)))
 
 
 def stream_sync(stream=None):

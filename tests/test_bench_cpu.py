@@ -73,3 +73,48 @@ def test_bench_has_no_undefined_names():
                 bound.add(node.name)
         loaded = {n.id for n in ast.walk(tree) if isinstance(n, ast.Name) and isinstance(n.ctx, ast.Load)}
         assert loaded <= bound, f"{path}: undefined {sorted(loaded - bound)}"
+
+
+def test_gpus_n_self_launches_n_ranks():
+    """bench.py --gpus 2 outside torchrun re-runs itself under
+    torch.distributed.run with 2 ranks (the multi-rank path): the reference
+    arm's line, printed by rank 0 alone, reports n_gpus = 2."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--config", "tiny", "--gpus", "2",
+                        "--steps", "1", "--warmup", "1"], cwd=ROOT, env=env, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["impl"] == "reference"
+
+
+def test_main_dispatch(monkeypatch):
+    """--gpus N > 1 without WORLD_SIZE -> self_launch; under torchrun
+    (WORLD_SIZE > 1) -> run_multi; otherwise run_single.  Default workload:
+    the north_star headline c4 (Llama-3-70B 8 x DP1 -> TP8)."""
+    calls = []
+    monkeypatch.setattr(bench, "self_launch", lambda a: calls.append(("self", a.gpus)) or 0)
+    monkeypatch.setattr(bench, "run_multi", lambda a: calls.append(("multi", a.gpus)) or 0)
+    monkeypatch.setattr(bench, "run_single", lambda a: calls.append(("single", a.config)) or 0)
+    for k in ("WORLD_SIZE", "RANK"):
+        monkeypatch.delenv(k, raising=False)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4"])
+    bench.main()
+    monkeypatch.setenv("WORLD_SIZE", "4")
+    monkeypatch.setenv("RANK", "0")
+    bench.main()
+    monkeypatch.delenv("WORLD_SIZE")
+    monkeypatch.setattr(sys, "argv", ["bench.py"])
+    bench.main()
+    assert calls == [("self", 4), ("multi", 4), ("single", "c4")]
+
+
+def test_process_matrix_of_virtual_ranks():
+    """8 engines on 2 GPUs (4 virtual ranks each): bytes between pools of one
+    process stay in its HBM; the rest crosses NVLink."""
+    m = np.arange(64, dtype=np.float64).reshape(8, 8)
+    pm = bench.proc_matrix(m, 4)
+    assert pm.shape == (2, 2) and pm.sum() == m.sum()
+    assert pm[0, 1] == m[:4, 4:].sum() and pm[1, 0] == m[4:, :4].sum()

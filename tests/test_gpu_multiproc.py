@@ -1,8 +1,11 @@
-"""One process per pool, peer pools mapped through CUDA IPC, each rank's
-reshard kernel pushing its atoms into the other ranks' pools (the N-GPU launch
-shape).  On a 1-GPU box both processes share cuda:0 (CUDA IPC between two
-processes on one device) and gloo carries the barrier; the data path is the
-same P2P-store kernel.  Whole pools are compared with the oracle."""
+"""One process per GPU, peer pools mapped through CUDA IPC, each process's
+reshard kernel pushing its atoms into the other processes' pools (the N-GPU
+launch shape), then the device-side group barrier (kv_group_barrier over
+IPC-shared counters: no host barrier on the data path), then the remap.  A
+process may own several consecutive pools (virtual ranks, kv_reshard_range).
+On a 1-GPU box the processes share cuda:0 (CUDA IPC between processes on one
+device); gloo carries only the setup (handle exchange) and the test's file
+hand-off.  Whole pools are compared with the oracle."""
 import os
 import socket
 import tempfile
@@ -28,10 +31,11 @@ def _free_port():
     return p
 
 
-def _workload(world, kind="dp_tp"):
+def _workload(world, kind="dp_tp", v=1):
     """dp_tp: DP_N -> TP_N merge; tp_dp: the split back (round-robin engines);
     gqa: H_kv=2 < N (replication, TP_N > kv_heads); tp_tp: TP2 pairs -> TP_N."""
     L, H, d, B, _ = GEOS[kind]
+    world = world * v   # pools
     w = synth.dp_to_tp(world, 6 * world, L=L, H=H, d=d, B=B, lo=1, hi=700, seed=4)
     if kind == "tp_dp":
         w = synth.Workload(w.name, L, H, d, B, 2, world, w.T, list(w.dst), list(w.src))
@@ -41,7 +45,7 @@ def _workload(world, kind="dp_tp"):
     return w
 
 
-def _rank(rank, world, port, outdir, kind, mode="push"):
+def _rank(rank, world, port, outdir, kind, mode="push", v=1):
     import torch
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -50,24 +54,27 @@ def _rank(rank, world, port, outdir, kind, mode="push"):
     try:
         from paper_2602_22593_b200 import comm
         from paper_2602_22593_b200 import flykv as F
-        w = _workload(world, kind)
+        w = _workload(world, kind, v)
         g = F.geometry(*GEOS[kind])
         _, _, M = F.kv_layout(g, 1)
         n0 = [F.kv_blocks_for(g, T, s[1]) for T, s in zip(w.T, w.src)]
         n1 = [F.kv_blocks_for(g, T, d[1]) for T, d in zip(w.T, w.dst)]
         nb, tabs = synth.realistic_pools(w, n0, n1)
-        pool = torch.empty((w.L, nb[rank], M), dtype=torch.uint8, device="cuda:0")
-        synth.fill_hash_torch(pool, rank)
+        mine = range(rank * v, (rank + 1) * v)   # the pools this process owns
+        pool = torch.empty((v, w.L, nb[rank], M), dtype=torch.uint8, device="cuda:0")
+        for k, gp in enumerate(mine):
+            synth.fill_hash_torch(pool[k], gp)
         if w.src[0][1] > w.H:  # GQA replicated sources: replicas identical (R10)
             raise RuntimeError("replicated sources not used here")
         torch.cuda.synchronize()
         if mode == "a2a":  # no peer mappings: other pools' addresses are never dereferenced
-            bases = [[pool[l].data_ptr() if r == rank else (1 << 44) + (r << 36) + (l << 30) for l in range(w.L)]
+            bases = [[pool[0, l].data_ptr() if r == rank else (1 << 44) + (r << 36) + (l << 30) for l in range(w.L)]
                      for r in range(world)]
             nbs, imported = nb, []
         else:
             bases, nbs, imported = comm.exchange_pools(pool, rank, world, w.L, M)
-        cache = F.KVCache(g, nbs, bases, [p for p in (2, 4, 8) if p <= world])
+        cache = F.KVCache(g, nbs, bases, [p for p in (2, 4, 8) if p <= world * v])
+        barrier = comm.DeviceBarrier(rank, world, [tuple(range(world))], "cuda:0", timeout_s=60)
         for s_, ids in zip(w.src, tabs):
             cache.reserve(s_, ids)
         stream = torch.cuda.Stream()
@@ -85,36 +92,50 @@ def _rank(rank, world, port, outdir, kind, mode="push"):
             recv = recv_h.to("cuda:0") if recv_h.numel() else torch.empty(16, dtype=torch.uint8, device="cuda:0")
             F.kv_unpack(plan, rank, recv, recv_off[rank], stream)
         else:
-            F.kv_reshard(plan, rank, stream)
-        comm.switch_barrier(stream, None, nccl=False)
-        n_res, n_ids = plan.resident(rank)
-        rp = torch.empty(n_res + 1, dtype=torch.int32, device="cuda:0")
-        ids = torch.empty(max(n_ids, 1), dtype=torch.int32, device="cuda:0")
-        meta = torch.empty((max(n_res, 1), 4), dtype=torch.int32, device="cuda:0")
-        F.kv_remap_block_tables(plan, rank, rp, ids, meta, stream)
+            F.kv_reshard_range(plan, mine.start, mine.stop, stream)
+        # a5 on the device: every process's pushes have landed before anyone remaps
+        barrier.wait(tuple(range(world)), stream)
+        out = {}
+        for gp in mine:
+            n_res, n_ids = plan.resident(gp)
+            rp = torch.empty(n_res + 1, dtype=torch.int32, device="cuda:0")
+            ids = torch.empty(max(n_ids, 1), dtype=torch.int32, device="cuda:0")
+            meta = torch.empty((max(n_res, 1), 4), dtype=torch.int32, device="cuda:0")
+            F.kv_remap_block_tables(plan, gp, rp, ids, meta, stream)
+            out[gp] = (rp, ids[:n_ids], meta[:n_res])
+        # a second barrier on the same counters: nobody reads pools before every
+        # process's remap (the test's own hand-off; counts advance to 2 x world)
+        barrier.wait(tuple(range(world)), stream)
         stream.synchronize()
+        barrier.check()
+        for k, gp in enumerate(mine):
+            np.save(os.path.join(outdir, f"pool{gp}.npy"), pool[k].cpu().numpy().reshape(-1))
+            rp, ids, meta = out[gp]
+            np.save(os.path.join(outdir, f"rp{gp}.npy"), rp.cpu().numpy())
+            np.save(os.path.join(outdir, f"ids{gp}.npy"), ids.cpu().numpy())
+            np.save(os.path.join(outdir, f"meta{gp}.npy"), meta.cpu().numpy())
         dist.barrier()
-        np.save(os.path.join(outdir, f"pool{rank}.npy"), pool.cpu().numpy().reshape(-1))
-        np.save(os.path.join(outdir, f"rp{rank}.npy"), rp.cpu().numpy())
-        np.save(os.path.join(outdir, f"ids{rank}.npy"), ids[:n_ids].cpu().numpy())
-        np.save(os.path.join(outdir, f"meta{rank}.npy"), meta[:n_res].cpu().numpy())
-        dist.barrier()
+        barrier.close()
         comm.close_pools(imported)
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,kind,mode", [(2, "dp_tp", "push"), (4, "dp_tp", "push"), (4, "tp_dp", "push"),
-                                             (4, "gqa", "push"), (4, "tp_tp", "push"),
-                                             (2, "dp_tp", "a2a"), (4, "tp_dp", "a2a"), (4, "gqa", "a2a"),
-                                             (4, "tp_tp", "a2a"), (8, "dp_tp", "push"), (8, "gqa", "push"),
-                                             (8, "tp_tp", "a2a")])
-def test_ipc_push_matches_oracle(world, kind, mode):
-    """push: every rank's reshard kernel stores into peer pools (CUDA IPC).
+@pytest.mark.parametrize("world,kind,mode,v", [(2, "dp_tp", "push", 1), (4, "dp_tp", "push", 1),
+                                               (4, "tp_dp", "push", 1), (4, "gqa", "push", 1),
+                                               (4, "tp_tp", "push", 1), (2, "dp_tp", "a2a", 1),
+                                               (4, "tp_dp", "a2a", 1), (4, "gqa", "a2a", 1),
+                                               (4, "tp_tp", "a2a", 1), (8, "dp_tp", "push", 1),
+                                               (8, "gqa", "push", 1), (8, "tp_tp", "a2a", 1),
+                                               (2, "dp_tp", "push", 4), (4, "dp_tp", "push", 2),
+                                               (2, "tp_dp", "push", 2), (2, "gqa", "push", 4)])
+def test_ipc_push_matches_oracle(world, kind, mode, v):
+    """push: every process's reshard kernel (kv_reshard_range over the v
+    pools it owns) stores into peer pools (CUDA IPC), then kv_group_barrier.
     a2a: kv_pack into per-destination chunks, all_to_all_single (gloo over
     host copies here; NCCL on GPUs), kv_unpack -- no peer mappings at all."""
     import torch.multiprocessing as mp
-    w = _workload(world, kind)
+    w = _workload(world, kind, v)
     og = O.Geom(*GEOS[kind])
     n0 = [O.num_blocks(og, T, s[1]) for T, s in zip(w.T, w.src)]
     n1 = [O.num_blocks(og, T, d[1]) for T, d in zip(w.T, w.dst)]
@@ -122,7 +143,7 @@ def test_ipc_push_matches_oracle(world, kind, mode):
     with tempfile.TemporaryDirectory() as td:
         ctx = mp.get_context("spawn")
         port = _free_port()
-        procs = [ctx.Process(target=_rank, args=(r, world, port, td, kind, mode)) for r in range(world)]
+        procs = [ctx.Process(target=_rank, args=(r, world, port, td, kind, mode, v)) for r in range(world)]
         for p in procs:
             p.start()
         for p in procs:
@@ -130,7 +151,7 @@ def test_ipc_push_matches_oracle(world, kind, mode):
             assert p.exitcode == 0
         M = O.block_bytes(og)
         pools = []
-        for r in range(world):
+        for r in range(world * v):
             a = np.zeros(og.L * nb[r] * M, dtype=np.uint8)
             synth.fill_hash_np(a, r)
             pools.append(a)
@@ -142,7 +163,7 @@ def test_ipc_push_matches_oracle(world, kind, mode):
             oreqs.append(O.Req(T, s, list(ids), d))
         st, otabs = O.switch(og, pools, held, oreqs)
         assert st == 0
-        for r in range(world):
+        for r in range(world * v):
             got = np.load(os.path.join(td, f"pool{r}.npy"))
             assert np.array_equal(got, pools[r]), f"rank {r} pool differs"
             rp, ids, meta = O.tables(og, r, oreqs, otabs)
