@@ -46,7 +46,8 @@ typedef enum {
     KV_ERR_BAD_BLOCK_TABLE = 7,    /* wrong length, out of range, not held, or shared (R14) */
     KV_ERR_DUPLICATE_REQUEST = 8,  /* same req_id twice in one plan (S:207 DoubleAllocate) */
     KV_ERR_BAD_STATE = 9,          /* call out of order (e.g. reshard after commit)    */
-    KV_ERR_CUDA = 10               /* a CUDA runtime call failed; see kv_last_error()  */
+    KV_ERR_CUDA = 10,              /* a CUDA runtime call failed; see kv_last_error()  */
+    KV_ERR_REPLICA_MISMATCH = 11   /* strict mode: replicated source heads differ (R10) */
 } kv_status;
 
 /* Model KV geometry.  block_base = B (DP tokens per block).  Requirement:
@@ -133,6 +134,11 @@ typedef struct {
 kv_status kv_cache_create(const kv_geometry* geom, int32_t n_gpus, const int32_t* num_blocks,
                           void* const* layer_base, const int32_t* tp_degrees, int32_t n_degrees,
                           kv_cache** out);
+/* Destroy a cache.  Plans of the cache that are still alive are detached:
+ * their device workspaces and tables are released here (after their last
+ * stream drains), and every later call on them returns KV_ERR_BAD_STATE
+ * except kv_plan_destroy (which then frees the handle), kv_plan_get_stats
+ * and kv_plan_dst_tables.  Destroy plans first to keep their tables. */
 void kv_cache_destroy(kv_cache* cache);
 
 /* Layout helpers (Eq.2/Eq.3): *h_loc = H_loc(p), *block_tokens = B(p),
@@ -325,8 +331,12 @@ kv_status kv_switch_back(kv_cache* cache, const kv_plan* prev, void* stream, kv_
  *   plans     host [n_waves] out: one committed plan per wave, tables as for
  *             kv_switch (kv_plan_tables); entries stay NULL past a failure,
  *             the caller destroys the non-NULL ones.
- * Errors: as kv_plan_switch / kv_switch for the failing wave (the earlier
- * waves have committed and completed). */
+ * Errors: as kv_plan_switch / kv_switch for the failing wave.  The earlier
+ * waves have committed (their sources are released) and completed, and
+ * their tables have been read back: plans[0..w-1] are the caller's only
+ * record of where those requests now live -- keep them.  plans[w] is set
+ * if the failing wave committed before its error (its host tables are then
+ * unavailable: kv_plan_tables(on_device = 0) returns BAD_STATE). */
 kv_status kv_switch_multi(kv_cache* cache, const kv_request* reqs, const int32_t* wave_ptr, int32_t n_waves,
                           void* stream, kv_plan** plans);
 
@@ -334,7 +344,8 @@ kv_status kv_switch_multi(kv_cache* cache, const kv_request* reqs, const int32_t
  * as pointers into plan-owned memory (valid until kv_plan_destroy):
  * on_device != 0 -> device pointers, else host pointers.  Layout as written
  * by kv_remap_block_tables (sizes from kv_plan_resident).  BAD_STATE if the
- * plan was not executed by kv_switch. */
+ * plan was not executed by kv_switch, or (host pointers) if its switch did
+ * not complete the read-back. */
 kv_status kv_plan_tables(const kv_plan* plan, int32_t gpu, int32_t on_device, const int32_t** req_ptr,
                          const int32_t** block_ids, const int32_t** per_req_meta);
 
@@ -352,7 +363,8 @@ kv_status kv_plan_commit(kv_plan* plan);
  * sources, and (if max_wave_bytes > 0) moves at most max_wave_bytes of
  * destination payload unless a single request exceeds it.  Simulates the
  * allocator; no state change.  wave_start: host [n_reqs + 1], wave k is
- * reqs[wave_start[k] .. wave_start[k+1]); *n_waves >= 1.  OUT_OF_BLOCKS if a
+ * reqs[wave_start[k] .. wave_start[k+1]); *n_waves >= 1 (0 for an empty list,
+ * with only wave_start[0] = 0 written).  OUT_OF_BLOCKS if a
  * request does not fit even alone.  The caller then runs, per wave:
  * kv_plan_switch -> kv_reshard -> barrier -> kv_remap_block_tables.
  */
@@ -424,7 +436,7 @@ kv_status kv_plan_get_stats(const kv_plan* plan, kv_plan_stats* stats, int64_t* 
  * Errors: KV_ERR_INVALID_ARG (NULL plan / n_rows, gpu out of range). */
 kv_status kv_plan_work_order(const kv_plan* plan, int32_t gpu, int32_t* n_rows, int64_t* out);
 /* Destroy a plan.  A plan that was never committed rolls back its
- * destination allocations. */
+ * destination allocations.  Safe on a plan detached by kv_cache_destroy. */
 void kv_plan_destroy(kv_plan* plan);
 
 /* ------------------------------------------------------- weight views */
@@ -576,6 +588,35 @@ const char* kv_last_error(void);
  * Errors: KV_ERR_INVALID_ARG (NULL cache, order not 0/1).  DESIGN.md 8.
  */
 kv_status kv_cache_set_work_order(kv_cache* cache, int32_t order);
+
+/*
+ * Strict replica mode (R10).  A source group of degree p0 > H holds each
+ * head on p0/H ranks (Eq.3 replication); the re-layout reads the
+ * lowest-owner replica only (canonical source, R10), so a corrupted replica
+ * would go unnoticed -- or a corrupted canonical one would be propagated.
+ *
+ * kv_verify_replicas: enqueue on `stream` a kernel comparing, for every
+ * moving request of the plan with p0 > H, every valid token (t < T) of
+ * every layer, K/V half and head in each non-canonical replica with the
+ * canonical replica; then one device->host copy and a stream sync.
+ *   mismatches  host out: atoms (request, layer, K/V, head, B-token chunk,
+ *               replica) with at least one differing valid byte
+ *   first       host out (may be NULL): the smallest mismatch code,
+ *               ((item * 2L + 2l + kv) << 32) | chunk, item = position in
+ *               (request, head, replica >= 1) order; UINT64_MAX if none
+ * Pools must be addressable from the current device.  Tail slots past T in
+ * the last chunk are not compared (stale, R9).  Errors: INVALID_ARG,
+ * BAD_STATE (committed or detached plan), KV_ERR_CUDA.
+ *
+ * kv_cache_set_strict(cache, 1): kv_switch / kv_switch_multi /
+ * kv_switch_waves / kv_switch_back verify every plan first (after its
+ * upload, before its reshard) and, on a mismatch, roll the plan back (no
+ * state change, no byte moved) and return KV_ERR_REPLICA_MISMATCH.  Costs
+ * one read of every replicated source byte and a host sync per plan with
+ * replicated sources.  Default 0 (off).
+ */
+kv_status kv_verify_replicas(kv_plan* plan, void* stream, int64_t* mismatches, uint64_t* first);
+kv_status kv_cache_set_strict(kv_cache* cache, int32_t strict);
 
 /* Tuning knob for the reshard kernel (process-wide): impl 0 = default
  * (LDG/STG warp copy, two atoms in flight per warp for 2/4 KiB atoms), 1 =

@@ -74,16 +74,24 @@ struct kv_cache {
     // synchronizations (release threshold = max) so a switch never waits on
     // the driver re-mapping freed workspace memory
     cudaMemPool_t pool = nullptr;
-    // pinned staging for descriptor uploads, guarded by an event
-    void* stage = nullptr;
-    size_t stage_bytes = 0;
-    cudaEvent_t stage_ev = nullptr;
-    bool stage_pending = false;
+    // pinned staging for descriptor uploads: a ring of kStageRing buffers,
+    // each guarded by an event, so planning wave w+1 never waits for the
+    // upload of wave w (queued behind wave w-1's kernels) to be consumed
+    static constexpr int kStageRing = 4;
+    void* stage[kStageRing] = {};
+    size_t stage_bytes[kStageRing] = {};
+    cudaEvent_t stage_ev[kStageRing] = {};
+    bool stage_pending[kStageRing] = {};
+    int stage_next = 0;
+    // plans not yet destroyed: kv_cache_destroy detaches them
+    std::unordered_set<kv_plan*> live;
     // pinned landing buffer of kv_switch's one device->host table copy
     void* back = nullptr;
     size_t back_bytes = 0;
     // kernel work order of new plans: 1 = destination-rotated (default), 0 = plan order
     int32_t work_order = 1;
+    // strict replica mode (kv_cache_set_strict, R10)
+    int32_t strict = 0;
 };
 
 struct ReqPlan {
@@ -98,6 +106,14 @@ struct ReqPlan {
 };
 
 enum { PLAN_PLANNED = 0, PLAN_COMMITTED = 1 };
+
+// A plan whose cache was destroyed (p->c == nullptr): every call but
+// kv_plan_destroy / kv_plan_get_stats / kv_plan_dst_tables returns BAD_STATE.
+#define PLAN_CHECK(p)                                                                         \
+    do {                                                                                      \
+        if (!(p)) return fail(KV_ERR_INVALID_ARG, "plan is NULL");                             \
+        if (!(p)->c) return fail(KV_ERR_BAD_STATE, "the plan's cache was destroyed");          \
+    } while (0)
 
 struct kv_plan {
     kv_cache* c = nullptr;
@@ -256,11 +272,25 @@ extern "C" kv_status kv_cache_create(const kv_geometry* geom, int32_t n_gpus, co
 
 extern "C" void kv_cache_destroy(kv_cache* c) {
     if (!c) return;
-    if (c->stage_ev) {
-        cudaEventSynchronize(c->stage_ev);
-        cudaEventDestroy(c->stage_ev);
+    // detach live plans: release their device workspaces (from this cache's
+    // pool) now; the caller still owns the handles, and kv_plan_destroy on a
+    // detached plan only frees its host memory
+    for (kv_plan* p : c->live) {
+        if (p->dbuf) cudaFreeAsync(p->dbuf, p->last_stream);
+        if (p->d_out) cudaFreeAsync(p->d_out, p->last_stream);
+        if (p->dbuf || p->d_out) cudaStreamSynchronize(p->last_stream);
+        p->dbuf = nullptr;
+        p->d_out = nullptr;
+        p->c = nullptr;
     }
-    if (c->stage) cudaFreeHost(c->stage);
+    c->live.clear();
+    for (int k = 0; k < kv_cache::kStageRing; ++k) {
+        if (c->stage_ev[k]) {
+            cudaEventSynchronize(c->stage_ev[k]);
+            cudaEventDestroy(c->stage_ev[k]);
+        }
+        if (c->stage[k]) cudaFreeHost(c->stage[k]);
+    }
     if (c->back) cudaFreeHost(c->back);
     if (c->d_layer_base) cudaFree(c->d_layer_base);
     if (c->pool) cudaMemPoolDestroy(c->pool);
@@ -744,6 +774,12 @@ static void layout_workspace(kv_plan* p) {
     p->dbytes = align(p->off_items + p->items.size() * sizeof(A2AItem));
 }
 
+extern "C" kv_status kv_cache_set_strict(kv_cache* c, int32_t strict) {
+    if (!c || (strict != 0 && strict != 1)) return fail(KV_ERR_INVALID_ARG, "bad kv_cache_set_strict arguments");
+    c->strict = strict;
+    return KV_OK;
+}
+
 extern "C" kv_status kv_cache_set_work_order(kv_cache* c, int32_t order) {
     if (!c || (order != 0 && order != 1)) return fail(KV_ERR_INVALID_ARG, "bad kv_cache_set_work_order arguments");
     c->work_order = order;
@@ -804,6 +840,7 @@ extern "C" kv_status kv_plan_switch(kv_cache* c, const kv_request* reqs, int32_t
     }
     build_remap_records(p, rid_off);
     layout_workspace(p);
+    c->live.insert(p);
     p->st.atom_bytes = c->atom_bytes;
     p->st.payload_bytes = p->st.n_atom_writes * c->atom_bytes;
     p->st.h2d_bytes = (int64_t)p->dbytes;
@@ -837,21 +874,25 @@ static kv_status ensure_device(kv_plan* p, cudaStream_t stream) {
         if (p->dev != dev) return fail(KV_ERR_BAD_STATE, "plan was uploaded to device %d, current is %d", p->dev, dev);
         return KV_OK;
     }
-    // pinned staging buffer shared by the cache's plans, reused once the
-    // previous upload has been consumed by the copy engine
-    if (!c->stage_ev) CUDA_TRY(cudaEventCreateWithFlags(&c->stage_ev, cudaEventDisableTiming));
-    if (c->stage_pending) {
-        CUDA_TRY(cudaEventSynchronize(c->stage_ev));
-        c->stage_pending = false;
+    // pinned staging from the cache's ring; a slot is reused once its
+    // previous upload has been consumed by the copy engine (kStageRing
+    // uploads may be in flight, e.g. the waves of kv_switch_multi)
+    const int k = c->stage_next;
+    c->stage_next = (k + 1) % kv_cache::kStageRing;
+    if (!c->stage_ev[k]) CUDA_TRY(cudaEventCreateWithFlags(&c->stage_ev[k], cudaEventDisableTiming));
+    if (c->stage_pending[k]) {
+        CUDA_TRY(cudaEventSynchronize(c->stage_ev[k]));
+        c->stage_pending[k] = false;
     }
-    if (c->stage_bytes < p->dbytes) {
-        if (c->stage) cudaFreeHost(c->stage);
-        c->stage = nullptr;
+    if (c->stage_bytes[k] < p->dbytes) {
+        if (c->stage[k]) cudaFreeHost(c->stage[k]);
+        c->stage[k] = nullptr;
+        c->stage_bytes[k] = 0;
         size_t want = std::max(p->dbytes, (size_t)1 << 20);
-        CUDA_TRY(cudaMallocHost(&c->stage, want));
-        c->stage_bytes = want;
+        CUDA_TRY(cudaMallocHost(&c->stage[k], want));
+        c->stage_bytes[k] = want;
     }
-    char* h = static_cast<char*>(c->stage);
+    char* h = static_cast<char*>(c->stage[k]);
     std::memcpy(h + p->off_seg_begin, p->seg_begin.data(), p->seg_begin.size() * sizeof(int64_t));
     if (!p->seg_of.empty()) std::memcpy(h + p->off_seg_of, p->seg_of.data(), p->seg_of.size() * sizeof(int32_t));
     if (!p->streams.empty()) std::memcpy(h + p->off_streams, p->streams.data(), p->streams.size() * sizeof(MixStream));
@@ -864,15 +905,15 @@ static kv_status ensure_device(kv_plan* p, cudaStream_t stream) {
     if (!p->items.empty()) std::memcpy(h + p->off_items, p->items.data(), p->items.size() * sizeof(A2AItem));
     CUDA_TRY(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&p->dbuf), p->dbytes, c->pool, stream));
     CUDA_TRY(cudaMemcpyAsync(p->dbuf, h, p->dbytes, cudaMemcpyHostToDevice, stream));
-    CUDA_TRY(cudaEventRecord(c->stage_ev, stream));
-    c->stage_pending = true;
+    CUDA_TRY(cudaEventRecord(c->stage_ev[k], stream));
+    c->stage_pending[k] = true;
     p->dev = dev;
     p->last_stream = stream;
     return KV_OK;
 }
 
 extern "C" kv_status kv_plan_upload(kv_plan* p, void* stream) {
-    if (!p) return fail(KV_ERR_INVALID_ARG, "plan is NULL");
+    PLAN_CHECK(p);
     return ensure_device(p, static_cast<cudaStream_t>(stream));
 }
 
@@ -913,7 +954,7 @@ static ReshardArgs reshard_args(const kv_plan* p, int32_t gpu) {
 }
 
 extern "C" kv_status kv_reshard_range(kv_plan* p, int32_t gpu_lo, int32_t gpu_hi, void* stream_) {
-    if (!p) return fail(KV_ERR_INVALID_ARG, "plan is NULL");
+    PLAN_CHECK(p);
     if (p->state != PLAN_PLANNED)
         return fail(KV_ERR_BAD_STATE, "plan already committed; its source blocks may be reused");
     const int32_t n = p->c->n_gpus;
@@ -937,14 +978,15 @@ extern "C" kv_status kv_reshard_range(kv_plan* p, int32_t gpu_lo, int32_t gpu_hi
 }
 
 extern "C" kv_status kv_reshard(kv_plan* p, int32_t gpu, void* stream_) {
-    if (!p) return fail(KV_ERR_INVALID_ARG, "plan is NULL");
+    PLAN_CHECK(p);
     if (gpu < -1 || gpu >= p->c->n_gpus) return fail(KV_ERR_INVALID_ARG, "gpu %d out of range", gpu);
     return gpu < 0 ? kv_reshard_range(p, 0, p->c->n_gpus, stream_) : kv_reshard_range(p, gpu, gpu + 1, stream_);
 }
 
 extern "C" kv_status kv_reshard_staged(kv_plan* p, int32_t gpu, void* staging, int64_t staging_bytes, int32_t mode,
                                        void* stream_) {
-    if (!p || !staging || (mode != 1 && mode != 2)) return fail(KV_ERR_INVALID_ARG, "bad kv_reshard_staged arguments");
+    PLAN_CHECK(p);
+    if (!staging || (mode != 1 && mode != 2)) return fail(KV_ERR_INVALID_ARG, "bad kv_reshard_staged arguments");
     if (p->state != PLAN_PLANNED) return fail(KV_ERR_BAD_STATE, "plan already committed");
     if (gpu < -1 || gpu >= p->c->n_gpus) return fail(KV_ERR_INVALID_ARG, "gpu %d out of range", gpu);
     cudaStream_t stream = static_cast<cudaStream_t>(stream_);
@@ -966,7 +1008,8 @@ extern "C" kv_status kv_reshard_staged(kv_plan* p, int32_t gpu, void* staging, i
 }
 
 extern "C" kv_status kv_pack(kv_plan* p, int32_t src_gpu, void* buf, const int64_t* chunk_off, void* stream_) {
-    if (!p || !buf || !chunk_off) return fail(KV_ERR_INVALID_ARG, "bad kv_pack arguments");
+    PLAN_CHECK(p);
+    if (!buf || !chunk_off) return fail(KV_ERR_INVALID_ARG, "bad kv_pack arguments");
     if (p->state != PLAN_PLANNED) return fail(KV_ERR_BAD_STATE, "plan already committed");
     const int32_t n = p->c->n_gpus;
     if (src_gpu < 0 || src_gpu >= n) return fail(KV_ERR_INVALID_ARG, "src_gpu %d out of range", src_gpu);
@@ -989,7 +1032,8 @@ extern "C" kv_status kv_pack(kv_plan* p, int32_t src_gpu, void* buf, const int64
 }
 
 extern "C" kv_status kv_unpack(kv_plan* p, int32_t dst_gpu, const void* buf, const int64_t* chunk_off, void* stream_) {
-    if (!p || !buf || !chunk_off) return fail(KV_ERR_INVALID_ARG, "bad kv_unpack arguments");
+    PLAN_CHECK(p);
+    if (!buf || !chunk_off) return fail(KV_ERR_INVALID_ARG, "bad kv_unpack arguments");
     if (p->state != PLAN_PLANNED) return fail(KV_ERR_BAD_STATE, "plan already committed");
     const int32_t n = p->c->n_gpus;
     if (dst_gpu < 0 || dst_gpu >= n) return fail(KV_ERR_INVALID_ARG, "dst_gpu %d out of range", dst_gpu);
@@ -1020,7 +1064,8 @@ extern "C" kv_status kv_unpack(kv_plan* p, int32_t dst_gpu, const void* buf, con
 }
 
 extern "C" kv_status kv_plan_resident(const kv_plan* p, int32_t gpu, int32_t* n_resident, int32_t* n_ids) {
-    if (!p || gpu < -1 || gpu >= p->c->n_gpus) return fail(KV_ERR_INVALID_ARG, "bad arguments");
+    PLAN_CHECK(p);
+    if (gpu < -1 || gpu >= p->c->n_gpus) return fail(KV_ERR_INVALID_ARG, "bad arguments");
     if (gpu < 0) {  // totals over every pool (packed all-GPU outputs)
         int32_t a = 0, b = 0;
         for (int32_t g = 0; g < p->c->n_gpus; ++g) {
@@ -1048,7 +1093,7 @@ static void commit(kv_plan* p) {
 }
 
 extern "C" kv_status kv_plan_commit(kv_plan* p) {
-    if (!p) return fail(KV_ERR_INVALID_ARG, "plan is NULL");
+    PLAN_CHECK(p);
     commit(p);
     return KV_OK;
 }
@@ -1096,6 +1141,11 @@ extern "C" kv_status kv_plan_waves(const kv_cache* c, const kv_request* reqs, in
             return fail(KV_ERR_OUT_OF_BLOCKS, "request %d does not fit even in a wave of its own", i);
         }
         wave_bytes += bytes;
+    }
+    if (n_reqs == 0) {  // no waves; wave_start[0] = 0 is the only entry written
+        wave_start[0] = 0;
+        *n_waves = 0;
+        return KV_OK;
     }
     if (n_reqs > start || w == 0) close_wave(n_reqs);
     wave_start[w] = n_reqs;
@@ -1257,7 +1307,7 @@ extern "C" kv_status kv_suggest_rank_ids(const kv_cache* c, const kv_request* re
 
 extern "C" kv_status kv_remap_block_tables(kv_plan* p, int32_t gpu, int32_t* req_ptr, int32_t* block_ids,
                                            int32_t* per_req_meta, void* stream_) {
-    if (!p) return fail(KV_ERR_INVALID_ARG, "plan is NULL");
+    PLAN_CHECK(p);
     kv_cache* c = p->c;
     if (gpu < -1 || gpu >= c->n_gpus) return fail(KV_ERR_INVALID_ARG, "gpu %d out of range", gpu);
     int32_t n_res = 0, n_ids = 0;
@@ -1343,7 +1393,8 @@ static void count_piece_range(const kv_plan* p, int32_t lo, int32_t hi, int64_t 
 }
 
 extern "C" kv_status kv_plan_work_order(const kv_plan* p, int32_t gpu, int32_t* n_rows, int64_t* out) {
-    if (!p || !n_rows || gpu < 0 || gpu >= p->c->n_gpus) return fail(KV_ERR_INVALID_ARG, "bad kv_plan_work_order arguments");
+    PLAN_CHECK(p);
+    if (!n_rows || gpu < 0 || gpu >= p->c->n_gpus) return fail(KV_ERR_INVALID_ARG, "bad kv_plan_work_order arguments");
     const int32_t n = p->c->n_gpus;
     const MixStream& ms = p->streams[gpu];
     const int64_t len = (gpu + 1 < n ? p->streams[gpu + 1].begin : p->mixed_end) - ms.begin;
@@ -1371,10 +1422,74 @@ extern "C" kv_status kv_plan_work_order(const kv_plan* p, int32_t gpu, int32_t* 
 
 extern "C" void kv_plan_destroy(kv_plan* p) {
     if (!p) return;
+    if (!p->c) {  // detached by kv_cache_destroy: device memory already released
+        delete p;
+        return;
+    }
+    p->c->live.erase(p);
     if (p->state == PLAN_PLANNED) rollback_allocations(p, (int32_t)p->reqs.size());
     if (p->dbuf) cudaFreeAsync(p->dbuf, p->last_stream);
     if (p->d_out) cudaFreeAsync(p->d_out, p->last_stream);
     delete p;
+}
+
+// R10 strict mode: (request, head, replica >= 1) items of the plan's moving
+// requests whose source degree exceeds H.
+static std::vector<ReplicaItem> replica_items(const kv_plan* p) {
+    std::vector<ReplicaItem> items;
+    const int32_t H = p->c->geo.num_kv_heads, B = p->c->geo.block_base;
+    for (const ReqPlan& q : p->reqs) {
+        if (!q.moving || q.src.degree <= H || q.T <= 0) continue;
+        const Layout l0 = layout_of(H, q.src.degree);
+        int32_t member_of[64];
+        for (int32_t m = 0; m < q.src.degree; ++m) member_of[q.src_rid[m]] = m;
+        for (int32_t h = 0; h < H; ++h)
+            for (int32_t j = 1; j < l0.rep; ++j)
+                items.push_back(ReplicaItem{q.src.first_gpu + member_of[h * l0.rep],
+                                            q.src.first_gpu + member_of[h * l0.rep + j], q.src_off, l0.k,
+                                            (int32_t)ceil_div(q.T, B), q.T});
+    }
+    return items;
+}
+
+extern "C" kv_status kv_verify_replicas(kv_plan* p, void* stream_, int64_t* mismatches, uint64_t* first) {
+    PLAN_CHECK(p);
+    if (!mismatches) return fail(KV_ERR_INVALID_ARG, "mismatches is NULL");
+    if (p->state != PLAN_PLANNED) return fail(KV_ERR_BAD_STATE, "plan already committed; its sources may be reused");
+    *mismatches = 0;
+    if (first) *first = UINT64_MAX;
+    const std::vector<ReplicaItem> items = replica_items(p);
+    if (items.empty()) return KV_OK;
+    cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+    kv_status s = ensure_device(p, stream);
+    if (s) return s;
+    kv_cache* c = p->c;
+    const size_t ib = items.size() * sizeof(ReplicaItem), ob = 256;
+    char* d = nullptr;
+    CUDA_TRY(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&d), ib + ob, c->pool, stream));
+    unsigned long long init[2] = {0ull, ~0ull}, out[2] = {0ull, ~0ull};
+    cudaError_t e = cudaMemcpyAsync(d, items.data(), ib, cudaMemcpyHostToDevice, stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d + ib, init, sizeof init, cudaMemcpyHostToDevice, stream);
+    VerifyArgs a{};
+    a.items = reinterpret_cast<const ReplicaItem*>(d);
+    a.tables = reinterpret_cast<const int32_t*>(p->dbuf + p->off_tables);
+    a.layer_base = c->d_layer_base;
+    a.n_items = (int32_t)items.size();
+    a.L = c->geo.num_layers;
+    a.B = c->geo.block_base;
+    a.atom_bytes = (int32_t)c->atom_bytes;
+    a.tok_bytes = c->geo.head_dim * c->geo.elem_bytes;
+    a.M = c->M;
+    a.out = reinterpret_cast<unsigned long long*>(d + ib);
+    if (e == cudaSuccess) e = launch_verify(a, stream);
+    if (e == cudaSuccess) g_launches.fetch_add(1);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out, d + ib, sizeof out, cudaMemcpyDeviceToHost, stream);
+    cudaFreeAsync(d, stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+    if (e != cudaSuccess) return cuda_fail(e, "kv_verify_replicas");
+    *mismatches = (int64_t)out[0];
+    if (first) *first = out[1];
+    return KV_OK;
 }
 
 // kv_switch without its read-back: plan, upload, reshard, all-pool remap into
@@ -1399,6 +1514,20 @@ static kv_status switch_enqueue(kv_cache* c, const kv_request* reqs, int32_t n_r
     s = ensure_device(p, stream);
     if (s) return abort_plan(s);
     p->last_stream = stream;
+    if (c->strict) {  // R10: replicated sources must agree before any byte moves
+        int64_t bad = 0;
+        uint64_t first = 0;
+        s = kv_verify_replicas(p, stream, &bad, &first);
+        if (s) return abort_plan(s);
+        if (bad)
+            return abort_plan(fail(KV_ERR_REPLICA_MISMATCH,
+                                   "%lld source atoms differ from their canonical replica (first: item %llu, "
+                                   "layer %llu, K/V %llu, chunk %llu); nothing moved",
+                                   (long long)bad, (unsigned long long)((first >> 32) / (2ull * c->geo.num_layers)),
+                                   (unsigned long long)(((first >> 32) % (2ull * c->geo.num_layers)) >> 1),
+                                   (unsigned long long)((first >> 32) & 1ull),
+                                   (unsigned long long)(first & 0xffffffffull)));
+    }
     cudaError_t e = cudaMallocFromPoolAsync(reinterpret_cast<void**>(&p->d_out), (size_t)elems * 4, c->pool, stream);
     if (e != cudaSuccess) return abort_plan(cuda_fail(e, "cudaMallocFromPoolAsync (tables)"));
     s = kv_reshard(p, -1, stream);
@@ -1455,7 +1584,13 @@ extern "C" kv_status kv_switch_multi(kv_cache* c, const kv_request* reqs, const 
     for (int32_t w = 0; w < n_waves; ++w) {
         kv_status s = switch_enqueue(c, reqs + wave_ptr[w], wave_ptr[w + 1] - wave_ptr[w], stream, &plans[w]);
         if (s) {
-            cudaStreamSynchronize(stream);
+            // waves 0..w-1 have committed (their sources are released): read
+            // their tables back so the caller keeps the only record of where
+            // those requests now live; then report the failing wave's error
+            const std::string why = g_err;
+            if (cudaStreamSynchronize(stream) == cudaSuccess)
+                for (int32_t k = 0; k < w; ++k) switch_read_back(plans[k], stream);
+            g_err = why;
             return s;
         }
     }
@@ -1535,8 +1670,11 @@ extern "C" kv_status kv_switch_back(kv_cache* c, const kv_plan* prev, void* stre
 
 extern "C" kv_status kv_plan_tables(const kv_plan* p, int32_t gpu, int32_t on_device, const int32_t** req_ptr,
                                     const int32_t** block_ids, const int32_t** per_req_meta) {
-    if (!p || gpu < 0 || gpu >= p->c->n_gpus) return fail(KV_ERR_INVALID_ARG, "bad kv_plan_tables arguments");
+    PLAN_CHECK(p);
+    if (gpu < 0 || gpu >= p->c->n_gpus) return fail(KV_ERR_INVALID_ARG, "bad kv_plan_tables arguments");
     if (!p->d_out) return fail(KV_ERR_BAD_STATE, "plan was not executed by kv_switch");
+    if (!on_device && p->h_out.empty())
+        return fail(KV_ERR_BAD_STATE, "the plan's tables were not read back (its switch did not complete)");
     const int32_t* base = on_device ? p->d_out : p->h_out.data();
     const int32_t* off = p->out_off.data() + 3 * gpu;  // packed layout of kv_remap_block_tables(gpu = -1)
     if (req_ptr) *req_ptr = base + off[0];
@@ -1740,6 +1878,7 @@ extern "C" const char* kv_strerror(kv_status s) {
         case KV_ERR_DUPLICATE_REQUEST: return "duplicate request";
         case KV_ERR_BAD_STATE: return "bad state";
         case KV_ERR_CUDA: return "CUDA error";
+        case KV_ERR_REPLICA_MISMATCH: return "replicated source heads differ";
     }
     return "unknown status";
 }

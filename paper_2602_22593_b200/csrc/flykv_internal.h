@@ -184,6 +184,25 @@ struct BarrierArgs {
     int32_t* status;
 };
 
+// Strict replica check (kv_verify_replicas): one non-canonical replica of
+// one head of one request, compared with the canonical (lowest-owner)
+// replica over chunks c < C, valid tokens only.
+struct ReplicaItem {
+    int32_t gpu_c, gpu_r;   // canonical and replica pools
+    int32_t src_tab, k0;    // source table offset, chunks per source block
+    int32_t C, T;           // chunks, tokens
+};
+
+struct VerifyArgs {
+    const ReplicaItem* items;
+    const int32_t* tables;
+    char* const* layer_base;
+    int32_t n_items, L, B;
+    int32_t atom_bytes, tok_bytes;  // B*d*e, d*e
+    int64_t M;
+    unsigned long long* out;        // [0] mismatching atoms, [1] smallest mismatch code
+};
+
 // Kernel launchers (flykv_kernels.cu, flykv_decode.cu).  Return cudaSuccess or the launch error.
 cudaError_t launch_reshard(const ReshardArgs& a, int device, cudaStream_t s);
 void set_reshard_impl(int impl, int ctas_per_sm);
@@ -192,5 +211,6 @@ cudaError_t launch_gather(const GatherSeg* segs, int n_seg, char* dst, cudaStrea
 cudaError_t launch_decode(const DecodeArgs& a, cudaStream_t s);
 cudaError_t launch_unpack(const UnpackArgs& a, int device, cudaStream_t s);
 cudaError_t launch_barrier(const BarrierArgs& a, cudaStream_t s);
+cudaError_t launch_verify(const VerifyArgs& a, cudaStream_t s);
 
 }  // namespace flykv

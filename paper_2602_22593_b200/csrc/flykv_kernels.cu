@@ -839,6 +839,45 @@ cudaError_t launch_barrier(const BarrierArgs& a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- verify
+// R10 strict mode: CTA (item, layer*2 + kv), one warp per chunk.  Under
+// replication (p0 > H) H_loc = 1, so chunk c of the head is at block
+// tab[c / k0], offset kv*M/2 + (c % k0) * atom in both replicas (uniform
+// IDs, R6).  Only the valid tokens of the last chunk are compared.
+__global__ void __launch_bounds__(256) flykv_verify_kernel(const VerifyArgs a) {
+    const ReplicaItem it = a.items[blockIdx.x];
+    const int32_t l = blockIdx.y >> 1, kv = blockIdx.y & 1;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int32_t c = wid; c < it.C; c += nw) {
+        const int32_t blk = __ldg(a.tables + it.src_tab + c / it.k0);
+        const int64_t off = (int64_t)blk * a.M + kv * (a.M >> 1) + (int64_t)(c % it.k0) * a.atom_bytes;
+        const char* x = a.layer_base[it.gpu_c * a.L + l] + off;
+        const char* y = a.layer_base[it.gpu_r * a.L + l] + off;
+        const int64_t tok = (c == it.C - 1) ? (int64_t)it.T - (int64_t)c * a.B : a.B;
+        const int64_t nbytes = tok * a.tok_bytes;
+        bool diff = false;
+        for (int64_t i = (int64_t)lane * 16; i + 16 <= nbytes; i += 32 * 16) {
+            const int4 u = ld_stream(reinterpret_cast<const int4*>(x + i));
+            const int4 v = ld_stream(reinterpret_cast<const int4*>(y + i));
+            diff |= (u.x != v.x) | (u.y != v.y) | (u.z != v.z) | (u.w != v.w);
+        }
+        for (int64_t i = (nbytes & ~(int64_t)15) + lane; i < nbytes; i += 32) diff |= x[i] != y[i];
+        if (__any_sync(0xffffffffu, diff) && lane == 0) {
+            atomicAdd(a.out, 1ull);
+            const unsigned long long code =
+                ((unsigned long long)((int64_t)blockIdx.x * 2 * a.L + blockIdx.y) << 32) | (unsigned)c;
+            atomicMin(a.out + 1, code);
+        }
+    }
+}
+
+cudaError_t launch_verify(const VerifyArgs& a, cudaStream_t s) {
+    if (a.n_items <= 0) return cudaSuccess;
+    dim3 grid((unsigned)a.n_items, (unsigned)(2 * a.L));
+    flykv_verify_kernel<<<grid, 256, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- gather
 struct GatherArgs {
     GatherSeg seg[3];

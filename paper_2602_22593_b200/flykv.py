@@ -33,13 +33,20 @@ STATUS_NAMES = {
     0: "KV_OK", 1: "KV_ERR_INVALID_ARG", 2: "KV_ERR_INDIVISIBLE_DEGREE", 3: "KV_ERR_UNKNOWN_GROUP",
     4: "KV_ERR_RANK_OUT_OF_RANGE", 5: "KV_ERR_INDIVISIBLE_EXTENT", 6: "KV_ERR_OUT_OF_BLOCKS",
     7: "KV_ERR_BAD_BLOCK_TABLE", 8: "KV_ERR_DUPLICATE_REQUEST", 9: "KV_ERR_BAD_STATE", 10: "KV_ERR_CUDA",
+    11: "KV_ERR_REPLICA_MISMATCH",
 }
 
 
 class FlyKVError(RuntimeError):
-    def __init__(self, status: int, msg: str):
+    """A non-OK kv_status.  `plans`: plans that committed before the error
+    (kv_switch*: their sources are released, so they are the caller's only
+    record of where those requests now live; host tables via host_tables
+    where the read-back completed)."""
+
+    def __init__(self, status: int, msg: str, plans=()):
         self.status = status
         self.name = STATUS_NAMES.get(status, str(status))
+        self.plans = list(plans)
         super().__init__(f"{self.name}: {msg}")
 
 
@@ -162,6 +169,8 @@ _sig("kv_last_error", C.c_char_p)
 _sig("kv_launch_count", C.c_int64)
 _sig("kv_set_reshard_impl", C.c_int, C.c_int32, C.c_int32)
 _sig("kv_cache_set_work_order", C.c_int, _P, C.c_int32)
+_sig("kv_cache_set_strict", C.c_int, _P, C.c_int32)
+_sig("kv_verify_replicas", C.c_int, _P, _P, _I64P, C.POINTER(C.c_uint64))
 _sig("kv_plan_work_order", C.c_int, _P, C.c_int32, _I32P, _I64P)
 
 EXPORTED = ["kv_cache_create", "kv_cache_destroy", "kv_layout", "kv_blocks_for", "kv_alloc", "kv_reserve",
@@ -172,7 +181,7 @@ EXPORTED = ["kv_cache_create", "kv_cache_destroy", "kv_layout", "kv_blocks_for",
             "weight_shard_view", "kv_gather_view", "kv_vmm_granularity", "kv_vmm_alloc", "kv_vmm_free",
             "weight_view_alias", "weight_view_unalias", "kv_paged_decode", "kv_ipc_export", "kv_ipc_import", "kv_ipc_close",
             "kv_group_barrier", "kv_stream_sync", "kv_strerror", "kv_last_error", "kv_launch_count", "kv_set_reshard_impl",
-            "kv_cache_set_work_order", "kv_plan_work_order"]
+            "kv_cache_set_work_order", "kv_plan_work_order", "kv_cache_set_strict", "kv_verify_replicas"]
 
 
 # ----------------------------------------------------------------- marshalling
@@ -285,6 +294,10 @@ class KVCache:
 
     def plan_switch(self, requests) -> "Plan":
         return kv_plan_switch(self, requests)
+
+    def set_strict(self, strict: bool = True):
+        """R10 strict mode: kv_switch* verify replicated sources first (kv_cache_set_strict)."""
+        _check(_lib.kv_cache_set_strict(self._h, int(bool(strict))))
 
     def set_work_order(self, order: int):
         """1 = destination-rotated (default), 0 = plan order (kv_cache_set_work_order)."""
@@ -452,11 +465,8 @@ def kv_switch(cache: KVCache, requests, stream=None) -> Plan:
     h = C.c_void_p()
     st = _lib.kv_switch(cache._h, ra.ptr, ra.n, stream_of(stream), C.byref(h))
     plan = Plan(cache, h, ra.n) if h.value else None
-    if st != KV_OK:
-        msg = _lib.kv_last_error().decode()
-        if plan is not None:
-            plan.destroy()
-        raise FlyKVError(st, msg)
+    if st != KV_OK:  # a plan returned with an error has committed: hand it over
+        raise FlyKVError(st, _lib.kv_last_error().decode(), [plan] if plan is not None else [])
     return plan
 
 
@@ -471,12 +481,8 @@ def kv_switch_multi(cache: KVCache, waves, stream=None) -> list:
     hs = (C.c_void_p * max(len(waves), 1))()
     st = _lib.kv_switch_multi(cache._h, ra.ptr, ptr.ctypes.data_as(_I32P), len(waves), stream_of(stream), hs)
     plans = [Plan(cache, C.c_void_p(hs[k]), len(w)) if hs[k] else None for k, w in enumerate(waves)]
-    if st != KV_OK:
-        msg = _lib.kv_last_error().decode()
-        for p in plans:
-            if p is not None:
-                p.destroy()
-        raise FlyKVError(st, msg)
+    if st != KV_OK:  # the waves before the failing one committed: hand them over
+        raise FlyKVError(st, _lib.kv_last_error().decode(), [p for p in plans if p is not None])
     return plans
 
 
@@ -499,18 +505,18 @@ def kv_switch_waves(cache: KVCache, requests, max_wave_bytes: int = 0, split: bo
             continue
         break
     plans = [Plan(cache, C.c_void_p(hs[k]), 0) if hs[k] else None for k in range(n_w.value)]
-    if st != KV_OK:
-        msg = _lib.kv_last_error().decode()
-        for p in plans:
-            if p is not None:
-                p.destroy()
-        raise FlyKVError(st, msg)
     waves = [[] for _ in range(n_w.value)]
-    for k in range(n_p.value):
+    for k in range(min(n_p.value, cap)):
         pc = buf[k]
-        waves[pc.wave].append((pc.req, pc.tok0, pc.tok1))
+        if pc.wave < len(waves):
+            waves[pc.wave].append((pc.req, pc.tok0, pc.tok1))
     for p, wv in zip(plans, waves):
-        p.n_reqs = len(wv)
+        if p is not None:
+            p.n_reqs = len(wv)
+    if st != KV_OK:  # committed waves before the failing one: hand them (and their pieces) over
+        err = FlyKVError(st, _lib.kv_last_error().decode(), [p for p in plans if p is not None])
+        err.waves = [wv for p, wv in zip(plans, waves) if p is not None]
+        raise err
     return waves, plans
 
 
@@ -521,10 +527,7 @@ def kv_switch_back(cache: KVCache, prev: Plan, stream=None) -> Plan:
     st = _lib.kv_switch_back(cache._h, prev._h, stream_of(stream), C.byref(h))
     plan = Plan(cache, h, prev.n_reqs) if h.value else None
     if st != KV_OK:
-        msg = _lib.kv_last_error().decode()
-        if plan is not None:
-            plan.destroy()
-        raise FlyKVError(st, msg)
+        raise FlyKVError(st, _lib.kv_last_error().decode(), [plan] if plan is not None else [])
     return plan
 
 
@@ -585,6 +588,14 @@ def piece_request(geom: Geometry, req, tok0: int, tok1: int):
 
 def kv_reshard(plan: Plan, gpu: int = -1, stream=None):
     _check(_lib.kv_reshard(plan._h, gpu, stream_of(stream)))
+
+
+def kv_verify_replicas(plan: Plan, stream=None):
+    """R10: (mismatching source atoms, first mismatch code or None) of the
+    plan's replicated sources (synchronises the stream)."""
+    n, first = C.c_int64(), C.c_uint64()
+    _check(_lib.kv_verify_replicas(plan._h, stream_of(stream), C.byref(n), C.byref(first)))
+    return n.value, (None if first.value == (1 << 64) - 1 else first.value)
 
 
 def kv_reshard_range(plan: Plan, gpu_lo: int, gpu_hi: int, stream=None):

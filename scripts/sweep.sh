@@ -6,6 +6,7 @@ run() { timeout 900 python bench.py --steps 10 --warmup 3 --no-cpu-baseline "$@"
 run --config tiny
 run --config c2
 run --config c4
+run --config c4fan
 run --config c4gqa4
 run --config c4gqa1
 run --config c3i --requests 64

@@ -99,10 +99,14 @@ def llama70b_dp8_tp8(n_req: int = 64, seed: int = 0, H: int = 8) -> Workload:
 
 
 def llama70b_fanout(n_req: int = 64, seed: int = 0) -> Workload:
-    """BASELINE configs[3] (ii): single DP replica on GPU0 -> TP8."""
+    """BASELINE configs[3] (ii): single DP replica on GPU0 -> TP8 (the merge
+    of a DP engine into one TP group).  Its sources sit at the
+    top of GPU0's pool (src_top): uniform destination IDs (R6) then come from
+    the low IDs every member has free, so GPUs 1-7 need pools only as large
+    as their share of the destination -- the whole switch fits one B200."""
     T = lengths(n_req, 512, 4096, seed)
     return Workload("llama3-70b DP1(gpu0)->TP8", 80, 8, 128, 16, 2, 8, T,
-                    [(0, 1)] * n_req, [(0, 8)] * n_req)
+                    [(0, 1)] * n_req, [(0, 8)] * n_req, extra={"src_top": True})
 
 
 def long_context_tp4_tp8(n_short: int = 128, seed: int = 0, long_T: int = 131072) -> Workload:
@@ -159,11 +163,12 @@ def pool_blocks(w: Workload, slack: float = 1.10, extra: int = 8) -> list:
 
 
 def source_tables(w: Workload, counts: list, num_blocks: list, seed: int = 1, window=None,
-                  contiguous: bool = False) -> list:
+                  contiguous: bool = False, top: bool = False) -> list:
     """Fragmented source tables: per source group a seeded permutation of the
-    IDs [0, window) (default: the whole pool), consumed in request order,
-    skipping IDs already used on any member GPU (groups may overlap).
-    counts[i] = blocks request i holds (computed by the caller's own code)."""
+    IDs [0, window) (default: the whole pool; top: the last `window` IDs of
+    the group's smallest pool), consumed in request order, skipping IDs
+    already used on any member GPU (groups may overlap).  counts[i] = blocks
+    request i holds (computed by the caller's own code)."""
     rng = np.random.default_rng(seed)
     perms, cursor = {}, {}
     used = [np.zeros(n, dtype=bool) for n in num_blocks]
@@ -173,9 +178,12 @@ def source_tables(w: Workload, counts: list, num_blocks: list, seed: int = 1, wi
         members = range(grp[0], grp[0] + grp[1])
         if grp not in perms:
             nb = min(num_blocks[g] for g in members)
+            lo = 0
             if window is not None:
-                nb = min(nb, int(window))
-            perms[grp] = (np.arange(nb, dtype=np.int32) if contiguous else rng.permutation(nb).astype(np.int32))
+                win = min(nb, int(window[grp] if isinstance(window, dict) else window))
+                lo = nb - win if top else 0
+                nb = win
+            perms[grp] = lo + (np.arange(nb, dtype=np.int32) if contiguous else rng.permutation(nb).astype(np.int32))
             cursor[grp] = 0
         perm, c = perms[grp], cursor[grp]
         ids = []
@@ -210,6 +218,14 @@ def realistic_pools(w: Workload, n_src: list, n_dst: list, frag: float = 1.25, s
             src_need[g] += a
         for g in range(d[0], d[0] + d[1]):
             dst_need[g] += b
+    if w.extra.get("src_top"):  # per-GPU pools: own source window on top + own destination need below
+        win = [int(frag * n) + 16 if n else 0 for n in src_need]
+        # forward: window on top, destinations below; reverse: the source need
+        # again next to the destination copy
+        nb = [max(win[g] + int(slack * dst_need[g]), int(slack * (src_need[g] + dst_need[g]))) + 32
+              for g in range(w.n_gpus)]
+        windows = {tuple(s): min(win[g] for g in range(s[0], s[0] + s[1])) for s in w.src}
+        return nb, source_tables(w, n_src, nb, seed=seed, window=windows, contiguous=contiguous, top=True)
     window = int(frag * max(src_need)) + 16
     nb_all = window + int(slack * max(max(dst_need), max(src_need))) + 32
     nb = [nb_all] * w.n_gpus

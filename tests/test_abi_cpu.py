@@ -530,3 +530,34 @@ def test_kv_switch_waves_schedule_retry_before_the_device():
         F.kv_switch_waves(c, reqs, max_wave_bytes=1, split=True)
     assert e.value.name == "KV_ERR_CUDA"
     assert all(np.array_equal(c.held_mask(g), before[g]) for g in (0, 1))
+
+
+def test_empty_wave_schedules():
+    """An empty request list has no waves: kv_plan_waves writes only
+    wave_start[0] (it used to write one entry past n_reqs + 1),
+    and kv_switch_waves(split=False) of nothing is a no-op that needs no
+    device."""
+    c = fake_cache((1, 4, 8, 4, 2), [64, 64])
+    assert F.kv_plan_waves(c, []) == []
+    waves, plans = F.kv_switch_waves(c, [], split=False)
+    assert waves == [] and plans == []
+    assert F.kv_plan_pieces(c, []) == []
+
+
+def test_cache_close_detaches_live_plans():
+    """KVCache.close() while a plan is alive detaches the plan:
+    calls on it return BAD_STATE instead of touching freed allocator state,
+    and destroying it afterwards is safe."""
+    c = fake_cache((1, 4, 8, 4, 2), [64, 64])
+    a = c.alloc((0, 1), 5)
+    plan = c.plan_switch([(1, 20, (0, 1), a, (0, 2))])
+    assert plan.resident(0) == (1, 3)
+    c.close()
+    with pytest.raises(F.FlyKVError) as e:
+        plan.resident(0)
+    assert e.value.name == "KV_ERR_BAD_STATE"
+    with pytest.raises(F.FlyKVError):
+        plan.commit()
+    assert len(plan.dst_tables()[0]) == 3         # host-side plan data stays readable
+    plan.destroy()
+    plan.destroy()

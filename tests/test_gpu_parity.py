@@ -241,7 +241,8 @@ def test_round_trip_restores_contents():
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("cfg,n_req,frag,impl", [("c2", 0, 1.25, 0), ("c4", 0, 1.25, 0), ("c4gqa4", 0, 1.25, 0),
+@pytest.mark.parametrize("cfg,n_req,frag,impl", [("c2", 0, 1.25, 0), ("c4", 0, 1.25, 0), ("c4fan", 0, 1.25, 0),
+                                                 ("c4gqa4", 0, 1.25, 0),
                                                  ("c4gqa1", 0, 1.25, 0), ("c3i", 64, 1.25, 0), ("c3ii", 64, 1.25, 0),
                                                  ("c5", 0, 1.0, 0), ("single", 0, 1.25, 0),
                                                  ("c2", 0, 1.25, 2), ("c4gqa4", 0, 1.25, 2),
@@ -250,11 +251,14 @@ def test_full_size_all_atoms(cfg, n_req, frag, impl):
     """Every BASELINE config at the size and in the launch configuration the
     bench times (virtual ranks on one B200, the bench's pool sizing and
     placement, one reshard launch; config 3 on the bench's 64-request prefix,
-    config 5 in full with `--frag 1.0`): destination tables equal the oracle's
-    allocator in full; EVERY destination atom (up to 13.4M x 4 KiB, all GQA
-    replicas) equals the content hash of the source position the oracle maps
-    it from; sampled free blocks keep their poison.  impl 2: the TMA bulk-ring
-    variant of the reshard kernel on the same checks."""
+    config 4(ii) = c4fan, the single-replica fan-out, config 5 in full with
+    `--frag 1.0`): destination tables equal the oracle's allocator in full,
+    and EVERY BYTE of every pool (up to 158 GB) equals the oracle's expected
+    pool -- every destination atom (up to 13.4M x 4 KiB, all GQA replicas)
+    the content hash of the source position the oracle maps it from, every
+    other byte (free blocks, released sources, tail slots past T) its
+    untouched content hash, so a stray write anywhere fails.  impl 2: the TMA
+    bulk-ring variant of the reshard kernel on the same checks."""
     F = _F()
     from paper_2602_22593_b200.engine import KVSwitchEngine
     F.set_reshard_impl(0 if impl == "a2a" else impl, 0)
@@ -305,36 +309,52 @@ def _full_size_all_atoms(F, KVSwitchEngine, cfg, n_req, frag, a2a=False):
         assert np.array_equal(host[gpu][1].numpy(), ids)
         assert np.array_equal(host[gpu][2].numpy(), meta)
         assert np.array_equal(eng.cache.held_mask(gpu), held[gpu])
-    # every destination atom of the full switch (all replicas): its 4 KiB
-    # equal the content hash of the source position the oracle maps it from
+    # Whole pools, every byte: the expected pool is the content hash
+    # everywhere (untouched blocks, freed sources, tail slots past T in the
+    # destination blocks, R9) with every destination atom (all replicas)
+    # replaced by the hash of the source position the oracle maps it from.
+    # Built and compared in chunks of 64 Mi words (atoms never straddle one).
     M = O.block_bytes(og)
     atom_words = og.B * og.d * og.e // 4
     ar = torch.arange(atom_words, dtype=torch.int64, device="cuda:0")
-    flat = [t.reshape(-1).view(torch.int32) for t in eng.pools.tensors]
-    checked = 0
+    per_gpu = {g: ([], [], []) for g in range(w.n_gpus)}
+    n_writes = 0
     for i in range(len(w.T)):
         sg, so, dg, do = O.atom_map(og, nb, w.T[i], w.src[i], tabs0[i], w.dst[i], otabs[i])
+        n_writes += dg.size
         for gd in np.unique(dg):
             m = dg == gd
-            s_g = torch.as_tensor(sg[m].astype(np.int64), device="cuda:0")
-            s_w = torch.as_tensor(so[m] // 4, device="cuda:0")
-            d_w = torch.as_tensor(do[m] // 4, device="cuda:0")
-            for c0 in range(0, s_w.numel(), 16384):
-                sl = slice(c0, c0 + 16384)
-                want = synth.hash32_torch(s_g[sl, None], s_w[sl, None] + ar[None, :])
-                got = flat[int(gd)][d_w[sl, None] + ar[None, :]]
-                assert torch.equal(got, want), f"request {i}: destination atoms differ"
-                checked += want.shape[0]
-    assert checked * og.B * og.d * og.e == plan.stats()[0]["payload_bytes"]
-    rng = np.random.default_rng(123)
-    # poison survives in blocks nobody holds
-    for gpu in range(w.n_gpus):
-        free = np.nonzero(held[gpu] == 0)[0]
-        for b in rng.choice(free, size=min(16, free.size), replace=False):
-            l = int(rng.integers(og.L))
-            w0 = (l * nb[gpu] * M + int(b) * M) // 4
-            got = eng.pools.tensors[gpu].view(torch.int32).view(-1)[w0:w0 + M // 4].cpu().numpy().view(np.uint32)
-            assert np.array_equal(got, synth.hash32_np(gpu, np.arange(w0, w0 + M // 4)))
+            per_gpu[int(gd)][0].append(sg[m].astype(np.int64))
+            per_gpu[int(gd)][1].append(so[m] // 4)
+            per_gpu[int(gd)][2].append(do[m] // 4)
+    assert n_writes * og.B * og.d * og.e == plan.stats()[0]["payload_bytes"]
+    chunk = 64 * 2 ** 20
+    assert chunk % atom_words == 0
+    for gd in range(w.n_gpus):
+        parts = per_gpu[gd]
+        if parts[0]:
+            d_w = torch.as_tensor(np.concatenate(parts[2]), device="cuda:0")
+            order = torch.argsort(d_w)
+            d_w = d_w[order]
+            s_g = torch.as_tensor(np.concatenate(parts[0]), device="cuda:0")[order]
+            s_w = torch.as_tensor(np.concatenate(parts[1]), device="cuda:0")[order]
+            assert d_w.numel() == torch.unique(d_w).numel()        # every destination atom written once
+        else:
+            d_w = s_g = s_w = torch.zeros(0, dtype=torch.int64, device="cuda:0")
+        flat = eng.pools.tensors[gd].reshape(-1).view(torch.int32)
+        for w0 in range(0, flat.numel(), chunk):
+            w1 = min(flat.numel(), w0 + chunk)
+            exp = synth.hash32_torch(gd, torch.arange(w0, w1, dtype=torch.int64, device="cuda:0"))
+            a, b = (int(x) for x in torch.searchsorted(d_w, torch.tensor([w0, w1], device="cuda:0")))
+            for c0 in range(a, b, 16384):
+                c1 = min(b, c0 + 16384)
+                exp.view(-1, atom_words)[(d_w[c0:c1] - w0) // atom_words] = synth.hash32_torch(
+                    s_g[c0:c1, None], s_w[c0:c1, None] + ar[None, :])
+            same = torch.equal(flat[w0:w1], exp)
+            if not same:
+                bad = torch.nonzero(flat[w0:w1] != exp)[:4].flatten() + w0
+                raise AssertionError(f"pool {gd}: words differ from the oracle's expected pool at {bad.tolist()}")
+            del exp
 
 
 def test_weight_views_gather():
@@ -444,6 +464,46 @@ def test_memory_bounded_waves_gpu(one_call):
     for gpu, t in enumerate(eng.pools.tensors):
         assert np.array_equal(t.cpu().numpy().reshape(-1), host[gpu])
         assert np.array_equal(eng.cache.held_mask(gpu), held[gpu])
+
+
+def test_failed_wave_keeps_committed_waves():
+    """kv_switch_multi whose second wave does not fit (OUT_OF_BLOCKS): the
+    first wave has committed (its sources are released), so the error hands
+    its plan over with its tables read back -- tables, pools and
+    allocator equal the oracle after wave 0 alone; the failing wave changed
+    nothing."""
+    F = _F()
+    from paper_2602_22593_b200.engine import KVSwitchEngine
+    geo = (2, 8, 64, 16, 2)
+    og = O.Geom(*geo)
+    nb = [56] * 8
+    eng = KVSwitchEngine(F.geometry(*geo), nb, "cuda:0")
+    for gpu, t in enumerate(eng.pools.tensors):
+        synth.fill_hash_torch(t, gpu, seed=78)
+    torch.cuda.synchronize()
+    host = [t.cpu().numpy().reshape(-1).copy() for t in eng.pools.tensors]
+    held = [np.zeros(n, dtype=np.uint8) for n in nb]
+    rng = np.random.default_rng(10)
+    reqs = []
+    for i in range(24):
+        T = int(rng.integers(80, 200))
+        src = (i % 8, 1)
+        reqs.append((i, T, src, oracle_alloc(eng.cache, held, src, O.num_blocks(og, T, 1)), (0, 8)))
+    (a, b) = F.kv_plan_waves(eng.cache, reqs)[0]
+    with pytest.raises(F.FlyKVError) as e:
+        F.kv_switch_multi(eng.cache, [reqs[a:b], reqs[b:]], eng.stream)
+    assert e.value.name == "KV_ERR_OUT_OF_BLOCKS" and len(e.value.plans) == 1
+    plan = e.value.plans[0]
+    oreqs = [O.Req(T, s, list(ids), d) for (_, T, s, ids, d) in reqs[a:b]]
+    st, otabs = O.switch(og, host, held, oreqs)
+    assert st == 0
+    assert [list(x) for x in plan.dst_tables()] == [list(y) for y in otabs]
+    for gpu in range(len(nb)):
+        rp, ids_, meta = plan.host_tables(gpu)
+        orp, oids, ometa = O.tables(og, gpu, oreqs, otabs)
+        assert np.array_equal(rp, orp) and np.array_equal(ids_, oids) and np.array_equal(meta, ometa)
+        assert np.array_equal(eng.cache.held_mask(gpu), held[gpu])
+        assert np.array_equal(eng.pools.tensors[gpu].cpu().numpy().reshape(-1), host[gpu])
 
 
 @pytest.mark.parametrize("seed", range(10))
@@ -758,3 +818,72 @@ def test_long_request_promoted_in_pieces(T, src, dst, H):
         a = orig[int(sg[k])][int(so[k]):int(so[k]) + atom]
         b = eng.pools.tensors[int(dg[k])].reshape(-1)[int(do[k]):int(do[k]) + atom].cpu().numpy()
         assert np.array_equal(a, b), f"atom {k}"
+
+
+def test_strict_replica_mode():
+    """R10 strict mode.  Sources at TP8 with H_kv = 2 hold every head on 4
+    ranks (Eq.3 replication); only the canonical (lowest-owner)
+    replica is read.  kv_verify_replicas finds a corrupted valid byte in a
+    non-canonical replica (and decodes where), ignores stale tail slots past
+    T (R9), and in strict mode kv_switch refuses the switch with no state
+    change and no byte moved; once the replica is repaired the switch runs
+    and matches the oracle."""
+    F = _F()
+    from paper_2602_22593_b200.engine import KVSwitchEngine
+    geo = (2, 2, 64, 16, 2)
+    og = O.Geom(*geo)
+    L, H, d, B, e = geo
+    nb = [48] * 8
+    eng = KVSwitchEngine(F.geometry(*geo), nb, "cuda:0")
+    for gpu, t in enumerate(eng.pools.tensors):
+        synth.fill_hash_torch(t, gpu, seed=91)
+    held = [np.zeros(n, dtype=np.uint8) for n in nb]
+    reqs = []
+    for i, T in enumerate((37, 64, 100)):
+        ids = oracle_alloc(eng.cache, held, (0, 8), O.num_blocks(og, T, 8))
+        idx = torch.as_tensor(np.asarray(ids, dtype=np.int64), device="cuda:0")
+        for h in range(H):   # the 3 other replicas of head h = copies of rank 4h (R10)
+            for j in range(1, 4):
+                eng.pools.tensors[4 * h + j][:, idx] = eng.pools.tensors[4 * h][:, idx]
+        reqs.append((i, T, (0, 8), ids, (i, 1)))
+    torch.cuda.synchronize()
+    plan = eng.plan(reqs)
+    assert F.kv_verify_replicas(plan, eng.stream) == (0, None)
+    plan.destroy()
+    M = O.block_bytes(og)
+    k0 = H          # chunks per source block at TP8 (B(8) = H * B)
+    blk = int(reqs[0][3][2 // k0])                      # request 0 (T = 37): chunk 2 holds tokens 32..36
+    base = blk * M + (2 % k0) * B * d * e               # layer 0, K half, head 0 (H_loc = 1), chunk 2
+    pool1 = eng.pools.tensors[1].view(-1)               # replica j = 1 of head 0
+    pool1[base + 6 * d * e] ^= 0xFF                     # token 38: stale tail slot, not compared
+    plan = eng.plan(reqs)
+    assert F.kv_verify_replicas(plan, eng.stream) == (0, None)
+    plan.destroy()
+    pool1[base + 3 * d * e + 5] ^= 0x01                 # token 35: valid
+    plan = eng.plan(reqs)
+    assert F.kv_verify_replicas(plan, eng.stream) == (1, 2)   # item 0 (req 0, head 0, replica 1), l 0, K, chunk 2
+    plan.destroy()
+    eng.cache.set_strict(True)
+    before = [t.clone() for t in eng.pools.tensors]
+    masks = [eng.cache.held_mask(g).copy() for g in range(8)]
+    with pytest.raises(F.FlyKVError) as err:
+        F.kv_switch(eng.cache, reqs, eng.stream)
+    assert err.value.name == "KV_ERR_REPLICA_MISMATCH" and err.value.plans == []
+    torch.cuda.synchronize()
+    assert all(torch.equal(a, b) for a, b in zip(before, eng.pools.tensors))
+    assert all(np.array_equal(eng.cache.held_mask(g), masks[g]) for g in range(8))
+    pool1[base + 3 * d * e + 5] ^= 0x01                 # repaired
+    plan = F.kv_switch(eng.cache, reqs, eng.stream)
+    st, otabs = O.switch(og, None, held, [O.Req(T, s, list(ids), dd) for (_, T, s, ids, dd) in reqs], copy=False)
+    assert st == 0 and [list(a) for a in plan.dst_tables()] == [list(b) for b in otabs]
+    for i, (_, T, s, ids, dd) in enumerate(reqs):      # every destination token equals the canonical source
+        for l in range(L):
+            for kv in range(2):
+                for h in range(H):
+                    for c in range(-(-T // B)):
+                        g0, o0 = O.locate(og, 0, 8, list(ids), kv, h, c * B)
+                        g1, o1 = O.locate(og, dd[0], 1, list(otabs[i]), kv, h, c * B)
+                        n = min(B, T - c * B) * d * e
+                        a = before[g0].view(-1)[l * nb[g0] * M + o0:][:n]
+                        b = eng.pools.tensors[g1].view(-1)[l * nb[g1] * M + o1:][:n]
+                        assert torch.equal(a, b)
