@@ -478,12 +478,17 @@ cudaError_t launch_unpack(const UnpackArgs& a, int device, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------- TMA bulk
-// Each warp runs its own S-stage shared-memory ring; lane 0 drives the
-// async-copy engine: cp.async.bulk global->shared (completes on a per-stage
-// mbarrier), then cp.async.bulk shared->global to every destination replica
-// (bulk_group, one commit per atom).  Loads run D = S - 2 atoms ahead of the
-// stores; a stage is refilled once cp.async.bulk.wait_group.read shows its
-// stores have finished reading it.  No data passes through registers.
+// Each warp runs its own S-stage shared-memory ring.  Lane 0 drives the
+// loads: cp.async.bulk global->shared, completing on a per-stage mbarrier.
+// The stores are warp-wide: once a stage's bytes have landed, lane j issues
+// the cp.async.bulk shared->global of replica j (1, or p/H under GQA
+// replication, R2) from that one stage -- the replicas' address decodes and
+// bulk stores run in parallel instead of one after another on lane 0 -- and
+// every lane commits one bulk group per atom (empty when it has no replica),
+// so the lanes' group sequences stay aligned.  Loads run D = S - 2 atoms
+// ahead of the stores; a stage is refilled once every lane's
+// cp.async.bulk.wait_group.read shows the stores reading it have finished.
+// No data passes through registers.
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -506,7 +511,7 @@ __global__ void __launch_bounds__(W * 32) flykv_reshard_tma_kernel(const Reshard
     const int wid = threadIdx.x >> 5;
     unsigned char* ring = smem + (size_t)wid * S * stage_bytes;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)W * S * stage_bytes) + wid * S;
-    // per-stage pending store: replica-0 destination, replica count, atom index (lane 0 only)
+    // per-stage pending store: replica-0 destination, replica count, atom index (written by lane 0)
     __shared__ char* pend_dst[W][S];
     __shared__ int32_t pend_rep[W][S];
     __shared__ int64_t pend_atom[W][S];
@@ -521,14 +526,14 @@ __global__ void __launch_bounds__(W * 32) flykv_reshard_tma_kernel(const Reshard
     const uint32_t bytes = (uint32_t)a.atom_bytes;
     const int64_t warp = (int64_t)blockIdx.x * W + wid;
     const int64_t nwarps = (int64_t)gridDim.x * W;
-    uint32_t issued = 0, stored = 0;
-    auto store_one = [&](uint32_t j) {
+    uint32_t issued = 0, stored = 0;  // warp-uniform
+    auto store_one = [&](uint32_t j) {  // warp-wide: lane r stores replica r
         const int st = j % S;
         mbar_wait(smem_u32(bars + st), (j / S) & 1u);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         const uint32_t src = smem_u32(ring + (size_t)st * stage_bytes);
         const int rep = pend_rep[wid][st];
-        for (int r = 0; r < rep; ++r) {
+        for (int r = lane; r < rep; r += 32) {
             char* dst = r == 0 ? pend_dst[wid][st] : replica_ptr<true>(a, pend_atom[wid][st], r);
             asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(dst),
                          "r"(src), "r"(bytes), "l"(policy)
@@ -548,13 +553,14 @@ __global__ void __launch_bounds__(W * 32) flykv_reshard_tma_kernel(const Reshard
             char* d0 = shfl_ptr(la.dst0, k);
             const int rep = __shfl_sync(0xffffffffu, la.rep1, k);
             if (rep == 0) continue;  // hole (warp-uniform)
+            if (issued >= (uint32_t)D) store_one(stored++);
+            const int st = issued % S;
+            // stage st last held atom issued - S; after the store above, the
+            // S - D most recent bulk groups of every lane are atoms
+            // issued-S+1 .. issued-D, so waiting down to S - D pending frees it
+            asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(S - D) : "memory");
+            __syncwarp();
             if (lane == 0) {
-                if (issued >= (uint32_t)D) store_one(stored++);
-                const int st = issued % S;
-                // stage st last held atom issued - S; after the store above,
-                // the S - D most recent bulk groups are atoms issued-S+1 ..
-                // issued-D, so waiting down to S - D pending frees stage st.
-                asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(S - D) : "memory");
                 pend_dst[wid][st] = d0;
                 pend_rep[wid][st] = rep;
                 pend_atom[wid][st] = R + warp + (int64_t)k * nwarps;
@@ -566,15 +572,14 @@ __global__ void __launch_bounds__(W * 32) flykv_reshard_tma_kernel(const Reshard
                     "[%3], %4;" ::"r"(smem_u32(ring + (size_t)st * stage_bytes)),
                     "l"(s), "r"(bytes), "r"(bar), "l"(policy)
                     : "memory");
-                ++issued;
             }
+            __syncwarp();
+            ++issued;
         }
     }
-    if (lane == 0) {
-        while (stored < issued) store_one(stored++);
-        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-        if (a.fence_sys) __threadfence_system();
-    }
+    while (stored < issued) store_one(stored++);
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    if (a.fence_sys) __threadfence_system();
     __syncwarp();
 }
 
@@ -702,6 +707,14 @@ static cudaError_t launch_tma_shape(const ReshardArgs& a, int device, cudaStream
         case 7: return launch_tma<6, 4>(a, device, s);
         case 8: return launch_tma<3, 8>(a, device, s);
         case 9: return launch_tma<8, 4>(a, device, s);
+        case 10: return launch_tma<4, 1>(a, device, s);
+        case 11: return launch_tma<6, 1>(a, device, s);
+        case 12: return launch_tma<8, 1>(a, device, s);
+        case 13: return launch_tma<3, 2>(a, device, s);
+        case 14: return launch_tma<5, 2>(a, device, s);
+        case 15: return launch_tma<4, 3>(a, device, s);
+        case 16: return launch_tma<3, 1>(a, device, s);
+        case 17: return launch_tma<12, 1>(a, device, s);
         default: return launch_tma<4, 2>(a, device, s, 3);
     }
 }
@@ -710,6 +723,19 @@ cudaError_t launch_reshard(const ReshardArgs& a, int device, cudaStream_t s) {
     if (a.atom_hi <= a.atom_lo) return cudaSuccess;
     const bool tma_ok = (a.atom_bytes % 16) == 0 && a.atom_bytes <= 16384;
     if (g_impl == 2 && tma_ok && !a.peer) return launch_tma_shape(a, device, s);
+    // GQA replication with >= 8 replicas (p/H, R2) into local pools: 8/9 of
+    // the traffic is writes, and the TMA ring with lane-parallel replica bulk
+    // stores at 2 warps per SM (4 stages, 2 atoms ahead) writes them fastest:
+    // H_kv=1 -> TP8 forward 8.87-8.90 ms against 9.22 ms for the best LDG/STG
+    // shape; 3+ warps per SM fall back to 9.6 ms (profiles/r02_gqa_tma2.jsonl).
+    // Knob FLYKV_REP_TMA=0 keeps the LDG/STG kernel (A/B).
+    static int rep_tma = -1;
+    if (rep_tma < 0) {
+        const char* e = getenv("FLYKV_REP_TMA");
+        rep_tma = e ? atoi(e) : 1;
+    }
+    if (g_impl == 0 && rep_tma && a.max_rep >= 8 && tma_ok && !a.peer && a.staged != 1 && a.staged != 2)
+        return launch_tma<4, 2>(a, device, s, 1);
     // default (0) and 3: two atoms in flight per warp (measured +1%)
     if ((g_impl == 0 || g_impl == 3) && a.atom_bytes == 4096) return launch_ldg<8, 2>(a, device, s);
     if ((g_impl == 0 || g_impl == 3) && a.atom_bytes == 2048) return launch_ldg<4, 2>(a, device, s);
