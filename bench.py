@@ -874,7 +874,7 @@ def run_multi(args):
             if v != 1:
                 raise SystemExit("--a2a needs one pool per process")
             _, mat = plan.stats()
-            send_off, recv_off = F.a2a_offsets(mat)
+            send_off, recv_off = F.a2a_offsets(plan)
             n_send, n_recv = int(mat[rank].sum()), int(mat[:, rank].sum())
             send = torch.empty(max(n_send, 16), dtype=torch.uint8, device=dev)
             recv = torch.empty(max(n_recv, 16), dtype=torch.uint8, device=dev)

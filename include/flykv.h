@@ -395,6 +395,17 @@ typedef struct {
 kv_status kv_plan_pieces(const kv_cache* cache, const kv_request* reqs, int32_t n_reqs, int64_t max_wave_bytes,
                          int32_t cap, kv_piece* pieces, int32_t* n_pieces);
 
+/* kv_piece_request: the plain request that moves tokens [tok0, tok1) of
+ * *req (a piece of kv_plan_pieces, R20): num_tokens = tok1 - tok0,
+ * src_blocks = req->src_blocks + tok0 / B(src degree) (a pointer into the
+ * caller's table, not a copy), n_src_blocks = ceil(tok1 / B(src)) -
+ * tok0 / B(src), same req_id, groups and rank IDs.  tok0 must start a
+ * source block (tok0 % B(src) == 0, as every piece does) and 0 <= tok0 <
+ * tok1 <= num_tokens; the whole range returns *req unchanged.  Errors:
+ * INVALID_ARG (NULL pointers, range), INDIVISIBLE_DEGREE (src degree). */
+kv_status kv_piece_request(const kv_geometry* geom, const kv_request* req, int32_t tok0, int32_t tok1,
+                           kv_request* out);
+
 /* kv_switch_waves: the whole memory-bounded switch in one call -- the wave
  * schedule (split = 0: kv_plan_waves, whole requests; split = 1:
  * kv_plan_pieces, block-aligned token pieces of a request when it cannot
@@ -426,6 +437,22 @@ kv_status kv_plan_dst_tables(const kv_plan* plan, int32_t* dst_ptr, int32_t* dst
  * destination bytes each source GPU sends to each destination GPU (row =
  * source), the input of the roofline of SURVEY 8(d). */
 kv_status kv_plan_get_stats(const kv_plan* plan, kv_plan_stats* stats, int64_t* bytes_matrix);
+
+/* kv_plan_a2a_offsets: the byte offsets of kv_pack / kv_unpack for
+ * all_to_all_single buffers, from the plan's bytes matrix (a function of
+ * the plan alone, so every process derives the same):
+ *   send_off  host [n_gpus * n_gpus] out (or NULL): send_off[s*n + d] =
+ *             offset of chunk (s -> d) in s's send buffer = sum over d' < d
+ *             of bytes[s][d'] (chunks in destination order)
+ *   recv_off  host [n_gpus * n_gpus] out (or NULL): recv_off[d*n + s] =
+ *             offset of chunk (s -> d) in d's receive buffer = sum over
+ *             s' < s of bytes[s'][d] (chunks in source order)
+ *   packed    host [n_gpus * n_gpus] out (or NULL): offset of chunk (s -> d)
+ *             in ONE buffer holding every chunk in row-major (s, d) order
+ *             (all pools in one process: pack then unpack in place)
+ * Row s of send_off is kv_pack's chunk_off for src_gpu s; row d of recv_off
+ * is kv_unpack's chunk_off for dst_gpu d.  Errors: INVALID_ARG, BAD_STATE. */
+kv_status kv_plan_a2a_offsets(const kv_plan* plan, int64_t* send_off, int64_t* recv_off, int64_t* packed);
 /* The kernel work order of source GPU `gpu` (kv_cache_set_work_order), for
  * link models: *n_rows receives the number of consecutive 1024-slot ranges of
  * the GPU's kernel slot order; out (host [n_rows * (n_gpus + 1)] or NULL)

@@ -45,9 +45,10 @@ def fit_two_points(p1: int, t1: float, p2: int, t2: float, kv_per_token: int) ->
 def relayout_reserve_bytes(T: int, L: int, H: int, d: int, B: int, p_src: int, p_dst: int, e: int = 2) -> float:
     """Per-GPU destination bytes a live re-layout of one T-token request
     needs next to its sources (R13): ceil(T / B(p_dst)) blocks of M bytes per
-    layer on each destination rank.  With memory-bounded waves (kv_plan_waves)
-    this bounds the transient reserve of a promotion."""
-    hloc = H // p_dst if p_dst <= H else 1
-    bp = B * (H // hloc)
-    M = 2 * H * B * d * e
-    return -(-T // bp) * M * L
+    layer on each destination rank -- block count and M from the library's
+    kv_blocks_for / kv_layout (Eq.2, Eq.3, M_block).  With memory-bounded
+    waves (kv_plan_waves) this bounds the transient reserve of a promotion."""
+    from . import flykv
+    g = flykv.geometry(L, H, d, B, e)
+    _, _, M = flykv.kv_layout(g, p_dst)
+    return flykv.kv_blocks_for(g, T, p_dst) * M * L

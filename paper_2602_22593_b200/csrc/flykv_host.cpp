@@ -1355,6 +1355,31 @@ extern "C" kv_status kv_plan_get_stats(const kv_plan* p, kv_plan_stats* st, int6
     return KV_OK;
 }
 
+extern "C" kv_status kv_plan_a2a_offsets(const kv_plan* p, int64_t* send_off, int64_t* recv_off, int64_t* packed) {
+    PLAN_CHECK(p);
+    const int32_t n = p->c->n_gpus;
+    const std::vector<int64_t>& m = p->bytes;  // m[s*n + d]
+    int64_t flat = 0;
+    for (int32_t s = 0; s < n; ++s) {
+        int64_t acc = 0;
+        for (int32_t d = 0; d < n; ++d) {
+            if (send_off) send_off[(size_t)s * n + d] = acc;
+            if (packed) packed[(size_t)s * n + d] = flat;
+            acc += m[(size_t)s * n + d];
+            flat += m[(size_t)s * n + d];
+        }
+    }
+    if (recv_off)
+        for (int32_t d = 0; d < n; ++d) {
+            int64_t acc = 0;
+            for (int32_t s = 0; s < n; ++s) {
+                recv_off[(size_t)d * n + s] = acc;
+                acc += m[(size_t)s * n + d];
+            }
+        }
+    return KV_OK;
+}
+
 // Bytes of slots [a0, a1) of the segment at piece-space position k: destination bytes
 // per GPU (replicas included) and, in column n, source reads.
 static void count_piece(const kv_plan* p, int32_t k, int64_t a0, int64_t a1, int64_t* row_out) {
@@ -1601,6 +1626,27 @@ extern "C" kv_status kv_switch_multi(kv_cache* c, const kv_request* reqs, const 
     return KV_OK;
 }
 
+extern "C" kv_status kv_piece_request(const kv_geometry* geom, const kv_request* req, int32_t tok0, int32_t tok1,
+                                      kv_request* out) {
+    kv_status s = check_geometry(geom);
+    if (s) return s;
+    if (!req || !out) return fail(KV_ERR_INVALID_ARG, "NULL argument");
+    s = check_degree(geom->num_kv_heads, req->src.degree);
+    if (s) return s;
+    *out = *req;
+    if (tok0 == 0 && tok1 == req->num_tokens) return KV_OK;  // the whole request (also an empty one)
+    const Layout l0 = layout_of(geom->num_kv_heads, req->src.degree);
+    const int32_t b0 = geom->block_base * l0.k;  // source block tokens B(p0), Eq.2
+    if (tok0 < 0 || tok1 <= tok0 || tok1 > req->num_tokens || tok0 % b0)
+        return fail(KV_ERR_INVALID_ARG, "piece [%d, %d) of a %d-token request (source blocks of %d tokens)", tok0, tok1,
+                    req->num_tokens, b0);
+    const int32_t first = tok0 / b0;
+    out->src_blocks = req->src_blocks ? req->src_blocks + first : nullptr;
+    out->n_src_blocks = (int32_t)ceil_div(tok1, b0) - first;
+    out->num_tokens = tok1 - tok0;
+    return KV_OK;
+}
+
 extern "C" kv_status kv_switch_waves(kv_cache* c, const kv_request* reqs, int32_t n_reqs, int64_t max_wave_bytes,
                                      int32_t split, void* stream, int32_t cap, kv_piece* pieces, int32_t* n_pieces,
                                      kv_plan** plans, int32_t* n_waves) {
@@ -1627,15 +1673,9 @@ extern "C" kv_status kv_switch_waves(kv_cache* c, const kv_request* reqs, int32_
     std::vector<int32_t> wave_ptr(1, 0);
     for (int32_t k = 0; k < *n_pieces; ++k) {
         const kv_piece& pc = pieces[k];
-        kv_request r = reqs[pc.req];
-        if (pc.tok0 != 0 || pc.tok1 != r.num_tokens) {
-            const Layout l0 = layout_of(c->geo.num_kv_heads, r.src.degree);
-            const int32_t b0 = c->geo.block_base * l0.k;  // source block tokens B(p0)
-            const int32_t first = pc.tok0 / b0;
-            r.src_blocks += first;
-            r.n_src_blocks = (int32_t)ceil_div(pc.tok1, b0) - first;
-            r.num_tokens = pc.tok1 - pc.tok0;
-        }
+        kv_request r{};
+        s = kv_piece_request(&c->geo, &reqs[pc.req], pc.tok0, pc.tok1, &r);
+        if (s) return s;
         sub[k] = r;
         if (k > 0 && pc.wave != pieces[k - 1].wave) wave_ptr.push_back(k);
     }

@@ -103,11 +103,9 @@ class KVSwitchEngine:
         buf: optional device uint8 buffer of >= payload bytes."""
         st, mat = plan.stats()
         n = self.n_gpus
-        flat = np.zeros(n * n + 1, dtype=np.int64)
-        flat[1:] = np.cumsum(mat.reshape(-1))
-        off = flat[:-1].reshape(n, n)
+        _, _, off = plan.a2a_offsets()      # chunk (s -> d) at off[s, d] of one row-major buffer
         if buf is None:
-            buf = torch.empty(max(int(flat[-1]), 16), dtype=torch.uint8, device=self.device)
+            buf = torch.empty(max(int(st["payload_bytes"]), 16), dtype=torch.uint8, device=self.device)
         with torch.cuda.stream(self.stream):
             for s_ in range(n):
                 if mat[s_].sum():

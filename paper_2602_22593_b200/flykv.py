@@ -150,6 +150,8 @@ _sig("kv_plan_pieces", C.c_int, _P, C.POINTER(Request), C.c_int32, C.c_int64, C.
 _sig("kv_switch_waves", C.c_int, _P, C.POINTER(Request), C.c_int32, C.c_int64, C.c_int32, _P, C.c_int32,
      C.POINTER(Piece), _I32P, C.POINTER(_P), _I32P)
 _sig("kv_plan_get_stats", C.c_int, _P, C.POINTER(PlanStats), _I64P)
+_sig("kv_plan_a2a_offsets", C.c_int, _P, _I64P, _I64P, _I64P)
+_sig("kv_piece_request", C.c_int, C.POINTER(Geometry), C.POINTER(Request), C.c_int32, C.c_int32, C.POINTER(Request))
 _sig("kv_plan_destroy", None, _P)
 _sig("weight_shard_view", C.c_int, C.POINTER(WeightDesc), C.c_int32, C.c_int32, C.POINTER(View))
 _sig("kv_gather_view", C.c_int, C.POINTER(View), _P, _P)
@@ -177,7 +179,8 @@ EXPORTED = ["kv_cache_create", "kv_cache_destroy", "kv_layout", "kv_blocks_for",
             "kv_free", "kv_free_count", "kv_held_mask", "kv_plan_switch", "kv_plan_upload", "kv_reshard", "kv_reshard_range", "kv_reshard_staged",
             "kv_pack", "kv_unpack", "kv_switch", "kv_switch_back", "kv_switch_multi", "kv_switch_waves", "kv_plan_tables", "kv_plan_resident",
             "kv_remap_block_tables", "kv_plan_dst_tables", "kv_plan_commit", "kv_plan_waves", "kv_plan_pieces",
-            "kv_suggest_rank_ids", "kv_plan_get_stats", "kv_plan_destroy",
+            "kv_suggest_rank_ids", "kv_plan_get_stats", "kv_plan_a2a_offsets", "kv_piece_request",
+            "kv_plan_destroy",
             "weight_shard_view", "kv_gather_view", "kv_vmm_granularity", "kv_vmm_alloc", "kv_vmm_free",
             "weight_view_alias", "weight_view_unalias", "kv_paged_decode", "kv_ipc_export", "kv_ipc_import", "kv_ipc_close",
             "kv_group_barrier", "kv_stream_sync", "kv_strerror", "kv_last_error", "kv_launch_count", "kv_set_reshard_impl",
@@ -373,6 +376,16 @@ class Plan:
         mat = np.zeros(n * n, dtype=np.int64)
         _check(_lib.kv_plan_get_stats(self._h, C.byref(st), mat.ctypes.data_as(_I64P)))
         return st.as_dict(), mat.reshape(n, n)
+
+    def a2a_offsets(self):
+        """(send_off, recv_off, packed): int64 [n, n] byte offsets of
+        kv_plan_a2a_offsets -- send_off[s] is kv_pack's chunk_off for source
+        s, recv_off[d] kv_unpack's for destination d, packed[s, d] the chunk
+        (s -> d) in one row-major buffer of every chunk."""
+        n = self.cache.n_gpus
+        out = [np.zeros(n * n, dtype=np.int64) for _ in range(3)]
+        _check(_lib.kv_plan_a2a_offsets(self._h, *(o.ctypes.data_as(_I64P) for o in out)))
+        return tuple(o.reshape(n, n) for o in out)
 
     def work_order(self, gpu: int) -> np.ndarray:
         """[n_pieces, n_gpus + 1] int64: destination bytes per GPU of each of
@@ -575,15 +588,16 @@ def kv_plan_pieces(cache: KVCache, requests, max_wave_bytes: int = 0) -> list:
 
 def piece_request(geom: Geometry, req, tok0: int, tok1: int):
     """The plain request that moves tokens [tok0, tok1) of `req` (a request
-    tuple as for kv_plan_switch), for a piece from kv_plan_pieces."""
-    rid, T, src, ids, dst = req[:5]
-    rest = tuple(req[5:])
-    if tok0 == 0 and tok1 == T:
-        return req
-    b0 = kv_layout(geom, src[1])[1]
-    ids = np.asarray(ids, dtype=np.int32)
-    sub = ids[tok0 // b0: -(-tok1 // b0)]
-    return (rid, tok1 - tok0, src, sub, dst) + rest
+    tuple as for kv_plan_switch), for a piece from kv_plan_pieces: the
+    library's kv_piece_request decides the source-table slice."""
+    ra = make_requests([req])
+    out = Request()
+    _check(_lib.kv_piece_request(C.byref(geom), ra.ptr, int(tok0), int(tok1), C.byref(out)))
+    base = ra.keep[0].__array_interface__["data"][0] if ra.keep else 0
+    ptr = C.cast(out.src_blocks, C.c_void_p).value or 0
+    first = (ptr - base) // 4 if ptr else 0
+    ids = np.asarray(req[3], dtype=np.int32).reshape(-1)[first:first + out.n_src_blocks].copy()
+    return (req[0], out.num_tokens, tuple(req[2]), ids, tuple(req[4])) + tuple(req[5:])
 
 
 def kv_reshard(plan: Plan, gpu: int = -1, stream=None):
@@ -608,16 +622,12 @@ def kv_reshard_staged(plan: Plan, gpu: int, staging, staging_bytes: int, mode: i
     _check(_lib.kv_reshard_staged(plan._h, gpu, ptr_of(staging), int(staging_bytes), mode, stream_of(stream)))
 
 
-def a2a_offsets(bytes_matrix):
-    """(send_off, recv_off) for all_to_all_single buffers: send_off[s] is the
-    exclusive prefix of row s (chunks s -> d in d order), recv_off[d] of
-    column d (chunks s -> d in s order); int64 [n, n] byte offsets."""
-    m = np.asarray(bytes_matrix, dtype=np.int64)
-    send = np.zeros_like(m)
-    recv = np.zeros_like(m)
-    send[:, 1:] = np.cumsum(m, axis=1)[:, :-1]
-    recv[1:, :] = np.cumsum(m, axis=0)[:-1, :]
-    return send, recv.T.copy()
+def a2a_offsets(plan: "Plan"):
+    """(send_off, recv_off) for all_to_all_single buffers (kv_plan_a2a_offsets):
+    send_off[s] = kv_pack's chunk_off for source s, recv_off[d] = kv_unpack's
+    for destination d; int64 [n, n] byte offsets."""
+    send, recv, _ = plan.a2a_offsets()
+    return send, recv
 
 
 def kv_pack(plan: Plan, src_gpu: int, buf, chunk_off, stream=None):

@@ -345,7 +345,7 @@ def test_pack_unpack_argument_errors():
             fn(plan, 2, 1 << 40, [0, 0])
         assert e.value.name == "KV_ERR_INVALID_ARG"
     _, mat = plan.stats()
-    send, recv = F.a2a_offsets(mat)
+    send, recv = F.a2a_offsets(plan)
     # chunk (s -> d) sits at send[s][d] in s's send buffer and at recv[d][s] in d's receive buffer
     assert send[0][0] == 0 and send[0][1] == mat[0][0] and recv[1][0] == 0 and recv[1][1] == mat[0][1]
     plan.commit()
@@ -561,3 +561,42 @@ def test_cache_close_detaches_live_plans():
     assert len(plan.dst_tables()[0]) == 3         # host-side plan data stays readable
     plan.destroy()
     plan.destroy()
+
+
+def test_a2a_offsets_are_exclusive_prefixes():
+    """kv_plan_a2a_offsets on a 4-GPU merge + split plan: send_off rows,
+    recv_off columns and the packed row-major layout are the exclusive
+    prefix sums of the plan's bytes matrix (written out here with numpy)."""
+    c = fake_cache((2, 8, 16, 4, 2), [64] * 4)
+    reqs = []
+    for i, (src, dst) in enumerate([((0, 1), (0, 4)), ((1, 1), (2, 2)), ((2, 2), (0, 1)), ((3, 1), (0, 2))]):
+        T = 9 + 7 * i
+        reqs.append((i, T, src, c.alloc(src, F.kv_blocks_for(c.geom, T, src[1])), dst))
+    plan = c.plan_switch(reqs)
+    _, m = plan.stats()
+    send, recv, packed = plan.a2a_offsets()
+    n = m.shape[0]
+    for s_ in range(n):
+        for d in range(n):
+            assert send[s_, d] == m[s_, :d].sum()
+            assert recv[d, s_] == m[:s_, d].sum()
+            assert packed[s_, d] == m.reshape(-1)[:s_ * n + d].sum()
+
+
+def test_piece_request_slices_the_source_table():
+    """kv_piece_request: tokens [tok0, tok1) of a request start at source
+    block tok0 / B(p0) (Eq.2: B(2) = 2B here) and span ceil(tok1 / B(p0)) -
+    tok0 / B(p0) blocks; the whole range is the request itself; a piece that
+    does not start on a source block is rejected."""
+    g = F.geometry(1, 4, 8, 4, 2)
+    ids = np.arange(100, 113, dtype=np.int32)          # 13 blocks of B(2) = 8 tokens: 100 tokens
+    req = (7, 100, (0, 2), ids, (0, 4))
+    p = F.piece_request(g, req, 16, 50)
+    assert p[0] == 7 and p[1] == 34 and p[2] == (0, 2) and p[4] == (0, 4)
+    assert list(p[3]) == list(range(102, 107))          # blocks 2 .. ceil(50/8)-1 = 6
+    whole = F.piece_request(g, req, 0, 100)
+    assert whole[:3] == req[:3] and list(whole[3]) == list(ids) and whole[4] == req[4]
+    with pytest.raises(F.FlyKVError):
+        F.piece_request(g, req, 12, 50)
+    with pytest.raises(F.FlyKVError):
+        F.piece_request(g, req, 16, 101)

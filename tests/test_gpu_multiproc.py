@@ -82,7 +82,7 @@ def _rank(rank, world, port, outdir, kind, mode="push", v=1):
                                         enumerate(zip(w.T, w.src, w.dst, tabs))])
         if mode == "a2a":  # pack -> all_to_all_single (gloo, host copies) -> unpack
             _, mat = plan.stats()
-            send_off, recv_off = F.a2a_offsets(mat)
+            send_off, recv_off = F.a2a_offsets(plan)
             send = torch.empty(max(int(mat[rank].sum()), 16), dtype=torch.uint8, device="cuda:0")
             F.kv_pack(plan, rank, send, send_off[rank], stream)
             stream.synchronize()
