@@ -68,6 +68,9 @@ def parse():
     ap.add_argument("--long-last", action="store_true", help="move the longest request to the end of the order")
     ap.add_argument("--lifo", action="store_true",
                     help="each switch moves the requests in the reverse order of the previous one (undo order)")
+    ap.add_argument("--nvls", action="store_true",
+                    help="N>1, GQA replication: NVLS multicast teams for the replicas (pools in shareable VMM memory, "
+                         "one multimem store per atom per team); reports why when the box cannot")
     ap.add_argument("--a2a", action="store_true",
                     help="N>1 comparator: kv_pack -> all_to_all_single -> kv_unpack instead of the P2P-push kernel")
     ap.add_argument("--frag", type=float, default=1.25, help="source placement window / source need")
@@ -829,13 +832,39 @@ def run_multi(args):
     g = F.geometry(w.L, w.H, w.d, w.B, w.e)
     _, _, M = F.kv_layout(g, 1)
     nb, tabs = pools_and_tables(w, args.frag, args.pool_slack, args.placement == "contiguous")
-    local_pools = torch.empty((v, w.L, nb[0], M), dtype=torch.uint8, device=dev)
+    nvls = None
+    if args.nvls:   # N2: NVLS multicast teams for GQA replicas, when the box allows
+        teams = sorted({d[1] // w.H for d in w.dst if d[1] > w.H})
+        reason, gran = None, 0
+        if v != 1:
+            reason = "needs one pool per GPU (engines == GPUs)"
+        elif same_dev:
+            reason = "ranks share one device; a multicast team needs distinct GPUs"
+        elif not teams:
+            reason = f"no GQA replication in this workload (destination degrees <= H_kv = {w.H})"
+        else:
+            ok, gran, why = F.mc_supported(max(teams), w.L * nb[0] * M)
+            reason = None if ok else why
+        nvls = {"requested": True, "enabled": reason is None, "reason": reason, "team_sizes": teams}
+    mcs = []
+    if nvls and nvls["enabled"]:
+        pool_mem, bases, nbs, imported_vmm = comm.exchange_pools_vmm(w.L * nb[0] * M, rank, world, w.L, M, nb[0],
+                                                                   dev.index, gran)
+        local_pools = pool_mem.tensor((1, w.L, nb[0], M))
+        imported = []
+    else:
+        pool_mem, imported_vmm = None, []
+        local_pools = torch.empty((v, w.L, nb[0], M), dtype=torch.uint8, device=dev)
     if not args.no_fill:
         for k, gp in enumerate(mine):
             synth.fill_hash_torch(local_pools[k], gp)
     torch.cuda.synchronize()
-    bases, nbs, imported = comm.exchange_pools(local_pools, rank, world, w.L, M)
+    if pool_mem is None:
+        bases, nbs, imported = comm.exchange_pools(local_pools, rank, world, w.L, M)
     cache = F.KVCache(g, nbs, bases, tuple(p for p in (2, 4, 8) if p <= w.n_gpus))
+    if pool_mem is not None:
+        for r_ in nvls["team_sizes"]:
+            mcs.append(comm.setup_multicast_teams(cache, pool_mem, rank, world, r_, w.L, M, nb[0], dev.index))
     if args.work_order is None:
         args.work_order = 0 if (same_dev or world == 1) else 1
     cache.set_work_order(args.work_order)
@@ -967,6 +996,12 @@ def run_multi(args):
                                           if cpool.host_bytes_per_group is not None else None)}
     barrier.close()
     comm.close_pools(imported)
+    torch.cuda.synchronize()
+    dist.barrier()
+    for m_ in mcs:
+        m_.free()
+    for pm_ in imported_vmm:
+        pm_.free()
     if rank == 0:
         payload_sum = sum(x[0]["payload_bytes"] for x in step_stats)
         payload = payload_sum / len(step_stats)
@@ -1020,11 +1055,15 @@ def run_multi(args):
                      "note": "per-rank wall clock from a host barrier to its tables on the host; max over ranks"}
                     if lat else None),
             "comm_pool": pool_cost,
+            "nvls": nvls,
             "gpu_launches": launches_all,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
     dist.barrier()
+    del local_pools
+    if pool_mem is not None:
+        pool_mem.free()
     dist.destroy_process_group()
     return 0
 

@@ -593,6 +593,72 @@ kv_status kv_group_barrier(uint64_t* const* flags, int32_t n_members, int32_t se
  * system-wide before a host-side barrier: synchronizes `stream`. */
 kv_status kv_stream_sync(void* stream);
 
+/* ------------------------------------------- NVLS multicast (N2, GQA) */
+/*
+ * GQA head replication (Eq.3): at a destination degree p > H,
+ * head h lives on the aligned team of p/H engines [g0 + h*p/H, +p/H) at the
+ * same block IDs and offsets.  With the team's pools bound to one NVLS
+ * multicast object, a sender that is a member of the team writes each atom
+ * once (multimem.st) and NVSwitch delivers it to every replica: its NVLink
+ * egress is one copy instead of p/H.
+ *
+ * Pool memory for this path: one physical allocation per pool, POSIX-fd
+ * shareable (kv_pool_alloc), mapped by peers through the exported descriptor
+ * (kv_pool_export -> pass the fd, e.g. SCM_RIGHTS -> kv_pool_import) rather
+ * than CUDA IPC.  align: round the size up to a multiple of this (the
+ * multicast granularity from kv_mc_supported; 0 = allocation granularity).
+ * The fd of kv_pool_export / kv_mc_create is the caller's (kv_close_fd).
+ *
+ * Team setup (every member process, in this order): the team leader
+ * kv_mc_create(team size, pool bytes) and sends its fd; the others
+ * kv_mc_import; every member kv_mc_add_device(own device); (all members
+ * added) kv_mc_bind(own pool); (all bound) kv_mc_map -> the multicast VA;
+ * then kv_cache_set_multicast(cache, team, layer bases inside that VA).
+ * kv_mc_supported(n_devices, bytes): *ok = 1 if the driver creates a
+ * multicast object of that team size (released again), else KV_ERR_CUDA
+ * with the driver's reason; *granularity = the recommended granularity.
+ * All: KV_ERR_INVALID_ARG on bad arguments, KV_ERR_CUDA with the driver's
+ * error otherwise.
+ */
+typedef struct kv_pool_mem kv_pool_mem;
+typedef struct kv_mc kv_mc;
+kv_status kv_pool_alloc(int32_t device, uint64_t bytes, uint64_t align, kv_pool_mem** out, void** dptr);
+kv_status kv_pool_export(const kv_pool_mem* pool, int32_t* fd);
+kv_status kv_pool_import(int32_t fd, uint64_t bytes, int32_t device, kv_pool_mem** out, void** dptr);
+kv_status kv_pool_free(kv_pool_mem* pool);
+kv_status kv_mc_supported(int32_t n_devices, uint64_t bytes, int32_t* ok, uint64_t* granularity);
+kv_status kv_mc_create(int32_t n_devices, uint64_t bytes, kv_mc** out, int32_t* fd);
+kv_status kv_mc_import(int32_t fd, uint64_t bytes, int32_t n_devices, kv_mc** out);
+kv_status kv_mc_add_device(kv_mc* mc, int32_t device);
+kv_status kv_mc_bind(kv_mc* mc, const kv_pool_mem* pool);
+kv_status kv_mc_map(kv_mc* mc, int32_t device, void** va);
+kv_status kv_mc_free(kv_mc* mc);
+kv_status kv_close_fd(int32_t fd);
+/* Allocated sizes (rounded up to the granularity): what kv_pool_import /
+ * kv_mc_import must be given on the other side. */
+kv_status kv_pool_size(const kv_pool_mem* pool, uint64_t* bytes);
+kv_status kv_mc_size(const kv_mc* mc, uint64_t* bytes);
+
+/*
+ * kv_cache_set_multicast: register the multicast mapping of replica team
+ * `team` (first_gpu = its first pool, degree = its size r = p/H) for this
+ * process: layer_base host [L] device pointers, layer l's region of every
+ * member pool as seen through the multicast VA (same offsets as the
+ * members' own layer_base).  From then on kv_reshard / kv_reshard_range
+ * write every atom whose replicas are exactly this team (destination degree
+ * p with p/H == r, identity destination rank IDs, replica 0 on first_gpu)
+ * with one multimem.st per 16 bytes instead of r stores.  Register only
+ * teams this process is a member of (a multicast VA is usable on member
+ * devices only); other teams keep per-replica stores.  layer_base NULL
+ * clears the team.  mode: 1 = multimem (the product path); 2 = emulation
+ * for single-GPU tests -- layer_base are ordinary pointers and the kernel
+ * stores once with st.global there (replicas 1..r-1 are NOT written), which
+ * checks the addressing without NVLS hardware.  Takes effect for launches
+ * after the call.  Errors: INVALID_ARG (team not aligned or r < 2, bad
+ * mode), KV_ERR_CUDA (upload).
+ */
+kv_status kv_cache_set_multicast(kv_cache* cache, kv_group team, void* const* layer_base, int32_t mode);
+
 /* ---------------------------------------------------------------- misc */
 const char* kv_strerror(kv_status s);
 const char* kv_last_error(void);

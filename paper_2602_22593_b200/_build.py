@@ -10,7 +10,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "lib", "libflykv.so")
-SOURCES = [os.path.join(CSRC, f) for f in ("flykv_host.cpp", "flykv_vmm.cpp", "flykv_kernels.cu", "flykv_decode.cu")]
+SOURCES = [os.path.join(CSRC, f) for f in ("flykv_host.cpp", "flykv_vmm.cpp", "flykv_nvls.cpp", "flykv_kernels.cu",
+                                                 "flykv_decode.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, "flykv_internal.h"), os.path.join(INCLUDE, "flykv.h")]
 
 NVCC_FLAGS = [

@@ -122,6 +122,102 @@ def exchange_pools(local: torch.Tensor, rank: int, world: int, L: int, M: int, g
     return bases, nbs, imported
 
 
+# ------------------------------------------------ file-descriptor passing
+def _sock_name(tag: str, rank: int) -> str:
+    """Abstract-namespace AF_UNIX address (no filesystem entry)."""
+    return f"\0flykv-{os.environ.get('MASTER_PORT', '0')}-{tag}-{rank}"
+
+
+def share_fds(fds_to_send: dict, rank: int, sources: dict, tag: str, group=None):
+    """Send each fd in fds_to_send {dest_rank: fd} to that rank and receive
+    one fd from every rank in sources {src_rank: True} over AF_UNIX SCM_RIGHTS
+    (the POSIX handles of kv_pool_export / kv_mc_create).  Collective over
+    the process group (two barriers).  Returns {src_rank: received fd}."""
+    import socket
+    import threading
+    srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+    srv.bind(_sock_name(tag, rank))
+    srv.listen(max(len(sources), 1))
+    got = {}
+
+    def serve():
+        for _ in range(len(sources)):
+            conn, _ = srv.accept()
+            with conn:
+                msg, fds, _, _ = socket.recv_fds(conn, 16, 1)
+                got[int(msg.decode())] = fds[0]
+    th = threading.Thread(target=serve)
+    th.start()
+    dist.barrier(group=group)          # every server is listening
+    for dst, fd in fds_to_send.items():
+        c = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+        c.connect(_sock_name(tag, dst))
+        socket.send_fds(c, [str(rank).encode()], [fd])
+        c.close()
+    th.join()
+    srv.close()
+    dist.barrier(group=group)
+    return got
+
+
+def exchange_pools_vmm(nbytes: int, rank: int, world: int, L: int, M: int, nb: int, device: int, align: int = 0,
+                       group=None):
+    """The NVLS-capable counterpart of exchange_pools: every process's pool is
+    one shareable physical allocation (kv_pool_alloc), and peers map it
+    through its POSIX handle (kv_pool_export -> SCM_RIGHTS -> kv_pool_import)
+    instead of CUDA IPC.  One pool per process.  Returns (local PoolMem,
+    layer_base [world][L], num_blocks [world], [PoolMem imported])."""
+    mine = flykv.PoolMem.alloc(device, nbytes, align)
+    fds = {r: mine.export_fd() for r in range(world) if r != rank}
+    got = share_fds(fds, rank, {r: True for r in range(world) if r != rank}, "pool", group)
+    for fd in fds.values():
+        flykv.close_fd(fd)
+    sizes = [None] * world
+    dist.all_gather_object(sizes, mine.nbytes, group=group)
+    imported, bases = [], []
+    for r in range(world):
+        if r == rank:
+            base = mine.ptr
+        else:
+            pm = flykv.PoolMem.import_fd(got[r], sizes[r], device)
+            flykv.close_fd(got[r])
+            imported.append(pm)
+            base = pm.ptr
+        bases.append([base + l * nb * M for l in range(L)])
+    return mine, bases, [nb] * world, imported
+
+
+def setup_multicast_teams(cache, pool: "flykv.PoolMem", rank: int, world: int, team_size: int, L: int, M: int,
+                          nb: int, device: int, group=None):
+    """N2: bind the pools of every aligned replica team of `team_size`
+    processes (one pool per process) to one NVLS multicast object and
+    register this process's team in the cache (kv_cache_set_multicast).
+    Order per the header: leader creates -> fd to members -> import ->
+    add_device (all) -> bind (all) -> map.  Returns the Multicast object."""
+    lead = rank - rank % team_size
+    members = list(range(lead, lead + team_size))
+    if rank == lead:
+        mc = flykv.Multicast.create(team_size, pool.nbytes)
+        send = {r: mc.fd for r in members if r != rank}
+        share_fds(send, rank, {}, f"mc{team_size}", group)
+    else:
+        got = share_fds({}, rank, {lead: True}, f"mc{team_size}", group)
+    sizes = [None] * world
+    dist.all_gather_object(sizes, mc.nbytes if rank == lead else 0, group=group)
+    if rank != lead:
+        mc = flykv.Multicast.import_fd(got[lead], sizes[lead], team_size)
+        flykv.close_fd(got[lead])
+    mc.add_device(device)
+    dist.barrier(group=group)          # every member added before any binds
+    mc.bind(pool)
+    dist.barrier(group=group)
+    va = mc.map(device)
+    cache.set_multicast((lead, team_size), [va + l * nb * M for l in range(L)], 1)
+    if rank == lead and mc.fd >= 0:
+        flykv.close_fd(mc.fd)
+    return mc
+
+
 class DeviceBarrier:
     """a5 between processes, on the device (kv_group_barrier).
 

@@ -92,6 +92,16 @@ struct kv_cache {
     int32_t work_order = 1;
     // strict replica mode (kv_cache_set_strict, R10)
     int32_t strict = 0;
+    // NVLS multicast teams of this process (kv_cache_set_multicast, N2):
+    // mc_team[g] = size of the team whose first pool is g (0 = none),
+    // mc_base[g*L + l] its layer-l multicast address; device copies uploaded
+    // before the next reshard when dirty
+    std::vector<int32_t> mc_team;
+    std::vector<void*> mc_base;
+    int32_t mc_mode = 0;
+    bool mc_dirty = false;
+    char** d_mc_base = nullptr;
+    int32_t* d_mc_team = nullptr;
 };
 
 struct ReqPlan {
@@ -293,6 +303,8 @@ extern "C" void kv_cache_destroy(kv_cache* c) {
     }
     if (c->back) cudaFreeHost(c->back);
     if (c->d_layer_base) cudaFree(c->d_layer_base);
+    if (c->d_mc_base) cudaFree(c->d_mc_base);
+    if (c->d_mc_team) cudaFree(c->d_mc_team);
     if (c->pool) cudaMemPoolDestroy(c->pool);
     delete c;
 }
@@ -774,6 +786,42 @@ static void layout_workspace(kv_plan* p) {
     p->dbytes = align(p->off_items + p->items.size() * sizeof(A2AItem));
 }
 
+extern "C" kv_status kv_cache_set_multicast(kv_cache* c, kv_group team, void* const* layer_base, int32_t mode) {
+    if (!c || (mode != 1 && mode != 2)) return fail(KV_ERR_INVALID_ARG, "bad kv_cache_set_multicast arguments");
+    const int32_t n = c->n_gpus, L = c->geo.num_layers;
+    if (team.degree < 2 || team.first_gpu < 0 || team.first_gpu % team.degree || team.first_gpu + team.degree > n)
+        return fail(KV_ERR_INVALID_ARG, "team [%d, +%d) is not an aligned group of >= 2 pools", team.first_gpu,
+                    team.degree);
+    if (c->mc_mode && c->mc_mode != mode)
+        return fail(KV_ERR_INVALID_ARG, "teams of one cache share one mode (%d registered)", c->mc_mode);
+    if (c->mc_team.empty()) {
+        c->mc_team.assign(n, 0);
+        c->mc_base.assign((size_t)n * L, nullptr);
+    }
+    for (int32_t l = 0; l < L; ++l) {
+        if (layer_base && !layer_base[l]) return fail(KV_ERR_INVALID_ARG, "layer %d multicast base is NULL", l);
+        c->mc_base[(size_t)team.first_gpu * L + l] = layer_base ? layer_base[l] : nullptr;
+    }
+    c->mc_team[team.first_gpu] = layer_base ? team.degree : 0;
+    bool any = false;
+    for (int32_t x : c->mc_team) any = any || x;
+    c->mc_mode = any ? mode : 0;
+    c->mc_dirty = true;
+    return KV_OK;
+}
+
+// Device copies of the multicast team tables (kv_cache_set_multicast).
+static kv_status ensure_mc(kv_cache* c) {
+    if (!c->mc_dirty || c->mc_team.empty()) return KV_OK;
+    const int32_t n = c->n_gpus, L = c->geo.num_layers;
+    if (!c->d_mc_base) CUDA_TRY(cudaMalloc(&c->d_mc_base, (size_t)n * L * sizeof(void*)));
+    if (!c->d_mc_team) CUDA_TRY(cudaMalloc(&c->d_mc_team, (size_t)n * sizeof(int32_t)));
+    CUDA_TRY(cudaMemcpy(c->d_mc_base, c->mc_base.data(), (size_t)n * L * sizeof(void*), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(c->d_mc_team, c->mc_team.data(), (size_t)n * sizeof(int32_t), cudaMemcpyHostToDevice));
+    c->mc_dirty = false;
+    return KV_OK;
+}
+
 extern "C" kv_status kv_cache_set_strict(kv_cache* c, int32_t strict) {
     if (!c || (strict != 0 && strict != 1)) return fail(KV_ERR_INVALID_ARG, "bad kv_cache_set_strict arguments");
     c->strict = strict;
@@ -965,6 +1013,13 @@ extern "C" kv_status kv_reshard_range(kv_plan* p, int32_t gpu_lo, int32_t gpu_hi
     if (s) return s;
     p->last_stream = stream;
     ReshardArgs a = reshard_args(p, gpu_lo, gpu_hi);
+    s = ensure_mc(p->c);
+    if (s) return s;
+    if (p->c->mc_mode && (p->c->atom_bytes == 4096 || p->c->atom_bytes == 2048)) {  // NVLS team stores
+        a.mc_base = p->c->d_mc_base;
+        a.mc_team = p->c->d_mc_team;
+        a.mc_mode = p->c->mc_mode;
+    }
     // a share of the pools (one process per GPU): destinations may be peer
     // pools, released system-wide before the group barrier
     const bool part = gpu_lo > 0 || gpu_hi < n;

@@ -113,6 +113,12 @@ struct ReshardArgs {
     int32_t staged;            // comparator only: 0 fused, 1 pack into staging, 2 unpack from staging
     char* staging;             // atom (i - atom_lo) at staging + (i - atom_lo) * atom_bytes
     int32_t rep_flags;         // GQA replica stores: bit 0 = decode replicas lane-parallel, bit 1 = replica-major order
+    // NVLS multicast teams (kv_cache_set_multicast): mc_team[g] = size of the
+    // replica team whose first pool is g (0 = none registered), mc_base[g*L + l]
+    // its layer-l multicast address; mc_mode 1 = multimem.st, 2 = emulation (st.global)
+    char* const* mc_base;
+    const int32_t* mc_team;
+    int32_t mc_mode;
     // staged == 3 (kv_pack): every (atom, replica) goes to the send chunk of
     // its destination GPU d at a2a_buf + a2a_off[d] + (base + pos) * atom_bytes,
     // base = a2a_base[seg.a2a + member], pos = a2a_pos(...) (flykv_kernels.cu)

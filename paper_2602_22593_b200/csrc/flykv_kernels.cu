@@ -33,6 +33,13 @@ __device__ __forceinline__ void st_stream(int4* p, const int4& v) {
                  : "memory");
 }
 
+// One 16-byte store through an NVLS multicast address: NVSwitch writes it to
+// every pool bound to the multicast object (the bits are stored as is).
+__device__ __forceinline__ void st_multimem(int4* p, const int4& v) {
+    asm volatile("multimem.st.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
 // Decoded atom: source pointer plus what is needed to form each
 // destination replica's pointer (kept in scalars, no local arrays).
 struct AtomAddr {
@@ -176,7 +183,7 @@ struct LaneAtom {
     int32_t rep1;
 };
 
-template <bool MIX>
+template <bool MIX, bool MC = false>
 __device__ __forceinline__ void lane_decode(const ReshardArgs& a, int64_t slot, LaneAtom& la) {
     const int64_t atom = unmix<MIX>(a, slot);
     if (atom < 0) {  // hole of the mixed order
@@ -192,6 +199,18 @@ __device__ __forceinline__ void lane_decode(const ReshardArgs& a, int64_t slot, 
     la.src = ad.src;
     la.rep1 = ad.rep1;
     la.dst0 = ad.src ? dst_ptr(a, ad, 0) : nullptr;
+    if constexpr (MC) {
+        // NVLS: the replicas of head h are the team [dst_g0 + h*rep1, +rep1)
+        // (identity rank IDs); if this process registered that team, one
+        // multimem store (rep1 = -1) replaces the rep1 per-replica stores
+        if (ad.rep1 > 1 && ad.dst_inv < 0 && a.staged == 0) {
+            const int32_t team = ad.dst_g0 + ad.h * ad.rep1;
+            if (__ldg(a.mc_team + team) == ad.rep1) {
+                la.dst0 = a.mc_base[(int64_t)team * a.L + ad.l] + ad.doff;
+                la.rep1 = -1;
+            }
+        }
+    }
     if ((a.staged == 1 || a.staged == 2) && la.rep1 > 0) {  // comparator: slot-order pack or unpack
         char* stg = a.staging + (slot - a.atom_lo) * (int64_t)a.atom_bytes;
         if (a.staged == 1) {
@@ -234,7 +253,7 @@ __device__ __forceinline__ int round_len(const ReshardArgs& a, int64_t R, int64_
     return span < 32 ? (int)span : 32;
 }
 
-template <int VPL, int U, bool MIX>
+template <int VPL, int U, bool MIX, bool MC = false>
 __global__ void __launch_bounds__(256, 2) flykv_reshard_kernel(const ReshardArgs a) {
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -250,7 +269,7 @@ __global__ void __launch_bounds__(256, 2) flykv_reshard_kernel(const ReshardArgs
         int64_t R = a.atom_lo;
         int n = round_len(a, R, warp, nwarps);
         LaneAtom la;
-        if (lane < n) lane_decode<MIX>(a, R + warp + lane * nwarps, la);
+        if (lane < n) lane_decode<MIX, MC>(a, R + warp + lane * nwarps, la);
         while (n > 0) {
             const int64_t first = R + warp;
             const int64_t Rn = R + 32 * nwarps;
@@ -275,7 +294,7 @@ __global__ void __launch_bounds__(256, 2) flykv_reshard_kernel(const ReshardArgs
 #pragma unroll
                     for (int i = 0; i < VPL; ++i) v[u][i] = ld_stream(src + i * 32);
                 }
-                if (k0 == 0 && lane < nn) lane_decode<MIX>(a, Rn + warp + lane * nwarps, nx);
+                if (k0 == 0 && lane < nn) lane_decode<MIX, MC>(a, Rn + warp + lane * nwarps, nx);
                 // GQA replicas (p > H): lane j decodes replica j's pointer, all
                 // replicas of an atom in one parallel pass while its loads are
                 // in flight; the stores receive them by shuffle
@@ -293,6 +312,20 @@ __global__ void __launch_bounds__(256, 2) flykv_reshard_kernel(const ReshardArgs
                                                  : replica_ptr<MIX>(a, first + (int64_t)(k0 + u) * nwarps, j);
                     return reinterpret_cast<int4*>(dj) + lane;
                 };
+                if constexpr (MC) {  // NVLS team stores: one (multicast) store per atom
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        if (rep[u] >= 0) continue;
+                        int4* dst = reinterpret_cast<int4*>(d0[u]) + lane;
+                        if (a.mc_mode == 1) {
+#pragma unroll
+                            for (int i = 0; i < VPL; ++i) st_multimem(dst + i * 32, v[u][i]);
+                        } else {
+#pragma unroll
+                            for (int i = 0; i < VPL; ++i) st_stream(dst + i * 32, v[u][i]);
+                        }
+                    }
+                }
                 if (a.rep_flags & 2) {  // replica-major: replica j of all U atoms, then j + 1
                     int maxr = 0;
 #pragma unroll
@@ -658,6 +691,13 @@ static cudaError_t launch_ldg(const ReshardArgs& a_in, int device, cudaStream_t 
     int64_t cap = (int64_t)sm_count_of(device) * per;
     int grid = (int)(want < cap ? want : cap);
     if (grid < 1) grid = 1;
+    if constexpr (VPL > 0 && U > 1) {  // NVLS team stores (kv_cache_set_multicast)
+        if (a.mc_mode) {
+            if (a.mixed) flykv_reshard_kernel<VPL, U, true, true><<<grid, threads, 0, s>>>(a);
+            else flykv_reshard_kernel<VPL, U, false, true><<<grid, threads, 0, s>>>(a);
+            return cudaGetLastError();
+        }
+    }
     if (a.mixed) flykv_reshard_kernel<VPL, U, true><<<grid, threads, 0, s>>>(a);
     else flykv_reshard_kernel<VPL, U, false><<<grid, threads, 0, s>>>(a);
     return cudaGetLastError();
@@ -722,7 +762,7 @@ static cudaError_t launch_tma_shape(const ReshardArgs& a, int device, cudaStream
 cudaError_t launch_reshard(const ReshardArgs& a, int device, cudaStream_t s) {
     if (a.atom_hi <= a.atom_lo) return cudaSuccess;
     const bool tma_ok = (a.atom_bytes % 16) == 0 && a.atom_bytes <= 16384;
-    if (g_impl == 2 && tma_ok && !a.peer) return launch_tma_shape(a, device, s);
+    if (g_impl == 2 && tma_ok && !a.peer && !a.mc_mode) return launch_tma_shape(a, device, s);
     // GQA replication with >= 8 replicas (p/H, R2) into local pools: 8/9 of
     // the traffic is writes, and the TMA ring with lane-parallel replica bulk
     // stores at 2 warps per SM (4 stages, 2 atoms ahead) writes them fastest:
@@ -734,7 +774,7 @@ cudaError_t launch_reshard(const ReshardArgs& a, int device, cudaStream_t s) {
         const char* e = getenv("FLYKV_REP_TMA");
         rep_tma = e ? atoi(e) : 1;
     }
-    if (g_impl == 0 && rep_tma && a.max_rep >= 8 && tma_ok && !a.peer && a.staged != 1 && a.staged != 2)
+    if (g_impl == 0 && rep_tma && a.max_rep >= 8 && tma_ok && !a.peer && !a.mc_mode && a.staged != 1 && a.staged != 2)
         return launch_tma<4, 2>(a, device, s, 1);
     // default (0) and 3: two atoms in flight per warp (measured +1%)
     if ((g_impl == 0 || g_impl == 3) && a.atom_bytes == 4096) return launch_ldg<8, 2>(a, device, s);

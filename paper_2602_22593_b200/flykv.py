@@ -166,6 +166,22 @@ _sig("kv_ipc_export", C.c_int, _P, C.POINTER(C.c_uint8), C.POINTER(C.c_uint64))
 _sig("kv_ipc_import", C.c_int, C.POINTER(C.c_uint8), C.c_uint64, C.POINTER(_P))
 _sig("kv_ipc_close", C.c_int, _P, C.c_uint64)
 _sig("kv_stream_sync", C.c_int, _P)
+_U64P = C.POINTER(C.c_uint64)
+_sig("kv_pool_alloc", C.c_int, C.c_int32, C.c_uint64, C.c_uint64, C.POINTER(_P), C.POINTER(_P))
+_sig("kv_pool_export", C.c_int, _P, _I32P)
+_sig("kv_pool_import", C.c_int, C.c_int32, C.c_uint64, C.c_int32, C.POINTER(_P), C.POINTER(_P))
+_sig("kv_pool_free", C.c_int, _P)
+_sig("kv_mc_supported", C.c_int, C.c_int32, C.c_uint64, _I32P, _U64P)
+_sig("kv_mc_create", C.c_int, C.c_int32, C.c_uint64, C.POINTER(_P), _I32P)
+_sig("kv_mc_import", C.c_int, C.c_int32, C.c_uint64, C.c_int32, C.POINTER(_P))
+_sig("kv_mc_add_device", C.c_int, _P, C.c_int32)
+_sig("kv_mc_bind", C.c_int, _P, _P)
+_sig("kv_mc_map", C.c_int, _P, C.c_int32, C.POINTER(_P))
+_sig("kv_mc_free", C.c_int, _P)
+_sig("kv_close_fd", C.c_int, C.c_int32)
+_sig("kv_pool_size", C.c_int, _P, _U64P)
+_sig("kv_mc_size", C.c_int, _P, _U64P)
+_sig("kv_cache_set_multicast", C.c_int, _P, Group, C.POINTER(_P), C.c_int32)
 _sig("kv_strerror", C.c_char_p, C.c_int)
 _sig("kv_last_error", C.c_char_p)
 _sig("kv_launch_count", C.c_int64)
@@ -184,7 +200,10 @@ EXPORTED = ["kv_cache_create", "kv_cache_destroy", "kv_layout", "kv_blocks_for",
             "weight_shard_view", "kv_gather_view", "kv_vmm_granularity", "kv_vmm_alloc", "kv_vmm_free",
             "weight_view_alias", "weight_view_unalias", "kv_paged_decode", "kv_ipc_export", "kv_ipc_import", "kv_ipc_close",
             "kv_group_barrier", "kv_stream_sync", "kv_strerror", "kv_last_error", "kv_launch_count", "kv_set_reshard_impl",
-            "kv_cache_set_work_order", "kv_plan_work_order", "kv_cache_set_strict", "kv_verify_replicas"]
+            "kv_cache_set_work_order", "kv_plan_work_order", "kv_cache_set_strict", "kv_verify_replicas",
+            "kv_pool_alloc", "kv_pool_export", "kv_pool_import", "kv_pool_free", "kv_mc_supported", "kv_mc_create",
+            "kv_mc_import", "kv_mc_add_device", "kv_mc_bind", "kv_mc_map", "kv_mc_free", "kv_close_fd",
+            "kv_cache_set_multicast", "kv_pool_size", "kv_mc_size"]
 
 
 # ----------------------------------------------------------------- marshalling
@@ -301,6 +320,14 @@ class KVCache:
     def set_strict(self, strict: bool = True):
         """R10 strict mode: kv_switch* verify replicated sources first (kv_cache_set_strict)."""
         _check(_lib.kv_cache_set_strict(self._h, int(bool(strict))))
+
+    def set_multicast(self, team, layer_base, mode: int = 1):
+        """Register (or, layer_base None, clear) the NVLS multicast mapping of
+        replica team (first_pool, size) -- kv_cache_set_multicast."""
+        arr = None
+        if layer_base is not None:
+            arr = (C.c_void_p * len(layer_base))(*[ptr_of(p) for p in layer_base])
+        _check(_lib.kv_cache_set_multicast(self._h, Group(*team), arr, mode))
 
     def set_work_order(self, order: int):
         """1 = destination-rotated (default), 0 = plan order (kv_cache_set_work_order)."""
@@ -739,3 +766,110 @@ def kv_group_barrier(flags, self_index: int, target: int, timeout_ns: int, statu
 
 def stream_sync(stream=None):
     _check(_lib.kv_stream_sync(stream_of(stream)))
+
+
+# ----------------------------------------------------------------- NVLS (N2)
+class PoolMem:
+    """One pool in a single shareable physical allocation (kv_pool_alloc /
+    kv_pool_import): .ptr device address, .nbytes; tensor() views it."""
+
+    def __init__(self, handle, ptr: int, nbytes: int, device: int):
+        self._h = handle
+        self.ptr = ptr
+        self.nbytes = nbytes
+        self.device = device
+
+    @classmethod
+    def alloc(cls, device: int, nbytes: int, align: int = 0) -> "PoolMem":
+        h, p, n = C.c_void_p(), C.c_void_p(), C.c_uint64()
+        _check(_lib.kv_pool_alloc(device, nbytes, align, C.byref(h), C.byref(p)))
+        _check(_lib.kv_pool_size(h, C.byref(n)))
+        return cls(h, int(p.value), int(n.value), device)
+
+    @classmethod
+    def import_fd(cls, fd: int, nbytes: int, device: int) -> "PoolMem":
+        h, p = C.c_void_p(), C.c_void_p()
+        _check(_lib.kv_pool_import(fd, nbytes, device, C.byref(h), C.byref(p)))
+        return cls(h, int(p.value), nbytes, device)
+
+    def export_fd(self) -> int:
+        fd = C.c_int32()
+        _check(_lib.kv_pool_export(self._h, C.byref(fd)))
+        return fd.value
+
+    def tensor(self, shape=None):
+        """A torch uint8 tensor aliasing the pool (no copy); shape may cover
+        less than the (granularity-rounded) allocation."""
+        import torch
+
+        class _Cai:
+            def __init__(s, ptr, n):
+                s.__cuda_array_interface__ = {"shape": (n,), "typestr": "|u1", "data": (ptr, False), "version": 3}
+        t = torch.as_tensor(_Cai(self.ptr, self.nbytes), device=f"cuda:{self.device}")
+        if shape is None:
+            return t
+        n = 1
+        for x in shape:
+            n *= x
+        return t[:n].view(*shape)
+
+    def free(self):
+        if getattr(self, "_h", None):
+            _lib.kv_pool_free(self._h)
+            self._h = None
+
+
+def mc_supported(n_devices: int, nbytes: int):
+    """(ok, granularity, reason): can the driver create an NVLS multicast
+    object for a team of n_devices (kv_mc_supported)?"""
+    ok, g = C.c_int32(), C.c_uint64()
+    st = _lib.kv_mc_supported(n_devices, nbytes, C.byref(ok), C.byref(g))
+    return bool(ok.value), int(g.value), ("" if st == KV_OK else _lib.kv_last_error().decode())
+
+
+class Multicast:
+    """An NVLS multicast object of one replica team (kv_mc_*)."""
+
+    def __init__(self, handle, fd: int = -1):
+        self._h = handle
+        self.fd = fd
+        self.va = 0
+
+    @classmethod
+    def create(cls, n_devices: int, nbytes: int) -> "Multicast":
+        h, fd = C.c_void_p(), C.c_int32()
+        _check(_lib.kv_mc_create(n_devices, nbytes, C.byref(h), C.byref(fd)))
+        return cls(h, fd.value)
+
+    @property
+    def nbytes(self) -> int:
+        n = C.c_uint64()
+        _check(_lib.kv_mc_size(self._h, C.byref(n)))
+        return int(n.value)
+
+    @classmethod
+    def import_fd(cls, fd: int, nbytes: int, n_devices: int) -> "Multicast":
+        h = C.c_void_p()
+        _check(_lib.kv_mc_import(fd, nbytes, n_devices, C.byref(h)))
+        return cls(h)
+
+    def add_device(self, device: int):
+        _check(_lib.kv_mc_add_device(self._h, device))
+
+    def bind(self, pool: PoolMem):
+        _check(_lib.kv_mc_bind(self._h, pool._h))
+
+    def map(self, device: int) -> int:
+        p = C.c_void_p()
+        _check(_lib.kv_mc_map(self._h, device, C.byref(p)))
+        self.va = int(p.value)
+        return self.va
+
+    def free(self):
+        if getattr(self, "_h", None):
+            _lib.kv_mc_free(self._h)
+            self._h = None
+
+
+def close_fd(fd: int):
+    _lib.kv_close_fd(fd)

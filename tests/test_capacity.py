@@ -46,3 +46,20 @@ def test_monotone_in_degree():
 def test_relayout_reserve():
     # 128K-token Llama-3.1-8B request promoted to TP8: ceil(131072/128) blocks x 64 KiB x 32 layers per rank
     assert cap.relayout_reserve_bytes(131072, 32, 8, 128, 16, 4, 8) == 1024 * 65536 * 32
+
+
+def test_table2_at_b200_memory():
+    """The B200 table (capacity.table2 with the box's measured total memory,
+    profiles/r02_n4_pool_capacity.json): the H200 model rows reproduce the
+    paper's Table 2, KV bytes per token come from kv_layout, and
+    the B200 rows scale by the memory ratio (weights unchanged)."""
+    t = cap.table2(191502876672)
+    assert t["kv_bytes_per_token"] == KV70
+    model = [r["model_h200_tokens"] for r in t["rows"]]
+    assert model[0] == 264000 and model[1] == 959000
+    assert model[2] == pytest.approx(2.3e6, rel=0.03) and model[3] == pytest.approx(1.9e6, rel=1e-3)
+    b200 = [r["tokens"] for r in t["rows"]]
+    assert b200 == sorted(b200[:3]) + [b200[3]] and all(x % 16 == 0 for x in b200)
+    assert b200[2] > b200[3] > b200[1]          # dynamic sits between static TP4 and TP8, as on H200
+    # per-GPU bytes scale with total memory at the fitted utilisation
+    assert t["per_gpu_bytes"] == pytest.approx(t["utilisation_of_total"] * 191502876672)

@@ -20,7 +20,8 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 GEO = (3, 8, 128, 16, 2)
-GEOS = {"dp_tp": (3, 8, 128, 16, 2), "tp_dp": (3, 8, 128, 16, 2), "gqa": (2, 2, 128, 16, 2), "tp_tp": (2, 8, 64, 16, 2)}
+GEOS = {"dp_tp": (3, 8, 128, 16, 2), "tp_dp": (3, 8, 128, 16, 2), "gqa": (2, 2, 128, 16, 2), "tp_tp": (2, 8, 64, 16, 2),
+        "gqa1": (2, 1, 128, 16, 2)}
 
 
 def _free_port():
@@ -61,7 +62,19 @@ def _rank(rank, world, port, outdir, kind, mode="push", v=1):
         n1 = [F.kv_blocks_for(g, T, d[1]) for T, d in zip(w.T, w.dst)]
         nb, tabs = synth.realistic_pools(w, n0, n1)
         mine = range(rank * v, (rank + 1) * v)   # the pools this process owns
-        pool = torch.empty((v, w.L, nb[rank], M), dtype=torch.uint8, device="cuda:0")
+        dev = int(os.environ.get("FLYKV_TEST_DEVICE_OF_RANK", "0")) and rank or 0
+        torch.cuda.set_device(dev)
+        vmm = None
+        if mode in ("vmm", "nvls"):   # pools in shareable VMM memory, mapped by peers through POSIX handles
+            align = 0
+            if mode == "nvls":
+                ok, align, why = F.mc_supported(w.n_gpus // w.H if w.n_gpus > w.H else 2, w.L * nb[rank] * M)
+                assert ok, why
+            vmm, bases_v, nbs_v, imported_v = comm.exchange_pools_vmm(w.L * nb[rank] * M, rank, world, w.L, M,
+                                                                      nb[rank], dev, align)
+            pool = vmm.tensor((1, w.L, nb[rank], M))
+        else:
+            pool = torch.empty((v, w.L, nb[rank], M), dtype=torch.uint8, device=f"cuda:{dev}")
         for k, gp in enumerate(mine):
             synth.fill_hash_torch(pool[k], gp)
         if w.src[0][1] > w.H:  # GQA replicated sources: replicas identical (R10)
@@ -71,13 +84,18 @@ def _rank(rank, world, port, outdir, kind, mode="push", v=1):
             bases = [[pool[0, l].data_ptr() if r == rank else (1 << 44) + (r << 36) + (l << 30) for l in range(w.L)]
                      for r in range(world)]
             nbs, imported = nb, []
+        elif vmm is not None:
+            bases, nbs, imported = bases_v, nbs_v, []
         else:
             bases, nbs, imported = comm.exchange_pools(pool, rank, world, w.L, M)
         cache = F.KVCache(g, nbs, bases, [p for p in (2, 4, 8) if p <= world * v])
-        barrier = comm.DeviceBarrier(rank, world, [tuple(range(world))], "cuda:0", timeout_s=60)
+        mcs = []
+        if mode == "nvls":   # one multicast team per aligned replica group (N2)
+            mcs.append(comm.setup_multicast_teams(cache, vmm, rank, world, world // w.H, w.L, M, nb[rank], dev))
+        barrier = comm.DeviceBarrier(rank, world, [tuple(range(world))], f"cuda:{dev}", timeout_s=60)
         for s_, ids in zip(w.src, tabs):
             cache.reserve(s_, ids)
-        stream = torch.cuda.Stream()
+        stream = torch.cuda.Stream(f"cuda:{dev}")
         plan = F.kv_plan_switch(cache, [(i, T, s_, ids, d) for i, (T, s_, d, ids) in
                                         enumerate(zip(w.T, w.src, w.dst, tabs))])
         if mode == "a2a":  # pack -> all_to_all_single (gloo, host copies) -> unpack
@@ -98,9 +116,9 @@ def _rank(rank, world, port, outdir, kind, mode="push", v=1):
         out = {}
         for gp in mine:
             n_res, n_ids = plan.resident(gp)
-            rp = torch.empty(n_res + 1, dtype=torch.int32, device="cuda:0")
-            ids = torch.empty(max(n_ids, 1), dtype=torch.int32, device="cuda:0")
-            meta = torch.empty((max(n_res, 1), 4), dtype=torch.int32, device="cuda:0")
+            rp = torch.empty(n_res + 1, dtype=torch.int32, device=f"cuda:{dev}")
+            ids = torch.empty(max(n_ids, 1), dtype=torch.int32, device=f"cuda:{dev}")
+            meta = torch.empty((max(n_res, 1), 4), dtype=torch.int32, device=f"cuda:{dev}")
             F.kv_remap_block_tables(plan, gp, rp, ids, meta, stream)
             out[gp] = (rp, ids[:n_ids], meta[:n_res])
         # a second barrier on the same counters: nobody reads pools before every
@@ -117,6 +135,14 @@ def _rank(rank, world, port, outdir, kind, mode="push", v=1):
         dist.barrier()
         barrier.close()
         comm.close_pools(imported)
+        for m_ in mcs:
+            m_.free()
+        if vmm is not None:
+            del pool
+            for pm in imported_v:
+                pm.free()
+            dist.barrier()
+            vmm.free()
     finally:
         dist.destroy_process_group()
 
@@ -128,7 +154,8 @@ def _rank(rank, world, port, outdir, kind, mode="push", v=1):
                                                (4, "tp_tp", "a2a", 1), (8, "dp_tp", "push", 1),
                                                (8, "gqa", "push", 1), (8, "tp_tp", "a2a", 1),
                                                (2, "dp_tp", "push", 4), (4, "dp_tp", "push", 2),
-                                               (2, "tp_dp", "push", 2), (2, "gqa", "push", 4)])
+                                               (2, "tp_dp", "push", 2), (2, "gqa", "push", 4),
+                                               (2, "dp_tp", "vmm", 1), (4, "gqa", "vmm", 1), (4, "tp_tp", "vmm", 1)])
 def test_ipc_push_matches_oracle(world, kind, mode, v):
     """push: every process's reshard kernel (kv_reshard_range over the v
     pools it owns) stores into peer pools (CUDA IPC), then kv_group_barrier.
@@ -170,3 +197,26 @@ def test_ipc_push_matches_oracle(world, kind, mode, v):
             assert np.array_equal(np.load(os.path.join(td, f"rp{r}.npy")), rp)
             assert np.array_equal(np.load(os.path.join(td, f"ids{r}.npy")), ids)
             assert np.array_equal(np.load(os.path.join(td, f"meta{r}.npy")), meta)
+
+
+def test_nvls_multicast_parity():
+    """N2 on NVLS hardware: one process per GPU, pools in shareable VMM
+    memory bound to one multicast object per replica team, DP -> TP with
+    H_kv < world: the kernel writes every replicated
+    atom once through the team's multimem mapping.  Whole pools equal the
+    oracle.  (H_kv = 1: one team of `world` GPUs.)  Needs >= 2 GPUs whose
+    driver creates multicast objects; skips
+    with the driver's reason otherwise."""
+    F = __import__("paper_2602_22593_b200.flykv", fromlist=["flykv"])
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip(f"NVLS multicast needs >= 2 GPUs ({n} visible)")
+    ok, _, why = F.mc_supported(2, 64 << 20)
+    if not ok:
+        pytest.skip(f"multicast unavailable: {why}")
+    world = 4 if n >= 4 else 2
+    os.environ["FLYKV_TEST_DEVICE_OF_RANK"] = "1"
+    try:
+        test_ipc_push_matches_oracle(world, "gqa1", "nvls", 1)
+    finally:
+        os.environ.pop("FLYKV_TEST_DEVICE_OF_RANK", None)

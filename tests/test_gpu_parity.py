@@ -887,3 +887,63 @@ def test_strict_replica_mode():
                         a = before[g0].view(-1)[l * nb[g0] * M + o0:][:n]
                         b = eng.pools.tensors[g1].view(-1)[l * nb[g1] * M + o1:][:n]
                         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("H,teams", [(1, [(0, 8)]), (2, [(4, 4)]), (4, [(2, 2), (6, 2)])])
+def test_multicast_team_addressing_emulated(H, teams):
+    """NVLS team stores (N2) without NVLS hardware: kv_cache_set_multicast in
+    emulation mode (2) registers each team's replica-0 layer bases as
+    ordinary pointers, so the kernel writes an atom whose replicas are a
+    registered team once, to the team's first pool, and skips the other
+    replicas (which the multicast fabric would deliver).  DP8 -> TP8 with
+    H_kv < 8: registered teams' first pools equal the oracle, their other
+    members stay untouched; unregistered teams get every replica."""
+    F = _F()
+    from paper_2602_22593_b200.engine import KVSwitchEngine
+    geo = (2, H, 128, 16, 2)
+    og = O.Geom(*geo)
+    nb = [320] * 8
+    eng = KVSwitchEngine(F.geometry(*geo), nb, "cuda:0")
+    for gpu, t in enumerate(eng.pools.tensors):
+        synth.fill_hash_torch(t, gpu, seed=55)
+    torch.cuda.synchronize()
+    host = [t.cpu().numpy().reshape(-1).copy() for t in eng.pools.tensors]
+    before = [h.copy() for h in host]
+    held = [np.zeros(n, dtype=np.uint8) for n in nb]
+    rng = np.random.default_rng(H)
+    reqs, oreqs = [], []
+    for i in range(12):
+        T = int(rng.integers(1, 300))
+        src = (i % 8, 1)
+        ids = oracle_alloc(eng.cache, held, src, O.num_blocks(og, T, 1))
+        reqs.append((i, T, src, ids, (0, 8)))
+        oreqs.append(O.Req(T, src, list(ids), (0, 8)))
+    bases = eng.pools.layer_base()
+    for t0, r in teams:
+        eng.cache.set_multicast((t0, r), bases[t0], mode=2)
+    plan = eng.plan(reqs)
+    F.kv_reshard(plan, -1, eng.stream)
+    torch.cuda.synchronize()
+    st, otabs = O.switch(og, host, held, oreqs)
+    assert st == 0 and [list(a) for a in plan.dst_tables()] == [list(b) for b in otabs]
+    skipped = {t0 + j for t0, r in teams for j in range(1, r)}
+    for g in range(8):
+        got = eng.pools.tensors[g].cpu().numpy().reshape(-1)
+        want = before[g] if g in skipped else host[g]
+        assert np.array_equal(got, want), f"pool {g}"
+    with pytest.raises(F.FlyKVError):
+        eng.cache.set_multicast((1, 2), bases[1], mode=2)      # not aligned
+    with pytest.raises(F.FlyKVError):
+        eng.cache.set_multicast((0, 2), bases[0], mode=1)      # one mode per cache
+
+
+def test_nvls_capability_report():
+    """kv_mc_supported answers for a team of 2 with a reason when the driver
+    refuses (this single-GPU box: cuMulticastCreate rejects every team size,
+    profiles/r02_probe_mc2.txt); with >= 2 GPUs the NVLS parity test in
+    test_gpu_multiproc.py runs instead of skipping."""
+    F = _F()
+    ok, gran, why = F.mc_supported(2, 64 << 20)
+    assert ok or why
+    if ok:
+        assert gran > 0 and gran % (2 << 20) == 0
