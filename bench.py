@@ -583,6 +583,7 @@ def run_single(args):
             e2e_payload = 0
             plan_ms = []
             enq_ms = []
+            phases = []
             for it in range(args.steps):
                 t0 = time.perf_counter()
                 if DEBUG:  # the same switch through the torch-plumbing engine, with enqueue timings
@@ -601,6 +602,8 @@ def run_single(args):
                 e2e_payload += st_["payload_bytes"]
                 d2h += d2h_b
                 plan_ms.append(0.0)
+                if not DEBUG:   # the library's own phase clock of this switch (kv_plan_stats t_*_ns)
+                    phases.append([st_[k] / 1e6 for k in ("t_plan_ns", "t_enqueue_ns", "t_wait_ns", "t_read_ns")])
             gc.enable()
             settle_switches()
             if os.environ.get("FLYKV_BENCH_DEBUG"):
@@ -614,12 +617,28 @@ def run_single(args):
                 plan_ms[it] = (time.perf_counter() - t0) * 1e3
                 p_.destroy()
             plan_ms = plan_ms[:min(args.steps, 10)]
+            tail = None
+            if phases:  # attribute the latency tail: phases of the median step vs the slowest step
+                order = np.argsort(lat_ms)
+                med, worst = int(order[len(order) // 2]), int(order[-1])
+
+                def split(k):
+                    ph = phases[k]
+                    return {"wall": round(lat_ms[k], 3), "plan": round(ph[0], 3), "enqueue": round(ph[1], 3),
+                            "device_wait": round(ph[2], 3), "table_copy": round(ph[3], 3),
+                            "python": round(lat_ms[k] - sum(ph), 3)}
+                tail = {"median_step": split(med), "slowest_step": split(worst),
+                        "device_wait_ms_p50_max": [round(float(np.percentile([p[2] for p in phases], 50)), 3),
+                                                   round(max(p[2] for p in phases), 3)],
+                        "note": "per-step host phases from the library (kv_plan_stats t_*_ns); python = wall minus "
+                                "the library's phases (marshalling, ctypes, the stream sync already done)"}
             e2e = {"value": round(e2e_payload / (sum(lat_ms) / 1e3) / 1e9, 3), "unit": "GB/s",
                    "h2d_bytes_per_step": int(h2d // len(lat_ms)), "d2h_bytes_per_step": int(d2h // len(lat_ms)),
                    "value_at_p50": round(e2e_payload / len(lat_ms) / (statistics.median(lat_ms) / 1e3) / 1e9, 3),
                    "switch_latency_ms_p50": round(statistics.median(lat_ms), 3),
                    "switch_latency_ms_p99": round(float(np.percentile(lat_ms, 99)), 3),
                    "host_plan_ms_p50": round(statistics.median(plan_ms), 3),
+                   "latency_breakdown": tail,
                    "api": ("KVSwitchEngine.switch(read_back=True)" if DEBUG else
                            "flykv.kv_switch / kv_switch_back: one C-ABI call per switch (plan, upload, "
                            "reshard, remap, one table read-back, sync); several waves: kv_switch_waves, one call "

@@ -106,6 +106,12 @@ typedef struct {
     int64_t n_buckets;      /* destination buckets of the kernels' work
                                order, summed over source GPUs
                                (kv_cache_set_work_order)                    */
+    /* host wall time of the phases of a kv_switch* call that ran this plan
+     * (0 otherwise), for attributing switch latency (R15): */
+    int64_t t_plan_ns;      /* kv_plan_switch: validate, allocate, plan     */
+    int64_t t_enqueue_ns;   /* descriptor upload + reshard + remap enqueue  */
+    int64_t t_wait_ns;      /* stream synchronisation: the device work      */
+    int64_t t_read_ns;      /* copy of the tables into the plan             */
 } kv_plan_stats;
 
 /* ---------------------------------------------------------------- cache */

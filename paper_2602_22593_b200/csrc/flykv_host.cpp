@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -1575,12 +1576,20 @@ extern "C" kv_status kv_verify_replicas(kv_plan* p, void* stream_, int64_t* mism
 // kv_switch without its read-back: plan, upload, reshard, all-pool remap into
 // plan-owned device tables (the remap commits the plan on the host).  *out
 // is set when the plan exists past planning (the caller destroys it).
+static inline int64_t now_ns() {
+    return std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now().time_since_epoch())
+        .count();
+}
+
 static kv_status switch_enqueue(kv_cache* c, const kv_request* reqs, int32_t n_reqs, cudaStream_t stream,
                                 kv_plan** out) {
     *out = nullptr;
     kv_plan* p = nullptr;
+    const int64_t t0 = now_ns();
     kv_status s = kv_plan_switch(c, reqs, n_reqs, &p);
     if (s) return s;
+    const int64_t t1 = now_ns();
+    p->st.t_plan_ns = t1 - t0;
     int32_t tot_res = 0, tot_ids = 0;
     kv_plan_resident(p, -1, &tot_res, &tot_ids);
     const int32_t n = c->n_gpus;
@@ -1614,6 +1623,7 @@ static kv_status switch_enqueue(kv_cache* c, const kv_request* reqs, int32_t n_r
     if (s) return abort_plan(s);
     // a5 is stream order here: every pool is addressable from this device
     s = kv_remap_block_tables(p, -1, p->d_out, p->d_out + p->out_rp, p->d_out + p->out_ids, stream);
+    p->st.t_enqueue_ns = now_ns() - t1;
     *out = p;  // the plan committed inside the remap call only if it got that far
     return s;
 }
@@ -1633,10 +1643,14 @@ static kv_status switch_read_back(kv_plan* p, cudaStream_t stream) {
         if (e != cudaSuccess) return cuda_fail(e, "cudaMallocHost (tables)");
         c->back_bytes = want;
     }
+    const int64_t t0 = now_ns();
     e = cudaMemcpyAsync(c->back, p->d_out, (size_t)elems * 4, cudaMemcpyDeviceToHost, stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
     if (e != cudaSuccess) return cuda_fail(e, "kv_switch table read-back");
+    const int64_t t1 = now_ns();
     p->h_out.assign(static_cast<int32_t*>(c->back), static_cast<int32_t*>(c->back) + elems);
+    p->st.t_wait_ns = t1 - t0;
+    p->st.t_read_ns = now_ns() - t1;
     return KV_OK;
 }
 

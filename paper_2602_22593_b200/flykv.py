@@ -74,7 +74,7 @@ class Request(C.Structure):
 class PlanStats(C.Structure):
     _fields_ = [(n, C.c_int64) for n in ("n_requests", "n_moving", "n_atoms", "n_atom_writes", "atom_bytes",
                                          "payload_bytes", "h2d_bytes", "n_segments", "n_atom_slots",
-                                         "n_buckets")]
+                                         "n_buckets", "t_plan_ns", "t_enqueue_ns", "t_wait_ns", "t_read_ns")]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
