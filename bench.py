@@ -584,6 +584,9 @@ def run_single(args):
             plan_ms = []
             enq_ms = []
             phases = []
+            for _ in range(max(args.warmup, 1)):   # untimed end-to-end warm-up switches
+                step_switch()
+                stream.synchronize()
             for it in range(args.steps):
                 t0 = time.perf_counter()
                 if DEBUG:  # the same switch through the torch-plumbing engine, with enqueue timings
@@ -992,6 +995,9 @@ def run_multi(args):
     h2d = d2h = 0
     e2e_payload = 0
     if not args.no_e2e:
+        for _ in range(max(args.warmup, 1)):   # untimed end-to-end warm-up switches
+            step(read_back=True)
+        torch.cuda.synchronize()
         for _ in range(args.steps):
             dist.barrier()
             t0 = time.perf_counter()

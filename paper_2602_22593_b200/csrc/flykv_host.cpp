@@ -917,6 +917,14 @@ static kv_status ensure_device(kv_plan* p, cudaStream_t stream) {
         CUDA_TRY(cudaMemPoolCreate(&c->pool, &props));
         uint64_t keep = UINT64_MAX;
         CUDA_TRY(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &keep));
+        // pinned host buffers up front (cudaMallocHost can take tens of ms:
+        // never inside a switch): the staging ring and kv_switch's landing buffer
+        for (int k = 0; k < kv_cache::kStageRing; ++k) {
+            CUDA_TRY(cudaMallocHost(&c->stage[k], (size_t)1 << 20));
+            c->stage_bytes[k] = (size_t)1 << 20;
+        }
+        CUDA_TRY(cudaMallocHost(&c->back, (size_t)1 << 20));
+        c->back_bytes = (size_t)1 << 20;
         c->dev = dev;
     }
     if (p->dbuf) {
