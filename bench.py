@@ -575,6 +575,30 @@ def run_single(args):
         kern_ms = [sum(a.elapsed_time(b) for a, b in pairs) for pairs in ev_pairs]
         plans.clear()
         clocks = clk.summary()
+        # context for the roofline: a torch device copy (a library kernel,
+        # not ours) run back to back for about as long as the timed region,
+        # on this box in this process -- the sustained copy rate next to
+        # MEASURED_PEAKS.json's burst figure (best of 10 short copies)
+        sustained = None
+        try:
+            n_cp = 2 ** 32
+            ca = torch.empty(n_cp, dtype=torch.uint8, device=dev)
+            cb = torch.empty(n_cp, dtype=torch.uint8, device=dev)
+            with torch.cuda.stream(stream):
+                for _ in range(3):
+                    cb.copy_(ca)
+                reps = max(8, int(total_ms / (2 * n_cp / 6.4e12 * 1e3)))
+                c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                c0.record(stream)
+                for _ in range(reps):
+                    cb.copy_(ca)
+                c1.record(stream)
+            torch.cuda.synchronize()
+            sustained = {"value": round(2 * n_cp * reps / (c0.elapsed_time(c1) / 1e3) / 1e9, 1), "unit": "GB/s",
+                         "how": f"torch copy_ of 4 GiB x {reps} back to back (read + write bytes), CUDA events"}
+            del ca, cb
+        except RuntimeError:
+            sustained = None
         # ------------------------------------------------ end-to-end region
         e2e = None
         lat_ms = []
@@ -709,7 +733,12 @@ def run_single(args):
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                      "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
                      "traffic_over_algorithmic_forward_launch": traffic_ratio, "peak_source": peak_src,
-                     "kernel": "flykv_reshard_kernel", "algorithmic_bytes_per_launch": int(algo_bytes)},
+                     "kernel": ("flykv_reshard_tma_kernel (>= 8 replicas, forward) / flykv_reshard_kernel"
+                                if max(max(d[1], s_[1]) for d, s_ in zip(w.dst, w.src)) >= 8 * w.H
+                                and os.environ.get("FLYKV_REP_TMA", "1") != "0" else "flykv_reshard_kernel"),
+                     "algorithmic_bytes_per_launch": int(algo_bytes),
+                     "sustained_copy_same_box": sustained,
+                     "frac_of_sustained_copy": (round(achieved / sustained["value"], 4) if sustained else None)},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,
