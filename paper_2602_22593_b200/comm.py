@@ -128,7 +128,7 @@ def _sock_name(tag: str, rank: int) -> str:
     return f"\0flykv-{os.environ.get('MASTER_PORT', '0')}-{tag}-{rank}"
 
 
-def share_fds(fds_to_send: dict, rank: int, sources: dict, tag: str, group=None):
+def share_fds(fds_to_send: dict, rank: int, sources: dict, tag: str, group=None, timeout_s: float = 120.0):
     """Send each fd in fds_to_send {dest_rank: fd} to that rank and receive
     one fd from every rank in sources {src_rank: True} over AF_UNIX SCM_RIGHTS
     (the POSIX handles of kv_pool_export / kv_mc_create).  Collective over
@@ -138,12 +138,17 @@ def share_fds(fds_to_send: dict, rank: int, sources: dict, tag: str, group=None)
     srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
     srv.bind(_sock_name(tag, rank))
     srv.listen(max(len(sources), 1))
+    srv.settimeout(timeout_s)        # a peer that never connects fails loudly, never hangs
     got = {}
 
     def serve():
         for _ in range(len(sources)):
-            conn, _ = srv.accept()
+            try:
+                conn, _ = srv.accept()
+            except OSError:
+                return
             with conn:
+                conn.settimeout(timeout_s)
                 msg, fds, _, _ = socket.recv_fds(conn, 16, 1)
                 got[int(msg.decode())] = fds[0]
     th = threading.Thread(target=serve)
@@ -151,11 +156,14 @@ def share_fds(fds_to_send: dict, rank: int, sources: dict, tag: str, group=None)
     dist.barrier(group=group)          # every server is listening
     for dst, fd in fds_to_send.items():
         c = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+        c.settimeout(timeout_s)
         c.connect(_sock_name(tag, dst))
         socket.send_fds(c, [str(rank).encode()], [fd])
         c.close()
     th.join()
     srv.close()
+    if set(got) != set(sources):
+        raise RuntimeError(f"share_fds({tag}): rank {rank} received from {sorted(got)}, expected {sorted(sources)}")
     dist.barrier(group=group)
     return got
 

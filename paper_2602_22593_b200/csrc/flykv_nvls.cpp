@@ -139,6 +139,7 @@ struct kv_mc {
     int32_t n_devices;
     CUdeviceptr va = 0;   // this process's multicast mapping (kv_mc_map)
     int bound_device = -1;
+    size_t bound_bytes = 0;
 };
 
 extern "C" kv_status kv_pool_alloc(int32_t device, uint64_t bytes, uint64_t align, kv_pool_mem** out, void** dptr) {
@@ -322,6 +323,7 @@ extern "C" kv_status kv_mc_bind(kv_mc* m, const kv_pool_mem* pool) {
     NvlsDrv& d = drv();
     NV_TRY(d.mc_bind(m->h, 0, pool->h, 0, pool->bytes, 0), "cuMulticastBindMem");
     m->bound_device = pool->device;
+    m->bound_bytes = pool->bytes;
     return KV_OK;
 }
 
@@ -350,7 +352,7 @@ extern "C" kv_status kv_mc_free(kv_mc* m) {
     }
     if (m->bound_device >= 0) {
         CUdevice dev;
-        if (d.device_get(&dev, m->bound_device) == CUDA_SUCCESS) d.mc_unbind(m->h, dev, 0, m->bytes);
+        if (d.device_get(&dev, m->bound_device) == CUDA_SUCCESS) d.mc_unbind(m->h, dev, 0, m->bound_bytes);
     }
     d.release(m->h);
     delete m;
