@@ -102,3 +102,46 @@ def test_pool_and_replicated_plans_gloo(world):
         if world == 4:
             assert o["keys"] == [(0, 1), (0, 1, 2, 3), (2, 3)]
             assert o["cover2"] == (0, 1, 2, 3)
+
+
+def _fd_worker(rank, world, port, tmpdir, q):
+    import tempfile
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # each rank opens its own file and sends its descriptor to every other rank
+        path = os.path.join(tmpdir, f"f{rank}")
+        with open(path, "w") as f:
+            f.write(f"rank {rank}")
+        fd = os.open(path, os.O_RDONLY)
+        got = comm.share_fds({r: fd for r in range(world) if r != rank}, rank,
+                             {r: True for r in range(world) if r != rank}, "test")
+        os.close(fd)
+        seen = {}
+        for src, rfd in got.items():   # pread: the receivers share one open file description
+            seen[src] = os.pread(rfd, 64, 0).decode()
+            os.close(rfd)
+        q.put((rank, seen))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_share_fds_gloo():
+    """The NVLS path's descriptor passing (comm.share_fds: SCM_RIGHTS over
+    abstract AF_UNIX sockets, the transport of kv_pool_export / kv_mc_create
+    handles) on 3 gloo ranks: every rank receives a working descriptor of
+    every other rank's file."""
+    import tempfile
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    with tempfile.TemporaryDirectory() as td:
+        procs = [ctx.Process(target=_fd_worker, args=(r, world, port, td, q)) for r in range(world)]
+        for p in procs:
+            p.start()
+        res = dict(q.get(timeout=120) for _ in range(world))
+        for p in procs:
+            p.join(timeout=60)
+    for r in range(world):
+        assert res[r] == {s: f"rank {s}" for s in range(world) if s != r}
