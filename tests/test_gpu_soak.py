@@ -59,14 +59,24 @@ SEEDS = [int(x) for x in os.environ.get("FLYKV_SOAK_SEEDS", "0,1,2").split(",")]
 ITERS = int(os.environ.get("FLYKV_SOAK_ITERS", "1200"))
 
 
-@pytest.mark.parametrize("seed", SEEDS)
-def test_serving_soak(seed):
+CASES = [(s, GEO) for s in SEEDS] + [(SEEDS[0], (2, 1, 64, 16, 2)), (SEEDS[0], (2, 2, 128, 16, 2))]
+
+
+@pytest.mark.parametrize("seed,geo", CASES)
+def test_serving_soak(seed, geo):
+    """H_kv = 8 (no replication) on every seed; H_kv = 1 and 2 (GQA
+    replication at TP > H_kv: the TMA replica kernel, replicated sources) on
+    the first seed, in strict replica mode (R10) with every other switch
+    through the one-call kv_switch, which verifies the replicas first."""
     F = pytest.importorskip("paper_2602_22593_b200.flykv")
     from paper_2602_22593_b200.engine import KVSwitchEngine
     rng = np.random.default_rng(seed)
-    og = O.Geom(*GEO)
+    og = O.Geom(*geo)
     nb = [NB] * N_GPUS
-    eng = KVSwitchEngine(F.geometry(*GEO), nb, "cuda:0")
+    eng = KVSwitchEngine(F.geometry(*geo), nb, "cuda:0")
+    strict = geo[1] < N_GPUS
+    if strict:
+        eng.cache.set_strict(True)
     dev = torch.device("cuda:0")
     flat = [t.reshape(-1).view(torch.int32) for t in eng.pools.tensors]
     atom_words = og.B * og.d * og.e // 4
@@ -119,7 +129,10 @@ def test_serving_soak(seed):
                 assert e.name == "KV_ERR_OUT_OF_BLOCKS"
                 continue
             for a, b in waves:
-                plan, tables, _ = eng.switch(reqs[a:b], read_back=True)
+                if strict and switches % 2:   # strict mode: kv_switch verifies replicated sources first
+                    plan = F.kv_switch(eng.cache, reqs[a:b], eng.stream)
+                else:
+                    plan, tables, _ = eng.switch(reqs[a:b], read_back=True)
                 st, otabs = O.switch(og, None, held, oreqs[a:b], copy=False)
                 assert st == 0
                 assert [list(x) for x in plan.dst_tables()] == [list(y) for y in otabs]
