@@ -299,6 +299,13 @@ kv_status kv_plan_resident(const kv_plan* plan, int32_t gpu, int32_t* n_resident
  * same stream, or an event the caller records.  Requests absent from the
  * plan are not listed and are untouched.
  */
+/* kv_plan_packed_offsets: where pool g's table starts in the packed outputs
+ * of kv_remap_block_tables(gpu = -1), as element offsets: out host
+ * [n_gpus * 3] = {req_ptr offset, block_ids offset, per_req_meta offset}
+ * per pool (the prefix sums stated above); totals (element counts of the
+ * three buffers) in totals host [3] or NULL.  Errors: INVALID_ARG, BAD_STATE. */
+kv_status kv_plan_packed_offsets(const kv_plan* plan, int32_t* out, int64_t* totals);
+
 kv_status kv_remap_block_tables(kv_plan* plan, int32_t gpu, int32_t* req_ptr, int32_t* block_ids,
                                 int32_t* per_req_meta, void* stream);
 

@@ -1400,6 +1400,20 @@ extern "C" kv_status kv_remap_block_tables(kv_plan* p, int32_t gpu, int32_t* req
     return KV_OK;
 }
 
+extern "C" kv_status kv_plan_packed_offsets(const kv_plan* p, int32_t* out, int64_t* totals) {
+    PLAN_CHECK(p);
+    if (!out) return fail(KV_ERR_INVALID_ARG, "out is NULL");
+    std::memcpy(out, p->out_off.data(), p->out_off.size() * sizeof(int32_t));
+    if (totals) {
+        int32_t r = 0, i = 0;
+        kv_plan_resident(p, -1, &r, &i);
+        totals[0] = (int64_t)r + p->c->n_gpus;
+        totals[1] = i;
+        totals[2] = 4 * (int64_t)r;
+    }
+    return KV_OK;
+}
+
 extern "C" kv_status kv_plan_dst_tables(const kv_plan* p, int32_t* dst_ptr, int32_t* dst_ids) {
     if (!p || !dst_ptr) return fail(KV_ERR_INVALID_ARG, "bad arguments");
     dst_ptr[0] = 0;

@@ -65,19 +65,16 @@ class KVSwitchEngine:
     def alloc_packed(self, plan: flykv.Plan):
         """Packed all-pool outputs of kv_remap_block_tables(gpu=-1) and the
         per-pool views into them: {g: GpuTable}, (req_ptr, block_ids, meta)."""
-        n = self.n_gpus
-        res = [plan.resident(g) for g in range(n)]
-        tot_res = sum(r for r, _ in res)
-        tot_ids = sum(i for _, i in res)
-        rp = torch.empty(tot_res + n, dtype=torch.int32, device=self.device)
-        ids = torch.empty(max(tot_ids, 1), dtype=torch.int32, device=self.device)
-        meta = torch.empty((max(tot_res, 1), 4), dtype=torch.int32, device=self.device)
-        views, o_r, o_i = {}, 0, 0
-        for g, (n_res, n_ids) in enumerate(res):
-            views[g] = GpuTable(rp[o_r + g:o_r + g + n_res + 1], ids[o_i:o_i + n_ids], meta[o_r:o_r + n_res])
-            o_r += n_res
-            o_i += n_ids
-        return views, (rp, ids, meta)
+        off, tot = plan.packed_offsets()        # the library's packed layout (kv_plan_packed_offsets)
+        rp = torch.empty(int(tot[0]), dtype=torch.int32, device=self.device)
+        ids = torch.empty(max(int(tot[1]), 1), dtype=torch.int32, device=self.device)
+        meta = torch.empty(max(int(tot[2]), 4), dtype=torch.int32, device=self.device)
+        views = {}
+        for g in range(self.n_gpus):
+            n_res, n_ids = plan.resident(g)
+            r0, i0, m0 = (int(x) for x in off[g])
+            views[g] = GpuTable(rp[r0:r0 + n_res + 1], ids[i0:i0 + n_ids], meta[m0:m0 + 4 * n_res].view(-1, 4))
+        return views, (rp, ids, meta.view(-1, 4))
 
     def execute(self, plan: flykv.Plan, gpus=None, tables=None):
         """Reshard every atom (one launch) and remap the tables: by default
@@ -130,12 +127,12 @@ class KVSwitchEngine:
                 if gpus is None:  # packed: three device->host copies for every pool's table
                     rp, ids, meta = (x.to("cpu", non_blocking=True) for x in self._packed)
                     self.stream.synchronize()
-                    o_r = o_i = 0
+                    off, _ = plan.packed_offsets()
+                    meta = meta.reshape(-1)
                     for g in range(self.n_gpus):
                         n_res, n_ids = plan.resident(g)
-                        host[g] = (rp[o_r + g:o_r + g + n_res + 1], ids[o_i:o_i + n_ids], meta[o_r:o_r + n_res])
-                        o_r += n_res
-                        o_i += n_ids
+                        r0, i0, m0 = (int(x) for x in off[g])
+                        host[g] = (rp[r0:r0 + n_res + 1], ids[i0:i0 + n_ids], meta[m0:m0 + 4 * n_res].view(-1, 4))
                 else:
                     for g, t in tables.items():
                         n_res, n_ids = plan.resident(g)

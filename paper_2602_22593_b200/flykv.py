@@ -151,6 +151,7 @@ _sig("kv_switch_waves", C.c_int, _P, C.POINTER(Request), C.c_int32, C.c_int64, C
      C.POINTER(Piece), _I32P, C.POINTER(_P), _I32P)
 _sig("kv_plan_get_stats", C.c_int, _P, C.POINTER(PlanStats), _I64P)
 _sig("kv_plan_a2a_offsets", C.c_int, _P, _I64P, _I64P, _I64P)
+_sig("kv_plan_packed_offsets", C.c_int, _P, _I32P, _I64P)
 _sig("kv_piece_request", C.c_int, C.POINTER(Geometry), C.POINTER(Request), C.c_int32, C.c_int32, C.POINTER(Request))
 _sig("kv_plan_destroy", None, _P)
 _sig("weight_shard_view", C.c_int, C.POINTER(WeightDesc), C.c_int32, C.c_int32, C.POINTER(View))
@@ -195,7 +196,7 @@ EXPORTED = ["kv_cache_create", "kv_cache_destroy", "kv_layout", "kv_blocks_for",
             "kv_free", "kv_free_count", "kv_held_mask", "kv_plan_switch", "kv_plan_upload", "kv_reshard", "kv_reshard_range", "kv_reshard_staged",
             "kv_pack", "kv_unpack", "kv_switch", "kv_switch_back", "kv_switch_multi", "kv_switch_waves", "kv_plan_tables", "kv_plan_resident",
             "kv_remap_block_tables", "kv_plan_dst_tables", "kv_plan_commit", "kv_plan_waves", "kv_plan_pieces",
-            "kv_suggest_rank_ids", "kv_plan_get_stats", "kv_plan_a2a_offsets", "kv_piece_request",
+            "kv_suggest_rank_ids", "kv_plan_get_stats", "kv_plan_a2a_offsets", "kv_piece_request", "kv_plan_packed_offsets",
             "kv_plan_destroy",
             "weight_shard_view", "kv_gather_view", "kv_vmm_granularity", "kv_vmm_alloc", "kv_vmm_free",
             "weight_view_alias", "weight_view_unalias", "kv_paged_decode", "kv_ipc_export", "kv_ipc_import", "kv_ipc_close",
@@ -413,6 +414,15 @@ class Plan:
         out = [np.zeros(n * n, dtype=np.int64) for _ in range(3)]
         _check(_lib.kv_plan_a2a_offsets(self._h, *(o.ctypes.data_as(_I64P) for o in out)))
         return tuple(o.reshape(n, n) for o in out)
+
+    def packed_offsets(self):
+        """(offsets int32 [n, 3], totals int64 [3]) of the packed all-pool
+        remap outputs (kv_plan_packed_offsets)."""
+        n = self.cache.n_gpus
+        off = np.zeros(3 * n, dtype=np.int32)
+        tot = np.zeros(3, dtype=np.int64)
+        _check(_lib.kv_plan_packed_offsets(self._h, off.ctypes.data_as(_I32P), tot.ctypes.data_as(_I64P)))
+        return off.reshape(n, 3), tot
 
     def work_order(self, gpu: int) -> np.ndarray:
         """[n_pieces, n_gpus + 1] int64: destination bytes per GPU of each of

@@ -600,3 +600,22 @@ def test_piece_request_slices_the_source_table():
         F.piece_request(g, req, 12, 50)
     with pytest.raises(F.FlyKVError):
         F.piece_request(g, req, 16, 101)
+
+
+def test_packed_offsets_are_the_documented_prefixes():
+    """kv_plan_packed_offsets: pool g's slice of the packed remap outputs
+    starts at req_ptr sum_{g'<g}(n_res[g'] + 1), block_ids sum n_ids[g'],
+    meta 4 * sum n_res[g'] (include/flykv.h, kv_remap_block_tables)."""
+    c = fake_cache((2, 8, 16, 4, 2), [64] * 4)
+    reqs = []
+    for i, (src, dst) in enumerate([((0, 1), (0, 4)), ((1, 1), (2, 2)), ((2, 2), (0, 1)), ((3, 1), (0, 2))]):
+        T = 11 + 9 * i
+        reqs.append((i, T, src, c.alloc(src, F.kv_blocks_for(c.geom, T, src[1])), dst))
+    plan = c.plan_switch(reqs)
+    off, tot = plan.packed_offsets()
+    res = [plan.resident(g) for g in range(4)]
+    for g in range(4):
+        assert off[g, 0] == sum(r + 1 for r, _ in res[:g])
+        assert off[g, 1] == sum(i for _, i in res[:g])
+        assert off[g, 2] == 4 * sum(r for r, _ in res[:g])
+    assert list(tot) == [sum(r for r, _ in res) + 4, sum(i for _, i in res), 4 * sum(r for r, _ in res)]
