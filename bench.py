@@ -727,6 +727,7 @@ def run_single(args):
                    "step": "plan + descriptor upload + reshard + remap (alternating direction)"},
         "switch_latency_ms": round(total_ms / args.steps, 4),
         "reshard_kernel_ms": round(kmean, 4),
+        "reshard_kernel_ms_steps": [round(x, 3) for x in kern_ms],   # per timed step (directions alternate)
         "reshard_kernel_ms_p50_p90": [round(float(np.percentile(kern_ms, 50)), 4),
                                       round(float(np.percentile(kern_ms, 90)), 4)],
         "modeled_nvlink": modeled,
