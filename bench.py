@@ -1024,14 +1024,26 @@ def run_multi(args):
     lat = []
     h2d = d2h = 0
     e2e_payload = 0
+    def step_one_call():
+        """One switch through the public one-call API for this process's
+        share (kv_switch_range: plan, upload, push, device barrier, remap of
+        the owned pools, one read-back, sync)."""
+        reqs = state["reqs"]
+        plan = F.kv_switch_range(cache, reqs, mine.start, mine.stop, barrier.arm(barrier_key(reqs)), stream)
+        _, tot = plan.packed_offsets()
+        new = plan.dst_tables()
+        state["reqs"] = [(rid, T, d, t, s_, drid, srid) for (rid, T, s_, _, d, srid, drid), t in zip(reqs, new)]
+        return plan, 4 * int(tot.sum())
+
+    e2e_step = step_one_call if not args.a2a else (lambda: step(read_back=True))
     if not args.no_e2e:
         for _ in range(max(args.warmup, 1)):   # untimed end-to-end warm-up switches
-            step(read_back=True)
+            e2e_step()
         torch.cuda.synchronize()
         for _ in range(args.steps):
             dist.barrier()
             t0 = time.perf_counter()
-            plan, hb = step(read_back=True)
+            plan, hb = e2e_step()
             lat.append((time.perf_counter() - t0) * 1e3)
             h2d += plan.stats()[0]["h2d_bytes"]
             e2e_payload += plan.stats()[0]["payload_bytes"]
@@ -1107,6 +1119,9 @@ def run_multi(args):
                      "d2h_bytes_per_step": int(d2h_all // max(len(lat), 1)),
                      "switch_latency_ms_p50": round(lat_p50, 3), "switch_latency_ms_p99": round(lat_p99, 3),
                      "switch_latency_ms_mean": round(lat_mean, 3),
+                     "api": ("flykv.kv_switch_range: one C-ABI call per rank per switch (plan, upload, push, "
+                             "device barrier, remap of the owned pools, one table read-back, sync)" if not args.a2a
+                             else "plan, kv_pack, all_to_all_single, kv_unpack, device barrier, remap, read-back"),
                      "note": "per-rank wall clock from a host barrier to its tables on the host; max over ranks"}
                     if lat else None),
             "comm_pool": pool_cost,

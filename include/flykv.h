@@ -333,6 +333,25 @@ kv_status kv_switch(kv_cache* cache, const kv_request* reqs, int32_t n_reqs, voi
  * committed; INVALID_ARG if prev belongs to another cache. */
 kv_status kv_switch_back(kv_cache* cache, const kv_plan* prev, void* stream, kv_plan** out);
 
+/*
+ * kv_switch_range: kv_switch for one process of a one-process-per-GPU job
+ * that owns pools [gpu_lo, gpu_hi) (every process calls it with the same
+ * request list): kv_plan_switch -> descriptor upload ->
+ * kv_reshard_range(gpu_lo, gpu_hi) (pushes into peer pools) ->
+ * kv_group_barrier(barrier_flags, n_members, self, barrier_target,
+ * timeout_ns, barrier_status) when n_members > 1 (a5: every member's pushes
+ * have landed) -> kv_remap_block_tables of each owned pool into the
+ * plan-owned packed buffer -> one device->host copy -> stream sync.  On
+ * KV_OK the owned pools' tables are available through kv_plan_tables (other
+ * pools' slices are not written).  Barrier arguments as for
+ * kv_group_barrier (the caller keeps the per-group counts).  Errors as
+ * kv_switch; a barrier timeout is reported by *barrier_status (or a trap
+ * when it is NULL), not by the return value.
+ */
+kv_status kv_switch_range(kv_cache* cache, const kv_request* reqs, int32_t n_reqs, int32_t gpu_lo, int32_t gpu_hi,
+                          uint64_t* const* barrier_flags, int32_t n_members, int32_t self, uint64_t barrier_target,
+                          int64_t timeout_ns, int32_t* barrier_status, void* stream, kv_plan** out);
+
 /* kv_switch_multi: a switch in waves (kv_plan_waves, or the block-aligned
  * pieces of kv_plan_pieces turned into plain requests) with no host sync
  * between the waves: each wave is planned once the previous one committed

@@ -260,14 +260,23 @@ class DeviceBarrier:
                 self.imported.append((b, o))
                 self.bases.append(b)
 
-    def wait(self, key, stream):
+    def arm(self, key):
+        """Arguments of the next barrier on `key` for a C call that runs it
+        itself (kv_switch_range): (flags, self index, target, timeout_ns,
+        status), the count advanced; None if this process has no peer in it."""
         key = tuple(key)
         if self.rank not in key or len(key) < 2:
-            return
+            return None
         self.count[key] += 1
         s = self.slot[key] * self.LINE * 8
-        flykv.kv_group_barrier([self.bases[m] + s for m in key], key.index(self.rank),
-                               self.count[key] * len(key), self.timeout_ns, self.status, stream)
+        return ([self.bases[m] + s for m in key], key.index(self.rank), self.count[key] * len(key), self.timeout_ns,
+                self.status)
+
+    def wait(self, key, stream):
+        args = self.arm(key)
+        if args is not None:
+            flags, me, target, timeout, status = args
+            flykv.kv_group_barrier(flags, me, target, timeout, status, stream)
 
     def check(self):
         """Raise if any wait timed out (a member never arrived)."""

@@ -1684,6 +1684,54 @@ extern "C" kv_status kv_switch(kv_cache* c, const kv_request* reqs, int32_t n_re
     return switch_read_back(*out, stream);
 }
 
+extern "C" kv_status kv_switch_range(kv_cache* c, const kv_request* reqs, int32_t n_reqs, int32_t gpu_lo,
+                                     int32_t gpu_hi, uint64_t* const* barrier_flags, int32_t n_members, int32_t self,
+                                     uint64_t barrier_target, int64_t timeout_ns, int32_t* barrier_status,
+                                     void* stream_, kv_plan** out) {
+    if (!c || !out) return fail(KV_ERR_INVALID_ARG, "bad kv_switch_range arguments");
+    *out = nullptr;
+    if (gpu_lo < 0 || gpu_hi > c->n_gpus || gpu_lo >= gpu_hi)
+        return fail(KV_ERR_INVALID_ARG, "pool range [%d, %d) is not inside [0, %d)", gpu_lo, gpu_hi, c->n_gpus);
+    if (n_members > 1 && !barrier_flags) return fail(KV_ERR_INVALID_ARG, "barrier_flags is NULL");
+    cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+    kv_plan* p = nullptr;
+    const int64_t t0 = now_ns();
+    kv_status s = kv_plan_switch(c, reqs, n_reqs, &p);
+    if (s) return s;
+    const int64_t t1 = now_ns();
+    p->st.t_plan_ns = t1 - t0;
+    int32_t tot_res = 0, tot_ids = 0;
+    kv_plan_resident(p, -1, &tot_res, &tot_ids);
+    p->out_rp = tot_res + c->n_gpus;
+    p->out_ids = p->out_rp + tot_ids;
+    const int64_t elems = p->out_ids + 4 * (int64_t)tot_res;
+    auto abort_plan = [&](kv_status st) {
+        kv_plan_destroy(p);
+        return st;
+    };
+    s = ensure_device(p, stream);
+    if (s) return abort_plan(s);
+    p->last_stream = stream;
+    cudaError_t e = cudaMallocFromPoolAsync(reinterpret_cast<void**>(&p->d_out), (size_t)elems * 4, c->pool, stream);
+    if (e != cudaSuccess) return abort_plan(cuda_fail(e, "cudaMallocFromPoolAsync (tables)"));
+    s = kv_reshard_range(p, gpu_lo, gpu_hi, stream);
+    if (s) return abort_plan(s);
+    if (n_members > 1) {  // a5: every member's pushes have landed before anyone remaps
+        s = kv_group_barrier(barrier_flags, n_members, self, barrier_target, timeout_ns, barrier_status, stream);
+        if (s) return abort_plan(s);
+    }
+    for (int32_t g = gpu_lo; g < gpu_hi; ++g) {  // the owned pools' tables, at their packed offsets
+        const int32_t* off = p->out_off.data() + 3 * g;
+        s = kv_remap_block_tables(p, g, p->d_out + off[0], p->d_out + p->out_rp + off[1],
+                                  p->d_out + p->out_ids + off[2], stream);
+        if (s) break;
+    }
+    p->st.t_enqueue_ns = now_ns() - t1;
+    *out = p;  // committed by the first remap call
+    if (s) return s;
+    return switch_read_back(p, stream);
+}
+
 extern "C" kv_status kv_switch_multi(kv_cache* c, const kv_request* reqs, const int32_t* wave_ptr, int32_t n_waves,
                                      void* stream_, kv_plan** plans) {
     if (!c || !wave_ptr || !plans || n_waves < 0 || (n_waves > 0 && wave_ptr[n_waves] > 0 && !reqs))

@@ -133,6 +133,8 @@ _sig("kv_remap_block_tables", C.c_int, _P, C.c_int32, _P, _P, _P, _P)
 _sig("kv_switch", C.c_int, _P, C.POINTER(Request), C.c_int32, _P, C.POINTER(_P))
 _sig("kv_plan_tables", C.c_int, _P, C.c_int32, C.c_int32, C.POINTER(_I32P), C.POINTER(_I32P), C.POINTER(_I32P))
 _sig("kv_switch_back", C.c_int, _P, _P, _P, C.POINTER(_P))
+_sig("kv_switch_range", C.c_int, _P, C.POINTER(Request), C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_void_p),
+     C.c_int32, C.c_int32, C.c_uint64, C.c_int64, _P, _P, C.POINTER(_P))
 _sig("kv_switch_multi", C.c_int, _P, C.POINTER(Request), _I32P, C.c_int32, _P, C.POINTER(_P))
 _sig("kv_pack", C.c_int, _P, C.c_int32, _P, _I64P, _P)
 _sig("kv_unpack", C.c_int, _P, C.c_int32, _P, _I64P, _P)
@@ -194,7 +196,7 @@ _sig("kv_plan_work_order", C.c_int, _P, C.c_int32, _I32P, _I64P)
 
 EXPORTED = ["kv_cache_create", "kv_cache_destroy", "kv_layout", "kv_blocks_for", "kv_alloc", "kv_reserve",
             "kv_free", "kv_free_count", "kv_held_mask", "kv_plan_switch", "kv_plan_upload", "kv_reshard", "kv_reshard_range", "kv_reshard_staged",
-            "kv_pack", "kv_unpack", "kv_switch", "kv_switch_back", "kv_switch_multi", "kv_switch_waves", "kv_plan_tables", "kv_plan_resident",
+            "kv_pack", "kv_unpack", "kv_switch", "kv_switch_back", "kv_switch_range", "kv_switch_multi", "kv_switch_waves", "kv_plan_tables", "kv_plan_resident",
             "kv_remap_block_tables", "kv_plan_dst_tables", "kv_plan_commit", "kv_plan_waves", "kv_plan_pieces",
             "kv_suggest_rank_ids", "kv_plan_get_stats", "kv_plan_a2a_offsets", "kv_piece_request", "kv_plan_packed_offsets",
             "kv_plan_destroy",
@@ -516,6 +518,28 @@ def kv_switch(cache: KVCache, requests, stream=None) -> Plan:
     st = _lib.kv_switch(cache._h, ra.ptr, ra.n, stream_of(stream), C.byref(h))
     plan = Plan(cache, h, ra.n) if h.value else None
     if st != KV_OK:  # a plan returned with an error has committed: hand it over
+        raise FlyKVError(st, _lib.kv_last_error().decode(), [plan] if plan is not None else [])
+    return plan
+
+
+def kv_switch_range(cache: KVCache, requests, gpu_lo: int, gpu_hi: int, barrier=None, stream=None) -> Plan:
+    """kv_switch for one process of a one-process-per-GPU job owning pools
+    [gpu_lo, gpu_hi): plan, upload, push, device group barrier, remap of the
+    owned pools, one read-back, sync -- one C call (kv_switch_range).
+    barrier: (flags, self_index, target, timeout_ns, status) from
+    comm.DeviceBarrier.arm(key), or None when no other process is involved."""
+    ra = make_requests(requests)
+    h = C.c_void_p()
+    if barrier is None:
+        arr, n_m, me, tgt, tmo, status = None, 0, 0, 0, 1, None
+    else:
+        flags, me, tgt, tmo, status = barrier
+        arr = (C.c_void_p * len(flags))(*[ptr_of(f) for f in flags])
+        n_m = len(flags)
+    st = _lib.kv_switch_range(cache._h, ra.ptr, ra.n, gpu_lo, gpu_hi, arr, n_m, me, int(tgt), int(tmo),
+                              ptr_of(status), stream_of(stream), C.byref(h))
+    plan = Plan(cache, h, ra.n) if h.value else None
+    if st != KV_OK:
         raise FlyKVError(st, _lib.kv_last_error().decode(), [plan] if plan is not None else [])
     return plan
 

@@ -96,9 +96,14 @@ def _rank(rank, world, port, outdir, kind, mode="push", v=1):
         for s_, ids in zip(w.src, tabs):
             cache.reserve(s_, ids)
         stream = torch.cuda.Stream(f"cuda:{dev}")
-        plan = F.kv_plan_switch(cache, [(i, T, s_, ids, d) for i, (T, s_, d, ids) in
-                                        enumerate(zip(w.T, w.src, w.dst, tabs))])
-        if mode == "a2a":  # pack -> all_to_all_single (gloo, host copies) -> unpack
+        reqs = [(i, T, s_, ids, d) for i, (T, s_, d, ids) in enumerate(zip(w.T, w.src, w.dst, tabs))]
+        if mode == "onecall":   # the public one-call API for this process's share (kv_switch_range)
+            plan = F.kv_switch_range(cache, reqs, mine.start, mine.stop, barrier.arm(tuple(range(world))), stream)
+        else:
+            plan = F.kv_plan_switch(cache, reqs)
+        if mode == "onecall":
+            pass
+        elif mode == "a2a":  # pack -> all_to_all_single (gloo, host copies) -> unpack
             _, mat = plan.stats()
             send_off, recv_off = F.a2a_offsets(plan)
             send = torch.empty(max(int(mat[rank].sum()), 16), dtype=torch.uint8, device="cuda:0")
@@ -111,10 +116,14 @@ def _rank(rank, world, port, outdir, kind, mode="push", v=1):
             F.kv_unpack(plan, rank, recv, recv_off[rank], stream)
         else:
             F.kv_reshard_range(plan, mine.start, mine.stop, stream)
-        # a5 on the device: every process's pushes have landed before anyone remaps
-        barrier.wait(tuple(range(world)), stream)
         out = {}
-        for gp in mine:
+        if mode == "onecall":   # tables the call read back (owned pools only)
+            for gp in mine:
+                rp, ids, meta = plan.host_tables(gp)
+                out[gp] = (torch.as_tensor(rp), torch.as_tensor(ids), torch.as_tensor(meta))
+        else:   # a5 on the device: every process's pushes have landed before anyone remaps
+            barrier.wait(tuple(range(world)), stream)
+        for gp in (mine if mode != "onecall" else ()):
             n_res, n_ids = plan.resident(gp)
             rp = torch.empty(n_res + 1, dtype=torch.int32, device=f"cuda:{dev}")
             ids = torch.empty(max(n_ids, 1), dtype=torch.int32, device=f"cuda:{dev}")
@@ -155,12 +164,17 @@ def _rank(rank, world, port, outdir, kind, mode="push", v=1):
                                                (8, "gqa", "push", 1), (8, "tp_tp", "a2a", 1),
                                                (2, "dp_tp", "push", 4), (4, "dp_tp", "push", 2),
                                                (2, "tp_dp", "push", 2), (2, "gqa", "push", 4),
-                                               (2, "dp_tp", "vmm", 1), (4, "gqa", "vmm", 1), (4, "tp_tp", "vmm", 1)])
+                                               (2, "dp_tp", "vmm", 1), (4, "gqa", "vmm", 1), (4, "tp_tp", "vmm", 1),
+                                               (2, "dp_tp", "onecall", 1), (4, "tp_dp", "onecall", 1),
+                                               (2, "gqa", "onecall", 4), (8, "dp_tp", "onecall", 1)])
 def test_ipc_push_matches_oracle(world, kind, mode, v):
     """push: every process's reshard kernel (kv_reshard_range over the v
     pools it owns) stores into peer pools (CUDA IPC), then kv_group_barrier.
     a2a: kv_pack into per-destination chunks, all_to_all_single (gloo over
-    host copies here; NCCL on GPUs), kv_unpack -- no peer mappings at all."""
+    host copies here; NCCL on GPUs), kv_unpack -- no peer mappings at all.
+    vmm: pools as shareable VMM allocations mapped through POSIX handles.
+    onecall: the whole share of each process through kv_switch_range (plan,
+    push, device barrier, remap, read-back in one C call)."""
     import torch.multiprocessing as mp
     w = _workload(world, kind, v)
     og = O.Geom(*GEOS[kind])
