@@ -619,3 +619,42 @@ def test_packed_offsets_are_the_documented_prefixes():
         assert off[g, 1] == sum(i for _, i in res[:g])
         assert off[g, 2] == 4 * sum(r for r, _ in res[:g])
     assert list(tot) == [sum(r for r, _ in res) + 4, sum(i for _, i in res), 4 * sum(r for r, _ in res)]
+
+
+def test_round2_entry_points_validate_before_the_device():
+    """Argument checks of this round's entry points need no GPU: bad pool
+    ranges (kv_reshard_range, kv_switch_range), barrier arguments
+    (kv_group_barrier), multicast teams (kv_cache_set_multicast), strict-mode
+    flags; kv_verify_replicas of a plan without replicated sources is (0,
+    none) without touching the device."""
+    c = fake_cache((1, 4, 8, 4, 2), [64] * 4)
+    a = c.alloc((0, 1), 5)
+    reqs = [(1, 20, (0, 1), a, (0, 2))]
+    plan = c.plan_switch(reqs)
+    for lo, hi in ((0, 0), (-1, 2), (2, 5), (3, 1)):
+        with pytest.raises(F.FlyKVError) as e:
+            F.kv_reshard_range(plan, lo, hi)
+        assert e.value.name == "KV_ERR_INVALID_ARG"
+    assert F.kv_verify_replicas(plan) == (0, None)
+    plan.destroy()
+    with pytest.raises(F.FlyKVError) as e:
+        F.kv_switch_range(c, reqs, 2, 9)
+    assert e.value.name == "KV_ERR_INVALID_ARG"
+    assert all(c.free_count(g) == 64 - (5 if g == 0 else 0) for g in range(4))   # nothing planned
+    for args in (([], 0, 1), ([1 << 40], 1, 1), ([1 << 40 | 4], 0, 1), ([1 << 40], 0, 0)):
+        flags, me, tmo = args
+        with pytest.raises(F.FlyKVError) as e:
+            F.kv_group_barrier(flags, me, 1, tmo)
+        assert e.value.name == "KV_ERR_INVALID_ARG"
+    bases = [1 << 40]
+    for team, mode in (((1, 2), 1), ((0, 1), 1), ((0, 8), 1), ((0, 2), 3)):
+        with pytest.raises(F.FlyKVError):
+            c.set_multicast(team, bases, mode)
+    c.set_multicast((2, 2), bases, 2)
+    with pytest.raises(F.FlyKVError):
+        c.set_multicast((0, 2), bases, 1)          # one mode per cache
+    c.set_multicast((2, 2), None, 2)               # cleared: the mode is free again
+    c.set_multicast((0, 2), bases, 1)
+    assert F._lib.kv_cache_set_strict(c._h, 2) == 1          # KV_ERR_INVALID_ARG: strict is 0 or 1
+    c.set_strict(True)
+    c.set_strict(False)
