@@ -254,7 +254,7 @@ __device__ __forceinline__ int round_len(const ReshardArgs& a, int64_t R, int64_
 }
 
 template <int VPL, int U, bool MIX, bool MC = false>
-__global__ void __launch_bounds__(256, 2) flykv_reshard_kernel(const ReshardArgs a) {
+__global__ void __launch_bounds__(U > 2 ? 128 : 256, U > 2 ? 1 : 2) flykv_reshard_kernel(const ReshardArgs a) {
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -662,7 +662,8 @@ static cudaError_t launch_ldg(const ReshardArgs& a_in, int device, cudaStream_t 
     static int per_sm = 0;
     if (per_sm == 0) {
         int nb = 0;
-        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, flykv_reshard_kernel<VPL, U, false>, 256, 0);
+        cudaError_t e =
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, flykv_reshard_kernel<VPL, U, false>, U > 2 ? 128 : 256, 0);
         if (e != cudaSuccess) return e;
         per_sm = nb > 0 ? nb : 1;
     }
@@ -676,7 +677,7 @@ static cudaError_t launch_ldg(const ReshardArgs& a_in, int device, cudaStream_t 
     // 10 warps per SM (2 x 160 threads; H_kv=1 TP8 5.55 ms vs 5.73-7.2 for
     // other shapes); 2-4 replicas with lane-parallel replica decode keep the
     // default 6 warps (H_kv=4 TP8 9.74 ms vs 9.86 with 8 warps).
-    int want_per = U == 1 ? 2 : 1, want_threads = U == 1 ? 256 : 192;
+    int want_per = U == 1 ? 2 : 1, want_threads = U == 1 ? 256 : U == 2 ? 192 : U == 3 ? 128 : 96;
     if (U > 1 && a.max_rep >= 8) {
         want_threads = 160;
         want_per = 2;
@@ -777,6 +778,14 @@ cudaError_t launch_reshard(const ReshardArgs& a, int device, cudaStream_t s) {
     if (g_impl == 0 && rep_tma && a.max_rep >= 8 && tma_ok && !a.peer && !a.mc_mode && a.staged != 1 && a.staged != 2)
         return launch_tma<4, 2>(a, device, s, 1);
     // default (0) and 3: two atoms in flight per warp (measured +1%)
+    // experiment knob FLYKV_U: atoms in flight per warp for 4 KiB atoms (2 default; 3, 4)
+    static int u_knob = -1;
+    if (u_knob < 0) {
+        const char* e = getenv("FLYKV_U");
+        u_knob = e ? atoi(e) : 2;
+    }
+    if ((g_impl == 0 || g_impl == 3) && a.atom_bytes == 4096 && u_knob == 3) return launch_ldg<8, 3>(a, device, s);
+    if ((g_impl == 0 || g_impl == 3) && a.atom_bytes == 4096 && u_knob == 4) return launch_ldg<8, 4>(a, device, s);
     if ((g_impl == 0 || g_impl == 3) && a.atom_bytes == 4096) return launch_ldg<8, 2>(a, device, s);
     if ((g_impl == 0 || g_impl == 3) && a.atom_bytes == 2048) return launch_ldg<4, 2>(a, device, s);
     switch (a.atom_bytes) {
