@@ -744,9 +744,12 @@ kv_status kv_verify_replicas(kv_plan* plan, void* stream, int64_t* mismatches, u
 kv_status kv_cache_set_strict(kv_cache* cache, int32_t strict);
 
 /* Tuning knob for the reshard kernel (process-wide): impl 0 = default
- * (LDG/STG warp copy, two atoms in flight per warp for 2/4 KiB atoms), 1 =
- * LDG/STG one atom per warp iteration, 2 = TMA bulk-copy ring (local pools
- * and kv_pack's send chunks only; peer pools always use LDG/STG), 3 = same as 0; ctas_per_sm 0 =
+ * (LDG/STG warp copy, two atoms in flight per warp for 2/4 KiB atoms; for
+ * >= 8 GQA replicas into local pools, the TMA bulk-copy ring with
+ * lane-parallel replica stores), 1 = LDG/STG one atom per warp iteration,
+ * 2 = TMA bulk-copy ring for every launch (local pools and kv_pack's send
+ * chunks only; peer pools and NVLS teams always use LDG/STG), 3 = LDG/STG
+ * with two atoms in flight, also for >= 8 replicas; ctas_per_sm 0 =
  * occupancy maximum.  Measured alternatives, see DESIGN.md section 7. */
 kv_status kv_set_reshard_impl(int32_t impl, int32_t ctas_per_sm);
 
