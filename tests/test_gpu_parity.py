@@ -25,7 +25,7 @@ def _F():
 
 
 def run_parity(geo, nb, spec, seed=0, per_gpu_launch=False, check_pools=True, staged=False, a2a=False,
-               work_order=1):
+               work_order=1, degrees=(2, 4, 8, 16)):
     """spec: list of (T, src_group, dst_group).  Runs the product on cuda:0
     (virtual ranks) and the oracle on host copies; asserts exact equality.
     work_order: the kernels' visiting order (kv_cache_set_work_order); it
@@ -34,7 +34,7 @@ def run_parity(geo, nb, spec, seed=0, per_gpu_launch=False, check_pools=True, st
     from paper_2602_22593_b200.engine import KVSwitchEngine
     og = O.Geom(*geo)
     g = F.geometry(*geo)
-    eng = KVSwitchEngine(g, nb, "cuda:0", tp_degrees=(2, 4, 8, 16))
+    eng = KVSwitchEngine(g, nb, "cuda:0", tp_degrees=degrees)
     eng.cache.set_work_order(work_order)
     for gpu, t in enumerate(eng.pools.tensors):
         synth.fill_hash_torch(t, gpu, seed=seed + 2)
@@ -164,6 +164,20 @@ def test_grid_ragged(H, p0, p1, work_order):
     spec = [(T, ((i * p0) % n_gpus, p0), (((i + 3) * p1) % n_gpus, p1)) for i, T in enumerate(Ts)]
     nb = [256] * n_gpus
     run_parity(geo, nb, spec, seed=H * 7 + p0 + 3 * p1, work_order=work_order)
+
+
+@pytest.mark.parametrize("n_gpus,H,p0,p1", [(16, 16, 1, 16), (16, 8, 1, 16), (16, 16, 8, 16), (16, 4, 16, 2),
+                                             (16, 2, 4, 16), (32, 8, 1, 32), (32, 32, 4, 32), (32, 4, 32, 8),
+                                             (64, 8, 1, 64), (64, 64, 64, 1)])
+def test_wide_groups(n_gpus, H, p0, p1):
+    """Degrees beyond one 8-GPU node (a B200 NVL72 rack is one NVLink domain
+    of 72 GPUs): 16-64 virtual pools, TP16/32/64 merges and splits, with
+    and without GQA replication (p > H), whole pools vs the oracle."""
+    geo = (2, H, 64, 16, 2)
+    Ts = [1, 17, 100, 257, 700, 64]
+    spec = [(T, ((i * p0) % n_gpus, p0), (((i + 1) * p1) % n_gpus, p1)) for i, T in enumerate(Ts)]
+    nb = [96] * n_gpus
+    run_parity(geo, nb, spec, seed=n_gpus + H + p0 + p1, degrees=(2, 4, 8, 16, 32, 64))
 
 
 @pytest.mark.parametrize("d,B,e", [(128, 16, 2), (24, 16, 2), (8, 4, 2), (256, 16, 2), (64, 16, 4), (16, 1, 2)])
