@@ -55,20 +55,24 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 EXAMPLE_SRC = os.path.join(ROOT, "examples", "c_switch_demo.c")
 EXAMPLE_BIN = os.path.join(ROOT, "examples", "bin", "c_switch_demo")
+EXAMPLE_MP_SRC = os.path.join(ROOT, "examples", "c_multiproc_demo.c")
+EXAMPLE_MP_BIN = os.path.join(ROOT, "examples", "bin", "c_multiproc_demo")
 
 
 def build_example() -> str:
-    """Plain C (gcc -std=c99) program against include/flykv.h + libflykv.so."""
+    """Plain C (gcc -std=c99) programs against include/flykv.h + libflykv.so:
+    the single-process demo (returned) and the multi-process one."""
     os.makedirs(os.path.dirname(EXAMPLE_BIN), exist_ok=True)
     cuda = os.path.dirname(os.path.dirname(nvcc())) if os.path.isabs(nvcc()) else "/usr/local/cuda"
-    cmd = ["gcc", "-std=c99", "-Wall", "-O2", "-o", EXAMPLE_BIN, EXAMPLE_SRC, "-I", INCLUDE,
-           "-I", os.path.join(cuda, "include"), "-L", os.path.dirname(LIB), "-lflykv",
-           "-L", os.path.join(cuda, "lib64"), "-lcudart", "-Wl,-rpath,$ORIGIN/../../paper_2602_22593_b200/lib",
-           "-Wl,-rpath," + os.path.join(cuda, "lib64")]
-    r = subprocess.run(cmd, capture_output=True, text=True)
-    if r.returncode != 0:
-        sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("gcc failed building examples/c_switch_demo")
+    for src, out in ((EXAMPLE_SRC, EXAMPLE_BIN), (EXAMPLE_MP_SRC, EXAMPLE_MP_BIN)):
+        cmd = ["gcc", "-std=c99", "-Wall", "-O2", "-o", out, src, "-I", INCLUDE,
+               "-I", os.path.join(cuda, "include"), "-L", os.path.dirname(LIB), "-lflykv",
+               "-L", os.path.join(cuda, "lib64"), "-lcudart", "-Wl,-rpath,$ORIGIN/../../paper_2602_22593_b200/lib",
+               "-Wl,-rpath," + os.path.join(cuda, "lib64")]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError(f"gcc failed building {os.path.relpath(out, ROOT)}")
     return EXAMPLE_BIN
 
 
