@@ -734,8 +734,8 @@ def run_single(args):
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                      "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
                      "traffic_over_algorithmic_forward_launch": traffic_ratio, "peak_source": peak_src,
-                     "kernel": ("flykv_reshard_tma_kernel (>= 8 replicas, forward) / flykv_reshard_kernel"
-                                if max(max(d[1], s_[1]) for d, s_ in zip(w.dst, w.src)) >= 8 * w.H
+                     "kernel": ("flykv_reshard_tma_kernel (>= 4 replicas, forward) / flykv_reshard_kernel"
+                                if max(max(d[1], s_[1]) for d, s_ in zip(w.dst, w.src)) >= 4 * w.H
                                 and os.environ.get("FLYKV_REP_TMA", "1") != "0" else "flykv_reshard_kernel"),
                      "algorithmic_bytes_per_launch": int(algo_bytes),
                      "sustained_copy_same_box": sustained,

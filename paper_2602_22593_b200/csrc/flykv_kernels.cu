@@ -654,11 +654,14 @@ template <int VPL, int U = 1>
 static cudaError_t launch_ldg(const ReshardArgs& a_in, int device, cudaStream_t s) {
     read_env_knobs();
     ReshardArgs a = a_in;
-    // Replica stores (GQA): with 2-4 replicas the lane-parallel replica
-    // decode is 1.2% faster; with 8 the serial re-decode between replica
-    // stores is 5% faster (spacing the store bursts) -- scripts/gpu_gqa_rep.sh,
-    // profiles/r01_gqa_rep.jsonl.
-    a.rep_flags = g_rep_flags >= 0 ? g_rep_flags : (a.max_rep > 1 && a.max_rep < 8 ? 1 : 0);
+    // Replica stores (GQA): 2-3 replicas: serial re-decode, replica-major
+    // (rep_flags 2) at 7 warps per SM (H_kv=4 -> TP8 forward 11.77 ms
+    // against 11.96 for lane-parallel decode at 6 warps, round 2,
+    // profiles/r02_gqa_replica_sweep.txt); 4-7 replicas (peer destinations;
+    // local ones take the TMA ring): lane-parallel decode; 8+: serial
+    // re-decode between replica stores, which spaces the store bursts
+    // (round 1, profiles/r01_gqa_rep.jsonl).
+    a.rep_flags = g_rep_flags >= 0 ? g_rep_flags : (a.max_rep > 1 && a.max_rep < 4 ? 2 : a.max_rep < 8 ? 1 : 0);
     static int per_sm = 0;
     if (per_sm == 0) {
         int nb = 0;
@@ -673,14 +676,16 @@ static cudaError_t launch_ldg(const ReshardArgs& a_in, int device, cudaStream_t 
     // measured optimum is 6 warps x 8 KiB = 48 KiB per SM (U=2: one 192-thread
     // CTA per SM: 6.45-6.59 TB/s on C2/C4, vs 6.26-6.30 with 8 warps and
     // 5.9 with 4; scripts/variants.py).  U=1: two 256-thread CTAs.
-    // GQA replication (p/H copies per read) is write-heavy: 8 replicas want
-    // 10 warps per SM (2 x 160 threads; H_kv=1 TP8 5.55 ms vs 5.73-7.2 for
-    // other shapes); 2-4 replicas with lane-parallel replica decode keep the
-    // default 6 warps (H_kv=4 TP8 9.74 ms vs 9.86 with 8 warps).
+    // GQA replication (p/H copies per read) is write-heavy: on this path
+    // (peer destinations, or FLYKV_REP_TMA=0) 8 replicas want 10 warps per
+    // SM (2 x 160 threads; round 1: H_kv=1 TP8 5.55 ms vs 5.73-7.2 for other
+    // shapes); 2-3 replicas with replica-major stores want 7 (224 threads).
     int want_per = U == 1 ? 2 : 1, want_threads = U == 1 ? 256 : U == 2 ? 192 : U == 3 ? 128 : 96;
-    if (U > 1 && a.max_rep >= 8) {
+    if (U == 2 && a.max_rep >= 8) {
         want_threads = 160;
         want_per = 2;
+    } else if (U == 2 && a.max_rep > 1 && a.max_rep < 4) {
+        want_threads = 224;  // 7 warps with the replica-major stores (above)
     }
     const int per = g_ctas_per_sm > 0 ? g_ctas_per_sm : (per_sm < want_per ? per_sm : want_per);
     const int threads = g_threads > 0 ? g_threads : want_threads;
@@ -764,19 +769,23 @@ cudaError_t launch_reshard(const ReshardArgs& a, int device, cudaStream_t s) {
     if (a.atom_hi <= a.atom_lo) return cudaSuccess;
     const bool tma_ok = (a.atom_bytes % 16) == 0 && a.atom_bytes <= 16384;
     if (g_impl == 2 && tma_ok && !a.peer && !a.mc_mode) return launch_tma_shape(a, device, s);
-    // GQA replication with >= 8 replicas (p/H, R2) into local pools: 8/9 of
+    // GQA replication with >= 4 replicas (p/H, R2) into local pools: most of
     // the traffic is writes, and the TMA ring with lane-parallel replica bulk
-    // stores at 2 warps per SM (4 stages, 2 atoms ahead) writes them fastest:
-    // H_kv=1 -> TP8 forward 8.87-8.90 ms against 9.22 ms for the best LDG/STG
-    // shape; 3+ warps per SM fall back to 9.6 ms (profiles/r02_gqa_tma2.jsonl).
-    // Knob FLYKV_REP_TMA=0 keeps the LDG/STG kernel (A/B).
+    // stores writes them fastest -- the more replicas, the fewer loads in
+    // flight it wants: 8 replicas at 2 warps per SM (2 CTAs x 1 warp, 4
+    // stages, 2 atoms ahead; H_kv=1 -> TP8 forward 8.82 ms against 9.22 ms
+    // for the best LDG/STG shape), 4 replicas at 6 warps per SM (6 CTAs x 1
+    // warp, 3 stages, 1 atom ahead; H_kv=2 forward 9.80 ms against 10.22 for
+    // the best LDG/STG shape and 10.57 for the round-1 default).  Sweeps:
+    // profiles/r02_gqa_tma*.jsonl, r02_gqa_replica_sweep.txt.  Knob
+    // FLYKV_REP_TMA=0 keeps the LDG/STG kernel (A/B).
     static int rep_tma = -1;
     if (rep_tma < 0) {
         const char* e = getenv("FLYKV_REP_TMA");
         rep_tma = e ? atoi(e) : 1;
     }
-    if (g_impl == 0 && rep_tma && a.max_rep >= 8 && tma_ok && !a.peer && !a.mc_mode && a.staged != 1 && a.staged != 2)
-        return launch_tma<4, 2>(a, device, s, 1);
+    if (g_impl == 0 && rep_tma && a.max_rep >= 4 && tma_ok && !a.peer && !a.mc_mode && a.staged != 1 && a.staged != 2)
+        return a.max_rep >= 8 ? launch_tma<4, 1>(a, device, s, 2) : launch_tma<3, 1>(a, device, s, 6);
     // default (0) and 3: two atoms in flight per warp (measured +1%)
     // experiment knob FLYKV_U: atoms in flight per warp for 4 KiB atoms (2 default; 3, 4)
     static int u_knob = -1;

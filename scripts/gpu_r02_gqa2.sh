@@ -1,12 +1,9 @@
 #!/bin/bash
-# TMA ring shapes at low occupancy for the 8-replica (H_kv=1 -> TP8) forward plan, and both directions.
+# H_kv=2 -> TP8 (4 replicas) and H_kv=4 (2 replicas) forward plans: replica strategy x launch shape.
 cd "$GRAFT_REPO_ROOT"
-mkdir -p gpurun_out
-: > gpurun_out/r02_gqa_tma2.jsonl
-for cfg in c4gqa1; do
-for shape in 0 10 11 12 13 14 15 16 17 3 4; do
-FLYKV_TMA_SHAPE=$shape VARIANTS="0:0,2:1,2:2,2:3,2:4" timeout 600 python scripts/variants.py $cfg 2>/dev/null | head -5 | tail -1 | python -c "import sys,json; d=json.loads(sys.stdin.read()); d['tma_shape']=$shape; print(json.dumps(d))" >> gpurun_out/r02_gqa_tma2.jsonl; echo $cfg $shape rc=$?
+for cfgname in c4gqa2 c4gqa4; do
+for cfg in "1 192 1" "2 224 1" "0 224 1" "2 256 1" "0 256 1" "2 192 1"; do
+set -- $cfg
+FLYKV_REP_FLAGS=$1 FLYKV_THREADS=$2 FLYKV_CTAS=$3 VARIANTS="0:0" timeout 600 python scripts/variants.py $cfgname 2>/dev/null | head -1 | python -c "
+import sys,json; d=json.loads(sys.stdin.read()); v=d['impl0_ctas0']; print('$cfgname rep_flags $1 threads $2 ctas $3: %.3f ms %.0f GB/s' % (v['ms'], v['GBps']))"
 done; done
-for shape in 0 10 13; do
-REVERSE=1 FLYKV_TMA_SHAPE=$shape VARIANTS="0:0,2:1,2:2,2:3" timeout 600 python scripts/variants.py c4gqa1 2>/dev/null | head -4 | tail -1 | python -c "import sys,json; d=json.loads(sys.stdin.read()); d['tma_shape']=$shape; d['reverse']=1; print(json.dumps(d))" >> gpurun_out/r02_gqa_tma2.jsonl; echo rev $shape rc=$?
-done

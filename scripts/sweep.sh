@@ -8,6 +8,7 @@ run --config c2
 run --config c4
 run --config c4fan
 run --config c4gqa4
+run --config c4gqa2
 run --config c4gqa1
 run --config c3i --requests 64
 run --config c3ii --requests 64

@@ -139,6 +139,7 @@ WORKLOADS = {
     "c4": llama70b_dp8_tp8,
     "c4fan": llama70b_fanout,
     "c4gqa4": lambda **kw: llama70b_dp8_tp8(H=4, **kw),
+    "c4gqa2": lambda **kw: llama70b_dp8_tp8(H=2, **kw),
     "c4gqa1": lambda **kw: llama70b_dp8_tp8(H=1, **kw),
     "c5": long_context_tp4_tp8,
     "single": single_promotion,
