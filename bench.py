@@ -411,7 +411,7 @@ def run_single(args):
             if grp[1] > 1:
                 rank_ids[grp] = F.kv_suggest_rank_ids(eng.cache, reqs0, grp)
         reqs0 = [r[:6] + (rank_ids.get(tuple(r[4])),) for r in reqs0]
-    state = {"reqs": reqs0}
+    state = {"reqs": reqs0, "n": 0}   # n: switches run so far (even before a forward switch)
     stream = eng.stream
 
     def flipped(reqs, plan):
@@ -419,6 +419,7 @@ def run_single(args):
         return [(rid, T, d, t, s, drid, srid) for (rid, T, s, _, d, srid, drid), t in zip(reqs, new)]
 
     ev_pairs = []      # per step: [(e0, e1) per wave] around the reshard launches
+    kern_fwd = []      # per timed step: did it start from the workload's initial layout
     step_stats = []    # per step: summed plan statistics over its waves
     n_waves = []
 
@@ -446,6 +447,7 @@ def run_single(args):
 
     def step(timed_kernel=False, read_back=False):
         """One whole switch (all waves).  Returns (tables, host copies)."""
+        state["n"] += 1
         reqs = state["reqs"]
         pairs, agg, host, plans_ = [], None, {}, []
         ws = waves_of(reqs)
@@ -482,6 +484,7 @@ def run_single(args):
                                  "flip %.2f\n" % tuple(d[:7]))
         if timed_kernel:
             ev_pairs.append(pairs)
+            kern_fwd.append(state["n"] % 2 == 1)
             step_stats.append(agg)
             n_waves.append(len(ws))
         return agg, host
@@ -493,6 +496,7 @@ def run_single(args):
         switch that reverses the previous one is kv_switch_back: the inverse
         request list is built inside the library, nothing is marshalled.
         Returns (aggregated stats, device->host bytes)."""
+        state["n"] += 1
         chain = state.setdefault("chain", [])
         if not (args.waves or args.pieces) and chain:
             plans_ = [F.kv_switch_back(eng.cache, chain[-1][2][0], stream)]
@@ -608,6 +612,7 @@ def run_single(args):
             plan_ms = []
             enq_ms = []
             phases = []
+            lat_fwd = []
             for _ in range(max(args.warmup, 1)):   # untimed end-to-end warm-up switches
                 step_switch()
                 stream.synchronize()
@@ -624,6 +629,7 @@ def run_single(args):
                 if DEBUG and (t1 - te) * 1e3 > 8:
                     sys.stderr.write("slow sync: %.2f ms\n" % ((t1 - te) * 1e3))
                 lat_ms.append((t1 - t0) * 1e3)
+                lat_fwd.append(state["n"] % 2 == 1)   # this switch started from the workload's initial layout
                 enq_ms.append((te - t0) * 1e3)
                 h2d += st_["h2d_bytes"]
                 e2e_payload += st_["payload_bytes"]
@@ -664,6 +670,12 @@ def run_single(args):
                    "value_at_p50": round(e2e_payload / len(lat_ms) / (statistics.median(lat_ms) / 1e3) / 1e9, 3),
                    "switch_latency_ms_p50": round(statistics.median(lat_ms), 3),
                    "switch_latency_ms_p99": round(float(np.percentile(lat_ms, 99)), 3),
+                   # directions alternate; under GQA replication they move different bytes, so the
+                   # pooled p50 can fall between them: the p50 of each direction
+                   "switch_latency_ms_p50_forward_reverse": [
+                       round(statistics.median([x for x, f in zip(lat_ms, lat_fwd) if f]), 3) if any(lat_fwd) else None,
+                       round(statistics.median([x for x, f in zip(lat_ms, lat_fwd) if not f]), 3)
+                       if not all(lat_fwd) else None],
                    "host_plan_ms_p50": round(statistics.median(plan_ms), 3),
                    "latency_breakdown": tail,
                    "api": ("KVSwitchEngine.switch(read_back=True)" if DEBUG else
@@ -728,6 +740,9 @@ def run_single(args):
         "switch_latency_ms": round(total_ms / args.steps, 4),
         "reshard_kernel_ms": round(kmean, 4),
         "reshard_kernel_ms_steps": [round(x, 3) for x in kern_ms],   # per timed step (directions alternate)
+        "reshard_kernel_ms_forward_reverse": [
+            round(statistics.mean([x for x, f in zip(kern_ms, kern_fwd) if f]), 4) if any(kern_fwd) else None,
+            round(statistics.mean([x for x, f in zip(kern_ms, kern_fwd) if not f]), 4) if not all(kern_fwd) else None],
         "reshard_kernel_ms_p50_p90": [round(float(np.percentile(kern_ms, 50)), 4),
                                       round(float(np.percentile(kern_ms, 90)), 4)],
         "modeled_nvlink": modeled,
