@@ -529,6 +529,28 @@ def run_single(args):
                 ws = [(reqs, [(i, 0, r[1]) for i, r in enumerate(reqs)])]
             state["reqs"] = flip_all(reqs, ws, plans_)
 
+    class _Tables:
+        """A finished plan's destination tables, kept after the plan is destroyed."""
+
+        def __init__(self, plan):
+            self.tabs = plan.dst_tables()
+
+        def dst_tables(self):
+            return self.tabs
+
+    def compact_chain():
+        """Between timed e2e steps: keep only the last switch's plan alive (the
+        next kv_switch_back needs it); older ones keep their tables and are
+        destroyed, so the library recycles their host buffers."""
+        chain = state.get("chain", [])
+        for k in range(len(chain) - 1):
+            r_, ws_, plans_ = chain[k]
+            if plans_ and not isinstance(plans_[0], _Tables):
+                done = [_Tables(p) for p in plans_]
+                for p in plans_:
+                    p.destroy()
+                chain[k] = (r_, ws_, done)
+
     with torch.cuda.stream(stream):
         if args.profile_steps:
             for _ in range(args.profile_steps):
@@ -616,6 +638,7 @@ def run_single(args):
             for _ in range(max(args.warmup, 1)):   # untimed end-to-end warm-up switches
                 step_switch()
                 stream.synchronize()
+                compact_chain()
             for it in range(args.steps):
                 t0 = time.perf_counter()
                 if DEBUG:  # the same switch through the torch-plumbing engine, with enqueue timings
@@ -630,6 +653,8 @@ def run_single(args):
                     sys.stderr.write("slow sync: %.2f ms\n" % ((t1 - te) * 1e3))
                 lat_ms.append((t1 - t0) * 1e3)
                 lat_fwd.append(state["n"] % 2 == 1)   # this switch started from the workload's initial layout
+                if not DEBUG:
+                    compact_chain()                   # outside the step's timed window
                 enq_ms.append((te - t0) * 1e3)
                 h2d += st_["h2d_bytes"]
                 e2e_payload += st_["payload_bytes"]

@@ -86,6 +86,9 @@ struct kv_cache {
     int stage_next = 0;
     // plans not yet destroyed: kv_cache_destroy detaches them
     std::unordered_set<kv_plan*> live;
+    // host table buffers of destroyed plans, reused by the next read-backs
+    // (a fresh allocation of a few hundred KB page-faults on every switch)
+    std::vector<std::vector<int32_t>> spare_h;
     // pinned landing buffer of kv_switch's one device->host table copy
     void* back = nullptr;
     size_t back_bytes = 0;
@@ -219,25 +222,41 @@ static int32_t group_min_blocks(const kv_cache* c, kv_group g) {
 // every member when found.  Returns false (nothing marked) if fewer than n.
 typedef std::vector<std::vector<uint64_t>> Bitmaps;
 
-static bool alloc_lowest_in(const kv_cache* c, Bitmaps& held, kv_group g, int32_t n, int32_t* out) {
+// start_word (optional, in/out): the scan starts at this word, and on
+// success it is advanced to the word of the last ID taken -- every ID below
+// it is then held on the group (lowest-first), so a later allocation on the
+// same group in the same plan can skip that prefix (allocations only add
+// held bits until the plan commits).  The taken bits are set word-wise.
+static bool alloc_lowest_in(const kv_cache* c, Bitmaps& held, kv_group g, int32_t n, int32_t* out,
+                            int32_t* start_word = nullptr) {
     if (n == 0) return true;
     const int32_t nb = group_min_blocks(c, g);
     const int32_t words = (nb + 63) >> 6;
-    int32_t got = 0;
-    for (int32_t w = 0; w < words && got < n; ++w) {
+    int32_t got = 0, w = start_word ? *start_word : 0, w_first = w, w_last = w;
+    thread_local std::vector<uint64_t> taken;
+    taken.clear();
+    for (; w < words && got < n; ++w) {
         uint64_t used = 0;
         for (int32_t r = 0; r < g.degree; ++r) used |= held[g.first_gpu + r][w];
         uint64_t fr = ~used;
         const int32_t top = nb - (w << 6);
         if (top < 64) fr &= (top <= 0) ? 0ull : ((1ull << top) - 1);
+        uint64_t mask = 0;
         while (fr && got < n) {
+            const uint64_t bit = fr & (~fr + 1);
             out[got++] = (w << 6) + __builtin_ctzll(fr);
-            fr &= fr - 1;
+            mask |= bit;
+            fr ^= bit;
         }
+        taken.push_back(mask);
+        w_last = w;
     }
     if (got < n) return false;
-    for (int32_t r = 0; r < g.degree; ++r)
-        for (int32_t k = 0; k < n; ++k) bit_set(held[g.first_gpu + r], out[k]);
+    for (int32_t r = 0; r < g.degree; ++r) {
+        std::vector<uint64_t>& bm = held[g.first_gpu + r];
+        for (int32_t k = w_first; k <= w_last; ++k) bm[k] |= taken[k - w_first];
+    }
+    if (start_word) *start_word = w_last;
     return true;
 }
 
@@ -507,6 +526,7 @@ static void init_requests(kv_plan* p, const kv_request* reqs, int32_t n_reqs) {
 static int32_t allocate_destinations(kv_plan* p) {
     kv_cache* c = p->c;
     const int32_t H = c->geo.num_kv_heads, B = c->geo.block_base;
+    std::vector<std::pair<int64_t, int32_t>> cursor;  // (group key, first word worth scanning)
     for (int32_t i = 0; i < (int32_t)p->reqs.size(); ++i) {
         ReqPlan& q = p->reqs[i];
         q.dst_off = (int32_t)p->tables.size();
@@ -518,7 +538,10 @@ static int32_t allocate_destinations(kv_plan* p) {
         const Layout l1 = layout_of(H, q.dst.degree);
         q.n1 = (int32_t)ceil_div(q.T, (int64_t)B * l1.k);
         p->tables.resize(p->tables.size() + q.n1);
-        if (!alloc_lowest(c, q.dst, q.n1, p->tables.data() + q.dst_off)) return i;
+        const int64_t key = ((int64_t)q.dst.first_gpu << 32) | (uint32_t)q.dst.degree;
+        auto it = std::find_if(cursor.begin(), cursor.end(), [&](const auto& e) { return e.first == key; });
+        if (it == cursor.end()) it = cursor.insert(cursor.end(), {key, 0});
+        if (!alloc_lowest_in(c, c->held, q.dst, q.n1, p->tables.data() + q.dst_off, &it->second)) return i;
     }
     return -1;
 }
@@ -1530,6 +1553,10 @@ extern "C" void kv_plan_destroy(kv_plan* p) {
         return;
     }
     p->c->live.erase(p);
+    if (p->h_out.capacity() && p->c->spare_h.size() < 4) {
+        p->h_out.clear();
+        p->c->spare_h.push_back(std::move(p->h_out));
+    }
     if (p->state == PLAN_PLANNED) rollback_allocations(p, (int32_t)p->reqs.size());
     if (p->dbuf) cudaFreeAsync(p->dbuf, p->last_stream);
     if (p->d_out) cudaFreeAsync(p->d_out, p->last_stream);
@@ -1670,6 +1697,10 @@ static kv_status switch_read_back(kv_plan* p, cudaStream_t stream) {
     if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
     if (e != cudaSuccess) return cuda_fail(e, "kv_switch table read-back");
     const int64_t t1 = now_ns();
+    if (p->h_out.capacity() < (size_t)elems && !c->spare_h.empty()) {  // reuse a destroyed plan's buffer
+        p->h_out.swap(c->spare_h.back());
+        c->spare_h.pop_back();
+    }
     p->h_out.assign(static_cast<int32_t*>(c->back), static_cast<int32_t*>(c->back) + elems);
     p->st.t_wait_ns = t1 - t0;
     p->st.t_read_ns = now_ns() - t1;
