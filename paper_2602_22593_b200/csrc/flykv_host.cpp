@@ -1020,7 +1020,17 @@ static ReshardArgs reshard_args(const kv_plan* p, int32_t lo, int32_t hi) {
     a.atom_hi = hi < n ? p->streams[hi].begin : p->mixed_end;
     // the first GPU with work (the stream search needs streams[st_lo].begin <= slot)
     while (a.st_lo + 1 < hi && p->streams[a.st_lo + 1].begin == a.atom_lo) ++a.st_lo;
-    for (int32_t g = a.st_lo; g < a.st_hi; ++g) a.mixed |= p->streams[g].nb > 1 ? 1 : 0;
+    // The kernels may index piece space with the mixed slot directly (MIX =
+    // false) only where the two coincide: every launched stream is a single
+    // bucket AND starts at the same offset in both spaces.  An earlier GPU
+    // with several buckets leaves holes in the mixed space, which shifts the
+    // later GPUs' mixed offsets past their piece-space ones -- so a launch of
+    // such a later single-bucket GPU alone (one process per GPU) must take
+    // the mapping too.  (Found by tests/test_gpu_fuzz.py, seed 82.)
+    for (int32_t g = a.st_lo; g < a.st_hi; ++g) {
+        const MixStream& ms = p->streams[g];
+        if (ms.nb > 1 || (ms.nb == 1 && ms.begin != p->buckets[ms.b0].start)) a.mixed = 1;
+    }
     a.L = c->geo.num_layers;
     a.atom_bytes = (int32_t)c->atom_bytes;
     a.M = c->M;

@@ -20,7 +20,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 GEO = (3, 8, 128, 16, 2)
-GEOS = {"dp_tp": (3, 8, 128, 16, 2), "tp_dp": (3, 8, 128, 16, 2), "gqa": (2, 2, 128, 16, 2), "tp_tp": (2, 8, 64, 16, 2),
+GEOS = {"hetero": (2, 8, 128, 16, 2), "dp_tp": (3, 8, 128, 16, 2), "tp_dp": (3, 8, 128, 16, 2), "gqa": (2, 2, 128, 16, 2), "tp_tp": (2, 8, 64, 16, 2),
         "gqa1": (2, 1, 128, 16, 2)}
 
 
@@ -40,6 +40,9 @@ def _workload(world, kind="dp_tp", v=1):
     w = synth.dp_to_tp(world, 6 * world, L=L, H=H, d=d, B=B, lo=1, hi=700, seed=4)
     if kind == "tp_dp":
         w = synth.Workload(w.name, L, H, d, B, 2, world, w.T, list(w.dst), list(w.src))
+    elif kind == "hetero":   # GPU 0 feeds two TP2 groups, the others one TP_world group (mixed-order offsets)
+        dst = [(((i // world) % 2) * 2, 2) if i % world == 0 else (0, world) for i in range(len(w.T))]
+        w = synth.Workload(w.name, L, H, d, B, 2, world, w.T, list(w.src), dst)
     elif kind == "tp_tp":
         w = synth.Workload(w.name, L, H, d, B, 2, world, w.T, [((i % (world // 2)) * 2, 2) for i in range(len(w.T))],
                            list(w.dst))
@@ -166,7 +169,9 @@ def _rank(rank, world, port, outdir, kind, mode="push", v=1):
                                                (2, "tp_dp", "push", 2), (2, "gqa", "push", 4),
                                                (2, "dp_tp", "vmm", 1), (4, "gqa", "vmm", 1), (4, "tp_tp", "vmm", 1),
                                                (2, "dp_tp", "onecall", 1), (4, "tp_dp", "onecall", 1),
-                                               (2, "gqa", "onecall", 4), (8, "dp_tp", "onecall", 1)])
+                                               (2, "gqa", "onecall", 4), (8, "dp_tp", "onecall", 1),
+                                               (4, "hetero", "push", 1), (4, "hetero", "onecall", 1),
+                                               (2, "hetero", "push", 2)])
 def test_ipc_push_matches_oracle(world, kind, mode, v):
     """push: every process's reshard kernel (kv_reshard_range over the v
     pools it owns) stores into peer pools (CUDA IPC), then kv_group_barrier.

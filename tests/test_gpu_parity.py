@@ -961,3 +961,20 @@ def test_nvls_capability_report():
     assert ok or why
     if ok:
         assert gran > 0 and gran % (2 << 20) == 0
+
+
+def test_single_bucket_gpu_after_mixed_gpu():
+    """Regression (found by tests/test_gpu_fuzz.py, seed 82): with the mixed
+    work order, a GPU whose atoms go to several destination groups leaves
+    holes in the mixed slot space, so a later GPU whose atoms all go to one
+    group starts at different offsets in the two spaces; launched alone (one
+    process per GPU: kv_reshard(plan, g)) it must still map its slots.  The
+    fuzz case itself (16-byte atoms, 16 pools), plus the multi-process
+    'hetero' cases in test_gpu_multiproc.py."""
+    geo = (2, 16, 16, 1, 1)
+    spec = [(166, (1, 1), (14, 1)),
+            (3, (0, 16), (0, 4), [0, 14, 4, 15, 1, 2, 6, 8, 3, 11, 10, 13, 5, 12, 7, 9], None),
+            (1, (4, 4), (0, 16), [0, 3, 1, 2], None),
+            (0, (0, 16), (0, 16)),
+            (233, (15, 1), (0, 16))]
+    run_parity(geo, [870] * 16, spec, seed=82, per_gpu_launch=True, work_order=1)
