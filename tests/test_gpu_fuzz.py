@@ -3,7 +3,8 @@ block size, element size), 2-16 virtual pools, random merges / splits /
 lateral moves / no-ops with random rank-ID permutations on both sides
 (incl. replicated sources and GQA destinations), random lengths incl. 0 and
 tails, either kernel work order, and one of the launch paths (one launch,
-per-pool launches, pack -> all-to-all -> unpack); whole pools, tables and
+per-pool launches, kv_reshard_range over a random partition of the pools,
+the one-call kv_switch, pack -> all-to-all -> unpack); whole pools, tables and
 allocator state bit-exact against the oracle (run_parity).  FLYKV_FUZZ_CASES
 (default 24) sets the count; FLYKV_FUZZ_SEED0 the first seed."""
 import os
@@ -42,14 +43,17 @@ def _case(seed):
         srid = [int(x) for x in rng.permutation(p0)] if p0 > 1 and rng.random() < 0.3 else None
         drid = [int(x) for x in rng.permutation(p1)] if p1 > 1 and rng.random() < 0.3 else None
         spec.append((T, (g0, p0), (g1, p1), srid, drid))
-    mode = str(rng.choice(["one", "one", "per_gpu", "a2a"]))
-    return (L, H, d, B, e), n_gpus, spec, mode, int(rng.integers(0, 2))
+    mode = str(rng.choice(["one", "one", "per_gpu", "a2a", "ranges", "switch"]))
+    cuts = sorted(set(int(x) for x in rng.integers(1, n_gpus, size=int(rng.integers(0, 4)))))
+    ranges = list(zip([0] + cuts, cuts + [n_gpus]))
+    return (L, H, d, B, e), n_gpus, spec, mode, int(rng.integers(0, 2)), ranges
 
 
 @pytest.mark.parametrize("seed", range(SEED0, SEED0 + N_CASES))
 def test_fuzz_parity(seed):
-    geo, n_gpus, spec, mode, work_order = _case(seed)
+    geo, n_gpus, spec, mode, work_order, ranges = _case(seed)
     B = geo[3]
     nb = 2 * sum(-(-x[0] // B) for x in spec) + 64   # room for every source and destination on any pool
     run_parity(geo, [nb] * n_gpus, spec, seed=seed, per_gpu_launch=mode == "per_gpu", a2a=mode == "a2a",
-               work_order=work_order, degrees=(2, 4, 8, 16))
+               work_order=work_order, degrees=(2, 4, 8, 16), ranges=ranges if mode == "ranges" else None,
+               one_call=mode == "switch")

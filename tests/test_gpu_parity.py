@@ -25,7 +25,7 @@ def _F():
 
 
 def run_parity(geo, nb, spec, seed=0, per_gpu_launch=False, check_pools=True, staged=False, a2a=False,
-               work_order=1, degrees=(2, 4, 8, 16)):
+               work_order=1, degrees=(2, 4, 8, 16), ranges=None, one_call=False):
     """spec: list of (T, src_group, dst_group).  Runs the product on cuda:0
     (virtual ranks) and the oracle on host copies; asserts exact equality.
     work_order: the kernels' visiting order (kv_cache_set_work_order); it
@@ -82,6 +82,20 @@ def run_parity(geo, nb, spec, seed=0, per_gpu_launch=False, check_pools=True, st
             F.kv_reshard(plan, gpu, eng.stream)
         for gpu, t in tables.items():
             F.kv_remap_block_tables(plan, gpu, t.req_ptr, t.block_ids, t.meta, eng.stream)
+    elif ranges is not None:   # kv_reshard_range over a partition of the pools (processes owning several)
+        tables = eng.alloc_tables(plan, range(len(nb)))
+        for lo, hi in ranges:
+            F.kv_reshard_range(plan, lo, hi, eng.stream)
+        for gpu, t in tables.items():
+            F.kv_remap_block_tables(plan, gpu, t.req_ptr, t.block_ids, t.meta, eng.stream)
+    elif one_call:   # kv_switch: the plan above is discarded, the one-call API re-plans the same requests
+        plan.destroy()
+        plan = F.kv_switch(eng.cache, freqs, eng.stream)
+        tables = {}
+        for gpu in range(len(nb)):
+            rp, ids_, meta_ = plan.host_tables(gpu)
+            tables[gpu] = type("T", (), {"req_ptr": torch.as_tensor(rp), "block_ids": torch.as_tensor(ids_),
+                                         "meta": torch.as_tensor(meta_)})
     else:  # default: one reshard launch + one packed all-pool remap launch
         tables = eng.execute(plan)
     torch.cuda.synchronize()
