@@ -32,14 +32,32 @@ def _free_port():
     return p
 
 
+def _geo(kind):
+    """rand<seed>: a seeded random geometry (H_kv 1-8) for the fuzz cases."""
+    if kind.startswith("rand"):
+        rng = np.random.default_rng(90000 + int(kind[4:]))
+        return (2, int(rng.choice([1, 2, 4, 8])), int(rng.choice([64, 128])), 16, 2)
+    return GEOS[kind]
+
+
 def _workload(world, kind="dp_tp", v=1):
     """dp_tp: DP_N -> TP_N merge; tp_dp: the split back (round-robin engines);
     gqa: H_kv=2 < N (replication, TP_N > kv_heads); tp_tp: TP2 pairs -> TP_N."""
-    L, H, d, B, _ = GEOS[kind]
+    L, H, d, B, _ = _geo(kind)
     world = world * v   # pools
     w = synth.dp_to_tp(world, 6 * world, L=L, H=H, d=d, B=B, lo=1, hi=700, seed=4)
     if kind == "tp_dp":
         w = synth.Workload(w.name, L, H, d, B, 2, world, w.T, list(w.dst), list(w.src))
+    elif kind.startswith("rand"):   # random merges / splits / lateral moves over every legal degree
+        rng = np.random.default_rng(91000 + int(kind[4:]))
+        degrees = [p for p in (1, 2, 4, 8) if p <= world and ((p <= H and H % p == 0) or (p > H and p % H == 0))]
+        src, dst, T = [], [], []
+        for _ in range(int(rng.integers(4, 14))):
+            p0, p1 = int(rng.choice(degrees)), int(rng.choice(degrees))
+            src.append((int(rng.integers(0, world // p0)) * p0, p0))
+            dst.append((int(rng.integers(0, world // p1)) * p1, p1))
+            T.append(int(rng.integers(1, 700)))
+        w = synth.Workload("rand", L, H, d, B, 2, world, T, src, dst)
     elif kind == "hetero":   # GPU 0 feeds two TP2 groups, the others one TP_world group (mixed-order offsets)
         dst = [(((i // world) % 2) * 2, 2) if i % world == 0 else (0, world) for i in range(len(w.T))]
         w = synth.Workload(w.name, L, H, d, B, 2, world, w.T, list(w.src), dst)
@@ -59,7 +77,7 @@ def _rank(rank, world, port, outdir, kind, mode="push", v=1):
         from paper_2602_22593_b200 import comm
         from paper_2602_22593_b200 import flykv as F
         w = _workload(world, kind, v)
-        g = F.geometry(*GEOS[kind])
+        g = F.geometry(*_geo(kind))
         _, _, M = F.kv_layout(g, 1)
         n0 = [F.kv_blocks_for(g, T, s[1]) for T, s in zip(w.T, w.src)]
         n1 = [F.kv_blocks_for(g, T, d[1]) for T, d in zip(w.T, w.dst)]
@@ -80,8 +98,8 @@ def _rank(rank, world, port, outdir, kind, mode="push", v=1):
             pool = torch.empty((v, w.L, nb[rank], M), dtype=torch.uint8, device=f"cuda:{dev}")
         for k, gp in enumerate(mine):
             synth.fill_hash_torch(pool[k], gp)
-        if w.src[0][1] > w.H:  # GQA replicated sources: replicas identical (R10)
-            raise RuntimeError("replicated sources not used here")
+        if w.src[0][1] > w.H and not kind.startswith("rand"):
+            raise RuntimeError("replicated sources not used here")   # (random cases: both sides read replica 0, R10)
         torch.cuda.synchronize()
         if mode == "a2a":  # no peer mappings: other pools' addresses are never dereferenced
             bases = [[pool[0, l].data_ptr() if r == rank else (1 << 44) + (r << 36) + (l << 30) for l in range(w.L)]
@@ -171,7 +189,10 @@ def _rank(rank, world, port, outdir, kind, mode="push", v=1):
                                                (2, "dp_tp", "onecall", 1), (4, "tp_dp", "onecall", 1),
                                                (2, "gqa", "onecall", 4), (8, "dp_tp", "onecall", 1),
                                                (4, "hetero", "push", 1), (4, "hetero", "onecall", 1),
-                                               (2, "hetero", "push", 2)])
+                                               (2, "hetero", "push", 2)]
+                         + [(int(np.random.default_rng(92000 + k).choice([2, 4])), f"rand{k}",
+                             ["push", "onecall"][k % 2], int(np.random.default_rng(93000 + k).choice([1, 2])))
+                            for k in range(int(os.environ.get("FLYKV_MP_FUZZ_CASES", "4")))])
 def test_ipc_push_matches_oracle(world, kind, mode, v):
     """push: every process's reshard kernel (kv_reshard_range over the v
     pools it owns) stores into peer pools (CUDA IPC), then kv_group_barrier.
@@ -182,7 +203,7 @@ def test_ipc_push_matches_oracle(world, kind, mode, v):
     push, device barrier, remap, read-back in one C call)."""
     import torch.multiprocessing as mp
     w = _workload(world, kind, v)
-    og = O.Geom(*GEOS[kind])
+    og = O.Geom(*_geo(kind))
     n0 = [O.num_blocks(og, T, s[1]) for T, s in zip(w.T, w.src)]
     n1 = [O.num_blocks(og, T, d[1]) for T, d in zip(w.T, w.dst)]
     nb, tabs = synth.realistic_pools(w, n0, n1)
