@@ -658,3 +658,57 @@ def test_round2_entry_points_validate_before_the_device():
     assert F._lib.kv_cache_set_strict(c._h, 2) == 1          # KV_ERR_INVALID_ARG: strict is 0 or 1
     c.set_strict(True)
     c.set_strict(False)
+
+
+def test_weight_views_fuzz_against_oracle():
+    """Random fused-QKV, column- and row-parallel shapes (incl. GQA m > H_kv,
+    padded leading dimensions, 1/2/4-byte elements): every segment of
+    weight_shard_view addresses exactly the rows / columns of the numpy
+    oracle's Eq.1 view, or both reject the same way."""
+    from oracle import weights as W
+    rng = np.random.default_rng(2024)
+    base = 1 << 36
+    for _ in range(400):
+        e = int(rng.choice([1, 2, 4]))
+        m = int(rng.choice([1, 2, 4, 8, 16]))
+        r = int(rng.integers(0, m))
+        kind = int(rng.integers(0, 3))
+        if kind == F.KV_W_QKV:
+            Hkv = int(rng.choice([1, 2, 4, 8]))
+            Hq = Hkv * int(rng.choice([1, 2, 4, 8]))
+            d = int(rng.choice([1, 2, 4]))
+            hidden = int(rng.integers(1, 9))
+            rows = (Hq + 2 * Hkv) * d
+            ld = hidden + int(rng.integers(0, 3))
+            full = np.arange(rows * ld).reshape(rows, ld)
+            try:
+                ref = W.view_qkv(full[:, :hidden], r, m, Hq, Hkv, d)
+            except (W.RankOutOfRange, W.IndivisibleExtent) as ex:
+                with pytest.raises(F.FlyKVError):
+                    F.weight_shard_view(F.weight_desc(base, rows, hidden, e, kind, ld=ld, num_q_heads=Hq,
+                                                      num_kv_heads=Hkv, head_dim=d), r, m)
+                continue
+            v = F.weight_shard_view(F.weight_desc(base, rows, hidden, e, kind, ld=ld, num_q_heads=Hq,
+                                                  num_kv_heads=Hkv, head_dim=d), r, m)
+            assert v.n_seg == len(ref)
+            for s, rs in zip(v.segments(), ref):
+                r0 = (s.ptr - base) // (e * ld)
+                assert (s.ptr - base) % (e * ld) == 0 and s.row0 == r0 and s.ld == ld and s.cols == hidden
+                assert np.array_equal(full[r0:r0 + s.rows, :hidden], rs)
+        else:
+            rows, cols = int(rng.integers(1, 33)), int(rng.integers(1, 33))
+            ld = cols + int(rng.integers(0, 3))
+            full = np.arange(rows * ld).reshape(rows, ld)
+            fn = W.view_col if kind == F.KV_W_COLUMN else W.view_row
+            try:
+                (ref,) = fn(full[:, :cols], r, m)
+            except (W.RankOutOfRange, W.IndivisibleExtent):
+                with pytest.raises(F.FlyKVError):
+                    F.weight_shard_view(F.weight_desc(base, rows, cols, e, kind, ld=ld), r, m)
+                continue
+            s = F.weight_shard_view(F.weight_desc(base, rows, cols, e, kind, ld=ld), r, m).seg[0]
+            off = s.ptr - base
+            assert off % e == 0 and s.ld == ld
+            r0, c0 = divmod(off // e, ld)
+            assert (s.row0, s.col0) == (r0, c0)
+            assert np.array_equal(full[r0:r0 + s.rows, c0:c0 + s.cols], ref)
