@@ -712,3 +712,41 @@ def test_weight_views_fuzz_against_oracle():
             r0, c0 = divmod(off // e, ld)
             assert (s.row0, s.col0) == (r0, c0)
             assert np.array_equal(full[r0:r0 + s.rows, c0:c0 + s.cols], ref)
+
+
+def test_suggested_rank_ids_are_optimal_by_brute_force():
+    """N2 pin: kv_suggest_rank_ids' assignment keeps as many bytes local as
+    the best of all p! rank-ID permutations of the destination group, with
+    the local bytes of each permutation counted from the oracle's atom map
+    (random sources of every degree, random source rank IDs, p = 2 and 4)."""
+    import itertools
+    rng = np.random.default_rng(77)
+    for case in range(30):
+        H = int(rng.choice([1, 2, 4, 8]))
+        geo = (1, H, 8, 4, 2)
+        og = O.Geom(*geo)
+        p = int(rng.choice([2, 4]))
+        dst = (int(rng.integers(0, 8 // p)) * p, p)
+        c = fake_cache(geo, [512] * 8)
+        mirror = [np.zeros(512, dtype=np.uint8) for _ in range(8)]
+        degs = [q for q in (1, 2, 4, 8) if (q <= H and H % q == 0) or (q > H and q % H == 0)]
+        if not ((p <= H and H % p == 0) or (p > H and p % H == 0)):
+            continue
+        reqs = []
+        for i in range(int(rng.integers(1, 5))):
+            q = int(rng.choice(degs))
+            src = (int(rng.integers(0, 8 // q)) * q, q)
+            T = int(rng.integers(1, 90))
+            srid = [int(x) for x in rng.permutation(q)] if q > 1 and rng.random() < 0.5 else None
+            reqs.append((i, T, src, oracle_alloc(c, mirror, src, O.num_blocks(og, T, q)), dst, srid))
+        sugg = F.kv_suggest_rank_ids(c, reqs, dst)
+
+        def local_bytes(rid):
+            tot = 0
+            for (_, T, s, ids, d, srid) in reqs:
+                tab1 = list(range(O.num_blocks(og, T, d[1])))          # IDs do not matter for locality
+                sg, _, dg, _ = O.atom_map(og, [512] * 8, T, s, list(ids), d, tab1, srid, rid)
+                tot += int((sg == dg).sum())
+            return tot
+        best = max(local_bytes(list(perm)) for perm in itertools.permutations(range(p)))
+        assert local_bytes(sugg) == best, (case, sugg)
