@@ -920,7 +920,12 @@ def run_multi(args):
     degrees = [p for p in (2, 4, 8) if p <= world and world % p == 0]
     cpool = comm.CommunicatorPool(world, degrees, backend="nccl" if nccl else "gloo")   # eager
     world_key = tuple(range(world))
-    barrier = comm.DeviceBarrier(rank, world, list(dict.fromkeys(list(cpool.keys) + [world_key])), dev)
+    barrier = comm.make_barrier(rank, world, list(dict.fromkeys(list(cpool.keys) + [world_key])), dev)
+    host_bar = isinstance(barrier, comm.HostBarrier)
+    bar_kind = "host" if host_bar else "device"
+    bar_desc = ("host: stream sync + process-group barrier (ranks share one GPU, where spinning launches of "
+                "different processes are not co-scheduled)" if host_bar
+                else "kv_group_barrier (device-side, IPC counters)")
     g = F.geometry(w.L, w.H, w.d, w.B, w.e)
     _, _, M = F.kv_layout(g, 1)
     nb, tabs = pools_and_tables(w, args.frag, args.pool_slack, args.placement == "contiguous")
@@ -1015,7 +1020,7 @@ def run_multi(args):
         if timed:
             e1.record(stream)
             ev_pairs.append((e0, e1))
-        barrier.wait(barrier_key(state["reqs"]), stream)   # a5 on the device
+        barrier.wait(barrier_key(state["reqs"]), stream)   # a5
         host_bytes = 0
         for gp in mine:
             n_res, n_ids = plan.resident(gp)
@@ -1146,10 +1151,10 @@ def run_multi(args):
                        "kv_heads": w.H, "head_dim": w.d, "block_base": w.B, "requests": len(w.T),
                        "tokens": w.tokens(), "payload_bytes_per_step": int(payload),
                        "l2": "inputs larger than L2, no flush needed",
-                       "barrier": "kv_group_barrier (device-side, IPC counters)",
-                       "step": ("plan + upload + pack + all_to_all_single + unpack + device barrier + remap"
+                       "barrier": bar_desc,
+                       "step": (f"plan + upload + pack + all_to_all_single + unpack + {bar_kind} barrier + remap"
                                 if args.a2a else
-                                "plan + upload + reshard (P2P push over NVLink) + device barrier + remap")},
+                                f"plan + upload + reshard (P2P push) + {bar_kind} barrier + remap")},
             "switch_latency_ms": round(total_ms / args.steps, 4),
             "reshard_kernel_ms": round(kern_ms, 4),
             "roofline": roof,
@@ -1159,9 +1164,10 @@ def run_multi(args):
                      "d2h_bytes_per_step": int(d2h_all // max(len(lat), 1)),
                      "switch_latency_ms_p50": round(lat_p50, 3), "switch_latency_ms_p99": round(lat_p99, 3),
                      "switch_latency_ms_mean": round(lat_mean, 3),
-                     "api": ("flykv.kv_switch_range: one C-ABI call per rank per switch (plan, upload, push, "
-                             "device barrier, remap of the owned pools, one table read-back, sync)" if not args.a2a
-                             else "plan, kv_pack, all_to_all_single, kv_unpack, device barrier, remap, read-back"),
+                     "api": (f"flykv.{'kv_switch_range_host' if host_bar else 'kv_switch_range'}: one C-ABI call "
+                             f"per rank per switch (plan, upload, push, {bar_kind} barrier, remap of the owned "
+                             "pools, one table read-back, sync)" if not args.a2a
+                             else f"plan, kv_pack, all_to_all_single, kv_unpack, {bar_kind} barrier, remap, read-back"),
                      "note": "per-rank wall clock from a host barrier to its tables on the host; max over ranks"}
                     if lat else None),
             "comm_pool": pool_cost,

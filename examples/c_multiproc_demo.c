@@ -1,16 +1,19 @@
 /*
  * c_multiproc_demo.c -- one process per pool, in plain C (no Python, no torch).
  *
- * N processes (fork; they share cuda:0 here, on a multi-GPU box each would
- * select its own device) each own one paged KV pool (cudaMalloc) and a
- * 128-byte line of barrier counters.  They exchange CUDA IPC handles of both
- * through a MAP_SHARED page, build identical caches and identical source
- * tables (kv_alloc is deterministic), then switch six DP requests DP_N ->
- * TP_N and back, each process calling kv_switch_range for its own pool: plan,
- * push of its atoms into the peers' pools, the device-side group barrier
- * (kv_group_barrier, a5), remap of its pool, read-back.  Check: every source
- * block of every layer a process owned is back, byte for byte, in the blocks
- * of its final DP tables.  Exit code 0 on success.
+ * N processes (fork) each own one paged KV pool (cudaMalloc) and a 128-byte
+ * line of barrier counters.  They exchange CUDA IPC handles of both through a
+ * MAP_SHARED page, build identical caches and identical source tables
+ * (kv_alloc is deterministic), then switch six DP requests DP_N -> TP_N and
+ * back, each process switching its own pool in one call: plan, push of its
+ * atoms into the peers' pools, the group barrier (a5), remap of its pool,
+ * read-back.  With >= N GPUs process r runs on device r and the barrier is
+ * the device-side kv_group_barrier inside kv_switch_range.  With fewer GPUs
+ * the processes share cuda:0 and call kv_switch_range_host with a host
+ * barrier callback: separate launches of different processes that spin on
+ * one another are not co-scheduled on one device.  Check: every source block
+ * of every layer a process owned is back, byte for byte, in the blocks of its
+ * final DP tables.  Exit code 0 on success.
  *
  * Build: gcc -std=c99 -o c_multiproc_demo c_multiproc_demo.c -I../include -lflykv -lcudart
  */
@@ -64,13 +67,29 @@ static void host_barrier(shared_t* sh, int n, int* gen) {
     while (__atomic_load_n(&sh->arrived, __ATOMIC_SEQ_CST) < n * *gen && !sh->failed) usleep(100);
 }
 
+/* kv_switch_range_host's callback: the host barrier over the processes */
+typedef struct {
+    shared_t* sh;
+    int n;
+    int* gen;
+} hb_ctx;
+
+static int32_t host_barrier_cb(void* ctx) {
+    hb_ctx* h = (hb_ctx*)ctx;
+    host_barrier(h->sh, h->n, h->gen);
+    return h->sh->failed ? 1 : 0;
+}
+
 static int run_rank(int rank, int n, shared_t* sh) {
     const kv_geometry geo = {L, 8, 64, 16, 2};
     int64_t M = 0;
     int32_t hl = 0, bt = 0, gen = 0;
     CHECK(kv_layout(&geo, 1, &hl, &bt, &M));
     const size_t pool_bytes = (size_t)L * NB * (size_t)M;
-    CUDA(cudaSetDevice(0));
+    int n_dev = 0;
+    CUDA(cudaGetDeviceCount(&n_dev));
+    const int own_gpu = n_dev >= n; /* one GPU per process: device barrier */
+    CUDA(cudaSetDevice(own_gpu ? rank : 0));
     uint8_t* pool = NULL;
     uint64_t* flags = NULL;
     CUDA(cudaMalloc((void**)&pool, pool_bytes));
@@ -125,9 +144,15 @@ static int run_rank(int rank, int n, shared_t* sh) {
     CUDA(cudaMalloc((void**)&status, sizeof(int32_t)));
     CUDA(cudaMemset(status, 0, sizeof(int32_t)));
 
-    /* DP_n -> TP_n, this process's share in one call (barrier = 1st on these counters) */
+    /* DP_n -> TP_n, this process's share in one call (device barrier: the
+     * 1st on these counters, target n) */
+    hb_ctx hb = {sh, n, &gen};
     kv_plan* p1 = NULL;
-    CHECK(kv_switch_range(c, fwd, NREQ, rank, rank + 1, ctr, n, rank, (uint64_t)n, timeout_ns, status, stream, &p1));
+    if (own_gpu)
+        CHECK(kv_switch_range(c, fwd, NREQ, rank, rank + 1, ctr, n, rank, (uint64_t)n, timeout_ns, status, stream,
+                              &p1));
+    else
+        CHECK(kv_switch_range_host(c, fwd, NREQ, rank, rank + 1, host_barrier_cb, &hb, stream, &p1));
     int32_t ptr[NREQ + 1], tp_ids[NREQ * NB];
     CHECK(kv_plan_dst_tables(p1, ptr, tp_ids));
     for (int i = 0; i < NREQ; ++i) {
@@ -136,8 +161,11 @@ static int run_rank(int rank, int n, shared_t* sh) {
     }
     /* and back, TP_n -> DP_n (2nd barrier: target 2n) */
     kv_plan* p2 = NULL;
-    CHECK(kv_switch_range(c, back, NREQ, rank, rank + 1, ctr, n, rank, 2 * (uint64_t)n, timeout_ns, status, stream,
-                          &p2));
+    if (own_gpu)
+        CHECK(kv_switch_range(c, back, NREQ, rank, rank + 1, ctr, n, rank, 2 * (uint64_t)n, timeout_ns, status,
+                              stream, &p2));
+    else
+        CHECK(kv_switch_range_host(c, back, NREQ, rank, rank + 1, host_barrier_cb, &hb, stream, &p2));
     int32_t st = 0;
     CUDA(cudaMemcpy(&st, status, sizeof st, cudaMemcpyDeviceToHost));
     if (st) {
@@ -201,7 +229,7 @@ int main(int argc, char** argv) {
         waitpid(pids[r], &status, 0);
         ok = ok && WIFEXITED(status) && WEXITSTATUS(status) == 0;
     }
-    printf(ok ? "multi-process round-trip byte-exact (%d processes, kv_switch_range + device barrier)\n"
+    printf(ok ? "multi-process round-trip byte-exact (%d processes, kv_switch_range / kv_switch_range_host)\n"
               : "FAILED (%d processes)\n", n);
     return ok ? 0 : 1;
 }

@@ -47,7 +47,8 @@ typedef enum {
     KV_ERR_DUPLICATE_REQUEST = 8,  /* same req_id twice in one plan (S:207 DoubleAllocate) */
     KV_ERR_BAD_STATE = 9,          /* call out of order (e.g. reshard after commit)    */
     KV_ERR_CUDA = 10,              /* a CUDA runtime call failed; see kv_last_error()  */
-    KV_ERR_REPLICA_MISMATCH = 11   /* strict mode: replicated source heads differ (R10) */
+    KV_ERR_REPLICA_MISMATCH = 11,  /* strict mode: replicated source heads differ (R10) */
+    KV_ERR_BARRIER = 12            /* a host barrier callback reported failure (kv_switch_range_host) */
 } kv_status;
 
 /* Model KV geometry.  block_base = B (DP tokens per block).  Requirement:
@@ -352,6 +353,28 @@ kv_status kv_switch_range(kv_cache* cache, const kv_request* reqs, int32_t n_req
                           uint64_t* const* barrier_flags, int32_t n_members, int32_t self, uint64_t barrier_target,
                           int64_t timeout_ns, int32_t* barrier_status, void* stream, kv_plan** out);
 
+/*
+ * kv_switch_range_host: kv_switch_range with a HOST barrier in place of
+ * kv_group_barrier (a5): after the owned pools' pushes the library
+ * synchronizes `stream` (the push kernel ends with a system-scope fence, so
+ * its peer stores are visible), then calls barrier(barrier_ctx) -- the
+ * caller's host barrier over the members (e.g. a gloo / NCCL barrier);
+ * when it returns every member's pushes have landed -- then remaps the
+ * owned pools and reads the tables back as kv_switch_range does.  For
+ * processes whose pools cannot spin on one another's device counters: ranks
+ * that share one GPU (separate launches that wait on one another are not
+ * guaranteed to be co-scheduled on one device), or peers without mapped
+ * counters.  barrier NULL: no other process is involved.
+ *   barrier  int32_t fn(void* ctx), returns 0 on success; called once, on the
+ *            calling thread, with no library lock held
+ * Errors as kv_switch_range; a non-zero callback return gives
+ * KV_ERR_BARRIER and the (uncommitted) plan is rolled back.
+ */
+typedef int32_t (*kv_host_barrier_fn)(void* ctx);
+kv_status kv_switch_range_host(kv_cache* cache, const kv_request* reqs, int32_t n_reqs, int32_t gpu_lo,
+                               int32_t gpu_hi, kv_host_barrier_fn barrier, void* barrier_ctx, void* stream,
+                               kv_plan** out);
+
 /* kv_switch_multi: a switch in waves (kv_plan_waves, or the block-aligned
  * pieces of kv_plan_pieces turned into plain requests) with no host sync
  * between the waves: each wave is planned once the previous one committed
@@ -621,6 +644,25 @@ kv_status kv_ipc_close(void* dptr, uint64_t offset);
 kv_status kv_group_barrier(uint64_t* const* flags, int32_t n_members, int32_t self, uint64_t target,
                            int64_t timeout_ns, int32_t* status, void* stream);
 
+/*
+ * kv_group_barrier_selftest (test utility): the device barrier of
+ * kv_group_barrier run by n_members emulated members, the CTAs of ONE
+ * cooperative launch on the current device (co-resident by construction;
+ * separate launches that spin on one another must not share a device).
+ * Per round k (1..rounds) member m stores k into its payload word, runs the
+ * same arrive/wait code as flykv_barrier_kernel on counters laid out as for
+ * kv_group_barrier (target k * n_members), then loads every member's
+ * payload.  *errors = loads that saw a value < k (a member passed the
+ * barrier before another's prior store was visible: must be 0); member
+ * `absent` (-1: none) never arrives, so the others end their wait after
+ * timeout_ns and *timeouts counts them.  Synchronous; allocates and frees
+ * its own device memory.  Errors: KV_ERR_INVALID_ARG (n_members outside
+ * [1, 64], rounds < 1, absent >= n_members, timeout <= 0, NULL outputs),
+ * KV_ERR_CUDA.
+ */
+kv_status kv_group_barrier_selftest(int32_t n_members, int32_t rounds, int32_t absent, int64_t timeout_ns,
+                                    int32_t* errors, int32_t* timeouts);
+
 /* Make all prior writes of this device (incl. NVLink peer stores) visible
  * system-wide before a host-side barrier: synchronizes `stream`. */
 kv_status kv_stream_sync(void* stream);
@@ -734,11 +776,14 @@ kv_status kv_cache_set_work_order(kv_cache* cache, int32_t order);
  * BAD_STATE (committed or detached plan), KV_ERR_CUDA.
  *
  * kv_cache_set_strict(cache, 1): kv_switch / kv_switch_multi /
- * kv_switch_waves / kv_switch_back verify every plan first (after its
- * upload, before its reshard) and, on a mismatch, roll the plan back (no
- * state change, no byte moved) and return KV_ERR_REPLICA_MISMATCH.  Costs
- * one read of every replicated source byte and a host sync per plan with
- * replicated sources.  Default 0 (off).
+ * kv_switch_waves / kv_switch_back / kv_switch_range / kv_switch_range_host
+ * verify every plan first (after its upload, before its reshard) and, on a
+ * mismatch, roll the plan back (no state change, no byte moved) and return
+ * KV_ERR_REPLICA_MISMATCH.  In a one-process-per-GPU job every process
+ * checks every replicated item (peers' pools through their mappings), so
+ * all processes reach the same decision.  Costs one read of every
+ * replicated source byte and a host sync per plan with replicated sources.
+ * Default 0 (off).
  */
 kv_status kv_verify_replicas(kv_plan* plan, void* stream, int64_t* mismatches, uint64_t* first);
 kv_status kv_cache_set_strict(kv_cache* cache, int32_t strict);

@@ -14,6 +14,9 @@
   device: per-process 64-bit counters in IPC-shared memory, one per pooled
   group, advanced by kv_group_barrier (system-scope release adds + acquire
   spin) -- no host round trip and no collective on the data path.
+  HostBarrier: the same interface on the host (stream sync + process-group
+  barrier) for ranks that share one GPU, where spinning launches of
+  different processes are not co-scheduled; make_barrier picks one.
 * A process may own several consecutive pools ("virtual ranks": the 8
   engines of a switch mapped onto fewer GPUs); exchange_pools and the
   barrier work on processes, the plan on pools.
@@ -21,6 +24,7 @@
 from __future__ import annotations
 
 import os
+import socket
 import time
 
 import torch
@@ -286,6 +290,61 @@ class DeviceBarrier:
     def close(self):
         close_pools(self.imported)
         self.imported = []
+
+
+class HostBarrier:
+    """a5 on the host, same interface as DeviceBarrier: wait(key, stream)
+    synchronizes the stream (this process's pushes have completed) and then
+    runs a process-group barrier over the key's members; arm(key) returns a
+    callable for kv_switch_range_host (the library syncs, then calls it).
+    For ranks that share one GPU: a device barrier there would be separate
+    launches spinning on one another on one device, which nothing
+    co-schedules."""
+
+    def __init__(self, rank: int, world: int, keys, group=None):
+        self.rank, self.world = rank, world
+        self.keys = [tuple(k) for k in keys]
+        self.slot = {k: i for i, k in enumerate(self.keys)}
+        self.groups = {}
+        for k in self.keys:   # new_group is collective: every rank, same order
+            self.groups[k] = group if len(k) == world else dist.new_group(list(k))
+
+    def arm(self, key):
+        key = tuple(key)
+        if self.rank not in key or len(key) < 2:
+            return None
+        g = self.groups[key]
+        return lambda: dist.barrier(group=g)
+
+    def wait(self, key, stream):
+        fn = self.arm(key)
+        if fn is not None:
+            flykv.stream_sync(stream)
+            fn()
+
+    def check(self):
+        pass
+
+    def close(self):
+        pass
+
+
+def ranks_share_a_device(device, group=None) -> bool:
+    """True when two ranks of the job run on the same physical GPU."""
+    props = torch.cuda.get_device_properties(device)
+    me = (socket.gethostname(), str(getattr(props, "uuid", "")) or f"{props.pci_bus_id}")
+    allv = [None] * dist.get_world_size(group)
+    dist.all_gather_object(allv, me, group=group)
+    return len(set(allv)) < len(allv)
+
+
+def make_barrier(rank: int, world: int, keys, device, timeout_s: float = 60.0, group=None):
+    """a5 for a one-process-per-GPU job: DeviceBarrier when every rank has
+    its own GPU; HostBarrier when ranks share one (test mode on a one-GPU
+    box)."""
+    if ranks_share_a_device(device, group):
+        return HostBarrier(rank, world, keys, group)
+    return DeviceBarrier(rank, world, keys, device, timeout_s, group)
 
 
 def close_pools(imported):

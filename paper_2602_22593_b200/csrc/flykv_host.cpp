@@ -1640,6 +1640,27 @@ static inline int64_t now_ns() {
         .count();
 }
 
+// R10 strict mode (kv_cache_set_strict): replicated sources must agree
+// before any byte moves.  Every process of a one-process-per-GPU job checks
+// every item of the plan (peers' pools through their mappings), so all of
+// them reach the same decision.
+static kv_status strict_check(kv_plan* p, cudaStream_t stream) {
+    kv_cache* c = p->c;
+    if (!c->strict) return KV_OK;
+    int64_t bad = 0;
+    uint64_t first = 0;
+    kv_status s = kv_verify_replicas(p, stream, &bad, &first);
+    if (s) return s;
+    if (bad)
+        return fail(KV_ERR_REPLICA_MISMATCH,
+                    "%lld source atoms differ from their canonical replica (first: item %llu, "
+                    "layer %llu, K/V %llu, chunk %llu); nothing moved",
+                    (long long)bad, (unsigned long long)((first >> 32) / (2ull * c->geo.num_layers)),
+                    (unsigned long long)(((first >> 32) % (2ull * c->geo.num_layers)) >> 1),
+                    (unsigned long long)((first >> 32) & 1ull), (unsigned long long)(first & 0xffffffffull));
+    return KV_OK;
+}
+
 static kv_status switch_enqueue(kv_cache* c, const kv_request* reqs, int32_t n_reqs, cudaStream_t stream,
                                 kv_plan** out) {
     *out = nullptr;
@@ -1662,20 +1683,8 @@ static kv_status switch_enqueue(kv_cache* c, const kv_request* reqs, int32_t n_r
     s = ensure_device(p, stream);
     if (s) return abort_plan(s);
     p->last_stream = stream;
-    if (c->strict) {  // R10: replicated sources must agree before any byte moves
-        int64_t bad = 0;
-        uint64_t first = 0;
-        s = kv_verify_replicas(p, stream, &bad, &first);
-        if (s) return abort_plan(s);
-        if (bad)
-            return abort_plan(fail(KV_ERR_REPLICA_MISMATCH,
-                                   "%lld source atoms differ from their canonical replica (first: item %llu, "
-                                   "layer %llu, K/V %llu, chunk %llu); nothing moved",
-                                   (long long)bad, (unsigned long long)((first >> 32) / (2ull * c->geo.num_layers)),
-                                   (unsigned long long)(((first >> 32) % (2ull * c->geo.num_layers)) >> 1),
-                                   (unsigned long long)((first >> 32) & 1ull),
-                                   (unsigned long long)(first & 0xffffffffull)));
-    }
+    s = strict_check(p, stream);
+    if (s) return abort_plan(s);
     cudaError_t e = cudaMallocFromPoolAsync(reinterpret_cast<void**>(&p->d_out), (size_t)elems * 4, c->pool, stream);
     if (e != cudaSuccess) return abort_plan(cuda_fail(e, "cudaMallocFromPoolAsync (tables)"));
     s = kv_reshard(p, -1, stream);
@@ -1725,15 +1734,14 @@ extern "C" kv_status kv_switch(kv_cache* c, const kv_request* reqs, int32_t n_re
     return switch_read_back(*out, stream);
 }
 
-extern "C" kv_status kv_switch_range(kv_cache* c, const kv_request* reqs, int32_t n_reqs, int32_t gpu_lo,
-                                     int32_t gpu_hi, uint64_t* const* barrier_flags, int32_t n_members, int32_t self,
-                                     uint64_t barrier_target, int64_t timeout_ns, int32_t* barrier_status,
-                                     void* stream_, kv_plan** out) {
-    if (!c || !out) return fail(KV_ERR_INVALID_ARG, "bad kv_switch_range arguments");
-    *out = nullptr;
-    if (gpu_lo < 0 || gpu_hi > c->n_gpus || gpu_lo >= gpu_hi)
-        return fail(KV_ERR_INVALID_ARG, "pool range [%d, %d) is not inside [0, %d)", gpu_lo, gpu_hi, c->n_gpus);
-    if (n_members > 1 && !barrier_flags) return fail(KV_ERR_INVALID_ARG, "barrier_flags is NULL");
+// kv_switch_range and kv_switch_range_host: plan, upload, push of the owned
+// pools, then `barrier` (a5: every member's pushes have landed), then the
+// owned pools' remaps and one read-back.  `barrier(plan, stream)` returns a
+// status; the plan is not committed before it (the first remap commits), so
+// a failed barrier rolls the plan back.
+template <typename Barrier>
+static kv_status switch_range_impl(kv_cache* c, const kv_request* reqs, int32_t n_reqs, int32_t gpu_lo,
+                                   int32_t gpu_hi, void* stream_, kv_plan** out, Barrier&& barrier) {
     cudaStream_t stream = static_cast<cudaStream_t>(stream_);
     kv_plan* p = nullptr;
     const int64_t t0 = now_ns();
@@ -1753,14 +1761,14 @@ extern "C" kv_status kv_switch_range(kv_cache* c, const kv_request* reqs, int32_
     s = ensure_device(p, stream);
     if (s) return abort_plan(s);
     p->last_stream = stream;
+    s = strict_check(p, stream);
+    if (s) return abort_plan(s);
     cudaError_t e = cudaMallocFromPoolAsync(reinterpret_cast<void**>(&p->d_out), (size_t)elems * 4, c->pool, stream);
     if (e != cudaSuccess) return abort_plan(cuda_fail(e, "cudaMallocFromPoolAsync (tables)"));
     s = kv_reshard_range(p, gpu_lo, gpu_hi, stream);
     if (s) return abort_plan(s);
-    if (n_members > 1) {  // a5: every member's pushes have landed before anyone remaps
-        s = kv_group_barrier(barrier_flags, n_members, self, barrier_target, timeout_ns, barrier_status, stream);
-        if (s) return abort_plan(s);
-    }
+    s = barrier(p, stream);
+    if (s) return abort_plan(s);
     for (int32_t g = gpu_lo; g < gpu_hi; ++g) {  // the owned pools' tables, at their packed offsets
         const int32_t* off = p->out_off.data() + 3 * g;
         s = kv_remap_block_tables(p, g, p->d_out + off[0], p->d_out + p->out_rp + off[1],
@@ -1771,6 +1779,40 @@ extern "C" kv_status kv_switch_range(kv_cache* c, const kv_request* reqs, int32_
     *out = p;  // committed by the first remap call
     if (s) return s;
     return switch_read_back(p, stream);
+}
+
+extern "C" kv_status kv_switch_range(kv_cache* c, const kv_request* reqs, int32_t n_reqs, int32_t gpu_lo,
+                                     int32_t gpu_hi, uint64_t* const* barrier_flags, int32_t n_members, int32_t self,
+                                     uint64_t barrier_target, int64_t timeout_ns, int32_t* barrier_status,
+                                     void* stream_, kv_plan** out) {
+    if (!c || !out) return fail(KV_ERR_INVALID_ARG, "bad kv_switch_range arguments");
+    *out = nullptr;
+    if (gpu_lo < 0 || gpu_hi > c->n_gpus || gpu_lo >= gpu_hi)
+        return fail(KV_ERR_INVALID_ARG, "pool range [%d, %d) is not inside [0, %d)", gpu_lo, gpu_hi, c->n_gpus);
+    if (n_members > 1 && !barrier_flags) return fail(KV_ERR_INVALID_ARG, "barrier_flags is NULL");
+    return switch_range_impl(c, reqs, n_reqs, gpu_lo, gpu_hi, stream_, out, [&](kv_plan*, cudaStream_t stream) {
+        if (n_members <= 1) return KV_OK;
+        return kv_group_barrier(barrier_flags, n_members, self, barrier_target, timeout_ns, barrier_status, stream);
+    });
+}
+
+extern "C" kv_status kv_switch_range_host(kv_cache* c, const kv_request* reqs, int32_t n_reqs, int32_t gpu_lo,
+                                          int32_t gpu_hi, kv_host_barrier_fn barrier, void* barrier_ctx,
+                                          void* stream_, kv_plan** out) {
+    if (!c || !out) return fail(KV_ERR_INVALID_ARG, "bad kv_switch_range_host arguments");
+    *out = nullptr;
+    if (gpu_lo < 0 || gpu_hi > c->n_gpus || gpu_lo >= gpu_hi)
+        return fail(KV_ERR_INVALID_ARG, "pool range [%d, %d) is not inside [0, %d)", gpu_lo, gpu_hi, c->n_gpus);
+    return switch_range_impl(c, reqs, n_reqs, gpu_lo, gpu_hi, stream_, out, [&](kv_plan*, cudaStream_t stream) {
+        if (!barrier) return KV_OK;
+        // this process's pushes (peer stores end with a system-scope fence)
+        // have completed before the host barrier is entered
+        cudaError_t e = cudaStreamSynchronize(stream);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize (before the host barrier)");
+        const int32_t rc = barrier(barrier_ctx);
+        if (rc != 0) return fail(KV_ERR_BARRIER, "host barrier callback returned %d", rc);
+        return KV_OK;
+    });
 }
 
 extern "C" kv_status kv_switch_multi(kv_cache* c, const kv_request* reqs, const int32_t* wave_ptr, int32_t n_waves,
@@ -2084,6 +2126,46 @@ extern "C" kv_status kv_group_barrier(uint64_t* const* flags, int32_t n_members,
     return KV_OK;
 }
 
+extern "C" kv_status kv_group_barrier_selftest(int32_t n_members, int32_t rounds, int32_t absent, int64_t timeout_ns,
+                                               int32_t* errors, int32_t* timeouts) {
+    if (n_members < 1 || n_members > 64 || rounds < 1 || absent >= n_members || timeout_ns <= 0 || !errors ||
+        !timeouts)
+        return fail(KV_ERR_INVALID_ARG, "bad kv_group_barrier_selftest arguments (n_members %d, rounds %d)",
+                    n_members, rounds);
+    // counters, payload (one 128-byte line per member each), errors, timeouts
+    const size_t line = 16 * sizeof(unsigned long long), bytes = 2 * (size_t)n_members * line + 2 * sizeof(int32_t);
+    char* buf = nullptr;
+    cudaError_t e = cudaMalloc(&buf, bytes);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc (barrier self-test)");
+    cudaStream_t st = nullptr;
+    kv_status s = KV_OK;
+    int32_t out[2] = {0, 0};
+    e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaMemsetAsync(buf, 0, bytes, st);
+    if (e == cudaSuccess) {
+        BarrierArgs a{};
+        auto* ctr = reinterpret_cast<unsigned long long*>(buf);
+        for (int32_t m = 0; m < n_members; ++m) a.flags[m] = ctr + 16 * m;
+        a.n = n_members;
+        a.self = 0;
+        a.target = 0;
+        a.timeout_ns = timeout_ns;
+        a.status = nullptr;
+        auto* payload = ctr + 16 * n_members;
+        auto* cnt = reinterpret_cast<int32_t*>(buf + 2 * (size_t)n_members * line);
+        e = launch_barrier_selftest(a, rounds, absent, payload, cnt, cnt + 1, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(out, cnt, sizeof(out), cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e == cudaSuccess) g_launches.fetch_add(1);
+    }
+    if (e != cudaSuccess) s = cuda_fail(e, "barrier self-test");
+    if (st) cudaStreamDestroy(st);
+    cudaFree(buf);
+    *errors = out[0];
+    *timeouts = out[1];
+    return s;
+}
+
 // ------------------------------------------------------------ misc
 extern "C" const char* kv_strerror(kv_status s) {
     switch (s) {
@@ -2099,6 +2181,7 @@ extern "C" const char* kv_strerror(kv_status s) {
         case KV_ERR_BAD_STATE: return "bad state";
         case KV_ERR_CUDA: return "CUDA error";
         case KV_ERR_REPLICA_MISMATCH: return "replicated source heads differ";
+        case KV_ERR_BARRIER: return "host barrier failed";
     }
     return "unknown status";
 }

@@ -217,6 +217,8 @@ cudaError_t launch_gather(const GatherSeg* segs, int n_seg, char* dst, cudaStrea
 cudaError_t launch_decode(const DecodeArgs& a, cudaStream_t s);
 cudaError_t launch_unpack(const UnpackArgs& a, int device, cudaStream_t s);
 cudaError_t launch_barrier(const BarrierArgs& a, cudaStream_t s);
+cudaError_t launch_barrier_selftest(const BarrierArgs& a, int32_t rounds, int32_t absent,
+                                    unsigned long long* payload, int32_t* errors, int32_t* timeouts, cudaStream_t s);
 cudaError_t launch_verify(const VerifyArgs& a, cudaStream_t s);
 
 }  // namespace flykv

@@ -897,30 +897,67 @@ cudaError_t launch_remap(const RemapArgs& a, int n_ctas, cudaStream_t s) {
 // none can pass barrier k+1 before all have arrived at it).  A member that
 // never arrives ends the wait after timeout_ns (%globaltimer): *status = 1
 // if status is given, else the kernel traps (a loud CUDA error, never a hang).
-__global__ void flykv_barrier_kernel(const BarrierArgs a) {
+__device__ __forceinline__ bool group_barrier(unsigned long long* const* flags, int n, int self, uint64_t target,
+                                              int64_t timeout_ns) {
     asm volatile("fence.sc.sys;" ::: "memory");
-    for (int m = 0; m < a.n; ++m)
-        asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(a.flags[m]) : "memory");
+    for (int m = 0; m < n; ++m) asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(flags[m]) : "memory");
     uint64_t t0, t, v;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     while (true) {
-        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(a.flags[a.self]) : "memory");
-        if (v >= a.target) break;
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags[self]) : "memory");
+        if (v >= target) return true;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        if ((int64_t)(t - t0) > a.timeout_ns) {
-            if (a.status) {
-                *a.status = 1;
-                return;
-            }
-            __trap();
-        }
+        if ((int64_t)(t - t0) > timeout_ns) return false;
         __nanosleep(200);
     }
+}
+
+__global__ void flykv_barrier_kernel(const BarrierArgs a) {
+    if (group_barrier(a.flags, a.n, a.self, a.target, a.timeout_ns)) return;
+    if (a.status) {
+        *a.status = 1;
+        return;
+    }
+    __trap();
 }
 
 cudaError_t launch_barrier(const BarrierArgs& a, cudaStream_t s) {
     flykv_barrier_kernel<<<1, 1, 0, s>>>(a);
     return cudaGetLastError();
+}
+
+// kv_group_barrier_selftest: the members of one group emulated as the CTAs of
+// ONE cooperative launch (co-resident by construction -- separate launches
+// that spin on one another are never run on one device).  CTA m is member m:
+// per round k it stores k into its payload word (its "push"), runs the
+// production barrier (group_barrier, target k*n on its own counter), then
+// loads every member's payload: a value < k means a member passed the
+// barrier before another's push was visible.  CTA `absent` never arrives
+// (timeout path).  counters: n lines of 16 u64; payload: n lines of 16 u64.
+__global__ void flykv_barrier_selftest_kernel(const BarrierArgs a, int32_t rounds, int32_t absent,
+                                              unsigned long long* payload, int32_t* errors, int32_t* timeouts) {
+    const int m = blockIdx.x;
+    if (threadIdx.x != 0 || m == absent) return;
+    for (int32_t k = 1; k <= rounds; ++k) {
+        volatile unsigned long long* mine = payload + 16 * m;
+        *mine = (unsigned long long)k;
+        if (!group_barrier(a.flags, a.n, m, (uint64_t)k * a.n, a.timeout_ns)) {
+            atomicAdd(timeouts, 1);
+            return;
+        }
+        for (int j = 0; j < a.n; ++j) {
+            const volatile unsigned long long* other = payload + 16 * j;
+            if (*other < (unsigned long long)k) atomicAdd(errors, 1);
+        }
+    }
+}
+
+cudaError_t launch_barrier_selftest(const BarrierArgs& a, int32_t rounds, int32_t absent,
+                                    unsigned long long* payload, int32_t* errors, int32_t* timeouts, cudaStream_t s) {
+    BarrierArgs aa = a;
+    void* args[] = {&aa, &rounds, &absent, &payload, &errors, &timeouts};
+    return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(flykv_barrier_selftest_kernel), dim3(a.n), dim3(32),
+                                       args, 0, s);
 }
 
 // ---------------------------------------------------------------- verify

@@ -33,7 +33,7 @@ STATUS_NAMES = {
     0: "KV_OK", 1: "KV_ERR_INVALID_ARG", 2: "KV_ERR_INDIVISIBLE_DEGREE", 3: "KV_ERR_UNKNOWN_GROUP",
     4: "KV_ERR_RANK_OUT_OF_RANGE", 5: "KV_ERR_INDIVISIBLE_EXTENT", 6: "KV_ERR_OUT_OF_BLOCKS",
     7: "KV_ERR_BAD_BLOCK_TABLE", 8: "KV_ERR_DUPLICATE_REQUEST", 9: "KV_ERR_BAD_STATE", 10: "KV_ERR_CUDA",
-    11: "KV_ERR_REPLICA_MISMATCH",
+    11: "KV_ERR_REPLICA_MISMATCH", 12: "KV_ERR_BARRIER",
 }
 
 
@@ -135,6 +135,10 @@ _sig("kv_plan_tables", C.c_int, _P, C.c_int32, C.c_int32, C.POINTER(_I32P), C.PO
 _sig("kv_switch_back", C.c_int, _P, _P, _P, C.POINTER(_P))
 _sig("kv_switch_range", C.c_int, _P, C.POINTER(Request), C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_void_p),
      C.c_int32, C.c_int32, C.c_uint64, C.c_int64, _P, _P, C.POINTER(_P))
+HOST_BARRIER_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p)
+_sig("kv_switch_range_host", C.c_int, _P, C.POINTER(Request), C.c_int32, C.c_int32, C.c_int32, HOST_BARRIER_FN, _P,
+     _P, C.POINTER(_P))
+_sig("kv_group_barrier_selftest", C.c_int, C.c_int32, C.c_int32, C.c_int32, C.c_int64, _I32P, _I32P)
 _sig("kv_switch_multi", C.c_int, _P, C.POINTER(Request), _I32P, C.c_int32, _P, C.POINTER(_P))
 _sig("kv_pack", C.c_int, _P, C.c_int32, _P, _I64P, _P)
 _sig("kv_unpack", C.c_int, _P, C.c_int32, _P, _I64P, _P)
@@ -196,13 +200,13 @@ _sig("kv_plan_work_order", C.c_int, _P, C.c_int32, _I32P, _I64P)
 
 EXPORTED = ["kv_cache_create", "kv_cache_destroy", "kv_layout", "kv_blocks_for", "kv_alloc", "kv_reserve",
             "kv_free", "kv_free_count", "kv_held_mask", "kv_plan_switch", "kv_plan_upload", "kv_reshard", "kv_reshard_range", "kv_reshard_staged",
-            "kv_pack", "kv_unpack", "kv_switch", "kv_switch_back", "kv_switch_range", "kv_switch_multi", "kv_switch_waves", "kv_plan_tables", "kv_plan_resident",
+            "kv_pack", "kv_unpack", "kv_switch", "kv_switch_back", "kv_switch_range", "kv_switch_range_host", "kv_switch_multi", "kv_switch_waves", "kv_plan_tables", "kv_plan_resident",
             "kv_remap_block_tables", "kv_plan_dst_tables", "kv_plan_commit", "kv_plan_waves", "kv_plan_pieces",
             "kv_suggest_rank_ids", "kv_plan_get_stats", "kv_plan_a2a_offsets", "kv_piece_request", "kv_plan_packed_offsets",
             "kv_plan_destroy",
             "weight_shard_view", "kv_gather_view", "kv_vmm_granularity", "kv_vmm_alloc", "kv_vmm_free",
             "weight_view_alias", "weight_view_unalias", "kv_paged_decode", "kv_ipc_export", "kv_ipc_import", "kv_ipc_close",
-            "kv_group_barrier", "kv_stream_sync", "kv_strerror", "kv_last_error", "kv_launch_count", "kv_set_reshard_impl",
+            "kv_group_barrier", "kv_group_barrier_selftest", "kv_stream_sync", "kv_strerror", "kv_last_error", "kv_launch_count", "kv_set_reshard_impl",
             "kv_cache_set_work_order", "kv_plan_work_order", "kv_cache_set_strict", "kv_verify_replicas",
             "kv_pool_alloc", "kv_pool_export", "kv_pool_import", "kv_pool_free", "kv_mc_supported", "kv_mc_create",
             "kv_mc_import", "kv_mc_add_device", "kv_mc_bind", "kv_mc_map", "kv_mc_free", "kv_close_fd",
@@ -524,12 +528,33 @@ def kv_switch(cache: KVCache, requests, stream=None) -> Plan:
 
 def kv_switch_range(cache: KVCache, requests, gpu_lo: int, gpu_hi: int, barrier=None, stream=None) -> Plan:
     """kv_switch for one process of a one-process-per-GPU job owning pools
-    [gpu_lo, gpu_hi): plan, upload, push, device group barrier, remap of the
-    owned pools, one read-back, sync -- one C call (kv_switch_range).
+    [gpu_lo, gpu_hi): plan, upload, push, group barrier, remap of the owned
+    pools, one read-back, sync -- one C call.
     barrier: (flags, self_index, target, timeout_ns, status) from
-    comm.DeviceBarrier.arm(key), or None when no other process is involved."""
+    comm.DeviceBarrier.arm(key) -> kv_switch_range (device barrier); a
+    callable from comm.HostBarrier.arm(key) -> kv_switch_range_host (the
+    library syncs the stream, then calls it); None when no other process is
+    involved."""
     ra = make_requests(requests)
     h = C.c_void_p()
+    if callable(barrier):
+        err = []
+
+        def _cb(_ctx):
+            try:
+                barrier()
+                return 0
+            except Exception as ex:  # reported as KV_ERR_BARRIER; the exception is chained below
+                err.append(ex)
+                return 1
+
+        st = _lib.kv_switch_range_host(cache._h, ra.ptr, ra.n, gpu_lo, gpu_hi, HOST_BARRIER_FN(_cb), None,
+                                       stream_of(stream), C.byref(h))
+        plan = Plan(cache, h, ra.n) if h.value else None
+        if st != KV_OK:
+            raise FlyKVError(st, _lib.kv_last_error().decode(), [plan] if plan is not None else []) from (
+                err[0] if err else None)
+        return plan
     if barrier is None:
         arr, n_m, me, tgt, tmo, status = None, 0, 0, 0, 1, None
     else:
@@ -796,6 +821,16 @@ def kv_group_barrier(flags, self_index: int, target: int, timeout_ns: int, statu
     arr = (C.c_void_p * len(flags))(*[ptr_of(f) for f in flags])
     _check(_lib.kv_group_barrier(arr, len(flags), self_index, int(target), int(timeout_ns), ptr_of(status),
                                  stream_of(stream)))
+
+
+def group_barrier_selftest(n_members: int, rounds: int, absent: int = -1, timeout_ns: int = int(5e9)):
+    """kv_group_barrier_selftest: the device barrier run by n_members members
+    emulated as the CTAs of one cooperative launch.  Returns (errors,
+    timeouts): ordering violations seen (must be 0) and members that ended
+    their wait by timeout (those waiting on `absent`)."""
+    e, t = C.c_int32(0), C.c_int32(0)
+    _check(_lib.kv_group_barrier_selftest(n_members, rounds, absent, int(timeout_ns), C.byref(e), C.byref(t)))
+    return int(e.value), int(t.value)
 
 
 def stream_sync(stream=None):

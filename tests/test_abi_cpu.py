@@ -623,8 +623,8 @@ def test_packed_offsets_are_the_documented_prefixes():
 
 def test_round2_entry_points_validate_before_the_device():
     """Argument checks of this round's entry points need no GPU: bad pool
-    ranges (kv_reshard_range, kv_switch_range), barrier arguments
-    (kv_group_barrier), multicast teams (kv_cache_set_multicast), strict-mode
+    ranges (kv_reshard_range, kv_switch_range, kv_switch_range_host), barrier
+    arguments (kv_group_barrier, kv_group_barrier_selftest), multicast teams (kv_cache_set_multicast), strict-mode
     flags; kv_verify_replicas of a plan without replicated sources is (0,
     none) without touching the device."""
     c = fake_cache((1, 4, 8, 4, 2), [64] * 4)
@@ -640,6 +640,14 @@ def test_round2_entry_points_validate_before_the_device():
     with pytest.raises(F.FlyKVError) as e:
         F.kv_switch_range(c, reqs, 2, 9)
     assert e.value.name == "KV_ERR_INVALID_ARG"
+    called = []   # kv_switch_range_host: the same checks, the callback never runs
+    with pytest.raises(F.FlyKVError) as e:
+        F.kv_switch_range(c, reqs, 2, 9, lambda: called.append(1))
+    assert e.value.name == "KV_ERR_INVALID_ARG" and not called
+    for n, rounds, absent, tmo in ((0, 1, -1, 1), (65, 1, -1, 1), (2, 0, -1, 1), (2, 1, 2, 1), (2, 1, -1, 0)):
+        with pytest.raises(F.FlyKVError) as e:   # barrier self-test arguments, before any device work
+            F.group_barrier_selftest(n, rounds, absent, tmo)
+        assert e.value.name == "KV_ERR_INVALID_ARG"
     assert all(c.free_count(g) == 64 - (5 if g == 0 else 0) for g in range(4))   # nothing planned
     for args in (([], 0, 1), ([1 << 40], 1, 1), ([1 << 40 | 4], 0, 1), ([1 << 40], 0, 0)):
         flags, me, tmo = args

@@ -1,8 +1,9 @@
 """The C ABI from plain C: examples/c_switch_demo.c (gcc -std=c99, no Python,
 no torch) allocates pools with cudaMalloc, switches DP2 -> TP2 -> DP2 and
 checks the round trip byte for byte; examples/c_multiproc_demo.c does the
-same with one forked process per pool (CUDA IPC, kv_switch_range, the
-device-side group barrier)."""
+same with one forked process per pool (CUDA IPC, kv_switch_range with the
+device-side group barrier when every process has its own GPU, else
+kv_switch_range_host with a host barrier)."""
 import os
 import subprocess
 
@@ -36,9 +37,9 @@ def test_c_example_runs():
 @pytest.mark.parametrize("n", [2, 4])
 def test_c_multiproc_example_runs(n):
     """examples/c_multiproc_demo.c: n forked processes, one pool each, CUDA
-    IPC peer pools, kv_switch_range (push + device barrier + remap) DP_n ->
-    TP_n -> DP_n, round trip byte-exact -- the multi-process path with no
-    Python anywhere."""
+    IPC peer pools, one call per switch (push + barrier + remap; on one GPU
+    kv_switch_range_host with a host barrier) DP_n -> TP_n -> DP_n, round
+    trip byte-exact -- the multi-process path with no Python anywhere."""
     r = subprocess.run([_bin(mp=True), str(n)], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "multi-process round-trip byte-exact" in r.stdout

@@ -145,3 +145,45 @@ def test_share_fds_gloo():
             p.join(timeout=60)
     for r in range(world):
         assert res[r] == {s: f"rank {s}" for s in range(world) if s != r}
+
+
+def _hb_worker(rank, world, port, q):
+    import time as _t
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        keys = [(0, 1), (2, 3), (0, 1, 2, 3)]
+        hb = comm.HostBarrier(rank, world, keys)
+        out = {"outside": hb.arm((2, 3) if rank < 2 else (0, 1)) is None}
+        # a member that arrives late holds the others: ranks 1 and 3 sleep 0.3 s
+        # before their subgroup barrier, so 0 and 2 leave it no earlier
+        fn = hb.arm((0, 1) if rank < 2 else (2, 3))
+        t0 = _t.perf_counter()
+        if rank % 2:
+            _t.sleep(0.3)
+        fn()
+        out["held_s"] = _t.perf_counter() - t0
+        hb.arm((0, 1, 2, 3))()
+        out["ok"] = True
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_host_barrier_gloo():
+    """comm.HostBarrier (a5 for ranks sharing one GPU) on 4 gloo ranks: the
+    callable arm(key) hands to kv_switch_range_host is a barrier over the
+    key's members only (the pooled subgroups), None for a non-member."""
+    world = 4
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_hb_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    for r in range(world):
+        assert res[r]["ok"] and res[r]["outside"]
+        assert res[r]["held_s"] >= 0.25

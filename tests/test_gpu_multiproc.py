@@ -1,11 +1,18 @@
 """One process per GPU, peer pools mapped through CUDA IPC, each process's
 reshard kernel pushing its atoms into the other processes' pools (the N-GPU
-launch shape), then the device-side group barrier (kv_group_barrier over
-IPC-shared counters: no host barrier on the data path), then the remap.  A
-process may own several consecutive pools (virtual ranks, kv_reshard_range).
+launch shape), then the group barrier (a5), then the remap.  A process may
+own several consecutive pools (virtual ranks, kv_reshard_range).  Whole pools
+are compared with the oracle.
+
 On a 1-GPU box the processes share cuda:0 (CUDA IPC between processes on one
-device); gloo carries only the setup (handle exchange) and the test's file
-hand-off.  Whole pools are compared with the oracle."""
+device).  There the barrier is comm.HostBarrier (stream sync + gloo barrier;
+kv_switch_range_host for the one-call mode): the device barrier would be
+separate launches of different processes spinning on one another on one
+device, which nothing co-schedules.  With one GPU per process
+(FLYKV_TEST_DEVICE_OF_RANK=1, >= world GPUs) comm.make_barrier picks the
+device barrier (kv_group_barrier over IPC-shared counters).  The device
+barrier's code itself is checked on one GPU by test_device_barrier_* (its
+members emulated as the CTAs of one cooperative launch)."""
 import os
 import socket
 import tempfile
@@ -113,7 +120,7 @@ def _rank(rank, world, port, outdir, kind, mode="push", v=1):
         mcs = []
         if mode == "nvls":   # one multicast team per aligned replica group (N2)
             mcs.append(comm.setup_multicast_teams(cache, vmm, rank, world, world // w.H, w.L, M, nb[rank], dev))
-        barrier = comm.DeviceBarrier(rank, world, [tuple(range(world))], f"cuda:{dev}", timeout_s=60)
+        barrier = comm.make_barrier(rank, world, [tuple(range(world))], f"cuda:{dev}", timeout_s=60)
         for s_, ids in zip(w.src, tabs):
             cache.reserve(s_, ids)
         stream = torch.cuda.Stream(f"cuda:{dev}")
@@ -142,7 +149,7 @@ def _rank(rank, world, port, outdir, kind, mode="push", v=1):
             for gp in mine:
                 rp, ids, meta = plan.host_tables(gp)
                 out[gp] = (torch.as_tensor(rp), torch.as_tensor(ids), torch.as_tensor(meta))
-        else:   # a5 on the device: every process's pushes have landed before anyone remaps
+        else:   # a5: every process's pushes have landed before anyone remaps
             barrier.wait(tuple(range(world)), stream)
         for gp in (mine if mode != "onecall" else ()):
             n_res, n_ids = plan.resident(gp)
@@ -237,6 +244,43 @@ def test_ipc_push_matches_oracle(world, kind, mode, v):
             assert np.array_equal(np.load(os.path.join(td, f"rp{r}.npy")), rp)
             assert np.array_equal(np.load(os.path.join(td, f"ids{r}.npy")), ids)
             assert np.array_equal(np.load(os.path.join(td, f"meta{r}.npy")), meta)
+
+
+@pytest.mark.parametrize("n", [1, 2, 4, 8, 64])
+def test_device_barrier_emulated_members(n):
+    """a5's device barrier (the production arrive/wait code) with n members
+    emulated as the CTAs of one cooperative launch: 2000 rounds, each member
+    publishes a store before every barrier and checks every member's store
+    after it -- no member ever passes early, none times out."""
+    F = __import__("paper_2602_22593_b200.flykv", fromlist=["flykv"])
+    assert F.group_barrier_selftest(n, 2000) == (0, 0)
+
+
+def test_device_barrier_absent_member_times_out():
+    """A member that never arrives: the others end their wait after the
+    timeout (reported, not a hang)."""
+    F = __import__("paper_2602_22593_b200.flykv", fromlist=["flykv"])
+    err, tmo = F.group_barrier_selftest(4, 3, absent=2, timeout_ns=int(20e6))
+    assert (err, tmo) == (0, 3)
+
+
+def test_device_barrier_prearrived_launch():
+    """kv_group_barrier as launched in production (one single-thread kernel
+    on the stream), with the other members' arrivals already in the
+    counter, so the launch waits on no other kernel: it passes, adds its
+    own arrival to every member's counter, and a wrong target times out
+    into the status word."""
+    F = __import__("paper_2602_22593_b200.flykv", fromlist=["flykv"])
+    ctr = torch.zeros(3 * 16, dtype=torch.int64, device="cuda:0")
+    ctr[0] = 2   # members 1 and 2 have arrived at barrier 1 on member 0's counter
+    status = torch.zeros(1, dtype=torch.int32, device="cuda:0")
+    flags = [ctr[16 * m:].data_ptr() for m in range(3)]
+    F.kv_group_barrier(flags, 0, 3, int(5e9), status)
+    torch.cuda.synchronize()
+    assert ctr[0].item() == 3 and ctr[16].item() == 1 and ctr[32].item() == 1 and status.item() == 0
+    F.kv_group_barrier(flags, 1, 3, int(20e6), status)   # member 1 only has 2 of 3: times out
+    torch.cuda.synchronize()
+    assert status.item() == 1 and ctr[16].item() == 2
 
 
 def test_nvls_multicast_parity():

@@ -897,6 +897,12 @@ def test_strict_replica_mode():
     with pytest.raises(F.FlyKVError) as err:
         F.kv_switch(eng.cache, reqs, eng.stream)
     assert err.value.name == "KV_ERR_REPLICA_MISMATCH" and err.value.plans == []
+    called = []   # the one-process-per-GPU calls refuse it too, before the push and the barrier
+    for bar in (None, lambda: called.append(1)):
+        with pytest.raises(F.FlyKVError) as err:
+            F.kv_switch_range(eng.cache, reqs, 0, 8, bar, eng.stream)
+        assert err.value.name == "KV_ERR_REPLICA_MISMATCH" and err.value.plans == []
+    assert not called
     torch.cuda.synchronize()
     assert all(torch.equal(a, b) for a, b in zip(before, eng.pools.tensors))
     assert all(np.array_equal(eng.cache.held_mask(g), masks[g]) for g in range(8))
