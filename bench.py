@@ -4,18 +4,20 @@
 Metric (BASELINE.json): "DP<->TP KV re-layout GB/s (% HBM/NVLink roofline) +
 switch latency ms".  A *step* is one whole live switch of the workload: the
 host planner (validation, allocation, segment index, descriptor upload), the
-reshard kernel over every atom, and the per-GPU block-table remap kernels
-(a1-a7).  Steps alternate direction (DP4 -> TP2x2, then
-back), so every step moves the full payload with fresh allocations.
+reshard kernel over every atom, and the block-table remap (DESIGN.md section
+1, a1-a7).  Steps alternate direction (DP -> TP, then back), so every step
+moves the full payload with fresh allocations.
 
-N=1 (default): BASELINE configs[1] (Llama-3.1-8B-shaped cache, 64 requests,
-DP4 -> TP2x2) with the 4 engines as virtual ranks (4 pools) on one B200; the
-bound is HBM (read + write of every byte).  N>1 (torchrun, one process per
-GPU, every GPU pushing its atoms into peer pools over NVLink, IPC-mapped,
-bound by NVLink per-direction bandwidth): N=4 runs configs[1] as stated
-(DP4 -> TP2x2 on 4 GPUs), N=8 the headline configs[3] (Llama-3-70B
-8 x DP1 -> TP8), N=2 a DP2 -> TP2 merge of the configs[1] geometry with the
-same ~4.9 GB per GPU ("weak" scaling: per-GPU bytes roughly fixed).
+N=1 (default): the north_star headline, BASELINE configs[3] (Llama-3-70B-
+shaped cache, 64 requests, 8 x DP1 -> TP8) with the 8 engines as virtual
+ranks (8 pools) on one B200; the bound is HBM (read + write of every byte).
+--config picks another workload (synth.WORKLOADS).  N>1: `bench.py --gpus N`
+outside torchrun launches N ranks itself (one process per GPU); the same
+switch runs with its engines mapped onto the N GPUs as blocks of 8/N virtual
+ranks ("strong" scaling), every GPU pushing its atoms into peer pools over
+NVLink (IPC-mapped), then the group barrier (device-side kv_group_barrier;
+the host barrier when FLYKV_SAME_DEVICE=1 puts every rank on cuda:0, a
+correctness mode, not an NVLink number).
 
 `value`  = payload bytes of the K timed steps / device time (CUDA events on
            the switch stream; max over ranks), pools resident in HBM.
