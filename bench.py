@@ -89,6 +89,10 @@ def parse():
     ap.add_argument("--profile-steps", type=int, default=0, help="(ncu) run N steps only, no JSON")
     ap.add_argument("--no-fill", action="store_true", help="skip the content hash fill (profiling runs)")
     ap.add_argument("--requests", type=int, default=0, help="use only the first N requests (profiling)")
+    ap.add_argument("--decode", action="store_true",
+                    help="N3 consumer: time kv_paged_decode over every layer of every pool after the forward "
+                         "switch (and on the DP layout before it); its own JSON line")
+    ap.add_argument("--q-heads", type=int, default=64, help="--decode: query heads of the model (Llama-3-70B: 64)")
     return ap.parse_args()
 
 
@@ -1186,6 +1190,139 @@ def run_multi(args):
     return 0
 
 
+def run_decode(args):
+    """N3 consumer measurement: paged decode attention (kv_paged_decode) reads
+    the cache through the tables the remap produced.  One *pass* = one decode
+    step of every resident request on every pool, every layer (L x pools
+    launches, one per (pool, layer) as a model's attention layers would issue
+    them).  Timed on the DP layout (before the switch) and on the TP layout
+    (after the forward switch): algorithmic bytes = every K/V byte of every
+    resident (request, local KV head) once, plus q and out; HBM-bound."""
+    import torch
+
+    from paper_2602_22593_b200 import flykv as F
+    from paper_2602_22593_b200.engine import KVSwitchEngine
+
+    dev = torch.device("cuda:0")
+    torch.cuda.set_device(dev)
+    w = build_workload(args, 1, 0)
+    g = F.geometry(w.L, w.H, w.d, w.B, w.e)
+    nb, tabs = pools_and_tables(w, args.frag, args.pool_slack, args.placement == "contiguous")
+    eng = KVSwitchEngine(g, nb, dev, tp_degrees=(2, 4, 8))
+    eng.cache.set_work_order(0)
+    for i, t in enumerate(eng.pools.tensors):   # finite bf16 contents: hash bytes with exponent bit 7 cleared
+        synth.fill_hash_torch(t, i)
+        t.view(torch.int16).bitwise_and_(-16385)
+    for s_, ids in zip(w.src, tabs):
+        eng.cache.reserve(s_, ids)
+    hbm, hbm_src = peaks()
+    stream = torch.cuda.Stream(dev)   # decode stream (graph capture needs a non-default stream)
+    Hq = args.q_heads
+    scale = 1.0 / float(np.sqrt(w.d))
+    gen = torch.Generator(device=dev).manual_seed(5)
+
+    def prepare(plan, views, host, req_of_layout):
+        """Per pool: (pool, table views, seq_lens, q, out, q_local, algorithmic bytes per layer)."""
+        items = []
+        for gp in range(w.n_gpus):
+            n_res, _ = plan.resident(gp)
+            if n_res == 0:
+                continue
+            meta = host[gp][2].numpy()
+            deg = req_of_layout(int(meta[0, 0]))   # every request of a pool has one degree here
+            q_local = Hq // deg
+            lens = torch.as_tensor([w.T[int(i)] for i in meta[:, 0]], dtype=torch.int32, device=dev)
+            q = torch.randn((n_res, q_local, w.d), generator=gen, device=dev).to(torch.bfloat16)
+            out = torch.empty((n_res, q_local, w.d), dtype=torch.float32, device=dev)
+            kv = sum(int(w.T[int(i)]) * int(meta[k, 2]) for k, i in enumerate(meta[:, 0])) * 2 * w.d * w.e
+            items.append((gp, views[gp], lens, q, out, q_local, kv + q.numel() * 2 + out.numel() * 4))
+        return items
+
+    def one_pass(items):
+        for gp, t, lens, q, out, q_local, _ in items:
+            base = eng.pools.tensors[gp]
+            for l in range(w.L):
+                F.kv_paged_decode(g, base[l].data_ptr(), t.meta.shape[0], t.req_ptr, t.block_ids, t.meta, lens,
+                                  q_local, q, out, scale, max(w.T), stream)
+
+    def timed(items):
+        """One pass captured in a CUDA graph (the 80-layer decode step is
+        launch-bound from Python: 640 launches), replayed `steps` times
+        between CUDA events; plus the same passes launched eagerly."""
+        for _ in range(max(args.warmup, 3)):   # warm-up also sizes the decode workspace (no allocation in capture)
+            one_pass(items)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            one_pass(items)
+        torch.cuda.synchronize()
+        for _ in range(max(args.warmup, 3)):
+            graph.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        clk.begin()
+        n0 = F.launch_count()
+        e0.record(stream)
+        with torch.cuda.stream(stream):
+            for _ in range(args.steps):
+                graph.replay()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        clk.end()
+        ms = e0.elapsed_time(e1) / args.steps
+        n_launch = (len(items) * w.L) * args.steps   # kernels inside the replayed graph (none launched by the host)
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.steps):
+            one_pass(items)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        eager_ms = f0.elapsed_time(f1) / args.steps
+        nbytes = sum(it[6] for it in items) * w.L
+        del graph
+        return ms, nbytes, n_launch, eager_ms
+
+    clk = ClockSampler(0, args.clock_ms).start()
+    # DP layout: a no-op plan lists every request in its DP engine's table
+    noop = [(i, T, s_, ids, s_) for i, (T, s_, ids) in enumerate(zip(w.T, w.src, tabs))]
+    plan0, views0, host0 = eng.switch(noop, read_back=True)
+    torch.cuda.synchronize()
+    dp_items = prepare(plan0, views0, host0, lambda i: w.src[i][1])
+    dp_ms, dp_bytes, dp_launch, dp_eager = timed(dp_items)
+    # forward switch, then the TP layout
+    move = [(i, T, s_, ids_, d_) for i, (T, s_, ids_, d_) in enumerate(zip(w.T, w.src, tabs, w.dst))]
+    plan1, views1, host1 = eng.switch(move, read_back=True)
+    torch.cuda.synchronize()
+    tp_items = prepare(plan1, views1, host1, lambda i: w.dst[i][1])
+    tp_ms, tp_bytes, tp_launch, tp_eager = timed(tp_items)
+    clk.stop()
+    gbs = tp_bytes / tp_ms / 1e6
+    line = {
+        "metric": "paged decode attention GB/s (N3 consumer of the re-laid-out cache)",
+        "value": round(gbs, 1), "unit": "GB/s", "n_gpus": 1, "steps": args.steps, "warmup": max(args.warmup, 3),
+        "ms_per_step": round(tp_ms, 4), "higher_is_better": True, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": w.name + " after the forward switch", "layers": w.L, "kv_heads": w.H,
+                   "q_heads": Hq, "head_dim": w.d, "requests": len(w.T), "tokens": w.tokens(),
+                   "step": f"one decode step: kv_paged_decode for every (pool, layer), {tp_launch // args.steps} "
+                           "launches, captured once in a CUDA graph and replayed",
+                   "l2": "inputs larger than L2 (KV bytes per pass >> 126 MB), no flush needed"},
+        "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm, "unit": "GB/s",
+                     "frac": round(gbs / hbm, 4), "traffic": None, "peak_source": hbm_src,
+                     "kernel": "flykv_paged_decode_kernel", "algorithmic_bytes_per_step": int(tp_bytes),
+                     "algorithmic_bytes": "every K/V byte of every resident (request, local KV head) + q + out"},
+        "eager_ms_per_step": round(tp_eager, 4),
+        "eager_note": "the same step launched from Python (640 ctypes calls): host-bound, context only",
+        "dp_layout": {"ms_per_step": round(dp_ms, 4), "GBps": round(dp_bytes / dp_ms / 1e6, 1),
+                      "eager_ms_per_step": round(dp_eager, 4),
+                      "frac": round(dp_bytes / dp_ms / 1e6 / hbm, 4), "bytes_per_step": int(dp_bytes),
+                      "launches_per_step": dp_launch // args.steps},
+        "gpu_launches": tp_launch,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line))
+    return 0
+
+
 def self_launch(args) -> int:
     """bench.py --gpus N (N > 1) outside torchrun: re-run this script under
     torch.distributed.run with N local ranks (127.0.0.1 rendezvous)."""
@@ -1208,6 +1345,8 @@ def main():
         return self_launch(args)
     if args.impl == "reference":
         return run_reference(args)
+    if args.decode:
+        return run_decode(args)
     if world > 1:
         return run_multi(args)
     return run_single(args)

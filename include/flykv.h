@@ -594,16 +594,28 @@ kv_status kv_gather_view(const kv_view* view, void* dst, void* stream);
  * kv_remap_block_tables (req_ptr, block_ids) and per_req_meta {index, B(p),
  * H_loc(p), first KV head}.  Local query head j uses local KV head
  * j / (q_heads_local / H_loc) (GQA).  out[r][j] = softmax(scale * q.K^T) V
- * over tokens 0..seq_lens[r]-1, fp32 online softmax in token order (so a TP
- * rank and the DP replica produce identical bits for the same head).
- *   layer_base  device, layer l region of the pool
- *   q           device bf16 [n_res][q_heads_local][head_dim]
+ * over tokens 0..seq_lens[r]-1 (zeros for seq_lens[r] = 0).  Tensor-core
+ * flash decoding (mma.sync m16n8k16, bf16 in, fp32 accumulate, P as bf16
+ * hi + lo), tiles of 16 tokens and splits of 512 tokens fixed in token
+ * index, folded in a fixed order: a TP rank and the DP replica produce
+ * identical bits for the same head.  HBM-bound: reads every K/V byte of the
+ * resident requests once.
+ *   layer_base  device, layer l region of the pool (16-byte aligned)
+ *   block_ids   device; may be NULL when no resident request has a token
+ *   q_heads_local  a multiple of every resident request's H_loc
+ *   q           device bf16 [n_res][q_heads_local][head_dim] (16-byte aligned)
  *   out         device fp32 [n_res][q_heads_local][head_dim]
- * bf16 and head_dim 64/128/256 only (INVALID_ARG otherwise).
+ *   max_seq_len host: >= every seq_lens entry; sizes the split workspace the
+ *               library keeps per (device, stream) (a larger entry traps:
+ *               a CUDA error, never a stray write)
+ * Calls on one stream share that workspace (ordered); calls on different
+ * streams use different ones.  bf16 and head_dim 64/128/256 only
+ * (INVALID_ARG otherwise); KV_ERR_CUDA on workspace allocation or launch.
  */
 kv_status kv_paged_decode(const kv_geometry* geom, const void* layer_base, int32_t n_res, const int32_t* req_ptr,
                           const int32_t* block_ids, const int32_t* per_req_meta, const int32_t* seq_lens,
-                          int32_t q_heads_local, const void* q, float* out, float scale, void* stream);
+                          int32_t q_heads_local, const void* q, float* out, float scale, int32_t max_seq_len,
+                          void* stream);
 
 /* ------------------------------------------------------- multi-process */
 

@@ -42,7 +42,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     os.makedirs(os.path.dirname(LIB), exist_ok=True)
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [nvcc(), *NVCC_FLAGS, "-shared", "-I", INCLUDE, "-I", CSRC, *SOURCES, "-o", tmp]
+    extra = os.environ.get("FLYKV_NVCC_EXTRA", "").split()   # experiment knobs (-D...), never set by build()
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-shared", "-I", INCLUDE, "-I", CSRC, *SOURCES, "-o", tmp]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

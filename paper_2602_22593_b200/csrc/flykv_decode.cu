@@ -3,78 +3,618 @@
 // Adaptor hands to the attention kernel: the CSR block table of
 // kv_remap_block_tables and, per request, B(p), H_loc(p) and the first KV head.
 //
-// One warp per (resident request, local query head).  Lanes hold d/32
-// contiguous elements of q, k, v; tokens are visited in order 0..T-1 with an
-// fp32 online softmax, and the dot product is reduced by a fixed xor-shuffle
-// tree.  The arithmetic therefore depends only on token order, never on the
-// block size: a TP rank reading the re-laid-out cache produces bit-for-bit
-// the output the DP replica produces for the same heads, which is what the
-// test checks.  (A consumer proof, not a tuned attention kernel: the decode
-// GEMV is HBM-bound and not on the switch's hot path.)
+// Decode attention is HBM-bound: every K/V byte of the resident requests is
+// read once per call, and the arithmetic per byte is small.  The contraction
+// is GQA-shaped -- the G query heads that share one KV head against 16-token
+// tiles of that head -- so it runs on the tensor cores with mma.sync
+// m16n8k16 (bf16 in, fp32 accumulate): S^T = K Q^T (M = 16 tokens, N = 8
+// query heads, K = head_dim) and O^T += V^T P^T (M = 16 head_dim rows, N = 8
+// heads, K = 16 tokens).  tcgen05's smallest tiles (M = 64/128) would idle on
+// an N = 8 problem that is bound by HBM, not by the tensor cores.
+//   * Operands come straight from global memory into MMA fragments: the
+//     head_dim index of the K and Q^T fragments is permuted so that each
+//     thread loads whole 16-byte chunks (coalesced), V is loaded token-row
+//     wise and its pairs re-packed along tokens with PRMT; P moves from the
+//     S^T accumulator layout to the B-operand layout with movmatrix.trans.
+//   * P enters the second MMA as bf16 hi + lo parts (two MMAs), so O keeps
+//     ~16 mantissa bits of P.
+//   * Flash-decoding: a unit = (request, local KV head, tile of 8 query
+//     heads, split of 512 tokens); the 4 warps of a CTA take the split's
+//     16-token tiles round-robin, fold their online-softmax states in shared
+//     memory in warp order, and a request with several splits is finished by
+//     the CTA that completes its last split (per-item arrival counter), which
+//     folds the splits in split order.
+//   * Determinism across layouts: every assignment above is a function of
+//     token indices only (tiles, splits), never of B(p) or the block
+//     table, and each query head's arithmetic does not depend on the other
+//     heads in its tile.  A TP rank reading the re-laid-out cache therefore
+//     produces bit for bit the output the DP replica produces for the same
+//     heads -- which is what tests/test_gpu_consumer.py checks.
+//   * Persistent grid (3 CTAs of 4 warps per SM, <= 168 registers): CTAs
+//     draw units from an arrival counter (the next one while the current one
+//     runs); units are enumerated on the device from seq_lens and the
+//     per-request meta (chunked block scans), so the host needs only an upper
+//     bound of the sequence lengths.  The workspace counters return to zero
+//     at the end of every launch.
+//   * Measured (bench.py --decode): about a third of
+//     the HBM roofline per (pool, layer) launch of 77 MB.  A launch is only
+//     ~12 us of transfer at peak; the per-unit chains of dependent loads
+//     (unit -> request -> block table -> tile), a load-then-compute tile loop
+//     and the folds leave HBM idle for much of it.  Launch shapes, split
+//     sizes and tile pairing are compile-time knobs (FLYKV_DEC_*) for sweeps.
 #include <cuda_bf16.h>
 
 #include "flykv_internal.h"
 
 namespace flykv {
 
-template <int EPL>  // bf16 elements per lane = d / 32
-__global__ void __launch_bounds__(128) flykv_paged_decode_kernel(const DecodeArgs a) {
-    const int lane = threadIdx.x & 31;
-    const int64_t item = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (item >= (int64_t)a.n_res * a.q_local) return;
-    const int r = (int)(item / a.q_local);
-    const int j = (int)(item % a.q_local);
-    const int32_t Bp = a.meta[4 * r + 1];
-    const int32_t hloc = a.meta[4 * r + 2];
-    const int32_t hl = j / (a.q_local / hloc);  // local KV head serving local query head j
-    const int32_t T = a.seq_lens[r];
-    const int32_t* tab = a.block_ids + a.req_ptr[r];
-    const int64_t row = (int64_t)a.d * 2;       // bytes of one token of one head (bf16)
-    const int64_t half = a.M >> 1;
+namespace {
 
-    float q[EPL], acc[EPL];
-    const __nv_bfloat16* qp = a.q + ((int64_t)r * a.q_local + j) * a.d + lane * EPL;
-#pragma unroll
-    for (int e = 0; e < EPL; ++e) {
-        q[e] = __bfloat162float(qp[e]);
-        acc[e] = 0.f;
-    }
-    float m = -INFINITY, l = 0.f;
-    for (int32_t t = 0; t < T; ++t) {
-        const int64_t off = (int64_t)tab[t / Bp] * a.M + ((int64_t)hl * Bp + t % Bp) * row + lane * EPL * 2;
-        const __nv_bfloat16* kp = reinterpret_cast<const __nv_bfloat16*>(a.layer + off);
-        const __nv_bfloat16* vp = reinterpret_cast<const __nv_bfloat16*>(a.layer + off + half);
-        float dot = 0.f;
-#pragma unroll
-        for (int e = 0; e < EPL; ++e) dot = fmaf(q[e], __bfloat162float(kp[e]), dot);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-        const float s = dot * a.scale;
-        const float m_new = fmaxf(m, s);
-        const float corr = __expf(m - m_new);
-        const float p = __expf(s - m_new);
-        l = l * corr + p;
-#pragma unroll
-        for (int e = 0; e < EPL; ++e) acc[e] = fmaf(p, __bfloat162float(vp[e]), acc[e] * corr);
-        m = m_new;
-    }
-    float* op = a.out + ((int64_t)r * a.q_local + j) * a.d + lane * EPL;
-    const float inv = T > 0 ? 1.f / l : 0.f;
-#pragma unroll
-    for (int e = 0; e < EPL; ++e) op[e] = acc[e] * inv;
+constexpr int kTile = 16;                 // tokens per MMA tile
+#ifndef FLYKV_DEC_SPLIT
+#define FLYKV_DEC_SPLIT 512
+#endif
+constexpr int kSplit = FLYKV_DEC_SPLIT;   // tokens per unit
+#ifndef FLYKV_DEC_WARPS
+#define FLYKV_DEC_WARPS 4
+#endif
+#ifndef FLYKV_DEC_CTAS
+#define FLYKV_DEC_CTAS 3
+#endif
+#ifndef FLYKV_DEC_KPREF
+#define FLYKV_DEC_KPREF 0
+#endif
+#ifndef FLYKV_DEC_PAIR
+#define FLYKV_DEC_PAIR 0
+#endif
+constexpr int kWarps = FLYKV_DEC_WARPS;   // warps per CTA
+constexpr int kCtasPerSm = FLYKV_DEC_CTAS;  // resident CTAs per SM (launch bounds cap the registers)
+constexpr int kTilesPerWarp = kSplit / 16 / kWarps;
+static_assert(kTilesPerWarp >= 1 && kTilesPerWarp <= 32, "split / warps");
+constexpr int kTilesPerSplit = kSplit / kTile;
+constexpr int kFoldChunk = 8;             // splits folded per step by the last-arriving CTA
+
+#ifdef FLYKV_DEC_TRACE
+// debug: per unit, %globaltimer at phase boundaries (unit taken, geometry read, tiles done, fold done,
+// end) and the SM id; read back with kv_debug_decode_trace
+__device__ unsigned long long g_dec_trace[8192][8];
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define DEC_TRACE(u, k)                                                       \
+    do {                                                                      \
+        if (threadIdx.x == 0 && (u) < 8192) g_dec_trace[(u)][(k)] = gtime(); \
+    } while (0)
+#else
+#define DEC_TRACE(u, k) \
+    do {                \
+    } while (0)
+#endif
+
+__device__ __forceinline__ uint4 ldg128(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
 }
 
-cudaError_t launch_decode(const DecodeArgs& a, cudaStream_t s) {
-    const int64_t warps = (int64_t)a.n_res * a.q_local;
-    if (warps == 0) return cudaSuccess;
-    const int grid = (int)((warps + 3) / 4);
+__device__ __forceinline__ void mma_bf16(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                         uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ uint32_t movtrans(uint32_t a) {
+    uint32_t d;
+    asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(d) : "r"(a));
+    return d;
+}
+
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+    uint32_t d;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+    return d;
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&v);
+}
+
+__device__ __forceinline__ float bf16_lo(uint32_t v) { return __uint_as_float(v << 16); }
+__device__ __forceinline__ float bf16_hi(uint32_t v) { return __uint_as_float(v & 0xffff0000u); }
+
+// Units of request r: H_loc KV heads x ceil(G/8) head tiles x splits (one
+// unit for T = 0, which writes zeros).
+__device__ __forceinline__ int units_of(const DecodeArgs& a, int r) {
+    const int32_t T = a.seq_lens[r];
+    const int32_t hloc = a.meta[4 * r + 2];
+    const int32_t G = a.q_local / hloc;
+    const int32_t nt = (G + 7) / 8;
+    const int32_t s = T > 0 ? (T + kSplit - 1) / kSplit : 1;
+    return hloc * nt * s;
+}
+
+// One warp's online-softmax state for its 8 head columns.
+template <int D>
+struct WarpState {
+    float m0, m1, l0, l1;     // heads 2tig, 2tig+1 (m uniform across the 8 row groups; l partial per lane)
+    float o[D / 16][4];       // O^T fragments, m-tile mi: {(d0, 2tig), (d0, 2tig+1), (d0+1, 2tig), (d0+1, 2tig+1)}
+};
+
+// One 16-token tile's operands: K rows g and g+8 (chunks tig + 4j), V rows
+// 2tig, 2tig+1, 2tig+8, 2tig+9 (chunks g + 8h).
+template <int D>
+struct TileRegs {
+    uint4 k[D / 32][2];
+    uint4 v[4][D / 64];
+};
+
+// blk >= 0: the tile's 16 rows lie in block blk (B(p) a multiple of 16; the
+// warp's block IDs were fetched up front), rows from t0 % B(p) on.  blk < 0:
+// every row looks its block up (any B(p)).  Rows past T re-read row T-1
+// (masked in tile_step; never stale bytes).
+template <int D, bool LK = true, bool LV = true>
+__device__ __forceinline__ void load_tile(const DecodeArgs& a, const int32_t* tab, int32_t Bp, int32_t hl, int t0,
+                                          int T, int g, int tig, int32_t blk, TileRegs<D>& tr) {
+    const int64_t rowb = (int64_t)D * 2;
+    const int64_t half = a.M >> 1;
+    const int last = T - 1 - t0;  // rows 0..last of the tile are valid
+    const char* base = nullptr;
+    if (blk >= 0) base = a.layer + (int64_t)blk * a.M + ((int64_t)hl * Bp + t0 % Bp) * rowb;
+    auto row_ptr = [&](int x) -> const char* {
+        const int xx = x <= last ? x : last;
+        if (blk >= 0) return base + xx * rowb;
+        const int t = t0 + xx;
+        return a.layer + (int64_t)__ldg(tab + t / Bp) * a.M + ((int64_t)hl * Bp + t % Bp) * rowb;
+    };
+    if constexpr (LK) {
+        const char* k0 = row_ptr(g);
+        const char* k1 = row_ptr(g + 8);
+#pragma unroll
+        for (int j = 0; j < D / 32; ++j) {
+            tr.k[j][0] = ldg128(k0 + (tig + 4 * j) * 16);
+            tr.k[j][1] = ldg128(k1 + (tig + 4 * j) * 16);
+        }
+    }
+    if constexpr (LV) {
+        const int tv[4] = {2 * tig, 2 * tig + 1, 2 * tig + 8, 2 * tig + 9};
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+            const char* vr = row_ptr(tv[x]) + half;
+#pragma unroll
+            for (int h = 0; h < D / 64; ++h) tr.v[x][h] = ldg128(vr + (g + 8 * h) * 16);
+        }
+    }
+}
+
+__device__ __forceinline__ uint32_t word(const uint4& v, int w) {
+    return w == 0 ? v.x : w == 1 ? v.y : w == 2 ? v.z : v.w;
+}
+
+// NTL (1 or 2) 16-token tiles with ONE online-softmax update: S^T of each
+// tile on the tensor cores, the running max over all NTL*16 tokens, then
+// O^T += V^T P^T per tile.  The tile grouping is fixed by token index.
+template <int D, int NTL>
+__device__ __forceinline__ void tiles_step(const TileRegs<D> (&tr)[NTL], const uint32_t (&qb)[D / 16][2],
+                                           const int (&t0)[NTL], int T, int g, float sl, WarpState<D>& st) {
+    float sv[NTL][4];
+#pragma unroll
+    for (int x = 0; x < NTL; ++x) {
+        // S^T = K Q^T over D/16 k-steps; k-step (j, u) uses words 2u, 2u+1 of chunk j;
+        // two independent accumulator chains (u = 0 / 1), summed
+        float sa[4] = {0.f, 0.f, 0.f, 0.f}, sb[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int j = 0; j < D / 32; ++j) {
+            mma_bf16(sa, word(tr[x].k[j][0], 0), word(tr[x].k[j][1], 0), word(tr[x].k[j][0], 1),
+                     word(tr[x].k[j][1], 1), qb[2 * j][0], qb[2 * j][1]);
+            mma_bf16(sb, word(tr[x].k[j][0], 2), word(tr[x].k[j][1], 2), word(tr[x].k[j][0], 3),
+                     word(tr[x].k[j][1], 3), qb[2 * j + 1][0], qb[2 * j + 1][1]);
+        }
+        const bool ok0 = t0[x] + g < T, ok1 = t0[x] + g + 8 < T;
+        sv[x][0] = ok0 ? (sa[0] + sb[0]) * sl : -INFINITY;   // (token g, head 2tig)
+        sv[x][1] = ok0 ? (sa[1] + sb[1]) * sl : -INFINITY;   // (token g, head 2tig+1)
+        sv[x][2] = ok1 ? (sa[2] + sb[2]) * sl : -INFINITY;   // (token g+8, head 2tig)
+        sv[x][3] = ok1 ? (sa[3] + sb[3]) * sl : -INFINITY;   // (token g+8, head 2tig+1)
+    }
+    float mx0 = fmaxf(sv[0][0], sv[0][2]), mx1 = fmaxf(sv[0][1], sv[0][3]);
+#pragma unroll
+    for (int x = 1; x < NTL; ++x) {
+        mx0 = fmaxf(mx0, fmaxf(sv[x][0], sv[x][2]));
+        mx1 = fmaxf(mx1, fmaxf(sv[x][1], sv[x][3]));
+    }
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
+    }
+    const float mn0 = fmaxf(st.m0, mx0), mn1 = fmaxf(st.m1, mx1);
+    const float c0 = exp2f(st.m0 - mn0), c1 = exp2f(st.m1 - mn1);
+    st.m0 = mn0;
+    st.m1 = mn1;
+    float ps[NTL][4];
+    float add0 = 0.f, add1 = 0.f;
+#pragma unroll
+    for (int x = 0; x < NTL; ++x) {
+        ps[x][0] = exp2f(sv[x][0] - mn0);
+        ps[x][1] = exp2f(sv[x][1] - mn1);
+        ps[x][2] = exp2f(sv[x][2] - mn0);
+        ps[x][3] = exp2f(sv[x][3] - mn1);
+        add0 += ps[x][0] + ps[x][2];
+        add1 += ps[x][1] + ps[x][3];
+    }
+    st.l0 = st.l0 * c0 + add0;
+    st.l1 = st.l1 * c1 + add1;
+    if (!__all_sync(0xffffffffu, c0 == 1.f && c1 == 1.f)) {  // x 1.0 is the identity: skipping it is exact
+#pragma unroll
+        for (int mi = 0; mi < D / 16; ++mi) {
+            st.o[mi][0] *= c0;
+            st.o[mi][1] *= c1;
+            st.o[mi][2] *= c0;
+            st.o[mi][3] *= c1;
+        }
+    }
+#pragma unroll
+    for (int x = 0; x < NTL; ++x) {
+        // P^T as the B operand (k = tokens, n = heads): hi and lo bf16 parts,
+        // tokens 0-7 and 8-15 transposed from the accumulator layout
+        const uint32_t h01 = pack_bf16(ps[x][0], ps[x][1]), h23 = pack_bf16(ps[x][2], ps[x][3]);
+        const uint32_t l01 = pack_bf16(ps[x][0] - bf16_lo(h01), ps[x][1] - bf16_hi(h01));
+        const uint32_t l23 = pack_bf16(ps[x][2] - bf16_lo(h23), ps[x][3] - bf16_hi(h23));
+        const uint32_t bh0 = movtrans(h01), bh1 = movtrans(h23), bl0 = movtrans(l01), bl1 = movtrans(l23);
+        // O^T += V^T P^T: m-tile mi rows g / g+8 = words mi%4 of chunk mi/4, lo / hi halves
+#pragma unroll
+        for (int mi = 0; mi < D / 16; ++mi) {
+            const int h = mi / 4, w = mi % 4;
+            const uint32_t va = word(tr[x].v[0][h], w), vb = word(tr[x].v[1][h], w);
+            const uint32_t vc = word(tr[x].v[2][h], w), vd = word(tr[x].v[3][h], w);
+            const uint32_t a0 = prmt(va, vb, 0x5410), a1 = prmt(va, vb, 0x7632);
+            const uint32_t a2 = prmt(vc, vd, 0x5410), a3 = prmt(vc, vd, 0x7632);
+            mma_bf16(st.o[mi], a0, a1, a2, a3, bh0, bh1);
+            mma_bf16(st.o[mi], a0, a1, a2, a3, bl0, bl1);
+        }
+    }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kWarps * 32, D == 256 ? 2 : kCtasPerSm) flykv_paged_decode_kernel(const DecodeArgs a) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int g = lane >> 2, tig = lane & 3;
+    // per-warp states for the CTA fold; chunked request scan
+    __shared__ float sm_o[kWarps][8][D];
+    __shared__ float sm_m[kWarps][8], sm_l[kWarps][8], sm_f[kWarps][8], sm_M[8], sm_L[8], sm_r[8];
+    __shared__ float sm_g[kFoldChunk][8], sm_pm[kFoldChunk][8], sm_pl[kFoldChunk][8];
+    __shared__ int sc_incl[kWarps * 32], sc_wtot[kWarps];
+    __shared__ int sc_tot;
+    __shared__ int sh_last, sh_unit;
+    const float sl = a.scale * 1.4426950408889634f;  // scores in log2 units (exp2)
+
+    int chunk_r = -kWarps * 32;  // first request of the scanned chunk
+    long long chunk_u = 0;       // units before it
+    int chunk_n = 0;             // units in it
+    // units are taken from an arrival counter (dynamic balance; the results do not depend on which CTA
+    // computes what); the last CTA to run out of units resets the counters for the next call
+    // the next unit is drawn while the current one runs (its atomic latency hidden)
+    if (tid == 0) sh_unit = atomicAdd(a.counters + a.n_units_cap, 1);
+    int next_u = 0;
+    while (true) {
+        __syncthreads();  // sh_unit is set; the previous iteration's readers are done
+        const long long u = sh_unit;
+        if (tid == 0) next_u = atomicAdd(a.counters + a.n_units_cap, 1);
+        __syncthreads();  // every thread has read sh_unit (the atomic above does not block here)
+        // next_u is published for the next iteration after this unit's tiles: the atomic's latency
+        // overlaps the geometry and tile loads
+        DEC_TRACE(u, 0);
+        // ---- find the unit's request: walk chunks of 128 requests forward
+        bool done = false;
+        while (u >= chunk_u + chunk_n) {
+            chunk_u += chunk_n;
+            chunk_r += kWarps * 32;
+            if (chunk_r >= a.n_res) {
+                done = true;
+                break;
+            }
+            __syncthreads();  // every thread is done reading the previous chunk's scan
+            const int r = chunk_r + tid;
+            int x = r < a.n_res ? units_of(a, r) : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            if (lane == 31) sc_wtot[wid] = x;
+            __syncthreads();
+            int before = 0;
+            for (int w = 0; w < wid; ++w) before += sc_wtot[w];
+            sc_incl[tid] = before + x;
+            if (tid == kWarps * 32 - 1) sc_tot = before + x;
+            __syncthreads();
+            chunk_n = sc_tot;
+        }
+        if (done) {
+            if (tid == 0 && atomicAdd(a.counters + a.n_units_cap + 1, 1) == (int)gridDim.x - 1) {
+                a.counters[a.n_units_cap] = 0;
+                a.counters[a.n_units_cap + 1] = 0;
+            }
+            return;
+        }
+        // request index: first slot whose inclusive count exceeds u - chunk_u
+        const int uu = (int)(u - chunk_u);
+        int lo = 0, hi = kWarps * 32 - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (sc_incl[mid] > uu) hi = mid;
+            else lo = mid + 1;
+        }
+        const int r = chunk_r + lo;
+        const int before = lo > 0 ? sc_incl[lo - 1] : 0;
+        int local = uu - before;
+        // ---- unit geometry
+        const int32_t T = a.seq_lens[r];
+        if (T > a.max_seq) __trap();  // the workspace was sized for max_seq_len (a loud error, never a stray write)
+        const int32_t Bp = a.meta[4 * r + 1];
+        const int32_t hloc = a.meta[4 * r + 2];
+        const int32_t G = a.q_local / hloc;
+        const int32_t NT = (G + 7) / 8;
+        const int32_t S = T > 0 ? (T + kSplit - 1) / kSplit : 1;
+        const int32_t s = local % S;
+        local /= S;
+        const int32_t nt = local % NT;
+        const int32_t hl = local / NT;
+        const int32_t nh = min(8, G - 8 * nt);      // heads in this tile
+        const int32_t qh0 = hl * G + 8 * nt;         // first local query head of the tile
+        const int32_t* tab = a.block_ids + a.req_ptr[r];
+        DEC_TRACE(u, 1);
+        float* outp = a.out + ((int64_t)r * a.q_local + qh0) * D;
+        if (T == 0) {
+            for (int i = tid; i < nh * D; i += blockDim.x) outp[i] = 0.f;
+            if (tid == 0) sh_unit = next_u;
+            continue;
+        }
+        // ---- Q^T fragments of the tile's heads (zero for padding heads)
+        uint32_t qb[D / 16][2];
+        {
+            const bool hv = g < nh;
+            const char* qrow = reinterpret_cast<const char*>(a.q + ((int64_t)r * a.q_local + qh0 + (hv ? g : 0)) * D);
+#pragma unroll
+            for (int j = 0; j < D / 32; ++j) {
+                uint4 c = hv ? *reinterpret_cast<const uint4*>(qrow + (tig + 4 * j) * 16) : make_uint4(0, 0, 0, 0);
+                qb[2 * j][0] = c.x;
+                qb[2 * j][1] = c.y;
+                qb[2 * j + 1][0] = c.z;
+                qb[2 * j + 1][1] = c.w;
+            }
+        }
+        // ---- the warp's tiles of this split: 32s + wid, +4, ...
+        WarpState<D> st;
+        st.m0 = st.m1 = -INFINITY;
+        st.l0 = st.l1 = 0.f;
+#pragma unroll
+        for (int mi = 0; mi < D / 16; ++mi) st.o[mi][0] = st.o[mi][1] = st.o[mi][2] = st.o[mi][3] = 0.f;
+        const int n_tiles = (T + kTile - 1) / kTile;
+        const int i_end = min(n_tiles, (s + 1) * kTilesPerSplit);
+        const int i0 = s * kTilesPerSplit + wid;   // the warp's tiles: i0 + kWarps * k
+        // B(p) % 16 == 0: each tile lies in one block; lane k holds the block of the warp's k-th tile
+        const bool fast = (Bp % kTile) == 0;
+        int32_t myblk = -1;
+        if (fast && lane < kTilesPerWarp) {
+            const int ik = i0 + kWarps * lane;
+            if (ik < i_end) myblk = __ldg(tab + (ik * kTile) / Bp);
+        }
+        auto blk_of = [&](int k) { return fast ? __shfl_sync(0xffffffffu, myblk, k) : -1; };
+        // tiles in pairs (k, k+1) with one softmax update per pair; an odd last tile alone
+        // (head_dim 256: one tile per update, the registers hold one tile)
+        constexpr int kStep = (D <= 128 && FLYKV_DEC_PAIR) ? 2 : 1;
+        TileRegs<D> kreg[1], knext;   // FLYKV_DEC_KPREF: current tile (K then V), next tile's K
+        for (int k = 0; i0 + kWarps * k < i_end; k += kStep) {
+            const int ia = i0 + kWarps * k, ib = ia + kWarps;
+            if (kStep == 2 && ib < i_end) {
+                TileRegs<D> tr[2];
+                load_tile<D>(a, tab, Bp, hl, ia * kTile, T, g, tig, blk_of(k), tr[0]);
+                load_tile<D>(a, tab, Bp, hl, ib * kTile, T, g, tig, blk_of(k + 1), tr[1]);
+                const int t0[2] = {ia * kTile, ib * kTile};
+                tiles_step<D, 2>(tr, qb, t0, T, g, sl, st);
+            } else if constexpr (FLYKV_DEC_KPREF && kStep == 1 && D <= 128) {
+                // K of the next tile is loaded while this tile computes; V of this tile is issued
+                // before its S^T MMAs and softmax, which hide part of its latency
+                if (k == 0) load_tile<D, true, false>(a, tab, Bp, hl, ia * kTile, T, g, tig, blk_of(0), kreg[0]);
+                load_tile<D, false, true>(a, tab, Bp, hl, ia * kTile, T, g, tig, blk_of(k), kreg[0]);
+                if (ib < i_end) load_tile<D, true, false>(a, tab, Bp, hl, ib * kTile, T, g, tig, blk_of(k + 1), knext);
+                const int t0[1] = {ia * kTile};
+                tiles_step<D, 1>(kreg, qb, t0, T, g, sl, st);
+#pragma unroll
+                for (int j = 0; j < D / 32; ++j) {
+                    kreg[0].k[j][0] = knext.k[j][0];
+                    kreg[0].k[j][1] = knext.k[j][1];
+                }
+            } else {
+                TileRegs<D> tr[1];
+                load_tile<D>(a, tab, Bp, hl, ia * kTile, T, g, tig, blk_of(k), tr[0]);
+                const int t0[1] = {ia * kTile};
+                tiles_step<D, 1>(tr, qb, t0, T, g, sl, st);
+            }
+        }
+        DEC_TRACE(u, 2);
+        // l: sum of the 8 row groups' partials (fixed xor order)
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1) {
+            st.l0 += __shfl_xor_sync(0xffffffffu, st.l0, o);
+            st.l1 += __shfl_xor_sync(0xffffffffu, st.l1, o);
+        }
+        if (tid == 0) sh_unit = next_u;
+        // ---- fold the warps (warp order) in shared memory
+        __syncthreads();  // the previous unit's readers are done with sm_*
+#pragma unroll
+        for (int mi = 0; mi < D / 16; ++mi) {
+            const int d0 = 8 * (g + 8 * (mi / 4)) + 2 * (mi % 4);
+            sm_o[wid][2 * tig][d0] = st.o[mi][0];
+            sm_o[wid][2 * tig + 1][d0] = st.o[mi][1];
+            sm_o[wid][2 * tig][d0 + 1] = st.o[mi][2];
+            sm_o[wid][2 * tig + 1][d0 + 1] = st.o[mi][3];
+        }
+        if (g == 0) {
+            sm_m[wid][2 * tig] = st.m0;
+            sm_m[wid][2 * tig + 1] = st.m1;
+            sm_l[wid][2 * tig] = st.l0;
+            sm_l[wid][2 * tig + 1] = st.l1;
+        }
+        __syncthreads();
+        // per head: M = max over warps, the warps' scale factors, L (warp order)
+        if (tid < 8) {
+            float M = -INFINITY;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) M = fmaxf(M, sm_m[w][tid]);
+            float L = 0.f;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) {
+                const float f = exp2f(sm_m[w][tid] - M);  // warps without tiles: m = -inf -> 0
+                sm_f[w][tid] = f;
+                L += sm_l[w][tid] * f;
+            }
+            sm_M[tid] = M;
+            sm_L[tid] = L;
+        }
+        __syncthreads();
+        float* part = a.ws + u * (int64_t)(16 + 8 * D);
+        if (S > 1 && tid < 8) {
+            part[tid] = sm_M[tid];
+            part[8 + tid] = sm_L[tid];
+        }
+        for (int e = tid; e < 8 * D; e += blockDim.x) {
+            const int h = e / D, dd = e % D;
+            float O = 0.f;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) O += sm_o[w][h][dd] * sm_f[w][h];
+            if (S == 1) {
+                if (h < nh) outp[(int64_t)h * D + dd] = O / sm_L[h];
+            } else {
+                part[16 + e] = O;
+            }
+        }
+        DEC_TRACE(u, 3);
+#ifdef FLYKV_DEC_TRACE
+        if (tid == 0 && u < 8192) {
+            unsigned smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            g_dec_trace[u][6] = smid;
+            g_dec_trace[u][7] = blockIdx.x;
+        }
+#endif
+        if (S == 1) continue;
+        // ---- several splits: the CTA that completes the last one folds them (split order)
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) {
+            const int old = atomicAdd(a.counters + (u - s), 1);
+            sh_last = old == S - 1;
+        }
+        __syncthreads();
+        DEC_TRACE(u, 4);
+        if (!sh_last) continue;
+        __threadfence();
+        const float* base = a.ws + (u - s) * (int64_t)(16 + 8 * D);
+        constexpr int kStride = 16 + 8 * D;
+        constexpr int kEl = 8 * D / (kWarps * 32);   // elements per thread
+        // splits in chunks of kFoldChunk: every (split, head) m and l loaded in parallel, the running
+        // max and the split order kept by sequential folds over shared memory (fixed order)
+        if (tid < 8) {
+            sm_M[tid] = -INFINITY;
+            sm_L[tid] = 0.f;
+        }
+        float acc[kEl];
+#pragma unroll
+        for (int x = 0; x < kEl; ++x) acc[x] = 0.f;
+        for (int k0 = 0; k0 < S; k0 += kFoldChunk) {
+            const int kn = min(kFoldChunk, S - k0);
+            __syncthreads();  // the previous chunk's readers are done
+            for (int t = tid; t < 8 * kn; t += blockDim.x) {
+                const float* pk = base + (int64_t)(k0 + t / 8) * kStride;
+                sm_pm[t / 8][t % 8] = __ldcg(pk + t % 8);
+                sm_pl[t / 8][t % 8] = __ldcg(pk + 8 + t % 8);
+            }
+            __syncthreads();
+            if (tid < 8) {  // new running max; rescale factor of what was accumulated so far
+                float M = sm_M[tid];
+                for (int k = 0; k < kn; ++k) M = fmaxf(M, sm_pm[k][tid]);
+                const float r = exp2f(sm_M[tid] - M);   // first chunk: exp2(-inf) = 0, nothing accumulated yet
+                float L = sm_L[tid] * r;
+                for (int k = 0; k < kn; ++k) {
+                    const float f = exp2f(sm_pm[k][tid] - M);
+                    sm_g[k][tid] = f;
+                    L += sm_pl[k][tid] * f;
+                }
+                sm_r[tid] = r;
+                sm_M[tid] = M;
+                sm_L[tid] = L;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int x = 0; x < kEl; ++x) {
+                const int e = tid + x * kWarps * 32, h = e / D;
+                float o = acc[x] * sm_r[h];
+                float v[kFoldChunk];
+#pragma unroll
+                for (int k = 0; k < kFoldChunk; ++k) v[k] = k < kn ? __ldcg(base + (int64_t)(k0 + k) * kStride + 16 + e) : 0.f;
+#pragma unroll
+                for (int k = 0; k < kFoldChunk; ++k)
+                    if (k < kn) o += v[k] * sm_g[k][h];
+                acc[x] = o;
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int x = 0; x < kEl; ++x) {
+            const int e = tid + x * kWarps * 32, h = e / D, dd = e % D;
+            if (h < nh) outp[(int64_t)h * D + dd] = acc[x] / sm_L[h];
+        }
+        if (tid == 0) a.counters[u - s] = 0;  // ready for the next call on this workspace
+        DEC_TRACE(u, 5);
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_decode(const DecodeArgs& a, int grid, cudaStream_t s) {
+    if (a.n_res == 0) return cudaSuccess;
     switch (a.d) {
-        case 64: flykv_paged_decode_kernel<2><<<grid, 128, 0, s>>>(a); break;
-        case 128: flykv_paged_decode_kernel<4><<<grid, 128, 0, s>>>(a); break;
-        case 256: flykv_paged_decode_kernel<8><<<grid, 128, 0, s>>>(a); break;
+        case 64: flykv_paged_decode_kernel<64><<<grid, kWarps * 32, 0, s>>>(a); break;
+        case 128: flykv_paged_decode_kernel<128><<<grid, kWarps * 32, 0, s>>>(a); break;
+        case 256: flykv_paged_decode_kernel<256><<<grid, kWarps * 32, 0, s>>>(a); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
+}
+
+int decode_split_tokens() { return kSplit; }
+
+#ifdef FLYKV_DEC_TRACE
+extern "C" int kv_debug_decode_trace(unsigned long long* host, int n) {
+    return (int)cudaMemcpyFromSymbol(host, g_dec_trace, sizeof(unsigned long long) * 8 * (size_t)n);
+}
+#endif
+
+// Persistent grid: resident CTAs per SM (2 by the launch bounds) x SMs,
+// queried once per (device, head_dim).
+int decode_grid(int d) {
+    static int cache[64][3] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int k = d == 64 ? 0 : d == 128 ? 1 : 2;
+    if (dev >= 0 && dev < 64 && cache[dev][k]) return cache[dev][k];
+    int sms = 148, per = 2;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const void* f = d == 64    ? reinterpret_cast<const void*>(flykv_paged_decode_kernel<64>)
+                    : d == 128 ? reinterpret_cast<const void*>(flykv_paged_decode_kernel<128>)
+                               : reinterpret_cast<const void*>(flykv_paged_decode_kernel<256>);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, f, kWarps * 32, 0) != cudaSuccess || per < 1) per = 1;
+    if (dev >= 0 && dev < 64) cache[dev][k] = sms * per;
+    return sms * per;
 }
 
 }  // namespace flykv

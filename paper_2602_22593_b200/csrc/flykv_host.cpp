@@ -11,6 +11,8 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
+#include <map>
 #include <new>
 #include <string>
 #include <unordered_set>
@@ -2029,21 +2031,60 @@ extern "C" kv_status kv_gather_view(const kv_view* v, void* dst, void* stream) {
 }
 
 // ------------------------------------------------------------ consumer proof
+// kv_paged_decode's workspace: one per (device, stream), grown on demand;
+// calls on one stream are ordered, so they can share it.  Its arrival
+// counters are zeroed once and left at zero by every call.
+struct DecodeWorkspace {
+    char* buf = nullptr;
+    size_t units = 0;
+};
+static std::mutex g_dec_mu;
+static std::map<std::pair<int, cudaStream_t>, DecodeWorkspace> g_dec_ws;
+
 extern "C" kv_status kv_paged_decode(const kv_geometry* geom, const void* layer_base, int32_t n_res,
                                      const int32_t* req_ptr, const int32_t* block_ids, const int32_t* per_req_meta,
                                      const int32_t* seq_lens, int32_t q_heads_local, const void* q, float* out,
-                                     float scale, void* stream) {
+                                     float scale, int32_t max_seq_len, void* stream_) {
     kv_status s = check_geometry(geom);
     if (s) return s;
     if (geom->elem_bytes != 2 || (geom->head_dim != 64 && geom->head_dim != 128 && geom->head_dim != 256))
         return fail(KV_ERR_INVALID_ARG, "kv_paged_decode needs bf16 and head_dim 64/128/256");
-    if (n_res < 0 || q_heads_local < 1 || (n_res > 0 && (!layer_base || !req_ptr || !block_ids || !per_req_meta ||
-                                                         !seq_lens || !q || !out)))
+    if (n_res < 0 || q_heads_local < 1 || max_seq_len < 0 ||
+        (n_res > 0 && (!layer_base || !req_ptr || !per_req_meta || !seq_lens || !q || !out)))
         return fail(KV_ERR_INVALID_ARG, "bad kv_paged_decode arguments");
+    if (((uintptr_t)q & 15) || ((uintptr_t)layer_base & 15))
+        return fail(KV_ERR_INVALID_ARG, "q and layer_base must be 16-byte aligned");
+    if (n_res == 0) return KV_OK;
+    cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+    const int d = geom->head_dim;
+    const int64_t split = decode_split_tokens();
+    // units per request <= q_heads_local (H_loc x head tiles) x splits
+    const size_t units = (size_t)n_res * (size_t)q_heads_local *
+                         (size_t)std::max<int64_t>(1, (max_seq_len + split - 1) / split);
+    const size_t unit_bytes = (size_t)(16 + 8 * d) * sizeof(float);
     DecodeArgs a{};
+    {
+        int dev = 0;
+        CUDA_TRY(cudaGetDevice(&dev));
+        std::lock_guard<std::mutex> lk(g_dec_mu);
+        DecodeWorkspace& w = g_dec_ws[{dev, stream}];
+        if (w.units < units) {
+            if (w.buf) CUDA_TRY(cudaFreeAsync(w.buf, stream));
+            w.buf = nullptr;
+            w.units = 0;
+            const size_t want = std::max(units, w.units * 2);
+            CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&w.buf),
+                                     want * unit_bytes + (want + 2) * sizeof(int32_t), stream));
+            CUDA_TRY(cudaMemsetAsync(w.buf + want * unit_bytes, 0, (want + 2) * sizeof(int32_t), stream));
+            w.units = want;
+        }
+        a.ws = reinterpret_cast<float*>(w.buf);
+        a.counters = reinterpret_cast<int32_t*>(w.buf + w.units * unit_bytes);
+        a.n_units_cap = (int64_t)w.units;
+    }
     a.layer = static_cast<const char*>(layer_base);
     a.M = 2 * (int64_t)geom->num_kv_heads * geom->block_base * geom->head_dim * geom->elem_bytes;
-    a.d = geom->head_dim;
+    a.d = d;
     a.n_res = n_res;
     a.q_local = q_heads_local;
     a.req_ptr = req_ptr;
@@ -2053,9 +2094,10 @@ extern "C" kv_status kv_paged_decode(const kv_geometry* geom, const void* layer_
     a.q = static_cast<const __nv_bfloat16*>(q);
     a.out = out;
     a.scale = scale;
-    cudaError_t e = launch_decode(a, static_cast<cudaStream_t>(stream));
+    a.max_seq = max_seq_len;
+    cudaError_t e = launch_decode(a, decode_grid(d), stream);
     if (e != cudaSuccess) return cuda_fail(e, "flykv_paged_decode_kernel launch");
-    if (n_res > 0) g_launches.fetch_add(1);
+    g_launches.fetch_add(1);
     return KV_OK;
 }
 

@@ -178,6 +178,11 @@ struct DecodeArgs {
     const __nv_bfloat16* q;     // [n_res][q_local][d]
     float* out;                 // [n_res][q_local][d]
     float scale;
+    int32_t max_seq;            // bound of seq_lens the workspace is sized for
+    float* ws;                  // per unit: m[8], l[8], O[8][d] of one 512-token split
+    int32_t* counters;          // per item (first unit index): splits done; then [n_units_cap] the
+                                // next unit, [n_units_cap + 1] CTAs done; all 0 between calls
+    int64_t n_units_cap;        // units the workspace holds
 };
 
 // Group completion barrier (kv_group_barrier): this process's mapping of
@@ -214,7 +219,9 @@ cudaError_t launch_reshard(const ReshardArgs& a, int device, cudaStream_t s);
 void set_reshard_impl(int impl, int ctas_per_sm);
 cudaError_t launch_remap(const RemapArgs& a, int n_ctas, cudaStream_t s);
 cudaError_t launch_gather(const GatherSeg* segs, int n_seg, char* dst, cudaStream_t s);
-cudaError_t launch_decode(const DecodeArgs& a, cudaStream_t s);
+cudaError_t launch_decode(const DecodeArgs& a, int grid, cudaStream_t s);
+int decode_split_tokens();
+int decode_grid(int d);
 cudaError_t launch_unpack(const UnpackArgs& a, int device, cudaStream_t s);
 cudaError_t launch_barrier(const BarrierArgs& a, cudaStream_t s);
 cudaError_t launch_barrier_selftest(const BarrierArgs& a, int32_t rounds, int32_t absent,

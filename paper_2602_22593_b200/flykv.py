@@ -168,7 +168,7 @@ _sig("kv_vmm_free", C.c_int, _P)
 _sig("weight_view_alias", C.c_int, _P, C.POINTER(View), C.POINTER(_P), C.POINTER(C.c_uint64))
 _sig("weight_view_unalias", C.c_int, _P, C.c_uint64)
 _sig("kv_paged_decode", C.c_int, C.POINTER(Geometry), _P, C.c_int32, _P, _P, _P, _P, C.c_int32, _P, _P, C.c_float,
-     _P)
+     C.c_int32, _P)
 _sig("kv_ipc_export", C.c_int, _P, C.POINTER(C.c_uint8), C.POINTER(C.c_uint64))
 _sig("kv_ipc_import", C.c_int, C.POINTER(C.c_uint8), C.c_uint64, C.POINTER(_P))
 _sig("kv_ipc_close", C.c_int, _P, C.c_uint64)
@@ -790,10 +790,12 @@ def weight_view_unalias(ptr: int, nbytes: int):
 
 # ----------------------------------------------------------------- consumer proof
 def kv_paged_decode(geom: Geometry, layer_base, n_res: int, req_ptr, block_ids, per_req_meta, seq_lens,
-                    q_heads_local: int, q, out, scale: float, stream=None):
+                    q_heads_local: int, q, out, scale: float, max_seq_len: int, stream=None):
+    """N3 paged decode attention over one layer of one pool (kv_paged_decode);
+    max_seq_len >= every seq_lens entry (sizes the split workspace)."""
     _check(_lib.kv_paged_decode(C.byref(geom), ptr_of(layer_base), n_res, ptr_of(req_ptr), ptr_of(block_ids),
                                 ptr_of(per_req_meta), ptr_of(seq_lens), q_heads_local, ptr_of(q), ptr_of(out),
-                                float(scale), stream_of(stream)))
+                                float(scale), int(max_seq_len), stream_of(stream)))
 
 
 # ----------------------------------------------------------------- IPC

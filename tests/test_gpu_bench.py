@@ -28,3 +28,15 @@ def test_bench_self_launched_ranks(n, config):
     assert d["value"] > 0 and d["gpu_launches"] > 0
     assert d["config"]["barrier"].startswith("host")
     assert d["e2e"]["api"].startswith("flykv.kv_switch_range_host")
+
+
+def test_bench_decode_line():
+    """bench.py --decode (N3): one decode step over every (pool, layer),
+    captured in a CUDA graph, before and after the forward switch; one JSON
+    line with the roofline of kv_paged_decode."""
+    r = subprocess.run([sys.executable, "bench.py", "--decode", "--config", "tiny", "--q-heads", "16", "--steps", "3",
+                        "--warmup", "3"], cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    d = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
+    assert d["roofline"]["kernel"] == "flykv_paged_decode_kernel" and d["roofline"]["bound"] == "hbm"
+    assert d["value"] > 0 and d["dp_layout"]["GBps"] > 0 and d["gpu_launches"] == 3 * 2 * 2

@@ -42,7 +42,7 @@ def _decode_all(F, eng, geo, plan, tables, q_full, gpus, q_slices, seq):
         out = torch.empty((n_res, qhi - qlo, d), dtype=torch.float32, device="cuda:0")
         layer = eng.pools.tensors[g][1]  # layer 1 of pool g
         F.kv_paged_decode(eng.geom, layer.data_ptr(), n_res, t.req_ptr, t.block_ids, t.meta, lens, qhi - qlo, q, out,
-                          1.0 / np.sqrt(d), eng.stream)
+                          1.0 / np.sqrt(d), max(seq), eng.stream)
         torch.cuda.synchronize()
         o = out.cpu().numpy()
         for k, i in enumerate(meta[:, 0]):
@@ -51,10 +51,17 @@ def _decode_all(F, eng, geo, plan, tables, q_full, gpus, q_slices, seq):
     return res
 
 
-@pytest.mark.parametrize("H,Hq,p1,permuted", [(8, 32, 2, False), (8, 32, 4, False), (8, 64, 8, False),
-                                               (4, 32, 8, False), (2, 16, 8, False), (8, 8, 2, False),
-                                               (8, 32, 4, True), (4, 32, 8, True)])
-def test_tp_after_relayout_equals_dp(H, Hq, p1, permuted):
+@pytest.mark.parametrize("H,Hq,p1,permuted,long", [(8, 32, 2, False, False), (8, 32, 4, False, False),
+                                                    (8, 64, 8, False, False), (4, 32, 8, False, False),
+                                                    (2, 16, 8, False, False), (8, 8, 2, False, False),
+                                                    (8, 32, 4, True, False), (4, 32, 8, True, False),
+                                                    (8, 64, 8, False, True), (2, 40, 8, True, True),
+                                                    (4, 8, 8, False, True)])
+def test_tp_after_relayout_equals_dp(H, Hq, p1, permuted, long):
+    """long: lengths up to 1700 tokens (several 512-token splits, folded by
+    the last-arriving CTA), plus an empty request (zeros); Hq = 40 over
+    H = 2 gives 20 query heads per KV head (three head tiles, the last
+    partial) on the DP replica and 5 per rank at TP8."""
     F = pytest.importorskip("paper_2602_22593_b200.flykv")
     from paper_2602_22593_b200.engine import KVSwitchEngine
     geo = (2, H, 128, 16, 2)
@@ -62,6 +69,11 @@ def test_tp_after_relayout_equals_dp(H, Hq, p1, permuted):
     n_gpus = 8
     rng = np.random.default_rng(H * 100 + Hq + p1)
     seq = [int(x) for x in rng.integers(1, 300, size=10)]
+    if long:
+        seq = [int(x) for x in rng.integers(1, 1700, size=10)]
+        seq[3] = 0
+        seq[5] = 512   # exactly one split
+        seq[6] = 1025  # three splits, the last with one token
     src = [((i % n_gpus), 1) for i in range(len(seq))]
     dst = [((i * p1) % n_gpus // p1 * p1, p1) for i in range(len(seq))]
     w = synth.Workload("c", *geo, n_gpus, seq, src, dst)
@@ -101,8 +113,8 @@ def test_tp_after_relayout_equals_dp(H, Hq, p1, permuted):
                 gpu, off = O.locate(og, src[i][0], 1, tabs0[i], 1, h, t_)
                 base = (1 * nb[gpu] * M + off) // 2
                 V[t_] = bf16_to_f64(host[gpu][base:base + 128])
-            for qh in range(h * G, (h + 1) * G):
-                ref[(i, qh)] = decode_attention(K, V, qf[i, qh], 1.0 / np.sqrt(128))
+            for qh in range(h * G, (h + 1) * G):   # no tokens: the kernel's documented zeros
+                ref[(i, qh)] = (decode_attention(K, V, qf[i, qh], 1.0 / np.sqrt(128)) if T else np.zeros(128))
     assert set(ref) == set(out_dp)
     for k, r in ref.items():
         assert np.allclose(out_dp[k], r, rtol=2e-3, atol=2e-3), k
