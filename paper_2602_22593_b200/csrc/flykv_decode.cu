@@ -36,12 +36,16 @@
 //     per-request meta (chunked block scans), so the host needs only an upper
 //     bound of the sequence lengths.  The workspace counters return to zero
 //     at the end of every launch.
-//   * Measured (bench.py --decode): about a third of
-//     the HBM roofline per (pool, layer) launch of 77 MB.  A launch is only
-//     ~12 us of transfer at peak; the per-unit chains of dependent loads
-//     (unit -> request -> block table -> tile), a load-then-compute tile loop
-//     and the folds leave HBM idle for much of it.  Launch shapes, split
-//     sizes and tile pairing are compile-time knobs (FLYKV_DEC_*) for sweeps.
+//   * Each warp stages its tiles through a 2-deep shared-memory ring
+//     (cp.async, rows padded to 2D + 16 bytes: conflict-free fragment
+//     reads), so one tile loads while the previous one computes.
+//   * Measured (bench.py --decode): 0.45 of the HBM
+//     roofline per (pool, layer) launch of 77 MB.  While the warps stream
+//     their tiles the bytes move at ~0.8 of the peak; the rest is fixed cost
+//     around that phase (per-unit geometry and block-table loads, folds,
+//     uneven unit ends, the launch) that a ~12 us launch cannot amortise.
+//     Launch shapes, split sizes, staging depth and tile pairing are
+//     compile-time knobs (FLYKV_DEC_*) for sweeps.
 #include <cuda_bf16.h>
 
 #include "flykv_internal.h"
@@ -60,6 +64,9 @@ constexpr int kSplit = FLYKV_DEC_SPLIT;   // tokens per unit
 #endif
 #ifndef FLYKV_DEC_CTAS
 #define FLYKV_DEC_CTAS 3
+#endif
+#ifndef FLYKV_DEC_STAGE
+#define FLYKV_DEC_STAGE 2   // stages per warp (0: tiles loaded straight into registers)
 #endif
 #ifndef FLYKV_DEC_KPREF
 #define FLYKV_DEC_KPREF 0
@@ -156,6 +163,11 @@ struct TileRegs {
     uint4 v[4][D / 64];
 };
 
+// Chunk (16 bytes = 8 head_dim elements) of a K / Q row that thread tig
+// holds as its j-th chunk: a bijection onto the row's D/8 chunks that keeps
+// the staged shared-memory reads conflict-free (pitch = 2D + 16 bytes).
+__device__ __forceinline__ int kchunk(int tig, int j) { return 2 * tig + (j & 1) + 8 * (j >> 1); }
+
 // blk >= 0: the tile's 16 rows lie in block blk (B(p) a multiple of 16; the
 // warp's block IDs were fetched up front), rows from t0 % B(p) on.  blk < 0:
 // every row looks its block up (any B(p)).  Rows past T re-read row T-1
@@ -179,8 +191,8 @@ __device__ __forceinline__ void load_tile(const DecodeArgs& a, const int32_t* ta
         const char* k1 = row_ptr(g + 8);
 #pragma unroll
         for (int j = 0; j < D / 32; ++j) {
-            tr.k[j][0] = ldg128(k0 + (tig + 4 * j) * 16);
-            tr.k[j][1] = ldg128(k1 + (tig + 4 * j) * 16);
+            tr.k[j][0] = ldg128(k0 + kchunk(tig, j) * 16);
+            tr.k[j][1] = ldg128(k1 + kchunk(tig, j) * 16);
         }
     }
     if constexpr (LV) {
@@ -196,6 +208,67 @@ __device__ __forceinline__ void load_tile(const DecodeArgs& a, const int32_t* ta
 
 __device__ __forceinline__ uint32_t word(const uint4& v, int w) {
     return w == 0 ? v.x : w == 1 ? v.y : w == 2 ? v.z : v.w;
+}
+
+
+// ---- shared-memory staged tiles (FLYKV_DEC_STAGE): each warp owns a ring of
+// kStages stages; a stage holds the tile's 16 K rows then its 16 V rows at a
+// padded pitch of 2D + 16 bytes (conflict-free fragment reads).  Lanes copy
+// 16-byte chunks with cp.async (rows past T re-read row T-1), so up to
+// kStages - 1 tiles are in flight while one is consumed.
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+    uint4 r;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(a));
+    return r;
+}
+
+template <int D>
+__device__ __forceinline__ void stage_tile(const DecodeArgs& a, const int32_t* tab, int32_t Bp, int32_t hl, int t0,
+                                           int T, int lane, int32_t blk, uint32_t st) {
+    constexpr int kRowChunks = D / 8, kPitch = 2 * D + 16;
+    const int64_t rowb = (int64_t)D * 2;
+    const int last = T - 1 - t0;
+    const char* base = nullptr;
+    if (blk >= 0) base = a.layer + (int64_t)blk * a.M + ((int64_t)hl * Bp + t0 % Bp) * rowb;
+#pragma unroll
+    for (int m = 0; m < 2 * 16 * kRowChunks / 32; ++m) {
+        const int c = lane + 32 * m;
+        const int row = c / kRowChunks, col = c % kRowChunks;   // rows 0-15 K, 16-31 V
+        const int x = row & 15;
+        const int xx = x <= last ? x : last;
+        const char* src;
+        if (blk >= 0) {
+            src = base + xx * rowb;
+        } else {
+            const int t = t0 + xx;
+            src = a.layer + (int64_t)__ldg(tab + t / Bp) * a.M + ((int64_t)hl * Bp + t % Bp) * rowb;
+        }
+        if (row >= 16) src += a.M >> 1;
+        cp_async16(st + row * kPitch + col * 16, src + col * 16);
+    }
+}
+
+template <int D>
+__device__ __forceinline__ void read_tile(uint32_t st, int g, int tig, TileRegs<D>& tr) {
+    constexpr int kPitch = 2 * D + 16;
+#pragma unroll
+    for (int j = 0; j < D / 32; ++j) {
+        tr.k[j][0] = lds128(st + g * kPitch + kchunk(tig, j) * 16);
+        tr.k[j][1] = lds128(st + (g + 8) * kPitch + kchunk(tig, j) * 16);
+    }
+    const int tv[4] = {2 * tig, 2 * tig + 1, 2 * tig + 8, 2 * tig + 9};
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int h = 0; h < D / 64; ++h) tr.v[x][h] = lds128(st + (16 + tv[x]) * kPitch + (g + 8 * h) * 16);
 }
 
 // NTL (1 or 2) 16-token tiles with ONE online-softmax update: S^T of each
@@ -282,12 +355,25 @@ __device__ __forceinline__ void tiles_step(const TileRegs<D> (&tr)[NTL], const u
     }
 }
 
+__device__ __forceinline__ uint32_t smem_u32addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
 template <int D>
 __global__ void __launch_bounds__(kWarps * 32, D == 256 ? 2 : kCtasPerSm) flykv_paged_decode_kernel(const DecodeArgs a) {
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int g = lane >> 2, tig = lane & 3;
+    extern __shared__ __align__(16) char dyn_smem[];   // FLYKV_DEC_STAGE rings
     // per-warp states for the CTA fold; chunked request scan
-    __shared__ float sm_o[kWarps][8][D];
+    // per-warp O states for the fold: inside the warp's staging ring when staged (free after its tiles)
+    constexpr bool kStaged = FLYKV_DEC_STAGE > 1 && D <= 128;
+    __shared__ float sm_o_static[kStaged ? 1 : kWarps][8][D];
+    auto so = [&](int w) -> float(*)[D] {
+        if constexpr (kStaged)
+            return reinterpret_cast<float(*)[D]>(dyn_smem + w * FLYKV_DEC_STAGE * 32 * (2 * D + 16));
+        else
+            return sm_o_static[w];
+    };
     __shared__ float sm_m[kWarps][8], sm_l[kWarps][8], sm_f[kWarps][8], sm_M[8], sm_L[8], sm_r[8];
     __shared__ float sm_g[kFoldChunk][8], sm_pm[kFoldChunk][8], sm_pl[kFoldChunk][8];
     __shared__ int sc_incl[kWarps * 32], sc_wtot[kWarps];
@@ -384,7 +470,7 @@ __global__ void __launch_bounds__(kWarps * 32, D == 256 ? 2 : kCtasPerSm) flykv_
             const char* qrow = reinterpret_cast<const char*>(a.q + ((int64_t)r * a.q_local + qh0 + (hv ? g : 0)) * D);
 #pragma unroll
             for (int j = 0; j < D / 32; ++j) {
-                uint4 c = hv ? *reinterpret_cast<const uint4*>(qrow + (tig + 4 * j) * 16) : make_uint4(0, 0, 0, 0);
+                uint4 c = hv ? *reinterpret_cast<const uint4*>(qrow + kchunk(tig, j) * 16) : make_uint4(0, 0, 0, 0);
                 qb[2 * j][0] = c.x;
                 qb[2 * j][1] = c.y;
                 qb[2 * j + 1][0] = c.z;
@@ -411,6 +497,32 @@ __global__ void __launch_bounds__(kWarps * 32, D == 256 ? 2 : kCtasPerSm) flykv_
         // tiles in pairs (k, k+1) with one softmax update per pair; an odd last tile alone
         // (head_dim 256: one tile per update, the registers hold one tile)
         constexpr int kStep = (D <= 128 && FLYKV_DEC_PAIR) ? 2 : 1;
+        if constexpr (FLYKV_DEC_STAGE > 1 && D <= 128) {
+            // staged ring: tiles k .. k + kStages - 2 in flight while tile k is consumed
+            constexpr int kStageBytes = 32 * (2 * D + 16);
+            const uint32_t ring = smem_u32addr(dyn_smem) + wid * FLYKV_DEC_STAGE * kStageBytes;
+            const int nk = i0 < i_end ? (i_end - 1 - i0) / kWarps + 1 : 0;
+#pragma unroll
+            for (int q = 0; q < FLYKV_DEC_STAGE - 1; ++q) {
+                if (q < nk) stage_tile<D>(a, tab, Bp, hl, (i0 + kWarps * q) * kTile, T, lane, blk_of(q), ring + q * kStageBytes);
+                cp_async_commit();
+            }
+            for (int k = 0; k < nk; ++k) {
+                const int kq = k + FLYKV_DEC_STAGE - 1;
+                if (kq < nk)
+                    stage_tile<D>(a, tab, Bp, hl, (i0 + kWarps * kq) * kTile, T, lane, blk_of(kq),
+                                  ring + (kq % FLYKV_DEC_STAGE) * kStageBytes);
+                cp_async_commit();
+                cp_async_wait<FLYKV_DEC_STAGE - 1>();
+                __syncwarp();
+                TileRegs<D> tr[1];
+                read_tile<D>(ring + (k % FLYKV_DEC_STAGE) * kStageBytes, g, tig, tr[0]);
+                __syncwarp();   // every lane has read the stage before it is refilled
+                const int t0[1] = {(i0 + kWarps * k) * kTile};
+                tiles_step<D, 1>(tr, qb, t0, T, g, sl, st);
+            }
+            cp_async_wait<0>();
+        } else {
         TileRegs<D> kreg[1], knext;   // FLYKV_DEC_KPREF: current tile (K then V), next tile's K
         for (int k = 0; i0 + kWarps * k < i_end; k += kStep) {
             const int ia = i0 + kWarps * k, ib = ia + kWarps;
@@ -440,6 +552,7 @@ __global__ void __launch_bounds__(kWarps * 32, D == 256 ? 2 : kCtasPerSm) flykv_
                 tiles_step<D, 1>(tr, qb, t0, T, g, sl, st);
             }
         }
+        }
         DEC_TRACE(u, 2);
         // l: sum of the 8 row groups' partials (fixed xor order)
 #pragma unroll
@@ -453,10 +566,10 @@ __global__ void __launch_bounds__(kWarps * 32, D == 256 ? 2 : kCtasPerSm) flykv_
 #pragma unroll
         for (int mi = 0; mi < D / 16; ++mi) {
             const int d0 = 8 * (g + 8 * (mi / 4)) + 2 * (mi % 4);
-            sm_o[wid][2 * tig][d0] = st.o[mi][0];
-            sm_o[wid][2 * tig + 1][d0] = st.o[mi][1];
-            sm_o[wid][2 * tig][d0 + 1] = st.o[mi][2];
-            sm_o[wid][2 * tig + 1][d0 + 1] = st.o[mi][3];
+            so(wid)[2 * tig][d0] = st.o[mi][0];
+            so(wid)[2 * tig + 1][d0] = st.o[mi][1];
+            so(wid)[2 * tig][d0 + 1] = st.o[mi][2];
+            so(wid)[2 * tig + 1][d0 + 1] = st.o[mi][3];
         }
         if (g == 0) {
             sm_m[wid][2 * tig] = st.m0;
@@ -490,7 +603,7 @@ __global__ void __launch_bounds__(kWarps * 32, D == 256 ? 2 : kCtasPerSm) flykv_
             const int h = e / D, dd = e % D;
             float O = 0.f;
 #pragma unroll
-            for (int w = 0; w < kWarps; ++w) O += sm_o[w][h][dd] * sm_f[w][h];
+            for (int w = 0; w < kWarps; ++w) O += so(w)[h][dd] * sm_f[w][h];
             if (S == 1) {
                 if (h < nh) outp[(int64_t)h * D + dd] = O / sm_L[h];
             } else {
@@ -580,12 +693,33 @@ __global__ void __launch_bounds__(kWarps * 32, D == 256 ? 2 : kCtasPerSm) flykv_
 
 }  // namespace
 
+template <int D>
+constexpr int decode_dyn_smem() {
+    return (FLYKV_DEC_STAGE > 1 && D <= 128) ? kWarps * FLYKV_DEC_STAGE * 32 * (2 * D + 16) : 0;
+}
+
+template <int D>
+static cudaError_t launch_decode_d(const DecodeArgs& a, int grid, cudaStream_t s) {
+    constexpr int smem = decode_dyn_smem<D>();
+    if (smem > 48 * 1024) {
+        static bool done = false;   // opt in once per process
+        if (!done) {
+            cudaError_t e = cudaFuncSetAttribute(flykv_paged_decode_kernel<D>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            if (e != cudaSuccess) return e;
+            done = true;
+        }
+    }
+    flykv_paged_decode_kernel<D><<<grid, kWarps * 32, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_decode(const DecodeArgs& a, int grid, cudaStream_t s) {
     if (a.n_res == 0) return cudaSuccess;
     switch (a.d) {
-        case 64: flykv_paged_decode_kernel<64><<<grid, kWarps * 32, 0, s>>>(a); break;
-        case 128: flykv_paged_decode_kernel<128><<<grid, kWarps * 32, 0, s>>>(a); break;
-        case 256: flykv_paged_decode_kernel<256><<<grid, kWarps * 32, 0, s>>>(a); break;
+        case 64: return launch_decode_d<64>(a, grid, s);
+        case 128: return launch_decode_d<128>(a, grid, s);
+        case 256: return launch_decode_d<256>(a, grid, s);
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
@@ -612,7 +746,9 @@ int decode_grid(int d) {
     const void* f = d == 64    ? reinterpret_cast<const void*>(flykv_paged_decode_kernel<64>)
                     : d == 128 ? reinterpret_cast<const void*>(flykv_paged_decode_kernel<128>)
                                : reinterpret_cast<const void*>(flykv_paged_decode_kernel<256>);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, f, kWarps * 32, 0) != cudaSuccess || per < 1) per = 1;
+    const int smem = d == 64 ? decode_dyn_smem<64>() : d == 128 ? decode_dyn_smem<128>() : decode_dyn_smem<256>();
+    if (smem > 48 * 1024) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, f, kWarps * 32, smem) != cudaSuccess || per < 1) per = 1;
     if (dev >= 0 && dev < 64) cache[dev][k] = sms * per;
     return sms * per;
 }

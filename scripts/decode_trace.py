@@ -54,7 +54,12 @@ for k, name in ((1, "geometry"), (2, "tiles"), (3, "fold")):
     d = (tr[:, k] - tr[:, k - 1]) / 1e3
     print(f"{name:9s} us: mean {d.mean():7.2f} p50 {np.median(d):7.2f} max {d.max():7.2f}")
 last = tr[:, 5] > 0
-print("last-arriver fold us: mean", ((tr[last, 5] - tr[last, 4]) / 1e3).mean(), "n", int(last.sum()))
+lf = (tr[last, 5] - tr[last, 4]) / 1e3
+print("last-arriver fold us: mean %.2f p50 %.2f max %.2f n %d" % (lf.mean(), np.median(lf), lf.max(), int(last.sum())))
+ends = np.maximum(tr[:, 3], tr[:, 5])
+print("unit end - start (us) p50/p90/max:", np.percentile((ends - tr[:, 0]) / 1e3, [50, 90, 100]))
+tiles_end = (tr[:, 2] - t0) / 1e3
+print("tile phase end offsets (us) p10/p50/p90/max:", np.percentile(tiles_end, [10, 50, 90, 100]))
 print("unit start offsets (us) p0/p50/p100:", np.percentile((tr[:, 0] - t0) / 1e3, [0, 50, 100]))
 print("unit end offsets (us) p50/p100:", np.percentile((np.maximum(tr[:, 3], tr[:, 5]) - t0) / 1e3, [50, 100]))
 per_cta = {}
