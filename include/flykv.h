@@ -609,7 +609,9 @@ kv_status kv_gather_view(const kv_view* view, void* dst, void* stream);
  *               library keeps per (device, stream) (a larger entry traps:
  *               a CUDA error, never a stray write)
  * Calls on one stream share that workspace (ordered); calls on different
- * streams use different ones.  bf16 and head_dim 64/128/256 only
+ * streams use different ones.  It grows outside stream capture only: a
+ * call captured into a CUDA graph that would need a larger workspace
+ * returns KV_ERR_BAD_STATE (call once with the same sizes before capturing).  bf16 and head_dim 64/128/256 only
  * (INVALID_ARG otherwise); KV_ERR_CUDA on workspace allocation or launch.
  */
 kv_status kv_paged_decode(const kv_geometry* geom, const void* layer_base, int32_t n_res, const int32_t* req_ptr,

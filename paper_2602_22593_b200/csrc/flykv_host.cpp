@@ -2069,6 +2069,13 @@ extern "C" kv_status kv_paged_decode(const kv_geometry* geom, const void* layer_
         std::lock_guard<std::mutex> lk(g_dec_mu);
         DecodeWorkspace& w = g_dec_ws[{dev, stream}];
         if (w.units < units) {
+            cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+            CUDA_TRY(cudaStreamIsCapturing(stream, &cap));
+            if (cap != cudaStreamCaptureStatusNone)   // a graph-owned buffer must not outlive its graph
+                return fail(KV_ERR_BAD_STATE,
+                            "kv_paged_decode: the stream's workspace (%zu units) is too small for %zu units and the "
+                            "stream is capturing; call once with the same or larger sizes before capture",
+                            w.units, units);
             if (w.buf) CUDA_TRY(cudaFreeAsync(w.buf, stream));
             w.buf = nullptr;
             w.units = 0;

@@ -758,3 +758,26 @@ def test_suggested_rank_ids_are_optimal_by_brute_force():
             return tot
         best = max(local_bytes(list(perm)) for perm in itertools.permutations(range(p)))
         assert local_bytes(sugg) == best, (case, sugg)
+
+
+def test_paged_decode_validates_before_the_device():
+    """kv_paged_decode argument checks need no GPU: geometry (bf16, head_dim
+    64/128/256), counts, NULL pointers, 16-byte alignment of q and the layer
+    base, a negative max_seq_len; n_res = 0 is a no-op."""
+    g = F.geometry(2, 4, 128, 16, 2)
+    a16 = 1 << 40
+    args = dict(layer_base=a16, n_res=4, req_ptr=a16, block_ids=a16, per_req_meta=a16, seq_lens=a16,
+                q_heads_local=8, q=a16, out=a16, scale=0.1, max_seq_len=100)
+
+    def call(geom=g, **kw):
+        d = dict(args, **kw)
+        F.kv_paged_decode(geom, d["layer_base"], d["n_res"], d["req_ptr"], d["block_ids"], d["per_req_meta"],
+                          d["seq_lens"], d["q_heads_local"], d["q"], d["out"], d["scale"], d["max_seq_len"])
+
+    for geom, kw in ((F.geometry(2, 4, 96, 16, 2), {}), (F.geometry(2, 4, 128, 16, 4), {}), (g, {"n_res": -1}),
+                     (g, {"q_heads_local": 0}), (g, {"req_ptr": None}), (g, {"q": a16 + 8}),
+                     (g, {"layer_base": a16 + 4}), (g, {"max_seq_len": -1}), (g, {"seq_lens": None})):
+        with pytest.raises(F.FlyKVError) as e:
+            call(geom, **kw)
+        assert e.value.name == "KV_ERR_INVALID_ARG", (geom.head_dim, kw)
+    call(n_res=0)   # nothing resident: no launch, no device work

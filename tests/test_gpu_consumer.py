@@ -134,3 +134,35 @@ def test_tp_after_relayout_equals_dp(H, Hq, p1, permuted, long):
     for k, v in out_dp.items():
         assert np.array_equal(out_tp[k], v), k
         assert np.allclose(out_tp[k], ref[k], rtol=2e-3, atol=2e-3), k   # and the fp64 oracle, directly
+
+
+def test_decode_workspace_not_grown_inside_graph_capture():
+    """kv_paged_decode under CUDA graph capture: a workspace that would have
+    to grow is refused (KV_ERR_BAD_STATE, nothing captured) -- a graph-owned
+    buffer must not outlive its graph; after one call outside capture the
+    same call captures and replays."""
+    F = pytest.importorskip("paper_2602_22593_b200.flykv")
+    g = F.geometry(1, 1, 128, 16, 2)
+    dev = "cuda:0"
+    layer = torch.zeros(4 * 2 * 16 * 128, dtype=torch.bfloat16, device=dev)      # 4 blocks, 1 head
+    rp = torch.tensor([0, 2], dtype=torch.int32, device=dev)
+    ids = torch.tensor([1, 3], dtype=torch.int32, device=dev)
+    meta = torch.tensor([[0, 16, 1, 0]], dtype=torch.int32, device=dev)
+    lens = torch.tensor([20], dtype=torch.int32, device=dev)
+    q = torch.randn((1, 2, 128), device=dev).to(torch.bfloat16)
+    out = torch.empty((1, 2, 128), dtype=torch.float32, device=dev)
+    s = torch.cuda.Stream()
+    graph = torch.cuda.CUDAGraph()
+    with pytest.raises(F.FlyKVError) as e:
+        with torch.cuda.graph(graph, stream=s):
+            F.kv_paged_decode(g, layer.data_ptr(), 1, rp, ids, meta, lens, 2, q, out, 0.1, 32, s)
+    assert e.value.name == "KV_ERR_BAD_STATE"
+    F.kv_paged_decode(g, layer.data_ptr(), 1, rp, ids, meta, lens, 2, q, out, 0.1, 32, s)   # sizes the workspace
+    s.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        F.kv_paged_decode(g, layer.data_ptr(), 1, rp, ids, meta, lens, 2, q, out, 0.1, 32, s)
+    out.fill_(7.0)
+    graph.replay()
+    torch.cuda.synchronize()
+    assert torch.all(out == 0)   # zero K/V: every score equal, output = mean of zero V rows
