@@ -387,12 +387,13 @@ __global__ void __launch_bounds__(kWarps * 32, D == 256 ? 2 : kCtasPerSm) flykv_
     // units are taken from an arrival counter (dynamic balance; the results do not depend on which CTA
     // computes what); the last CTA to run out of units resets the counters for the next call
     // the next unit is drawn while the current one runs (its atomic latency hidden)
-    if (tid == 0) sh_unit = atomicAdd(a.counters + a.n_units_cap, 1);
+    // CTA b starts with unit b; later units come from the counter, offset past the grid
+    if (tid == 0) sh_unit = blockIdx.x;
     int next_u = 0;
     while (true) {
         __syncthreads();  // sh_unit is set; the previous iteration's readers are done
         const long long u = sh_unit;
-        if (tid == 0) next_u = atomicAdd(a.counters + a.n_units_cap, 1);
+        if (tid == 0) next_u = (int)gridDim.x + atomicAdd(a.counters + a.n_units_cap, 1);
         __syncthreads();  // every thread has read sh_unit (the atomic above does not block here)
         // next_u is published for the next iteration after this unit's tiles: the atomic's latency
         // overlaps the geometry and tile loads
