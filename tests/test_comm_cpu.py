@@ -187,3 +187,30 @@ def test_host_barrier_gloo():
     for r in range(world):
         assert res[r]["ok"] and res[r]["outside"]
         assert res[r]["held_s"] >= 0.25
+
+
+def test_device_barrier_arm_bookkeeping():
+    """comm.DeviceBarrier.arm without a device: per key, the k-th barrier's
+    target is k x members on the 128-byte line of that key in every
+    member's counter buffer; a non-member or a one-member key gets None
+    (nothing to wait for)."""
+    b = object.__new__(comm.DeviceBarrier)
+    b.rank, b.world = 1, 4
+    b.keys = [(0, 1), (2, 3), (0, 1, 2, 3)]
+    b.slot = {k: i for i, k in enumerate(b.keys)}
+    b.count = {k: 0 for k in b.keys}
+    b.timeout_ns = 123
+    b.status = "status"
+    b.bases = [1000 * (r + 1) << 20 for r in range(4)]
+    flags, me, target, tmo, st = b.arm((0, 1))
+    assert (me, target, tmo, st) == (1, 2, 123, "status")
+    assert flags == [b.bases[0], b.bases[1]]
+    assert b.arm((0, 1))[2] == 4 and b.arm((0, 1, 2, 3))[2] == 4 and b.arm((0, 1, 2, 3))[2] == 8
+    flags4 = b.arm((0, 1, 2, 3))[0]
+    assert flags4 == [x + 2 * comm.DeviceBarrier.LINE * 8 for x in b.bases]
+    assert b.arm((2, 3)) is None and b.count[(2, 3)] == 0
+    b.rank = 0
+    b.keys.append((0,))
+    b.slot[(0,)] = 3
+    b.count[(0,)] = 0
+    assert b.arm((0,)) is None
