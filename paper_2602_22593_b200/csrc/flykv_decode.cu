@@ -137,17 +137,6 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 __device__ __forceinline__ float bf16_lo(uint32_t v) { return __uint_as_float(v << 16); }
 __device__ __forceinline__ float bf16_hi(uint32_t v) { return __uint_as_float(v & 0xffff0000u); }
 
-// Units of request r: H_loc KV heads x ceil(G/8) head tiles x splits (one
-// unit for T = 0, which writes zeros).
-__device__ __forceinline__ int units_of(const DecodeArgs& a, int r) {
-    const int32_t T = a.seq_lens[r];
-    const int32_t hloc = a.meta[4 * r + 2];
-    const int32_t G = a.q_local / hloc;
-    const int32_t nt = (G + 7) / 8;
-    const int32_t s = T > 0 ? (T + kSplit - 1) / kSplit : 1;
-    return hloc * nt * s;
-}
-
 // One warp's online-softmax state for its 8 head columns.
 template <int D>
 struct WarpState {
@@ -377,6 +366,7 @@ __global__ void __launch_bounds__(kWarps * 32, D == 256 ? 2 : kCtasPerSm) flykv_
     __shared__ float sm_m[kWarps][8], sm_l[kWarps][8], sm_f[kWarps][8], sm_M[8], sm_L[8], sm_r[8];
     __shared__ float sm_g[kFoldChunk][8], sm_pm[kFoldChunk][8], sm_pl[kFoldChunk][8];
     __shared__ int sc_incl[kWarps * 32], sc_wtot[kWarps];
+    __shared__ int sc_T[kWarps * 32], sc_Bp[kWarps * 32], sc_hloc[kWarps * 32], sc_rp[kWarps * 32];  // the chunk's requests
     __shared__ int sc_tot;
     __shared__ int sh_last, sh_unit;
     const float sl = a.scale * 1.4426950408889634f;  // scores in log2 units (exp2)
@@ -409,7 +399,18 @@ __global__ void __launch_bounds__(kWarps * 32, D == 256 ? 2 : kCtasPerSm) flykv_
             }
             __syncthreads();  // every thread is done reading the previous chunk's scan
             const int r = chunk_r + tid;
-            int x = r < a.n_res ? units_of(a, r) : 0;
+            int x = 0;
+            if (r < a.n_res) {   // the chunk's request fields, kept for the units' geometry
+                const int32_t T = a.seq_lens[r], Bp = a.meta[4 * r + 1], hloc = a.meta[4 * r + 2];
+                sc_T[tid] = T;
+                sc_Bp[tid] = Bp;
+                sc_hloc[tid] = hloc;
+                sc_rp[tid] = a.req_ptr[r];
+                const int32_t G = a.q_local / hloc;
+                // units of request r: H_loc KV heads x ceil(G/8) head tiles x splits (one unit for T = 0,
+                // which writes zeros)
+                x = hloc * ((G + 7) / 8) * (T > 0 ? (T + kSplit - 1) / kSplit : 1);
+            }
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const int y = __shfl_up_sync(0xffffffffu, x, o);
@@ -443,10 +444,10 @@ __global__ void __launch_bounds__(kWarps * 32, D == 256 ? 2 : kCtasPerSm) flykv_
         const int before = lo > 0 ? sc_incl[lo - 1] : 0;
         int local = uu - before;
         // ---- unit geometry
-        const int32_t T = a.seq_lens[r];
+        const int32_t T = sc_T[lo];
         if (T > a.max_seq) __trap();  // the workspace was sized for max_seq_len (a loud error, never a stray write)
-        const int32_t Bp = a.meta[4 * r + 1];
-        const int32_t hloc = a.meta[4 * r + 2];
+        const int32_t Bp = sc_Bp[lo];
+        const int32_t hloc = sc_hloc[lo];
         const int32_t G = a.q_local / hloc;
         const int32_t NT = (G + 7) / 8;
         const int32_t S = T > 0 ? (T + kSplit - 1) / kSplit : 1;
@@ -456,7 +457,7 @@ __global__ void __launch_bounds__(kWarps * 32, D == 256 ? 2 : kCtasPerSm) flykv_
         const int32_t hl = local / NT;
         const int32_t nh = min(8, G - 8 * nt);      // heads in this tile
         const int32_t qh0 = hl * G + 8 * nt;         // first local query head of the tile
-        const int32_t* tab = a.block_ids + a.req_ptr[r];
+        const int32_t* tab = a.block_ids + sc_rp[lo];
         DEC_TRACE(u, 1);
         float* outp = a.out + ((int64_t)r * a.q_local + qh0) * D;
         if (T == 0) {
