@@ -166,3 +166,70 @@ def test_decode_workspace_not_grown_inside_graph_capture():
     graph.replay()
     torch.cuda.synchronize()
     assert torch.all(out == 0)   # zero K/V: every score equal, output = mean of zero V rows
+
+
+@pytest.mark.parametrize("case", range(36))
+def test_decode_random_geometry_against_fp64(case):
+    """kv_paged_decode on random geometries straight from a pool: head_dim
+    64/128/256, block_base 8/16/32 (B(p) not a multiple of 16 takes the
+    per-row table lookup), degrees with and without GQA replication, 1-16
+    query heads per KV head, lengths 0-1300 (several 512-token splits),
+    random block IDs.  Member 0 of the group reads its heads; every
+    (request, query head) equals fp64 attention over the tokens
+    oracle.locate places, within fp32 tolerance."""
+    F = pytest.importorskip("paper_2602_22593_b200.flykv")
+    rng = np.random.default_rng(7100 + case)
+    d = int(rng.choice([64, 128, 256]))
+    B = int(rng.choice([8, 16, 32]))
+    H = int(rng.choice([1, 2, 4, 8]))
+    p = int(rng.choice([p_ for p_ in (1, 2, 4, 8) if (p_ <= H and H % p_ == 0) or (p_ > H and p_ % H == 0)]))
+    og = O.Geom(1, H, d, B, 2)
+    hloc = H // p if p <= H else 1
+    Bp = B * H // hloc
+    G = int(rng.choice([1, 2, 3, 8, 16]))
+    q_local = hloc * G
+    n_req = int(rng.integers(1, 7))
+    seq = [int(x) for x in rng.integers(0, 1300, size=n_req)]
+    if case % 5 == 0:
+        seq[0] = 0
+    counts = [O.num_blocks(og, T, p) for T in seq]
+    M = O.block_bytes(og)
+    nb = sum(counts) + 3
+    perm = [int(x) for x in rng.permutation(nb)]
+    tabs, k = [], 0
+    for c in counts:
+        tabs.append(perm[k:k + c])
+        k += c
+    pool = torch.randn(nb * M // 2, device="cuda:0").to(torch.bfloat16)   # finite contents everywhere
+    host = pool.view(torch.int16).cpu().numpy().view(np.uint16)
+    rp = np.concatenate([[0], np.cumsum(counts)]).astype(np.int32)
+    ids = np.concatenate([np.asarray(t, dtype=np.int32) for t in tabs] + [np.zeros(0, np.int32)])
+    first_head = 0                                                          # member 0 of the group
+    meta = np.array([[i, Bp, hloc, first_head] for i in range(n_req)], dtype=np.int32)
+    dev = lambda a: torch.as_tensor(a, device="cuda:0")                     # noqa: E731
+    q = torch.randn((n_req, q_local, d), device="cuda:0").to(torch.bfloat16)
+    out = torch.empty((n_req, q_local, d), dtype=torch.float32, device="cuda:0")
+    scale = 1.0 / np.sqrt(d)
+    F.kv_paged_decode(F.geometry(1, H, d, B, 2), pool.data_ptr(), n_req, dev(rp), dev(ids) if ids.size else None,
+                      dev(meta), dev(np.asarray(seq, np.int32)), q_local, q, out, scale, max(max(seq), 1))
+    torch.cuda.synchronize()
+    o = out.cpu().numpy()
+    qf = q.float().cpu().numpy().astype(np.float64)
+
+    def bf(u16):
+        return (u16.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+
+    for i, T in enumerate(seq):
+        for hl in range(hloc):
+            h = hl if p <= H else 0          # member 0's heads: [0, H_loc), or head 0 under replication
+            K = np.zeros((T, d))
+            V = np.zeros((T, d))
+            for t_ in range(T):
+                g_, off = O.locate(og, 0, p, tabs[i], 0, h, t_)
+                assert g_ == 0
+                K[t_] = bf(host[off // 2:off // 2 + d])
+                _, off = O.locate(og, 0, p, tabs[i], 1, h, t_)
+                V[t_] = bf(host[off // 2:off // 2 + d])
+            for j in range(hl * G, (hl + 1) * G):
+                ref = decode_attention(K, V, qf[i, j], scale) if T else np.zeros(d)
+                assert np.allclose(o[i, j], ref, rtol=2e-3, atol=2e-3), (case, i, j)
