@@ -79,7 +79,8 @@ constexpr int kCtasPerSm = FLYKV_DEC_CTAS;  // resident CTAs per SM (launch boun
 constexpr int kTilesPerWarp = kSplit / 16 / kWarps;
 static_assert(kTilesPerWarp >= 1 && kTilesPerWarp <= 32, "split / warps");
 constexpr int kTilesPerSplit = kSplit / kTile;
-constexpr int kFoldChunk = 8;             // splits folded per step by the last-arriving CTA
+constexpr int kFoldChunk = 8;             // partials folded per step by a folding CTA
+constexpr int kGroup = 16;                // splits per first-level fold group
 
 #ifdef FLYKV_DEC_TRACE
 // debug: per unit, %globaltimer at phase boundaries (unit taken, geometry read, tiles done, fold done,
@@ -344,6 +345,79 @@ __device__ __forceinline__ void tiles_step(const TileRegs<D> (&tr)[NTL], const u
     }
 }
 
+// Fold n partials (m[8], l[8], O[8][D] each) at base + k * step * kPart,
+// k = 0..n-1 in order: in chunks of kFoldChunk partials every (partial, head)
+// m and l are loaded in parallel and the running max is kept by sequential
+// folds over shared memory (a fixed order).  Result: out[h][d] = O / L for
+// the nh heads, or the folded (M, L, O) written as a partial at `to`
+// (which may be base: every read happens before the write).
+template <int D>
+__device__ __forceinline__ void fold_partials(const float* base, int step, int n, int nh, float* out, float* to,
+                                              int tid, float* sm_M, float* sm_L, float* sm_r,
+                                              float (*sm_g)[8], float (*sm_pm)[8], float (*sm_pl)[8]) {
+    constexpr int kPart = 16 + 8 * D;
+    constexpr int kEl = 8 * D / (kWarps * 32);   // elements per thread
+    const int64_t stride = (int64_t)step * kPart;
+    if (tid < 8) {
+        sm_M[tid] = -INFINITY;
+        sm_L[tid] = 0.f;
+    }
+    float acc[kEl];
+#pragma unroll
+    for (int x = 0; x < kEl; ++x) acc[x] = 0.f;
+    for (int k0 = 0; k0 < n; k0 += kFoldChunk) {
+        const int kn = min(kFoldChunk, n - k0);
+        __syncthreads();  // the previous chunk's readers are done
+        for (int t = tid; t < 8 * kn; t += kWarps * 32) {
+            const float* pk = base + (k0 + t / 8) * stride;
+            sm_pm[t / 8][t % 8] = __ldcg(pk + t % 8);
+            sm_pl[t / 8][t % 8] = __ldcg(pk + 8 + t % 8);
+        }
+        __syncthreads();
+        if (tid < 8) {  // new running max; rescale factor of what was accumulated so far
+            float M = sm_M[tid];
+            for (int k = 0; k < kn; ++k) M = fmaxf(M, sm_pm[k][tid]);
+            const float r = exp2f(sm_M[tid] - M);   // first chunk: exp2(-inf) = 0, nothing accumulated yet
+            float L = sm_L[tid] * r;
+            for (int k = 0; k < kn; ++k) {
+                const float f = exp2f(sm_pm[k][tid] - M);
+                sm_g[k][tid] = f;
+                L += sm_pl[k][tid] * f;
+            }
+            sm_r[tid] = r;
+            sm_M[tid] = M;
+            sm_L[tid] = L;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int x = 0; x < kEl; ++x) {
+            const int e = tid + x * kWarps * 32, h = e / D;
+            float o = acc[x] * sm_r[h];
+            float v[kFoldChunk];
+#pragma unroll
+            for (int k = 0; k < kFoldChunk; ++k) v[k] = k < kn ? __ldcg(base + (k0 + k) * stride + 16 + e) : 0.f;
+#pragma unroll
+            for (int k = 0; k < kFoldChunk; ++k)
+                if (k < kn) o += v[k] * sm_g[k][h];
+            acc[x] = o;
+        }
+    }
+    __syncthreads();   // every read of the partials is done (to may alias base)
+#pragma unroll
+    for (int x = 0; x < kEl; ++x) {
+        const int e = tid + x * kWarps * 32, h = e / D, dd = e % D;
+        if (out) {
+            if (h < nh) out[(int64_t)h * D + dd] = acc[x] / sm_L[h];
+        } else {
+            to[16 + e] = acc[x];
+        }
+    }
+    if (to && tid < 8) {
+        to[tid] = sm_M[tid];
+        to[8 + tid] = sm_L[tid];
+    }
+}
+
 __device__ __forceinline__ uint32_t smem_u32addr(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -596,7 +670,8 @@ __global__ void __launch_bounds__(kWarps * 32, D == 256 ? 2 : kCtasPerSm) flykv_
             sm_L[tid] = L;
         }
         __syncthreads();
-        float* part = a.ws + u * (int64_t)(16 + 8 * D);
+        constexpr int kPart = 16 + 8 * D;
+        float* part = a.ws + u * (int64_t)kPart;
         if (S > 1 && tid < 8) {
             part[tid] = sm_M[tid];
             part[8 + tid] = sm_L[tid];
@@ -622,73 +697,44 @@ __global__ void __launch_bounds__(kWarps * 32, D == 256 ? 2 : kCtasPerSm) flykv_
         }
 #endif
         if (S == 1) continue;
-        // ---- several splits: the CTA that completes the last one folds them (split order)
+        // ---- several splits: a fixed two-level tree.  Splits form groups of kGroup (by split index);
+        // the CTA that completes a group's last split folds the group (split order); with one group
+        // that is the output, otherwise the group's fold replaces its first split's partial and the
+        // CTA that completes the last group folds the groups (group order).  Counters: the group's
+        // first unit (groups), the item's second unit (the item).
+        const long long u0 = u - s;                     // the item's first unit
+        const int grp = s / kGroup, ng = (S + kGroup - 1) / kGroup;
+        const int gn = min(kGroup, S - grp * kGroup);   // splits in this group
         __threadfence();
         __syncthreads();
         if (tid == 0) {
-            const int old = atomicAdd(a.counters + (u - s), 1);
-            sh_last = old == S - 1;
+            const int old = atomicAdd(a.counters + u0 + grp * kGroup, 1);
+            sh_last = old == gn - 1;
         }
         __syncthreads();
         DEC_TRACE(u, 4);
         if (!sh_last) continue;
         __threadfence();
-        const float* base = a.ws + (u - s) * (int64_t)(16 + 8 * D);
-        constexpr int kStride = 16 + 8 * D;
-        constexpr int kEl = 8 * D / (kWarps * 32);   // elements per thread
-        // splits in chunks of kFoldChunk: every (split, head) m and l loaded in parallel, the running
-        // max and the split order kept by sequential folds over shared memory (fixed order)
-        if (tid < 8) {
-            sm_M[tid] = -INFINITY;
-            sm_L[tid] = 0.f;
-        }
-        float acc[kEl];
-#pragma unroll
-        for (int x = 0; x < kEl; ++x) acc[x] = 0.f;
-        for (int k0 = 0; k0 < S; k0 += kFoldChunk) {
-            const int kn = min(kFoldChunk, S - k0);
-            __syncthreads();  // the previous chunk's readers are done
-            for (int t = tid; t < 8 * kn; t += blockDim.x) {
-                const float* pk = base + (int64_t)(k0 + t / 8) * kStride;
-                sm_pm[t / 8][t % 8] = __ldcg(pk + t % 8);
-                sm_pl[t / 8][t % 8] = __ldcg(pk + 8 + t % 8);
+        if (tid == 0) a.counters[u0 + grp * kGroup] = 0;   // ready for the next call on this workspace
+        if (ng == 1) {
+            fold_partials<D>(a.ws + u0 * (int64_t)kPart, 1, S, nh, outp, nullptr, tid, sm_M, sm_L, sm_r, sm_g, sm_pm,
+                             sm_pl);
+        } else {
+            float* gslot = a.ws + (u0 + grp * kGroup) * (int64_t)kPart;
+            fold_partials<D>(gslot, 1, gn, 8, nullptr, gslot, tid, sm_M, sm_L, sm_r, sm_g, sm_pm, sm_pl);
+            __threadfence();
+            __syncthreads();
+            if (tid == 0) {
+                const int old = atomicAdd(a.counters + u0 + 1, 1);
+                sh_last = old == ng - 1;
             }
             __syncthreads();
-            if (tid < 8) {  // new running max; rescale factor of what was accumulated so far
-                float M = sm_M[tid];
-                for (int k = 0; k < kn; ++k) M = fmaxf(M, sm_pm[k][tid]);
-                const float r = exp2f(sm_M[tid] - M);   // first chunk: exp2(-inf) = 0, nothing accumulated yet
-                float L = sm_L[tid] * r;
-                for (int k = 0; k < kn; ++k) {
-                    const float f = exp2f(sm_pm[k][tid] - M);
-                    sm_g[k][tid] = f;
-                    L += sm_pl[k][tid] * f;
-                }
-                sm_r[tid] = r;
-                sm_M[tid] = M;
-                sm_L[tid] = L;
-            }
-            __syncthreads();
-#pragma unroll
-            for (int x = 0; x < kEl; ++x) {
-                const int e = tid + x * kWarps * 32, h = e / D;
-                float o = acc[x] * sm_r[h];
-                float v[kFoldChunk];
-#pragma unroll
-                for (int k = 0; k < kFoldChunk; ++k) v[k] = k < kn ? __ldcg(base + (int64_t)(k0 + k) * kStride + 16 + e) : 0.f;
-#pragma unroll
-                for (int k = 0; k < kFoldChunk; ++k)
-                    if (k < kn) o += v[k] * sm_g[k][h];
-                acc[x] = o;
-            }
+            if (!sh_last) continue;
+            __threadfence();
+            if (tid == 0) a.counters[u0 + 1] = 0;
+            fold_partials<D>(a.ws + u0 * (int64_t)kPart, kGroup, ng, nh, outp, nullptr, tid, sm_M, sm_L, sm_r, sm_g,
+                             sm_pm, sm_pl);
         }
-        __syncthreads();
-#pragma unroll
-        for (int x = 0; x < kEl; ++x) {
-            const int e = tid + x * kWarps * 32, h = e / D, dd = e % D;
-            if (h < nh) outp[(int64_t)h * D + dd] = acc[x] / sm_L[h];
-        }
-        if (tid == 0) a.counters[u - s] = 0;  // ready for the next call on this workspace
         DEC_TRACE(u, 5);
     }
 }

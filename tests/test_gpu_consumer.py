@@ -168,7 +168,7 @@ def test_decode_workspace_not_grown_inside_graph_capture():
     assert torch.all(out == 0)   # zero K/V: every score equal, output = mean of zero V rows
 
 
-@pytest.mark.parametrize("case", range(36))
+@pytest.mark.parametrize("case", list(range(36)) + ["long"])
 def test_decode_random_geometry_against_fp64(case):
     """kv_paged_decode on random geometries straight from a pool: head_dim
     64/128/256, block_base 8/16/32 (B(p) not a multiple of 16 takes the
@@ -178,7 +178,8 @@ def test_decode_random_geometry_against_fp64(case):
     (request, query head) equals fp64 attention over the tokens
     oracle.locate places, within fp32 tolerance."""
     F = pytest.importorskip("paper_2602_22593_b200.flykv")
-    rng = np.random.default_rng(7100 + case)
+    long = case == "long"   # 20,000 and 8,193 tokens: 40 and 17 splits, two fold levels (groups of 16)
+    rng = np.random.default_rng(7100 + (99 if long else case))
     d = int(rng.choice([64, 128, 256]))
     B = int(rng.choice([8, 16, 32]))
     H = int(rng.choice([1, 2, 4, 8]))
@@ -190,7 +191,11 @@ def test_decode_random_geometry_against_fp64(case):
     q_local = hloc * G
     n_req = int(rng.integers(1, 7))
     seq = [int(x) for x in rng.integers(0, 1300, size=n_req)]
-    if case % 5 == 0:
+    if long:
+        d, B, H, p, G = 128, 16, 1, 1, 2
+        og = O.Geom(1, H, d, B, 2)
+        hloc, Bp, q_local, n_req, seq = 1, B, 2, 3, [20000, 8193, 700]
+    elif case % 5 == 0:
         seq[0] = 0
     counts = [O.num_blocks(og, T, p) for T in seq]
     M = O.block_bytes(og)
