@@ -619,6 +619,12 @@ kv_status kv_paged_decode(const kv_geometry* geom, const void* layer_base, int32
                           int32_t q_heads_local, const void* q, float* out, float scale, int32_t max_seq_len,
                           void* stream);
 
+/* kv_paged_decode_release: free the decode workspace the library keeps for
+ * `stream` on the current device (stream-ordered; a later kv_paged_decode on
+ * that stream allocates a new one).  Call before destroying a stream that
+ * ran kv_paged_decode.  KV_OK if there is none; KV_ERR_CUDA on failure. */
+kv_status kv_paged_decode_release(void* stream);
+
 /* ------------------------------------------------------- multi-process */
 
 /* CUDA IPC helpers for peer pools (one process per GPU).  kv_ipc_export

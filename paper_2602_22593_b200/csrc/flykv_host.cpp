@@ -2108,6 +2108,19 @@ extern "C" kv_status kv_paged_decode(const kv_geometry* geom, const void* layer_
     return KV_OK;
 }
 
+extern "C" kv_status kv_paged_decode_release(void* stream_) {
+    cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_dec_mu);
+    auto it = g_dec_ws.find({dev, stream});
+    if (it == g_dec_ws.end()) return KV_OK;
+    char* buf = it->second.buf;
+    g_dec_ws.erase(it);
+    if (buf) CUDA_TRY(cudaFreeAsync(buf, stream));
+    return KV_OK;
+}
+
 // ------------------------------------------------------------ IPC (peer pools)
 typedef int (*cuMemGetAddressRange_t)(unsigned long long*, size_t*, unsigned long long);
 

@@ -169,6 +169,7 @@ _sig("weight_view_alias", C.c_int, _P, C.POINTER(View), C.POINTER(_P), C.POINTER
 _sig("weight_view_unalias", C.c_int, _P, C.c_uint64)
 _sig("kv_paged_decode", C.c_int, C.POINTER(Geometry), _P, C.c_int32, _P, _P, _P, _P, C.c_int32, _P, _P, C.c_float,
      C.c_int32, _P)
+_sig("kv_paged_decode_release", C.c_int, _P)
 _sig("kv_ipc_export", C.c_int, _P, C.POINTER(C.c_uint8), C.POINTER(C.c_uint64))
 _sig("kv_ipc_import", C.c_int, C.POINTER(C.c_uint8), C.c_uint64, C.POINTER(_P))
 _sig("kv_ipc_close", C.c_int, _P, C.c_uint64)
@@ -205,7 +206,7 @@ EXPORTED = ["kv_cache_create", "kv_cache_destroy", "kv_layout", "kv_blocks_for",
             "kv_suggest_rank_ids", "kv_plan_get_stats", "kv_plan_a2a_offsets", "kv_piece_request", "kv_plan_packed_offsets",
             "kv_plan_destroy",
             "weight_shard_view", "kv_gather_view", "kv_vmm_granularity", "kv_vmm_alloc", "kv_vmm_free",
-            "weight_view_alias", "weight_view_unalias", "kv_paged_decode", "kv_ipc_export", "kv_ipc_import", "kv_ipc_close",
+            "weight_view_alias", "weight_view_unalias", "kv_paged_decode", "kv_paged_decode_release", "kv_ipc_export", "kv_ipc_import", "kv_ipc_close",
             "kv_group_barrier", "kv_group_barrier_selftest", "kv_stream_sync", "kv_strerror", "kv_last_error", "kv_launch_count", "kv_set_reshard_impl",
             "kv_cache_set_work_order", "kv_plan_work_order", "kv_cache_set_strict", "kv_verify_replicas",
             "kv_pool_alloc", "kv_pool_export", "kv_pool_import", "kv_pool_free", "kv_mc_supported", "kv_mc_create",
@@ -796,6 +797,11 @@ def kv_paged_decode(geom: Geometry, layer_base, n_res: int, req_ptr, block_ids, 
     _check(_lib.kv_paged_decode(C.byref(geom), ptr_of(layer_base), n_res, ptr_of(req_ptr), ptr_of(block_ids),
                                 ptr_of(per_req_meta), ptr_of(seq_lens), q_heads_local, ptr_of(q), ptr_of(out),
                                 float(scale), int(max_seq_len), stream_of(stream)))
+
+
+def kv_paged_decode_release(stream=None):
+    """Free the decode workspace kept for `stream` (kv_paged_decode_release)."""
+    _check(_lib.kv_paged_decode_release(stream_of(stream)))
 
 
 # ----------------------------------------------------------------- IPC

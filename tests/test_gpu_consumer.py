@@ -166,6 +166,13 @@ def test_decode_workspace_not_grown_inside_graph_capture():
     graph.replay()
     torch.cuda.synchronize()
     assert torch.all(out == 0)   # zero K/V: every score equal, output = mean of zero V rows
+    del graph
+    F.kv_paged_decode_release(s)   # workspace freed; the next call on the stream allocates a new one
+    F.kv_paged_decode_release(s)   # none left: a no-op
+    out.fill_(7.0)
+    F.kv_paged_decode(g, layer.data_ptr(), 1, rp, ids, meta, lens, 2, q, out, 0.1, 32, s)
+    s.synchronize()
+    assert torch.all(out == 0)
 
 
 @pytest.mark.parametrize("case", list(range(36)) + ["long"])
