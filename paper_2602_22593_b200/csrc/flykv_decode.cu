@@ -457,10 +457,7 @@ __global__ void __launch_bounds__(kWarps * 32, D == 256 ? 2 : kCtasPerSm) flykv_
     while (true) {
         __syncthreads();  // sh_unit is set; the previous iteration's readers are done
         const long long u = sh_unit;
-        if (tid == 0) next_u = (int)gridDim.x + atomicAdd(a.counters + a.n_units_cap, 1);
-        __syncthreads();  // every thread has read sh_unit (the atomic above does not block here)
-        // next_u is published for the next iteration after this unit's tiles: the atomic's latency
-        // overlaps the geometry and tile loads
+        __syncthreads();  // every thread has read sh_unit
         DEC_TRACE(u, 0);
         // ---- find the unit's request: walk chunks of 128 requests forward
         bool done = false;
@@ -506,6 +503,9 @@ __global__ void __launch_bounds__(kWarps * 32, D == 256 ? 2 : kCtasPerSm) flykv_
             }
             return;
         }
+        // the next unit is drawn now (CTAs without a unit never touch the counter) and published
+        // after this unit's tiles: the atomic's latency overlaps the geometry and tile loads
+        if (tid == 0) next_u = (int)gridDim.x + atomicAdd(a.counters + a.n_units_cap, 1);
         // request index: first slot whose inclusive count exceeds u - chunk_u
         const int uu = (int)(u - chunk_u);
         int lo = 0, hi = kWarps * 32 - 1;
