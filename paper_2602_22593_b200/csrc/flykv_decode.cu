@@ -519,7 +519,9 @@ __global__ void __launch_bounds__(kWarps * 32, D == 256 ? 2 : kCtasPerSm) flykv_
         int local = uu - before;
         // ---- unit geometry
         const int32_t T = sc_T[lo];
-        if (T > a.max_seq) __trap();  // the workspace was sized for max_seq_len (a loud error, never a stray write)
+        // the workspace was sized for max_seq_len: a longer request (or a unit index it pushed past the
+        // workspace) is a loud error, never a stray write
+        if (T > a.max_seq || u >= a.n_units_cap) __trap();
         const int32_t Bp = sc_Bp[lo];
         const int32_t hloc = sc_hloc[lo];
         const int32_t G = a.q_local / hloc;
