@@ -39,7 +39,9 @@
 //   * Each warp stages its tiles through a 2-deep shared-memory ring
 //     (cp.async, rows padded to 2D + 16 bytes: conflict-free fragment
 //     reads), so one tile loads while the previous one computes.
-//   * Measured (bench.py --decode): 0.45 of the HBM
+//   * Consecutive launches overlap through programmatic dependent launch
+//     (the next grid scans its requests, then waits for this one).
+//   * Measured (bench.py --decode): 0.49 of the HBM
 //     roofline per (pool, layer) launch of 77 MB.  While the warps stream
 //     their tiles the bytes move at ~0.8 of the peak; the rest is fixed cost
 //     around that phase (per-unit geometry and block-table loads, folds,
@@ -67,6 +69,9 @@ constexpr int kSplit = FLYKV_DEC_SPLIT;   // tokens per unit
 #endif
 #ifndef FLYKV_DEC_STAGE
 #define FLYKV_DEC_STAGE 2   // stages per warp (0: tiles loaded straight into registers)
+#endif
+#ifndef FLYKV_DEC_PDL
+#define FLYKV_DEC_PDL 1     // programmatic dependent launch between consecutive decode launches
 #endif
 #ifndef FLYKV_DEC_KPREF
 #define FLYKV_DEC_KPREF 0
@@ -451,6 +456,13 @@ __global__ void __launch_bounds__(kWarps * 32, D == 256 ? 2 : kCtasPerSm) flykv_
     // units are taken from an arrival counter (dynamic balance; the results do not depend on which CTA
     // computes what); the last CTA to run out of units resets the counters for the next call
     // the next unit is drawn while the current one runs (its atomic latency hidden)
+#if FLYKV_DEC_PDL
+    // programmatic dependent launch: the next kernel on the stream may be scheduled now; it runs its
+    // request scan, then waits (griddepcontrol.wait) for this grid to complete before touching
+    // anything this grid reads or writes
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+    bool waited = false;
     // CTA b starts with unit b; later units come from the counter, offset past the grid
     if (tid == 0) sh_unit = blockIdx.x;
     int next_u = 0;
@@ -496,6 +508,12 @@ __global__ void __launch_bounds__(kWarps * 32, D == 256 ? 2 : kCtasPerSm) flykv_
             __syncthreads();
             chunk_n = sc_tot;
         }
+#if FLYKV_DEC_PDL
+        if (!waited) {   // the previous grid on the stream (workspace, q, out) has completed
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            waited = true;
+        }
+#endif
         if (done) {
             if (tid == 0 && atomicAdd(a.counters + a.n_units_cap + 1, 1) == (int)gridDim.x - 1) {
                 a.counters[a.n_units_cap] = 0;
@@ -760,8 +778,22 @@ static cudaError_t launch_decode_d(const DecodeArgs& a, int grid, cudaStream_t s
             done = true;
         }
     }
+#if FLYKV_DEC_PDL
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kWarps * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, flykv_paged_decode_kernel<D>, a);
+#else
     flykv_paged_decode_kernel<D><<<grid, kWarps * 32, smem, s>>>(a);
     return cudaGetLastError();
+#endif
 }
 
 cudaError_t launch_decode(const DecodeArgs& a, int grid, cudaStream_t s) {
