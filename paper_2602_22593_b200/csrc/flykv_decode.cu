@@ -46,8 +46,8 @@
 //     their tiles the bytes move at ~0.8 of the peak; the rest is fixed cost
 //     around that phase (per-unit geometry and block-table loads, folds,
 //     uneven unit ends, the launch) that a ~12 us launch cannot amortise.
-//     Launch shapes, split sizes, staging depth and tile pairing are
-//     compile-time knobs (FLYKV_DEC_*) for sweeps.
+//     Launch shapes, split sizes, staging depth and programmatic dependent
+//     launch are compile-time knobs (FLYKV_DEC_*) for sweeps.
 #include <cuda_bf16.h>
 
 #include "flykv_internal.h"
@@ -72,12 +72,6 @@ constexpr int kSplit = FLYKV_DEC_SPLIT;   // tokens per unit
 #endif
 #ifndef FLYKV_DEC_PDL
 #define FLYKV_DEC_PDL 1     // programmatic dependent launch between consecutive decode launches
-#endif
-#ifndef FLYKV_DEC_KPREF
-#define FLYKV_DEC_KPREF 0
-#endif
-#ifndef FLYKV_DEC_PAIR
-#define FLYKV_DEC_PAIR 0
 #endif
 constexpr int kWarps = FLYKV_DEC_WARPS;   // warps per CTA
 constexpr int kCtasPerSm = FLYKV_DEC_CTAS;  // resident CTAs per SM (launch bounds cap the registers)
@@ -167,7 +161,7 @@ __device__ __forceinline__ int kchunk(int tig, int j) { return 2 * tig + (j & 1)
 // warp's block IDs were fetched up front), rows from t0 % B(p) on.  blk < 0:
 // every row looks its block up (any B(p)).  Rows past T re-read row T-1
 // (masked in tile_step; never stale bytes).
-template <int D, bool LK = true, bool LV = true>
+template <int D>
 __device__ __forceinline__ void load_tile(const DecodeArgs& a, const int32_t* tab, int32_t Bp, int32_t hl, int t0,
                                           int T, int g, int tig, int32_t blk, TileRegs<D>& tr) {
     const int64_t rowb = (int64_t)D * 2;
@@ -181,23 +175,19 @@ __device__ __forceinline__ void load_tile(const DecodeArgs& a, const int32_t* ta
         const int t = t0 + xx;
         return a.layer + (int64_t)__ldg(tab + t / Bp) * a.M + ((int64_t)hl * Bp + t % Bp) * rowb;
     };
-    if constexpr (LK) {
-        const char* k0 = row_ptr(g);
-        const char* k1 = row_ptr(g + 8);
+    const char* k0 = row_ptr(g);
+    const char* k1 = row_ptr(g + 8);
 #pragma unroll
-        for (int j = 0; j < D / 32; ++j) {
-            tr.k[j][0] = ldg128(k0 + kchunk(tig, j) * 16);
-            tr.k[j][1] = ldg128(k1 + kchunk(tig, j) * 16);
-        }
+    for (int j = 0; j < D / 32; ++j) {
+        tr.k[j][0] = ldg128(k0 + kchunk(tig, j) * 16);
+        tr.k[j][1] = ldg128(k1 + kchunk(tig, j) * 16);
     }
-    if constexpr (LV) {
-        const int tv[4] = {2 * tig, 2 * tig + 1, 2 * tig + 8, 2 * tig + 9};
+    const int tv[4] = {2 * tig, 2 * tig + 1, 2 * tig + 8, 2 * tig + 9};
 #pragma unroll
-        for (int x = 0; x < 4; ++x) {
-            const char* vr = row_ptr(tv[x]) + half;
+    for (int x = 0; x < 4; ++x) {
+        const char* vr = row_ptr(tv[x]) + half;
 #pragma unroll
-            for (int h = 0; h < D / 64; ++h) tr.v[x][h] = ldg128(vr + (g + 8 * h) * 16);
-        }
+        for (int h = 0; h < D / 64; ++h) tr.v[x][h] = ldg128(vr + (g + 8 * h) * 16);
     }
 }
 
@@ -266,9 +256,10 @@ __device__ __forceinline__ void read_tile(uint32_t st, int g, int tig, TileRegs<
         for (int h = 0; h < D / 64; ++h) tr.v[x][h] = lds128(st + (16 + tv[x]) * kPitch + (g + 8 * h) * 16);
 }
 
-// NTL (1 or 2) 16-token tiles with ONE online-softmax update: S^T of each
-// tile on the tensor cores, the running max over all NTL*16 tokens, then
-// O^T += V^T P^T per tile.  The tile grouping is fixed by token index.
+// NTL 16-token tiles with ONE online-softmax update: S^T of each tile on the
+// tensor cores, the running max over all NTL*16 tokens, then O^T += V^T P^T
+// per tile.  The kernel uses NTL = 1 (two tiles per update needed registers
+// that cost resident CTAs: profiles/r02_decode_history.txt).
 template <int D, int NTL>
 __device__ __forceinline__ void tiles_step(const TileRegs<D> (&tr)[NTL], const uint32_t (&qb)[D / 16][2],
                                            const int (&t0)[NTL], int T, int g, float sl, WarpState<D>& st) {
@@ -590,9 +581,6 @@ __global__ void __launch_bounds__(kWarps * 32, D == 256 ? 2 : kCtasPerSm) flykv_
             if (ik < i_end) myblk = __ldg(tab + (ik * kTile) / Bp);
         }
         auto blk_of = [&](int k) { return fast ? __shfl_sync(0xffffffffu, myblk, k) : -1; };
-        // tiles in pairs (k, k+1) with one softmax update per pair; an odd last tile alone
-        // (head_dim 256: one tile per update, the registers hold one tile)
-        constexpr int kStep = (D <= 128 && FLYKV_DEC_PAIR) ? 2 : 1;
         if constexpr (FLYKV_DEC_STAGE > 1 && D <= 128) {
             // staged ring: tiles k .. k + kStages - 2 in flight while tile k is consumed
             constexpr int kStageBytes = 32 * (2 * D + 16);
@@ -618,36 +606,14 @@ __global__ void __launch_bounds__(kWarps * 32, D == 256 ? 2 : kCtasPerSm) flykv_
                 tiles_step<D, 1>(tr, qb, t0, T, g, sl, st);
             }
             cp_async_wait<0>();
-        } else {
-        TileRegs<D> kreg[1], knext;   // FLYKV_DEC_KPREF: current tile (K then V), next tile's K
-        for (int k = 0; i0 + kWarps * k < i_end; k += kStep) {
-            const int ia = i0 + kWarps * k, ib = ia + kWarps;
-            if (kStep == 2 && ib < i_end) {
-                TileRegs<D> tr[2];
-                load_tile<D>(a, tab, Bp, hl, ia * kTile, T, g, tig, blk_of(k), tr[0]);
-                load_tile<D>(a, tab, Bp, hl, ib * kTile, T, g, tig, blk_of(k + 1), tr[1]);
-                const int t0[2] = {ia * kTile, ib * kTile};
-                tiles_step<D, 2>(tr, qb, t0, T, g, sl, st);
-            } else if constexpr (FLYKV_DEC_KPREF && kStep == 1 && D <= 128) {
-                // K of the next tile is loaded while this tile computes; V of this tile is issued
-                // before its S^T MMAs and softmax, which hide part of its latency
-                if (k == 0) load_tile<D, true, false>(a, tab, Bp, hl, ia * kTile, T, g, tig, blk_of(0), kreg[0]);
-                load_tile<D, false, true>(a, tab, Bp, hl, ia * kTile, T, g, tig, blk_of(k), kreg[0]);
-                if (ib < i_end) load_tile<D, true, false>(a, tab, Bp, hl, ib * kTile, T, g, tig, blk_of(k + 1), knext);
-                const int t0[1] = {ia * kTile};
-                tiles_step<D, 1>(kreg, qb, t0, T, g, sl, st);
-#pragma unroll
-                for (int j = 0; j < D / 32; ++j) {
-                    kreg[0].k[j][0] = knext.k[j][0];
-                    kreg[0].k[j][1] = knext.k[j][1];
-                }
-            } else {
+        } else {   // head_dim 256 (or FLYKV_DEC_STAGE=0): each tile loaded into registers, then consumed
+            for (int k = 0; i0 + kWarps * k < i_end; ++k) {
+                const int ia = i0 + kWarps * k;
                 TileRegs<D> tr[1];
                 load_tile<D>(a, tab, Bp, hl, ia * kTile, T, g, tig, blk_of(k), tr[0]);
                 const int t0[1] = {ia * kTile};
                 tiles_step<D, 1>(tr, qb, t0, T, g, sl, st);
             }
-        }
         }
         DEC_TRACE(u, 2);
         // l: sum of the 8 row groups' partials (fixed xor order)
