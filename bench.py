@@ -1289,12 +1289,18 @@ def run_decode(args):
     torch.cuda.synchronize()
     dp_items = prepare(plan0, views0, host0, lambda i: w.src[i][1])
     dp_ms, dp_bytes, dp_launch, dp_eager = timed(dp_items)
+    os.environ["FLYKV_DECODE_PDL"] = "0"   # the same step with every launch waiting for the previous one
+    dp_ms_serial = timed(dp_items)[0]
+    os.environ.pop("FLYKV_DECODE_PDL", None)
     # forward switch, then the TP layout
     move = [(i, T, s_, ids_, d_) for i, (T, s_, ids_, d_) in enumerate(zip(w.T, w.src, tabs, w.dst))]
     plan1, views1, host1 = eng.switch(move, read_back=True)
     torch.cuda.synchronize()
     tp_items = prepare(plan1, views1, host1, lambda i: w.dst[i][1])
     tp_ms, tp_bytes, tp_launch, tp_eager = timed(tp_items)
+    os.environ["FLYKV_DECODE_PDL"] = "0"
+    tp_ms_serial = timed(tp_items)[0]
+    os.environ.pop("FLYKV_DECODE_PDL", None)
     clk.stop()
     gbs = tp_bytes / tp_ms / 1e6
     line = {
@@ -1304,16 +1310,23 @@ def run_decode(args):
         "config": {"workload": w.name + " after the forward switch", "layers": w.L, "kv_heads": w.H,
                    "q_heads": Hq, "head_dim": w.d, "requests": len(w.T), "tokens": w.tokens(),
                    "step": f"one decode step: kv_paged_decode for every (pool, layer), {tp_launch // args.steps} "
-                           "launches, captured once in a CUDA graph and replayed",
+                           "launches back to back (programmatic dependent launch overlaps each launch's tiles "
+                           "with the previous one's tail), captured once in a CUDA graph and replayed",
                    "l2": "inputs larger than L2 (KV bytes per pass >> 126 MB), no flush needed"},
         "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm, "unit": "GB/s",
                      "frac": round(gbs / hbm, 4), "traffic": None, "peak_source": hbm_src,
                      "kernel": "flykv_paged_decode_kernel", "algorithmic_bytes_per_step": int(tp_bytes),
                      "algorithmic_bytes": "every K/V byte of every resident (request, local KV head) + q + out"},
+        "serialized": {"ms_per_step": round(tp_ms_serial, 4), "GBps": round(tp_bytes / tp_ms_serial / 1e6, 1),
+                       "frac": round(tp_bytes / tp_ms_serial / 1e6 / hbm, 4),
+                       "note": "FLYKV_DECODE_PDL=0: no programmatic dependent launch, every launch starts after "
+                               "the previous one completed (as when a model's other layer kernels sit between "
+                               "two attention launches); value/roofline overlap consecutive launches"},
         "eager_ms_per_step": round(tp_eager, 4),
         "eager_note": "the same step launched from Python (640 ctypes calls): host-bound, context only",
         "dp_layout": {"ms_per_step": round(dp_ms, 4), "GBps": round(dp_bytes / dp_ms / 1e6, 1),
                       "eager_ms_per_step": round(dp_eager, 4),
+                      "serialized_frac": round(dp_bytes / dp_ms_serial / 1e6 / hbm, 4),
                       "frac": round(dp_bytes / dp_ms / 1e6 / hbm, 4), "bytes_per_step": int(dp_bytes),
                       "launches_per_step": dp_launch // args.steps},
         "gpu_launches": tp_launch,

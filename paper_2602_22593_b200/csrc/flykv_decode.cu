@@ -39,16 +39,21 @@
 //   * Each warp stages its tiles through a 2-deep shared-memory ring
 //     (cp.async, rows padded to 2D + 16 bytes: conflict-free fragment
 //     reads), so one tile loads while the previous one computes.
-//   * Consecutive launches overlap through programmatic dependent launch
-//     (the next grid scans its requests, then waits for this one).
-//   * Measured (bench.py --decode): 0.49 of the HBM
-//     roofline per (pool, layer) launch of 77 MB.  While the warps stream
+//   * Consecutive launches overlap through programmatic dependent launch:
+//     the next grid scans its requests and runs its tiles (the cache, q and
+//     the tables are never written by a decode grid) and waits for this one
+//     only before its workspace and out.
+//   * Measured (bench.py --decode): 0.65 of the HBM
+//     roofline back to back, 0.45 with every (pool, layer) launch of 77 MB
+//     serialized.  While the warps stream
 //     their tiles the bytes move at ~0.8 of the peak; the rest is fixed cost
 //     around that phase (per-unit geometry and block-table loads, folds,
 //     uneven unit ends, the launch) that a ~12 us launch cannot amortise.
 //     Launch shapes, split sizes, staging depth and programmatic dependent
 //     launch are compile-time knobs (FLYKV_DEC_*) for sweeps.
 #include <cuda_bf16.h>
+
+#include <cstdlib>
 
 #include "flykv_internal.h"
 
@@ -454,6 +459,14 @@ __global__ void __launch_bounds__(kWarps * 32, D == 256 ? 2 : kCtasPerSm) flykv_
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #endif
     bool waited = false;
+    auto pdl_wait = [&]() {   // the previous grid on the stream has completed (its workspace and out)
+#if FLYKV_DEC_PDL
+        if (!waited) {
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            waited = true;
+        }
+#endif
+    };
     // CTA b starts with unit b; later units come from the counter, offset past the grid
     if (tid == 0) sh_unit = blockIdx.x;
     int next_u = 0;
@@ -499,22 +512,14 @@ __global__ void __launch_bounds__(kWarps * 32, D == 256 ? 2 : kCtasPerSm) flykv_
             __syncthreads();
             chunk_n = sc_tot;
         }
-#if FLYKV_DEC_PDL
-        if (!waited) {   // the previous grid on the stream (workspace, q, out) has completed
-            asm volatile("griddepcontrol.wait;" ::: "memory");
-            waited = true;
-        }
-#endif
         if (done) {
+            pdl_wait();
             if (tid == 0 && atomicAdd(a.counters + a.n_units_cap + 1, 1) == (int)gridDim.x - 1) {
                 a.counters[a.n_units_cap] = 0;
                 a.counters[a.n_units_cap + 1] = 0;
             }
             return;
         }
-        // the next unit is drawn now (CTAs without a unit never touch the counter) and published
-        // after this unit's tiles: the atomic's latency overlaps the geometry and tile loads
-        if (tid == 0) next_u = (int)gridDim.x + atomicAdd(a.counters + a.n_units_cap, 1);
         // request index: first slot whose inclusive count exceeds u - chunk_u
         const int uu = (int)(u - chunk_u);
         int lo = 0, hi = kWarps * 32 - 1;
@@ -546,23 +551,11 @@ __global__ void __launch_bounds__(kWarps * 32, D == 256 ? 2 : kCtasPerSm) flykv_
         DEC_TRACE(u, 1);
         float* outp = a.out + ((int64_t)r * a.q_local + qh0) * D;
         if (T == 0) {
+            pdl_wait();
+            if (tid == 0) next_u = (int)gridDim.x + atomicAdd(a.counters + a.n_units_cap, 1);
             for (int i = tid; i < nh * D; i += blockDim.x) outp[i] = 0.f;
             if (tid == 0) sh_unit = next_u;
             continue;
-        }
-        // ---- Q^T fragments of the tile's heads (zero for padding heads)
-        uint32_t qb[D / 16][2];
-        {
-            const bool hv = g < nh;
-            const char* qrow = reinterpret_cast<const char*>(a.q + ((int64_t)r * a.q_local + qh0 + (hv ? g : 0)) * D);
-#pragma unroll
-            for (int j = 0; j < D / 32; ++j) {
-                uint4 c = hv ? *reinterpret_cast<const uint4*>(qrow + kchunk(tig, j) * 16) : make_uint4(0, 0, 0, 0);
-                qb[2 * j][0] = c.x;
-                qb[2 * j][1] = c.y;
-                qb[2 * j + 1][0] = c.z;
-                qb[2 * j + 1][1] = c.w;
-            }
         }
         // ---- the warp's tiles of this split: 32s + wid, +4, ...
         WarpState<D> st;
@@ -581,16 +574,33 @@ __global__ void __launch_bounds__(kWarps * 32, D == 256 ? 2 : kCtasPerSm) flykv_
             if (ik < i_end) myblk = __ldg(tab + (ik * kTile) / Bp);
         }
         auto blk_of = [&](int k) { return fast ? __shfl_sync(0xffffffffu, myblk, k) : -1; };
-        if constexpr (FLYKV_DEC_STAGE > 1 && D <= 128) {
-            // staged ring: tiles k .. k + kStages - 2 in flight while tile k is consumed
-            constexpr int kStageBytes = 32 * (2 * D + 16);
-            const uint32_t ring = smem_u32addr(dyn_smem) + wid * FLYKV_DEC_STAGE * kStageBytes;
-            const int nk = i0 < i_end ? (i_end - 1 - i0) / kWarps + 1 : 0;
+        constexpr bool kStagedLoop = FLYKV_DEC_STAGE > 1 && D <= 128;
+        constexpr int kStageBytes = 32 * (2 * D + 16);
+        const uint32_t ring = smem_u32addr(dyn_smem) + wid * FLYKV_DEC_STAGE * kStageBytes;
+        const int nk = i0 < i_end ? (i_end - 1 - i0) / kWarps + 1 : 0;
+        if constexpr (kStagedLoop) {
 #pragma unroll
             for (int q = 0; q < FLYKV_DEC_STAGE - 1; ++q) {
                 if (q < nk) stage_tile<D>(a, tab, Bp, hl, (i0 + kWarps * q) * kTile, T, lane, blk_of(q), ring + q * kStageBytes);
                 cp_async_commit();
             }
+        }
+        // ---- Q^T fragments of the tile's heads (zero for padding heads)
+        uint32_t qb[D / 16][2];
+        {
+            const bool hv = g < nh;
+            const char* qrow = reinterpret_cast<const char*>(a.q + ((int64_t)r * a.q_local + qh0 + (hv ? g : 0)) * D);
+#pragma unroll
+            for (int j = 0; j < D / 32; ++j) {
+                uint4 c = hv ? *reinterpret_cast<const uint4*>(qrow + kchunk(tig, j) * 16) : make_uint4(0, 0, 0, 0);
+                qb[2 * j][0] = c.x;
+                qb[2 * j][1] = c.y;
+                qb[2 * j + 1][0] = c.z;
+                qb[2 * j + 1][1] = c.w;
+            }
+        }
+        if constexpr (kStagedLoop) {
+            // staged ring: tiles k .. k + kStages - 2 in flight while tile k is consumed
             for (int k = 0; k < nk; ++k) {
                 const int kq = k + FLYKV_DEC_STAGE - 1;
                 if (kq < nk)
@@ -622,7 +632,15 @@ __global__ void __launch_bounds__(kWarps * 32, D == 256 ? 2 : kCtasPerSm) flykv_
             st.l0 += __shfl_xor_sync(0xffffffffu, st.l0, o);
             st.l1 += __shfl_xor_sync(0xffffffffu, st.l1, o);
         }
-        if (tid == 0) sh_unit = next_u;
+        // the tiles above read only the cache, q and the tables, which the previous decode grid on the
+        // stream does not write: with programmatic dependent launch they overlap that grid's tail.
+        // From here on (workspace, out) the previous grid must have completed.
+        pdl_wait();
+        // the next unit (CTAs without a unit never touch the counter)
+        if (tid == 0) {
+            next_u = (int)gridDim.x + atomicAdd(a.counters + a.n_units_cap, 1);
+            sh_unit = next_u;
+        }
         // ---- fold the warps (warp order) in shared memory
         __syncthreads();  // the previous unit's readers are done with sm_*
 #pragma unroll
@@ -745,6 +763,13 @@ static cudaError_t launch_decode_d(const DecodeArgs& a, int grid, cudaStream_t s
         }
     }
 #if FLYKV_DEC_PDL
+    // FLYKV_DECODE_PDL=0 (read per call): launch without the programmatic edge, every launch after the
+    // previous one completed (the bench reports both)
+    const char* env = std::getenv("FLYKV_DECODE_PDL");
+    if (env && env[0] == '0') {
+        flykv_paged_decode_kernel<D><<<grid, kWarps * 32, smem, s>>>(a);
+        return cudaGetLastError();
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kWarps * 32);
