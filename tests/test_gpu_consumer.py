@@ -245,3 +245,40 @@ def test_decode_random_geometry_against_fp64(case):
             for j in range(hl * G, (hl + 1) * G):
                 ref = decode_attention(K, V, qf[i, j], scale) if T else np.zeros(d)
                 assert np.allclose(o[i, j], ref, rtol=2e-3, atol=2e-3), (case, i, j)
+
+
+def test_decode_back_to_back_launches_same_out():
+    """Consecutive kv_paged_decode launches on one stream overlap through
+    programmatic dependent launch; a launch's tiles may run under the
+    previous one's tail, but its workspace and out writes wait for it.  Two
+    launches with different q into the same out (and a third with a longer
+    length bound's workspace) leave exactly the last launch's result."""
+    F = pytest.importorskip("paper_2602_22593_b200.flykv")
+    rng = np.random.default_rng(77)
+    g = F.geometry(1, 2, 128, 16, 2)
+    og = O.Geom(1, 2, 128, 16, 2)
+    seq = [1500, 700, 33, 2600]
+    counts = [O.num_blocks(og, T, 1) for T in seq]
+    M = O.block_bytes(og)
+    nb = sum(counts) + 2
+    perm = [int(x) for x in rng.permutation(nb)]
+    rp = np.concatenate([[0], np.cumsum(counts)]).astype(np.int32)
+    ids = np.asarray(perm[:sum(counts)], dtype=np.int32)
+    meta = np.array([[i, 16, 2, 0] for i in range(len(seq))], dtype=np.int32)
+    dev = lambda a: torch.as_tensor(a, device="cuda:0")                     # noqa: E731
+    pool = torch.randn(nb * M // 2, device="cuda:0").to(torch.bfloat16)
+    lens = dev(np.asarray(seq, np.int32))
+    qs = [torch.randn((len(seq), 8, 128), device="cuda:0").to(torch.bfloat16) for _ in range(3)]
+    s = torch.cuda.Stream()
+    out = torch.empty((len(seq), 8, 128), dtype=torch.float32, device="cuda:0")
+    ref = torch.empty_like(out)
+    args = (pool.data_ptr(), len(seq), dev(rp), dev(ids), dev(meta), lens, 8)
+    for k in range(3):   # back to back on one stream, same out
+        F.kv_paged_decode(g, *args, qs[k], out, 0.09, 4096 if k < 2 else 8192, s)
+    s.synchronize()
+    s2 = torch.cuda.Stream()
+    F.kv_paged_decode(g, *args, qs[2], ref, 0.09, 8192, s2)
+    s2.synchronize()
+    assert torch.equal(out, ref)
+    F.kv_paged_decode_release(s)
+    F.kv_paged_decode_release(s2)
