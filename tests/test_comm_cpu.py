@@ -214,3 +214,33 @@ def test_device_barrier_arm_bookkeeping():
     b.slot[(0,)] = 3
     b.count[(0,)] = 0
     assert b.arm((0,)) is None
+
+
+def _share_worker(rank, world, port, same, q):
+    import types
+    import torch
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        uuid = "GPU-A" if same else f"GPU-{rank}"
+        torch.cuda.get_device_properties = lambda dev: types.SimpleNamespace(uuid=uuid, pci_bus_id=0)
+        q.put((rank, comm.ranks_share_a_device("cuda:0")))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("same", [True, False])
+def test_ranks_share_a_device_gloo(same):
+    """comm.make_barrier's test: ranks reporting one GPU UUID share a device
+    (-> HostBarrier); distinct UUIDs do not (-> DeviceBarrier)."""
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_share_worker, args=(r, world, port, same, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    assert all(v is same for v in res.values())
