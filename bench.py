@@ -59,7 +59,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c4",
                     help="workload key of synth.WORKLOADS; default c4 = the north_star headline (Llama-3-70B "
-                         "8 x DP1 -> TP8), its 8 engines mapped onto the N GPUs as 8/N virtual ranks each")
+                         "8 x DP1 -> TP8), its 8 engines mapped onto the N GPUs as 8/N virtual ranks each "
+                         "(strong scaling); 'weak' = synth.weak_merge(N): two engines per GPU, per-GPU bytes fixed")
     ap.add_argument("--cpu-sample-reqs", type=int, default=4,
                     help="oracle sample (first N requests) per step of --impl reference and of cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -204,7 +205,8 @@ class ClockSampler:
 def build_workload(args, world: int, rank: int):
     """The same workload at every N (strong scaling): its engines are mapped
     onto the N GPUs as consecutive blocks of engines/N virtual ranks."""
-    w = synth.WORKLOADS[args.config]()
+    # "weak": the weak-scaling series (per-GPU bytes fixed, engines = 2 x GPUs); the others are fixed workloads
+    w = synth.weak_merge(world) if args.config == "weak" else synth.WORKLOADS[args.config]()
     if args.requests:
         w = synth.Workload(w.name + f" first{args.requests}", w.L, w.H, w.d, w.B, w.e, w.n_gpus,
                            w.T[:args.requests], w.src[:args.requests], w.dst[:args.requests])
@@ -378,7 +380,7 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": "DP<->TP KV re-layout GB/s", "value": gbs, "unit": "GB/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": cpu["ms_per_switch"],
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "higher_is_better": True, "scaling": "weak" if args.config == "weak" else "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": w.name + (f" ({w.n_gpus} engines)" if w.n_gpus > 1 else ""),
                    "layers": w.L, "kv_heads": w.H, "head_dim": w.d, "block_base": w.B, "requests": len(w.T),
                    "tokens": w.tokens(), "sample": cpu["sample"]},
@@ -754,7 +756,7 @@ def run_single(args):
     line = {
         "metric": "DP<->TP KV re-layout GB/s", "value": round(value, 3), "unit": "GB/s", "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4),
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "higher_is_better": True, "scaling": "weak" if args.config == "weak" else "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic",
         "config": {"workload": w.name + (f" ({w.n_gpus} virtual ranks on 1 GPU)" if w.n_gpus > 1 else ""),
                    "layers": w.L, "kv_heads": w.H, "head_dim": w.d, "block_base": w.B, "requests": len(w.T),
@@ -1147,7 +1149,7 @@ def run_multi(args):
         line = {
             "metric": "DP<->TP KV re-layout GB/s", "value": round(payload_sum / (total_ms / 1e3) / 1e9, 3),
             "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True, "scaling": "strong",
+            "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True, "scaling": "weak" if args.config == "weak" else "strong",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": w.name + (f" ({v} virtual ranks per GPU)" if v > 1 else "") +
                        (" (ranks share cuda:0, gloo plumbing)" if same_dev else "") +

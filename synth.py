@@ -98,6 +98,22 @@ def llama70b_dp8_tp8(n_req: int = 64, seed: int = 0, H: int = 8) -> Workload:
     return Workload(f"llama3-70b DP8->TP8 H{H}", 80, H, 128, 16, 2, 8, T, src, dst)
 
 
+def weak_merge(n_gpus: int, per_engine: int = 8, engines_per_gpu: int = 2, seed: int = 0) -> Workload:
+    """Weak-scaling series (round-1 review): Llama-3-70B geometry, two DP
+    engines per GPU (so one GPU already has a real merge), 8 requests per
+    engine with the same lengths T ~ U[512, 4096] on every engine, merged
+    into TP groups of min(E, 8) engines (E = 2 x GPUs: TP2 on 1 GPU, TP4 on
+    2, TP8 on 4, 2 x TP8 on 8).  Per-GPU bytes are the same at every N."""
+    E = engines_per_gpu * n_gpus
+    p = min(E, 8)
+    Te = lengths(per_engine, 512, 4096, seed)
+    T = [t for _ in range(E) for t in Te]
+    src = [(e, 1) for e in range(E) for _ in range(per_engine)]
+    dst = [((e // p) * p, p) for e in range(E) for _ in range(per_engine)]
+    return Workload(f"llama3-70b weak DP{E}->TP{p}x{E // p} ({per_engine} req/engine, {engines_per_gpu} engines/GPU)",
+                    80, 8, 128, 16, 2, E, T, src, dst)
+
+
 def llama70b_fanout(n_req: int = 64, seed: int = 0) -> Workload:
     """BASELINE configs[3] (ii): single DP replica on GPU0 -> TP8 (the merge
     of a DP engine into one TP group).  Its sources sit at the

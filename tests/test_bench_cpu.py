@@ -118,3 +118,17 @@ def test_process_matrix_of_virtual_ranks():
     pm = bench.proc_matrix(m, 4)
     assert pm.shape == (2, 2) and pm.sum() == m.sum()
     assert pm[0, 1] == m[:4, 4:].sum() and pm[1, 0] == m[4:, :4].sum()
+
+
+def test_weak_series_keeps_per_gpu_bytes():
+    """--config weak (synth.weak_merge): two DP engines per GPU merged into TP
+    groups of min(2N, 8); every GPU sources the same requests at every N."""
+    import synth
+    per_gpu = set()
+    for n in (1, 2, 4, 8):
+        w = synth.weak_merge(n)
+        assert w.n_gpus == 2 * n and len(w.T) == 16 * n
+        assert all(d[1] == min(2 * n, 8) and d[0] % d[1] == 0 for d in w.dst)
+        for g in range(0, w.n_gpus, 2):   # GPU g // 2 owns engines g, g + 1
+            per_gpu.add(tuple(sorted(T for T, s in zip(w.T, w.src) if s[0] in (g, g + 1))))
+    assert len(per_gpu) == 1
