@@ -1,6 +1,6 @@
 #!/bin/bash
 # For a multi-GPU (NVSwitch) box -- not runnable on the one-GPU gpurun boxes:
-# the strong-scaling series of the headline switch, the NCCL all-to-all
+# the strong-scaling series of the headline switch, the weak-scaling series, the NCCL all-to-all
 # comparator, the NVLS multicast path for GQA replicas, the NVLS parity test,
 # and NVLink tx/rx bytes of one rank's push kernel (ncu metric names checked
 # offline with `ncu --query-metrics --chip gb100`).
@@ -12,6 +12,10 @@ for g in 1 2 4 8; do
   [ "$g" -le "$n" ] || continue
   timeout 900 python bench.py --gpus $g --steps 20 --warmup 5 >> gpurun_out/scale.jsonl 2> gpurun_out/scale_n$g.err; echo "c4 N=$g rc=$?"
   grep -c "NCCL INFO.*nranks $g" gpurun_out/scale_n$g.err
+done
+for g in 1 2 4 8; do   # weak-scaling series: per-GPU bytes fixed
+  [ "$g" -le "$n" ] || continue
+  timeout 900 python bench.py --gpus $g --config weak --steps 20 --warmup 5 >> gpurun_out/scale.jsonl 2>/dev/null; echo "weak N=$g rc=$?"
 done
 for g in 2 8; do
   [ "$g" -le "$n" ] || continue
