@@ -1240,23 +1240,25 @@ def run_decode(args):
             items.append((gp, views[gp], lens, q, out, q_local, kv + q.numel() * 2 + out.numel() * 4))
         return items
 
-    def one_pass(items):
+    def one_pass(items, after=True):
+        """after: KV_DECODE_AFTER_DECODE on every launch -- the kernel before each is a decode launch (or, for
+        the first, one of this library's kernels, none of which lets its dependents start early)."""
         for gp, t, lens, q, out, q_local, _ in items:
             base = eng.pools.tensors[gp]
             for l in range(w.L):
                 F.kv_paged_decode(g, base[l].data_ptr(), t.meta.shape[0], t.req_ptr, t.block_ids, t.meta, lens,
-                                  q_local, q, out, scale, max(w.T), stream)
+                                  q_local, q, out, scale, max(w.T), stream, after_decode=after)
 
-    def timed(items):
+    def timed(items, after=True):
         """One pass captured in a CUDA graph (the 80-layer decode step is
         launch-bound from Python: 640 launches), replayed `steps` times
         between CUDA events; plus the same passes launched eagerly."""
         for _ in range(max(args.warmup, 3)):   # warm-up also sizes the decode workspace (no allocation in capture)
-            one_pass(items)
+            one_pass(items, after)
         torch.cuda.synchronize()
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph, stream=stream):
-            one_pass(items)
+            one_pass(items, after)
         torch.cuda.synchronize()
         for _ in range(max(args.warmup, 3)):
             graph.replay()
@@ -1276,7 +1278,7 @@ def run_decode(args):
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record(stream)
         for _ in range(args.steps):
-            one_pass(items)
+            one_pass(items, after)
         f1.record(stream)
         torch.cuda.synchronize()
         eager_ms = f0.elapsed_time(f1) / args.steps
@@ -1291,18 +1293,14 @@ def run_decode(args):
     torch.cuda.synchronize()
     dp_items = prepare(plan0, views0, host0, lambda i: w.src[i][1])
     dp_ms, dp_bytes, dp_launch, dp_eager = timed(dp_items)
-    os.environ["FLYKV_DECODE_PDL"] = "0"   # the same step with every launch waiting for the previous one
-    dp_ms_serial = timed(dp_items)[0]
-    os.environ.pop("FLYKV_DECODE_PDL", None)
+    dp_ms_serial = timed(dp_items, after=False)[0]   # every launch waits for the previous one
     # forward switch, then the TP layout
     move = [(i, T, s_, ids_, d_) for i, (T, s_, ids_, d_) in enumerate(zip(w.T, w.src, tabs, w.dst))]
     plan1, views1, host1 = eng.switch(move, read_back=True)
     torch.cuda.synchronize()
     tp_items = prepare(plan1, views1, host1, lambda i: w.dst[i][1])
     tp_ms, tp_bytes, tp_launch, tp_eager = timed(tp_items)
-    os.environ["FLYKV_DECODE_PDL"] = "0"
-    tp_ms_serial = timed(tp_items)[0]
-    os.environ.pop("FLYKV_DECODE_PDL", None)
+    tp_ms_serial = timed(tp_items, after=False)[0]
     clk.stop()
     gbs = tp_bytes / tp_ms / 1e6
     line = {
@@ -1321,9 +1319,9 @@ def run_decode(args):
                      "algorithmic_bytes": "every K/V byte of every resident (request, local KV head) + q + out"},
         "serialized": {"ms_per_step": round(tp_ms_serial, 4), "GBps": round(tp_bytes / tp_ms_serial / 1e6, 1),
                        "frac": round(tp_bytes / tp_ms_serial / 1e6 / hbm, 4),
-                       "note": "FLYKV_DECODE_PDL=0: no programmatic dependent launch, every launch starts after "
-                               "the previous one completed (as when a model's other layer kernels sit between "
-                               "two attention launches); value/roofline overlap consecutive launches"},
+                       "note": "flags 0: every launch starts after the previous one completed (as when a model's "
+                               "other layer kernels sit between two attention launches); value/roofline use "
+                               "KV_DECODE_AFTER_DECODE, consecutive decode launches overlapped"},
         "eager_ms_per_step": round(tp_eager, 4),
         "eager_note": "the same step launched from Python (640 ctypes calls): host-bound, context only",
         "dp_layout": {"ms_per_step": round(dp_ms, 4), "GBps": round(dp_bytes / dp_ms / 1e6, 1),

@@ -608,16 +608,31 @@ kv_status kv_gather_view(const kv_view* view, void* dst, void* stream);
  *   max_seq_len host: >= every seq_lens entry; sizes the split workspace the
  *               library keeps per (device, stream) (a larger entry traps:
  *               a CUDA error, never a stray write)
+ *   flags       0, or KV_DECODE_AFTER_DECODE: the kernel enqueued right
+ *               before this one on the stream is a kv_paged_decode launch
+ *               (e.g. the same layer of the next pool), or any kernel that
+ *               does not let its dependents start early (no
+ *               griddepcontrol.launch_dependents /
+ *               cudaTriggerProgrammaticLaunchCompletion before it is done).
+ *               The launch then overlaps a previous decode launch through
+ *               programmatic dependent launch: it reads the cache, q and the
+ *               tables before that launch completes (a decode grid never
+ *               writes them) and waits only before its workspace and out.
+ *               Wrong after a kernel that triggers its dependents early and
+ *               writes q, the cache or the tables; without the flag a launch
+ *               waits for the previous kernel as usual.  Other bits:
+ *               KV_ERR_INVALID_ARG.
  * Calls on one stream share that workspace (ordered); calls on different
  * streams use different ones.  It grows outside stream capture only: a
  * call captured into a CUDA graph that would need a larger workspace
  * returns KV_ERR_BAD_STATE (call once with the same sizes before capturing).  bf16 and head_dim 64/128/256 only
  * (INVALID_ARG otherwise); KV_ERR_CUDA on workspace allocation or launch.
  */
+#define KV_DECODE_AFTER_DECODE 1
 kv_status kv_paged_decode(const kv_geometry* geom, const void* layer_base, int32_t n_res, const int32_t* req_ptr,
                           const int32_t* block_ids, const int32_t* per_req_meta, const int32_t* seq_lens,
                           int32_t q_heads_local, const void* q, float* out, float scale, int32_t max_seq_len,
-                          void* stream);
+                          int32_t flags, void* stream);
 
 /* kv_paged_decode_release: free the decode workspace the library keeps for
  * `stream` on the current device (stream-ordered; a later kv_paged_decode on

@@ -39,10 +39,12 @@
 //   * Each warp stages its tiles through a 2-deep shared-memory ring
 //     (cp.async, rows padded to 2D + 16 bytes: conflict-free fragment
 //     reads), so one tile loads while the previous one computes.
-//   * Consecutive launches overlap through programmatic dependent launch:
-//     the next grid scans its requests and runs its tiles (the cache, q and
-//     the tables are never written by a decode grid) and waits for this one
-//     only before its workspace and out.
+//   * With KV_DECODE_AFTER_DECODE (the previous launch on the stream is a
+//     decode grid), consecutive launches overlap through programmatic
+//     dependent launch: the next grid scans its requests and runs its tiles
+//     (a decode grid never writes the cache, q or the tables) and waits for
+//     the previous one only before its workspace and out.  Without the flag
+//     a launch waits for the previous kernel as usual.
 //   * Measured (bench.py --decode): 0.65 of the HBM
 //     roofline back to back, 0.45 with every (pool, layer) launch of 77 MB
 //     serialized.  While the warps stream
@@ -52,8 +54,6 @@
 //     Launch shapes, split sizes, staging depth and programmatic dependent
 //     launch are compile-time knobs (FLYKV_DEC_*) for sweeps.
 #include <cuda_bf16.h>
-
-#include <cstdlib>
 
 #include "flykv_internal.h"
 
@@ -751,7 +751,7 @@ constexpr int decode_dyn_smem() {
 }
 
 template <int D>
-static cudaError_t launch_decode_d(const DecodeArgs& a, int grid, cudaStream_t s) {
+static cudaError_t launch_decode_d(const DecodeArgs& a, int grid, bool pdl, cudaStream_t s) {
     constexpr int smem = decode_dyn_smem<D>();
     if (smem > 48 * 1024) {
         static bool done = false;   // opt in once per process
@@ -763,36 +763,32 @@ static cudaError_t launch_decode_d(const DecodeArgs& a, int grid, cudaStream_t s
         }
     }
 #if FLYKV_DEC_PDL
-    // FLYKV_DECODE_PDL=0 (read per call): launch without the programmatic edge, every launch after the
-    // previous one completed (the bench reports both)
-    const char* env = std::getenv("FLYKV_DECODE_PDL");
-    if (env && env[0] == '0') {
-        flykv_paged_decode_kernel<D><<<grid, kWarps * 32, smem, s>>>(a);
-        return cudaGetLastError();
+    if (pdl) {   // KV_DECODE_AFTER_DECODE: overlap with the previous launch on the stream (a decode grid)
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(kWarps * 32);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, flykv_paged_decode_kernel<D>, a);
     }
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kWarps * 32);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, flykv_paged_decode_kernel<D>, a);
 #else
+    (void)pdl;
+#endif
     flykv_paged_decode_kernel<D><<<grid, kWarps * 32, smem, s>>>(a);
     return cudaGetLastError();
-#endif
 }
 
-cudaError_t launch_decode(const DecodeArgs& a, int grid, cudaStream_t s) {
+cudaError_t launch_decode(const DecodeArgs& a, int grid, bool pdl, cudaStream_t s) {
     if (a.n_res == 0) return cudaSuccess;
     switch (a.d) {
-        case 64: return launch_decode_d<64>(a, grid, s);
-        case 128: return launch_decode_d<128>(a, grid, s);
-        case 256: return launch_decode_d<256>(a, grid, s);
+        case 64: return launch_decode_d<64>(a, grid, pdl, s);
+        case 128: return launch_decode_d<128>(a, grid, pdl, s);
+        case 256: return launch_decode_d<256>(a, grid, pdl, s);
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();

@@ -2044,12 +2044,12 @@ static std::map<std::pair<int, cudaStream_t>, DecodeWorkspace> g_dec_ws;
 extern "C" kv_status kv_paged_decode(const kv_geometry* geom, const void* layer_base, int32_t n_res,
                                      const int32_t* req_ptr, const int32_t* block_ids, const int32_t* per_req_meta,
                                      const int32_t* seq_lens, int32_t q_heads_local, const void* q, float* out,
-                                     float scale, int32_t max_seq_len, void* stream_) {
+                                     float scale, int32_t max_seq_len, int32_t flags, void* stream_) {
     kv_status s = check_geometry(geom);
     if (s) return s;
     if (geom->elem_bytes != 2 || (geom->head_dim != 64 && geom->head_dim != 128 && geom->head_dim != 256))
         return fail(KV_ERR_INVALID_ARG, "kv_paged_decode needs bf16 and head_dim 64/128/256");
-    if (n_res < 0 || q_heads_local < 1 || max_seq_len < 0 ||
+    if (n_res < 0 || q_heads_local < 1 || max_seq_len < 0 || (flags & ~KV_DECODE_AFTER_DECODE) ||
         (n_res > 0 && (!layer_base || !req_ptr || !per_req_meta || !seq_lens || !q || !out)))
         return fail(KV_ERR_INVALID_ARG, "bad kv_paged_decode arguments");
     if (((uintptr_t)q & 15) || ((uintptr_t)layer_base & 15))
@@ -2102,7 +2102,7 @@ extern "C" kv_status kv_paged_decode(const kv_geometry* geom, const void* layer_
     a.out = out;
     a.scale = scale;
     a.max_seq = max_seq_len;
-    cudaError_t e = launch_decode(a, decode_grid(d), stream);
+    cudaError_t e = launch_decode(a, decode_grid(d), (flags & KV_DECODE_AFTER_DECODE) != 0, stream);
     if (e != cudaSuccess) return cuda_fail(e, "flykv_paged_decode_kernel launch");
     g_launches.fetch_add(1);
     return KV_OK;

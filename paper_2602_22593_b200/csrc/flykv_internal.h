@@ -219,7 +219,7 @@ cudaError_t launch_reshard(const ReshardArgs& a, int device, cudaStream_t s);
 void set_reshard_impl(int impl, int ctas_per_sm);
 cudaError_t launch_remap(const RemapArgs& a, int n_ctas, cudaStream_t s);
 cudaError_t launch_gather(const GatherSeg* segs, int n_seg, char* dst, cudaStream_t s);
-cudaError_t launch_decode(const DecodeArgs& a, int grid, cudaStream_t s);
+cudaError_t launch_decode(const DecodeArgs& a, int grid, bool pdl, cudaStream_t s);
 int decode_split_tokens();
 int decode_grid(int d);
 cudaError_t launch_unpack(const UnpackArgs& a, int device, cudaStream_t s);

@@ -168,7 +168,8 @@ _sig("kv_vmm_free", C.c_int, _P)
 _sig("weight_view_alias", C.c_int, _P, C.POINTER(View), C.POINTER(_P), C.POINTER(C.c_uint64))
 _sig("weight_view_unalias", C.c_int, _P, C.c_uint64)
 _sig("kv_paged_decode", C.c_int, C.POINTER(Geometry), _P, C.c_int32, _P, _P, _P, _P, C.c_int32, _P, _P, C.c_float,
-     C.c_int32, _P)
+     C.c_int32, C.c_int32, _P)
+KV_DECODE_AFTER_DECODE = 1
 _sig("kv_paged_decode_release", C.c_int, _P)
 _sig("kv_ipc_export", C.c_int, _P, C.POINTER(C.c_uint8), C.POINTER(C.c_uint64))
 _sig("kv_ipc_import", C.c_int, C.POINTER(C.c_uint8), C.c_uint64, C.POINTER(_P))
@@ -791,12 +792,15 @@ def weight_view_unalias(ptr: int, nbytes: int):
 
 # ----------------------------------------------------------------- consumer proof
 def kv_paged_decode(geom: Geometry, layer_base, n_res: int, req_ptr, block_ids, per_req_meta, seq_lens,
-                    q_heads_local: int, q, out, scale: float, max_seq_len: int, stream=None):
+                    q_heads_local: int, q, out, scale: float, max_seq_len: int, stream=None, after_decode=False):
     """N3 paged decode attention over one layer of one pool (kv_paged_decode);
-    max_seq_len >= every seq_lens entry (sizes the split workspace)."""
+    max_seq_len >= every seq_lens entry (sizes the split workspace).
+    after_decode: the previous kernel on the stream is a kv_paged_decode
+    launch (KV_DECODE_AFTER_DECODE: the launches overlap)."""
     _check(_lib.kv_paged_decode(C.byref(geom), ptr_of(layer_base), n_res, ptr_of(req_ptr), ptr_of(block_ids),
                                 ptr_of(per_req_meta), ptr_of(seq_lens), q_heads_local, ptr_of(q), ptr_of(out),
-                                float(scale), int(max_seq_len), stream_of(stream)))
+                                float(scale), int(max_seq_len), KV_DECODE_AFTER_DECODE if after_decode else 0,
+                                stream_of(stream)))
 
 
 def kv_paged_decode_release(stream=None):

@@ -781,3 +781,5 @@ def test_paged_decode_validates_before_the_device():
             call(geom, **kw)
         assert e.value.name == "KV_ERR_INVALID_ARG", (geom.head_dim, kw)
     call(n_res=0)   # nothing resident: no launch, no device work
+    st = F._lib.kv_paged_decode(F.C.byref(g), a16, 4, a16, a16, a16, a16, 8, a16, a16, 0.1, 100, 2, None)
+    assert F.STATUS_NAMES[st] == "KV_ERR_INVALID_ARG"   # unknown flag bits

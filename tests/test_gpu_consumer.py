@@ -42,7 +42,7 @@ def _decode_all(F, eng, geo, plan, tables, q_full, gpus, q_slices, seq):
         out = torch.empty((n_res, qhi - qlo, d), dtype=torch.float32, device="cuda:0")
         layer = eng.pools.tensors[g][1]  # layer 1 of pool g
         F.kv_paged_decode(eng.geom, layer.data_ptr(), n_res, t.req_ptr, t.block_ids, t.meta, lens, qhi - qlo, q, out,
-                          1.0 / np.sqrt(d), max(seq), eng.stream)
+                          1.0 / np.sqrt(d), max(seq), eng.stream, after_decode=True)   # after our own kernels only
         torch.cuda.synchronize()
         o = out.cpu().numpy()
         for k, i in enumerate(meta[:, 0]):
@@ -248,9 +248,10 @@ def test_decode_random_geometry_against_fp64(case):
 
 
 def test_decode_back_to_back_launches_same_out():
-    """Consecutive kv_paged_decode launches on one stream overlap through
-    programmatic dependent launch; a launch's tiles may run under the
-    previous one's tail, but its workspace and out writes wait for it.  Two
+    """Consecutive kv_paged_decode launches on one stream with
+    KV_DECODE_AFTER_DECODE overlap through programmatic dependent launch; a
+    launch's tiles may run under the previous one's tail, but its workspace
+    and out writes wait for it.  Two
     launches with different q into the same out (and a third with a longer
     length bound's workspace) leave exactly the last launch's result."""
     F = pytest.importorskip("paper_2602_22593_b200.flykv")
@@ -273,8 +274,8 @@ def test_decode_back_to_back_launches_same_out():
     out = torch.empty((len(seq), 8, 128), dtype=torch.float32, device="cuda:0")
     ref = torch.empty_like(out)
     args = (pool.data_ptr(), len(seq), dev(rp), dev(ids), dev(meta), lens, 8)
-    for k in range(3):   # back to back on one stream, same out
-        F.kv_paged_decode(g, *args, qs[k], out, 0.09, 4096 if k < 2 else 8192, s)
+    for k in range(3):   # back to back on one stream, same out, overlapped (KV_DECODE_AFTER_DECODE)
+        F.kv_paged_decode(g, *args, qs[k], out, 0.09, 4096 if k < 2 else 8192, s, after_decode=k > 0)
     s.synchronize()
     s2 = torch.cuda.Stream()
     F.kv_paged_decode(g, *args, qs[2], ref, 0.09, 8192, s2)
