@@ -247,7 +247,8 @@ def test_decode_random_geometry_against_fp64(case):
                 assert np.allclose(o[i, j], ref, rtol=2e-3, atol=2e-3), (case, i, j)
 
 
-def test_decode_back_to_back_launches_same_out():
+@pytest.mark.parametrize("d", [64, 128, 256])
+def test_decode_back_to_back_launches_same_out(d):
     """Consecutive kv_paged_decode launches on one stream with
     KV_DECODE_AFTER_DECODE overlap through programmatic dependent launch; a
     launch's tiles may run under the previous one's tail, but its workspace
@@ -256,8 +257,8 @@ def test_decode_back_to_back_launches_same_out():
     length bound's workspace) leave exactly the last launch's result."""
     F = pytest.importorskip("paper_2602_22593_b200.flykv")
     rng = np.random.default_rng(77)
-    g = F.geometry(1, 2, 128, 16, 2)
-    og = O.Geom(1, 2, 128, 16, 2)
+    g = F.geometry(1, 2, d, 16, 2)
+    og = O.Geom(1, 2, d, 16, 2)
     seq = [1500, 700, 33, 2600]
     counts = [O.num_blocks(og, T, 1) for T in seq]
     M = O.block_bytes(og)
@@ -269,9 +270,9 @@ def test_decode_back_to_back_launches_same_out():
     dev = lambda a: torch.as_tensor(a, device="cuda:0")                     # noqa: E731
     pool = torch.randn(nb * M // 2, device="cuda:0").to(torch.bfloat16)
     lens = dev(np.asarray(seq, np.int32))
-    qs = [torch.randn((len(seq), 8, 128), device="cuda:0").to(torch.bfloat16) for _ in range(3)]
+    qs = [torch.randn((len(seq), 8, d), device="cuda:0").to(torch.bfloat16) for _ in range(3)]
     s = torch.cuda.Stream()
-    out = torch.empty((len(seq), 8, 128), dtype=torch.float32, device="cuda:0")
+    out = torch.empty((len(seq), 8, d), dtype=torch.float32, device="cuda:0")
     ref = torch.empty_like(out)
     args = (pool.data_ptr(), len(seq), dev(rp), dev(ids), dev(meta), lens, 8)
     for k in range(3):   # back to back on one stream, same out, overlapped (KV_DECODE_AFTER_DECODE)
